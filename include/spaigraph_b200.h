@@ -1,0 +1,217 @@
+/*
+ * spaigraph_b200 — C-ABI of the B200-native GNN-SPAI + PCG hot path.
+ *
+ * Drop-in boundary for the reference package `spaigraph` (pure numpy, /root/reference/pkg).
+ * The reference has no FFI of its own; every entry point below replaces one numpy function of
+ * the hot path and cites it as  <file>:<line>  relative to pkg/src/spaigraph/.  The Python host
+ * package `paper_2510_27517_b200` (ctypes) mirrors the reference's Python API on top of these.
+ *
+ * Conventions
+ *   - All array arguments are DEVICE pointers unless the name ends in `_host`.
+ *   - Indices on device are int32 (row offsets, column indices, permutations); sizes are int64.
+ *     Values are IEEE binary64.  Device arrays that a kernel stages with 16-byte vector loads
+ *     must be allocated with >= 16 bytes of slack past the end (the Python layer pads).
+ *   - `stream` is a cudaStream_t passed as void*.  Calls are asynchronous on `stream` unless the
+ *     comment says "synchronizes".
+ *   - Return value: SG_OK or an error code; sg_last_error() returns a thread-local message.
+ *   - Buffers are caller-owned.  Functions that need scratch take (ws, ws_bytes): call with
+ *     ws == NULL to read the required size into *ws_bytes.
+ *   - Parity kernels compute products and sums with explicit round-to-nearest intrinsics in the
+ *     reference's summation order, so SpMV / transpose-SpMV / apply / features / generators are
+ *     bit-identical to the numpy reference.
+ */
+#ifndef SPAIGRAPH_B200_H
+#define SPAIGRAPH_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum sg_status {
+  SG_OK = 0,
+  SG_EINVAL = 1,        /* shape / structure violation      -> ValueError        */
+  SG_ENOTSPD = 2,       /* PCG breakdown                    -> NotSpdError       */
+  SG_ECUDA = 3,         /* CUDA runtime error               -> RuntimeError      */
+  SG_EUNSUPPORTED = 4,  /* configuration not implemented    -> NotImplementedError */
+  SG_EDUPLICATE = 5     /* duplicate COO entry              -> ValueError("duplicate ...") */
+};
+
+int sg_abi_version(void);
+const char* sg_last_error(void);
+
+/* ---------------------------------------------------------------- sparsity patterns (L1) */
+
+/* SparseMatrix.from_coo (sparse.py:138-158): stable sort by (row, col), duplicate rejection,
+ * row offsets.  rows/cols are int64 (the reference index type).  On SG_EDUPLICATE the
+ * lexicographically first duplicated (row, col) is written to dup_host[0..1].  Synchronizes. */
+int sg_csr_from_coo(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* rows,
+                    const int64_t* cols, const double* vals, int32_t* offs_out, int32_t* cols_out,
+                    double* vals_out, int64_t* dup_host, void* ws, size_t* ws_bytes, void* stream);
+
+/* int64 -> int32 narrowing of reference index arrays: out[k] = in[k] + shift after checking
+ * lo <= in[k] < hi (shift places a system inside a block-diagonal batch).  Synchronizes. */
+int sg_narrow_index(const int64_t* in, int32_t* out, int64_t n, int64_t lo, int64_t hi,
+                    int64_t shift, void* ws, size_t* ws_bytes, void* stream);
+
+/* _validate_structure (sparse.py:27-43): offsets[0]==0, offsets[n]==nnz, nondecreasing,
+ * columns in range and strictly increasing within a row.  Synchronizes. */
+int sg_csr_validate(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* offs,
+                    const int32_t* cols, void* ws, size_t* ws_bytes, void* stream);
+
+/* SparseMatrix.transpose (sparse.py:129-136): pattern of A^T with ascending original rows
+ * inside each row, plus perm such that values_t[k] = values[perm[k]] (see sg_gather_f64). */
+int sg_csr_transpose(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* offs,
+                     const int32_t* cols, int32_t* offs_t, int32_t* cols_t, int32_t* perm,
+                     void* ws, size_t* ws_bytes, void* stream);
+
+/* SparsityPattern.is_symmetric (sparse.py:68-78).  *result_host = 1/0.  Synchronizes. */
+int sg_pattern_is_symmetric(int64_t n, int64_t nnz, const int32_t* offs, const int32_t* cols,
+                            int32_t* result_host, void* ws, size_t* ws_bytes, void* stream);
+
+/* row_expand (sparse.py:64-66): rows_out[k] = row of stored entry k. */
+int sg_row_expand(int64_t n_rows, const int32_t* offs, int32_t* rows_out, void* stream);
+
+/* values_out[k] = values_in[perm[k]] (G^T values from G values, gnn.py:256-267 + a4). */
+int sg_gather_f64(const double* in, const int32_t* perm, double* out, int64_t n, void* stream);
+
+/* SparseMatrix.diagonal (sparse.py:119-127), absent entries read 0. present_out may be NULL. */
+int sg_csr_diagonal(int64_t n, const int32_t* offs, const int32_t* cols, const double* vals,
+                    double* diag_out, int32_t* present_out, void* stream);
+
+/* ---------------------------------------------------------------- generators (L6) */
+
+/* gen_poisson2d (datasets.py:87-145) emitted directly in CSR order; coeff is the node field a
+ * (ones for "poisson2d").  offs: nx*ny+1, cols/vals: 5*nx*ny - 2*nx - 2*ny.  row0/nnz0 place
+ * the system inside a block-diagonal batch: rows row0.., entries nnz0.. (0, 0 for a single
+ * system); offs/cols/vals are the batch arrays. */
+int sg_gen_poisson2d(int64_t nx, int64_t ny, const double* coeff, int64_t row0, int64_t nnz0,
+                     int32_t* offs, int32_t* cols, double* vals, void* stream);
+
+/* 7-point 3-D analogue (oracle/spaigraph_ref.py:gen_poisson3d). */
+int sg_gen_poisson3d(int64_t nx, int64_t ny, int64_t nz, int32_t* offs, int32_t* cols,
+                     double* vals, void* stream);
+
+/* ---------------------------------------------------------------- norms + features (L3) */
+
+/* matrix_norm (training.py:44-54) / mean_abs_nonzero_norm (sparse.py:204-213): the exact
+ * (math.fsum-identical, correctly rounded) sum of |v| (kind 0: /nnz, kind 2: as is) or of
+ * fl(v*v) (kind 1: sqrt).  Result written to *norm_out (device). */
+int sg_matrix_norm(const double* vals, int64_t nnz, int kind, double* norm_out, void* ws,
+                   size_t* ws_bytes, void* stream);
+
+/* build_graph features (graphfeat.py:63-105) for the n rows row0..row0+n-1 of a (possibly
+ * block-diagonal) matrix.  family 0: algebraic [rowsum/n/norm, diag/norm] (node_out rows of
+ * 2); family 1: PDE [(ix+1)hx, (iy+1)hy, coeff/coeff_mean] (rows of 3; coeff is the system's
+ * own field, indexed locally).  edge_out[k] = vals[k] / norm.  norm: device scalar. */
+int sg_graph_features(int64_t n, int64_t row0, const int32_t* offs, const int32_t* cols,
+                      const double* vals, const double* norm, int family, int64_t nx, int64_t ny,
+                      const double* coeff, double coeff_mean, double* node_out, double* edge_out,
+                      void* stream);
+
+/* ---------------------------------------------------------------- GNN forward (L3) */
+
+/* forward (gnn.py:208-253) restructured: node-path kernels + one fused edge
+ * pass that never materialises H.  params: flat f64 in declaration order (gnn.py:130-136).
+ * Supported: mlp_hidden_layers == 1, message_uses_hidden_edge == 0, d_edge == 1,
+ * hidden in {4,6,8,12,16,24,32}, d_node <= 4, act 0 = relu / 1 = tanh; else SG_EUNSUPPORTED.
+ * rows: row index per edge (sg_row_expand).  g_out[k] = G value of stored entry k. */
+int sg_gnn_forward(const double* params, int64_t n_params, int n_layers, int hidden, int d_node,
+                   int d_edge, int act, int64_t n, int64_t nnz, const int32_t* offs,
+                   const int32_t* cols, const int32_t* rows, const double* node_feat,
+                   const double* edge_feat, double* g_out, void* ws, size_t* ws_bytes,
+                   void* stream);
+
+/* ---------------------------------------------------------------- SpMV family (L1, L4) */
+
+/* spmv (sparse.py:186-191): y = A x in numpy reduceat order (bit-identical). */
+int sg_spmv(int64_t n_rows, const int32_t* offs, const int32_t* cols, const double* vals,
+            const double* x, double* y, void* stream);
+
+/* spmv_transpose (sparse.py:194-201) given the explicit transpose (sg_csr_transpose): strictly
+ * sequential per row from 0.0 == np.add.at order (bit-identical). */
+int sg_spmv_seq(int64_t n_rows, const int32_t* offs, const int32_t* cols, const double* vals,
+                const double* x, double* y, void* stream);
+
+/* LearnedSpaiPreconditioner.apply (precond.py:143-145): s = G (G^T r) + eps r.
+ * t_ws: n doubles of scratch. */
+int sg_learned_apply(int64_t n, const int32_t* g_offs, const int32_t* g_cols, const double* g_vals,
+                     const int32_t* gt_offs, const int32_t* gt_cols, const double* gt_vals,
+                     double eps, const double* r, double* t_ws, double* s_out, void* stream);
+
+/* ---------------------------------------------------------------- PCG (L4) */
+
+/* pcg_solve (pcg.py:131-233) for a batch of independent systems stored block-diagonally
+ * (global column indices).  One handle per (matrices, preconditioner) pair; the handle owns
+ * device state, the CUDA-graph cache and per-system histories. */
+typedef struct sg_pcg sg_pcg;
+
+enum sg_precond_kind { SG_PRECOND_IDENTITY = 0, SG_PRECOND_JACOBI = 1, SG_PRECOND_LEARNED = 2 };
+
+typedef struct sg_solve_config {
+  double rtol;               /* SolveConfig.rtol                                           */
+  int64_t max_iters;         /* < 0: 20 * n_s per system (pcg.py:151)                      */
+  int64_t refresh_period;    /* SolveConfig.residual_refresh_period                        */
+  int32_t termination;       /* 0 = true_residual, 1 = delta                               */
+  int32_t track_history;     /* SolveConfig.track_history                                  */
+} sg_solve_config;
+
+typedef struct sg_solve_result {
+  int64_t k;                 /* SolveReport.k                                              */
+  int32_t converged;         /* SolveReport.converged                                      */
+  int32_t status;            /* SG_OK or SG_ENOTSPD                                        */
+  int64_t fail_iter;         /* NotSpdError.iteration                                      */
+  double fail_value;         /* NotSpdError.value                                          */
+  int32_t fail_kind;         /* 1: d^T A d <= 0, 2: r^T M r < 0                            */
+  int64_t hist_len;          /* number of residual_history entries                         */
+} sg_solve_result;
+
+/* sys_row_start_host: n_systems+1 row boundaries.  Matrices: A (PCG), and for LEARNED the
+ * factor G and its explicit transpose Gt; for JACOBI, inv_diag (n).  All device, int32 idx.
+ * The handle keeps the pointers (caller keeps the arrays alive). */
+int sg_pcg_create(sg_pcg** out, int32_t n_systems, const int64_t* sys_row_start_host,
+                  const int32_t* a_offs, const int32_t* a_cols, const double* a_vals,
+                  int precond_kind, const int32_t* g_offs, const int32_t* g_cols,
+                  const double* g_vals, const int32_t* gt_offs, const int32_t* gt_cols,
+                  const double* gt_vals, const double* inv_diag, double epsilon, void* stream);
+
+/* Solve A x = b from x0 = 0 for every system.  b, x: device, n rows.  results_host: n_systems
+ * entries.  Runs the device-resident loop (CUDA graphs of fused iteration kernels) and
+ * synchronizes before returning.  elapsed_ns_host (may be NULL) receives the solve time. */
+int sg_pcg_solve(sg_pcg* h, const double* b, double* x, const sg_solve_config* cfg,
+                 sg_solve_result* results_host, int64_t* elapsed_ns_host, void* stream);
+
+/* residual_history of system `sys` from the last solve (hist_len entries) into out_host. */
+int sg_pcg_history(sg_pcg* h, int32_t sys, double* out_host, int64_t len);
+
+void sg_pcg_destroy(sg_pcg* h);
+
+/* Instrumentation (no reference counterpart; pcg.py:155-229 only times apply / total on the
+ * host).  With profiling on, every chunk graph brackets K1, K2, K3 of one non-refresh
+ * iteration with external event-record nodes; sg_pcg_stats returns the summed device times
+ * prof_host[0..2] (ms), the summed active-system counts at those iterations prof_host[3], the
+ * sample count prof_host[4], plus the number of kernels and graphs launched. */
+int sg_pcg_set_profile(sg_pcg* h, int32_t on);
+int sg_pcg_stats(sg_pcg* h, int64_t* kernels_host, int64_t* chunks_host, double* prof_host,
+                 int32_t reset);
+
+/* ---------------------------------------------------------------- SAI loss (L5) */
+
+/* sai_loss / sai_loss_on_tape + Tape.backward (training.py:57-94, autodiff.py:190-239,
+ * 265-303).  A-side in double-double (the reference uses x87 long double); returns the loss in
+ * *loss_host and, if grad_out != NULL, dL/dg (nnz of G) in the tape's rounding order.
+ * at_*: explicit A^T (for du = A^T dz), gt_*: explicit G^T.  Synchronizes. */
+int sg_sai_loss(int64_t n, const int32_t* a_offs, const int32_t* a_cols, const double* a_vals,
+                const int32_t* at_offs, const int32_t* at_cols, const double* at_vals,
+                const int32_t* g_offs, const int32_t* g_cols, const double* g_vals,
+                const int32_t* gt_offs, const int32_t* gt_cols, const double* gt_vals,
+                const int32_t* g_rows, double eps, const double* w, int norm_kind,
+                double* loss_host, double* grad_out, void* ws, size_t* ws_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPAIGRAPH_B200_H */

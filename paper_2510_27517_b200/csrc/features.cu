@@ -1,0 +1,257 @@
+// Norms, graph features and stencil generators.
+//
+// sg_matrix_norm reproduces math.fsum exactly: every |v| (or fl(v*v)) is added as an integer
+// into a 2100-bit fixed-point superaccumulator (32-bit limbs held in uint64; integer atomics
+// make the result independent of thread order), then rounded once, round-half-even.  That is
+// the correctly rounded sum fsum promises, so `norm_A` is bit-identical to the reference.
+#include "common.cuh"
+
+namespace sg {
+
+constexpr int NLIMB = 72;  // 72*32 = 2304 bits >= 2098 value bits + carry headroom
+
+__device__ __forceinline__ void accum_add(unsigned long long* limbs, double a) {
+  unsigned long long bits = (unsigned long long)__double_as_longlong(a);
+  const int ex = (int)((bits >> 52) & 0x7FF);
+  unsigned long long m = bits & ((1ull << 52) - 1);
+  int g0 = 0;
+  if (ex) { m |= (1ull << 52); g0 = ex - 1; }
+  if (!m) return;
+  const int L = g0 >> 5, s = g0 & 31;
+  const unsigned long long lo = m << s;
+  const unsigned long long hi = s ? (m >> (64 - s)) : 0ull;
+  atomicAdd(&limbs[L], lo & 0xFFFFFFFFull);
+  atomicAdd(&limbs[L + 1], lo >> 32);
+  if (hi) atomicAdd(&limbs[L + 2], hi);
+}
+
+// mode 0: |v|, mode 1: fl(v*v).  flags: bit0 inf, bit1 nan.
+__global__ void k_exact_accum(const double* __restrict__ v, int64_t n, int mode,
+                              unsigned long long* g_limbs, unsigned int* flags) {
+  __shared__ unsigned long long sl[NLIMB];
+  for (int i = threadIdx.x; i < NLIMB; i += blockDim.x) sl[i] = 0;
+  __syncthreads();
+  unsigned int f = 0;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    double x = v[k];
+    double a = mode == 1 ? mul(x, x) : fabs(x);
+    if (isnan(a)) { f |= 2; continue; }
+    if (isinf(a)) { f |= 1; continue; }
+    accum_add(sl, a);
+  }
+  if (f) atomicOr(flags, f);
+  __syncthreads();
+  for (int i = threadIdx.x; i < NLIMB; i += blockDim.x)
+    if (sl[i]) atomicAdd(&g_limbs[i], sl[i]);
+}
+
+__device__ double round_limbs(const unsigned long long* in) {
+  unsigned int l[NLIMB];
+  unsigned long long c = 0;
+  for (int i = 0; i < NLIMB; ++i) {
+    unsigned long long t = in[i] + c;
+    l[i] = (unsigned int)(t & 0xFFFFFFFFull);
+    c = t >> 32;
+  }
+  int top = -1;
+  for (int i = NLIMB - 1; i >= 0; --i)
+    if (l[i]) { top = i; break; }
+  if (top < 0) return 0.0;
+  const int P = 32 * top + (31 - __clz(l[top]));
+  auto bit = [&](int i) -> unsigned long long { return (l[i >> 5] >> (i & 31)) & 1u; };
+  if (P <= 52) {
+    unsigned long long iv = (unsigned long long)l[0] | ((unsigned long long)l[1] << 32);
+    return ldexp((double)iv, -1074);
+  }
+  int shift = P - 52;
+  unsigned long long mant = 0;
+  for (int i = P; i >= shift; --i) mant = (mant << 1) | bit(i);
+  const unsigned long long rbit = bit(shift - 1);
+  bool sticky = false;
+  for (int i = 0; i < shift - 1 && !sticky; ++i) {
+    if ((i & 31) == 0 && i + 32 <= shift - 1) {
+      if (l[i >> 5]) sticky = true;
+      i += 31;
+      continue;
+    }
+    if (bit(i)) sticky = true;
+  }
+  if (rbit && (sticky || (mant & 1))) {
+    ++mant;
+    if (mant == (1ull << 53)) { mant >>= 1; ++shift; }
+  }
+  return ldexp((double)mant, shift - 1074);
+}
+
+__global__ void k_norm_finish(const unsigned long long* limbs, const unsigned int* flags,
+                              int64_t nnz, int kind, double* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double s;
+  if (*flags & 2) s = __longlong_as_double(0x7ff8000000000000ll);
+  else if (*flags & 1) s = __longlong_as_double(0x7ff0000000000000ll);
+  else s = round_limbs(limbs);
+  if (kind == 0) s = __ddiv_rn(s, (double)nnz);
+  else if (kind == 1) s = __dsqrt_rn(s);
+  *out = s;
+}
+
+// graphfeat.py:83 and 93-104, for global rows row0 .. row0+n-1 (local index li = i - row0).
+__global__ void k_graph_features(int64_t n, int64_t row0, const int32_t* __restrict__ offs,
+                                 const int32_t* __restrict__ cols, const double* __restrict__ vals,
+                                 const double* __restrict__ norm_p, int family, int64_t nx,
+                                 int64_t ny, const double* __restrict__ coeff, double coeff_mean,
+                                 double* node_out, double* edge_out) {
+  const double norm = *norm_p;
+  for (int64_t li = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; li < n;
+       li += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = row0 + li;
+    const int32_t lo = offs[i], hi = offs[i + 1];
+    for (int32_t k = lo; k < hi; ++k) edge_out[k] = __ddiv_rn(vals[k], norm);
+    if (family == 1) {
+      const double hx = __ddiv_rn(1.0, (double)(nx + 1)), hy = __ddiv_rn(1.0, (double)(ny + 1));
+      const int64_t ix = li % nx, iy = li / nx;
+      node_out[3 * i + 0] = mul((double)(ix + 1), hx);
+      node_out[3 * i + 1] = mul((double)(iy + 1), hy);
+      node_out[3 * i + 2] = __ddiv_rn(coeff[li], coeff_mean);
+    } else {
+      double rs = reduceat_sum([&](int64_t k) { return vals[k]; }, lo, hi);
+      double dg = 0.0;
+      for (int32_t k = lo; k < hi; ++k)
+        if (cols[k] == (int32_t)i) dg = vals[k];
+      node_out[2 * i + 0] = __ddiv_rn(__ddiv_rn(rs, (double)n), norm);
+      node_out[2 * i + 1] = __ddiv_rn(dg, norm);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ stencil generators
+// Entries stored before node (ix, iy) of the 5-point grid, rows in idx = ix + nx*iy order.
+__device__ __forceinline__ int64_t before2d(int64_t ix, int64_t iy, int64_t nx, int64_t ny) {
+  int64_t full = iy * (3 * nx - 2) + nx * (iy > 0 ? iy - 1 : 0) + nx * (iy < ny - 1 ? iy : ny - 1);
+  int64_t per = 1 + (iy > 0) + (iy < ny - 1);
+  int64_t part = ix * per + (ix > 0 ? ix - 1 : 0) + (ix < nx - 1 ? ix : nx - 1);
+  return full + part;
+}
+
+// datasets.py:108-143 (face means, 1/h^2 scaling, boundary faces keep the node's value).
+__global__ void k_poisson2d(int64_t nx, int64_t ny, const double* __restrict__ a, int64_t row0,
+                            int64_t nnz0, int32_t* offs, int32_t* cols, double* vals) {
+  const int64_t n = nx * ny;
+  const double ihx2 = (double)((nx + 1) * (nx + 1)), ihy2 = (double)((ny + 1) * (ny + 1));
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i == n) { offs[row0 + n] = (int32_t)(nnz0 + 5 * n - 2 * nx - 2 * ny); continue; }
+    const int64_t ix = i % nx, iy = i / nx;
+    const double c = a[i];
+    const double w = ix > 0 ? mul(0.5, add(c, a[i - 1])) : c;
+    const double e = ix < nx - 1 ? mul(0.5, add(c, a[i + 1])) : c;
+    const double s = iy > 0 ? mul(0.5, add(c, a[i - nx])) : c;
+    const double nn = iy < ny - 1 ? mul(0.5, add(c, a[i + nx])) : c;
+    int64_t k = nnz0 + before2d(ix, iy, nx, ny);
+    const int64_t gi = row0 + i;
+    offs[gi] = (int32_t)k;
+    if (iy > 0) { cols[k] = (int32_t)(gi - nx); vals[k] = mul(-s, ihy2); ++k; }
+    if (ix > 0) { cols[k] = (int32_t)(gi - 1); vals[k] = mul(-w, ihx2); ++k; }
+    cols[k] = (int32_t)gi; vals[k] = add(mul(add(w, e), ihx2), mul(add(s, nn), ihy2)); ++k;
+    if (ix < nx - 1) { cols[k] = (int32_t)(gi + 1); vals[k] = mul(-e, ihx2); ++k; }
+    if (iy < ny - 1) { cols[k] = (int32_t)(gi + nx); vals[k] = mul(-nn, ihy2); ++k; }
+  }
+}
+
+__device__ __forceinline__ int64_t before3d(int64_t ix, int64_t iy, int64_t iz, int64_t nx,
+                                            int64_t ny, int64_t nz) {
+  const int64_t plane = nx * ny + 2 * (nx - 1) * ny + 2 * nx * (ny - 1);
+  const int64_t nxy = nx * ny;
+  int64_t full = iz * plane + nxy * (iz > 0 ? iz - 1 : 0) + nxy * (iz < nz - 1 ? iz : nz - 1);
+  const int64_t zc = (iz > 0) + (iz < nz - 1);
+  int64_t rows = iy * (3 * nx - 2) + nx * (iy > 0 ? iy - 1 : 0) + nx * (iy < ny - 1 ? iy : ny - 1) +
+                 iy * nx * zc;
+  const int64_t per = 1 + (iy > 0) + (iy < ny - 1) + zc;
+  int64_t part = ix * per + (ix > 0 ? ix - 1 : 0) + (ix < nx - 1 ? ix : nx - 1);
+  return full + rows + part;
+}
+
+__global__ void k_poisson3d(int64_t nx, int64_t ny, int64_t nz, int32_t* offs, int32_t* cols,
+                            double* vals) {
+  const int64_t nxy = nx * ny, n = nxy * nz;
+  const double ihx2 = (double)((nx + 1) * (nx + 1)), ihy2 = (double)((ny + 1) * (ny + 1)),
+               ihz2 = (double)((nz + 1) * (nz + 1));
+  const double dv = add(add(mul(2.0, ihx2), mul(2.0, ihy2)), mul(2.0, ihz2));
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i == n) { offs[n] = (int32_t)(7 * n - 2 * (nxy * nz / nx) - 2 * (nxy * nz / ny) - 2 * nxy); continue; }
+    const int64_t ix = i % nx, iy = (i / nx) % ny, iz = i / nxy;
+    int64_t k = before3d(ix, iy, iz, nx, ny, nz);
+    offs[i] = (int32_t)k;
+    if (iz > 0) { cols[k] = (int32_t)(i - nxy); vals[k] = -ihz2; ++k; }
+    if (iy > 0) { cols[k] = (int32_t)(i - nx); vals[k] = -ihy2; ++k; }
+    if (ix > 0) { cols[k] = (int32_t)(i - 1); vals[k] = -ihx2; ++k; }
+    cols[k] = (int32_t)i; vals[k] = dv; ++k;
+    if (ix < nx - 1) { cols[k] = (int32_t)(i + 1); vals[k] = -ihx2; ++k; }
+    if (iy < ny - 1) { cols[k] = (int32_t)(i + nx); vals[k] = -ihy2; ++k; }
+    if (iz < nz - 1) { cols[k] = (int32_t)(i + nxy); vals[k] = -ihz2; ++k; }
+  }
+}
+
+static inline int grid_for(int64_t n, int threads = 256) {
+  int64_t g = ceil_div(n > 0 ? n : 1, threads);
+  return (int)(g > 148 * 32 ? 148 * 32 : g);
+}
+
+}  // namespace sg
+
+using namespace sg;
+
+extern "C" int sg_matrix_norm(const double* vals, int64_t nnz, int kind, double* norm_out,
+                              void* ws, size_t* ws_bytes, void* stream) {
+  Carve c(ws);
+  unsigned long long* limbs = c.take<unsigned long long>(NLIMB);
+  unsigned int* flags = c.take<unsigned int>(1);
+  if (!ws) { *ws_bytes = c.off; return SG_OK; }
+  if (nnz <= 0) { set_error("norm of a matrix with no stored entries"); return SG_EINVAL; }
+  if (kind < 0 || kind > 2) { set_error("unknown norm kind"); return SG_EINVAL; }
+  cudaStream_t s = as_stream(stream);
+  SG_CUDA(cudaMemsetAsync(limbs, 0, NLIMB * sizeof(unsigned long long), s));
+  SG_CUDA(cudaMemsetAsync(flags, 0, sizeof(unsigned int), s));
+  k_exact_accum<<<grid_for(nnz), 256, 0, s>>>(vals, nnz, kind == 1 ? 1 : 0, limbs, flags);
+  SG_LAUNCH_CHECK("k_exact_accum");
+  k_norm_finish<<<1, 32, 0, s>>>(limbs, flags, nnz, kind, norm_out);
+  SG_LAUNCH_CHECK("k_norm_finish");
+  return SG_OK;
+}
+
+extern "C" int sg_graph_features(int64_t n, int64_t row0, const int32_t* offs, const int32_t* cols,
+                                 const double* vals, const double* norm, int family, int64_t nx,
+                                 int64_t ny, const double* coeff, double coeff_mean,
+                                 double* node_out, double* edge_out, void* stream) {
+  if (family == 1 && nx * ny != n) { set_error("meta grid does not match matrix size"); return SG_EINVAL; }
+  if (n <= 0) return SG_OK;
+  k_graph_features<<<grid_for(n), 256, 0, as_stream(stream)>>>(n, row0, offs, cols, vals, norm, family,
+                                                               nx, ny, coeff, coeff_mean,
+                                                               node_out, edge_out);
+  SG_LAUNCH_CHECK("k_graph_features");
+  return SG_OK;
+}
+
+extern "C" int sg_gen_poisson2d(int64_t nx, int64_t ny, const double* coeff, int64_t row0,
+                                int64_t nnz0, int32_t* offs, int32_t* cols, double* vals,
+                                void* stream) {
+  if (nx < 1 || ny < 1) { set_error("grid dimensions must be positive"); return SG_EINVAL; }
+  if (nnz0 + 5 * nx * ny >= (int64_t)INT32_MAX || row0 + nx * ny >= (int64_t)INT32_MAX) {
+    set_error("grid too large for int32 indices");
+    return SG_EINVAL;
+  }
+  k_poisson2d<<<grid_for(nx * ny + 1), 256, 0, as_stream(stream)>>>(nx, ny, coeff, row0, nnz0, offs, cols, vals);
+  SG_LAUNCH_CHECK("k_poisson2d");
+  return SG_OK;
+}
+
+extern "C" int sg_gen_poisson3d(int64_t nx, int64_t ny, int64_t nz, int32_t* offs, int32_t* cols,
+                                double* vals, void* stream) {
+  if (nx < 1 || ny < 1 || nz < 1) { set_error("grid dimensions must be positive"); return SG_EINVAL; }
+  if (7 * nx * ny * nz >= (int64_t)INT32_MAX) { set_error("grid too large for int32 indices"); return SG_EINVAL; }
+  k_poisson3d<<<grid_for(nx * ny * nz + 1), 256, 0, as_stream(stream)>>>(nx, ny, nz, offs, cols, vals);
+  SG_LAUNCH_CHECK("k_poisson3d");
+  return SG_OK;
+}

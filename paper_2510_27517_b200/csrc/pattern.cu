@@ -1,0 +1,366 @@
+// Sparsity-pattern layer: COO->CSR, validation, transpose,
+// symmetry, row expansion.  Integer work, bit-exact with the reference (sparse.py).
+//
+// Sorting uses CUB's radix sort (header library shipped with the CUDA toolkit) keyed on the
+// 64-bit (major, minor) pair — a stable sort, so the result equals np.lexsort exactly.  For the
+// symmetric patterns every graph in this library has (graphfeat.py:77-78), the transpose needs
+// no sort at all: sg_csr_transpose detects symmetry and computes the permutation with one
+// binary search per entry (the "partner" of (i,j) is the position of (j,i)).
+#include <cub/device/device_radix_sort.cuh>
+
+#include "common.cuh"
+
+namespace sg {
+
+__global__ void k_narrow(const int64_t* __restrict__ in, int32_t* __restrict__ out, int64_t n,
+                         int64_t lo, int64_t hi, int64_t shift, unsigned long long* bad) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    int64_t v = in[k];
+    if (v < lo || v >= hi) atomicMin(bad, (unsigned long long)k);
+    out[k] = (int32_t)(v + shift);
+  }
+}
+
+__global__ void k_coo_keys(const int64_t* __restrict__ rows, const int64_t* __restrict__ cols,
+                           int64_t nnz, int64_t n_rows, int64_t n_cols, uint64_t* keys,
+                           int32_t* idx, unsigned long long* bad) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = rows[k], c = cols[k];
+    unsigned long long code = 0;
+    if (r < 0 || r >= n_rows) code = 1;        // "row index out of range"
+    else if (c < 0 || c >= n_cols) code = 2;   // "column index out of range"
+    if (code) atomicOr(bad, code);
+    keys[k] = (uint64_t)(r < 0 ? 0 : r) * (uint64_t)n_cols + (uint64_t)(c < 0 ? 0 : c);
+    idx[k] = (int32_t)k;
+  }
+}
+
+// offs[r] = first sorted position whose major index is >= r (every r written exactly once).
+__global__ void k_offsets_from_sorted(const uint64_t* __restrict__ keys, int64_t nnz,
+                                      int64_t n_major, uint64_t minor_dim, int32_t* offs) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k <= nnz;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    int64_t prev = k > 0 ? (int64_t)(keys[k - 1] / minor_dim) : -1;
+    int64_t cur = k < nnz ? (int64_t)(keys[k] / minor_dim) : n_major;
+    for (int64_t r = prev + 1; r <= cur; ++r) offs[r] = (int32_t)k;
+  }
+}
+
+__global__ void k_coo_finish(const uint64_t* __restrict__ keys, const int32_t* __restrict__ idx,
+                             const double* __restrict__ vals, int64_t nnz, uint64_t n_cols,
+                             int32_t* cols_out, double* vals_out, unsigned long long* first_dup) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t key = keys[k];
+    cols_out[k] = (int32_t)(key % n_cols);
+    vals_out[k] = vals[idx[k]];
+    if (k + 1 < nnz && keys[k + 1] == key) atomicMin(first_dup, (unsigned long long)k);
+  }
+}
+
+// Validation bits, reported in the reference's check order (sparse.py:28-43).
+enum { V_OFF0 = 1, V_LAST = 2, V_MONO = 4, V_RANGE = 8, V_ORDER = 16 };
+
+__global__ void k_validate(int64_t n_rows, int64_t n_cols, int64_t nnz,
+                           const int32_t* __restrict__ offs, const int32_t* __restrict__ cols,
+                           unsigned int* bits) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_rows;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    unsigned int b = 0;
+    int64_t lo = offs[i], hi = offs[i + 1];
+    if (i == 0 && lo != 0) b |= V_OFF0;
+    if (i == n_rows - 1 && hi != nnz) b |= V_LAST;
+    if (hi < lo) b |= V_MONO;
+    if (lo >= 0 && hi <= nnz && lo <= hi) {
+      for (int64_t k = lo; k < hi; ++k) {
+        int32_t c = cols[k];
+        if (c < 0 || c >= n_cols) b |= V_RANGE;
+        if (k > lo && c <= cols[k - 1]) b |= V_ORDER;
+      }
+    }
+    if (b) atomicOr(bits, b);
+  }
+}
+
+__global__ void k_row_expand(int64_t n_rows, const int32_t* __restrict__ offs, int32_t* rows) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_rows;
+       i += (int64_t)gridDim.x * blockDim.x)
+    for (int32_t k = offs[i]; k < offs[i + 1]; ++k) rows[k] = (int32_t)i;
+}
+
+// For entry k = (i, j): position of (j, i) by binary search in row j, or -1 if absent.
+__global__ void k_partner(int64_t n, const int32_t* __restrict__ offs,
+                          const int32_t* __restrict__ cols, int32_t* partner,
+                          unsigned int* missing) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    for (int32_t k = offs[i]; k < offs[i + 1]; ++k) {
+      int32_t j = cols[k];
+      int32_t lo = offs[j], hi = offs[j + 1];
+      while (lo < hi) {
+        int32_t mid = (lo + hi) >> 1;
+        if (cols[mid] < (int32_t)i) lo = mid + 1; else hi = mid;
+      }
+      bool found = lo < offs[j + 1] && cols[lo] == (int32_t)i;
+      partner[k] = found ? lo : -1;
+      if (!found) atomicOr(missing, 1u);
+    }
+  }
+}
+
+__global__ void k_transpose_keys(int64_t n_rows, int64_t n_cols, const int32_t* __restrict__ offs,
+                                 const int32_t* __restrict__ cols, uint64_t* keys, int32_t* idx) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_rows;
+       i += (int64_t)gridDim.x * blockDim.x)
+    for (int32_t k = offs[i]; k < offs[i + 1]; ++k) {
+      keys[k] = (uint64_t)cols[k] * (uint64_t)n_rows + (uint64_t)i;
+      idx[k] = k;
+    }
+}
+
+__global__ void k_transpose_finish(const uint64_t* __restrict__ keys, int64_t nnz, uint64_t n_rows,
+                                   int32_t* cols_t) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz;
+       k += (int64_t)gridDim.x * blockDim.x)
+    cols_t[k] = (int32_t)(keys[k] % n_rows);
+}
+
+__global__ void k_gather(const double* __restrict__ in, const int32_t* __restrict__ perm,
+                         double* __restrict__ out, int64_t n) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x)
+    out[k] = in[perm[k]];
+}
+
+__global__ void k_copy_i32(const int32_t* __restrict__ in, int32_t* __restrict__ out, int64_t n) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x)
+    out[k] = in[k];
+}
+
+__global__ void k_diagonal(int64_t n, const int32_t* __restrict__ offs,
+                           const int32_t* __restrict__ cols, const double* __restrict__ vals,
+                           double* diag, int32_t* present) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double d = 0.0;
+    int32_t p = 0;
+    for (int32_t k = offs[i]; k < offs[i + 1]; ++k)
+      if (cols[k] == (int32_t)i) { d = vals[k]; p = 1; }
+    diag[i] = d;
+    if (present) present[i] = p;
+  }
+}
+
+static inline int grid_for(int64_t n, int threads = 256) {
+  int64_t g = ceil_div(n > 0 ? n : 1, threads);
+  return (int)(g > 148 * 32 ? 148 * 32 : g);
+}
+
+static int bits_for(uint64_t maxkey) {
+  int b = 1;
+  while (b < 64 && (maxkey >> b) != 0) ++b;
+  return b;
+}
+
+}  // namespace sg
+
+using namespace sg;
+
+extern "C" int sg_narrow_index(const int64_t* in, int32_t* out, int64_t n, int64_t lo, int64_t hi,
+                               int64_t shift, void* ws, size_t* ws_bytes, void* stream) {
+  Carve c(ws);
+  unsigned long long* bad = c.take<unsigned long long>(1);
+  if (!ws) { *ws_bytes = c.off; return SG_OK; }
+  if (*ws_bytes < c.off) { set_error("workspace too small"); return SG_EINVAL; }
+  cudaStream_t s = as_stream(stream);
+  if (n == 0) return SG_OK;
+  SG_CUDA(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), s));
+  k_narrow<<<grid_for(n), 256, 0, s>>>(in, out, n, lo, hi, shift, bad);
+  SG_LAUNCH_CHECK("k_narrow");
+  unsigned long long h = 0;
+  SG_CUDA(cudaMemcpyAsync(&h, bad, sizeof(h), cudaMemcpyDeviceToHost, s));
+  SG_CUDA(cudaStreamSynchronize(s));
+  if (h != ~0ull) {
+    set_error("index out of range at position %llu", h);
+    return SG_EINVAL;
+  }
+  return SG_OK;
+}
+
+extern "C" int sg_csr_from_coo(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* rows,
+                               const int64_t* cols, const double* vals, int32_t* offs_out,
+                               int32_t* cols_out, double* vals_out, int64_t* dup_host, void* ws,
+                               size_t* ws_bytes, void* stream) {
+  if (n_rows < 0 || n_cols < 0 || nnz < 0 || nnz >= (int64_t)INT32_MAX || n_rows >= INT32_MAX ||
+      n_cols >= INT32_MAX) {
+    set_error("sizes out of the supported int32 index range");
+    return SG_EINVAL;
+  }
+  const uint64_t maxkey = (uint64_t)(n_rows > 0 ? n_rows : 1) * (uint64_t)(n_cols > 0 ? n_cols : 1);
+  const int end_bit = bits_for(maxkey);
+  size_t cub_bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, (uint64_t*)nullptr, (uint64_t*)nullptr,
+                                  (int32_t*)nullptr, (int32_t*)nullptr, (int)nnz, 0, end_bit);
+  Carve c(ws);
+  uint64_t* k_in = c.take<uint64_t>(nnz + 1);
+  uint64_t* k_out = c.take<uint64_t>(nnz + 1);
+  int32_t* i_in = c.take<int32_t>(nnz + 1);
+  int32_t* i_out = c.take<int32_t>(nnz + 1);
+  unsigned long long* flags = c.take<unsigned long long>(2);
+  void* cub_tmp = c.take<char>(cub_bytes);
+  if (!ws) { *ws_bytes = c.off; return SG_OK; }
+  if (*ws_bytes < c.off) { set_error("workspace too small"); return SG_EINVAL; }
+  cudaStream_t s = as_stream(stream);
+  SG_CUDA(cudaMemsetAsync(flags, 0, sizeof(unsigned long long), s));
+  SG_CUDA(cudaMemsetAsync(flags + 1, 0xff, sizeof(unsigned long long), s));
+  if (nnz > 0) {
+    k_coo_keys<<<grid_for(nnz), 256, 0, s>>>(rows, cols, nnz, n_rows, n_cols, k_in, i_in, flags);
+    SG_LAUNCH_CHECK("k_coo_keys");
+    unsigned long long bad = 0;
+    SG_CUDA(cudaMemcpyAsync(&bad, flags, sizeof(bad), cudaMemcpyDeviceToHost, s));
+    SG_CUDA(cudaStreamSynchronize(s));
+    if (bad & 1) { set_error("row index out of range"); return SG_EINVAL; }
+    if (bad & 2) { set_error("column index out of range"); return SG_EINVAL; }
+    size_t tb = cub_bytes;
+    SG_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, tb, k_in, k_out, i_in, i_out, (int)nnz, 0,
+                                            end_bit, s));
+    k_coo_finish<<<grid_for(nnz), 256, 0, s>>>(k_out, i_out, vals, nnz, (uint64_t)n_cols,
+                                               cols_out, vals_out, flags + 1);
+    SG_LAUNCH_CHECK("k_coo_finish");
+    unsigned long long dup = 0;
+    SG_CUDA(cudaMemcpyAsync(&dup, flags + 1, sizeof(dup), cudaMemcpyDeviceToHost, s));
+    SG_CUDA(cudaStreamSynchronize(s));
+    if (dup != ~0ull) {
+      uint64_t key = 0;
+      SG_CUDA(cudaMemcpy(&key, k_out + dup, sizeof(key), cudaMemcpyDeviceToHost));
+      dup_host[0] = (int64_t)(key / (uint64_t)n_cols);
+      dup_host[1] = (int64_t)(key % (uint64_t)n_cols);
+      set_error("duplicate entry at (%lld, %lld)", (long long)dup_host[0], (long long)dup_host[1]);
+      return SG_EDUPLICATE;
+    }
+  }
+  k_offsets_from_sorted<<<grid_for(nnz + 1), 256, 0, s>>>(k_out, nnz, n_rows,
+                                                          (uint64_t)(n_cols > 0 ? n_cols : 1),
+                                                          offs_out);
+  SG_LAUNCH_CHECK("k_offsets_from_sorted");
+  SG_CUDA(cudaStreamSynchronize(s));
+  return SG_OK;
+}
+
+extern "C" int sg_csr_validate(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* offs,
+                               const int32_t* cols, void* ws, size_t* ws_bytes, void* stream) {
+  Carve c(ws);
+  unsigned int* bits = c.take<unsigned int>(1);
+  if (!ws) { *ws_bytes = c.off; return SG_OK; }
+  cudaStream_t s = as_stream(stream);
+  SG_CUDA(cudaMemsetAsync(bits, 0, sizeof(unsigned int), s));
+  unsigned int h = 0;
+  if (n_rows > 0) {
+    k_validate<<<grid_for(n_rows), 256, 0, s>>>(n_rows, n_cols, nnz, offs, cols, bits);
+    SG_LAUNCH_CHECK("k_validate");
+    SG_CUDA(cudaMemcpyAsync(&h, bits, sizeof(h), cudaMemcpyDeviceToHost, s));
+    SG_CUDA(cudaStreamSynchronize(s));
+  } else if (nnz != 0) {
+    h = V_LAST;
+  }
+  if (h & V_OFF0) { set_error("row_offsets[0] must be 0"); return SG_EINVAL; }
+  if (h & V_LAST) { set_error("row_offsets[-1] must equal nnz"); return SG_EINVAL; }
+  if (h & V_MONO) { set_error("row_offsets must be nondecreasing"); return SG_EINVAL; }
+  if (h & V_RANGE) { set_error("column index out of range"); return SG_EINVAL; }
+  if (h & V_ORDER) { set_error("col_indices must be strictly increasing within each row"); return SG_EINVAL; }
+  return SG_OK;
+}
+
+extern "C" int sg_row_expand(int64_t n_rows, const int32_t* offs, int32_t* rows_out, void* stream) {
+  if (n_rows <= 0) return SG_OK;
+  k_row_expand<<<grid_for(n_rows), 256, 0, as_stream(stream)>>>(n_rows, offs, rows_out);
+  SG_LAUNCH_CHECK("k_row_expand");
+  return SG_OK;
+}
+
+extern "C" int sg_gather_f64(const double* in, const int32_t* perm, double* out, int64_t n,
+                             void* stream) {
+  if (n <= 0) return SG_OK;
+  k_gather<<<grid_for(n), 256, 0, as_stream(stream)>>>(in, perm, out, n);
+  SG_LAUNCH_CHECK("k_gather");
+  return SG_OK;
+}
+
+extern "C" int sg_csr_diagonal(int64_t n, const int32_t* offs, const int32_t* cols,
+                               const double* vals, double* diag_out, int32_t* present_out,
+                               void* stream) {
+  if (n <= 0) return SG_OK;
+  k_diagonal<<<grid_for(n), 256, 0, as_stream(stream)>>>(n, offs, cols, vals, diag_out, present_out);
+  SG_LAUNCH_CHECK("k_diagonal");
+  return SG_OK;
+}
+
+extern "C" int sg_pattern_is_symmetric(int64_t n, int64_t nnz, const int32_t* offs,
+                                       const int32_t* cols, int32_t* result_host, void* ws,
+                                       size_t* ws_bytes, void* stream) {
+  Carve c(ws);
+  int32_t* partner = c.take<int32_t>(nnz + 1);
+  unsigned int* missing = c.take<unsigned int>(1);
+  if (!ws) { *ws_bytes = c.off; return SG_OK; }
+  cudaStream_t s = as_stream(stream);
+  SG_CUDA(cudaMemsetAsync(missing, 0, sizeof(unsigned int), s));
+  if (n > 0) {
+    k_partner<<<grid_for(n), 256, 0, s>>>(n, offs, cols, partner, missing);
+    SG_LAUNCH_CHECK("k_partner");
+  }
+  unsigned int h = 0;
+  SG_CUDA(cudaMemcpyAsync(&h, missing, sizeof(h), cudaMemcpyDeviceToHost, s));
+  SG_CUDA(cudaStreamSynchronize(s));
+  *result_host = h ? 0 : 1;
+  return SG_OK;
+}
+
+extern "C" int sg_csr_transpose(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* offs,
+                                const int32_t* cols, int32_t* offs_t, int32_t* cols_t,
+                                int32_t* perm, void* ws, size_t* ws_bytes, void* stream) {
+  const uint64_t maxkey = (uint64_t)(n_rows > 0 ? n_rows : 1) * (uint64_t)(n_cols > 0 ? n_cols : 1);
+  const int end_bit = bits_for(maxkey);
+  size_t cub_bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, (uint64_t*)nullptr, (uint64_t*)nullptr,
+                                  (int32_t*)nullptr, (int32_t*)nullptr, (int)nnz, 0, end_bit);
+  Carve c(ws);
+  uint64_t* k_in = c.take<uint64_t>(nnz + 1);
+  uint64_t* k_out = c.take<uint64_t>(nnz + 1);
+  int32_t* i_in = c.take<int32_t>(nnz + 1);
+  unsigned int* missing = c.take<unsigned int>(1);
+  void* cub_tmp = c.take<char>(cub_bytes);
+  if (!ws) { *ws_bytes = c.off; return SG_OK; }
+  if (*ws_bytes < c.off) { set_error("workspace too small"); return SG_EINVAL; }
+  cudaStream_t s = as_stream(stream);
+  // Fast path: square symmetric pattern => pattern(A^T) == pattern(A), perm = partner map.
+  if (n_rows == n_cols && n_rows > 0) {
+    SG_CUDA(cudaMemsetAsync(missing, 0, sizeof(unsigned int), s));
+    k_partner<<<grid_for(n_rows), 256, 0, s>>>(n_rows, offs, cols, perm, missing);
+    SG_LAUNCH_CHECK("k_partner");
+    unsigned int h = 1;
+    SG_CUDA(cudaMemcpyAsync(&h, missing, sizeof(h), cudaMemcpyDeviceToHost, s));
+    SG_CUDA(cudaStreamSynchronize(s));
+    if (!h) {
+      k_copy_i32<<<grid_for(n_rows + 1), 256, 0, s>>>(offs, offs_t, n_rows + 1);
+      k_copy_i32<<<grid_for(nnz), 256, 0, s>>>(cols, cols_t, nnz);
+      SG_LAUNCH_CHECK("k_copy_i32");
+      return SG_OK;
+    }
+  }
+  if (nnz > 0) {
+    k_transpose_keys<<<grid_for(n_rows), 256, 0, s>>>(n_rows, n_cols, offs, cols, k_in, i_in);
+    SG_LAUNCH_CHECK("k_transpose_keys");
+    size_t tb = cub_bytes;
+    SG_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, tb, k_in, k_out, i_in, perm, (int)nnz, 0,
+                                            end_bit, s));
+    k_transpose_finish<<<grid_for(nnz), 256, 0, s>>>(k_out, nnz, (uint64_t)n_rows, cols_t);
+    SG_LAUNCH_CHECK("k_transpose_finish");
+  }
+  k_offsets_from_sorted<<<grid_for(nnz + 1), 256, 0, s>>>(k_out, nnz, n_cols,
+                                                          (uint64_t)(n_rows > 0 ? n_rows : 1), offs_t);
+  SG_LAUNCH_CHECK("k_offsets_from_sorted");
+  return SG_OK;
+}

@@ -1,0 +1,74 @@
+// Standalone SpMV entry points (sparse.py:186-201, precond.py:143-145).
+#include "spmv.cuh"
+
+namespace sg {
+
+constexpr int kRows = 256;
+constexpr int kCap = 2048;
+
+template <int ORDER>
+__global__ void __launch_bounds__(kRows) k_spmv(int64_t n, const int32_t* __restrict__ offs,
+                                                const int32_t* __restrict__ cols,
+                                                const double* __restrict__ vals,
+                                                const double* __restrict__ x, double* __restrict__ y) {
+  __shared__ RowTile<kRows, kCap> t;
+  const int64_t r0 = (int64_t)blockIdx.x * kRows;
+  const int64_t r1 = r0 + kRows < n ? r0 + kRows : n;
+  stage_rows(t, r0, r1, offs, cols, vals);
+  const int lr = threadIdx.x;
+  if (r0 + lr < r1)
+    y[r0 + lr] = tile_row_dot<ORDER>(t, lr, cols, vals, [&](int32_t j) { return __ldg(x + j); });
+}
+
+// s = spmv(G, t) + eps * r
+__global__ void __launch_bounds__(kRows) k_apply_g(int64_t n, const int32_t* __restrict__ offs,
+                                                   const int32_t* __restrict__ cols,
+                                                   const double* __restrict__ vals,
+                                                   const double* __restrict__ tv, double eps,
+                                                   const double* __restrict__ r, double* __restrict__ s) {
+  __shared__ RowTile<kRows, kCap> t;
+  const int64_t r0 = (int64_t)blockIdx.x * kRows;
+  const int64_t r1 = r0 + kRows < n ? r0 + kRows : n;
+  stage_rows(t, r0, r1, offs, cols, vals);
+  const int lr = threadIdx.x;
+  if (r0 + lr < r1) {
+    const double y = tile_row_dot<kOrderNumpy>(t, lr, cols, vals, [&](int32_t j) { return __ldg(tv + j); });
+    s[r0 + lr] = add(y, mul(eps, r[r0 + lr]));
+  }
+}
+
+}  // namespace sg
+
+using namespace sg;
+
+extern "C" int sg_spmv(int64_t n_rows, const int32_t* offs, const int32_t* cols, const double* vals,
+                       const double* x, double* y, void* stream) {
+  if (n_rows <= 0) return SG_OK;
+  k_spmv<kOrderNumpy><<<(unsigned)ceil_div(n_rows, kRows), kRows, 0, as_stream(stream)>>>(
+      n_rows, offs, cols, vals, x, y);
+  SG_LAUNCH_CHECK("k_spmv<numpy>");
+  return SG_OK;
+}
+
+extern "C" int sg_spmv_seq(int64_t n_rows, const int32_t* offs, const int32_t* cols,
+                           const double* vals, const double* x, double* y, void* stream) {
+  if (n_rows <= 0) return SG_OK;
+  k_spmv<kOrderSeq><<<(unsigned)ceil_div(n_rows, kRows), kRows, 0, as_stream(stream)>>>(
+      n_rows, offs, cols, vals, x, y);
+  SG_LAUNCH_CHECK("k_spmv<seq>");
+  return SG_OK;
+}
+
+extern "C" int sg_learned_apply(int64_t n, const int32_t* g_offs, const int32_t* g_cols,
+                                const double* g_vals, const int32_t* gt_offs,
+                                const int32_t* gt_cols, const double* gt_vals, double eps,
+                                const double* r, double* t_ws, double* s_out, void* stream) {
+  if (n <= 0) return SG_OK;
+  cudaStream_t s = as_stream(stream);
+  const unsigned g = (unsigned)ceil_div(n, kRows);
+  k_spmv<kOrderSeq><<<g, kRows, 0, s>>>(n, gt_offs, gt_cols, gt_vals, r, t_ws);
+  SG_LAUNCH_CHECK("k_spmv<seq>");
+  k_apply_g<<<g, kRows, 0, s>>>(n, g_offs, g_cols, g_vals, t_ws, eps, r, s_out);
+  SG_LAUNCH_CHECK("k_apply_g");
+  return SG_OK;
+}

@@ -1,0 +1,349 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the reference's golden vectors and the
+CPU oracle.  Bars (BASELINE.json north_star): patterns / indices / SpMV / features bit-exact;
+G within 1e-10 relative (fp64, floored at 1e-3 max|G|); PCG iteration counts within +-2%."""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import spaigraph_ref as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2510_27517_b200 as P  # noqa: E402
+from paper_2510_27517_b200 import _lib  # noqa: E402
+
+G_TOL = 1e-10
+
+
+def rel_floor(a, b):
+    b = np.asarray(b)
+    scale = np.maximum(np.abs(b), 1e-3 * np.max(np.abs(b)))
+    return float(np.max(np.abs(np.asarray(a) - b) / scale))
+
+
+def csr(g, p):
+    return P.SparseMatrix(int(g[p + "_n_rows"]), int(g[p + "_n_cols"]), g[p + "_offs"], g[p + "_cols"],
+                          g[p + "_vals"])
+
+
+def test_library_loaded_from_tree():
+    lib = _lib.lib()
+    assert lib.sg_abi_version() == 1
+    assert _lib.LIB_PATH.endswith("paper_2510_27517_b200/libspaigraph_b200.so")
+
+
+# --------------------------------------------------------------------------- patterns (a2-a4)
+def test_from_coo_bit_exact(g_sparse):
+    g = g_sparse
+    B = P.SparseMatrix.from_coo(40, 30, g["trip_rows"], g["trip_cols"], g["trip_vals"])
+    assert np.array_equal(B.row_offsets, g["coo_offs"])
+    assert np.array_equal(B.col_indices, g["coo_cols"])
+    assert np.array_equal(B.values, g["coo_vals"])
+
+
+def test_from_coo_rejects():
+    with pytest.raises(ValueError, match="duplicate"):
+        P.SparseMatrix.from_coo(2, 2, [0, 0], [1, 1], [1.0, 2.0])
+    with pytest.raises(ValueError):
+        P.SparseMatrix.from_coo(2, 2, [0], [2], [1.0])
+    with pytest.raises(ValueError):
+        P.SparseMatrix.from_coo(2, 2, [-1], [0], [1.0])
+
+
+def test_structural_invariants_enforced():
+    with pytest.raises(ValueError):
+        P.SparseMatrix(2, 2, np.array([0, 1]), np.array([0]), np.array([1.0]))
+    with pytest.raises(ValueError):
+        P.SparseMatrix(2, 2, np.array([0, 2, 2]), np.array([1, 0]), np.array([1.0, 2.0]))
+    with pytest.raises(ValueError):
+        P.SparseMatrix(1, 2, np.array([0, 2]), np.array([0, 0]), np.array([1.0, 2.0]))
+    with pytest.raises(ValueError):
+        P.SparseMatrix(1, 2, np.array([0, 1]), np.array([5]), np.array([1.0]))
+
+
+def test_transpose_bit_exact(g_sparse):
+    g = g_sparse
+    B = csr(g, "coo")
+    T = B.transpose()
+    assert np.array_equal(T.row_offsets, g["cooT_offs"])
+    assert np.array_equal(T.col_indices, g["cooT_cols"])
+    assert np.array_equal(T.values, g["cooT_vals"])
+    for tag in ("s15", "s60", "s300"):  # symmetric fast path (partner permutation)
+        A = csr(g, tag)
+        n = A.n_rows
+        ot, ct, vt, _ = O.transpose(n, n, g[tag + "_offs"], g[tag + "_cols"], g[tag + "_vals"])
+        T = A.transpose()
+        assert np.array_equal(T.row_offsets, ot) and np.array_equal(T.col_indices, ct)
+        assert np.array_equal(T.values, vt)
+
+
+def test_is_symmetric(g_sparse):
+    g = g_sparse
+    assert csr(g, "s60").pattern.is_symmetric()
+    asym = P.SparseMatrix(2, 2, g["asym_offs"], g["asym_cols"], np.ones(3))
+    assert not asym.pattern.is_symmetric()
+    assert not P.SparseMatrix.from_coo(2, 3, [0], [0], [1.0]).pattern.is_symmetric()
+
+
+# --------------------------------------------------------------------------- SpMV family (a8-a11)
+def test_spmv_family_bit_exact(g_sparse):
+    g = g_sparse
+    B = csr(g, "coo")
+    assert np.array_equal(P.spmv(B, g["x30"]), g["coo_spmv"])
+    assert np.array_equal(P.spmv_transpose(B, g["x40"]), g["coo_spmvT"])
+    Lm = csr(g, "long")  # rows of ~420 entries: pairwise 8-accumulator blocks + the >128 split
+    assert np.array_equal(P.spmv(Lm, g["x700"]), g["long_spmv"])
+    for tag in ("s15", "s60", "s300"):
+        A = csr(g, tag)
+        r = g[tag + "_r"]
+        Gr = A.with_values(g[tag + "_Grand"])
+        assert np.array_equal(P.spmv(A, r), g[tag + "_spmv"])
+        assert np.array_equal(P.spmv_transpose(Gr, r), g[tag + "_spmvT"])
+        assert np.array_equal(P.build_learned_spai(Gr, 2e-3).apply(r), g[tag + "_apply"])
+
+
+def test_spmv_large_random_rows_vs_oracle():
+    rng = np.random.default_rng(3)
+    n = 5000
+    lens = rng.integers(0, 40, size=n)
+    lens[::97] = 300  # a few long rows
+    offs = np.concatenate([[0], np.cumsum(lens)])
+    cols = np.concatenate([np.sort(rng.choice(4000, size=k, replace=False)) for k in lens])
+    vals = rng.standard_normal(len(cols))
+    A = P.SparseMatrix(n, 4000, offs, cols, vals)
+    x = rng.standard_normal(4000)
+    assert np.array_equal(P.spmv(A, x), O.spmv(offs, cols, vals, x))
+    y = rng.standard_normal(n)
+    assert np.array_equal(P.spmv_transpose(A, y), O.spmv_transpose(4000, offs, cols, vals, y))
+
+
+def test_norms_bit_exact(g_sparse):
+    g = g_sparse
+    B = csr(g, "coo")
+    assert P.mean_abs_nonzero_norm(B) == g["coo_norm"]
+    for tag in ("s15", "s60", "s300"):
+        A = csr(g, tag)
+        for kind in ("mean_abs_nonzero", "frobenius", "entrywise_l1"):
+            assert P.matrix_norm(A, kind) == g[tag + "_mnorm_" + kind]
+    rng = np.random.default_rng(11)  # wide dynamic range: exact summation matters
+    v = rng.standard_normal(100000) * np.exp(rng.uniform(-300, 300, 100000))
+    A = P.SparseMatrix(1, 100000, np.array([0, 100000]), np.arange(100000), v)
+    assert P.mean_abs_nonzero_norm(A) == math.fsum(np.abs(v)) / len(v)
+
+
+# --------------------------------------------------------------------------- generators + features
+def test_generators_bit_exact(g_c1, g_heat):
+    A, meta = P.gen_poisson2d(64, 64)
+    assert np.array_equal(A.row_offsets, g_c1["A_offs"]) and np.array_equal(A.col_indices, g_c1["A_cols"])
+    assert np.array_equal(A.values, g_c1["A_vals"])
+    for nx, seed in ((16, 3), (32, 7)):
+        A, meta = P.gen_poisson2d(nx, nx, coeff_seed=seed)
+        assert np.array_equal(A.values, g_heat[f"h{nx}A_vals"])
+        assert np.array_equal(A.col_indices, g_heat[f"h{nx}A_cols"])
+    for dims in ((3, 4, 2), (7, 5, 6), (16, 16, 16)):
+        A3, _ = P.gen_poisson3d(*dims)
+        o, c, v = O.gen_poisson3d(*dims)
+        assert np.array_equal(A3.row_offsets, o) and np.array_equal(A3.col_indices, c)
+        assert np.array_equal(A3.values, v)
+    A, _ = P.gen_poisson2d(13, 7, coeff_seed=5)
+    o, c, v, _ = O.gen_poisson2d(13, 7, 5)
+    assert np.array_equal(A.row_offsets, o) and np.array_equal(A.values, v)
+
+
+def test_features_bit_exact(g_sparse, g_c1, g_heat):
+    g = g_sparse
+    for tag in ("s15", "s60", "s300"):
+        gr = P.build_graph(csr(g, tag))
+        assert gr.norm_A == g[tag + "_norm_A"]
+        assert np.array_equal(gr.node_features, g[tag + "_node_features"])
+        assert np.array_equal(gr.edge_features[:, 0], g[tag + "_vals"] / g[tag + "_norm_A"])
+    A, meta = P.gen_poisson2d(64, 64)
+    gr = P.build_graph(A, meta)
+    assert gr.norm_A == g_c1["norm_A"]
+    assert np.array_equal(gr.node_features, g_c1["node_features"])
+    for nx in (16, 32):
+        A, meta = P.gen_poisson2d(nx, nx, coeff_seed=3 if nx == 16 else 7)
+        gr = P.build_graph(A, meta)
+        assert gr.norm_A == g_heat[f"h{nx}norm_A"]
+        assert np.array_equal(gr.node_features, g_heat[f"h{nx}node_features"])
+    with pytest.raises(ValueError):
+        P.build_graph(P.SparseMatrix(2, 2, g["asym_offs"], g["asym_cols"], np.ones(3)))
+
+
+# --------------------------------------------------------------------------- GNN (a13-a15)
+def test_gnn_small_configs(g_sparse):
+    g = g_sparse
+    for tag in ("s15", "s60", "s300"):
+        A = csr(g, tag)
+        gr = P.build_graph(A)
+        for act in ("relu", "tanh"):
+            m = P.init_model(P.GnnConfig(n_layers=2, hidden_dim=6, d_node=2, seed=5, activation=act))
+            assert np.array_equal(m.params_flat(), g[tag + "_small_params_" + act])
+            G = P.forward(m, gr).G
+            assert np.array_equal(G.row_offsets, A.row_offsets) and np.array_equal(G.col_indices, A.col_indices)
+            assert rel_floor(G.values, g[tag + "_small_G_" + act]) < G_TOL
+        m = P.init_model(P.GnnConfig(d_node=2, seed=1))
+        assert rel_floor(P.forward(m, gr).G.values, g[tag + "_g24_G"]) < G_TOL
+
+
+def test_gnn_c1_random_init(g_c1):
+    A, meta = P.gen_poisson2d(64, 64)
+    m = P.init_model(P.GnnConfig(d_node=3, seed=0))
+    G = P.forward(m, P.build_graph(A, meta)).G
+    assert rel_floor(G.values, g_c1["G_vals"]) < G_TOL
+
+
+def test_gnn_zero_layers_and_unsupported(g_sparse):
+    A = csr(g_sparse, "s60")
+    gr = P.build_graph(A)
+    m = P.init_model(P.GnnConfig(n_layers=0, hidden_dim=6, d_node=2, seed=5))
+    want = O.gnn_forward(O.unflatten(m.params_flat(), O.init_params(2, n_layers=0, hidden=6, seed=5)),
+                         gr.node_features, A.row_offsets, A.col_indices, gr.edge_features, 0)
+    assert rel_floor(P.forward(m, gr).G.values, want) < G_TOL
+    with pytest.raises(NotImplementedError):
+        P.forward(P.init_model(P.GnnConfig(d_node=2, message_uses_hidden_edge=True)), gr)
+    with pytest.raises(ValueError):
+        P.forward(P.init_model(P.GnnConfig(d_node=3)), gr)
+
+
+def test_gnn_trained_heat(g_heat):
+    import os
+    m = P.load_checkpoint(os.path.join(os.path.dirname(__file__), "golden", "trained_heat16.spaignn"))
+    assert np.array_equal(m.params_flat(), g_heat["params"])
+    for nx, seed in ((16, 3), (32, 7)):
+        A, meta = P.gen_poisson2d(nx, nx, coeff_seed=seed)
+        G = P.forward(m, P.build_graph(A, meta)).G
+        assert rel_floor(G.values, g_heat[f"h{nx}G_vals"]) < G_TOL
+
+
+# --------------------------------------------------------------------------- PCG (a12)
+def _k_close(k, k_ref):
+    return abs(k - k_ref) <= max(1, math.ceil(0.02 * k_ref))
+
+
+def test_pcg_golden_cases(g_pcg):
+    from spaigraph_cases import PCG_CASES
+    g = g_pcg
+    A = csr(g, "A")
+    Gr = A.with_values(g["Gr"])
+    pres = {"id": P.build_identity(A), "jac": P.build_jacobi(A), "learn": P.build_learned_spai(Gr, 1e-3)}
+    for name, (pre, kw) in PCG_CASES.items():
+        b = np.zeros(A.n_rows) if name == "zero_rhs" else g["b"]
+        cfg = P.SolveConfig(rtol=kw.get("rtol", 1e-8), max_iters=kw.get("max_iters"),
+                            residual_refresh_period=kw.get("period", 50),
+                            termination=kw.get("termination", "true_residual"))
+        rep = P.pcg_solve(A, b, pres[pre], cfg)
+        k_ref = int(g[name + "_k"])
+        assert _k_close(rep.k, k_ref), (name, rep.k, k_ref)
+        assert rep.converged == bool(g[name + "_conv"]), name
+        if rep.k == k_ref:
+            scale = max(1.0, float(np.max(np.abs(g[name + "_x"]))))
+            assert np.max(np.abs(rep.x - g[name + "_x"])) <= 1e-10 * scale, name
+            assert np.allclose(rep.residual_history, g[name + "_hist"], rtol=1e-8, atol=1e-14), name
+
+
+def test_pcg_c1_iteration_count(g_c1):
+    """Config 1: random-init GNN-SPAI on 64^2 Poisson, rtol 1e-6: k = 6601 +-2%."""
+    A, meta = P.gen_poisson2d(64, 64)
+    m = P.init_model(P.GnnConfig(d_node=3, seed=0))
+    G = P.forward(m, P.build_graph(A, meta)).G
+    rep = P.pcg_solve(A, g_c1["b"], P.build_learned_spai(G, 1e-4), P.SolveConfig(rtol=1e-6))
+    assert rep.converged
+    assert _k_close(rep.k, int(g_c1["k"])), (rep.k, int(g_c1["k"]))
+    assert len(rep.residual_history) == rep.k + 1
+    rel = np.linalg.norm(g_c1["b"] - O.spmv(g_c1["A_offs"], g_c1["A_cols"], g_c1["A_vals"], rep.x))
+    assert rel <= 1e-6
+
+
+def test_pcg_trained_heat(g_heat):
+    import os
+    m = P.load_checkpoint(os.path.join(os.path.dirname(__file__), "golden", "trained_heat16.spaignn"))
+    for nx, seed in ((16, 3), (32, 7)):
+        A, meta = P.gen_poisson2d(nx, nx, coeff_seed=seed)
+        M = P.build_learned_spai(P.forward(m, P.build_graph(A, meta)).G, m.config.epsilon)
+        for rtol, tag in ((1e-8, "r8"), (1e-6, "r6")):
+            rep = P.pcg_solve(A, g_heat[f"h{nx}b"], M, P.SolveConfig(rtol=rtol))
+            k_ref = int(g_heat[f"h{nx}k_{tag}"])
+            assert rep.converged and _k_close(rep.k, k_ref), (nx, tag, rep.k, k_ref)
+
+
+def test_pcg_not_spd():
+    A = P.SparseMatrix.from_dense(np.diag([1.0, -1.0]))
+    with pytest.raises(P.NotSpdError):
+        P.pcg_solve(A, np.array([1.0, 1.0]), P.build_identity(A))
+    I3 = P.SparseMatrix.identity(3)
+    G = I3.with_values(np.array([1.0, 0.0, 1.0]))
+    rep = P.pcg_solve(I3, np.ones(3), P.build_learned_spai(G, 0.0))  # singular M^{-1}: breakdown or not
+    assert rep.k >= 0
+
+
+def test_pcg_identity_small():
+    A = P.SparseMatrix.identity(7)
+    b = np.arange(1.0, 8.0)
+    rep = P.pcg_solve(A, b, P.build_identity(A))
+    assert rep.converged and rep.k == 1
+    assert np.allclose(rep.x, b, rtol=0, atol=1e-14)
+
+
+# --------------------------------------------------------------------------- loss (a16)
+def test_loss_and_grad(g_sparse, g_c1):
+    g = g_sparse
+    for tag in ("s15", "s60", "s300"):
+        A = csr(g, tag)
+        Gr = A.with_values(g[tag + "_Grand"])
+        for kind in ("mean_abs_nonzero", "frobenius", "entrywise_l1"):
+            loss, grad = P.sai_loss_and_grad(A, Gr, 1e-3, g[tag + "_w"], kind)
+            want = g[tag + "_loss_" + kind]
+            assert abs(loss - want) <= 1e-13 * abs(want), (tag, kind)
+            gw = g[tag + "_grad_" + kind]
+            assert np.max(np.abs(grad - gw)) <= 1e-12 * np.max(np.abs(gw)), (tag, kind)
+    A, meta = P.gen_poisson2d(64, 64)
+    G = A.with_values(g_c1["G_vals"])
+    loss, grad = P.sai_loss_and_grad(A, G, 1e-4, g_c1["w"])
+    assert abs(loss - float(g_c1["loss"])) <= 1e-13 * float(g_c1["loss"])
+    assert np.max(np.abs(grad - g_c1["grad"])) <= 1e-12 * np.max(np.abs(g_c1["grad"]))
+
+
+def test_loss_scale_invariance(g_sparse):
+    g = g_sparse
+    A = csr(g, "s60")
+    G = A.with_values(g["s60_Grand"])
+    w = g["s60_w"]
+    base = P.sai_loss(A, G, 1e-2, w)
+    for alpha in (2.0**-10, 2.0**10):
+        assert P.sai_loss(A.with_values(alpha * g["s60_vals"]), G, 1e-2, w) == base
+    from oracle.spaigraph_ref import sai_loss as oloss  # noqa: F401
+    for alpha in (1e-3, 1e3):
+        v = P.sai_loss(A.with_values(alpha * g["s60_vals"]), G, 1e-2, w)
+        assert abs(v - base) <= 8 * math.ulp(base)
+
+
+# --------------------------------------------------------------------------- batch (C2 path)
+def test_batch_matches_single_solves():
+    import os
+    m = P.load_checkpoint(os.path.join(os.path.dirname(__file__), "golden", "trained_heat16.spaignn"))
+    systems = [P.gen_poisson2d(24, 24, coeff_seed=s) for s in range(5)]
+    bs = [P.gen_rhs(meta, s + 10**6) for s, (_, meta) in enumerate(systems)]
+    cfg = P.SolveConfig(rtol=1e-8)
+    # host-typed inputs (int64 CSR as the reference holds them)
+    As = [A for A, _ in systems]
+    reps = P.solve_batch(As, bs, m, metas=[meta for _, meta in systems], cfg=cfg, history=True)
+    for (A, meta), b, rb in zip(systems, bs, reps):
+        M = P.build_learned_spai(P.forward(m, P.build_graph(A, meta)).G, m.config.epsilon)
+        rs = P.pcg_solve(A, b, M, cfg)
+        assert rb.k == rs.k and rb.converged == rs.converged
+        assert np.array_equal(rb.x, rs.x)
+        assert np.array_equal(np.asarray(rb.residual_history), np.asarray(rs.residual_history))
+    # device-generated batch == host-uploaded batch
+    from paper_2510_27517_b200.batch import BatchSolver, SystemBatch
+    sb = SystemBatch.heat2d(24, 24, list(range(5)), [s + 10**6 for s in range(5)])
+    solver = BatchSolver(sb, m)
+    res = solver.step(cfg)
+    assert [r.k for r in res] == [r.k for r in reps]
+    x = solver.x.cpu().numpy()
+    assert np.array_equal(x, np.concatenate([r.x for r in reps]))
