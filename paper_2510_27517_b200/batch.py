@@ -117,12 +117,17 @@ class SystemBatch:
             if pde:
                 coeff[r0:r0 + rows[k]].copy_(torch.from_numpy(np.ascontiguousarray(metas[k].coeff, dtype=np.float64)))
         offs[n:n + 1].fill_(nnz)
-        a = DeviceCsr(n, n, offs, cols, vals)
         L.call_ws(lib.sg_csr_validate, n, n, nnz, L.ptr(offs), L.ptr(cols), what="validate batch")
-        if into is not None and into.a.offs is offs:
-            a._rows, a._t = into.a._rows, into.a._t
         grids = [tuple(m.grid) for m in metas] if pde else None
         means = [float(np.asarray(m.coeff, dtype=np.float64).mean()) for m in metas] if pde else None
+        if into is not None and into.a.offs is offs:
+            # same device buffers refilled in place: keep the object (and its cached row index,
+            # transpose permutation and any PCG handle built on it); the pattern may differ, so
+            # drop the pattern-derived caches
+            into.a.refresh_pattern()
+            into.grids, into.coeff, into.coeff_mean = grids, coeff, means
+            return into
+        a = DeviceCsr(n, n, offs, cols, vals)
         return SystemBatch(a, row_start, nnz_start, b, grids, coeff, means)
 
 
@@ -145,7 +150,7 @@ class BatchSolver:
         self.gt_vals = L.empty(a.nnz, torch.float64)
         self.x = L.empty(a.n_rows, torch.float64)
         self._norm_ws = None
-        self.g = None
+        self.g = L.empty(a.nnz, torch.float64)  # G values; fixed buffer so the PCG handle is reused
         self.handle = None
 
     def build_graph(self):
@@ -174,14 +179,14 @@ class BatchSolver:
     def build_factor(self):
         """G = GNN(graph) on the union graph; explicit G^T values via the transpose permutation."""
         a = self.batch.a
-        self.g = forward_device(self.model, a, self.node, self.edge, self.batch.d_node)
+        forward_device(self.model, a, self.node, self.edge, self.batch.d_node, out=self.g)
         _, _, perm = a.transpose_pattern()
         L.check(L.lib().sg_gather_f64(L.ptr(self.g), L.ptr(perm), L.ptr(self.gt_vals), a.nnz, L.stream_ptr()))
 
     def solve(self, cfg: SolveConfig):
         a = self.batch.a
         ot, ct, _ = a.transpose_pattern()
-        if self.handle is None or self.handle.g.vals.data_ptr() != self.g.data_ptr():
+        if self.handle is None or self.handle.a is not a:
             g_dev = a.with_values(self.g)
             gt_dev = DeviceCsr(a.n_cols, a.n_rows, ot, ct, self.gt_vals)
             self.handle = PcgHandle(a, self.batch.row_start, L.PRECOND_LEARNED, g_dev, gt_dev, None,

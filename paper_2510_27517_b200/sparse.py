@@ -46,13 +46,23 @@ class DeviceCsr:
         """(offs_t, cols_t, perm) with values_t = values[perm] (sparse.py:129-136)."""
         if self._t is None:
             import torch
-            ot = L.empty(self.n_cols + 1, torch.int32)
-            ct = L.empty(self.nnz, torch.int32)
-            perm = L.empty(self.nnz, torch.int32)
-            L.call_ws(L.lib().sg_csr_transpose, self.n_rows, self.n_cols, self.nnz, L.ptr(self.offs),
-                      L.ptr(self.cols), L.ptr(ot), L.ptr(ct), L.ptr(perm), what="transpose")
-            self._t = (ot, ct, perm)
+            self._t = (L.empty(self.n_cols + 1, torch.int32), L.empty(self.nnz, torch.int32),
+                       L.empty(self.nnz, torch.int32))
+            self._compute_transpose()
         return self._t
+
+    def _compute_transpose(self):
+        ot, ct, perm = self._t
+        L.call_ws(L.lib().sg_csr_transpose, self.n_rows, self.n_cols, self.nnz, L.ptr(self.offs),
+                  L.ptr(self.cols), L.ptr(ot), L.ptr(ct), L.ptr(perm), what="transpose")
+
+    def refresh_pattern(self):
+        """Recompute the pattern-derived caches IN PLACE after the index arrays were refilled
+        (keeps every pointer a captured PCG handle holds valid)."""
+        if self._rows is not None:
+            L.check(L.lib().sg_row_expand(self.n_rows, L.ptr(self.offs), L.ptr(self._rows), L.stream_ptr()))
+        if self._t is not None:
+            self._compute_transpose()
 
     def with_values(self, vals):
         d = DeviceCsr(self.n_rows, self.n_cols, self.offs, self.cols, vals)

