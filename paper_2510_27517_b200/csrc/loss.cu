@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(kRows) k_loss_spmv(int64_t n, const int32_t* _
   stage_rows(t, r0, r1, offs, cols, vals);
   const int lr = threadIdx.x;
   if (r0 + lr < r1) {
-    double v = tile_row_dot<ORDER>(t, lr, cols, vals, [&](int32_t j) { return __ldg(x + j); });
+    double v = tile_row_dot<ORDER, false, 0>(t, lr, cols, vals, XF{x, nullptr, 0.0});
     if (addv) v = add(v, mul(eps, addv[r0 + lr]));
     y[r0 + lr] = v;
   }

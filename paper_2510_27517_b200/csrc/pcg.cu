@@ -49,6 +49,13 @@ struct Ctl {
 
 __global__ void k_snapshot(Ctl* c) { c->snap = c->n_active; }
 
+__global__ void k_max_row(const int32_t* __restrict__ offs, int64_t n, unsigned int* out) {
+  unsigned int m = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    m = max(m, (unsigned int)(offs[i + 1] - offs[i]));
+  atomicMax(out, m);
+}
+
 struct Dev {
   // block table
   const long long* blk_r0;
@@ -117,7 +124,7 @@ __device__ __forceinline__ void put_hist(const Dev& D, int sys, long long i, dou
 
 // ------------------------------------------------------------------ setup
 // r = b; t = G^T b; partial ||b||^2
-template <int PRE>
+template <int PRE, bool SH>
 __global__ void __launch_bounds__(PR) k_setup1(Dev D) {
   __shared__ RowTile<PR, PCAP> T;
   __shared__ double red[PR / 32];
@@ -135,8 +142,7 @@ __global__ void __launch_bounds__(PR) k_setup1(Dev D) {
     D.x[i] = 0.0;
     pbb = mul(bi, bi);
     if (PRE == SG_PRECOND_LEARNED)
-      D.t[i] = tile_row_dot<kOrderSeq>(T, threadIdx.x, D.gt_cols, D.gt_vals,
-                                       [&](int32_t j) { return __ldg(D.b + j); });
+      D.t[i] = tile_row_dot<kOrderSeq, SH, 0>(T, threadIdx.x, D.gt_cols, D.gt_vals, XF{D.b, nullptr, 0.0});
   }
   if (arrive(D, sys, pbb, 0.0, red, &flag)) {
     const double bb = gather_partials(D, sys, 0, red);
@@ -149,18 +155,17 @@ __global__ void __launch_bounds__(PR) k_setup1(Dev D) {
   }
 }
 
-template <int PRE>
+template <int PRE, bool SH>
 __device__ __forceinline__ double apply_row(const Dev& D, const RowTile<PR, PCAP>& T, int lr,
-                                            long long i, const double* r) {
+                                            long long i, const double* r, double eps) {
   if (PRE == SG_PRECOND_IDENTITY) return r[i];
   if (PRE == SG_PRECOND_JACOBI) return mul(r[i], D.inv_diag[i]);
-  const double y = tile_row_dot<kOrderNumpy>(T, lr, D.g_cols, D.g_vals,
-                                             [&](int32_t j) { return __ldcg(D.t + j); });
-  return add(y, mul(D.ctl->eps, r[i]));
+  const double y = tile_row_dot<kOrderNumpy, SH, 0>(T, lr, D.g_cols, D.g_vals, XF{D.t, nullptr, 0.0});
+  return add(y, mul(eps, r[i]));
 }
 
 // s = M r0; delta0 = r.s; NotSpd check; top-of-loop checks for i = 0.
-template <int PRE>
+template <int PRE, bool SH>
 __global__ void __launch_bounds__(PR) k_setup2(Dev D) {
   __shared__ RowTile<PR, PCAP> T;
   __shared__ double red[PR / 32];
@@ -171,7 +176,7 @@ __global__ void __launch_bounds__(PR) k_setup2(Dev D) {
   const long long i = r0 + threadIdx.x;
   double prs = 0.0;
   if (i < r1) {
-    const double si = apply_row<PRE>(D, T, threadIdx.x, i, D.r0);
+    const double si = apply_row<PRE, SH>(D, T, threadIdx.x, i, D.r0, D.ctl->eps);
     D.s[i] = si;
     prs = mul(D.r0[i], si);
   }
@@ -212,7 +217,7 @@ __global__ void __launch_bounds__(PR) k_setup2(Dev D) {
 }
 
 // ------------------------------------------------------------------ K1
-template <int PRE>
+template <int PRE, bool SH>
 __global__ void __launch_bounds__(PR) k_iter1(Dev D, int par) {
   __shared__ RowTile<PR, PCAP> T;
   __shared__ double red[PR / 32];
@@ -234,15 +239,12 @@ __global__ void __launch_bounds__(PR) k_iter1(Dev D, int par) {
     if (run) {
       const double dni = add(D.s[i], mul(beta, dc[i]));
       dn[i] = dni;
-      const double qi = tile_row_dot<kOrderNumpy>(T, threadIdx.x, D.a_cols, D.a_vals, [&](int32_t j) {
-        return add(__ldg(D.s + j), mul(beta, __ldg(dc + j)));
-      });
+      const double qi = tile_row_dot<kOrderNumpy, SH, 1>(T, threadIdx.x, D.a_cols, D.a_vals, XF{D.s, dc, beta});
       D.q[i] = qi;
       pdq = mul(dni, qi);
     }
     if (fresh) {
-      const double ax = tile_row_dot<kOrderNumpy>(T, threadIdx.x, D.a_cols, D.a_vals,
-                                                  [&](int32_t j) { return __ldg(D.x + j); });
+      const double ax = tile_row_dot<kOrderNumpy, SH, 0>(T, threadIdx.x, D.a_cols, D.a_vals, XF{D.x, nullptr, 0.0});
       const double rf = sub(D.b[i], ax);
       if (run) rc[i] = rf;
       prr = mul(rf, rf);
@@ -279,7 +281,7 @@ __global__ void __launch_bounds__(PR) k_iter1(Dev D, int par) {
 }
 
 // ------------------------------------------------------------------ K2 (non-refresh)
-template <int PRE>
+template <int PRE, bool SH>
 __global__ void __launch_bounds__(PR) k_iter2(Dev D, int par) {
   __shared__ RowTile<PR, PCAP> T;
   __shared__ double red[PR / 32];
@@ -300,9 +302,7 @@ __global__ void __launch_bounds__(PR) k_iter2(Dev D, int par) {
     rn[i] = rni;
     prr = mul(rni, rni);
     if (PRE == SG_PRECOND_LEARNED)
-      D.t[i] = tile_row_dot<kOrderSeq>(T, threadIdx.x, D.gt_cols, D.gt_vals, [&](int32_t j) {
-        return sub(__ldg(rc + j), mul(alpha, __ldg(D.q + j)));
-      });
+      D.t[i] = tile_row_dot<kOrderSeq, SH, 2>(T, threadIdx.x, D.gt_cols, D.gt_vals, XF{rc, D.q, alpha});
   }
   if (arrive(D, sys, prr, 0.0, red, &flag)) {
     const double rr = gather_partials(D, sys, 0, red);
@@ -324,6 +324,7 @@ __global__ void __launch_bounds__(PR) k_refresh_x(Dev D, int par) {
   if (i < r1) D.x[i] = add(D.x[i], mul(alpha, dn[i]));
 }
 
+template <bool SH>
 __global__ void __launch_bounds__(PR) k_refresh_r(Dev D, int par) {
   __shared__ RowTile<PR, PCAP> T;
   __shared__ double red[PR / 32];
@@ -336,8 +337,7 @@ __global__ void __launch_bounds__(PR) k_refresh_r(Dev D, int par) {
   const long long i = r0 + threadIdx.x;
   double prr = 0.0;
   if (i < r1) {
-    const double ax = tile_row_dot<kOrderNumpy>(T, threadIdx.x, D.a_cols, D.a_vals,
-                                                [&](int32_t j) { return __ldg(D.x + j); });
+    const double ax = tile_row_dot<kOrderNumpy, SH, 0>(T, threadIdx.x, D.a_cols, D.a_vals, XF{D.x, nullptr, 0.0});
     const double rni = sub(D.b[i], ax);
     rn[i] = rni;
     prr = mul(rni, rni);
@@ -351,6 +351,7 @@ __global__ void __launch_bounds__(PR) k_refresh_r(Dev D, int par) {
   }
 }
 
+template <bool SH>
 __global__ void __launch_bounds__(PR) k_refresh_t(Dev D, int par) {
   __shared__ RowTile<PR, PCAP> T;
   int sys; long long r0, r1;
@@ -360,12 +361,11 @@ __global__ void __launch_bounds__(PR) k_refresh_t(Dev D, int par) {
   stage_rows(T, r0, r1, D.gt_offs, D.gt_cols, D.gt_vals);
   const long long i = r0 + threadIdx.x;
   if (i < r1)
-    D.t[i] = tile_row_dot<kOrderSeq>(T, threadIdx.x, D.gt_cols, D.gt_vals,
-                                     [&](int32_t j) { return __ldcg(rn + j); });
+    D.t[i] = tile_row_dot<kOrderSeq, SH, 0>(T, threadIdx.x, D.gt_cols, D.gt_vals, XF{rn, nullptr, 0.0});
 }
 
 // ------------------------------------------------------------------ K3
-template <int PRE>
+template <int PRE, bool SH>
 __global__ void __launch_bounds__(PR) k_iter3(Dev D, int par, int refreshed) {
   __shared__ RowTile<PR, PCAP> T;
   __shared__ double red[PR / 32];
@@ -378,7 +378,7 @@ __global__ void __launch_bounds__(PR) k_iter3(Dev D, int par, int refreshed) {
   const long long i = r0 + threadIdx.x;
   double prs = 0.0;
   if (i < r1) {
-    const double si = apply_row<PRE>(D, T, threadIdx.x, i, rn);
+    const double si = apply_row<PRE, SH>(D, T, threadIdx.x, i, rn, D.ctl->eps);
     D.s[i] = si;
     prs = mul(rn[i], si);
   }
@@ -439,6 +439,7 @@ struct sg_pcg {
   std::map<std::vector<int>, int> graph_kernels;
   int chunk = 0;
   int64_t period = 0;
+  int short_rows = 0;
   // instrumentation: kernel launches, and (when profiling) event nodes around the kernels of
   // one non-refresh iteration per chunk -> per-kernel device time sampled inside the solve
   int64_t kernels = 0, chunks = 0;
@@ -463,26 +464,36 @@ int dispatch_pre(int pre, F f) {
 
 // Launches one iteration; returns the number of kernels launched through *nk.  With `ev`
 // (profiling), external event-record nodes bracket K1, K2 and K3.
-int launch_iteration(sg_pcg* h, cudaStream_t s, int par, bool refresh, cudaEvent_t* ev, int* nk) {
+// (preconditioner kind) x (SHORT: every row of A, G, G^T has <= 8 entries)
+template <class F>
+int dispatch(const sg_pcg* h, F f) {
   return dispatch_pre(h->pre, [&](auto P) -> int {
+    if (h->short_rows) return f(P, std::integral_constant<bool, true>());
+    return f(P, std::integral_constant<bool, false>());
+  });
+}
+
+int launch_iteration(sg_pcg* h, cudaStream_t s, int par, bool refresh, cudaEvent_t* ev, int* nk) {
+  return dispatch(h, [&](auto P, auto SHc) -> int {
     constexpr int PRE = decltype(P)::value;
+    constexpr bool SH = decltype(SHc)::value;
     const unsigned g = (unsigned)h->nblk;
     int k = 0;
     if (ev) {
       k_snapshot<<<1, 1, 0, s>>>(h->ctl); ++k;
       SG_CUDA(cudaEventRecordWithFlags(ev[0], s, cudaEventRecordExternal));
     }
-    k_iter1<PRE><<<g, PR, 0, s>>>(h->D, par); ++k;
+    k_iter1<PRE, SH><<<g, PR, 0, s>>>(h->D, par); ++k;
     if (ev) SG_CUDA(cudaEventRecordWithFlags(ev[1], s, cudaEventRecordExternal));
     if (!refresh) {
-      k_iter2<PRE><<<g, PR, 0, s>>>(h->D, par); ++k;
+      k_iter2<PRE, SH><<<g, PR, 0, s>>>(h->D, par); ++k;
     } else {
       k_refresh_x<<<g, PR, 0, s>>>(h->D, par); ++k;
-      k_refresh_r<<<g, PR, 0, s>>>(h->D, par); ++k;
-      if (PRE == SG_PRECOND_LEARNED) { k_refresh_t<<<g, PR, 0, s>>>(h->D, par); ++k; }
+      k_refresh_r<SH><<<g, PR, 0, s>>>(h->D, par); ++k;
+      if (PRE == SG_PRECOND_LEARNED) { k_refresh_t<SH><<<g, PR, 0, s>>>(h->D, par); ++k; }
     }
     if (ev) SG_CUDA(cudaEventRecordWithFlags(ev[2], s, cudaEventRecordExternal));
-    k_iter3<PRE><<<g, PR, 0, s>>>(h->D, par, refresh ? 1 : 0); ++k;
+    k_iter3<PRE, SH><<<g, PR, 0, s>>>(h->D, par, refresh ? 1 : 0); ++k;
     if (ev) SG_CUDA(cudaEventRecordWithFlags(ev[3], s, cudaEventRecordExternal));
     SG_LAUNCH_CHECK("pcg iteration");
     *nk += k;
@@ -607,6 +618,22 @@ extern "C" int sg_pcg_create(sg_pcg** out, int32_t n_systems, const int64_t* sys
   SG_CUDA(cudaHostAlloc(&h->pinned_active, 2 * sizeof(unsigned int), cudaHostAllocDefault));
   SG_CUDA(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
   for (int k = 0; k < 4; ++k) SG_CUDA(cudaEventCreate(&h->ev[k]));
+  {  // longest row of every matrix the loop touches -> SHORT kernels when all are <= 8
+    unsigned int* mx = counter;  // reuse (zeroed again below)
+    SG_CUDA(cudaMemsetAsync(mx, 0, sizeof(unsigned int), s));
+    const int gb = (int)(n / 256 + 1 < 148 * 8 ? n / 256 + 1 : 148 * 8);
+    k_max_row<<<gb, 256, 0, s>>>(a_offs, n, mx);
+    if (precond_kind == SG_PRECOND_LEARNED) {
+      k_max_row<<<gb, 256, 0, s>>>(g_offs, n, mx);
+      k_max_row<<<gb, 256, 0, s>>>(gt_offs, n, mx);
+    }
+    SG_LAUNCH_CHECK("k_max_row");
+    unsigned int hm = 0;
+    SG_CUDA(cudaMemcpyAsync(&hm, mx, sizeof(hm), cudaMemcpyDeviceToHost, s));
+    SG_CUDA(cudaStreamSynchronize(s));
+    h->short_rows = hm <= 8 ? 1 : 0;
+    SG_CUDA(cudaMemsetAsync(counter, 0, S * sizeof(unsigned int), s));
+  }
   SG_CUDA(cudaStreamSynchronize(s));
   *out = h;
   return SG_OK;
@@ -654,10 +681,11 @@ extern "C" int sg_pcg_solve(sg_pcg* h, const double* b, double* x, const sg_solv
   // setup
   const unsigned g = (unsigned)h->nblk;
   if (g) {
-    rc = dispatch_pre(h->pre, [&](auto P) -> int {
+    rc = dispatch(h, [&](auto P, auto SHc) -> int {
       constexpr int PRE = decltype(P)::value;
-      k_setup1<PRE><<<g, PR, 0, s>>>(h->D);
-      k_setup2<PRE><<<g, PR, 0, s>>>(h->D);
+      constexpr bool SH = decltype(SHc)::value;
+      k_setup1<PRE, SH><<<g, PR, 0, s>>>(h->D);
+      k_setup2<PRE, SH><<<g, PR, 0, s>>>(h->D);
       SG_LAUNCH_CHECK("pcg setup");
       return SG_OK;
     });

@@ -17,7 +17,7 @@ __global__ void __launch_bounds__(kRows) k_spmv(int64_t n, const int32_t* __rest
   stage_rows(t, r0, r1, offs, cols, vals);
   const int lr = threadIdx.x;
   if (r0 + lr < r1)
-    y[r0 + lr] = tile_row_dot<ORDER>(t, lr, cols, vals, [&](int32_t j) { return __ldg(x + j); });
+    y[r0 + lr] = tile_row_dot<ORDER, false, 0>(t, lr, cols, vals, XF{x, nullptr, 0.0});
 }
 
 // s = spmv(G, t) + eps * r
@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(kRows) k_apply_g(int64_t n, const int32_t* __r
   stage_rows(t, r0, r1, offs, cols, vals);
   const int lr = threadIdx.x;
   if (r0 + lr < r1) {
-    const double y = tile_row_dot<kOrderNumpy>(t, lr, cols, vals, [&](int32_t j) { return __ldg(tv + j); });
+    const double y = tile_row_dot<kOrderNumpy, false, 0>(t, lr, cols, vals, XF{tv, nullptr, 0.0});
     s[r0 + lr] = add(y, mul(eps, r[r0 + lr]));
   }
 }

@@ -9,6 +9,10 @@
 //   kOrderSeq:   ((0 + v0) + v1) + ...  == np.add.at into zeros          (spmv_transpose, :194)
 // Products are rounded before summation (no FMA), so results are bit-identical to numpy.
 // Blocks whose nonzeros exceed the shared-memory capacity fall back to direct global loads.
+//
+// Two code shapes per order: SHORT (every row has <= 8 entries, e.g. the 5- and 7-point
+// stencils: numpy's pairwise sum degenerates to a sequential loop) and general (8-accumulator
+// blocks and the recursive split for > 129 entries, the latter out of line).
 #pragma once
 
 #include "common.cuh"
@@ -17,25 +21,52 @@ namespace sg {
 
 enum SumOrder { kOrderNumpy = 0, kOrderSeq = 1 };
 
-template <class F>
-__device__ __noinline__ double pairwise_long(const F& f, int64_t lo, int64_t n) {
-  return pairwise_sum(f, lo, n);
+// Operand of the product val_k * X(col_k):
+//   XM 0: X(j) = a[j]      XM 1: X(j) = a[j] + c b[j]      XM 2: X(j) = a[j] - c b[j]
+// (XM 1/2 rebuild a vector being updated in the same pass, e.g. d' = s + beta d, without
+// waiting for the update to land in memory.)
+struct XF {
+  const double* a;
+  const double* b;
+  double c;
+};
+
+template <int XM>
+__device__ __forceinline__ double xval(const XF& f, int32_t j) {
+  if (XM == 0) return __ldg(f.a + j);
+  if (XM == 1) return add(__ldg(f.a + j), mul(f.c, __ldg(f.b + j)));
+  return sub(__ldg(f.a + j), mul(f.c, __ldg(f.b + j)));
 }
 
-// Row reduction over entries [lo, hi) of a product functor p(k), in the requested order.
-template <int ORDER, class P>
-__device__ __forceinline__ double row_reduce(const P& p, int lo, int hi) {
-  if (ORDER == kOrderSeq) {
+// Out-of-line general row reduction (long rows): plain pointer arguments only, so calling it
+// does not force the caller's state through local memory.
+template <int ORDER, int XM>
+__device__ __noinline__ double row_general(const double* __restrict__ sv, const int32_t* __restrict__ sc,
+                                           int lo, int hi, XF f) {
+  auto p = [&](int64_t k) { return mul(sv[k], xval<XM>(f, sc[k])); };
+  if (ORDER == kOrderSeq) return sequential_sum(p, lo, hi);
+  return reduceat_sum(p, lo, hi);
+}
+
+// Row reduction over [lo, hi) of val_k * X(col_k) in ORDER.
+template <int ORDER, bool SHORT, int XM>
+__device__ __forceinline__ double row_reduce(const double* __restrict__ sv, const int32_t* __restrict__ sc,
+                                             int lo, int hi, const XF& f) {
+  if (SHORT || hi - lo <= 8) {
+    if (hi <= lo) return 0.0;
+    if (ORDER == kOrderSeq) {
+      double s = 0.0;
+      for (int k = lo; k < hi; ++k) s = add(s, mul(sv[k], xval<XM>(f, sc[k])));
+      return s;
+    }
+    // numpy: v[lo] + pairwise(v[lo+1:hi]); pairwise of < 8 values is sequential from 0.0
+    const double first = mul(sv[lo], xval<XM>(f, sc[lo]));
+    if (hi - lo == 1) return first;
     double s = 0.0;
-    for (int k = lo; k < hi; ++k) s = add(s, p(k));
-    return s;
+    for (int k = lo + 1; k < hi; ++k) s = add(s, mul(sv[k], xval<XM>(f, sc[k])));
+    return add(first, s);
   }
-  if (hi <= lo) return 0.0;
-  const int m = hi - lo - 1;
-  const double first = p(lo);
-  if (m == 0) return first;
-  if (m <= 128) return add(first, pairwise_leaf(p, (int64_t)lo + 1, (int64_t)m));
-  return add(first, pairwise_long(p, (int64_t)lo + 1, (int64_t)m));
+  return row_general<ORDER, XM>(sv, sc, lo, hi, f);
 }
 
 // Shared-memory tile of one CTA's rows.
@@ -81,17 +112,13 @@ __device__ __forceinline__ void stage_rows(RowTile<ROWS, CAP>& t, int64_t r0, in
 }
 
 // y_i = sum_k val_k * X(col_k) for local row `lr` of a staged tile, in ORDER.
-template <int ORDER, int ROWS, int CAP, class XF>
+template <int ORDER, bool SHORT, int XM, int ROWS, int CAP>
 __device__ __forceinline__ double tile_row_dot(const RowTile<ROWS, CAP>& t, int lr,
                                                const int32_t* __restrict__ cols,
-                                               const double* __restrict__ vals, const XF& xf) {
+                                               const double* __restrict__ vals, const XF& f) {
   const int lo = t.offs[lr], hi = t.offs[lr + 1];
-  if (t.staged) {
-    const double* sv = t.vals - t.base_v;
-    const int32_t* sc = t.cols - t.base_c;
-    return row_reduce<ORDER>([&](int64_t k) { return mul(sv[k], xf(sc[k])); }, lo, hi);
-  }
-  return row_reduce<ORDER>([&](int64_t k) { return mul(__ldg(vals + k), xf(__ldg(cols + k))); }, lo, hi);
+  if (t.staged) return row_reduce<ORDER, SHORT, XM>(t.vals - t.base_v, t.cols - t.base_c, lo, hi, f);
+  return row_reduce<ORDER, SHORT, XM>(vals, cols, lo, hi, f);
 }
 
 }  // namespace sg
