@@ -1,31 +1,38 @@
 // Batched, device-resident PCG (pcg.py:131-233).
 //
-// A batch of independent SPD systems is stored block-diagonally (global column indices).  CTAs
-// own ROWS consecutive rows of ONE system, so every dot product is a per-system sum of per-CTA
-// partials, reduced deterministically (fixed-shape trees) by the last CTA of that system to
-// arrive ("last block" finalizer).  The finalizer runs the reference's scalar control flow
-// (alpha, beta, NotSpd checks, refresh, the fresh-residual re-check, max_iters, delta test,
-// history) on device, so a system that stops simply makes its CTAs exit early in later
-// launches.  The host only launches CUDA graphs of C iterations and polls one counter.
+// A batch of independent SPD systems is stored block-diagonally (global column indices).  Rows
+// are cut into TILES of PR rows that never straddle two systems; every dot product is a
+// per-system sum of per-tile partials, reduced deterministically (fixed-shape trees) by the CTA
+// that completes the system's last tile.  That CTA also runs the reference's scalar control
+// flow (alpha, beta, NotSpd checks, refresh, the fresh-residual re-check, max_iters, the delta
+// test, history) on device, so a system that stops makes its tiles be skipped afterwards.  The
+// host only launches CUDA graphs of one refresh period of iterations and polls one counter.
 //
-// One iteration = three fused kernels (four + two extra on refresh iterations):
+// Kernels are PERSISTENT: gridDim = SMs x resident CTAs, tiles assigned round-robin (so the work
+// of every system spreads over all SMs, which keeps the load balanced while systems drop out).
+// Each CTA runs a 2-stage pipeline: while it reduces tile k from shared memory, the TMA engine
+// (cp.async.bulk + mbarrier) streams the row offsets, values and column indices of its next
+// tile into the other buffer.
+//
+// One iteration = three fused kernels (two more on refresh iterations):
 //   K1  d' = s + beta d (on the fly for neighbours), q = A d', partial d'.q
 //       [+ r_fresh = b - A x and ||r_fresh||^2 when a fresh check / certification is pending]
 //   K2  x += alpha d', r' = r - alpha q (on the fly), t = G^T r', partial ||r'||^2
 //   K3  s = G t + eps r' (or r' / r' * inv_diag), partial r'.s, finalizer
 // Refresh iterations (i > 0, i % period == 0) replace K2 by: x += alpha d'; r' = b - A x;
-// t = G^T r'.  Every vector update uses the reference's roundings (no FMA), every SpMV the
-// reference's summation order, so the only arithmetic difference from numpy is the order of
-// the dot-product reductions (numpy uses OpenBLAS ddot).
+// t = G^T r'.  Vector updates use the reference's roundings (no FMA), SpMVs its summation order,
+// so the only arithmetic difference from numpy is the order of the dot-product reductions
+// (numpy uses OpenBLAS ddot).
 #include <map>
 #include <vector>
 
 #include "spmv.cuh"
+#include "tma.cuh"
 
 namespace sg {
 
-constexpr int PR = 256;    // rows per CTA (= threads per CTA)
-constexpr int PCAP = 2048; // staged nonzeros per CTA (8 per row on average)
+constexpr int PR = 256;    // rows per tile (= threads per CTA)
+constexpr int PCAP = 2048; // staged nonzeros per tile (8 per row on average)
 
 enum { ST_RUN = 0, ST_CERTIFY = 1, ST_DONE = 2 };
 enum { FL_FRESH = 1 };
@@ -57,16 +64,17 @@ __global__ void k_max_row(const int32_t* __restrict__ offs, int64_t n, unsigned 
 }
 
 struct Dev {
-  // block table
+  // tile table
   const long long* blk_r0;
   const int* blk_sys;
   const int* sys_blk0;
+  const long long* sys_r1;  // per system end row
+  int nblk;
   // matrices
   const int32_t *a_offs, *a_cols; const double* a_vals;
   const int32_t *g_offs, *g_cols; const double* g_vals;
   const int32_t *gt_offs, *gt_cols; const double* gt_vals;
   const double* inv_diag;
-  const long long* sys_r1;  // per system end row
   // vectors
   double *b, *x, *r0, *r1, *d0, *d1, *q, *s, *t;
   // reduction scratch
@@ -76,39 +84,133 @@ struct Dev {
   Ctl* ctl;
 };
 
-__device__ __forceinline__ void block_rows(const Dev& D, int& sys, long long& r0, long long& r1) {
-  sys = D.blk_sys[blockIdx.x];
-  r0 = D.blk_r0[blockIdx.x];
-  const long long e = r0 + PR;
-  const long long se = D.sys_r1[sys];
-  r1 = e < se ? e : se;
+// ------------------------------------------------------------------ tile pipeline
+struct __align__(16) Pipe {
+  double vals[2][PCAP + 2];
+  int32_t cols[2][PCAP + 4];
+  int32_t offs[2][PR + 8];
+  uint64_t bar[2];
+  int meta[2][4];  // base_v, base_c, base_o, staged
+  double red[PR / 32];
+  int flag;
+};
+
+struct Mat {
+  const int32_t* offs;
+  const int32_t* cols;
+  const double* vals;
+};
+
+// Issue the bulk copies of tile t into buffer `buf` (one thread).
+__device__ __forceinline__ void issue_tile(const Dev& D, Pipe& P, const Mat& M, int t, int buf) {
+  const int sys = D.blk_sys[t];
+  const long long r0 = D.blk_r0[t];
+  const long long r1 = min(r0 + PR, D.sys_r1[sys]);
+  const int e0 = __ldg(M.offs + r0), e1 = __ldg(M.offs + r1);
+  const int a0v = e0 & ~1, a1v = (e1 + 1) & ~1;
+  const int a0c = e0 & ~3, a1c = (e1 + 3) & ~3;
+  const long long o0 = r0 & ~3LL, o1 = (r1 + 1 + 3) & ~3LL;
+  const bool fits = (a1v - a0v) <= PCAP + 2 && (a1c - a0c) <= PCAP + 4;
+  const uint32_t ob = (uint32_t)((o1 - o0) * 4);
+  const uint32_t vb = fits ? (uint32_t)((a1v - a0v) * 8) : 0u;
+  const uint32_t cb = fits ? (uint32_t)((a1c - a0c) * 4) : 0u;
+  P.meta[buf][0] = a0v;
+  P.meta[buf][1] = a0c;
+  P.meta[buf][2] = (int)o0;
+  P.meta[buf][3] = fits ? 1 : 0;
+  fence_proxy_async_smem();
+  mbar_arrive_expect_tx(&P.bar[buf], ob + vb + cb);
+  bulk_g2s(P.offs[buf], M.offs + o0, ob, &P.bar[buf]);
+  if (vb) bulk_g2s(P.vals[buf], M.vals + a0v, vb, &P.bar[buf]);
+  if (cb) bulk_g2s(P.cols[buf], M.cols + a0c, cb, &P.bar[buf]);
 }
 
-// Publish this CTA's two partials; returns true in ALL threads of the last CTA of `sys`.
-__device__ __forceinline__ bool arrive(const Dev& D, int sys, double p0, double p1,
-                                       double* red, int* flag) {
-  double a = block_sum(p0, red);
-  double b = block_sum(p1, red);
+// View of one staged tile: pointers valid for global entry / row indices of that tile.
+struct TileView {
+  const double* v;
+  const int32_t* c;
+  const int32_t* o;  // o[i] = row offset of global row i
+};
+
+__device__ __forceinline__ TileView view(const Pipe& P, const Mat& M, int buf) {
+  TileView tv;
+  tv.o = P.offs[buf] - P.meta[buf][2];
+  if (P.meta[buf][3]) {
+    tv.v = P.vals[buf] - P.meta[buf][0];
+    tv.c = P.cols[buf] - P.meta[buf][1];
+  } else {
+    tv.v = M.vals;
+    tv.c = M.cols;
+  }
+  return tv;
+}
+
+// Next tile >= t (stride gridDim.x) whose system satisfies `want(status)`; D.nblk if none.
+template <class Want>
+__device__ __forceinline__ int next_tile(const Dev& D, int t, const Want& want) {
+  for (; t < D.nblk; t += gridDim.x)
+    if (want(D.st[D.blk_sys[t]].status)) return t;
+  return D.nblk;
+}
+
+// Round-robin persistent loop over the CTA's tiles with a 2-stage TMA pipeline.
+// body(t, sys, r0, r1, TileView) is executed by all threads and must be CTA-uniform.
+template <bool STAGE, class Want, class Body>
+__device__ __forceinline__ void tile_loop(const Dev& D, Pipe& P, const Mat& M, const Want& want, const Body& body) {
+  if (STAGE && threadIdx.x == 0) {
+    mbar_init(&P.bar[0], 1);
+    mbar_init(&P.bar[1], 1);
+    mbar_init_fence();
+  }
+  __syncthreads();
+  int t = next_tile(D, blockIdx.x, want);
+  if (STAGE && threadIdx.x == 0 && t < D.nblk) issue_tile(D, P, M, t, 0);
+  int buf = 0;
+  uint32_t phase0 = 0, phase1 = 0;
+  while (t < D.nblk) {
+    const int tn = next_tile(D, t + gridDim.x, want);
+    if (STAGE && threadIdx.x == 0 && tn < D.nblk) issue_tile(D, P, M, tn, buf ^ 1);
+    const int sys = D.blk_sys[t];
+    const long long r0 = D.blk_r0[t];
+    const long long r1 = min(r0 + PR, D.sys_r1[sys]);
+    TileView tv{M.vals, M.cols, M.offs};
+    if (STAGE) {
+      mbar_wait(&P.bar[buf], buf ? phase1 : phase0);
+      if (buf) phase1 ^= 1u; else phase0 ^= 1u;
+      tv = view(P, M, buf);
+    }
+    body(t, sys, r0, r1, tv);
+    __syncthreads();  // buffer `buf` is free again; body's shared scratch may be reused
+    t = tn;
+    buf ^= 1;
+  }
+}
+
+// Publish tile t's two partials; returns true in ALL threads of the CTA that completed the
+// last tile of `sys`.
+__device__ __forceinline__ bool arrive(const Dev& D, Pipe& P, int t, int sys, double p0, double p1) {
+  const double a = block_sum(p0, P.red);
+  const double b = block_sum(p1, P.red);
   if (threadIdx.x == 0) {
-    D.part[2 * blockIdx.x + 0] = a;
-    D.part[2 * blockIdx.x + 1] = b;
+    D.part[2 * t + 0] = a;
+    D.part[2 * t + 1] = b;
     __threadfence();
     const unsigned int nb = (unsigned)(D.sys_blk0[sys + 1] - D.sys_blk0[sys]);
     const unsigned int old = atomicAdd(&D.counter[sys], 1u);
-    *flag = (old == nb - 1);
+    P.flag = (old == nb - 1);
   }
   __syncthreads();
-  const bool last = *flag;
+  const bool last = P.flag;
   if (last) __threadfence();
   return last;
 }
 
 // Deterministic per-system sum of partial slot `which` (valid in thread 0).
-__device__ __forceinline__ double gather_partials(const Dev& D, int sys, int which, double* red) {
+__device__ __forceinline__ double gather_partials(const Dev& D, Pipe& P, int sys, int which) {
   const int b0 = D.sys_blk0[sys], b1 = D.sys_blk0[sys + 1];
   double v = 0.0;
   for (int b = b0 + threadIdx.x; b < b1; b += blockDim.x) v += __ldcg(&D.part[2 * b + which]);
-  return block_sum(v, red);
+  return block_sum(v, P.red);
 }
 
 __device__ __forceinline__ void finish(const Dev& D, SysState& S, int conv) {
@@ -122,296 +224,298 @@ __device__ __forceinline__ void put_hist(const Dev& D, int sys, long long i, dou
   if (c.track && i < c.hcap) c.hist[(long long)sys * c.hcap + i] = v;
 }
 
+struct WantAll { __device__ bool operator()(int) const { return true; } };
+struct WantRun { __device__ bool operator()(int s) const { return s == ST_RUN; } };
+struct WantLive { __device__ bool operator()(int s) const { return s != ST_DONE; } };
+
+template <int PRE>
+__device__ __forceinline__ Mat mat_g(const Dev& D) { return Mat{D.g_offs, D.g_cols, D.g_vals}; }
+__device__ __forceinline__ Mat mat_gt(const Dev& D) { return Mat{D.gt_offs, D.gt_cols, D.gt_vals}; }
+__device__ __forceinline__ Mat mat_a(const Dev& D) { return Mat{D.a_offs, D.a_cols, D.a_vals}; }
+
+template <int ORDER, bool SH, int XM>
+__device__ __forceinline__ double trow(const TileView& tv, long long i, const XF& f) {
+  return row_reduce<ORDER, SH, XM>(tv.v, tv.c, tv.o[i], tv.o[i + 1], f);
+}
+
 // ------------------------------------------------------------------ setup
-// r = b; t = G^T b; partial ||b||^2
+// r = b; d = 0; x = 0; t = G^T b; partial ||b||^2
 template <int PRE, bool SH>
 __global__ void __launch_bounds__(PR) k_setup1(Dev D) {
-  __shared__ RowTile<PR, PCAP> T;
-  __shared__ double red[PR / 32];
-  __shared__ int flag;
-  int sys; long long r0, r1;
-  block_rows(D, sys, r0, r1);
-  if (PRE == SG_PRECOND_LEARNED) stage_rows(T, r0, r1, D.gt_offs, D.gt_cols, D.gt_vals);
-  const long long i = r0 + threadIdx.x;
-  double pbb = 0.0;
-  if (i < r1) {
-    const double bi = D.b[i];
-    D.r0[i] = bi;
-    D.d0[i] = 0.0;
-    D.d1[i] = 0.0;
-    D.x[i] = 0.0;
-    pbb = mul(bi, bi);
-    if (PRE == SG_PRECOND_LEARNED)
-      D.t[i] = tile_row_dot<kOrderSeq, SH, 0>(T, threadIdx.x, D.gt_cols, D.gt_vals, XF{D.b, nullptr, 0.0});
-  }
-  if (arrive(D, sys, pbb, 0.0, red, &flag)) {
-    const double bb = gather_partials(D, sys, 0, red);
-    if (threadIdx.x == 0) {
-      SysState& S = D.st[sys];
-      S.norm_b = __dsqrt_rn(bb);
-      S.rr = bb;
-      D.counter[sys] = 0;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Pipe& P = *reinterpret_cast<Pipe*>(smem_raw);
+  tile_loop<PRE == SG_PRECOND_LEARNED>(D, P, mat_gt(D), WantAll{},
+      [&](int t, int sys, long long r0, long long r1, const TileView& tv) {
+    const long long i = r0 + threadIdx.x;
+    double pbb = 0.0;
+    if (i < r1) {
+      const double bi = D.b[i];
+      D.r0[i] = bi;
+      D.d0[i] = 0.0;
+      D.d1[i] = 0.0;
+      D.x[i] = 0.0;
+      pbb = mul(bi, bi);
+      if (PRE == SG_PRECOND_LEARNED) D.t[i] = trow<kOrderSeq, SH, 0>(tv, i, XF{D.b, nullptr, 0.0});
     }
-  }
+    if (arrive(D, P, t, sys, pbb, 0.0)) {
+      const double bb = gather_partials(D, P, sys, 0);
+      if (threadIdx.x == 0) {
+        SysState& S = D.st[sys];
+        S.norm_b = __dsqrt_rn(bb);
+        S.rr = bb;
+        D.counter[sys] = 0;
+      }
+    }
+  });
 }
 
 template <int PRE, bool SH>
-__device__ __forceinline__ double apply_row(const Dev& D, const RowTile<PR, PCAP>& T, int lr,
-                                            long long i, const double* r, double eps) {
+__device__ __forceinline__ double apply_row(const Dev& D, const TileView& tv, long long i, const double* r,
+                                            double eps) {
   if (PRE == SG_PRECOND_IDENTITY) return r[i];
   if (PRE == SG_PRECOND_JACOBI) return mul(r[i], D.inv_diag[i]);
-  const double y = tile_row_dot<kOrderNumpy, SH, 0>(T, lr, D.g_cols, D.g_vals, XF{D.t, nullptr, 0.0});
+  const double y = trow<kOrderNumpy, SH, 0>(tv, i, XF{D.t, nullptr, 0.0});
   return add(y, mul(eps, r[i]));
 }
 
 // s = M r0; delta0 = r.s; NotSpd check; top-of-loop checks for i = 0.
 template <int PRE, bool SH>
 __global__ void __launch_bounds__(PR) k_setup2(Dev D) {
-  __shared__ RowTile<PR, PCAP> T;
-  __shared__ double red[PR / 32];
-  __shared__ int flag;
-  int sys; long long r0, r1;
-  block_rows(D, sys, r0, r1);
-  if (PRE == SG_PRECOND_LEARNED) stage_rows(T, r0, r1, D.g_offs, D.g_cols, D.g_vals);
-  const long long i = r0 + threadIdx.x;
-  double prs = 0.0;
-  if (i < r1) {
-    const double si = apply_row<PRE, SH>(D, T, threadIdx.x, i, D.r0, D.ctl->eps);
-    D.s[i] = si;
-    prs = mul(D.r0[i], si);
-  }
-  if (arrive(D, sys, prs, 0.0, red, &flag)) {
-    const double rs = gather_partials(D, sys, 0, red);
-    if (threadIdx.x == 0) {
-      SysState& S = D.st[sys];
-      D.counter[sys] = 0;
-      const Ctl& c = *D.ctl;
-      S.i = 0;
-      S.beta = 0.0;
-      S.flags = 0;
-      S.notspd = 0;
-      S.converged = 0;
-      if (S.norm_b == 0.0) {  // pcg.py:159-164
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Pipe& P = *reinterpret_cast<Pipe*>(smem_raw);
+  const double eps = D.ctl->eps;
+  tile_loop<PRE == SG_PRECOND_LEARNED>(D, P, mat_g<PRE>(D), WantAll{},
+      [&](int t, int sys, long long r0, long long r1, const TileView& tv) {
+    const long long i = r0 + threadIdx.x;
+    double prs = 0.0;
+    if (i < r1) {
+      const double si = apply_row<PRE, SH>(D, tv, i, D.r0, eps);
+      D.s[i] = si;
+      prs = mul(D.r0[i], si);
+    }
+    if (arrive(D, P, t, sys, prs, 0.0)) {
+      const double rs = gather_partials(D, P, sys, 0);
+      if (threadIdx.x == 0) {
+        SysState& S = D.st[sys];
+        D.counter[sys] = 0;
+        const Ctl& c = *D.ctl;
+        S.i = 0;
+        S.beta = 0.0;
+        S.flags = 0;
+        S.notspd = 0;
+        S.converged = 0;
         S.hist_len = 1;
-        put_hist(D, sys, 0, 0.0);
-        finish(D, S, 1);
-        return;
-      }
-      S.hist_len = 1;
-      put_hist(D, sys, 0, __ddiv_rn(__dsqrt_rn(S.rr), S.norm_b));
-      S.delta = rs;
-      if (rs < 0.0) {  // pcg.py:171-172
-        S.notspd = 1; S.fail_iter = 0; S.fail_value = rs; S.fail_kind = 2;
-        finish(D, S, 0);
-        return;
-      }
-      S.delta0 = rs;
-      S.rtol2d0 = mul(mul(c.rtol, c.rtol), rs);
-      if (c.delta_mode) {
-        if (S.max_iters <= 0 || rs <= S.rtol2d0) S.status = ST_CERTIFY;
-      } else if (S.max_iters <= 0) {
-        finish(D, S, 0);
+        if (S.norm_b == 0.0) {  // pcg.py:159-164
+          put_hist(D, sys, 0, 0.0);
+          finish(D, S, 1);
+          return;
+        }
+        put_hist(D, sys, 0, __ddiv_rn(__dsqrt_rn(S.rr), S.norm_b));
+        S.delta = rs;
+        if (rs < 0.0) {  // pcg.py:171-172
+          S.notspd = 1; S.fail_iter = 0; S.fail_value = rs; S.fail_kind = 2;
+          finish(D, S, 0);
+          return;
+        }
+        S.delta0 = rs;
+        S.rtol2d0 = mul(mul(c.rtol, c.rtol), rs);
+        if (c.delta_mode) {
+          if (S.max_iters <= 0 || rs <= S.rtol2d0) S.status = ST_CERTIFY;
+        } else if (S.max_iters <= 0) {
+          finish(D, S, 0);
+        }
       }
     }
-  }
+  });
 }
 
 // ------------------------------------------------------------------ K1
 template <int PRE, bool SH>
 __global__ void __launch_bounds__(PR) k_iter1(Dev D, int par) {
-  __shared__ RowTile<PR, PCAP> T;
-  __shared__ double red[PR / 32];
-  __shared__ int flag;
-  int sys; long long r0, r1;
-  block_rows(D, sys, r0, r1);
-  const int status = D.st[sys].status;
-  if (status == ST_DONE) return;
-  const bool run = status == ST_RUN;
-  const bool fresh = run ? (D.st[sys].flags & FL_FRESH) != 0 : true;
-  const double beta = D.st[sys].beta;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Pipe& P = *reinterpret_cast<Pipe*>(smem_raw);
   double* dc = par ? D.d1 : D.d0;
   double* dn = par ? D.d0 : D.d1;
   double* rc = par ? D.r1 : D.r0;
-  stage_rows(T, r0, r1, D.a_offs, D.a_cols, D.a_vals);
-  const long long i = r0 + threadIdx.x;
-  double pdq = 0.0, prr = 0.0;
-  if (i < r1) {
-    if (run) {
-      const double dni = add(D.s[i], mul(beta, dc[i]));
-      dn[i] = dni;
-      const double qi = tile_row_dot<kOrderNumpy, SH, 1>(T, threadIdx.x, D.a_cols, D.a_vals, XF{D.s, dc, beta});
-      D.q[i] = qi;
-      pdq = mul(dni, qi);
-    }
-    if (fresh) {
-      const double ax = tile_row_dot<kOrderNumpy, SH, 0>(T, threadIdx.x, D.a_cols, D.a_vals, XF{D.x, nullptr, 0.0});
-      const double rf = sub(D.b[i], ax);
-      if (run) rc[i] = rf;
-      prr = mul(rf, rf);
-    }
-  }
-  if (arrive(D, sys, pdq, prr, red, &flag)) {
-    const double dq = gather_partials(D, sys, 0, red);
-    const double rrf = gather_partials(D, sys, 1, red);
-    if (threadIdx.x == 0) {
-      SysState& S = D.st[sys];
-      D.counter[sys] = 0;
-      const Ctl& c = *D.ctl;
-      if (!run) {  // delta-test certification (pcg.py:217-220)
-        const double rel = __ddiv_rn(__dsqrt_rn(rrf), S.norm_b);
-        finish(D, S, rel <= c.rtol);
-        return;
+  tile_loop<true>(D, P, mat_a(D), WantLive{},
+      [&](int t, int sys, long long r0, long long r1, const TileView& tv) {
+    const int status = D.st[sys].status;
+    const bool run = status == ST_RUN;
+    const bool fresh = run ? (D.st[sys].flags & FL_FRESH) != 0 : true;
+    const double beta = D.st[sys].beta;
+    const long long i = r0 + threadIdx.x;
+    double pdq = 0.0, prr = 0.0;
+    if (i < r1) {
+      if (run) {
+        const double dni = add(D.s[i], mul(beta, dc[i]));
+        dn[i] = dni;
+        const double qi = trow<kOrderNumpy, SH, 1>(tv, i, XF{D.s, dc, beta});
+        D.q[i] = qi;
+        pdq = mul(dni, qi);
       }
-      if (S.flags & FL_FRESH) {  // pcg.py:208-215
-        S.flags &= ~FL_FRESH;
-        const double rel = __ddiv_rn(__dsqrt_rn(rrf), S.norm_b);
-        put_hist(D, sys, S.i, rel);
-        if (rel <= c.rtol) { finish(D, S, 1); return; }
-        if (S.i >= S.max_iters) { finish(D, S, 0); return; }
+      if (fresh) {
+        const double rf = sub(D.b[i], trow<kOrderNumpy, SH, 0>(tv, i, XF{D.x, nullptr, 0.0}));
+        if (run) rc[i] = rf;
+        prr = mul(rf, rf);
       }
-      if (dq <= 0.0) {  // pcg.py:182-184
-        S.notspd = 1; S.fail_iter = S.i; S.fail_value = dq; S.fail_kind = 1;
-        finish(D, S, 0);
-        return;
-      }
-      S.dq = dq;
-      S.alpha = __ddiv_rn(S.delta, dq);
     }
-  }
+    if (arrive(D, P, t, sys, pdq, prr)) {
+      const double dq = gather_partials(D, P, sys, 0);
+      const double rrf = gather_partials(D, P, sys, 1);
+      if (threadIdx.x == 0) {
+        SysState& S = D.st[sys];
+        D.counter[sys] = 0;
+        const Ctl& c = *D.ctl;
+        if (!run) {  // delta-test certification (pcg.py:217-220)
+          const double rel = __ddiv_rn(__dsqrt_rn(rrf), S.norm_b);
+          finish(D, S, rel <= c.rtol);
+          return;
+        }
+        if (S.flags & FL_FRESH) {  // pcg.py:208-215
+          S.flags &= ~FL_FRESH;
+          const double rel = __ddiv_rn(__dsqrt_rn(rrf), S.norm_b);
+          put_hist(D, sys, S.i, rel);
+          if (rel <= c.rtol) { finish(D, S, 1); return; }
+          if (S.i >= S.max_iters) { finish(D, S, 0); return; }
+        }
+        if (dq <= 0.0) {  // pcg.py:182-184
+          S.notspd = 1; S.fail_iter = S.i; S.fail_value = dq; S.fail_kind = 1;
+          finish(D, S, 0);
+          return;
+        }
+        S.dq = dq;
+        S.alpha = __ddiv_rn(S.delta, dq);
+      }
+    }
+  });
 }
 
 // ------------------------------------------------------------------ K2 (non-refresh)
 template <int PRE, bool SH>
 __global__ void __launch_bounds__(PR) k_iter2(Dev D, int par) {
-  __shared__ RowTile<PR, PCAP> T;
-  __shared__ double red[PR / 32];
-  __shared__ int flag;
-  int sys; long long r0, r1;
-  block_rows(D, sys, r0, r1);
-  if (D.st[sys].status != ST_RUN) return;
-  const double alpha = D.st[sys].alpha;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Pipe& P = *reinterpret_cast<Pipe*>(smem_raw);
   const double* dn = par ? D.d0 : D.d1;
   const double* rc = par ? D.r1 : D.r0;
   double* rn = par ? D.r0 : D.r1;
-  if (PRE == SG_PRECOND_LEARNED) stage_rows(T, r0, r1, D.gt_offs, D.gt_cols, D.gt_vals);
-  const long long i = r0 + threadIdx.x;
-  double prr = 0.0;
-  if (i < r1) {
-    D.x[i] = add(D.x[i], mul(alpha, dn[i]));
-    const double rni = sub(rc[i], mul(alpha, D.q[i]));
-    rn[i] = rni;
-    prr = mul(rni, rni);
-    if (PRE == SG_PRECOND_LEARNED)
-      D.t[i] = tile_row_dot<kOrderSeq, SH, 2>(T, threadIdx.x, D.gt_cols, D.gt_vals, XF{rc, D.q, alpha});
-  }
-  if (arrive(D, sys, prr, 0.0, red, &flag)) {
-    const double rr = gather_partials(D, sys, 0, red);
-    if (threadIdx.x == 0) {
-      D.st[sys].rr = rr;
-      D.counter[sys] = 0;
+  tile_loop<PRE == SG_PRECOND_LEARNED>(D, P, mat_gt(D), WantRun{},
+      [&](int t, int sys, long long r0, long long r1, const TileView& tv) {
+    const double alpha = D.st[sys].alpha;
+    const long long i = r0 + threadIdx.x;
+    double prr = 0.0;
+    if (i < r1) {
+      D.x[i] = add(D.x[i], mul(alpha, dn[i]));
+      const double rni = sub(rc[i], mul(alpha, D.q[i]));
+      rn[i] = rni;
+      prr = mul(rni, rni);
+      if (PRE == SG_PRECOND_LEARNED) D.t[i] = trow<kOrderSeq, SH, 2>(tv, i, XF{rc, D.q, alpha});
     }
-  }
+    if (arrive(D, P, t, sys, prr, 0.0)) {
+      const double rr = gather_partials(D, P, sys, 0);
+      if (threadIdx.x == 0) {
+        D.st[sys].rr = rr;
+        D.counter[sys] = 0;
+      }
+    }
+  });
 }
 
 // ------------------------------------------------------------------ K2 refresh variants
 __global__ void __launch_bounds__(PR) k_refresh_x(Dev D, int par) {
-  int sys; long long r0, r1;
-  block_rows(D, sys, r0, r1);
-  if (D.st[sys].status != ST_RUN) return;
-  const double alpha = D.st[sys].alpha;
   const double* dn = par ? D.d0 : D.d1;
-  const long long i = r0 + threadIdx.x;
-  if (i < r1) D.x[i] = add(D.x[i], mul(alpha, dn[i]));
+  for (int t = blockIdx.x; t < D.nblk; t += gridDim.x) {
+    const int sys = D.blk_sys[t];
+    if (D.st[sys].status != ST_RUN) continue;
+    const double alpha = D.st[sys].alpha;
+    const long long r0 = D.blk_r0[t];
+    const long long i = r0 + threadIdx.x;
+    if (i < min(r0 + PR, D.sys_r1[sys])) D.x[i] = add(D.x[i], mul(alpha, dn[i]));
+  }
 }
 
 template <bool SH>
 __global__ void __launch_bounds__(PR) k_refresh_r(Dev D, int par) {
-  __shared__ RowTile<PR, PCAP> T;
-  __shared__ double red[PR / 32];
-  __shared__ int flag;
-  int sys; long long r0, r1;
-  block_rows(D, sys, r0, r1);
-  if (D.st[sys].status != ST_RUN) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Pipe& P = *reinterpret_cast<Pipe*>(smem_raw);
   double* rn = par ? D.r0 : D.r1;
-  stage_rows(T, r0, r1, D.a_offs, D.a_cols, D.a_vals);
-  const long long i = r0 + threadIdx.x;
-  double prr = 0.0;
-  if (i < r1) {
-    const double ax = tile_row_dot<kOrderNumpy, SH, 0>(T, threadIdx.x, D.a_cols, D.a_vals, XF{D.x, nullptr, 0.0});
-    const double rni = sub(D.b[i], ax);
-    rn[i] = rni;
-    prr = mul(rni, rni);
-  }
-  if (arrive(D, sys, prr, 0.0, red, &flag)) {
-    const double rr = gather_partials(D, sys, 0, red);
-    if (threadIdx.x == 0) {
-      D.st[sys].rr = rr;
-      D.counter[sys] = 0;
+  tile_loop<true>(D, P, mat_a(D), WantRun{},
+      [&](int t, int sys, long long r0, long long r1, const TileView& tv) {
+    const long long i = r0 + threadIdx.x;
+    double prr = 0.0;
+    if (i < r1) {
+      const double rni = sub(D.b[i], trow<kOrderNumpy, SH, 0>(tv, i, XF{D.x, nullptr, 0.0}));
+      rn[i] = rni;
+      prr = mul(rni, rni);
     }
-  }
+    if (arrive(D, P, t, sys, prr, 0.0)) {
+      const double rr = gather_partials(D, P, sys, 0);
+      if (threadIdx.x == 0) {
+        D.st[sys].rr = rr;
+        D.counter[sys] = 0;
+      }
+    }
+  });
 }
 
 template <bool SH>
 __global__ void __launch_bounds__(PR) k_refresh_t(Dev D, int par) {
-  __shared__ RowTile<PR, PCAP> T;
-  int sys; long long r0, r1;
-  block_rows(D, sys, r0, r1);
-  if (D.st[sys].status != ST_RUN) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Pipe& P = *reinterpret_cast<Pipe*>(smem_raw);
   const double* rn = par ? D.r0 : D.r1;
-  stage_rows(T, r0, r1, D.gt_offs, D.gt_cols, D.gt_vals);
-  const long long i = r0 + threadIdx.x;
-  if (i < r1)
-    D.t[i] = tile_row_dot<kOrderSeq, SH, 0>(T, threadIdx.x, D.gt_cols, D.gt_vals, XF{rn, nullptr, 0.0});
+  tile_loop<true>(D, P, mat_gt(D), WantRun{},
+      [&](int t, int sys, long long r0, long long r1, const TileView& tv) {
+    const long long i = r0 + threadIdx.x;
+    if (i < r1) D.t[i] = trow<kOrderSeq, SH, 0>(tv, i, XF{rn, nullptr, 0.0});
+  });
 }
 
 // ------------------------------------------------------------------ K3
 template <int PRE, bool SH>
 __global__ void __launch_bounds__(PR) k_iter3(Dev D, int par, int refreshed) {
-  __shared__ RowTile<PR, PCAP> T;
-  __shared__ double red[PR / 32];
-  __shared__ int flag;
-  int sys; long long r0, r1;
-  block_rows(D, sys, r0, r1);
-  if (D.st[sys].status != ST_RUN) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Pipe& P = *reinterpret_cast<Pipe*>(smem_raw);
   const double* rn = par ? D.r0 : D.r1;
-  if (PRE == SG_PRECOND_LEARNED) stage_rows(T, r0, r1, D.g_offs, D.g_cols, D.g_vals);
-  const long long i = r0 + threadIdx.x;
-  double prs = 0.0;
-  if (i < r1) {
-    const double si = apply_row<PRE, SH>(D, T, threadIdx.x, i, rn, D.ctl->eps);
-    D.s[i] = si;
-    prs = mul(rn[i], si);
-  }
-  if (arrive(D, sys, prs, 0.0, red, &flag)) {
-    const double rs = gather_partials(D, sys, 0, red);
-    if (threadIdx.x == 0) {
-      SysState& S = D.st[sys];
-      D.counter[sys] = 0;
-      const Ctl& c = *D.ctl;
-      const double delta_old = S.delta;
-      S.delta = rs;
-      if (rs < 0.0) {  // pcg.py:196-198
-        S.notspd = 1; S.fail_iter = S.i; S.fail_value = rs; S.fail_kind = 2;
-        finish(D, S, 0);
-        return;
-      }
-      S.beta = __ddiv_rn(rs, delta_old);
-      S.i += 1;
-      const double rel = __ddiv_rn(__dsqrt_rn(S.rr), S.norm_b);
-      put_hist(D, sys, S.i, rel);
-      S.hist_len = S.i + 1;
-      if (!c.delta_mode) {
-        if (rel <= c.rtol) {
-          if (refreshed) { finish(D, S, 1); return; }
-          S.flags |= FL_FRESH;
-        } else if (S.i >= S.max_iters) {
+  const double eps = D.ctl->eps;
+  tile_loop<PRE == SG_PRECOND_LEARNED>(D, P, mat_g<PRE>(D), WantRun{},
+      [&](int t, int sys, long long r0, long long r1, const TileView& tv) {
+    const long long i = r0 + threadIdx.x;
+    double prs = 0.0;
+    if (i < r1) {
+      const double si = apply_row<PRE, SH>(D, tv, i, rn, eps);
+      D.s[i] = si;
+      prs = mul(rn[i], si);
+    }
+    if (arrive(D, P, t, sys, prs, 0.0)) {
+      const double rs = gather_partials(D, P, sys, 0);
+      if (threadIdx.x == 0) {
+        SysState& S = D.st[sys];
+        D.counter[sys] = 0;
+        const Ctl& c = *D.ctl;
+        const double delta_old = S.delta;
+        S.delta = rs;
+        if (rs < 0.0) {  // pcg.py:196-198
+          S.notspd = 1; S.fail_iter = S.i; S.fail_value = rs; S.fail_kind = 2;
           finish(D, S, 0);
+          return;
         }
-      } else if (S.i >= S.max_iters || rs <= S.rtol2d0) {
-        S.status = ST_CERTIFY;
+        S.beta = __ddiv_rn(rs, delta_old);
+        S.i += 1;
+        const double rel = __ddiv_rn(__dsqrt_rn(S.rr), S.norm_b);
+        put_hist(D, sys, S.i, rel);
+        S.hist_len = S.i + 1;
+        if (!c.delta_mode) {
+          if (rel <= c.rtol) {
+            if (refreshed) { finish(D, S, 1); return; }
+            S.flags |= FL_FRESH;
+          } else if (S.i >= S.max_iters) {
+            finish(D, S, 0);
+          }
+        } else if (S.i >= S.max_iters || rs <= S.rtol2d0) {
+          S.status = ST_CERTIFY;
+        }
       }
     }
-  }
+  });
 }
 
 }  // namespace sg
@@ -440,6 +544,7 @@ struct sg_pcg {
   int chunk = 0;
   int64_t period = 0;
   int short_rows = 0;
+  unsigned grid = 0;  // persistent CTAs per kernel
   // instrumentation: kernel launches, and (when profiling) event nodes around the kernels of
   // one non-refresh iteration per chunk -> per-kernel device time sampled inside the solve
   int64_t kernels = 0, chunks = 0;
@@ -462,8 +567,6 @@ int dispatch_pre(int pre, F f) {
   return SG_EINVAL;
 }
 
-// Launches one iteration; returns the number of kernels launched through *nk.  With `ev`
-// (profiling), external event-record nodes bracket K1, K2 and K3.
 // (preconditioner kind) x (SHORT: every row of A, G, G^T has <= 8 entries)
 template <class F>
 int dispatch(const sg_pcg* h, F f) {
@@ -473,27 +576,58 @@ int dispatch(const sg_pcg* h, F f) {
   });
 }
 
+constexpr size_t kSmem = sizeof(Pipe);
+
+// Opt every pipelined kernel of this (PRE, SH) into the dynamic shared memory it needs and
+// size the persistent grid from the occupancy of the heaviest one.
+int configure(sg_pcg* h) {
+  return dispatch(h, [&](auto P, auto SHc) -> int {
+    constexpr int PRE = decltype(P)::value;
+    constexpr bool SH = decltype(SHc)::value;
+    const void* fns[] = {(const void*)k_setup1<PRE, SH>, (const void*)k_setup2<PRE, SH>,
+                         (const void*)k_iter1<PRE, SH>, (const void*)k_iter2<PRE, SH>,
+                         (const void*)k_iter3<PRE, SH>, (const void*)k_refresh_r<SH>,
+                         (const void*)k_refresh_t<SH>};
+    int occ = 1 << 30;
+    for (const void* f : fns) {
+      SG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
+      int o = 0;
+      SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, f, PR, kSmem));
+      occ = o < occ ? o : occ;
+    }
+    int dev = 0, sms = 0;
+    SG_CUDA(cudaGetDevice(&dev));
+    SG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const long long g = (long long)sms * (occ > 0 ? occ : 1);
+    h->grid = (unsigned)(g < h->nblk ? g : h->nblk);
+    if (h->grid == 0) h->grid = 1;
+    return SG_OK;
+  });
+}
+
+// Launches one iteration; returns the number of kernels launched through *nk.  With `ev`
+// (profiling), external event-record nodes bracket K1, K2 and K3.
 int launch_iteration(sg_pcg* h, cudaStream_t s, int par, bool refresh, cudaEvent_t* ev, int* nk) {
   return dispatch(h, [&](auto P, auto SHc) -> int {
     constexpr int PRE = decltype(P)::value;
     constexpr bool SH = decltype(SHc)::value;
-    const unsigned g = (unsigned)h->nblk;
+    const unsigned g = h->grid;
     int k = 0;
     if (ev) {
       k_snapshot<<<1, 1, 0, s>>>(h->ctl); ++k;
       SG_CUDA(cudaEventRecordWithFlags(ev[0], s, cudaEventRecordExternal));
     }
-    k_iter1<PRE, SH><<<g, PR, 0, s>>>(h->D, par); ++k;
+    k_iter1<PRE, SH><<<g, PR, kSmem, s>>>(h->D, par); ++k;
     if (ev) SG_CUDA(cudaEventRecordWithFlags(ev[1], s, cudaEventRecordExternal));
     if (!refresh) {
-      k_iter2<PRE, SH><<<g, PR, 0, s>>>(h->D, par); ++k;
+      k_iter2<PRE, SH><<<g, PR, kSmem, s>>>(h->D, par); ++k;
     } else {
       k_refresh_x<<<g, PR, 0, s>>>(h->D, par); ++k;
-      k_refresh_r<SH><<<g, PR, 0, s>>>(h->D, par); ++k;
-      if (PRE == SG_PRECOND_LEARNED) { k_refresh_t<SH><<<g, PR, 0, s>>>(h->D, par); ++k; }
+      k_refresh_r<SH><<<g, PR, kSmem, s>>>(h->D, par); ++k;
+      if (PRE == SG_PRECOND_LEARNED) { k_refresh_t<SH><<<g, PR, kSmem, s>>>(h->D, par); ++k; }
     }
     if (ev) SG_CUDA(cudaEventRecordWithFlags(ev[2], s, cudaEventRecordExternal));
-    k_iter3<PRE, SH><<<g, PR, 0, s>>>(h->D, par, refresh ? 1 : 0); ++k;
+    k_iter3<PRE, SH><<<g, PR, kSmem, s>>>(h->D, par, refresh ? 1 : 0); ++k;
     if (ev) SG_CUDA(cudaEventRecordWithFlags(ev[3], s, cudaEventRecordExternal));
     SG_LAUNCH_CHECK("pcg iteration");
     *nk += k;
@@ -608,6 +742,7 @@ extern "C" int sg_pcg_create(sg_pcg** out, int32_t n_systems, const int64_t* sys
   SG_CUDA(cudaMemsetAsync(counter, 0, S * sizeof(unsigned int), s));
   Dev& D = h->D;
   D.blk_r0 = d_blk_r0; D.blk_sys = d_blk_sys; D.sys_blk0 = d_sys_blk0; D.sys_r1 = d_sys_r1;
+  D.nblk = h->nblk;
   D.a_offs = a_offs; D.a_cols = a_cols; D.a_vals = a_vals;
   D.g_offs = g_offs; D.g_cols = g_cols; D.g_vals = g_vals;
   D.gt_offs = gt_offs; D.gt_cols = gt_cols; D.gt_vals = gt_vals;
@@ -634,6 +769,8 @@ extern "C" int sg_pcg_create(sg_pcg** out, int32_t n_systems, const int64_t* sys
     h->short_rows = hm <= 8 ? 1 : 0;
     SG_CUDA(cudaMemsetAsync(counter, 0, S * sizeof(unsigned int), s));
   }
+  int rc = configure(h);
+  if (rc) return rc;
   SG_CUDA(cudaStreamSynchronize(s));
   *out = h;
   return SG_OK;
@@ -654,6 +791,7 @@ extern "C" int sg_pcg_solve(sg_pcg* h, const double* b, double* x, const sg_solv
   if (chunk != h->chunk || period != h->period) {
     for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);
     h->graphs.clear();
+    h->graph_kernels.clear();
     h->chunk = chunk;
     h->period = period;
   }
@@ -679,27 +817,21 @@ extern "C" int sg_pcg_solve(sg_pcg* h, const double* b, double* x, const sg_solv
   SG_CUDA(cudaMemcpyAsync(h->ctl, &ctl, sizeof(Ctl), cudaMemcpyHostToDevice, s));
   if (h->n > 0) SG_CUDA(cudaMemcpyAsync(h->D.b, b, h->n * sizeof(double), cudaMemcpyDeviceToDevice, s));
   // setup
-  const unsigned g = (unsigned)h->nblk;
-  if (g) {
-    rc = dispatch(h, [&](auto P, auto SHc) -> int {
-      constexpr int PRE = decltype(P)::value;
-      constexpr bool SH = decltype(SHc)::value;
-      k_setup1<PRE, SH><<<g, PR, 0, s>>>(h->D);
-      k_setup2<PRE, SH><<<g, PR, 0, s>>>(h->D);
-      SG_LAUNCH_CHECK("pcg setup");
-      return SG_OK;
-    });
-    if (rc) return rc;
-  } else {
-    // all systems empty: nothing to iterate (norm_b == 0 path)
-    for (int k = 0; k < h->S; ++k) { st[k].status = ST_DONE; st[k].converged = 1; st[k].hist_len = 1; }
-    SG_CUDA(cudaMemcpyAsync(h->st, st.data(), st.size() * sizeof(SysState), cudaMemcpyHostToDevice, s));
-  }
+  const unsigned g = h->grid;
+  rc = dispatch(h, [&](auto P, auto SHc) -> int {
+    constexpr int PRE = decltype(P)::value;
+    constexpr bool SH = decltype(SHc)::value;
+    k_setup1<PRE, SH><<<g, PR, kSmem, s>>>(h->D);
+    k_setup2<PRE, SH><<<g, PR, kSmem, s>>>(h->D);
+    SG_LAUNCH_CHECK("pcg setup");
+    return SG_OK;
+  });
+  if (rc) return rc;
+  h->kernels += 2;
   // device-resident loop: graphs of `chunk` iterations, poll the active count between chunks
-  if (g) h->kernels += 2;
   int64_t it = 0;
   int prev_prof = -1;
-  while (g) {
+  for (;;) {
     SG_CUDA(cudaMemcpyAsync(h->pinned_active, &h->ctl->n_active, 2 * sizeof(unsigned int),
                             cudaMemcpyDeviceToHost, s));
     SG_CUDA(cudaStreamSynchronize(s));
@@ -712,6 +844,7 @@ extern "C" int sg_pcg_solve(sg_pcg* h, const double* b, double* x, const sg_solv
         h->prof_active += h->pinned_active[1];
         h->prof_samples += 1;
       }
+      cudaGetLastError();  // an unrecorded event must not poison later launch checks
     }
     if (h->pinned_active[0] == 0) break;
     if (cfg->track_history) {
