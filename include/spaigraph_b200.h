@@ -192,7 +192,9 @@ void sg_pcg_destroy(sg_pcg* h);
  * host).  With profiling on, every chunk graph brackets K1, K2, K3 of one non-refresh
  * iteration with external event-record nodes; sg_pcg_stats returns the summed device times
  * prof_host[0..2] (ms), the summed active-system counts at those iterations prof_host[3], the
- * sample count prof_host[4], plus the number of kernels and graphs launched. */
+ * sample count prof_host[4], the storage format prof_host[5] (number of diagonals when the
+ * diagonal-major DIA format is in use, 0 for CSR), plus the number of kernels and graphs
+ * launched.  prof_host must hold 6 doubles. */
 int sg_pcg_set_profile(sg_pcg* h, int32_t on);
 int sg_pcg_stats(sg_pcg* h, int64_t* kernels_host, int64_t* chunks_host, double* prof_host,
                  int32_t reset);

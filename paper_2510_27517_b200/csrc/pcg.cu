@@ -1,18 +1,13 @@
 // Batched, device-resident PCG (pcg.py:131-233).
 //
 // A batch of independent SPD systems is stored block-diagonally (global column indices).  Rows
-// are cut into TILES of PR rows that never straddle two systems; every dot product is a
-// per-system sum of per-tile partials, reduced deterministically (fixed-shape trees) by the CTA
-// that completes the system's last tile.  That CTA also runs the reference's scalar control
-// flow (alpha, beta, NotSpd checks, refresh, the fresh-residual re-check, max_iters, the delta
-// test, history) on device, so a system that stops makes its tiles be skipped afterwards.  The
-// host only launches CUDA graphs of one refresh period of iterations and polls one counter.
-//
-// Kernels are PERSISTENT: gridDim = SMs x resident CTAs, tiles assigned round-robin (so the work
-// of every system spreads over all SMs, which keeps the load balanced while systems drop out).
-// Each CTA runs a 2-stage pipeline: while it reduces tile k from shared memory, the TMA engine
-// (cp.async.bulk + mbarrier) streams the row offsets, values and column indices of its next
-// tile into the other buffer.
+// are cut into TILES of PR rows that never straddle two systems; one CTA per tile.  Every dot
+// product is a per-system sum of per-tile partials, reduced deterministically (fixed-shape
+// trees) by the CTA that completes the system's last tile.  That CTA also runs the reference's
+// scalar control flow (alpha, beta, NotSpd checks, refresh, the fresh-residual re-check,
+// max_iters, the delta test, history) on device; a stopped system's tiles exit immediately in
+// later launches.  The host only launches CUDA graphs of one refresh period of iterations and
+// polls one counter.
 //
 // One iteration = three fused kernels (two more on refresh iterations):
 //   K1  d' = s + beta d (on the fly for neighbours), q = A d', partial d'.q
@@ -23,16 +18,25 @@
 // t = G^T r'.  Vector updates use the reference's roundings (no FMA), SpMVs its summation order,
 // so the only arithmetic difference from numpy is the order of the dot-product reductions
 // (numpy uses OpenBLAS ddot).
+//
+// Two storage formats for the matrices, chosen per handle:
+//   DIA  (stencil patterns: <= 8 distinct diagonals, symmetric, G on A's pattern — the 2-D/3-D
+//        Poisson / diffusion configs).  Values diagonal-major [ndiag][n] with a per-row presence
+//        mask; no index traffic at all, every load coalesced.  G^T is never stored: row i of G^T
+//        on diagonal d is G's mirror diagonal at row i + off[d].  Rows are reduced over the
+//        PRESENT diagonals only, in ascending column order, so sums match CSR bit for bit.
+//   CSR  (anything else): CSR-stream tiles staged through shared memory (spmv.cuh).
+#include <algorithm>
 #include <map>
 #include <vector>
 
 #include "spmv.cuh"
-#include "tma.cuh"
 
 namespace sg {
 
 constexpr int PR = 256;    // rows per tile (= threads per CTA)
 constexpr int PCAP = 2048; // staged nonzeros per tile (8 per row on average)
+constexpr int MAXD = 8;    // DIA: max diagonals
 
 enum { ST_RUN = 0, ST_CERTIFY = 1, ST_DONE = 2 };
 enum { FL_FRESH = 1 };
@@ -54,27 +58,28 @@ struct Ctl {
   unsigned int snap;   // n_active seen right before the profiled iteration of a chunk
 };
 
-__global__ void k_snapshot(Ctl* c) { c->snap = c->n_active; }
-
-__global__ void k_max_row(const int32_t* __restrict__ offs, int64_t n, unsigned int* out) {
-  unsigned int m = 0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    m = max(m, (unsigned int)(offs[i + 1] - offs[i]));
-  atomicMax(out, m);
-}
+struct Dia {
+  int nd;
+  int off[MAXD];       // ascending column offsets
+  int mir[MAXD];       // mirror diagonal: off[mir[d]] == -off[d]
+  long long n;
+  const double* a;     // [nd][n]
+  const double* g;     // [nd][n]
+  const unsigned char* mask;  // [n], bit d: entry (i, i+off[d]) stored
+};
 
 struct Dev {
   // tile table
   const long long* blk_r0;
   const int* blk_sys;
   const int* sys_blk0;
-  const long long* sys_r1;  // per system end row
-  int nblk;
-  // matrices
+  const long long* sys_r1;
+  // matrices (CSR)
   const int32_t *a_offs, *a_cols; const double* a_vals;
   const int32_t *g_offs, *g_cols; const double* g_vals;
   const int32_t *gt_offs, *gt_cols; const double* gt_vals;
   const double* inv_diag;
+  Dia dia;
   // vectors
   double *b, *x, *r0, *r1, *d0, *d1, *q, *s, *t;
   // reduction scratch
@@ -84,133 +89,96 @@ struct Dev {
   Ctl* ctl;
 };
 
-// ------------------------------------------------------------------ tile pipeline
-struct __align__(16) Pipe {
-  double vals[2][PCAP + 2];
-  int32_t cols[2][PCAP + 4];
-  int32_t offs[2][PR + 8];
-  uint64_t bar[2];
-  int meta[2][4];  // base_v, base_c, base_o, staged
-  double red[PR / 32];
-  int flag;
-};
+__global__ void k_snapshot(Ctl* c) { c->snap = c->n_active; }
 
-struct Mat {
-  const int32_t* offs;
-  const int32_t* cols;
-  const double* vals;
-};
-
-// Issue the bulk copies of tile t into buffer `buf` (one thread).
-__device__ __forceinline__ void issue_tile(const Dev& D, Pipe& P, const Mat& M, int t, int buf) {
-  const int sys = D.blk_sys[t];
-  const long long r0 = D.blk_r0[t];
-  const long long r1 = min(r0 + PR, D.sys_r1[sys]);
-  const int e0 = __ldg(M.offs + r0), e1 = __ldg(M.offs + r1);
-  const int a0v = e0 & ~1, a1v = (e1 + 1) & ~1;
-  const int a0c = e0 & ~3, a1c = (e1 + 3) & ~3;
-  const long long o0 = r0 & ~3LL, o1 = (r1 + 1 + 3) & ~3LL;
-  const bool fits = (a1v - a0v) <= PCAP + 2 && (a1c - a0c) <= PCAP + 4;
-  const uint32_t ob = (uint32_t)((o1 - o0) * 4);
-  const uint32_t vb = fits ? (uint32_t)((a1v - a0v) * 8) : 0u;
-  const uint32_t cb = fits ? (uint32_t)((a1c - a0c) * 4) : 0u;
-  P.meta[buf][0] = a0v;
-  P.meta[buf][1] = a0c;
-  P.meta[buf][2] = (int)o0;
-  P.meta[buf][3] = fits ? 1 : 0;
-  fence_proxy_async_smem();
-  mbar_arrive_expect_tx(&P.bar[buf], ob + vb + cb);
-  bulk_g2s(P.offs[buf], M.offs + o0, ob, &P.bar[buf]);
-  if (vb) bulk_g2s(P.vals[buf], M.vals + a0v, vb, &P.bar[buf]);
-  if (cb) bulk_g2s(P.cols[buf], M.cols + a0c, cb, &P.bar[buf]);
+__global__ void k_max_row(const int32_t* __restrict__ offs, int64_t n, unsigned int* out) {
+  unsigned int m = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    m = max(m, (unsigned int)(offs[i + 1] - offs[i]));
+  atomicMax(out, m);
 }
 
-// View of one staged tile: pointers valid for global entry / row indices of that tile.
-struct TileView {
-  const double* v;
-  const int32_t* c;
-  const int32_t* o;  // o[i] = row offset of global row i
-};
-
-__device__ __forceinline__ TileView view(const Pipe& P, const Mat& M, int buf) {
-  TileView tv;
-  tv.o = P.offs[buf] - P.meta[buf][2];
-  if (P.meta[buf][3]) {
-    tv.v = P.vals[buf] - P.meta[buf][0];
-    tv.c = P.cols[buf] - P.meta[buf][1];
-  } else {
-    tv.v = M.vals;
-    tv.c = M.cols;
-  }
-  return tv;
+__global__ void k_differ(const int32_t* __restrict__ a, const int32_t* __restrict__ b, int64_t n, unsigned int* flag) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+    if (a[k] != b[k]) { *flag = 1u; return; }
 }
 
-// Next tile >= t (stride gridDim.x) whose system satisfies `want(status)`; D.nblk if none.
-template <class Want>
-__device__ __forceinline__ int next_tile(const Dev& D, int t, const Want& want) {
-  for (; t < D.nblk; t += gridDim.x)
-    if (want(D.st[D.blk_sys[t]].status)) return t;
-  return D.nblk;
-}
-
-// Round-robin persistent loop over the CTA's tiles with a 2-stage TMA pipeline.
-// body(t, sys, r0, r1, TileView) is executed by all threads and must be CTA-uniform.
-template <bool STAGE, class Want, class Body>
-__device__ __forceinline__ void tile_loop(const Dev& D, Pipe& P, const Mat& M, const Want& want, const Body& body) {
-  if (STAGE && threadIdx.x == 0) {
-    mbar_init(&P.bar[0], 1);
-    mbar_init(&P.bar[1], 1);
-    mbar_init_fence();
-  }
-  __syncthreads();
-  int t = next_tile(D, blockIdx.x, want);
-  if (STAGE && threadIdx.x == 0 && t < D.nblk) issue_tile(D, P, M, t, 0);
-  int buf = 0;
-  uint32_t phase0 = 0, phase1 = 0;
-  while (t < D.nblk) {
-    const int tn = next_tile(D, t + gridDim.x, want);
-    if (STAGE && threadIdx.x == 0 && tn < D.nblk) issue_tile(D, P, M, tn, buf ^ 1);
-    const int sys = D.blk_sys[t];
-    const long long r0 = D.blk_r0[t];
-    const long long r1 = min(r0 + PR, D.sys_r1[sys]);
-    TileView tv{M.vals, M.cols, M.offs};
-    if (STAGE) {
-      mbar_wait(&P.bar[buf], buf ? phase1 : phase0);
-      if (buf) phase1 ^= 1u; else phase0 ^= 1u;
-      tv = view(P, M, buf);
+// ------------------------------------------------------------------ DIA detection / conversion
+// Insert every (col - row) into a 16-slot device set; overflow => not DIA-able.
+__global__ void k_dia_offsets(const int32_t* __restrict__ offs, const int32_t* __restrict__ cols, int64_t n,
+                              int* slots, int* nslots, int* overflow) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    for (int32_t k = offs[i]; k < offs[i + 1]; ++k) {
+      const int o = cols[k] - (int)i;
+      bool found = false;
+      const int cnt = min(*(volatile int*)nslots, 16);
+      for (int s = 0; s < cnt && !found; ++s) found = ((volatile int*)slots)[s] == o;
+      if (found) continue;
+      for (int s = 0; s < 16; ++s) {
+        const int prev = atomicCAS(&slots[s], INT_MIN, o);
+        if (prev == INT_MIN) { atomicMax(nslots, s + 1); found = true; break; }
+        if (prev == o) { found = true; break; }
+      }
+      if (!found) *overflow = 1;
     }
-    body(t, sys, r0, r1, tv);
-    __syncthreads();  // buffer `buf` is free again; body's shared scratch may be reused
-    t = tn;
-    buf ^= 1;
   }
 }
 
-// Publish tile t's two partials; returns true in ALL threads of the CTA that completed the
-// last tile of `sys`.
-__device__ __forceinline__ bool arrive(const Dev& D, Pipe& P, int t, int sys, double p0, double p1) {
-  const double a = block_sum(p0, P.red);
-  const double b = block_sum(p1, P.red);
+// CSR -> diagonal-major values (+ presence mask).  Every slot of every row is written.
+__global__ void k_csr_to_dia(const int32_t* __restrict__ offs, const int32_t* __restrict__ cols,
+                             const double* __restrict__ vals, int64_t n, Dia dia, double* out,
+                             unsigned char* mask) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double v[MAXD];
+#pragma unroll
+    for (int d = 0; d < MAXD; ++d) v[d] = 0.0;
+    unsigned int m = 0;
+    for (int32_t k = offs[i]; k < offs[i + 1]; ++k) {
+      const int o = cols[k] - (int)i;
+#pragma unroll
+      for (int d = 0; d < MAXD; ++d)
+        if (d < dia.nd && dia.off[d] == o) { v[d] = vals[k]; m |= 1u << d; }
+    }
+#pragma unroll
+    for (int d = 0; d < MAXD; ++d)
+      if (d < dia.nd) out[(int64_t)d * n + i] = v[d];
+    if (mask) mask[i] = (unsigned char)m;
+  }
+}
+
+// ------------------------------------------------------------------ shared per-tile plumbing
+__device__ __forceinline__ void block_rows(const Dev& D, int& sys, long long& r0, long long& r1) {
+  sys = D.blk_sys[blockIdx.x];
+  r0 = D.blk_r0[blockIdx.x];
+  const long long e = r0 + PR;
+  const long long se = D.sys_r1[sys];
+  r1 = e < se ? e : se;
+}
+
+// Publish this CTA's two partials; returns true in ALL threads of the last CTA of `sys`.
+__device__ __forceinline__ bool arrive(const Dev& D, int sys, double p0, double p1, double* red, int* flag) {
+  const double a = block_sum(p0, red);
+  const double b = block_sum(p1, red);
   if (threadIdx.x == 0) {
-    D.part[2 * t + 0] = a;
-    D.part[2 * t + 1] = b;
+    D.part[2 * blockIdx.x + 0] = a;
+    D.part[2 * blockIdx.x + 1] = b;
     __threadfence();
     const unsigned int nb = (unsigned)(D.sys_blk0[sys + 1] - D.sys_blk0[sys]);
     const unsigned int old = atomicAdd(&D.counter[sys], 1u);
-    P.flag = (old == nb - 1);
+    *flag = (old == nb - 1);
   }
   __syncthreads();
-  const bool last = P.flag;
+  const bool last = *flag;
   if (last) __threadfence();
   return last;
 }
 
 // Deterministic per-system sum of partial slot `which` (valid in thread 0).
-__device__ __forceinline__ double gather_partials(const Dev& D, Pipe& P, int sys, int which) {
+__device__ __forceinline__ double gather_partials(const Dev& D, int sys, int which, double* red) {
   const int b0 = D.sys_blk0[sys], b1 = D.sys_blk0[sys + 1];
   double v = 0.0;
   for (int b = b0 + threadIdx.x; b < b1; b += blockDim.x) v += __ldcg(&D.part[2 * b + which]);
-  return block_sum(v, P.red);
+  return block_sum(v, red);
 }
 
 __device__ __forceinline__ void finish(const Dev& D, SysState& S, int conv) {
@@ -224,298 +192,365 @@ __device__ __forceinline__ void put_hist(const Dev& D, int sys, long long i, dou
   if (c.track && i < c.hcap) c.hist[(long long)sys * c.hcap + i] = v;
 }
 
-struct WantAll { __device__ bool operator()(int) const { return true; } };
-struct WantRun { __device__ bool operator()(int s) const { return s == ST_RUN; } };
-struct WantLive { __device__ bool operator()(int s) const { return s != ST_DONE; } };
-
-template <int PRE>
-__device__ __forceinline__ Mat mat_g(const Dev& D) { return Mat{D.g_offs, D.g_cols, D.g_vals}; }
-__device__ __forceinline__ Mat mat_gt(const Dev& D) { return Mat{D.gt_offs, D.gt_cols, D.gt_vals}; }
-__device__ __forceinline__ Mat mat_a(const Dev& D) { return Mat{D.a_offs, D.a_cols, D.a_vals}; }
-
-template <int ORDER, bool SH, int XM>
-__device__ __forceinline__ double trow(const TileView& tv, long long i, const XF& f) {
-  return row_reduce<ORDER, SH, XM>(tv.v, tv.c, tv.o[i], tv.o[i + 1], f);
+// ------------------------------------------------------------------ finalizers (thread 0)
+__device__ void fin_setup1(const Dev& D, int sys, double bb) {
+  SysState& S = D.st[sys];
+  S.norm_b = __dsqrt_rn(bb);
+  S.rr = bb;
+  D.counter[sys] = 0;
 }
 
-// ------------------------------------------------------------------ setup
+__device__ void fin_setup2(const Dev& D, int sys, double rs) {
+  SysState& S = D.st[sys];
+  D.counter[sys] = 0;
+  const Ctl& c = *D.ctl;
+  S.i = 0;
+  S.beta = 0.0;
+  S.flags = 0;
+  S.notspd = 0;
+  S.converged = 0;
+  S.hist_len = 1;
+  if (S.norm_b == 0.0) {  // pcg.py:159-164
+    put_hist(D, sys, 0, 0.0);
+    finish(D, S, 1);
+    return;
+  }
+  put_hist(D, sys, 0, __ddiv_rn(__dsqrt_rn(S.rr), S.norm_b));
+  S.delta = rs;
+  if (rs < 0.0) {  // pcg.py:171-172
+    S.notspd = 1; S.fail_iter = 0; S.fail_value = rs; S.fail_kind = 2;
+    finish(D, S, 0);
+    return;
+  }
+  S.delta0 = rs;
+  S.rtol2d0 = mul(mul(c.rtol, c.rtol), rs);
+  if (c.delta_mode) {
+    if (S.max_iters <= 0 || rs <= S.rtol2d0) S.status = ST_CERTIFY;
+  } else if (S.max_iters <= 0) {
+    finish(D, S, 0);
+  }
+}
+
+__device__ void fin_k1(const Dev& D, int sys, bool run, double dq, double rrf) {
+  SysState& S = D.st[sys];
+  D.counter[sys] = 0;
+  const Ctl& c = *D.ctl;
+  if (!run) {  // delta-test certification (pcg.py:217-220)
+    const double rel = __ddiv_rn(__dsqrt_rn(rrf), S.norm_b);
+    finish(D, S, rel <= c.rtol);
+    return;
+  }
+  if (S.flags & FL_FRESH) {  // pcg.py:208-215
+    S.flags &= ~FL_FRESH;
+    const double rel = __ddiv_rn(__dsqrt_rn(rrf), S.norm_b);
+    put_hist(D, sys, S.i, rel);
+    if (rel <= c.rtol) { finish(D, S, 1); return; }
+    if (S.i >= S.max_iters) { finish(D, S, 0); return; }
+  }
+  if (dq <= 0.0) {  // pcg.py:182-184
+    S.notspd = 1; S.fail_iter = S.i; S.fail_value = dq; S.fail_kind = 1;
+    finish(D, S, 0);
+    return;
+  }
+  S.dq = dq;
+  S.alpha = __ddiv_rn(S.delta, dq);
+}
+
+__device__ void fin_rr(const Dev& D, int sys, double rr) {
+  D.st[sys].rr = rr;
+  D.counter[sys] = 0;
+}
+
+__device__ void fin_k3(const Dev& D, int sys, double rs, int refreshed) {
+  SysState& S = D.st[sys];
+  D.counter[sys] = 0;
+  const Ctl& c = *D.ctl;
+  const double delta_old = S.delta;
+  S.delta = rs;
+  if (rs < 0.0) {  // pcg.py:196-198
+    S.notspd = 1; S.fail_iter = S.i; S.fail_value = rs; S.fail_kind = 2;
+    finish(D, S, 0);
+    return;
+  }
+  S.beta = __ddiv_rn(rs, delta_old);
+  S.i += 1;
+  const double rel = __ddiv_rn(__dsqrt_rn(S.rr), S.norm_b);
+  put_hist(D, sys, S.i, rel);
+  S.hist_len = S.i + 1;
+  if (!c.delta_mode) {
+    if (rel <= c.rtol) {
+      if (refreshed) { finish(D, S, 1); return; }
+      S.flags |= FL_FRESH;
+    } else if (S.i >= S.max_iters) {
+      finish(D, S, 0);
+    }
+  } else if (S.i >= S.max_iters || rs <= S.rtol2d0) {
+    S.status = ST_CERTIFY;
+  }
+}
+
+// ------------------------------------------------------------------ row operators
+// CSR: a staged RowTile.  DIA: diagonal-major values + mask.  Both expose
+//   A(i, X)  : numpy-order  sum_k A_ik X(col_k)
+//   G(i, X)  : numpy-order  sum_k G_ik X(col_k)
+//   Gt(i, X) : add.at order sum_k (G^T)_ik X(col_k)
+template <bool SH>
+struct CsrOps {
+  const RowTile<PR, PCAP>* T;
+  long long r0;
+  const int32_t* cols;
+  const double* vals;
+  template <int ORDER, int XM>
+  __device__ __forceinline__ double row(long long i, const XF& f) const {
+    return tile_row_dot<ORDER, SH, XM>(*T, (int)(i - r0), cols, vals, f);
+  }
+};
+
+// numpy-order reduction over the present diagonals of row i of a diagonal-major matrix.
+template <int ND, int XM>
+__device__ __forceinline__ double dia_row_numpy(const Dia& dd, const double* __restrict__ V, long long i,
+                                                unsigned int m, const XF& f) {
+  double first = 0.0, s = 0.0;
+  bool have = false, more = false;
+#pragma unroll
+  for (int d = 0; d < ND; ++d) {
+    if (m & (1u << d)) {
+      const double p = mul(__ldg(V + (long long)d * dd.n + i), xval<XM>(f, (int32_t)(i + dd.off[d])));
+      if (!have) { first = p; have = true; }
+      else { s = add(s, p); more = true; }
+    }
+  }
+  return more ? add(first, s) : first;
+}
+
+// add.at order over row i of G^T, read from G's mirror diagonals.
+template <int ND, int XM>
+__device__ __forceinline__ double dia_row_t_seq(const Dia& dd, const double* __restrict__ V, long long i,
+                                                unsigned int m, const XF& f) {
+  double s = 0.0;
+#pragma unroll
+  for (int d = 0; d < ND; ++d) {
+    if (m & (1u << d)) {
+      const long long j = i + dd.off[d];
+      s = add(s, mul(__ldg(V + (long long)dd.mir[d] * dd.n + j), xval<XM>(f, (int32_t)j)));
+    }
+  }
+  return s;
+}
+
+// ------------------------------------------------------------------ kernels
+// FMT 0 = CSR (SH: short rows), FMT 1 = DIA with ND diagonals.
+template <int FMT, int ND>
+struct Fmt {};
+
+#define SG_KERNEL_PROLOGUE                      \
+  __shared__ RowTile<PR, (FMT == 0 ? PCAP : 4)> T; \
+  __shared__ double red[PR / 32];               \
+  __shared__ int flag;                          \
+  int sys; long long r0, r1;                    \
+  block_rows(D, sys, r0, r1);                   \
+  const long long i = r0 + threadIdx.x;         \
+  (void)T;
+
+// A-row (numpy order) for either format.
+template <int FMT, int ND, bool SH, int XM>
+__device__ __forceinline__ double rowA(const Dev& D, const RowTile<PR, (FMT == 0 ? PCAP : 4)>& T, long long i,
+                                       long long r0, unsigned int m, const XF& f) {
+  if (FMT == 1) return dia_row_numpy<ND, XM>(D.dia, D.dia.a, i, m, f);
+  return tile_row_dot<kOrderNumpy, SH, XM>(*reinterpret_cast<const RowTile<PR, PCAP>*>(&T), (int)(i - r0),
+                                           D.a_cols, D.a_vals, f);
+}
+template <int FMT, int ND, bool SH, int XM>
+__device__ __forceinline__ double rowG(const Dev& D, const RowTile<PR, (FMT == 0 ? PCAP : 4)>& T, long long i,
+                                       long long r0, unsigned int m, const XF& f) {
+  if (FMT == 1) return dia_row_numpy<ND, XM>(D.dia, D.dia.g, i, m, f);
+  return tile_row_dot<kOrderNumpy, SH, XM>(*reinterpret_cast<const RowTile<PR, PCAP>*>(&T), (int)(i - r0),
+                                           D.g_cols, D.g_vals, f);
+}
+template <int FMT, int ND, bool SH, int XM>
+__device__ __forceinline__ double rowGt(const Dev& D, const RowTile<PR, (FMT == 0 ? PCAP : 4)>& T, long long i,
+                                        long long r0, unsigned int m, const XF& f) {
+  if (FMT == 1) return dia_row_t_seq<ND, XM>(D.dia, D.dia.g, i, m, f);
+  return tile_row_dot<kOrderSeq, SH, XM>(*reinterpret_cast<const RowTile<PR, PCAP>*>(&T), (int)(i - r0),
+                                         D.gt_cols, D.gt_vals, f);
+}
+
+template <int FMT>
+__device__ __forceinline__ void stage(const Dev& D, RowTile<PR, (FMT == 0 ? PCAP : 4)>& T, long long r0,
+                                      long long r1, const int32_t* offs, const int32_t* cols, const double* vals) {
+  if (FMT == 0) stage_rows(*reinterpret_cast<RowTile<PR, PCAP>*>(&T), r0, r1, offs, cols, vals);
+}
+
+__device__ __forceinline__ unsigned int dmask(const Dev& D, long long i, long long r1, int FMT) {
+  return (FMT == 1 && i < r1) ? (unsigned int)D.dia.mask[i] : 0u;
+}
+
 // r = b; d = 0; x = 0; t = G^T b; partial ||b||^2
-template <int PRE, bool SH>
+template <int PRE, int FMT, int ND, bool SH>
 __global__ void __launch_bounds__(PR) k_setup1(Dev D) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  Pipe& P = *reinterpret_cast<Pipe*>(smem_raw);
-  tile_loop<PRE == SG_PRECOND_LEARNED>(D, P, mat_gt(D), WantAll{},
-      [&](int t, int sys, long long r0, long long r1, const TileView& tv) {
-    const long long i = r0 + threadIdx.x;
-    double pbb = 0.0;
-    if (i < r1) {
-      const double bi = D.b[i];
-      D.r0[i] = bi;
-      D.d0[i] = 0.0;
-      D.d1[i] = 0.0;
-      D.x[i] = 0.0;
-      pbb = mul(bi, bi);
-      if (PRE == SG_PRECOND_LEARNED) D.t[i] = trow<kOrderSeq, SH, 0>(tv, i, XF{D.b, nullptr, 0.0});
-    }
-    if (arrive(D, P, t, sys, pbb, 0.0)) {
-      const double bb = gather_partials(D, P, sys, 0);
-      if (threadIdx.x == 0) {
-        SysState& S = D.st[sys];
-        S.norm_b = __dsqrt_rn(bb);
-        S.rr = bb;
-        D.counter[sys] = 0;
-      }
-    }
-  });
+  SG_KERNEL_PROLOGUE
+  if (PRE == SG_PRECOND_LEARNED) stage<FMT>(D, T, r0, r1, D.gt_offs, D.gt_cols, D.gt_vals);
+  const unsigned int m = dmask(D, i, r1, FMT);
+  double pbb = 0.0;
+  if (i < r1) {
+    const double bi = D.b[i];
+    D.r0[i] = bi;
+    D.d0[i] = 0.0;
+    D.d1[i] = 0.0;
+    D.x[i] = 0.0;
+    pbb = mul(bi, bi);
+    if (PRE == SG_PRECOND_LEARNED) D.t[i] = rowGt<FMT, ND, SH, 0>(D, T, i, r0, m, XF{D.b, nullptr, 0.0});
+  }
+  if (arrive(D, sys, pbb, 0.0, red, &flag)) {
+    const double bb = gather_partials(D, sys, 0, red);
+    if (threadIdx.x == 0) fin_setup1(D, sys, bb);
+  }
 }
 
-template <int PRE, bool SH>
-__device__ __forceinline__ double apply_row(const Dev& D, const TileView& tv, long long i, const double* r,
+template <int PRE, int FMT, int ND, bool SH>
+__device__ __forceinline__ double apply_row(const Dev& D, const RowTile<PR, (FMT == 0 ? PCAP : 4)>& T,
+                                            long long i, long long r0, unsigned int m, const double* r,
                                             double eps) {
   if (PRE == SG_PRECOND_IDENTITY) return r[i];
   if (PRE == SG_PRECOND_JACOBI) return mul(r[i], D.inv_diag[i]);
-  const double y = trow<kOrderNumpy, SH, 0>(tv, i, XF{D.t, nullptr, 0.0});
+  const double y = rowG<FMT, ND, SH, 0>(D, T, i, r0, m, XF{D.t, nullptr, 0.0});
   return add(y, mul(eps, r[i]));
 }
 
 // s = M r0; delta0 = r.s; NotSpd check; top-of-loop checks for i = 0.
-template <int PRE, bool SH>
+template <int PRE, int FMT, int ND, bool SH>
 __global__ void __launch_bounds__(PR) k_setup2(Dev D) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  Pipe& P = *reinterpret_cast<Pipe*>(smem_raw);
-  const double eps = D.ctl->eps;
-  tile_loop<PRE == SG_PRECOND_LEARNED>(D, P, mat_g<PRE>(D), WantAll{},
-      [&](int t, int sys, long long r0, long long r1, const TileView& tv) {
-    const long long i = r0 + threadIdx.x;
-    double prs = 0.0;
-    if (i < r1) {
-      const double si = apply_row<PRE, SH>(D, tv, i, D.r0, eps);
-      D.s[i] = si;
-      prs = mul(D.r0[i], si);
-    }
-    if (arrive(D, P, t, sys, prs, 0.0)) {
-      const double rs = gather_partials(D, P, sys, 0);
-      if (threadIdx.x == 0) {
-        SysState& S = D.st[sys];
-        D.counter[sys] = 0;
-        const Ctl& c = *D.ctl;
-        S.i = 0;
-        S.beta = 0.0;
-        S.flags = 0;
-        S.notspd = 0;
-        S.converged = 0;
-        S.hist_len = 1;
-        if (S.norm_b == 0.0) {  // pcg.py:159-164
-          put_hist(D, sys, 0, 0.0);
-          finish(D, S, 1);
-          return;
-        }
-        put_hist(D, sys, 0, __ddiv_rn(__dsqrt_rn(S.rr), S.norm_b));
-        S.delta = rs;
-        if (rs < 0.0) {  // pcg.py:171-172
-          S.notspd = 1; S.fail_iter = 0; S.fail_value = rs; S.fail_kind = 2;
-          finish(D, S, 0);
-          return;
-        }
-        S.delta0 = rs;
-        S.rtol2d0 = mul(mul(c.rtol, c.rtol), rs);
-        if (c.delta_mode) {
-          if (S.max_iters <= 0 || rs <= S.rtol2d0) S.status = ST_CERTIFY;
-        } else if (S.max_iters <= 0) {
-          finish(D, S, 0);
-        }
-      }
-    }
-  });
-}
-
-// ------------------------------------------------------------------ K1
-template <int PRE, bool SH>
-__global__ void __launch_bounds__(PR) k_iter1(Dev D, int par) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  Pipe& P = *reinterpret_cast<Pipe*>(smem_raw);
-  double* dc = par ? D.d1 : D.d0;
-  double* dn = par ? D.d0 : D.d1;
-  double* rc = par ? D.r1 : D.r0;
-  tile_loop<true>(D, P, mat_a(D), WantLive{},
-      [&](int t, int sys, long long r0, long long r1, const TileView& tv) {
-    const int status = D.st[sys].status;
-    const bool run = status == ST_RUN;
-    const bool fresh = run ? (D.st[sys].flags & FL_FRESH) != 0 : true;
-    const double beta = D.st[sys].beta;
-    const long long i = r0 + threadIdx.x;
-    double pdq = 0.0, prr = 0.0;
-    if (i < r1) {
-      if (run) {
-        const double dni = add(D.s[i], mul(beta, dc[i]));
-        dn[i] = dni;
-        const double qi = trow<kOrderNumpy, SH, 1>(tv, i, XF{D.s, dc, beta});
-        D.q[i] = qi;
-        pdq = mul(dni, qi);
-      }
-      if (fresh) {
-        const double rf = sub(D.b[i], trow<kOrderNumpy, SH, 0>(tv, i, XF{D.x, nullptr, 0.0}));
-        if (run) rc[i] = rf;
-        prr = mul(rf, rf);
-      }
-    }
-    if (arrive(D, P, t, sys, pdq, prr)) {
-      const double dq = gather_partials(D, P, sys, 0);
-      const double rrf = gather_partials(D, P, sys, 1);
-      if (threadIdx.x == 0) {
-        SysState& S = D.st[sys];
-        D.counter[sys] = 0;
-        const Ctl& c = *D.ctl;
-        if (!run) {  // delta-test certification (pcg.py:217-220)
-          const double rel = __ddiv_rn(__dsqrt_rn(rrf), S.norm_b);
-          finish(D, S, rel <= c.rtol);
-          return;
-        }
-        if (S.flags & FL_FRESH) {  // pcg.py:208-215
-          S.flags &= ~FL_FRESH;
-          const double rel = __ddiv_rn(__dsqrt_rn(rrf), S.norm_b);
-          put_hist(D, sys, S.i, rel);
-          if (rel <= c.rtol) { finish(D, S, 1); return; }
-          if (S.i >= S.max_iters) { finish(D, S, 0); return; }
-        }
-        if (dq <= 0.0) {  // pcg.py:182-184
-          S.notspd = 1; S.fail_iter = S.i; S.fail_value = dq; S.fail_kind = 1;
-          finish(D, S, 0);
-          return;
-        }
-        S.dq = dq;
-        S.alpha = __ddiv_rn(S.delta, dq);
-      }
-    }
-  });
-}
-
-// ------------------------------------------------------------------ K2 (non-refresh)
-template <int PRE, bool SH>
-__global__ void __launch_bounds__(PR) k_iter2(Dev D, int par) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  Pipe& P = *reinterpret_cast<Pipe*>(smem_raw);
-  const double* dn = par ? D.d0 : D.d1;
-  const double* rc = par ? D.r1 : D.r0;
-  double* rn = par ? D.r0 : D.r1;
-  tile_loop<PRE == SG_PRECOND_LEARNED>(D, P, mat_gt(D), WantRun{},
-      [&](int t, int sys, long long r0, long long r1, const TileView& tv) {
-    const double alpha = D.st[sys].alpha;
-    const long long i = r0 + threadIdx.x;
-    double prr = 0.0;
-    if (i < r1) {
-      D.x[i] = add(D.x[i], mul(alpha, dn[i]));
-      const double rni = sub(rc[i], mul(alpha, D.q[i]));
-      rn[i] = rni;
-      prr = mul(rni, rni);
-      if (PRE == SG_PRECOND_LEARNED) D.t[i] = trow<kOrderSeq, SH, 2>(tv, i, XF{rc, D.q, alpha});
-    }
-    if (arrive(D, P, t, sys, prr, 0.0)) {
-      const double rr = gather_partials(D, P, sys, 0);
-      if (threadIdx.x == 0) {
-        D.st[sys].rr = rr;
-        D.counter[sys] = 0;
-      }
-    }
-  });
-}
-
-// ------------------------------------------------------------------ K2 refresh variants
-__global__ void __launch_bounds__(PR) k_refresh_x(Dev D, int par) {
-  const double* dn = par ? D.d0 : D.d1;
-  for (int t = blockIdx.x; t < D.nblk; t += gridDim.x) {
-    const int sys = D.blk_sys[t];
-    if (D.st[sys].status != ST_RUN) continue;
-    const double alpha = D.st[sys].alpha;
-    const long long r0 = D.blk_r0[t];
-    const long long i = r0 + threadIdx.x;
-    if (i < min(r0 + PR, D.sys_r1[sys])) D.x[i] = add(D.x[i], mul(alpha, dn[i]));
+  SG_KERNEL_PROLOGUE
+  if (PRE == SG_PRECOND_LEARNED) stage<FMT>(D, T, r0, r1, D.g_offs, D.g_cols, D.g_vals);
+  const unsigned int m = dmask(D, i, r1, FMT);
+  double prs = 0.0;
+  if (i < r1) {
+    const double si = apply_row<PRE, FMT, ND, SH>(D, T, i, r0, m, D.r0, D.ctl->eps);
+    D.s[i] = si;
+    prs = mul(D.r0[i], si);
+  }
+  if (arrive(D, sys, prs, 0.0, red, &flag)) {
+    const double rs = gather_partials(D, sys, 0, red);
+    if (threadIdx.x == 0) fin_setup2(D, sys, rs);
   }
 }
 
-template <bool SH>
-__global__ void __launch_bounds__(PR) k_refresh_r(Dev D, int par) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  Pipe& P = *reinterpret_cast<Pipe*>(smem_raw);
+template <int PRE, int FMT, int ND, bool SH>
+__global__ void __launch_bounds__(PR) k_iter1(Dev D, int par) {
+  SG_KERNEL_PROLOGUE
+  const int status = D.st[sys].status;
+  if (status == ST_DONE) return;
+  const bool run = status == ST_RUN;
+  const bool fresh = run ? (D.st[sys].flags & FL_FRESH) != 0 : true;
+  const double beta = D.st[sys].beta;
+  double* dc = par ? D.d1 : D.d0;
+  double* dn = par ? D.d0 : D.d1;
+  double* rc = par ? D.r1 : D.r0;
+  stage<FMT>(D, T, r0, r1, D.a_offs, D.a_cols, D.a_vals);
+  const unsigned int m = dmask(D, i, r1, FMT);
+  double pdq = 0.0, prr = 0.0;
+  if (i < r1) {
+    if (run) {
+      const double dni = add(D.s[i], mul(beta, dc[i]));
+      dn[i] = dni;
+      const double qi = rowA<FMT, ND, SH, 1>(D, T, i, r0, m, XF{D.s, dc, beta});
+      D.q[i] = qi;
+      pdq = mul(dni, qi);
+    }
+    if (fresh) {
+      const double rf = sub(D.b[i], rowA<FMT, ND, SH, 0>(D, T, i, r0, m, XF{D.x, nullptr, 0.0}));
+      if (run) rc[i] = rf;
+      prr = mul(rf, rf);
+    }
+  }
+  if (arrive(D, sys, pdq, prr, red, &flag)) {
+    const double dq = gather_partials(D, sys, 0, red);
+    const double rrf = gather_partials(D, sys, 1, red);
+    if (threadIdx.x == 0) fin_k1(D, sys, run, dq, rrf);
+  }
+}
+
+template <int PRE, int FMT, int ND, bool SH>
+__global__ void __launch_bounds__(PR) k_iter2(Dev D, int par) {
+  SG_KERNEL_PROLOGUE
+  if (D.st[sys].status != ST_RUN) return;
+  const double alpha = D.st[sys].alpha;
+  const double* dn = par ? D.d0 : D.d1;
+  const double* rc = par ? D.r1 : D.r0;
   double* rn = par ? D.r0 : D.r1;
-  tile_loop<true>(D, P, mat_a(D), WantRun{},
-      [&](int t, int sys, long long r0, long long r1, const TileView& tv) {
-    const long long i = r0 + threadIdx.x;
-    double prr = 0.0;
-    if (i < r1) {
-      const double rni = sub(D.b[i], trow<kOrderNumpy, SH, 0>(tv, i, XF{D.x, nullptr, 0.0}));
-      rn[i] = rni;
-      prr = mul(rni, rni);
-    }
-    if (arrive(D, P, t, sys, prr, 0.0)) {
-      const double rr = gather_partials(D, P, sys, 0);
-      if (threadIdx.x == 0) {
-        D.st[sys].rr = rr;
-        D.counter[sys] = 0;
-      }
-    }
-  });
+  if (PRE == SG_PRECOND_LEARNED) stage<FMT>(D, T, r0, r1, D.gt_offs, D.gt_cols, D.gt_vals);
+  const unsigned int m = dmask(D, i, r1, FMT);
+  double prr = 0.0;
+  if (i < r1) {
+    D.x[i] = add(D.x[i], mul(alpha, dn[i]));
+    const double rni = sub(rc[i], mul(alpha, D.q[i]));
+    rn[i] = rni;
+    prr = mul(rni, rni);
+    if (PRE == SG_PRECOND_LEARNED) D.t[i] = rowGt<FMT, ND, SH, 2>(D, T, i, r0, m, XF{rc, D.q, alpha});
+  }
+  if (arrive(D, sys, prr, 0.0, red, &flag)) {
+    const double rr = gather_partials(D, sys, 0, red);
+    if (threadIdx.x == 0) fin_rr(D, sys, rr);
+  }
 }
 
-template <bool SH>
+__global__ void __launch_bounds__(PR) k_refresh_x(Dev D, int par) {
+  int sys; long long r0, r1;
+  block_rows(D, sys, r0, r1);
+  if (D.st[sys].status != ST_RUN) return;
+  const double alpha = D.st[sys].alpha;
+  const double* dn = par ? D.d0 : D.d1;
+  const long long i = r0 + threadIdx.x;
+  if (i < r1) D.x[i] = add(D.x[i], mul(alpha, dn[i]));
+}
+
+template <int FMT, int ND, bool SH>
+__global__ void __launch_bounds__(PR) k_refresh_r(Dev D, int par) {
+  SG_KERNEL_PROLOGUE
+  if (D.st[sys].status != ST_RUN) return;
+  double* rn = par ? D.r0 : D.r1;
+  stage<FMT>(D, T, r0, r1, D.a_offs, D.a_cols, D.a_vals);
+  const unsigned int m = dmask(D, i, r1, FMT);
+  double prr = 0.0;
+  if (i < r1) {
+    const double rni = sub(D.b[i], rowA<FMT, ND, SH, 0>(D, T, i, r0, m, XF{D.x, nullptr, 0.0}));
+    rn[i] = rni;
+    prr = mul(rni, rni);
+  }
+  if (arrive(D, sys, prr, 0.0, red, &flag)) {
+    const double rr = gather_partials(D, sys, 0, red);
+    if (threadIdx.x == 0) fin_rr(D, sys, rr);
+  }
+}
+
+template <int FMT, int ND, bool SH>
 __global__ void __launch_bounds__(PR) k_refresh_t(Dev D, int par) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  Pipe& P = *reinterpret_cast<Pipe*>(smem_raw);
+  SG_KERNEL_PROLOGUE
+  if (D.st[sys].status != ST_RUN) return;
   const double* rn = par ? D.r0 : D.r1;
-  tile_loop<true>(D, P, mat_gt(D), WantRun{},
-      [&](int t, int sys, long long r0, long long r1, const TileView& tv) {
-    const long long i = r0 + threadIdx.x;
-    if (i < r1) D.t[i] = trow<kOrderSeq, SH, 0>(tv, i, XF{rn, nullptr, 0.0});
-  });
+  stage<FMT>(D, T, r0, r1, D.gt_offs, D.gt_cols, D.gt_vals);
+  const unsigned int m = dmask(D, i, r1, FMT);
+  if (i < r1) D.t[i] = rowGt<FMT, ND, SH, 0>(D, T, i, r0, m, XF{rn, nullptr, 0.0});
+  (void)red; (void)flag;
 }
 
-// ------------------------------------------------------------------ K3
-template <int PRE, bool SH>
+template <int PRE, int FMT, int ND, bool SH>
 __global__ void __launch_bounds__(PR) k_iter3(Dev D, int par, int refreshed) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  Pipe& P = *reinterpret_cast<Pipe*>(smem_raw);
+  SG_KERNEL_PROLOGUE
+  if (D.st[sys].status != ST_RUN) return;
   const double* rn = par ? D.r0 : D.r1;
-  const double eps = D.ctl->eps;
-  tile_loop<PRE == SG_PRECOND_LEARNED>(D, P, mat_g<PRE>(D), WantRun{},
-      [&](int t, int sys, long long r0, long long r1, const TileView& tv) {
-    const long long i = r0 + threadIdx.x;
-    double prs = 0.0;
-    if (i < r1) {
-      const double si = apply_row<PRE, SH>(D, tv, i, rn, eps);
-      D.s[i] = si;
-      prs = mul(rn[i], si);
-    }
-    if (arrive(D, P, t, sys, prs, 0.0)) {
-      const double rs = gather_partials(D, P, sys, 0);
-      if (threadIdx.x == 0) {
-        SysState& S = D.st[sys];
-        D.counter[sys] = 0;
-        const Ctl& c = *D.ctl;
-        const double delta_old = S.delta;
-        S.delta = rs;
-        if (rs < 0.0) {  // pcg.py:196-198
-          S.notspd = 1; S.fail_iter = S.i; S.fail_value = rs; S.fail_kind = 2;
-          finish(D, S, 0);
-          return;
-        }
-        S.beta = __ddiv_rn(rs, delta_old);
-        S.i += 1;
-        const double rel = __ddiv_rn(__dsqrt_rn(S.rr), S.norm_b);
-        put_hist(D, sys, S.i, rel);
-        S.hist_len = S.i + 1;
-        if (!c.delta_mode) {
-          if (rel <= c.rtol) {
-            if (refreshed) { finish(D, S, 1); return; }
-            S.flags |= FL_FRESH;
-          } else if (S.i >= S.max_iters) {
-            finish(D, S, 0);
-          }
-        } else if (S.i >= S.max_iters || rs <= S.rtol2d0) {
-          S.status = ST_CERTIFY;
-        }
-      }
-    }
-  });
+  if (PRE == SG_PRECOND_LEARNED) stage<FMT>(D, T, r0, r1, D.g_offs, D.g_cols, D.g_vals);
+  const unsigned int m = dmask(D, i, r1, FMT);
+  double prs = 0.0;
+  if (i < r1) {
+    const double si = apply_row<PRE, FMT, ND, SH>(D, T, i, r0, m, rn, D.ctl->eps);
+    D.s[i] = si;
+    prs = mul(rn[i], si);
+  }
+  if (arrive(D, sys, prs, 0.0, red, &flag)) {
+    const double rs = gather_partials(D, sys, 0, red);
+    if (threadIdx.x == 0) fin_k3(D, sys, rs, refreshed);
+  }
 }
 
 }  // namespace sg
@@ -544,7 +579,12 @@ struct sg_pcg {
   int chunk = 0;
   int64_t period = 0;
   int short_rows = 0;
-  unsigned grid = 0;  // persistent CTAs per kernel
+  // DIA format (0 = CSR)
+  int dia_nd = 0;
+  void* dia_mem = nullptr;
+  double* dia_g = nullptr;
+  double* dia_a = nullptr;
+  unsigned char* dia_mask = nullptr;
   // instrumentation: kernel launches, and (when profiling) event nodes around the kernels of
   // one non-refresh iteration per chunk -> per-kernel device time sampled inside the solve
   int64_t kernels = 0, chunks = 0;
@@ -567,67 +607,49 @@ int dispatch_pre(int pre, F f) {
   return SG_EINVAL;
 }
 
-// (preconditioner kind) x (SHORT: every row of A, G, G^T has <= 8 entries)
+// f(PRE, FMT, ND, SH) over the handle's configuration.
 template <class F>
 int dispatch(const sg_pcg* h, F f) {
+  using std::integral_constant;
   return dispatch_pre(h->pre, [&](auto P) -> int {
-    if (h->short_rows) return f(P, std::integral_constant<bool, true>());
-    return f(P, std::integral_constant<bool, false>());
-  });
-}
-
-constexpr size_t kSmem = sizeof(Pipe);
-
-// Opt every pipelined kernel of this (PRE, SH) into the dynamic shared memory it needs and
-// size the persistent grid from the occupancy of the heaviest one.
-int configure(sg_pcg* h) {
-  return dispatch(h, [&](auto P, auto SHc) -> int {
-    constexpr int PRE = decltype(P)::value;
-    constexpr bool SH = decltype(SHc)::value;
-    const void* fns[] = {(const void*)k_setup1<PRE, SH>, (const void*)k_setup2<PRE, SH>,
-                         (const void*)k_iter1<PRE, SH>, (const void*)k_iter2<PRE, SH>,
-                         (const void*)k_iter3<PRE, SH>, (const void*)k_refresh_r<SH>,
-                         (const void*)k_refresh_t<SH>};
-    int occ = 1 << 30;
-    for (const void* f : fns) {
-      SG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
-      int o = 0;
-      SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, f, PR, kSmem));
-      occ = o < occ ? o : occ;
+    switch (h->dia_nd) {
+      case 5: return f(P, integral_constant<int, 1>(), integral_constant<int, 5>(), integral_constant<bool, true>());
+      case 7: return f(P, integral_constant<int, 1>(), integral_constant<int, 7>(), integral_constant<bool, true>());
+      case 1: case 2: case 3: case 4: case 6: case 8:
+        return f(P, integral_constant<int, 1>(), integral_constant<int, 8>(), integral_constant<bool, true>());
+      default: break;
     }
-    int dev = 0, sms = 0;
-    SG_CUDA(cudaGetDevice(&dev));
-    SG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const long long g = (long long)sms * (occ > 0 ? occ : 1);
-    h->grid = (unsigned)(g < h->nblk ? g : h->nblk);
-    if (h->grid == 0) h->grid = 1;
-    return SG_OK;
+    if (h->short_rows)
+      return f(P, integral_constant<int, 0>(), integral_constant<int, 0>(), integral_constant<bool, true>());
+    return f(P, integral_constant<int, 0>(), integral_constant<int, 0>(), integral_constant<bool, false>());
   });
 }
 
 // Launches one iteration; returns the number of kernels launched through *nk.  With `ev`
 // (profiling), external event-record nodes bracket K1, K2 and K3.
 int launch_iteration(sg_pcg* h, cudaStream_t s, int par, bool refresh, cudaEvent_t* ev, int* nk) {
-  return dispatch(h, [&](auto P, auto SHc) -> int {
+  return dispatch(h, [&](auto P, auto Fc, auto Nc, auto SHc) -> int {
     constexpr int PRE = decltype(P)::value;
+    constexpr int FMT = decltype(Fc)::value;
+    constexpr int ND = decltype(Nc)::value;
     constexpr bool SH = decltype(SHc)::value;
-    const unsigned g = h->grid;
+    const unsigned g = (unsigned)h->nblk;
     int k = 0;
     if (ev) {
       k_snapshot<<<1, 1, 0, s>>>(h->ctl); ++k;
       SG_CUDA(cudaEventRecordWithFlags(ev[0], s, cudaEventRecordExternal));
     }
-    k_iter1<PRE, SH><<<g, PR, kSmem, s>>>(h->D, par); ++k;
+    k_iter1<PRE, FMT, ND, SH><<<g, PR, 0, s>>>(h->D, par); ++k;
     if (ev) SG_CUDA(cudaEventRecordWithFlags(ev[1], s, cudaEventRecordExternal));
     if (!refresh) {
-      k_iter2<PRE, SH><<<g, PR, kSmem, s>>>(h->D, par); ++k;
+      k_iter2<PRE, FMT, ND, SH><<<g, PR, 0, s>>>(h->D, par); ++k;
     } else {
       k_refresh_x<<<g, PR, 0, s>>>(h->D, par); ++k;
-      k_refresh_r<SH><<<g, PR, kSmem, s>>>(h->D, par); ++k;
-      if (PRE == SG_PRECOND_LEARNED) { k_refresh_t<SH><<<g, PR, kSmem, s>>>(h->D, par); ++k; }
+      k_refresh_r<FMT, ND, SH><<<g, PR, 0, s>>>(h->D, par); ++k;
+      if (PRE == SG_PRECOND_LEARNED) { k_refresh_t<FMT, ND, SH><<<g, PR, 0, s>>>(h->D, par); ++k; }
     }
     if (ev) SG_CUDA(cudaEventRecordWithFlags(ev[2], s, cudaEventRecordExternal));
-    k_iter3<PRE, SH><<<g, PR, kSmem, s>>>(h->D, par, refresh ? 1 : 0); ++k;
+    k_iter3<PRE, FMT, ND, SH><<<g, PR, 0, s>>>(h->D, par, refresh ? 1 : 0); ++k;
     if (ev) SG_CUDA(cudaEventRecordWithFlags(ev[3], s, cudaEventRecordExternal));
     SG_LAUNCH_CHECK("pcg iteration");
     *nk += k;
@@ -682,6 +704,83 @@ int ensure_hist(sg_pcg* h, long long need, cudaStream_t s) {
   tmp.hcap = cap;
   SG_CUDA(cudaMemcpyAsync(h->ctl, &tmp, sizeof(Ctl), cudaMemcpyHostToDevice, s));
   SG_CUDA(cudaStreamSynchronize(s));
+  return SG_OK;
+}
+
+// Decide the DIA format: A's pattern must have <= MAXD distinct diagonals forming a symmetric
+// set, G must share A's pattern (same arrays, or equal), and G^T's pattern must equal it.
+int same_pattern(const int32_t* ao, const int32_t* ac, const int32_t* bo, const int32_t* bc, int64_t n,
+                 bool* same, cudaStream_t s) {
+  *same = true;
+  if (ao == bo && ac == bc) return SG_OK;
+  int32_t nnz[2] = {0, 0};
+  SG_CUDA(cudaMemcpyAsync(&nnz[0], ao + n, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  SG_CUDA(cudaMemcpyAsync(&nnz[1], bo + n, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  SG_CUDA(cudaStreamSynchronize(s));
+  if (nnz[0] != nnz[1]) { *same = false; return SG_OK; }
+  unsigned int* flag = nullptr;
+  SG_CUDA(cudaMalloc(&flag, sizeof(unsigned int)));
+  SG_CUDA(cudaMemsetAsync(flag, 0, sizeof(unsigned int), s));
+  const int gb = 148 * 8;
+  k_differ<<<gb, 256, 0, s>>>(ao, bo, n + 1, flag);
+  k_differ<<<gb, 256, 0, s>>>(ac, bc, nnz[0], flag);
+  SG_LAUNCH_CHECK("k_differ");
+  unsigned int hf = 0;
+  SG_CUDA(cudaMemcpyAsync(&hf, flag, sizeof(hf), cudaMemcpyDeviceToHost, s));
+  SG_CUDA(cudaStreamSynchronize(s));
+  cudaFree(flag);
+  *same = hf == 0;
+  return SG_OK;
+}
+
+int setup_dia(sg_pcg* h, const int32_t* a_offs, const int32_t* a_cols, const int32_t* g_offs,
+              const int32_t* g_cols, const int32_t* gt_offs, const int32_t* gt_cols, cudaStream_t s) {
+  h->dia_nd = 0;
+  const int64_t n = h->n;
+  if (h->pre == SG_PRECOND_LEARNED) {  // G (and G^T) must sit on A's pattern
+    bool s1 = false, s2 = false;
+    int rc = same_pattern(a_offs, a_cols, g_offs, g_cols, n, &s1, s);
+    if (rc) return rc;
+    rc = same_pattern(a_offs, a_cols, gt_offs, gt_cols, n, &s2, s);
+    if (rc) return rc;
+    if (!s1 || !s2) return SG_OK;
+  }
+  int* scratch = nullptr;
+  SG_CUDA(cudaMalloc(&scratch, 32 * sizeof(int)));
+  std::vector<int> init(18, INT_MIN);
+  init[16] = 0;
+  init[17] = 0;
+  SG_CUDA(cudaMemcpyAsync(scratch, init.data(), 18 * sizeof(int), cudaMemcpyHostToDevice, s));
+  const int gb = (int)(n / 256 + 1 < 148 * 8 ? n / 256 + 1 : 148 * 8);
+  k_dia_offsets<<<gb, 256, 0, s>>>(a_offs, a_cols, n, scratch, scratch + 16, scratch + 17);
+  SG_LAUNCH_CHECK("k_dia_offsets");
+  std::vector<int> out(18);
+  SG_CUDA(cudaMemcpyAsync(out.data(), scratch, 18 * sizeof(int), cudaMemcpyDeviceToHost, s));
+  SG_CUDA(cudaStreamSynchronize(s));
+  cudaFree(scratch);
+  const int cnt = out[16];
+  if (out[17] || cnt < 1 || cnt > MAXD) return SG_OK;
+  std::vector<int> offs(out.begin(), out.begin() + cnt);
+  std::sort(offs.begin(), offs.end());
+  Dia dia{};
+  dia.nd = cnt;
+  dia.n = n;
+  for (int d = 0; d < cnt; ++d) {
+    dia.off[d] = offs[d];
+    auto it = std::find(offs.begin(), offs.end(), -offs[d]);
+    if (it == offs.end()) return SG_OK;  // offset set not symmetric
+    dia.mir[d] = (int)(it - offs.begin());
+  }
+  const size_t vbytes = (size_t)cnt * n * sizeof(double);
+  SG_CUDA(cudaMalloc(&h->dia_mem, 2 * vbytes + n + 64));
+  h->dia_a = reinterpret_cast<double*>(h->dia_mem);
+  h->dia_g = reinterpret_cast<double*>(reinterpret_cast<char*>(h->dia_mem) + vbytes);
+  h->dia_mask = reinterpret_cast<unsigned char*>(h->dia_mem) + 2 * vbytes;
+  dia.a = h->dia_a;
+  dia.g = h->dia_g;
+  dia.mask = h->dia_mask;
+  h->D.dia = dia;
+  h->dia_nd = cnt;
   return SG_OK;
 }
 
@@ -742,7 +841,6 @@ extern "C" int sg_pcg_create(sg_pcg** out, int32_t n_systems, const int64_t* sys
   SG_CUDA(cudaMemsetAsync(counter, 0, S * sizeof(unsigned int), s));
   Dev& D = h->D;
   D.blk_r0 = d_blk_r0; D.blk_sys = d_blk_sys; D.sys_blk0 = d_sys_blk0; D.sys_r1 = d_sys_r1;
-  D.nblk = h->nblk;
   D.a_offs = a_offs; D.a_cols = a_cols; D.a_vals = a_vals;
   D.g_offs = g_offs; D.g_cols = g_cols; D.g_vals = g_vals;
   D.gt_offs = gt_offs; D.gt_cols = gt_cols; D.gt_vals = gt_vals;
@@ -753,7 +851,7 @@ extern "C" int sg_pcg_create(sg_pcg** out, int32_t n_systems, const int64_t* sys
   SG_CUDA(cudaHostAlloc(&h->pinned_active, 2 * sizeof(unsigned int), cudaHostAllocDefault));
   SG_CUDA(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
   for (int k = 0; k < 4; ++k) SG_CUDA(cudaEventCreate(&h->ev[k]));
-  {  // longest row of every matrix the loop touches -> SHORT kernels when all are <= 8
+  {  // longest row of every matrix the loop touches -> SHORT CSR kernels when all are <= 8
     unsigned int* mx = counter;  // reuse (zeroed again below)
     SG_CUDA(cudaMemsetAsync(mx, 0, sizeof(unsigned int), s));
     const int gb = (int)(n / 256 + 1 < 148 * 8 ? n / 256 + 1 : 148 * 8);
@@ -769,7 +867,7 @@ extern "C" int sg_pcg_create(sg_pcg** out, int32_t n_systems, const int64_t* sys
     h->short_rows = hm <= 8 ? 1 : 0;
     SG_CUDA(cudaMemsetAsync(counter, 0, S * sizeof(unsigned int), s));
   }
-  int rc = configure(h);
+  int rc = setup_dia(h, a_offs, a_cols, g_offs, g_cols, gt_offs, gt_cols, s);
   if (rc) return rc;
   SG_CUDA(cudaStreamSynchronize(s));
   *out = h;
@@ -795,6 +893,16 @@ extern "C" int sg_pcg_solve(sg_pcg* h, const double* b, double* x, const sg_solv
     h->chunk = chunk;
     h->period = period;
   }
+  // DIA: (re)build the diagonal-major values from the CSR arrays (values may change between
+  // solves: a new G from the GNN, a refilled A)
+  if (h->dia_nd) {
+    const int gb = (int)(h->n / 256 + 1 < 148 * 16 ? h->n / 256 + 1 : 148 * 16);
+    k_csr_to_dia<<<gb, 256, 0, s>>>(h->D.a_offs, h->D.a_cols, h->D.a_vals, h->n, h->D.dia, h->dia_a, h->dia_mask);
+    if (h->pre == SG_PRECOND_LEARNED)
+      k_csr_to_dia<<<gb, 256, 0, s>>>(h->D.g_offs, h->D.g_cols, h->D.g_vals, h->n, h->D.dia, h->dia_g, nullptr);
+    SG_LAUNCH_CHECK("k_csr_to_dia");
+    h->kernels += h->pre == SG_PRECOND_LEARNED ? 2 : 1;
+  }
   // per-system state
   std::vector<SysState> st(h->S);
   for (int k = 0; k < h->S; ++k) {
@@ -817,12 +925,14 @@ extern "C" int sg_pcg_solve(sg_pcg* h, const double* b, double* x, const sg_solv
   SG_CUDA(cudaMemcpyAsync(h->ctl, &ctl, sizeof(Ctl), cudaMemcpyHostToDevice, s));
   if (h->n > 0) SG_CUDA(cudaMemcpyAsync(h->D.b, b, h->n * sizeof(double), cudaMemcpyDeviceToDevice, s));
   // setup
-  const unsigned g = h->grid;
-  rc = dispatch(h, [&](auto P, auto SHc) -> int {
+  const unsigned g = (unsigned)h->nblk;
+  rc = dispatch(h, [&](auto P, auto Fc, auto Nc, auto SHc) -> int {
     constexpr int PRE = decltype(P)::value;
+    constexpr int FMT = decltype(Fc)::value;
+    constexpr int ND = decltype(Nc)::value;
     constexpr bool SH = decltype(SHc)::value;
-    k_setup1<PRE, SH><<<g, PR, kSmem, s>>>(h->D);
-    k_setup2<PRE, SH><<<g, PR, kSmem, s>>>(h->D);
+    k_setup1<PRE, FMT, ND, SH><<<g, PR, 0, s>>>(h->D);
+    k_setup2<PRE, FMT, ND, SH><<<g, PR, 0, s>>>(h->D);
     SG_LAUNCH_CHECK("pcg setup");
     return SG_OK;
   });
@@ -911,6 +1021,7 @@ extern "C" int sg_pcg_stats(sg_pcg* h, int64_t* kernels_host, int64_t* chunks_ho
     for (int k = 0; k < 3; ++k) prof_host[k] = h->prof_ms[k];
     prof_host[3] = h->prof_active;
     prof_host[4] = h->prof_samples;
+    prof_host[5] = h->dia_nd;
   }
   if (reset) {
     h->kernels = h->chunks = 0;
@@ -929,6 +1040,7 @@ extern "C" void sg_pcg_destroy(sg_pcg* h) {
   if (h->pinned_active) cudaFreeHost(h->pinned_active);
   cudaDeviceSynchronize();
   if (h->hist) cudaFree(h->hist);
+  if (h->dia_mem) cudaFree(h->dia_mem);
   if (h->mem) cudaFree(h->mem);
   delete h;
 }
