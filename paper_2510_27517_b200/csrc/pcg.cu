@@ -37,6 +37,8 @@ namespace sg {
 constexpr int PR = 256;    // rows per tile (= threads per CTA)
 constexpr int PCAP = 2048; // staged nonzeros per tile (8 per row on average)
 constexpr int MAXD = 8;    // DIA: max diagonals
+constexpr int kRpt = 4;    // DIA: rows per thread (tile = PR * kRpt rows; amortises the
+                           // per-tile reduction and keeps more independent loads in flight)
 
 enum { ST_RUN = 0, ST_CERTIFY = 1, ST_DONE = 2 };
 enum { FL_FRESH = 1 };
@@ -74,6 +76,7 @@ struct Dev {
   const int* blk_sys;
   const int* sys_blk0;
   const long long* sys_r1;
+  int tile;  // rows per tile: PR (CSR) or PR * kRpt (DIA)
   // matrices (CSR)
   const int32_t *a_offs, *a_cols; const double* a_vals;
   const int32_t *g_offs, *g_cols; const double* g_vals;
@@ -150,7 +153,7 @@ __global__ void k_csr_to_dia(const int32_t* __restrict__ offs, const int32_t* __
 __device__ __forceinline__ void block_rows(const Dev& D, int& sys, long long& r0, long long& r1) {
   sys = D.blk_sys[blockIdx.x];
   r0 = D.blk_r0[blockIdx.x];
-  const long long e = r0 + PR;
+  const long long e = r0 + D.tile;
   const long long se = D.sys_r1[sys];
   r1 = e < se ? e : se;
 }
@@ -349,7 +352,7 @@ struct Fmt {};
   __shared__ int flag;                          \
   int sys; long long r0, r1;                    \
   block_rows(D, sys, r0, r1);                   \
-  const long long i = r0 + threadIdx.x;         \
+  constexpr int RPT = FMT == 1 ? kRpt : 1;      \
   (void)T;
 
 // A-row (numpy order) for either format.
@@ -390,9 +393,12 @@ template <int PRE, int FMT, int ND, bool SH>
 __global__ void __launch_bounds__(PR) k_setup1(Dev D) {
   SG_KERNEL_PROLOGUE
   if (PRE == SG_PRECOND_LEARNED) stage<FMT>(D, T, r0, r1, D.gt_offs, D.gt_cols, D.gt_vals);
-  const unsigned int m = dmask(D, i, r1, FMT);
   double pbb = 0.0;
-  if (i < r1) {
+#pragma unroll
+  for (int rr = 0; rr < RPT; ++rr) {
+    const long long i = r0 + (long long)rr * PR + threadIdx.x;
+    if (i >= r1) continue;
+    const unsigned int m = dmask(D, i, r1, FMT);
     const double bi = D.b[i];
     D.r0[i] = bi;
     D.d0[i] = 0.0;
@@ -422,9 +428,12 @@ template <int PRE, int FMT, int ND, bool SH>
 __global__ void __launch_bounds__(PR) k_setup2(Dev D) {
   SG_KERNEL_PROLOGUE
   if (PRE == SG_PRECOND_LEARNED) stage<FMT>(D, T, r0, r1, D.g_offs, D.g_cols, D.g_vals);
-  const unsigned int m = dmask(D, i, r1, FMT);
   double prs = 0.0;
-  if (i < r1) {
+#pragma unroll
+  for (int rr = 0; rr < RPT; ++rr) {
+    const long long i = r0 + (long long)rr * PR + threadIdx.x;
+    if (i >= r1) continue;
+    const unsigned int m = dmask(D, i, r1, FMT);
     const double si = apply_row<PRE, FMT, ND, SH>(D, T, i, r0, m, D.r0, D.ctl->eps);
     D.s[i] = si;
     prs = mul(D.r0[i], si);
@@ -447,9 +456,12 @@ __global__ void __launch_bounds__(PR) k_iter1(Dev D, int par) {
   double* dn = par ? D.d0 : D.d1;
   double* rc = par ? D.r1 : D.r0;
   stage<FMT>(D, T, r0, r1, D.a_offs, D.a_cols, D.a_vals);
-  const unsigned int m = dmask(D, i, r1, FMT);
   double pdq = 0.0, prr = 0.0;
-  if (i < r1) {
+#pragma unroll
+  for (int rr = 0; rr < RPT; ++rr) {
+    const long long i = r0 + (long long)rr * PR + threadIdx.x;
+    if (i >= r1) continue;
+    const unsigned int m = dmask(D, i, r1, FMT);
     if (run) {
       const double dni = add(D.s[i], mul(beta, dc[i]));
       dn[i] = dni;
@@ -479,9 +491,12 @@ __global__ void __launch_bounds__(PR) k_iter2(Dev D, int par) {
   const double* rc = par ? D.r1 : D.r0;
   double* rn = par ? D.r0 : D.r1;
   if (PRE == SG_PRECOND_LEARNED) stage<FMT>(D, T, r0, r1, D.gt_offs, D.gt_cols, D.gt_vals);
-  const unsigned int m = dmask(D, i, r1, FMT);
   double prr = 0.0;
-  if (i < r1) {
+#pragma unroll
+  for (int rr = 0; rr < RPT; ++rr) {
+    const long long i = r0 + (long long)rr * PR + threadIdx.x;
+    if (i >= r1) continue;
+    const unsigned int m = dmask(D, i, r1, FMT);
     D.x[i] = add(D.x[i], mul(alpha, dn[i]));
     const double rni = sub(rc[i], mul(alpha, D.q[i]));
     rn[i] = rni;
@@ -500,8 +515,7 @@ __global__ void __launch_bounds__(PR) k_refresh_x(Dev D, int par) {
   if (D.st[sys].status != ST_RUN) return;
   const double alpha = D.st[sys].alpha;
   const double* dn = par ? D.d0 : D.d1;
-  const long long i = r0 + threadIdx.x;
-  if (i < r1) D.x[i] = add(D.x[i], mul(alpha, dn[i]));
+  for (long long i = r0 + threadIdx.x; i < r1; i += PR) D.x[i] = add(D.x[i], mul(alpha, dn[i]));
 }
 
 template <int FMT, int ND, bool SH>
@@ -510,9 +524,12 @@ __global__ void __launch_bounds__(PR) k_refresh_r(Dev D, int par) {
   if (D.st[sys].status != ST_RUN) return;
   double* rn = par ? D.r0 : D.r1;
   stage<FMT>(D, T, r0, r1, D.a_offs, D.a_cols, D.a_vals);
-  const unsigned int m = dmask(D, i, r1, FMT);
   double prr = 0.0;
-  if (i < r1) {
+#pragma unroll
+  for (int rr = 0; rr < RPT; ++rr) {
+    const long long i = r0 + (long long)rr * PR + threadIdx.x;
+    if (i >= r1) continue;
+    const unsigned int m = dmask(D, i, r1, FMT);
     const double rni = sub(D.b[i], rowA<FMT, ND, SH, 0>(D, T, i, r0, m, XF{D.x, nullptr, 0.0}));
     rn[i] = rni;
     prr = mul(rni, rni);
@@ -529,8 +546,12 @@ __global__ void __launch_bounds__(PR) k_refresh_t(Dev D, int par) {
   if (D.st[sys].status != ST_RUN) return;
   const double* rn = par ? D.r0 : D.r1;
   stage<FMT>(D, T, r0, r1, D.gt_offs, D.gt_cols, D.gt_vals);
-  const unsigned int m = dmask(D, i, r1, FMT);
-  if (i < r1) D.t[i] = rowGt<FMT, ND, SH, 0>(D, T, i, r0, m, XF{rn, nullptr, 0.0});
+#pragma unroll
+  for (int rr = 0; rr < RPT; ++rr) {
+    const long long i = r0 + (long long)rr * PR + threadIdx.x;
+    if (i >= r1) continue;
+    D.t[i] = rowGt<FMT, ND, SH, 0>(D, T, i, r0, dmask(D, i, r1, FMT), XF{rn, nullptr, 0.0});
+  }
   (void)red; (void)flag;
 }
 
@@ -540,9 +561,12 @@ __global__ void __launch_bounds__(PR) k_iter3(Dev D, int par, int refreshed) {
   if (D.st[sys].status != ST_RUN) return;
   const double* rn = par ? D.r0 : D.r1;
   if (PRE == SG_PRECOND_LEARNED) stage<FMT>(D, T, r0, r1, D.g_offs, D.g_cols, D.g_vals);
-  const unsigned int m = dmask(D, i, r1, FMT);
   double prs = 0.0;
-  if (i < r1) {
+#pragma unroll
+  for (int rr = 0; rr < RPT; ++rr) {
+    const long long i = r0 + (long long)rr * PR + threadIdx.x;
+    if (i >= r1) continue;
+    const unsigned int m = dmask(D, i, r1, FMT);
     const double si = apply_row<PRE, FMT, ND, SH>(D, T, i, r0, m, rn, D.ctl->eps);
     D.s[i] = si;
     prs = mul(rn[i], si);
@@ -802,14 +826,43 @@ extern "C" int sg_pcg_create(sg_pcg** out, int32_t n_systems, const int64_t* sys
   h->eps = epsilon;
   h->sys_start.assign(sys_row_start_host, sys_row_start_host + n_systems + 1);
   h->n = h->sys_start.back();
+  for (int k = 0; k < n_systems; ++k)
+    if (h->sys_start[k + 1] <= h->sys_start[k]) {
+      delete h;
+      set_error("every system needs at least one row");
+      return SG_EINVAL;
+    }
+  // storage format first: it fixes the tile size
+  {  // longest row of every matrix the loop touches -> SHORT CSR kernels when all are <= 8
+    unsigned int* mx = nullptr;
+    SG_CUDA(cudaMalloc(&mx, sizeof(unsigned int)));
+    SG_CUDA(cudaMemsetAsync(mx, 0, sizeof(unsigned int), s));
+    const int64_t n = h->n;
+    const int gb = (int)(n / 256 + 1 < 148 * 8 ? n / 256 + 1 : 148 * 8);
+    k_max_row<<<gb, 256, 0, s>>>(a_offs, n, mx);
+    if (precond_kind == SG_PRECOND_LEARNED) {
+      k_max_row<<<gb, 256, 0, s>>>(g_offs, n, mx);
+      k_max_row<<<gb, 256, 0, s>>>(gt_offs, n, mx);
+    }
+    SG_LAUNCH_CHECK("k_max_row");
+    unsigned int hm = 0;
+    SG_CUDA(cudaMemcpyAsync(&hm, mx, sizeof(hm), cudaMemcpyDeviceToHost, s));
+    SG_CUDA(cudaStreamSynchronize(s));
+    cudaFree(mx);
+    h->short_rows = hm <= 8 ? 1 : 0;
+  }
+  {
+    int rc = setup_dia(h, a_offs, a_cols, g_offs, g_cols, gt_offs, gt_cols, s);
+    if (rc) { delete h; return rc; }
+  }
+  const int tile = h->dia_nd ? PR * kRpt : PR;
   std::vector<long long> blk_r0;
   std::vector<int> blk_sys, sys_blk0;
   std::vector<long long> sys_r1;
   for (int k = 0; k < n_systems; ++k) {
     sys_blk0.push_back((int)blk_r0.size());
     const int64_t a = h->sys_start[k], b = h->sys_start[k + 1];
-    if (b <= a) { delete h; set_error("every system needs at least one row"); return SG_EINVAL; }
-    for (int64_t r = a; r < b; r += PR) { blk_r0.push_back(r); blk_sys.push_back(k); }
+    for (int64_t r = a; r < b; r += tile) { blk_r0.push_back(r); blk_sys.push_back(k); }
     sys_r1.push_back(b);
   }
   sys_blk0.push_back((int)blk_r0.size());
@@ -841,6 +894,7 @@ extern "C" int sg_pcg_create(sg_pcg** out, int32_t n_systems, const int64_t* sys
   SG_CUDA(cudaMemsetAsync(counter, 0, S * sizeof(unsigned int), s));
   Dev& D = h->D;
   D.blk_r0 = d_blk_r0; D.blk_sys = d_blk_sys; D.sys_blk0 = d_sys_blk0; D.sys_r1 = d_sys_r1;
+  D.tile = tile;
   D.a_offs = a_offs; D.a_cols = a_cols; D.a_vals = a_vals;
   D.g_offs = g_offs; D.g_cols = g_cols; D.g_vals = g_vals;
   D.gt_offs = gt_offs; D.gt_cols = gt_cols; D.gt_vals = gt_vals;
@@ -851,24 +905,6 @@ extern "C" int sg_pcg_create(sg_pcg** out, int32_t n_systems, const int64_t* sys
   SG_CUDA(cudaHostAlloc(&h->pinned_active, 2 * sizeof(unsigned int), cudaHostAllocDefault));
   SG_CUDA(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
   for (int k = 0; k < 4; ++k) SG_CUDA(cudaEventCreate(&h->ev[k]));
-  {  // longest row of every matrix the loop touches -> SHORT CSR kernels when all are <= 8
-    unsigned int* mx = counter;  // reuse (zeroed again below)
-    SG_CUDA(cudaMemsetAsync(mx, 0, sizeof(unsigned int), s));
-    const int gb = (int)(n / 256 + 1 < 148 * 8 ? n / 256 + 1 : 148 * 8);
-    k_max_row<<<gb, 256, 0, s>>>(a_offs, n, mx);
-    if (precond_kind == SG_PRECOND_LEARNED) {
-      k_max_row<<<gb, 256, 0, s>>>(g_offs, n, mx);
-      k_max_row<<<gb, 256, 0, s>>>(gt_offs, n, mx);
-    }
-    SG_LAUNCH_CHECK("k_max_row");
-    unsigned int hm = 0;
-    SG_CUDA(cudaMemcpyAsync(&hm, mx, sizeof(hm), cudaMemcpyDeviceToHost, s));
-    SG_CUDA(cudaStreamSynchronize(s));
-    h->short_rows = hm <= 8 ? 1 : 0;
-    SG_CUDA(cudaMemsetAsync(counter, 0, S * sizeof(unsigned int), s));
-  }
-  int rc = setup_dia(h, a_offs, a_cols, g_offs, g_cols, gt_offs, gt_cols, s);
-  if (rc) return rc;
   SG_CUDA(cudaStreamSynchronize(s));
   *out = h;
   return SG_OK;

@@ -249,7 +249,11 @@ def test_pcg_golden_cases(g_pcg):
             # relative residuals start at 1; near convergence (1e-9) different dot orders differ
             # in their leading digits (the oracle with fsum dots shows the same), so compare with
             # an absolute tolerance on the relative residual
-            assert np.allclose(rep.residual_history, g[name + "_hist"], rtol=1e-6, atol=1e-8), name
+            # The random-factor cases are chaotic in their intermediate residuals: the oracle run
+            # with math.fsum dots (same k, x within 5e-10) already differs from the reference's
+            # OpenBLAS-dot history by 3e-3 at iteration 29 of learn_p3.
+            rt = 1e-2 if pre == "learn" else 1e-6
+            assert np.allclose(rep.residual_history, g[name + "_hist"], rtol=rt, atol=1e-8), name
 
 
 def test_pcg_c1_iteration_count(g_c1):
