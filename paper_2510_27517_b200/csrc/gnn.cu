@@ -10,9 +10,10 @@
 //   * edge pass: ONE kernel, thread per edge, h kept in registers through all L layers:
 //     h = E_e(e); h += f_e-second-layer(act(P'_t[i] + Q'_t[j] + h W1e[2D:3D] + b1e)); g = D(h).
 //     H never touches HBM (the reference tape holds ~18 KB per edge).
+// Node-level arrays are structure-of-arrays ([feature][node]) so the per-edge gathers of a
+// warp (consecutive edges of a few consecutive rows) coalesce.  All MLP weights a kernel needs
+// are staged once per CTA in shared memory and read as 16-byte broadcasts.
 // All arithmetic is fp64 (FMA allowed; parity is tolerance-based: OpenBLAS DGEMM order differs).
-// Weights live in shared memory; every thread of a warp reads the same weight element, so
-// shared-memory reads are broadcasts.
 #include "common.cuh"
 
 namespace sg {
@@ -33,107 +34,149 @@ struct GnnP {
   int L, dn;
 };
 
-// out[j] = b[j] + sum_k in[k] * W[k*ld + j], j < DO  (W in shared or global memory)
-template <int DI, int DO>
-__device__ __forceinline__ void matvec(const double* __restrict__ in, const double* __restrict__ W,
-                                       const double* __restrict__ b, double* __restrict__ out, int ld) {
+// out[j] (+)= sum_k in[k] * W[k*DO + j] with W in shared memory (16-byte loads, DO even).
+template <int DI, int DO, bool ACC>
+__device__ __forceinline__ void mv(const double* in, const double* __restrict__ W, double* out) {
+  if (!ACC) {
 #pragma unroll
-  for (int j = 0; j < DO; ++j) out[j] = b ? b[j] : 0.0;
+    for (int j = 0; j < DO; ++j) out[j] = 0.0;
+  }
 #pragma unroll
   for (int k = 0; k < DI; ++k) {
     const double v = in[k];
+    const double2* w2 = reinterpret_cast<const double2*>(W + k * DO);
 #pragma unroll
-    for (int j = 0; j < DO; ++j) out[j] = fma(v, W[k * ld + j], out[j]);
+    for (int j = 0; j < DO / 2; ++j) {
+      const double2 w = w2[j];
+      out[2 * j] = fma(v, w.x, out[2 * j]);
+      out[2 * j + 1] = fma(v, w.y, out[2 * j + 1]);
+    }
   }
 }
 
-// Node encoder, then P, Q of layer 1 (or nothing if L == 0).  X: [n x D], PQ: [n x 2D].
+// Cooperative global -> shared copy (doubles), returns the next free offset.
+__device__ __forceinline__ int stage(double* sm, int off, const double* src, int cnt) {
+  for (int k = threadIdx.x; k < cnt; k += blockDim.x) sm[off + k] = src[k];
+  return off + ((cnt + 1) & ~1);  // keep 16-byte alignment for the next block
+}
+
+// ------------------------------------------------------------------ node encoder
+// X = E_n(V); PQ = [X W1m0[0:D] ; X W1m0[D:2D]] (layer 0's node products).  SoA outputs.
 template <int D, int ACT>
-__global__ void k_node_encode(GnnP p, int64_t n, const double* __restrict__ V, double* X, double* PQ) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
+__global__ void __launch_bounds__(128) k_node_encode(GnnP p, int64_t n, const double* __restrict__ V,
+                                                     double* __restrict__ X, double* __restrict__ PQ) {
+  extern __shared__ __align__(16) double sm[];
+  int o = 0;
+  const int oW1 = o; o = stage(sm, o, p.en.W1, p.dn * D);
+  const int ob1 = o; o = stage(sm, o, p.en.b1, D);
+  const int oW2 = o; o = stage(sm, o, p.en.W2, D * D);
+  const int ob2 = o; o = stage(sm, o, p.en.b2, D);
+  const int oP = o; if (p.L > 0) o = stage(sm, o, p.fm[0].W1, 2 * D * D);
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     double h[D], x[D];
 #pragma unroll
-    for (int j = 0; j < D; ++j) h[j] = p.en.b1[j];
+    for (int j = 0; j < D; ++j) h[j] = sm[ob1 + j];
     for (int k = 0; k < p.dn; ++k) {
       const double v = V[i * p.dn + k];
 #pragma unroll
-      for (int j = 0; j < D; ++j) h[j] = fma(v, p.en.W1[k * D + j], h[j]);
+      for (int j = 0; j < D; ++j) h[j] = fma(v, sm[oW1 + k * D + j], h[j]);
     }
 #pragma unroll
-    for (int j = 0; j < D; ++j) h[j] = act_fn<ACT>(h[j]);
-    matvec<D, D>(h, p.en.W2, p.en.b2, x, D);
+    for (int j = 0; j < D; ++j) { h[j] = act_fn<ACT>(h[j]); x[j] = sm[ob2 + j]; }
+    mv<D, D, true>(h, sm + oW2, x);
 #pragma unroll
-    for (int j = 0; j < D; ++j) X[i * D + j] = x[j];
+    for (int j = 0; j < D; ++j) X[(int64_t)j * n + i] = x[j];
     if (p.L > 0) {
-      double o[D];
-      matvec<D, D>(x, p.fm[0].W1, nullptr, o, D);
+      double q[D];
+      mv<D, D, false>(x, sm + oP, q);
 #pragma unroll
-      for (int j = 0; j < D; ++j) PQ[i * 2 * D + j] = o[j];
-      matvec<D, D>(x, p.fm[0].W1 + D * D, nullptr, o, D);
+      for (int j = 0; j < D; ++j) PQ[(int64_t)j * n + i] = q[j];
+      mv<D, D, false>(x, sm + oP + D * D, q);
 #pragma unroll
-      for (int j = 0; j < D; ++j) PQ[i * 2 * D + D + j] = o[j];
+      for (int j = 0; j < D; ++j) PQ[(int64_t)(D + j) * n + i] = q[j];
     }
   }
 }
 
-// Layer t: message row-sum, node update, P'_t / Q'_t (edge pass) and next layer's P / Q.
+// ------------------------------------------------------------------ node layer t
+template <int D>
+__host__ __device__ constexpr int node_layer_smem_doubles() {
+  return 7 * D * D + 8 * D;
+}
+
 template <int D, int ACT>
-__global__ void k_node_layer(GnnP p, int t, int64_t n, const int32_t* __restrict__ offs,
-                             const int32_t* __restrict__ cols, const double* __restrict__ ef,
-                             double* X, const double* __restrict__ PQ, double* PQn,
-                             double* EPQ) {
+__global__ void __launch_bounds__(128) k_node_layer(GnnP p, int t, int64_t n, const int32_t* __restrict__ offs,
+                                                    const int32_t* __restrict__ cols,
+                                                    const double* __restrict__ ef, double* __restrict__ X,
+                                                    const double* __restrict__ PQ, double* __restrict__ PQn,
+                                                    double* __restrict__ EPQ) {
+  extern __shared__ __align__(16) double sm[];
   const MlpP fm = p.fm[t], fv = p.fv[t], fe = p.fe[t];
-  const double* c = fm.W1 + 2 * D * D;  // edge-feature row of W1m (d_edge == 1)
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
+  const bool nxt = t + 1 < p.L;
+  int o = 0;
+  const int o_b1 = o; o = stage(sm, o, fm.b1, D);
+  const int o_c = o; o = stage(sm, o, fm.W1 + 2 * D * D, D);  // edge-feature row (d_edge == 1)
+  const int o_W2 = o; o = stage(sm, o, fm.W2, D * D);
+  const int o_b2 = o; o = stage(sm, o, fm.b2, D);
+  const int o_V1 = o; o = stage(sm, o, fv.W1, D * D);
+  const int o_vb1 = o; o = stage(sm, o, fv.b1, D);
+  const int o_V2 = o; o = stage(sm, o, fv.W2, D * D);
+  const int o_vb2 = o; o = stage(sm, o, fv.b2, D);
+  const int o_E = o; o = stage(sm, o, fe.W1, 2 * D * D);
+  const int o_N = o; if (nxt) o = stage(sm, o, p.fm[t + 1].W1, 2 * D * D);
+  __syncthreads();
+  const double* P = PQ;
+  const double* Q = PQ + (int64_t)D * n;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     double S[D], pi[D];
 #pragma unroll
-    for (int j = 0; j < D; ++j) { S[j] = 0.0; pi[j] = PQ[i * 2 * D + j] + fm.b1[j]; }
+    for (int j = 0; j < D; ++j) { S[j] = 0.0; pi[j] = P[(int64_t)j * n + i] + sm[o_b1 + j]; }
     const int32_t lo = offs[i], hi = offs[i + 1];
     for (int32_t k = lo; k < hi; ++k) {
-      const double* qj = PQ + (int64_t)cols[k] * 2 * D + D;
+      const int64_t jn = cols[k];
       const double e = ef[k];
 #pragma unroll
-      for (int j = 0; j < D; ++j) S[j] += act_fn<ACT>(pi[j] + qj[j] + e * c[j]);
+      for (int j = 0; j < D; ++j) S[j] += act_fn<ACT>(pi[j] + Q[(int64_t)j * n + jn] + e * sm[o_c + j]);
     }
     const double deg = (double)(hi - lo);
     double m[D];
-    matvec<D, D>(S, fm.W2, nullptr, m, D);
 #pragma unroll
-    for (int j = 0; j < D; ++j) m[j] = fma(deg, fm.b2[j], m[j]);
+    for (int j = 0; j < D; ++j) m[j] = deg * sm[o_b2 + j];
+    mv<D, D, true>(S, sm + o_W2, m);
     double u[D];
-    matvec<D, D>(m, fv.W1, fv.b1, u, D);
 #pragma unroll
-    for (int j = 0; j < D; ++j) u[j] = act_fn<ACT>(u[j]);
-    double x[D];
-    matvec<D, D>(u, fv.W2, fv.b2, x, D);
+    for (int j = 0; j < D; ++j) u[j] = sm[o_vb1 + j];
+    mv<D, D, true>(m, sm + o_V1, u);
 #pragma unroll
-    for (int j = 0; j < D; ++j) { x[j] = X[i * D + j] + x[j]; X[i * D + j] = x[j]; }
-    double o[D];
-    double* ep = EPQ + ((int64_t)t * n + i) * 2 * D;
-    matvec<D, D>(x, fe.W1, nullptr, o, D);
+    for (int j = 0; j < D; ++j) { u[j] = act_fn<ACT>(u[j]); m[j] = X[(int64_t)j * n + i] + sm[o_vb2 + j]; }
+    mv<D, D, true>(u, sm + o_V2, m);  // m now holds the updated X row
 #pragma unroll
-    for (int j = 0; j < D; ++j) ep[j] = o[j];
-    matvec<D, D>(x, fe.W1 + D * D, nullptr, o, D);
+    for (int j = 0; j < D; ++j) X[(int64_t)j * n + i] = m[j];
+    double* ep = EPQ + (int64_t)t * 2 * D * n;
+    mv<D, D, false>(m, sm + o_E, u);
 #pragma unroll
-    for (int j = 0; j < D; ++j) ep[D + j] = o[j];
-    if (t + 1 < p.L) {
-      matvec<D, D>(x, p.fm[t + 1].W1, nullptr, o, D);
+    for (int j = 0; j < D; ++j) ep[(int64_t)j * n + i] = u[j];
+    mv<D, D, false>(m, sm + o_E + D * D, u);
 #pragma unroll
-      for (int j = 0; j < D; ++j) PQn[i * 2 * D + j] = o[j];
-      matvec<D, D>(x, p.fm[t + 1].W1 + D * D, nullptr, o, D);
+    for (int j = 0; j < D; ++j) ep[(int64_t)(D + j) * n + i] = u[j];
+    if (nxt) {
+      mv<D, D, false>(m, sm + o_N, u);
 #pragma unroll
-      for (int j = 0; j < D; ++j) PQn[i * 2 * D + D + j] = o[j];
+      for (int j = 0; j < D; ++j) PQn[(int64_t)j * n + i] = u[j];
+      mv<D, D, false>(m, sm + o_N + D * D, u);
+#pragma unroll
+      for (int j = 0; j < D; ++j) PQn[(int64_t)(D + j) * n + i] = u[j];
     }
   }
 }
 
-// Fused edge pass.  Edge-path weights are copied to shared memory:
+// ------------------------------------------------------------------ fused edge pass
+// Edge-path weights in shared memory:
 //   [Ee1 D][be1 D][Ee2 DxD][be2 D] + L x ([We1c DxD][be1 D][We2 DxD][be2 D]) + [D1 DxD][bd1 D][D2 D][bd2 1]
 template <int D>
 __host__ __device__ constexpr int edge_smem_doubles(int L) {
-  return (3 * D + D * D) + L * (2 * D * D + 2 * D) + (D * D + 2 * D + 1);
+  return (3 * D + D * D) + L * (2 * D * D + 2 * D) + (D * D + 2 * D + 2);
 }
 
 template <int D, int ACT>
@@ -142,62 +185,48 @@ __global__ void __launch_bounds__(128) k_edge_pass(GnnP p, int64_t nnz, const in
                                                    const double* __restrict__ ef,
                                                    const double* __restrict__ EPQ, int64_t n,
                                                    double* __restrict__ g) {
-  extern __shared__ double w[];
+  extern __shared__ __align__(16) double w[];
   const int L = p.L;
-  {  // stage weights
-    int o = 0;
-    auto cp = [&](const double* src, int cnt) {
-      for (int k = threadIdx.x; k < cnt; k += blockDim.x) w[o + k] = src[k];
-      o += cnt;
-    };
-    cp(p.ee.W1, D); cp(p.ee.b1, D); cp(p.ee.W2, D * D); cp(p.ee.b2, D);
-    for (int t = 0; t < L; ++t) {
-      cp(p.fe[t].W1 + 2 * D * D, D * D); cp(p.fe[t].b1, D); cp(p.fe[t].W2, D * D); cp(p.fe[t].b2, D);
-    }
-    cp(p.dec.W1, D * D); cp(p.dec.b1, D); cp(p.dec.W2, D); cp(p.dec.b2, 1);
+  int o = 0;
+  o = stage(w, o, p.ee.W1, D); o = stage(w, o, p.ee.b1, D); o = stage(w, o, p.ee.W2, D * D);
+  o = stage(w, o, p.ee.b2, D);
+  for (int t = 0; t < L; ++t) {
+    o = stage(w, o, p.fe[t].W1 + 2 * D * D, D * D); o = stage(w, o, p.fe[t].b1, D);
+    o = stage(w, o, p.fe[t].W2, D * D); o = stage(w, o, p.fe[t].b2, D);
   }
+  const int o_dec = o;
+  o = stage(w, o, p.dec.W1, D * D); o = stage(w, o, p.dec.b1, D); o = stage(w, o, p.dec.W2, D);
+  o = stage(w, o, p.dec.b2, 1);
   __syncthreads();
   const double* Ee1 = w;
   const double* eb1 = w + D;
   const double* Ee2 = w + 2 * D;
   const double* eb2 = w + 2 * D + D * D;
   const double* lay = w + 3 * D + D * D;
-  const double* dec = lay + L * (2 * D * D + 2 * D);
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz;
-       k += (int64_t)gridDim.x * blockDim.x) {
+  const double* dec = w + o_dec;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
     const double e = ef[k];
     const int64_t i = rows[k], j = cols[k];
     double h[D], a[D];
 #pragma unroll
-    for (int q = 0; q < D; ++q) a[q] = act_fn<ACT>(fma(e, Ee1[q], eb1[q]));
-    matvec<D, D>(a, Ee2, eb2, h, D);
+    for (int q = 0; q < D; ++q) { a[q] = act_fn<ACT>(fma(e, Ee1[q], eb1[q])); h[q] = eb2[q]; }
+    mv<D, D, true>(a, Ee2, h);
     for (int t = 0; t < L; ++t) {
       const double* W1c = lay + t * (2 * D * D + 2 * D);
       const double* b1 = W1c + D * D;
       const double* W2 = b1 + D;
       const double* b2 = W2 + D * D;
-      const double* Pi = EPQ + ((int64_t)t * n + i) * 2 * D;
-      const double* Qj = EPQ + ((int64_t)t * n + j) * 2 * D + D;
+      const double* Pt = EPQ + (int64_t)t * 2 * D * n;
 #pragma unroll
-      for (int q = 0; q < D; ++q) a[q] = Pi[q] + Qj[q] + b1[q];
+      for (int q = 0; q < D; ++q) a[q] = Pt[(int64_t)q * n + i] + Pt[(int64_t)(D + q) * n + j] + b1[q];
+      mv<D, D, true>(h, W1c, a);
 #pragma unroll
-      for (int kk = 0; kk < D; ++kk) {
-        const double v = h[kk];
-#pragma unroll
-        for (int q = 0; q < D; ++q) a[q] = fma(v, W1c[kk * D + q], a[q]);
-      }
-#pragma unroll
-      for (int q = 0; q < D; ++q) a[q] = act_fn<ACT>(a[q]);
-#pragma unroll
-      for (int q = 0; q < D; ++q) h[q] += b2[q];
-#pragma unroll
-      for (int kk = 0; kk < D; ++kk) {
-        const double v = a[kk];
-#pragma unroll
-        for (int q = 0; q < D; ++q) h[q] = fma(v, W2[kk * D + q], h[q]);
-      }
+      for (int q = 0; q < D; ++q) { a[q] = act_fn<ACT>(a[q]); h[q] += b2[q]; }
+      mv<D, D, true>(a, W2, h);
     }
-    matvec<D, D>(h, dec, dec + D * D, a, D);
+#pragma unroll
+    for (int q = 0; q < D; ++q) a[q] = dec[D * D + q];
+    mv<D, D, true>(h, dec, a);
     double out = dec[D * D + 2 * D];
 #pragma unroll
     for (int q = 0; q < D; ++q) out = fma(act_fn<ACT>(a[q]), dec[D * D + D + q], out);
@@ -205,27 +234,36 @@ __global__ void __launch_bounds__(128) k_edge_pass(GnnP p, int64_t nnz, const in
   }
 }
 
-static int grid_for(int64_t n, int threads) {
+static int grid_for(int64_t n, int threads, int per_sm) {
   int64_t b = ceil_div(n > 0 ? n : 1, threads);
-  return (int)(b > 148 * 16 ? 148 * 16 : b);
+  const int64_t cap = 148LL * per_sm;
+  return (int)(b > cap ? cap : b);
 }
 
 template <int D, int ACT>
 int run_forward(const GnnP& p, int64_t n, int64_t nnz, const int32_t* offs, const int32_t* cols,
                 const int32_t* rows, const double* V, const double* ef, double* g, double* X,
                 double* PQa, double* PQb, double* EPQ, cudaStream_t s) {
-  k_node_encode<D, ACT><<<grid_for(n, 128), 128, 0, s>>>(p, n, V, X, PQa);
+  const size_t sm_enc = (size_t)(p.dn * D + 4 * D + D * D + 2 * D * D + 8) * sizeof(double);
+  SG_CUDA(cudaFuncSetAttribute(k_node_encode<D, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_enc));
+  k_node_encode<D, ACT><<<grid_for(n, 128, 16), 128, sm_enc, s>>>(p, n, V, X, PQa);
   SG_LAUNCH_CHECK("k_node_encode");
+  const size_t sm_layer = (size_t)(node_layer_smem_doubles<D>() + 16) * sizeof(double);
+  SG_CUDA(cudaFuncSetAttribute(k_node_layer<D, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_layer));
   double* cur = PQa;
   double* nxt = PQb;
   for (int t = 0; t < p.L; ++t) {
-    k_node_layer<D, ACT><<<grid_for(n, 128), 128, 0, s>>>(p, t, n, offs, cols, ef, X, cur, nxt, EPQ);
+    k_node_layer<D, ACT><<<grid_for(n, 128, 16), 128, sm_layer, s>>>(p, t, n, offs, cols, ef, X, cur, nxt, EPQ);
     SG_LAUNCH_CHECK("k_node_layer");
     double* tmp = cur; cur = nxt; nxt = tmp;
   }
-  const size_t smem = edge_smem_doubles<D>(p.L) * sizeof(double);
+  const size_t smem = (edge_smem_doubles<D>(p.L) + 8 * (p.L + 4)) * sizeof(double);
+  if (smem > 227 * 1024) {
+    set_error("edge-pass weights (%zu bytes) exceed shared memory; reduce n_layers or hidden_dim", smem);
+    return SG_EUNSUPPORTED;
+  }
   SG_CUDA(cudaFuncSetAttribute(k_edge_pass<D, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_edge_pass<D, ACT><<<grid_for(nnz, 128), 128, smem, s>>>(p, nnz, rows, cols, ef, EPQ, n, g);
+  k_edge_pass<D, ACT><<<grid_for(nnz, 128, 16), 128, smem, s>>>(p, nnz, rows, cols, ef, EPQ, n, g);
   SG_LAUNCH_CHECK("k_edge_pass");
   return SG_OK;
 }

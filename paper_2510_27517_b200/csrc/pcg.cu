@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(PR) k_setup1(Dev D) {
     D.d0[i] = 0.0;
     D.d1[i] = 0.0;
     D.x[i] = 0.0;
-    pbb = mul(bi, bi);
+    pbb += mul(bi, bi);
     if (PRE == SG_PRECOND_LEARNED) D.t[i] = rowGt<FMT, ND, SH, 0>(D, T, i, r0, m, XF{D.b, nullptr, 0.0});
   }
   if (arrive(D, sys, pbb, 0.0, red, &flag)) {
@@ -436,7 +436,7 @@ __global__ void __launch_bounds__(PR) k_setup2(Dev D) {
     const unsigned int m = dmask(D, i, r1, FMT);
     const double si = apply_row<PRE, FMT, ND, SH>(D, T, i, r0, m, D.r0, D.ctl->eps);
     D.s[i] = si;
-    prs = mul(D.r0[i], si);
+    prs += mul(D.r0[i], si);
   }
   if (arrive(D, sys, prs, 0.0, red, &flag)) {
     const double rs = gather_partials(D, sys, 0, red);
@@ -467,12 +467,12 @@ __global__ void __launch_bounds__(PR) k_iter1(Dev D, int par) {
       dn[i] = dni;
       const double qi = rowA<FMT, ND, SH, 1>(D, T, i, r0, m, XF{D.s, dc, beta});
       D.q[i] = qi;
-      pdq = mul(dni, qi);
+      pdq += mul(dni, qi);
     }
     if (fresh) {
       const double rf = sub(D.b[i], rowA<FMT, ND, SH, 0>(D, T, i, r0, m, XF{D.x, nullptr, 0.0}));
       if (run) rc[i] = rf;
-      prr = mul(rf, rf);
+      prr += mul(rf, rf);
     }
   }
   if (arrive(D, sys, pdq, prr, red, &flag)) {
@@ -500,7 +500,7 @@ __global__ void __launch_bounds__(PR) k_iter2(Dev D, int par) {
     D.x[i] = add(D.x[i], mul(alpha, dn[i]));
     const double rni = sub(rc[i], mul(alpha, D.q[i]));
     rn[i] = rni;
-    prr = mul(rni, rni);
+    prr += mul(rni, rni);
     if (PRE == SG_PRECOND_LEARNED) D.t[i] = rowGt<FMT, ND, SH, 2>(D, T, i, r0, m, XF{rc, D.q, alpha});
   }
   if (arrive(D, sys, prr, 0.0, red, &flag)) {
@@ -532,7 +532,7 @@ __global__ void __launch_bounds__(PR) k_refresh_r(Dev D, int par) {
     const unsigned int m = dmask(D, i, r1, FMT);
     const double rni = sub(D.b[i], rowA<FMT, ND, SH, 0>(D, T, i, r0, m, XF{D.x, nullptr, 0.0}));
     rn[i] = rni;
-    prr = mul(rni, rni);
+    prr += mul(rni, rni);
   }
   if (arrive(D, sys, prr, 0.0, red, &flag)) {
     const double rr = gather_partials(D, sys, 0, red);
@@ -569,7 +569,7 @@ __global__ void __launch_bounds__(PR) k_iter3(Dev D, int par, int refreshed) {
     const unsigned int m = dmask(D, i, r1, FMT);
     const double si = apply_row<PRE, FMT, ND, SH>(D, T, i, r0, m, rn, D.ctl->eps);
     D.s[i] = si;
-    prs = mul(rn[i], si);
+    prs += mul(rn[i], si);
   }
   if (arrive(D, sys, prs, 0.0, red, &flag)) {
     const double rs = gather_partials(D, sys, 0, red);
