@@ -185,7 +185,9 @@ def run_ours(a, rank, world, local):
     ms = max_over_ranks(ms_local, dev)
     kernels, chunks, prof = solver.handle.stats(reset=True)
     L = model.config.n_layers
-    gpu_launches = a.steps * (3 * S + (2 + L) + 1) + kernels
+    # per step: batched norm (2) + batched features (1) + GNN (encode, L layers, edge pass) +
+    # G^T gather (1) + everything the PCG handle launched (DIA conversion, setup, graph nodes)
+    gpu_launches = a.steps * (3 + (2 + L) + 1) + kernels
     k_all, conv_all = gather_stats(ks[-1], [r.converged for r in res], dev)
 
     # ---- roofline of the PCG iteration kernels (sampled live by in-graph event nodes)

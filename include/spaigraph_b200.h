@@ -102,6 +102,23 @@ int sg_gen_poisson3d(int64_t nx, int64_t ny, int64_t nz, int32_t* offs, int32_t*
 int sg_matrix_norm(const double* vals, int64_t nnz, int kind, double* norm_out, void* ws,
                    size_t* ws_bytes, void* stream);
 
+/* sg_matrix_norm for n_seg independent value segments (one per system of a block-diagonal
+ * batch): seg_start (device, n_seg+1) delimits them; norms_out[k] per segment.  Same exact
+ * summation; one launch for the whole batch. */
+int sg_matrix_norm_batched(const double* vals, const int64_t* seg_start, int32_t n_seg,
+                           int64_t max_seg_len, int kind, double* norms_out, void* ws,
+                           size_t* ws_bytes, void* stream);
+
+/* build_graph features for every system of a block-diagonal batch in one launch: row_start
+ * (device, n_sys+1), norms (device, per system, sg_matrix_norm_batched), family as below, and
+ * for family 1 per-system grid sizes nx/ny (device int64), coeff aligned with rows (device) and
+ * per-system coeff_mean (device, numpy's pairwise mean of the host field). */
+int sg_graph_features_batched(const int64_t* row_start, int32_t n_sys, int64_t n, const int32_t* offs,
+                              const int32_t* cols, const double* vals, const double* norms, int family,
+                              const int64_t* nx, const int64_t* ny, const double* coeff,
+                              const double* coeff_mean, double* node_out, double* edge_out,
+                              void* stream);
+
 /* build_graph features (graphfeat.py:63-105) for the n rows row0..row0+n-1 of a (possibly
  * block-diagonal) matrix.  family 0: algebraic [rowsum/n/norm, diag/norm] (node_out rows of
  * 2); family 1: PDE [(ix+1)hx, (iy+1)hy, coeff/coeff_mean] (rows of 3; coeff is the system's

@@ -44,6 +44,9 @@ SIGNATURES = {
     "sg_gen_poisson2d": (C.c_int, [i64, i64, vp, i64, i64, vp, vp, vp, vp]),
     "sg_gen_poisson3d": (C.c_int, [i64, i64, i64, vp, vp, vp, vp]),
     "sg_matrix_norm": (C.c_int, [vp, i64, C.c_int, vp, vp, szp, vp]),
+    "sg_matrix_norm_batched": (C.c_int, [vp, vp, i32, i64, C.c_int, vp, vp, szp, vp]),
+    "sg_graph_features_batched": (C.c_int, [vp, i32, i64, vp, vp, vp, vp, C.c_int, vp, vp, vp, vp, vp,
+                                            vp, vp]),
     "sg_graph_features": (C.c_int, [i64, i64, vp, vp, vp, vp, C.c_int, i64, i64, vp, f64, vp, vp, vp]),
     "sg_gnn_forward": (C.c_int, [vp, i64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, i64, i64,
                                  vp, vp, vp, vp, vp, vp, vp, szp, vp]),

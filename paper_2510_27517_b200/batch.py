@@ -153,28 +153,43 @@ class BatchSolver:
         self.g = L.empty(a.nnz, torch.float64)  # G values; fixed buffer so the PCG handle is reused
         self.handle = None
 
-    def build_graph(self):
-        """Per-system exact norm + features (graphfeat.py:63-105) into the batch arrays."""
+    def _meta_device(self):
+        """Per-system metadata on device (row / nnz boundaries, grids, coefficient means)."""
         import torch
-        bt, a, lib = self.batch, self.batch.a, L.lib()
-        if self._norm_ws is None:
-            self._norm_ws = L.workspace(lib.sg_matrix_norm, None, int(np.max(np.diff(bt.nnz_start))), 0, None)
-        ws, wsb = self._norm_ws
-        sp = L.stream_ptr()
-        for k in range(bt.n_systems):
-            r0, r1 = int(bt.row_start[k]), int(bt.row_start[k + 1])
-            e0, e1 = int(bt.nnz_start[k]), int(bt.nnz_start[k + 1])
-            normk = C.c_void_p(self.norms.data_ptr() + 8 * k)
-            L.check(lib.sg_matrix_norm(C.c_void_p(a.vals.data_ptr() + 8 * e0), e1 - e0, 0, normk, L.ptr(ws),
-                                       C.byref(wsb), sp))
+        bt = self.batch
+        key = (id(bt), tuple(bt.coeff_mean or ()), tuple(bt.grids or ()))
+        if getattr(self, "_meta_key", None) != key:
+            self._row_start_d = L.to_device(bt.row_start, torch.int64)
+            self._nnz_start_d = L.to_device(bt.nnz_start, torch.int64)
             if bt.grids is not None:
-                nx, ny = bt.grids[k]
-                L.check(lib.sg_graph_features(r1 - r0, r0, L.ptr(a.offs), L.ptr(a.cols), L.ptr(a.vals), normk, 1,
-                                              nx, ny, C.c_void_p(bt.coeff.data_ptr() + 8 * r0), bt.coeff_mean[k],
-                                              L.ptr(self.node), L.ptr(self.edge), sp))
-            else:
-                L.check(lib.sg_graph_features(r1 - r0, r0, L.ptr(a.offs), L.ptr(a.cols), L.ptr(a.vals), normk, 0,
-                                              0, 0, None, 1.0, L.ptr(self.node), L.ptr(self.edge), sp))
+                self._nx_d = L.to_device(np.array([g[0] for g in bt.grids], dtype=np.int64), torch.int64)
+                self._ny_d = L.to_device(np.array([g[1] for g in bt.grids], dtype=np.int64), torch.int64)
+                self._cmean_d = L.to_device(np.asarray(bt.coeff_mean, dtype=np.float64), torch.float64)
+            self._meta_key = key
+        return self._row_start_d, self._nnz_start_d
+
+    def build_graph(self):
+        """Exact per-system norms + features (graphfeat.py:63-105) for the whole batch: two
+        launches (segmented exact sum, batched features), independent of the batch size."""
+        bt, a, lib = self.batch, self.batch.a, L.lib()
+        rs, ns = self._meta_device()
+        max_len = int(np.max(np.diff(bt.nnz_start)))
+        if self._norm_ws is None or self._norm_ws[2] != (bt.n_systems, max_len):
+            buf, nb = L.workspace(lib.sg_matrix_norm_batched, None, None, bt.n_systems, max_len, 0, None)
+            self._norm_ws = (buf, nb, (bt.n_systems, max_len))
+        ws, wsb, _ = self._norm_ws
+        sp = L.stream_ptr()
+        L.check(lib.sg_matrix_norm_batched(L.ptr(a.vals), L.ptr(ns), bt.n_systems, max_len, 0, L.ptr(self.norms),
+                                           L.ptr(ws), C.byref(wsb), sp))
+        if bt.grids is not None:
+            L.check(lib.sg_graph_features_batched(L.ptr(rs), bt.n_systems, a.n_rows, L.ptr(a.offs), L.ptr(a.cols),
+                                                  L.ptr(a.vals), L.ptr(self.norms), 1, L.ptr(self._nx_d),
+                                                  L.ptr(self._ny_d), L.ptr(bt.coeff), L.ptr(self._cmean_d),
+                                                  L.ptr(self.node), L.ptr(self.edge), sp))
+        else:
+            L.check(lib.sg_graph_features_batched(L.ptr(rs), bt.n_systems, a.n_rows, L.ptr(a.offs), L.ptr(a.cols),
+                                                  L.ptr(a.vals), L.ptr(self.norms), 0, None, None, None, None,
+                                                  L.ptr(self.node), L.ptr(self.edge), sp))
 
     def build_factor(self):
         """G = GNN(graph) on the union graph; explicit G^T values via the transpose permutation."""

@@ -10,13 +10,9 @@ namespace sg {
 
 constexpr int NLIMB = 72;  // 72*32 = 2304 bits >= 2098 value bits + carry headroom
 
-__device__ __forceinline__ void accum_add(unsigned long long* limbs, double a) {
-  unsigned long long bits = (unsigned long long)__double_as_longlong(a);
-  const int ex = (int)((bits >> 52) & 0x7FF);
-  unsigned long long m = bits & ((1ull << 52) - 1);
-  int g0 = 0;
-  if (ex) { m |= (1ull << 52); g0 = ex - 1; }
-  if (!m) return;
+// Add an integer mantissa sum `m` (< 2^63) whose least significant bit sits at fixed-point
+// position g0 (one limb = 32 bits).
+__device__ __forceinline__ void accum_add_int(unsigned long long* limbs, unsigned long long m, int g0) {
   const int L = g0 >> 5, s = g0 & 31;
   const unsigned long long lo = m << s;
   const unsigned long long hi = s ? (m >> (64 - s)) : 0ull;
@@ -25,25 +21,54 @@ __device__ __forceinline__ void accum_add(unsigned long long* limbs, double a) {
   if (hi) atomicAdd(&limbs[L + 2], hi);
 }
 
+// Segmented exact accumulation: blockIdx.y = segment (system), blockIdx.x strides over it.
+// Lanes holding values with the same binary exponent first sum their mantissas as integers
+// (__match_any_sync: <= 32 x 2^53 < 2^58, exact), so one shared-memory atomic triple is issued
+// per distinct exponent per warp instead of per value.
 // mode 0: |v|, mode 1: fl(v*v).  flags: bit0 inf, bit1 nan.
-__global__ void k_exact_accum(const double* __restrict__ v, int64_t n, int mode,
+__global__ void k_exact_accum(const double* __restrict__ v, const int64_t* __restrict__ seg, int mode,
                               unsigned long long* g_limbs, unsigned int* flags) {
   __shared__ unsigned long long sl[NLIMB];
   for (int i = threadIdx.x; i < NLIMB; i += blockDim.x) sl[i] = 0;
   __syncthreads();
+  const int sg = blockIdx.y;
+  const int64_t lo = seg[sg], hi = seg[sg + 1];
   unsigned int f = 0;
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
-       k += (int64_t)gridDim.x * blockDim.x) {
-    double x = v[k];
-    double a = mode == 1 ? mul(x, x) : fabs(x);
-    if (isnan(a)) { f |= 2; continue; }
-    if (isinf(a)) { f |= 1; continue; }
-    accum_add(sl, a);
+  const int lane = threadIdx.x & 31;
+  // warp-uniform trip count so that every lane takes part in __match_any_sync
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t base = lo + (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
+  for (int64_t kb = base; kb < hi; kb += stride) {
+    const int64_t k = kb + lane;
+    int key = -1;  // -1: no contribution
+    unsigned long long m = 0;
+    if (k < hi) {
+      const double x = v[k];
+      const double a = mode == 1 ? mul(x, x) : fabs(x);
+      if (isnan(a)) f |= 2;
+      else if (isinf(a)) f |= 1;
+      else {
+        const unsigned long long bits = (unsigned long long)__double_as_longlong(a);
+        const int ex = (int)((bits >> 52) & 0x7FF);
+        m = bits & ((1ull << 52) - 1);
+        if (ex) m |= (1ull << 52);
+        if (m) key = ex ? ex - 1 : 0;  // fixed-point position of the mantissa's lsb
+      }
+    }
+    const unsigned int peers = __match_any_sync(0xffffffffu, key);
+    // each lane sums the mantissas of its group (exact integer arithmetic, uniform shuffles)
+    unsigned long long gsum = 0;
+#pragma unroll 4
+    for (int src = 0; src < 32; ++src) {
+      const unsigned long long ms = __shfl_sync(0xffffffffu, m, src);
+      if ((peers >> src) & 1u) gsum += ms;
+    }
+    if (key >= 0 && lane == __ffs(peers) - 1) accum_add_int(sl, gsum, key);
   }
-  if (f) atomicOr(flags, f);
+  if (f) atomicOr(&flags[sg], f);
   __syncthreads();
   for (int i = threadIdx.x; i < NLIMB; i += blockDim.x)
-    if (sl[i]) atomicAdd(&g_limbs[i], sl[i]);
+    if (sl[i]) atomicAdd(&g_limbs[(int64_t)sg * NLIMB + i], sl[i]);
 }
 
 __device__ double round_limbs(const unsigned long long* in) {
@@ -84,16 +109,19 @@ __device__ double round_limbs(const unsigned long long* in) {
   return ldexp((double)mant, shift - 1074);
 }
 
+// One block per segment (thread 0 works): round the segment's limbs once, apply the kind.
 __global__ void k_norm_finish(const unsigned long long* limbs, const unsigned int* flags,
-                              int64_t nnz, int kind, double* out) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+                              const int64_t* __restrict__ seg, int kind, double* out) {
+  if (threadIdx.x != 0) return;
+  const int sg = blockIdx.x;
+  const int64_t nnz = seg[sg + 1] - seg[sg];
   double s;
-  if (*flags & 2) s = __longlong_as_double(0x7ff8000000000000ll);
-  else if (*flags & 1) s = __longlong_as_double(0x7ff0000000000000ll);
-  else s = round_limbs(limbs);
+  if (flags[sg] & 2) s = __longlong_as_double(0x7ff8000000000000ll);
+  else if (flags[sg] & 1) s = __longlong_as_double(0x7ff0000000000000ll);
+  else s = round_limbs(limbs + (int64_t)sg * NLIMB);
   if (kind == 0) s = __ddiv_rn(s, (double)nnz);
   else if (kind == 1) s = __dsqrt_rn(s);
-  *out = s;
+  out[sg] = s;
 }
 
 // graphfeat.py:83 and 93-104, for global rows row0 .. row0+n-1 (local index li = i - row0).
@@ -120,6 +148,42 @@ __global__ void k_graph_features(int64_t n, int64_t row0, const int32_t* __restr
       for (int32_t k = lo; k < hi; ++k)
         if (cols[k] == (int32_t)i) dg = vals[k];
       node_out[2 * i + 0] = __ddiv_rn(__ddiv_rn(rs, (double)n), norm);
+      node_out[2 * i + 1] = __ddiv_rn(dg, norm);
+    }
+  }
+}
+
+// Batched features: every row of a block-diagonal batch, system found by binary search.
+__global__ void k_graph_features_batched(const int64_t* __restrict__ row_start, int n_sys, int64_t n,
+                                         const int32_t* __restrict__ offs, const int32_t* __restrict__ cols,
+                                         const double* __restrict__ vals, const double* __restrict__ norms,
+                                         int family, const int64_t* __restrict__ nx_arr,
+                                         const int64_t* __restrict__ ny_arr, const double* __restrict__ coeff,
+                                         const double* __restrict__ coeff_mean, double* node_out,
+                                         double* edge_out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int lo = 0, hi = n_sys;  // largest sg with row_start[sg] <= i
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (row_start[mid] <= i) lo = mid; else hi = mid;
+    }
+    const int sg = lo;
+    const int64_t r0 = row_start[sg], ns = row_start[sg + 1] - r0, li = i - r0;
+    const double norm = norms[sg];
+    const int32_t e0 = offs[i], e1 = offs[i + 1];
+    for (int32_t k = e0; k < e1; ++k) edge_out[k] = __ddiv_rn(vals[k], norm);
+    if (family == 1) {
+      const int64_t nx = nx_arr[sg], ny = ny_arr[sg];
+      const double hx = __ddiv_rn(1.0, (double)(nx + 1)), hy = __ddiv_rn(1.0, (double)(ny + 1));
+      node_out[3 * i + 0] = mul((double)(li % nx + 1), hx);
+      node_out[3 * i + 1] = mul((double)(li / nx + 1), hy);
+      node_out[3 * i + 2] = __ddiv_rn(coeff[i], coeff_mean[sg]);
+    } else {
+      const double rs = reduceat_sum([&](int64_t k) { return vals[k]; }, e0, e1);
+      double dg = 0.0;
+      for (int32_t k = e0; k < e1; ++k)
+        if (cols[k] == (int32_t)i) dg = vals[k];
+      node_out[2 * i + 0] = __ddiv_rn(__ddiv_rn(rs, (double)ns), norm);
       node_out[2 * i + 1] = __ddiv_rn(dg, norm);
     }
   }
@@ -203,22 +267,44 @@ static inline int grid_for(int64_t n, int threads = 256) {
 
 using namespace sg;
 
+static int norm_segments(const double* vals, const int64_t* seg_dev, int32_t n_seg, int64_t max_len, int kind,
+                         double* out, unsigned long long* limbs, unsigned int* flags, cudaStream_t s) {
+  if (kind < 0 || kind > 2) { set_error("unknown norm kind"); return SG_EINVAL; }
+  SG_CUDA(cudaMemsetAsync(limbs, 0, (size_t)n_seg * NLIMB * sizeof(unsigned long long), s));
+  SG_CUDA(cudaMemsetAsync(flags, 0, (size_t)n_seg * sizeof(unsigned int), s));
+  int bx = (int)ceil_div(max_len > 0 ? max_len : 1, 256);
+  const int cap = (int)ceil_div(148 * 16, n_seg);
+  if (bx > cap) bx = cap < 1 ? 1 : cap;
+  k_exact_accum<<<dim3(bx, n_seg), 256, 0, s>>>(vals, seg_dev, kind == 1 ? 1 : 0, limbs, flags);
+  SG_LAUNCH_CHECK("k_exact_accum");
+  k_norm_finish<<<n_seg, 32, 0, s>>>(limbs, flags, seg_dev, kind, out);
+  SG_LAUNCH_CHECK("k_norm_finish");
+  return SG_OK;
+}
+
 extern "C" int sg_matrix_norm(const double* vals, int64_t nnz, int kind, double* norm_out,
                               void* ws, size_t* ws_bytes, void* stream) {
   Carve c(ws);
   unsigned long long* limbs = c.take<unsigned long long>(NLIMB);
   unsigned int* flags = c.take<unsigned int>(1);
+  int64_t* seg = c.take<int64_t>(2);
   if (!ws) { *ws_bytes = c.off; return SG_OK; }
   if (nnz <= 0) { set_error("norm of a matrix with no stored entries"); return SG_EINVAL; }
-  if (kind < 0 || kind > 2) { set_error("unknown norm kind"); return SG_EINVAL; }
   cudaStream_t s = as_stream(stream);
-  SG_CUDA(cudaMemsetAsync(limbs, 0, NLIMB * sizeof(unsigned long long), s));
-  SG_CUDA(cudaMemsetAsync(flags, 0, sizeof(unsigned int), s));
-  k_exact_accum<<<grid_for(nnz), 256, 0, s>>>(vals, nnz, kind == 1 ? 1 : 0, limbs, flags);
-  SG_LAUNCH_CHECK("k_exact_accum");
-  k_norm_finish<<<1, 32, 0, s>>>(limbs, flags, nnz, kind, norm_out);
-  SG_LAUNCH_CHECK("k_norm_finish");
-  return SG_OK;
+  const int64_t h[2] = {0, nnz};
+  SG_CUDA(cudaMemcpyAsync(seg, h, sizeof(h), cudaMemcpyHostToDevice, s));
+  return norm_segments(vals, seg, 1, nnz, kind, norm_out, limbs, flags, s);
+}
+
+extern "C" int sg_matrix_norm_batched(const double* vals, const int64_t* seg_start, int32_t n_seg,
+                                      int64_t max_seg_len, int kind, double* norms_out, void* ws,
+                                      size_t* ws_bytes, void* stream) {
+  Carve c(ws);
+  unsigned long long* limbs = c.take<unsigned long long>((size_t)(n_seg > 0 ? n_seg : 1) * NLIMB);
+  unsigned int* flags = c.take<unsigned int>(n_seg > 0 ? n_seg : 1);
+  if (!ws) { *ws_bytes = c.off; return SG_OK; }
+  if (n_seg <= 0) return SG_OK;
+  return norm_segments(vals, seg_start, n_seg, max_seg_len, kind, norms_out, limbs, flags, as_stream(stream));
 }
 
 extern "C" int sg_graph_features(int64_t n, int64_t row0, const int32_t* offs, const int32_t* cols,
@@ -231,6 +317,19 @@ extern "C" int sg_graph_features(int64_t n, int64_t row0, const int32_t* offs, c
                                                                nx, ny, coeff, coeff_mean,
                                                                node_out, edge_out);
   SG_LAUNCH_CHECK("k_graph_features");
+  return SG_OK;
+}
+
+extern "C" int sg_graph_features_batched(const int64_t* row_start, int32_t n_sys, int64_t n, const int32_t* offs,
+                                         const int32_t* cols, const double* vals, const double* norms, int family,
+                                         const int64_t* nx, const int64_t* ny, const double* coeff,
+                                         const double* coeff_mean, double* node_out, double* edge_out,
+                                         void* stream) {
+  if (n <= 0 || n_sys <= 0) return SG_OK;
+  k_graph_features_batched<<<grid_for(n), 256, 0, as_stream(stream)>>>(row_start, n_sys, n, offs, cols, vals, norms,
+                                                                      family, nx, ny, coeff, coeff_mean, node_out,
+                                                                      edge_out);
+  SG_LAUNCH_CHECK("k_graph_features_batched");
   return SG_OK;
 }
 

@@ -390,7 +390,7 @@ __device__ __forceinline__ unsigned int dmask(const Dev& D, long long i, long lo
 
 // r = b; d = 0; x = 0; t = G^T b; partial ||b||^2
 template <int PRE, int FMT, int ND, bool SH>
-__global__ void __launch_bounds__(PR) k_setup1(Dev D) {
+__global__ void __launch_bounds__(PR, FMT == 1 ? 8 : 1) k_setup1(Dev D) {
   SG_KERNEL_PROLOGUE
   if (PRE == SG_PRECOND_LEARNED) stage<FMT>(D, T, r0, r1, D.gt_offs, D.gt_cols, D.gt_vals);
   double pbb = 0.0;
@@ -425,7 +425,7 @@ __device__ __forceinline__ double apply_row(const Dev& D, const RowTile<PR, (FMT
 
 // s = M r0; delta0 = r.s; NotSpd check; top-of-loop checks for i = 0.
 template <int PRE, int FMT, int ND, bool SH>
-__global__ void __launch_bounds__(PR) k_setup2(Dev D) {
+__global__ void __launch_bounds__(PR, FMT == 1 ? 8 : 1) k_setup2(Dev D) {
   SG_KERNEL_PROLOGUE
   if (PRE == SG_PRECOND_LEARNED) stage<FMT>(D, T, r0, r1, D.g_offs, D.g_cols, D.g_vals);
   double prs = 0.0;
@@ -445,7 +445,7 @@ __global__ void __launch_bounds__(PR) k_setup2(Dev D) {
 }
 
 template <int PRE, int FMT, int ND, bool SH>
-__global__ void __launch_bounds__(PR) k_iter1(Dev D, int par) {
+__global__ void __launch_bounds__(PR, FMT == 1 ? 8 : 1) k_iter1(Dev D, int par) {
   SG_KERNEL_PROLOGUE
   const int status = D.st[sys].status;
   if (status == ST_DONE) return;
@@ -483,7 +483,7 @@ __global__ void __launch_bounds__(PR) k_iter1(Dev D, int par) {
 }
 
 template <int PRE, int FMT, int ND, bool SH>
-__global__ void __launch_bounds__(PR) k_iter2(Dev D, int par) {
+__global__ void __launch_bounds__(PR, FMT == 1 ? 8 : 1) k_iter2(Dev D, int par) {
   SG_KERNEL_PROLOGUE
   if (D.st[sys].status != ST_RUN) return;
   const double alpha = D.st[sys].alpha;
@@ -519,7 +519,7 @@ __global__ void __launch_bounds__(PR) k_refresh_x(Dev D, int par) {
 }
 
 template <int FMT, int ND, bool SH>
-__global__ void __launch_bounds__(PR) k_refresh_r(Dev D, int par) {
+__global__ void __launch_bounds__(PR, FMT == 1 ? 8 : 1) k_refresh_r(Dev D, int par) {
   SG_KERNEL_PROLOGUE
   if (D.st[sys].status != ST_RUN) return;
   double* rn = par ? D.r0 : D.r1;
@@ -541,7 +541,7 @@ __global__ void __launch_bounds__(PR) k_refresh_r(Dev D, int par) {
 }
 
 template <int FMT, int ND, bool SH>
-__global__ void __launch_bounds__(PR) k_refresh_t(Dev D, int par) {
+__global__ void __launch_bounds__(PR, FMT == 1 ? 8 : 1) k_refresh_t(Dev D, int par) {
   SG_KERNEL_PROLOGUE
   if (D.st[sys].status != ST_RUN) return;
   const double* rn = par ? D.r0 : D.r1;
@@ -556,7 +556,7 @@ __global__ void __launch_bounds__(PR) k_refresh_t(Dev D, int par) {
 }
 
 template <int PRE, int FMT, int ND, bool SH>
-__global__ void __launch_bounds__(PR) k_iter3(Dev D, int par, int refreshed) {
+__global__ void __launch_bounds__(PR, FMT == 1 ? 8 : 1) k_iter3(Dev D, int par, int refreshed) {
   SG_KERNEL_PROLOGUE
   if (D.st[sys].status != ST_RUN) return;
   const double* rn = par ? D.r0 : D.r1;
