@@ -1,19 +1,26 @@
-// GNN forward (gnn.py:208-253) restructured for the GPU.
+// GNN forward (gnn.py:208-253) restructured for the GPU, on FP64 tensor
+// cores.
 //
 // With message_uses_hidden_edge = False the node path never reads the edge state H, and the
 // first layer of every MLP on a concatenation is linear.  So
 //   * node path, per layer t: P = X W1m[0:D], Q = X W1m[D:2D] are node-level products; the
 //     message MLP's hidden activations are summed per CSR row, act(P_i + Q_j + e_k c + b1),
 //     and its (linear) second layer is applied AFTER the row sum: m = S W2m + deg b2m;
-//     X += f_v(m).  One kernel per layer, thread per row, fused with the node-level products
-//     the next stages need (P'_t, Q'_t for the edge pass; P, Q for layer t+1).
-//   * edge pass: ONE kernel, thread per edge, h kept in registers through all L layers:
+//     X += f_v(m).  One kernel per layer, fused with the node-level products the next stages
+//     need (P'_t, Q'_t for the edge pass; P, Q for layer t+1).
+//   * edge pass: ONE kernel; h stays in registers through all L layers:
 //     h = E_e(e); h += f_e-second-layer(act(P'_t[i] + Q'_t[j] + h W1e[2D:3D] + b1e)); g = D(h).
 //     H never touches HBM (the reference tape holds ~18 KB per edge).
-// Node-level arrays are structure-of-arrays ([feature][node]) so the per-edge gathers of a
-// warp (consecutive edges of a few consecutive rows) coalesce.  All MLP weights a kernel needs
-// are staged once per CTA in shared memory and read as 16-byte broadcasts.
-// All arithmetic is fp64 (FMA allowed; parity is tolerance-based: OpenBLAS DGEMM order differs).
+//
+// Every [rows x D] . [D x D] product runs on the FP64 tensor cores (mma.sync.m8n8k4.f64, DMMA):
+// a warp owns 8 rows (8 edges or 8 nodes); lane (r = lane/4, c = lane%4) holds the features
+// f = 8*nb + 2*c + s (nb < D/8, s < 2) of row r — exactly the accumulator layout of the MMA.
+// Feeding an accumulator back as the next A operand only needs the k dimension permuted, which
+// is folded into the weights: the B fragments are pre-arranged in shared memory so that k-step
+// kb pairs with the lane's held value v[kb].  Activations, biases and residuals are
+// elementwise in that layout, so consecutive matvecs never shuffle data between lanes.
+// Node-level arrays are row-major [node][DP] (DP = D padded to 8), so the 4 lanes of a row read
+// 64 contiguous bytes per n-tile.  fp64 throughout (parity is tolerance-based).
 #include "common.cuh"
 
 namespace sg {
@@ -34,67 +41,128 @@ struct GnnP {
   int L, dn;
 };
 
-// out[j] (+)= sum_k in[k] * W[k*DO + j] with W in shared memory (16-byte loads, DO even).
-template <int DI, int DO, bool ACC>
-__device__ __forceinline__ void mv(const double* in, const double* __restrict__ W, double* out) {
-  if (!ACC) {
-#pragma unroll
-    for (int j = 0; j < DO; ++j) out[j] = 0.0;
-  }
-#pragma unroll
-  for (int k = 0; k < DI; ++k) {
-    const double v = in[k];
-    const double2* w2 = reinterpret_cast<const double2*>(W + k * DO);
-#pragma unroll
-    for (int j = 0; j < DO / 2; ++j) {
-      const double2 w = w2[j];
-      out[2 * j] = fma(v, w.x, out[2 * j]);
-      out[2 * j + 1] = fma(v, w.y, out[2 * j + 1]);
-    }
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <int D>
+struct Shape {
+  static constexpr int DP = (D + 7) / 8 * 8;  // padded width
+  static constexpr int NB = DP / 8;           // n-tiles (8 outputs each)
+  static constexpr int KS = DP / 4;           // k-steps (4 inputs each) == values held per lane
+  static constexpr int FRAG = KS * NB * 32;   // doubles per weight matrix in fragment layout
+};
+
+// Feature held by lane-column c at value index v (v = 2*nb + s).
+__device__ __forceinline__ int feat(int v, int c) { return 8 * (v >> 1) + 2 * c + (v & 1); }
+
+// Stage W (rows row0.. of a row-major [rows x D] matrix, D_in = D used rows) into fragment
+// layout: frag[(kb*NB + nb)*32 + lane] = W[row0 + feat(kb, lane%4)][8*nb + lane/4] (0 if padded).
+template <int D>
+__device__ void stage_frag(double* dst, const double* __restrict__ W, int row0) {
+  using S = Shape<D>;
+  for (int idx = threadIdx.x; idx < S::FRAG; idx += blockDim.x) {
+    const int ln = idx & 31, kbnb = idx >> 5;
+    const int kb = kbnb / S::NB, nb = kbnb % S::NB;
+    const int k = feat(kb, ln & 3), nn = 8 * nb + (ln >> 2);
+    dst[idx] = (k < D && nn < D) ? W[(int64_t)(row0 + k) * D + nn] : 0.0;
   }
 }
 
-// Cooperative global -> shared copy (doubles), returns the next free offset.
-__device__ __forceinline__ int stage(double* sm, int off, const double* src, int cnt) {
-  for (int k = threadIdx.x; k < cnt; k += blockDim.x) sm[off + k] = src[k];
-  return off + ((cnt + 1) & ~1);  // keep 16-byte alignment for the next block
+// Padded vector (bias / single weight row) into shared memory.
+template <int D>
+__device__ void stage_vec(double* dst, const double* __restrict__ v) {
+  for (int f = threadIdx.x; f < Shape<D>::DP; f += blockDim.x) dst[f] = f < D ? v[f] : 0.0;
+}
+
+// out (accumulator layout) += in (accumulator layout) . W (fragment layout in shared memory)
+template <int D>
+__device__ __forceinline__ void mv(const double* in, const double* __restrict__ Wf, double* out, int lane) {
+  using S = Shape<D>;
+#pragma unroll
+  for (int nb = 0; nb < S::NB; ++nb) {
+    double d0 = out[2 * nb], d1 = out[2 * nb + 1];
+#pragma unroll
+    for (int kb = 0; kb < S::KS; ++kb) dmma(d0, d1, in[kb], Wf[(kb * S::NB + nb) * 32 + lane]);
+    out[2 * nb] = d0;
+    out[2 * nb + 1] = d1;
+  }
+}
+
+// Row-major padded row access for the lane's values: row[v] for v = 2nb + s -> row + feat.
+__device__ __forceinline__ void load_row(double* v, const double* __restrict__ row, int c, int KS) {
+  for (int nb = 0; nb < KS / 2; ++nb) {
+    const double2 p = *reinterpret_cast<const double2*>(row + 8 * nb + 2 * c);
+    v[2 * nb] = p.x;
+    v[2 * nb + 1] = p.y;
+  }
 }
 
 // ------------------------------------------------------------------ node encoder
-// X = E_n(V); PQ = [X W1m0[0:D] ; X W1m0[D:2D]] (layer 0's node products).  SoA outputs.
+// X = E_n(V); PQ = [X W1m0[0:D] | X W1m0[D:2D]] (layer 0's node products), rows padded to DP.
 template <int D, int ACT>
 __global__ void __launch_bounds__(128) k_node_encode(GnnP p, int64_t n, const double* __restrict__ V,
                                                      double* __restrict__ X, double* __restrict__ PQ) {
+  using S = Shape<D>;
+  constexpr int DP = S::DP, KS = S::KS;
   extern __shared__ __align__(16) double sm[];
-  int o = 0;
-  const int oW1 = o; o = stage(sm, o, p.en.W1, p.dn * D);
-  const int ob1 = o; o = stage(sm, o, p.en.b1, D);
-  const int oW2 = o; o = stage(sm, o, p.en.W2, D * D);
-  const int ob2 = o; o = stage(sm, o, p.en.b2, D);
-  const int oP = o; if (p.L > 0) o = stage(sm, o, p.fm[0].W1, 2 * D * D);
+  double* W1 = sm;                     // [4][DP] rows of E_n's first layer (d_node <= 4)
+  double* b1 = W1 + 4 * DP;
+  double* b2 = b1 + DP;
+  double* F2 = b2 + DP;                // E_n second layer
+  double* FP = F2 + S::FRAG;           // layer-0 P weights
+  double* FQ = FP + S::FRAG;           // layer-0 Q weights
+  for (int k = 0; k < 4; ++k)
+    for (int f = threadIdx.x; f < DP; f += blockDim.x)
+      W1[k * DP + f] = (k < p.dn && f < D) ? p.en.W1[k * D + f] : 0.0;
+  stage_vec<D>(b1, p.en.b1);
+  stage_vec<D>(b2, p.en.b2);
+  stage_frag<D>(F2, p.en.W2, 0);
+  if (p.L > 0) {
+    stage_frag<D>(FP, p.fm[0].W1, 0);
+    stage_frag<D>(FQ, p.fm[0].W1, D);
+  }
   __syncthreads();
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    double h[D], x[D];
+  const int lane = threadIdx.x & 31, r = lane >> 2, c = lane & 3;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
+  for (int64_t base = (int64_t)(blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5)) * 8; base < n; base += warps * 8) {
+    const int64_t i = base + r;
+    const bool ok = i < n;
+    double h[KS], x[KS];
 #pragma unroll
-    for (int j = 0; j < D; ++j) h[j] = sm[ob1 + j];
-    for (int k = 0; k < p.dn; ++k) {
-      const double v = V[i * p.dn + k];
-#pragma unroll
-      for (int j = 0; j < D; ++j) h[j] = fma(v, sm[oW1 + k * D + j], h[j]);
+    for (int v = 0; v < KS; ++v) {
+      const int f = feat(v, c);
+      double a = b1[f];
+      for (int k = 0; k < p.dn; ++k) a = fma(ok ? V[i * p.dn + k] : 0.0, W1[k * DP + f], a);
+      h[v] = act_fn<ACT>(a);
+      x[v] = b2[f];
     }
+    mv<D>(h, F2, x, lane);
+    if (ok) {
 #pragma unroll
-    for (int j = 0; j < D; ++j) { h[j] = act_fn<ACT>(h[j]); x[j] = sm[ob2 + j]; }
-    mv<D, D, true>(h, sm + oW2, x);
-#pragma unroll
-    for (int j = 0; j < D; ++j) X[(int64_t)j * n + i] = x[j];
+      for (int nb = 0; nb < KS / 2; ++nb)
+        *reinterpret_cast<double2*>(X + i * DP + 8 * nb + 2 * c) = make_double2(x[2 * nb], x[2 * nb + 1]);
+    }
     if (p.L > 0) {
-      double q[D];
-      mv<D, D, false>(x, sm + oP, q);
+      double q[KS];
 #pragma unroll
-      for (int j = 0; j < D; ++j) PQ[(int64_t)j * n + i] = q[j];
-      mv<D, D, false>(x, sm + oP + D * D, q);
+      for (int v = 0; v < KS; ++v) q[v] = 0.0;
+      mv<D>(x, FP, q, lane);
+      if (ok) {
 #pragma unroll
-      for (int j = 0; j < D; ++j) PQ[(int64_t)(D + j) * n + i] = q[j];
+        for (int nb = 0; nb < KS / 2; ++nb)
+          *reinterpret_cast<double2*>(PQ + i * 2 * DP + 8 * nb + 2 * c) = make_double2(q[2 * nb], q[2 * nb + 1]);
+      }
+#pragma unroll
+      for (int v = 0; v < KS; ++v) q[v] = 0.0;
+      mv<D>(x, FQ, q, lane);
+      if (ok) {
+#pragma unroll
+        for (int nb = 0; nb < KS / 2; ++nb)
+          *reinterpret_cast<double2*>(PQ + i * 2 * DP + DP + 8 * nb + 2 * c) = make_double2(q[2 * nb], q[2 * nb + 1]);
+      }
     }
   }
 }
@@ -102,7 +170,7 @@ __global__ void __launch_bounds__(128) k_node_encode(GnnP p, int64_t n, const do
 // ------------------------------------------------------------------ node layer t
 template <int D>
 __host__ __device__ constexpr int node_layer_smem_doubles() {
-  return 7 * D * D + 8 * D;
+  return 7 * Shape<D>::FRAG + 6 * Shape<D>::DP;
 }
 
 template <int D, int ACT>
@@ -111,72 +179,101 @@ __global__ void __launch_bounds__(128) k_node_layer(GnnP p, int t, int64_t n, co
                                                     const double* __restrict__ ef, double* __restrict__ X,
                                                     const double* __restrict__ PQ, double* __restrict__ PQn,
                                                     double* __restrict__ EPQ) {
+  using S = Shape<D>;
+  constexpr int DP = S::DP, KS = S::KS, F = S::FRAG;
   extern __shared__ __align__(16) double sm[];
   const MlpP fm = p.fm[t], fv = p.fv[t], fe = p.fe[t];
   const bool nxt = t + 1 < p.L;
-  int o = 0;
-  const int o_b1 = o; o = stage(sm, o, fm.b1, D);
-  const int o_c = o; o = stage(sm, o, fm.W1 + 2 * D * D, D);  // edge-feature row (d_edge == 1)
-  const int o_W2 = o; o = stage(sm, o, fm.W2, D * D);
-  const int o_b2 = o; o = stage(sm, o, fm.b2, D);
-  const int o_V1 = o; o = stage(sm, o, fv.W1, D * D);
-  const int o_vb1 = o; o = stage(sm, o, fv.b1, D);
-  const int o_V2 = o; o = stage(sm, o, fv.W2, D * D);
-  const int o_vb2 = o; o = stage(sm, o, fv.b2, D);
-  const int o_E = o; o = stage(sm, o, fe.W1, 2 * D * D);
-  const int o_N = o; if (nxt) o = stage(sm, o, p.fm[t + 1].W1, 2 * D * D);
+  double* Fm2 = sm;
+  double* Fv1 = Fm2 + F;
+  double* Fv2 = Fv1 + F;
+  double* Fea = Fv2 + F;
+  double* Feb = Fea + F;
+  double* Fna = Feb + F;
+  double* Fnb = Fna + F;
+  double* b1 = Fnb + F;
+  double* cc = b1 + DP;
+  double* b2 = cc + DP;
+  double* vb1 = b2 + DP;
+  double* vb2 = vb1 + DP;
+  stage_frag<D>(Fm2, fm.W2, 0);
+  stage_frag<D>(Fv1, fv.W1, 0);
+  stage_frag<D>(Fv2, fv.W2, 0);
+  stage_frag<D>(Fea, fe.W1, 0);
+  stage_frag<D>(Feb, fe.W1, D);
+  if (nxt) {
+    stage_frag<D>(Fna, p.fm[t + 1].W1, 0);
+    stage_frag<D>(Fnb, p.fm[t + 1].W1, D);
+  }
+  stage_vec<D>(b1, fm.b1);
+  stage_vec<D>(cc, fm.W1 + 2 * D * D);  // edge-feature row of W1m (d_edge == 1)
+  stage_vec<D>(b2, fm.b2);
+  stage_vec<D>(vb1, fv.b1);
+  stage_vec<D>(vb2, fv.b2);
   __syncthreads();
-  const double* P = PQ;
-  const double* Q = PQ + (int64_t)D * n;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    double S[D], pi[D];
+  const int lane = threadIdx.x & 31, r = lane >> 2, c = lane & 3;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
+  for (int64_t base = (int64_t)(blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5)) * 8; base < n; base += warps * 8) {
+    const int64_t i = base + r;
+    const bool ok = i < n;
+    const int64_t ic = ok ? i : n - 1;
+    double S_[KS], pi[KS], cv[KS];
+    load_row(pi, PQ + ic * 2 * DP, c, KS);
 #pragma unroll
-    for (int j = 0; j < D; ++j) { S[j] = 0.0; pi[j] = P[(int64_t)j * n + i] + sm[o_b1 + j]; }
-    const int32_t lo = offs[i], hi = offs[i + 1];
+    for (int v = 0; v < KS; ++v) {
+      const int f = feat(v, c);
+      S_[v] = 0.0;
+      pi[v] += b1[f];
+      cv[v] = cc[f];
+    }
+    const int32_t lo = offs[ic], hi = ok ? offs[ic + 1] : lo;
     for (int32_t k = lo; k < hi; ++k) {
       const int64_t jn = cols[k];
       const double e = ef[k];
+      double q[KS];
+      load_row(q, PQ + jn * 2 * DP + DP, c, KS);
 #pragma unroll
-      for (int j = 0; j < D; ++j) S[j] += act_fn<ACT>(pi[j] + Q[(int64_t)j * n + jn] + e * sm[o_c + j]);
+      for (int v = 0; v < KS; ++v) S_[v] += act_fn<ACT>(pi[v] + q[v] + e * cv[v]);
     }
     const double deg = (double)(hi - lo);
-    double m[D];
+    double m[KS], u[KS];
 #pragma unroll
-    for (int j = 0; j < D; ++j) m[j] = deg * sm[o_b2 + j];
-    mv<D, D, true>(S, sm + o_W2, m);
-    double u[D];
+    for (int v = 0; v < KS; ++v) { const int f = feat(v, c); m[v] = deg * b2[f]; u[v] = vb1[f]; }
+    mv<D>(S_, Fm2, m, lane);
+    mv<D>(m, Fv1, u, lane);
+    double xo[KS];
+    load_row(xo, X + ic * DP, c, KS);
 #pragma unroll
-    for (int j = 0; j < D; ++j) u[j] = sm[o_vb1 + j];
-    mv<D, D, true>(m, sm + o_V1, u);
+    for (int v = 0; v < KS; ++v) { u[v] = act_fn<ACT>(u[v]); xo[v] += vb2[feat(v, c)]; }
+    mv<D>(u, Fv2, xo, lane);  // xo = X + f_v(m): the updated node state
+    if (ok) {
 #pragma unroll
-    for (int j = 0; j < D; ++j) { u[j] = act_fn<ACT>(u[j]); m[j] = X[(int64_t)j * n + i] + sm[o_vb2 + j]; }
-    mv<D, D, true>(u, sm + o_V2, m);  // m now holds the updated X row
+      for (int nb = 0; nb < KS / 2; ++nb)
+        *reinterpret_cast<double2*>(X + i * DP + 8 * nb + 2 * c) = make_double2(xo[2 * nb], xo[2 * nb + 1]);
+    }
+    double* ep = EPQ + ((int64_t)t * n) * 2 * DP;
+    const double* Fs[4] = {Fea, Feb, Fna, Fnb};
+    double* dstb[4] = {ep, ep + DP, PQn, PQn + DP};
+    const int nout = nxt ? 4 : 2;
+    for (int o = 0; o < nout; ++o) {
 #pragma unroll
-    for (int j = 0; j < D; ++j) X[(int64_t)j * n + i] = m[j];
-    double* ep = EPQ + (int64_t)t * 2 * D * n;
-    mv<D, D, false>(m, sm + o_E, u);
+      for (int v = 0; v < KS; ++v) u[v] = 0.0;
+      mv<D>(xo, Fs[o], u, lane);
+      if (ok) {
 #pragma unroll
-    for (int j = 0; j < D; ++j) ep[(int64_t)j * n + i] = u[j];
-    mv<D, D, false>(m, sm + o_E + D * D, u);
-#pragma unroll
-    for (int j = 0; j < D; ++j) ep[(int64_t)(D + j) * n + i] = u[j];
-    if (nxt) {
-      mv<D, D, false>(m, sm + o_N, u);
-#pragma unroll
-      for (int j = 0; j < D; ++j) PQn[(int64_t)j * n + i] = u[j];
-      mv<D, D, false>(m, sm + o_N + D * D, u);
-#pragma unroll
-      for (int j = 0; j < D; ++j) PQn[(int64_t)(D + j) * n + i] = u[j];
+        for (int nb = 0; nb < KS / 2; ++nb)
+          *reinterpret_cast<double2*>(dstb[o] + i * 2 * DP + 8 * nb + 2 * c) = make_double2(u[2 * nb], u[2 * nb + 1]);
+      }
     }
   }
 }
 
 // ------------------------------------------------------------------ fused edge pass
-// Edge-path weights in shared memory:
-//   [Ee1 D][be1 D][Ee2 DxD][be2 D] + L x ([We1c DxD][be1 D][We2 DxD][be2 D]) + [D1 DxD][bd1 D][D2 D][bd2 1]
+// Shared memory: per layer [We1c frag][We2 frag][be1][be2]; then [Ee2 frag][D1 frag]
+// [Ee1][eb1][eb2][bd1][D2] (padded vectors) and the scalar bd2.
 template <int D>
 __host__ __device__ constexpr int edge_smem_doubles(int L) {
-  return (3 * D + D * D) + L * (2 * D * D + 2 * D) + (D * D + 2 * D + 2);
+  return L * (2 * Shape<D>::FRAG + 2 * Shape<D>::DP) + 2 * Shape<D>::FRAG + 5 * Shape<D>::DP + 2;
 }
 
 template <int D, int ACT>
@@ -185,85 +282,108 @@ __global__ void __launch_bounds__(128) k_edge_pass(GnnP p, int64_t nnz, const in
                                                    const double* __restrict__ ef,
                                                    const double* __restrict__ EPQ, int64_t n,
                                                    double* __restrict__ g) {
+  using S = Shape<D>;
+  constexpr int DP = S::DP, KS = S::KS, F = S::FRAG;
   extern __shared__ __align__(16) double w[];
   const int L = p.L;
-  int o = 0;
-  o = stage(w, o, p.ee.W1, D); o = stage(w, o, p.ee.b1, D); o = stage(w, o, p.ee.W2, D * D);
-  o = stage(w, o, p.ee.b2, D);
+  const int per = 2 * F + 2 * DP;
   for (int t = 0; t < L; ++t) {
-    o = stage(w, o, p.fe[t].W1 + 2 * D * D, D * D); o = stage(w, o, p.fe[t].b1, D);
-    o = stage(w, o, p.fe[t].W2, D * D); o = stage(w, o, p.fe[t].b2, D);
+    double* base = w + t * per;
+    stage_frag<D>(base, p.fe[t].W1, 2 * D);
+    stage_frag<D>(base + F, p.fe[t].W2, 0);
+    stage_vec<D>(base + 2 * F, p.fe[t].b1);
+    stage_vec<D>(base + 2 * F + DP, p.fe[t].b2);
   }
-  const int o_dec = o;
-  o = stage(w, o, p.dec.W1, D * D); o = stage(w, o, p.dec.b1, D); o = stage(w, o, p.dec.W2, D);
-  o = stage(w, o, p.dec.b2, 1);
+  double* FE2 = w + L * per;
+  double* FD1 = FE2 + F;
+  double* e1 = FD1 + F;
+  double* eb1 = e1 + DP;
+  double* eb2 = eb1 + DP;
+  double* db1 = eb2 + DP;
+  double* d2 = db1 + DP;
+  double* db2 = d2 + DP;
+  stage_frag<D>(FE2, p.ee.W2, 0);
+  stage_frag<D>(FD1, p.dec.W1, 0);
+  stage_vec<D>(e1, p.ee.W1);
+  stage_vec<D>(eb1, p.ee.b1);
+  stage_vec<D>(eb2, p.ee.b2);
+  stage_vec<D>(db1, p.dec.b1);
+  stage_vec<D>(d2, p.dec.W2);
+  if (threadIdx.x == 0) db2[0] = p.dec.b2[0];
   __syncthreads();
-  const double* Ee1 = w;
-  const double* eb1 = w + D;
-  const double* Ee2 = w + 2 * D;
-  const double* eb2 = w + 2 * D + D * D;
-  const double* lay = w + 3 * D + D * D;
-  const double* dec = w + o_dec;
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
-    const double e = ef[k];
-    const int64_t i = rows[k], j = cols[k];
-    double h[D], a[D];
+  const int lane = threadIdx.x & 31, r = lane >> 2, c = lane & 3;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
+  for (int64_t base = (int64_t)(blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5)) * 8; base < nnz; base += warps * 8) {
+    const int64_t k = base + r;
+    const bool ok = k < nnz;
+    const int64_t kc = ok ? k : nnz - 1;
+    const double e = ef[kc];
+    const int64_t i = rows[kc], j = cols[kc];
+    double h[KS], a[KS];
 #pragma unroll
-    for (int q = 0; q < D; ++q) { a[q] = act_fn<ACT>(fma(e, Ee1[q], eb1[q])); h[q] = eb2[q]; }
-    mv<D, D, true>(a, Ee2, h);
+    for (int v = 0; v < KS; ++v) {
+      const int f = feat(v, c);
+      a[v] = act_fn<ACT>(fma(e, e1[f], eb1[f]));
+      h[v] = eb2[f];
+    }
+    mv<D>(a, FE2, h, lane);
     for (int t = 0; t < L; ++t) {
-      const double* W1c = lay + t * (2 * D * D + 2 * D);
-      const double* b1 = W1c + D * D;
-      const double* W2 = b1 + D;
-      const double* b2 = W2 + D * D;
-      const double* Pt = EPQ + (int64_t)t * 2 * D * n;
+      const double* lay = w + t * per;
+      const double* Pt = EPQ + (int64_t)t * n * 2 * DP;
+      double q[KS];
+      load_row(a, Pt + i * 2 * DP, c, KS);
+      load_row(q, Pt + j * 2 * DP + DP, c, KS);
 #pragma unroll
-      for (int q = 0; q < D; ++q) a[q] = Pt[(int64_t)q * n + i] + Pt[(int64_t)(D + q) * n + j] + b1[q];
-      mv<D, D, true>(h, W1c, a);
+      for (int v = 0; v < KS; ++v) a[v] += q[v] + lay[2 * F + feat(v, c)];
+      mv<D>(h, lay, a, lane);
 #pragma unroll
-      for (int q = 0; q < D; ++q) { a[q] = act_fn<ACT>(a[q]); h[q] += b2[q]; }
-      mv<D, D, true>(a, W2, h);
+      for (int v = 0; v < KS; ++v) { a[v] = act_fn<ACT>(a[v]); h[v] += lay[2 * F + DP + feat(v, c)]; }
+      mv<D>(a, lay + F, h, lane);
     }
 #pragma unroll
-    for (int q = 0; q < D; ++q) a[q] = dec[D * D + q];
-    mv<D, D, true>(h, dec, a);
-    double out = dec[D * D + 2 * D];
+    for (int v = 0; v < KS; ++v) a[v] = db1[feat(v, c)];
+    mv<D>(h, FD1, a, lane);
+    double part = 0.0;
 #pragma unroll
-    for (int q = 0; q < D; ++q) out = fma(act_fn<ACT>(a[q]), dec[D * D + D + q], out);
-    g[k] = out;
+    for (int v = 0; v < KS; ++v) part = fma(act_fn<ACT>(a[v]), d2[feat(v, c)], part);
+    part += __shfl_xor_sync(0xffffffffu, part, 1);
+    part += __shfl_xor_sync(0xffffffffu, part, 2);
+    if (ok && c == 0) g[k] = part + db2[0];
   }
 }
 
-static int grid_for(int64_t n, int threads, int per_sm) {
-  int64_t b = ceil_div(n > 0 ? n : 1, threads);
+static int grid_for(int64_t rows, int per_sm) {
+  const int64_t groups = (rows + 7) / 8;       // 8 rows per warp
+  int64_t b = (groups + 3) / 4;                // 4 warps per CTA
   const int64_t cap = 148LL * per_sm;
-  return (int)(b > cap ? cap : b);
+  return (int)(b > cap ? cap : (b < 1 ? 1 : b));
 }
 
 template <int D, int ACT>
 int run_forward(const GnnP& p, int64_t n, int64_t nnz, const int32_t* offs, const int32_t* cols,
                 const int32_t* rows, const double* V, const double* ef, double* g, double* X,
                 double* PQa, double* PQb, double* EPQ, cudaStream_t s) {
-  const size_t sm_enc = (size_t)(p.dn * D + 4 * D + D * D + 2 * D * D + 8) * sizeof(double);
+  using S = Shape<D>;
+  const size_t sm_enc = (size_t)(6 * S::DP + 3 * S::FRAG + 16) * sizeof(double);
   SG_CUDA(cudaFuncSetAttribute(k_node_encode<D, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_enc));
-  k_node_encode<D, ACT><<<grid_for(n, 128, 16), 128, sm_enc, s>>>(p, n, V, X, PQa);
+  k_node_encode<D, ACT><<<grid_for(n, 8), 128, sm_enc, s>>>(p, n, V, X, PQa);
   SG_LAUNCH_CHECK("k_node_encode");
   const size_t sm_layer = (size_t)(node_layer_smem_doubles<D>() + 16) * sizeof(double);
   SG_CUDA(cudaFuncSetAttribute(k_node_layer<D, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_layer));
   double* cur = PQa;
   double* nxt = PQb;
   for (int t = 0; t < p.L; ++t) {
-    k_node_layer<D, ACT><<<grid_for(n, 128, 16), 128, sm_layer, s>>>(p, t, n, offs, cols, ef, X, cur, nxt, EPQ);
+    k_node_layer<D, ACT><<<grid_for(n, 8), 128, sm_layer, s>>>(p, t, n, offs, cols, ef, X, cur, nxt, EPQ);
     SG_LAUNCH_CHECK("k_node_layer");
     double* tmp = cur; cur = nxt; nxt = tmp;
   }
-  const size_t smem = (edge_smem_doubles<D>(p.L) + 8 * (p.L + 4)) * sizeof(double);
+  const size_t smem = (edge_smem_doubles<D>(p.L) + 16) * sizeof(double);
   if (smem > 227 * 1024) {
     set_error("edge-pass weights (%zu bytes) exceed shared memory; reduce n_layers or hidden_dim", smem);
     return SG_EUNSUPPORTED;
   }
   SG_CUDA(cudaFuncSetAttribute(k_edge_pass<D, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_edge_pass<D, ACT><<<grid_for(nnz, 128, 16), 128, smem, s>>>(p, nnz, rows, cols, ef, EPQ, n, g);
+  k_edge_pass<D, ACT><<<grid_for(nnz, 8), 128, smem, s>>>(p, nnz, rows, cols, ef, EPQ, n, g);
   SG_LAUNCH_CHECK("k_edge_pass");
   return SG_OK;
 }
@@ -291,12 +411,12 @@ extern "C" int sg_gnn_forward(const double* params, int64_t n_params, int n_laye
                               const int32_t* offs, const int32_t* cols, const int32_t* rows,
                               const double* node_feat, const double* edge_feat, double* g_out,
                               void* ws, size_t* ws_bytes, void* stream) {
-  const int64_t D = hidden, L = n_layers;
+  const int64_t D = hidden, L = n_layers, DP = (hidden + 7) / 8 * 8;
   Carve c(ws);
-  double* X = c.take<double>(n * D);
-  double* PQa = c.take<double>(n * 2 * D);
-  double* PQb = c.take<double>(n * 2 * D);
-  double* EPQ = c.take<double>((L > 0 ? L : 1) * n * 2 * D);
+  double* X = c.take<double>(n * DP);
+  double* PQa = c.take<double>(n * 2 * DP);
+  double* PQb = c.take<double>(n * 2 * DP);
+  double* EPQ = c.take<double>((L > 0 ? L : 1) * n * 2 * DP);
   if (!ws) { *ws_bytes = c.off; return SG_OK; }
   if (*ws_bytes < c.off) { set_error("workspace too small"); return SG_EINVAL; }
   if (d_edge != 1) { set_error("d_edge must be 1 on the GPU path"); return SG_EUNSUPPORTED; }
