@@ -227,23 +227,36 @@ def run_ours(a, rank, world, local):
     if not a.no_e2e:
         As, bs, metas = [], [], []
         a_dev = batch.a
-        offs_h = a_dev.offs.cpu().numpy().astype(np.int64)
-        cols_h = a_dev.cols.cpu().numpy().astype(np.int64)
-        vals_h = a_dev.vals.cpu().numpy()
-        b_h = batch.b.cpu().numpy()
-        coeff_h = batch.coeff.cpu().numpy()
+
+        def pinned(t):  # host copy in page-locked memory (the contract's "pinned host memory")
+            h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+            h.copy_(t)
+            return h.numpy()
+
+        offs_h = pinned(a_dev.offs.to(torch.int64))
+        cols_h = pinned(a_dev.cols.to(torch.int64))
+        vals_h = pinned(a_dev.vals)
+        b_h = pinned(batch.b)
+        coeff_h = pinned(batch.coeff)
 
         class HostCsr:  # reference-typed host system (int64 CSR, f64 values)
             def __init__(self, n, o, c, v):
                 self.n_rows = self.n_cols = n
                 self.row_offsets, self.col_indices, self.values = o, c, v
 
+        # per-system reference-typed arrays (local int64 indices) living in pinned memory
+        loc_offs = torch.empty(S * (n1 + 1), dtype=torch.int64, pin_memory=True).numpy()
+        loc_cols = torch.empty(len(cols_h), dtype=torch.int64, pin_memory=True).numpy()
         for k in range(S):
             r0, r1 = int(batch.row_start[k]), int(batch.row_start[k + 1])
             e0_, e1_ = int(batch.nnz_start[k]), int(batch.nnz_start[k + 1])
-            As.append(HostCsr(r1 - r0, offs_h[r0:r1 + 1] - e0_, cols_h[e0_:e1_] - r0, vals_h[e0_:e1_].copy()))
-            bs.append(b_h[r0:r1].copy())
-            metas.append(ProblemMeta(family="heat2d", n=r1 - r0, grid=(a.nx, a.nx), coeff=coeff_h[r0:r1].copy(),
+            o_k = loc_offs[k * (n1 + 1):(k + 1) * (n1 + 1)]
+            np.subtract(offs_h[r0:r1 + 1], e0_, out=o_k)
+            c_k = loc_cols[e0_:e1_]
+            np.subtract(cols_h[e0_:e1_], r0, out=c_k)
+            As.append(HostCsr(r1 - r0, o_k, c_k, vals_h[e0_:e1_]))
+            bs.append(b_h[r0:r1])
+            metas.append(ProblemMeta(family="heat2d", n=r1 - r0, grid=(a.nx, a.nx), coeff=coeff_h[r0:r1],
                                      coeff_seed=ids[k]))
         h2d = sum(A.row_offsets.nbytes + A.col_indices.nbytes + A.values.nbytes for A in As) + \
             sum(b.nbytes for b in bs) + sum(m.coeff.nbytes for m in metas)

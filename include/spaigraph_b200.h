@@ -56,6 +56,13 @@ int sg_csr_from_coo(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* 
 int sg_narrow_index(const int64_t* in, int32_t* out, int64_t n, int64_t lo, int64_t hi,
                     int64_t shift, void* ws, size_t* ws_bytes, void* stream);
 
+/* Batched narrowing for block-diagonal batches: element k of segment s (seg_start[s] <= k <
+ * seg_start[s+1], device arrays) must satisfy 0 <= in[k] < bound[s]; out[k] = in[k] + shift[s].
+ * One launch for every system's offsets (or columns).  Synchronizes. */
+int sg_narrow_index_segments(const int64_t* in, int32_t* out, int64_t n, const int64_t* seg_start,
+                             const int64_t* bound, const int64_t* shift, int32_t n_seg, void* ws,
+                             size_t* ws_bytes, void* stream);
+
 /* _validate_structure (sparse.py:27-43): offsets[0]==0, offsets[n]==nnz, nondecreasing,
  * columns in range and strictly increasing within a row.  Synchronizes. */
 int sg_csr_validate(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t* offs,

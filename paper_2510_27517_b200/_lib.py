@@ -35,6 +35,7 @@ SIGNATURES = {
     "sg_last_error": (C.c_char_p, []),
     "sg_csr_from_coo": (C.c_int, [i64, i64, i64, vp, vp, vp, vp, vp, vp, C.POINTER(C.c_int64), vp, szp, vp]),
     "sg_narrow_index": (C.c_int, [vp, vp, i64, i64, i64, i64, vp, szp, vp]),
+    "sg_narrow_index_segments": (C.c_int, [vp, vp, i64, vp, vp, vp, i32, vp, szp, vp]),
     "sg_csr_validate": (C.c_int, [i64, i64, i64, vp, vp, vp, szp, vp]),
     "sg_csr_transpose": (C.c_int, [i64, i64, i64, vp, vp, vp, vp, vp, vp, szp, vp]),
     "sg_pattern_is_symmetric": (C.c_int, [i64, i64, vp, vp, C.POINTER(C.c_int32), vp, szp, vp]),

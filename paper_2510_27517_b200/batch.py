@@ -91,44 +91,63 @@ class SystemBatch:
         if n + 1 > 2**31 - 1 or nnz > 2**31 - 1:
             raise ValueError("batch too large for int32 device indices")
         pde = metas is not None and all(getattr(m, "family", None) in ("poisson2d", "heat2d") for m in metas)
-        if into is not None and np.array_equal(into.row_start, row_start) and np.array_equal(into.nnz_start, nnz_start):
+        reuse = (into is not None and np.array_equal(into.row_start, row_start)
+                 and np.array_equal(into.nnz_start, nnz_start) and getattr(into, "_stage", None) is not None)
+        if reuse:
             offs, cols, vals, b = into.a.offs, into.a.cols, into.a.vals, into.b
             coeff = into.coeff if pde else None
+            so, sc, seg_o, seg_c = into._stage
         else:
             offs, cols = L.empty(n + 1, torch.int32), L.empty(nnz, torch.int32)
             vals, b = L.empty(nnz, torch.float64), L.empty(n, torch.float64)
             coeff = L.empty(n, torch.float64) if pde else None
-        stage64 = torch.empty(max(max(nnzs), max(rows) + 1), dtype=torch.int64, device=L.device())
+            so, sc = L.empty(n, torch.int64), L.empty(nnz, torch.int64)
+            # per-segment tables for the batched narrowing: (start, bound, shift)
+            seg_o = (L.to_device(row_start, torch.int64), L.to_device(np.asarray(nnzs) + 1, torch.int64),
+                     L.to_device(nnz_start[:-1], torch.int64))
+            seg_c = (L.to_device(nnz_start, torch.int64), L.to_device(np.asarray(rows), torch.int64),
+                     L.to_device(row_start[:-1], torch.int64))
         lib = L.lib()
+        # H2D: one async copy per host array (asynchronous when the host array is pinned)
         for k, A in enumerate(As):
             r0, e0 = int(row_start[k]), int(nnz_start[k])
             if A.n_rows != A.n_cols:
                 raise ValueError("systems must be square")
-            o = np.ascontiguousarray(A.row_offsets, dtype=np.int64)
-            c = np.ascontiguousarray(A.col_indices, dtype=np.int64)
-            stage64[: len(o)].copy_(torch.from_numpy(o))
-            L.call_ws(lib.sg_narrow_index, L.ptr(stage64), C.c_void_p(offs.data_ptr() + 4 * r0), len(o) - 1,
-                      0, nnzs[k] + 1, e0, what="narrow offsets")
-            stage64[: len(c)].copy_(torch.from_numpy(c))
-            L.call_ws(lib.sg_narrow_index, L.ptr(stage64), C.c_void_p(cols.data_ptr() + 4 * e0), len(c),
-                      0, rows[k], r0, what="narrow columns")
-            vals[e0:e0 + nnzs[k]].copy_(torch.from_numpy(np.ascontiguousarray(A.values, dtype=np.float64)))
-            b[r0:r0 + rows[k]].copy_(torch.from_numpy(np.ascontiguousarray(bs[k], dtype=np.float64)))
+            o = np.asarray(A.row_offsets)
+            if o.dtype != np.int64 or len(o) != rows[k] + 1:
+                o = np.ascontiguousarray(o, dtype=np.int64)
+                if len(o) != rows[k] + 1:
+                    raise ValueError("row_offsets must have length n_rows + 1")
+            so[r0:r0 + rows[k]].copy_(torch.from_numpy(o[:-1]), non_blocking=True)
+            sc[e0:e0 + nnzs[k]].copy_(torch.from_numpy(np.ascontiguousarray(A.col_indices, dtype=np.int64)),
+                                      non_blocking=True)
+            vals[e0:e0 + nnzs[k]].copy_(torch.from_numpy(np.ascontiguousarray(A.values, dtype=np.float64)),
+                                        non_blocking=True)
+            b[r0:r0 + rows[k]].copy_(torch.from_numpy(np.ascontiguousarray(bs[k], dtype=np.float64)),
+                                     non_blocking=True)
             if pde:
-                coeff[r0:r0 + rows[k]].copy_(torch.from_numpy(np.ascontiguousarray(metas[k].coeff, dtype=np.float64)))
+                coeff[r0:r0 + rows[k]].copy_(torch.from_numpy(np.ascontiguousarray(metas[k].coeff, dtype=np.float64)),
+                                             non_blocking=True)
+        # int64 -> int32 with per-system range checks and block-diagonal shifts: two launches
+        L.call_ws(lib.sg_narrow_index_segments, L.ptr(so), L.ptr(offs), n, L.ptr(seg_o[0]), L.ptr(seg_o[1]),
+                  L.ptr(seg_o[2]), S, what="narrow offsets")
+        L.call_ws(lib.sg_narrow_index_segments, L.ptr(sc), L.ptr(cols), nnz, L.ptr(seg_c[0]), L.ptr(seg_c[1]),
+                  L.ptr(seg_c[2]), S, what="narrow columns")
         offs[n:n + 1].fill_(nnz)
         L.call_ws(lib.sg_csr_validate, n, n, nnz, L.ptr(offs), L.ptr(cols), what="validate batch")
         grids = [tuple(m.grid) for m in metas] if pde else None
         means = [float(np.asarray(m.coeff, dtype=np.float64).mean()) for m in metas] if pde else None
-        if into is not None and into.a.offs is offs:
+        if reuse:
             # same device buffers refilled in place: keep the object (and its cached row index,
             # transpose permutation and any PCG handle built on it); the pattern may differ, so
-            # drop the pattern-derived caches
+            # recompute the pattern-derived caches in place
             into.a.refresh_pattern()
             into.grids, into.coeff, into.coeff_mean = grids, coeff, means
             return into
         a = DeviceCsr(n, n, offs, cols, vals)
-        return SystemBatch(a, row_start, nnz_start, b, grids, coeff, means)
+        out = SystemBatch(a, row_start, nnz_start, b, grids, coeff, means)
+        out._stage = (so, sc, seg_o, seg_c)
+        return out
 
 
 def _rhs(n, seed):

@@ -22,6 +22,23 @@ __global__ void k_narrow(const int64_t* __restrict__ in, int32_t* __restrict__ o
   }
 }
 
+// Segmented narrowing for block-diagonal batches: element k of segment s (seg[s] <= k <
+// seg[s+1]) must satisfy 0 <= v < bound[s]; out[k] = v + shift[s].
+__global__ void k_narrow_seg(const int64_t* __restrict__ in, int32_t* __restrict__ out, int64_t n,
+                             const int64_t* __restrict__ seg, const int64_t* __restrict__ bound,
+                             const int64_t* __restrict__ shift, int n_seg, unsigned long long* bad) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    int lo = 0, hi = n_seg;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (seg[mid] <= k) lo = mid; else hi = mid;
+    }
+    const int64_t v = in[k];
+    if (v < 0 || v >= bound[lo]) atomicMin(bad, (unsigned long long)k);
+    out[k] = (int32_t)(v + shift[lo]);
+  }
+}
+
 __global__ void k_coo_keys(const int64_t* __restrict__ rows, const int64_t* __restrict__ cols,
                            int64_t nnz, int64_t n_rows, int64_t n_cols, uint64_t* keys,
                            int32_t* idx, unsigned long long* bad) {
@@ -185,6 +202,28 @@ extern "C" int sg_narrow_index(const int64_t* in, int32_t* out, int64_t n, int64
   SG_CUDA(cudaStreamSynchronize(s));
   if (h != ~0ull) {
     set_error("index out of range at position %llu", h);
+    return SG_EINVAL;
+  }
+  return SG_OK;
+}
+
+extern "C" int sg_narrow_index_segments(const int64_t* in, int32_t* out, int64_t n, const int64_t* seg_start,
+                                        const int64_t* bound, const int64_t* shift, int32_t n_seg, void* ws,
+                                        size_t* ws_bytes, void* stream) {
+  Carve c(ws);
+  unsigned long long* bad = c.take<unsigned long long>(1);
+  if (!ws) { *ws_bytes = c.off; return SG_OK; }
+  if (*ws_bytes < c.off) { set_error("workspace too small"); return SG_EINVAL; }
+  if (n <= 0 || n_seg <= 0) return SG_OK;
+  cudaStream_t s = as_stream(stream);
+  SG_CUDA(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), s));
+  k_narrow_seg<<<grid_for(n), 256, 0, s>>>(in, out, n, seg_start, bound, shift, n_seg, bad);
+  SG_LAUNCH_CHECK("k_narrow_seg");
+  unsigned long long h = 0;
+  SG_CUDA(cudaMemcpyAsync(&h, bad, sizeof(h), cudaMemcpyDeviceToHost, s));
+  SG_CUDA(cudaStreamSynchronize(s));
+  if (h != ~0ull) {
+    set_error("index out of range at position %llu of the batch", h);
     return SG_EINVAL;
   }
   return SG_OK;
