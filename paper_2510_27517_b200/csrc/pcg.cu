@@ -326,6 +326,40 @@ __device__ __forceinline__ double dia_row_numpy(const Dia& dd, const double* __r
   return more ? add(first, s) : first;
 }
 
+// Same numpy-order row reduction for an exactly SYMMETRIC matrix stored by its lower half: the
+// entry on an upper diagonal d (off > 0) is read from the mirror (lower) diagonal at row
+// i + off, so the upper diagonals are never streamed from HBM.
+template <int ND, int XM>
+__device__ __forceinline__ double dia_row_numpy_sym(const Dia& dd, const double* __restrict__ V, long long i,
+                                                    unsigned int m, const XF& f) {
+  double first = 0.0, s = 0.0;
+  bool have = false, more = false;
+#pragma unroll
+  for (int d = 0; d < ND; ++d) {
+    if (m & (1u << d)) {
+      const long long j = i + dd.off[d];
+      const double a = dd.off[d] > 0 ? __ldg(V + (long long)dd.mir[d] * dd.n + j) : __ldg(V + (long long)d * dd.n + i);
+      const double p = mul(a, xval<XM>(f, (int32_t)j));
+      if (!have) { first = p; have = true; }
+      else { s = add(s, p); more = true; }
+    }
+  }
+  return more ? add(first, s) : first;
+}
+
+// Bitwise check that a diagonal-major matrix equals its transpose on the stored pattern.
+__global__ void k_dia_symcheck(Dia dia, const double* __restrict__ V, unsigned int* asym) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < dia.n; i += (long long)gridDim.x * blockDim.x) {
+    const unsigned int m = dia.mask[i];
+    for (int d = 0; d < dia.nd; ++d)
+      if ((m & (1u << d)) && dia.off[d] > 0) {
+        const double up = V[(long long)d * dia.n + i];
+        const double lo = V[(long long)dia.mir[d] * dia.n + i + dia.off[d]];
+        if (__double_as_longlong(up) != __double_as_longlong(lo)) { *asym = 1u; return; }
+      }
+  }
+}
+
 // add.at order over row i of G^T, read from G's mirror diagonals.
 template <int ND, int XM>
 __device__ __forceinline__ double dia_row_t_seq(const Dia& dd, const double* __restrict__ V, long long i,
@@ -352,7 +386,7 @@ struct Fmt {};
   __shared__ int flag;                          \
   int sys; long long r0, r1;                    \
   block_rows(D, sys, r0, r1);                   \
-  constexpr int RPT = FMT == 1 ? kRpt : 1;      \
+  constexpr int RPT = FMT >= 1 ? kRpt : 1;      \
   (void)T;
 
 // A-row (numpy order) for either format.
@@ -360,20 +394,21 @@ template <int FMT, int ND, bool SH, int XM>
 __device__ __forceinline__ double rowA(const Dev& D, const RowTile<PR, (FMT == 0 ? PCAP : 4)>& T, long long i,
                                        long long r0, unsigned int m, const XF& f) {
   if (FMT == 1) return dia_row_numpy<ND, XM>(D.dia, D.dia.a, i, m, f);
+  if (FMT == 2) return dia_row_numpy_sym<ND, XM>(D.dia, D.dia.a, i, m, f);
   return tile_row_dot<kOrderNumpy, SH, XM>(*reinterpret_cast<const RowTile<PR, PCAP>*>(&T), (int)(i - r0),
                                            D.a_cols, D.a_vals, f);
 }
 template <int FMT, int ND, bool SH, int XM>
 __device__ __forceinline__ double rowG(const Dev& D, const RowTile<PR, (FMT == 0 ? PCAP : 4)>& T, long long i,
                                        long long r0, unsigned int m, const XF& f) {
-  if (FMT == 1) return dia_row_numpy<ND, XM>(D.dia, D.dia.g, i, m, f);
+  if (FMT >= 1) return dia_row_numpy<ND, XM>(D.dia, D.dia.g, i, m, f);
   return tile_row_dot<kOrderNumpy, SH, XM>(*reinterpret_cast<const RowTile<PR, PCAP>*>(&T), (int)(i - r0),
                                            D.g_cols, D.g_vals, f);
 }
 template <int FMT, int ND, bool SH, int XM>
 __device__ __forceinline__ double rowGt(const Dev& D, const RowTile<PR, (FMT == 0 ? PCAP : 4)>& T, long long i,
                                         long long r0, unsigned int m, const XF& f) {
-  if (FMT == 1) return dia_row_t_seq<ND, XM>(D.dia, D.dia.g, i, m, f);
+  if (FMT >= 1) return dia_row_t_seq<ND, XM>(D.dia, D.dia.g, i, m, f);
   return tile_row_dot<kOrderSeq, SH, XM>(*reinterpret_cast<const RowTile<PR, PCAP>*>(&T), (int)(i - r0),
                                          D.gt_cols, D.gt_vals, f);
 }
@@ -385,12 +420,12 @@ __device__ __forceinline__ void stage(const Dev& D, RowTile<PR, (FMT == 0 ? PCAP
 }
 
 __device__ __forceinline__ unsigned int dmask(const Dev& D, long long i, long long r1, int FMT) {
-  return (FMT == 1 && i < r1) ? (unsigned int)D.dia.mask[i] : 0u;
+  return (FMT >= 1 && i < r1) ? (unsigned int)D.dia.mask[i] : 0u;
 }
 
 // r = b; d = 0; x = 0; t = G^T b; partial ||b||^2
 template <int PRE, int FMT, int ND, bool SH>
-__global__ void __launch_bounds__(PR, FMT == 1 ? 8 : 1) k_setup1(Dev D) {
+__global__ void __launch_bounds__(PR, FMT >= 1 ? 8 : 1) k_setup1(Dev D) {
   SG_KERNEL_PROLOGUE
   if (PRE == SG_PRECOND_LEARNED) stage<FMT>(D, T, r0, r1, D.gt_offs, D.gt_cols, D.gt_vals);
   double pbb = 0.0;
@@ -425,7 +460,7 @@ __device__ __forceinline__ double apply_row(const Dev& D, const RowTile<PR, (FMT
 
 // s = M r0; delta0 = r.s; NotSpd check; top-of-loop checks for i = 0.
 template <int PRE, int FMT, int ND, bool SH>
-__global__ void __launch_bounds__(PR, FMT == 1 ? 8 : 1) k_setup2(Dev D) {
+__global__ void __launch_bounds__(PR, FMT >= 1 ? 8 : 1) k_setup2(Dev D) {
   SG_KERNEL_PROLOGUE
   if (PRE == SG_PRECOND_LEARNED) stage<FMT>(D, T, r0, r1, D.g_offs, D.g_cols, D.g_vals);
   double prs = 0.0;
@@ -445,7 +480,7 @@ __global__ void __launch_bounds__(PR, FMT == 1 ? 8 : 1) k_setup2(Dev D) {
 }
 
 template <int PRE, int FMT, int ND, bool SH>
-__global__ void __launch_bounds__(PR, FMT == 1 ? 8 : 1) k_iter1(Dev D, int par) {
+__global__ void __launch_bounds__(PR, FMT >= 1 ? 8 : 1) k_iter1(Dev D, int par) {
   SG_KERNEL_PROLOGUE
   const int status = D.st[sys].status;
   if (status == ST_DONE) return;
@@ -483,7 +518,7 @@ __global__ void __launch_bounds__(PR, FMT == 1 ? 8 : 1) k_iter1(Dev D, int par) 
 }
 
 template <int PRE, int FMT, int ND, bool SH>
-__global__ void __launch_bounds__(PR, FMT == 1 ? 8 : 1) k_iter2(Dev D, int par) {
+__global__ void __launch_bounds__(PR, FMT >= 1 ? 8 : 1) k_iter2(Dev D, int par) {
   SG_KERNEL_PROLOGUE
   if (D.st[sys].status != ST_RUN) return;
   const double alpha = D.st[sys].alpha;
@@ -519,7 +554,7 @@ __global__ void __launch_bounds__(PR) k_refresh_x(Dev D, int par) {
 }
 
 template <int FMT, int ND, bool SH>
-__global__ void __launch_bounds__(PR, FMT == 1 ? 8 : 1) k_refresh_r(Dev D, int par) {
+__global__ void __launch_bounds__(PR, FMT >= 1 ? 8 : 1) k_refresh_r(Dev D, int par) {
   SG_KERNEL_PROLOGUE
   if (D.st[sys].status != ST_RUN) return;
   double* rn = par ? D.r0 : D.r1;
@@ -541,7 +576,7 @@ __global__ void __launch_bounds__(PR, FMT == 1 ? 8 : 1) k_refresh_r(Dev D, int p
 }
 
 template <int FMT, int ND, bool SH>
-__global__ void __launch_bounds__(PR, FMT == 1 ? 8 : 1) k_refresh_t(Dev D, int par) {
+__global__ void __launch_bounds__(PR, FMT >= 1 ? 8 : 1) k_refresh_t(Dev D, int par) {
   SG_KERNEL_PROLOGUE
   if (D.st[sys].status != ST_RUN) return;
   const double* rn = par ? D.r0 : D.r1;
@@ -556,7 +591,7 @@ __global__ void __launch_bounds__(PR, FMT == 1 ? 8 : 1) k_refresh_t(Dev D, int p
 }
 
 template <int PRE, int FMT, int ND, bool SH>
-__global__ void __launch_bounds__(PR, FMT == 1 ? 8 : 1) k_iter3(Dev D, int par, int refreshed) {
+__global__ void __launch_bounds__(PR, FMT >= 1 ? 8 : 1) k_iter3(Dev D, int par, int refreshed) {
   SG_KERNEL_PROLOGUE
   if (D.st[sys].status != ST_RUN) return;
   const double* rn = par ? D.r0 : D.r1;
@@ -605,6 +640,8 @@ struct sg_pcg {
   int short_rows = 0;
   // DIA format (0 = CSR)
   int dia_nd = 0;
+  int a_sym = 0;      // DIA: A bitwise symmetric on its pattern -> lower-half reads only
+  unsigned int* d_flag = nullptr;
   void* dia_mem = nullptr;
   double* dia_g = nullptr;
   double* dia_a = nullptr;
@@ -636,6 +673,13 @@ template <class F>
 int dispatch(const sg_pcg* h, F f) {
   using std::integral_constant;
   return dispatch_pre(h->pre, [&](auto P) -> int {
+    if (h->dia_nd && h->a_sym) {  // DIA, A stored by its lower half (bitwise symmetric A)
+      switch (h->dia_nd) {
+        case 5: return f(P, integral_constant<int, 2>(), integral_constant<int, 5>(), integral_constant<bool, true>());
+        case 7: return f(P, integral_constant<int, 2>(), integral_constant<int, 7>(), integral_constant<bool, true>());
+        default: return f(P, integral_constant<int, 2>(), integral_constant<int, 8>(), integral_constant<bool, true>());
+      }
+    }
     switch (h->dia_nd) {
       case 5: return f(P, integral_constant<int, 1>(), integral_constant<int, 5>(), integral_constant<bool, true>());
       case 7: return f(P, integral_constant<int, 1>(), integral_constant<int, 7>(), integral_constant<bool, true>());
@@ -936,8 +980,21 @@ extern "C" int sg_pcg_solve(sg_pcg* h, const double* b, double* x, const sg_solv
     k_csr_to_dia<<<gb, 256, 0, s>>>(h->D.a_offs, h->D.a_cols, h->D.a_vals, h->n, h->D.dia, h->dia_a, h->dia_mask);
     if (h->pre == SG_PRECOND_LEARNED)
       k_csr_to_dia<<<gb, 256, 0, s>>>(h->D.g_offs, h->D.g_cols, h->D.g_vals, h->n, h->D.dia, h->dia_g, nullptr);
-    SG_LAUNCH_CHECK("k_csr_to_dia");
-    h->kernels += h->pre == SG_PRECOND_LEARNED ? 2 : 1;
+    if (!h->d_flag) SG_CUDA(cudaMalloc(&h->d_flag, sizeof(unsigned int)));
+    SG_CUDA(cudaMemsetAsync(h->d_flag, 0, sizeof(unsigned int), s));
+    k_dia_symcheck<<<gb, 256, 0, s>>>(h->D.dia, h->dia_a, h->d_flag);
+    SG_LAUNCH_CHECK("k_csr_to_dia / k_dia_symcheck");
+    h->kernels += h->pre == SG_PRECOND_LEARNED ? 3 : 2;
+    unsigned int asym = 1;
+    SG_CUDA(cudaMemcpyAsync(&asym, h->d_flag, sizeof(asym), cudaMemcpyDeviceToHost, s));
+    SG_CUDA(cudaStreamSynchronize(s));
+    const int sym = asym ? 0 : 1;
+    if (sym != h->a_sym) {  // kernel variant changes: captured graphs are stale
+      for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);
+      h->graphs.clear();
+      h->graph_kernels.clear();
+      h->a_sym = sym;
+    }
   }
   // per-system state
   std::vector<SysState> st(h->S);
@@ -1077,6 +1134,7 @@ extern "C" void sg_pcg_destroy(sg_pcg* h) {
   cudaDeviceSynchronize();
   if (h->hist) cudaFree(h->hist);
   if (h->dia_mem) cudaFree(h->dia_mem);
+  if (h->d_flag) cudaFree(h->d_flag);
   if (h->mem) cudaFree(h->mem);
   delete h;
 }
