@@ -310,20 +310,38 @@ struct CsrOps {
 };
 
 // numpy-order reduction over the present diagonals of row i of a diagonal-major matrix.
-template <int ND, int XM>
-__device__ __forceinline__ double dia_row_numpy(const Dia& dd, const double* __restrict__ V, long long i,
-                                                unsigned int m, const XF& f) {
+// Loads are issued unconditionally first (padded slots are zeros; neighbour indices are clamped
+// into the array), so no load waits for the mask; the mask only selects which products enter
+// the sum, in the reference's order.
+__device__ __forceinline__ long long clampi(long long j, long long n) { return j < 0 ? 0 : (j >= n ? n - 1 : j); }
+
+template <int ND>
+__device__ __forceinline__ double combine_numpy(const double (&p)[ND], unsigned int m) {
   double first = 0.0, s = 0.0;
   bool have = false, more = false;
 #pragma unroll
   for (int d = 0; d < ND; ++d) {
     if (m & (1u << d)) {
-      const double p = mul(__ldg(V + (long long)d * dd.n + i), xval<XM>(f, (int32_t)(i + dd.off[d])));
-      if (!have) { first = p; have = true; }
-      else { s = add(s, p); more = true; }
+      if (!have) { first = p[d]; have = true; }
+      else { s = add(s, p[d]); more = true; }
     }
   }
   return more ? add(first, s) : first;
+}
+
+template <int ND, int XM>
+__device__ __forceinline__ double dia_row_numpy(const Dia& dd, const double* __restrict__ V, long long i,
+                                                unsigned int m, const XF& f) {
+  constexpr int NA = ND > 0 ? ND : 1;
+  double a[NA], x[NA], p[NA];
+#pragma unroll
+  for (int d = 0; d < ND; ++d) {
+    a[d] = __ldg(V + (long long)d * dd.n + i);
+    x[d] = xval<XM>(f, (int32_t)clampi(i + dd.off[d], dd.n));
+  }
+#pragma unroll
+  for (int d = 0; d < ND; ++d) p[d] = mul(a[d], x[d]);
+  return combine_numpy<NA>(p, m);
 }
 
 // Same numpy-order row reduction for an exactly SYMMETRIC matrix stored by its lower half: the
@@ -332,19 +350,17 @@ __device__ __forceinline__ double dia_row_numpy(const Dia& dd, const double* __r
 template <int ND, int XM>
 __device__ __forceinline__ double dia_row_numpy_sym(const Dia& dd, const double* __restrict__ V, long long i,
                                                     unsigned int m, const XF& f) {
-  double first = 0.0, s = 0.0;
-  bool have = false, more = false;
+  constexpr int NA = ND > 0 ? ND : 1;
+  double a[NA], x[NA], p[NA];
 #pragma unroll
   for (int d = 0; d < ND; ++d) {
-    if (m & (1u << d)) {
-      const long long j = i + dd.off[d];
-      const double a = dd.off[d] > 0 ? __ldg(V + (long long)dd.mir[d] * dd.n + j) : __ldg(V + (long long)d * dd.n + i);
-      const double p = mul(a, xval<XM>(f, (int32_t)j));
-      if (!have) { first = p; have = true; }
-      else { s = add(s, p); more = true; }
-    }
+    const long long j = clampi(i + dd.off[d], dd.n);
+    a[d] = dd.off[d] > 0 ? __ldg(V + (long long)dd.mir[d] * dd.n + j) : __ldg(V + (long long)d * dd.n + i);
+    x[d] = xval<XM>(f, (int32_t)j);
   }
-  return more ? add(first, s) : first;
+#pragma unroll
+  for (int d = 0; d < ND; ++d) p[d] = mul(a[d], x[d]);
+  return combine_numpy<NA>(p, m);
 }
 
 // Bitwise check that a diagonal-major matrix equals its transpose on the stored pattern.
@@ -364,14 +380,18 @@ __global__ void k_dia_symcheck(Dia dia, const double* __restrict__ V, unsigned i
 template <int ND, int XM>
 __device__ __forceinline__ double dia_row_t_seq(const Dia& dd, const double* __restrict__ V, long long i,
                                                 unsigned int m, const XF& f) {
-  double s = 0.0;
+  constexpr int NA = ND > 0 ? ND : 1;
+  double a[NA], x[NA];
 #pragma unroll
   for (int d = 0; d < ND; ++d) {
-    if (m & (1u << d)) {
-      const long long j = i + dd.off[d];
-      s = add(s, mul(__ldg(V + (long long)dd.mir[d] * dd.n + j), xval<XM>(f, (int32_t)j)));
-    }
+    const long long j = clampi(i + dd.off[d], dd.n);
+    a[d] = __ldg(V + (long long)dd.mir[d] * dd.n + j);
+    x[d] = xval<XM>(f, (int32_t)j);
   }
+  double s = 0.0;
+#pragma unroll
+  for (int d = 0; d < ND; ++d)
+    if (m & (1u << d)) s = add(s, mul(a[d], x[d]));
   return s;
 }
 
