@@ -212,6 +212,11 @@ int sg_pcg_history(sg_pcg* h, int32_t sys, double* out_host, int64_t len);
 
 void sg_pcg_destroy(sg_pcg* h);
 
+/* Re-point a handle at new value arrays on the SAME patterns (e.g. a new G from the GNN on A's
+ * pattern, or refilled A values): avoids rebuilding the handle and its captured graphs. */
+int sg_pcg_rebind_values(sg_pcg* h, const double* a_vals, const double* g_vals, const double* gt_vals,
+                         const double* inv_diag);
+
 /* Instrumentation (no reference counterpart; pcg.py:155-229 only times apply / total on the
  * host).  With profiling on, every chunk graph brackets K1, K2, K3 of one non-refresh
  * iteration with external event-record nodes; sg_pcg_stats returns the summed device times

@@ -1114,6 +1114,25 @@ extern "C" int sg_pcg_history(sg_pcg* h, int32_t sys, double* out_host, int64_t 
   return SG_OK;
 }
 
+extern "C" int sg_pcg_rebind_values(sg_pcg* h, const double* a_vals, const double* g_vals, const double* gt_vals,
+                                    const double* inv_diag) {
+  if (!h) { set_error("null handle"); return SG_EINVAL; }
+  const bool changed = h->D.a_vals != a_vals || h->D.g_vals != g_vals || h->D.gt_vals != gt_vals ||
+                       h->D.inv_diag != inv_diag;
+  h->D.a_vals = a_vals;
+  h->D.g_vals = g_vals;
+  h->D.gt_vals = gt_vals;
+  h->D.inv_diag = inv_diag;
+  // DIA graphs only read handle-owned arrays (refilled at every solve); CSR graphs captured the
+  // value pointers and must be re-captured
+  if (changed && !h->dia_nd) {
+    for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);
+    h->graphs.clear();
+    h->graph_kernels.clear();
+  }
+  return SG_OK;
+}
+
 extern "C" int sg_pcg_set_profile(sg_pcg* h, int32_t on) {
   if (!h) { set_error("null handle"); return SG_EINVAL; }
   if ((on != 0) != (h->profile != 0)) {

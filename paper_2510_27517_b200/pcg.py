@@ -143,25 +143,46 @@ class PcgHandle:
             pass
 
 
+_HANDLES: "OrderedDict" = None
+_MAX_HANDLES = 4
+
+
 def _handle_for(A: SparseMatrix, M: Preconditioner) -> PcgHandle:
-    cache = M.__dict__.setdefault("_pcg_handles", {})
-    key = id(A)
-    if key in cache and cache[key][0] is A:
-        return cache[key][1]
+    """Solver handle for (A, M).  Handles are cached per (patterns, kind, epsilon): a new factor
+    on the same pattern (a new GNN output) or new A values only re-point the handle
+    (`sg_pcg_rebind_values`), keeping its workspace and captured graphs."""
+    global _HANDLES
+    from collections import OrderedDict
+    if _HANDLES is None:
+        _HANDLES = OrderedDict()
     a = A.device()
     starts = np.array([0, A.n_rows], dtype=np.int64)
     if isinstance(M, LearnedSpaiPreconditioner):
         if M.n != A.n_rows:
             raise ValueError(f"dimension mismatch: operator is {M.n}, matrix is {A.n_rows}")
-        h = PcgHandle(a, starts, L.PRECOND_LEARNED, M.factor.device(), M.factor_t(), None, M.epsilon)
+        g, gt, inv, kind, eps = M.factor.device(), M.factor_t(), None, L.PRECOND_LEARNED, M.epsilon
     elif isinstance(M, JacobiPreconditioner):
-        h = PcgHandle(a, starts, L.PRECOND_JACOBI, inv_diag=M.inv_diag_dev)
+        g, gt, inv, kind, eps = None, None, M.inv_diag_dev, L.PRECOND_JACOBI, 0.0
     elif isinstance(M, IdentityPreconditioner):
-        h = PcgHandle(a, starts, L.PRECOND_IDENTITY)
+        g, gt, inv, kind, eps = None, None, None, L.PRECOND_IDENTITY, 0.0
     else:
         raise TypeError(f"preconditioner {type(M).__name__} is not supported by the fused GPU solver "
                         "(supported: learned SPAI, Jacobi, identity)")
-    cache[key] = (A, h)
+    if isinstance(M, JacobiPreconditioner) and M.n != A.n_rows:
+        raise ValueError(f"dimension mismatch: operator is {M.n}, matrix is {A.n_rows}")
+    pat = lambda d: (None if d is None else (d.offs.data_ptr(), d.cols.data_ptr(), d.n_rows, d.nnz))  # noqa: E731
+    key = (pat(a), pat(g), pat(gt), kind, eps)
+    h = _HANDLES.get(key)
+    if h is not None:
+        L.check(L.lib().sg_pcg_rebind_values(h._h, L.ptr(a.vals), L.ptr(g.vals if g else None),
+                                             L.ptr(gt.vals if gt else None), L.ptr(inv)))
+        h.a, h.g, h.gt, h.inv_diag = a, g, gt, inv  # keep the new value arrays alive
+        _HANDLES.move_to_end(key)
+        return h
+    h = PcgHandle(a, starts, kind, g, gt, inv, eps)
+    _HANDLES[key] = h
+    while len(_HANDLES) > _MAX_HANDLES:
+        _HANDLES.popitem(last=False)[1].close()
     return h
 
 
