@@ -78,6 +78,19 @@ int sg_csr_transpose(int64_t n_rows, int64_t n_cols, int64_t nnz, const int32_t*
 int sg_pattern_is_symmetric(int64_t n, int64_t nnz, const int32_t* offs, const int32_t* cols,
                             int32_t* result_host, void* ws, size_t* ws_bytes, void* stream);
 
+/* A^2 pattern (no reference counterpart — the paper's future work):
+ * pattern(|A| |A|), rows sorted.  Two calls: out_cols == NULL computes out_offs (n+1) and
+ * *out_nnz_host; then call again with out_cols (out_nnz entries) to fill.  Rows with more than
+ * 2048 candidate products return SG_EUNSUPPORTED. */
+int sg_pattern_square(int64_t n, const int32_t* offs, const int32_t* cols, int32_t* out_offs,
+                      int32_t* out_cols, int64_t* out_nnz_host, void* ws, size_t* ws_bytes, void* stream);
+
+/* A's values on a superset pattern P (explicit zeros elsewhere; explicit zeros are
+ * pattern-significant, sparse.py:3-6).  SG_EINVAL if P does not contain pattern(A). */
+int sg_csr_pad_to_pattern(int64_t n, const int32_t* a_offs, const int32_t* a_cols, const double* a_vals,
+                          const int32_t* p_offs, const int32_t* p_cols, double* out_vals, void* ws,
+                          size_t* ws_bytes, void* stream);
+
 /* row_expand (sparse.py:64-66): rows_out[k] = row of stored entry k. */
 int sg_row_expand(int64_t n_rows, const int32_t* offs, int32_t* rows_out, void* stream);
 

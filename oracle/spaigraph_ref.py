@@ -193,6 +193,34 @@ def diagonal(n, offs, cols, vals):
     return d
 
 
+def pattern_square(n, offs, cols):
+    """SURVEY.md §8(a) a5 (no reference function; the paper lists two-hop patterns as future
+    work): the STRUCTURAL pattern of |A| |A| — (i, j) is stored iff some k has
+    (i, k) and (k, j) stored.  Restated with scipy on an all-ones copy (no cancellation),
+    sorted indices."""
+    import scipy.sparse as sp
+    offs = np.asarray(offs, dtype=np.int64)
+    cols = np.asarray(cols, dtype=np.int64)
+    B = sp.csr_matrix((np.ones(len(cols)), cols, offs), shape=(n, n))
+    P = (B @ B).tocsr()
+    P.sort_indices()
+    return P.indptr.astype(np.int64), P.indices.astype(np.int64)
+
+
+def pad_to_pattern(offs, cols, vals, p_offs, p_cols):
+    """A's values scattered onto a superset pattern, explicit zeros elsewhere."""
+    n = len(offs) - 1
+    out = np.zeros(len(p_cols))
+    rows = row_expand(offs)
+    prow = row_expand(p_offs)
+    key_p = prow * n + np.asarray(p_cols)
+    key_a = rows * n + np.asarray(cols)
+    pos = np.searchsorted(key_p, key_a)
+    assert np.array_equal(key_p[pos], key_a), "pattern does not contain A"
+    out[pos] = vals
+    return out
+
+
 # ----------------------------------------------------------------------------------------------
 # L6 generators  (datasets.py) + the new 3-D generator of SURVEY.md §8(d) C3
 # ----------------------------------------------------------------------------------------------

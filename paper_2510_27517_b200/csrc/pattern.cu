@@ -171,6 +171,105 @@ __global__ void k_diagonal(int64_t n, const int32_t* __restrict__ offs,
   }
 }
 
+// ------------------------------------------------------------------ A^2 pattern
+// pattern(|A| |A|): row i = sorted union over k in cols(A_i) of cols(A_k).  One warp per row:
+// gather the candidates into a per-warp shared buffer, bitonic-sort (warp-synchronous), then
+// count (pass 1) or emit (pass 2) the distinct values.  Rows with more than SQ_CAP candidates
+// are reported (SG_EUNSUPPORTED).
+constexpr int SQ_CAP = 2048;
+constexpr int SQ_WARPS = 4;
+
+__device__ int sq_gather_sort(int64_t i, const int32_t* __restrict__ offs, const int32_t* __restrict__ cols,
+                              int32_t* buf, unsigned int* overflow) {
+  const int lane = threadIdx.x & 31;
+  int m = 0;
+  for (int32_t a = offs[i]; a < offs[i + 1]; ++a) {
+    const int32_t k = cols[a];
+    const int32_t lo = offs[k], len = offs[k + 1] - lo;
+    if (m + len > SQ_CAP) { if (lane == 0) atomicOr(overflow, 1u); return -1; }
+    for (int t = lane; t < len; t += 32) buf[m + t] = cols[lo + t];
+    m += len;
+  }
+  int p2 = 1;
+  while (p2 < m) p2 <<= 1;
+  for (int t = m + lane; t < p2; t += 32) buf[t] = INT_MAX;
+  __syncwarp();
+  for (int size = 2; size <= p2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = lane; t < (p2 >> 1); t += 32) {
+        const int lo = 2 * t - (t & (stride - 1));
+        const int hi = lo + stride;
+        const bool up = (lo & size) == 0;
+        const int32_t x = buf[lo], y = buf[hi];
+        if ((x > y) == up) { buf[lo] = y; buf[hi] = x; }
+      }
+      __syncwarp();
+    }
+  }
+  return m;
+}
+
+__global__ void __launch_bounds__(32 * SQ_WARPS) k_square_pattern(int64_t n, const int32_t* __restrict__ offs,
+                                                                 const int32_t* __restrict__ cols, int32_t* counts,
+                                                                 const int32_t* __restrict__ out_offs,
+                                                                 int32_t* out_cols, unsigned int* overflow) {
+  __shared__ int32_t sbuf[SQ_WARPS][SQ_CAP];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int32_t* buf = sbuf[w];
+  for (int64_t i = (int64_t)blockIdx.x * SQ_WARPS + w; i < n; i += (int64_t)gridDim.x * SQ_WARPS) {
+    const int m = sq_gather_sort(i, offs, cols, buf, overflow);
+    if (m < 0) continue;
+    int written = 0;
+    for (int base = 0; base < m; base += 32) {
+      const int t = base + lane;
+      const bool first = t < m && (t == 0 || buf[t] != buf[t - 1]);
+      const unsigned int bal = __ballot_sync(0xffffffffu, first);
+      if (out_cols && first) out_cols[out_offs[i] + written + __popc(bal & ((1u << lane) - 1))] = buf[t];
+      written += __popc(bal);
+    }
+    if (!out_cols && lane == 0) counts[i] = written;
+    __syncwarp();
+  }
+}
+
+// Scatter A's values onto a superset pattern P (both CSR, sorted rows): explicit zeros elsewhere.
+__global__ void k_pad_to_pattern(int64_t n, const int32_t* __restrict__ a_offs, const int32_t* __restrict__ a_cols,
+                                 const double* __restrict__ a_vals, const int32_t* __restrict__ p_offs,
+                                 const int32_t* __restrict__ p_cols, double* out, unsigned int* missing) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t ka = a_offs[i];
+    const int32_t ea = a_offs[i + 1];
+    for (int32_t kp = p_offs[i]; kp < p_offs[i + 1]; ++kp) {
+      const int32_t c = p_cols[kp];
+      double v = 0.0;
+      if (ka < ea && a_cols[ka] == c) { v = a_vals[ka]; ++ka; }
+      out[kp] = v;
+    }
+    if (ka != ea) atomicOr(missing, 1u);
+  }
+}
+
+// Exclusive scan of counts into offsets (one block; the pattern build is not on the hot loop).
+__global__ void k_scan_counts(const int32_t* __restrict__ counts, int64_t n, int32_t* offs, unsigned int* big) {
+  __shared__ long long part[1024];
+  const int T = blockDim.x;
+  const int64_t chunk = (n + T - 1) / T;
+  const int64_t lo = threadIdx.x * chunk, hi = min(n, lo + chunk);
+  long long s = 0;
+  for (int64_t i = lo; i < hi; ++i) s += counts[i];
+  part[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long acc = 0;
+    for (int t = 0; t < T; ++t) { const long long v = part[t]; part[t] = acc; acc += v; }
+    if (acc >= INT32_MAX) *big = 1u;
+    offs[n] = (int32_t)acc;
+  }
+  __syncthreads();
+  long long acc = part[threadIdx.x];
+  for (int64_t i = lo; i < hi; ++i) { offs[i] = (int32_t)acc; acc += counts[i]; }
+}
+
 static inline int grid_for(int64_t n, int threads = 256) {
   int64_t g = ceil_div(n > 0 ? n : 1, threads);
   return (int)(g > 148 * 32 ? 148 * 32 : g);
@@ -204,6 +303,52 @@ extern "C" int sg_narrow_index(const int64_t* in, int32_t* out, int64_t n, int64
     set_error("index out of range at position %llu", h);
     return SG_EINVAL;
   }
+  return SG_OK;
+}
+
+extern "C" int sg_pattern_square(int64_t n, const int32_t* offs, const int32_t* cols, int32_t* out_offs,
+                                 int32_t* out_cols, int64_t* out_nnz_host, void* ws, size_t* ws_bytes, void* stream) {
+  Carve c(ws);
+  int32_t* counts = c.take<int32_t>(n + 1);
+  unsigned int* flags = c.take<unsigned int>(2);
+  if (!ws) { *ws_bytes = c.off; return SG_OK; }
+  if (*ws_bytes < c.off) { set_error("workspace too small"); return SG_EINVAL; }
+  cudaStream_t s = as_stream(stream);
+  const int grid = (int)(ceil_div(n > 0 ? n : 1, SQ_WARPS) < 148 * 16 ? ceil_div(n > 0 ? n : 1, SQ_WARPS) : 148 * 16);
+  if (!out_cols) {  // pass 1: offsets + nnz
+    SG_CUDA(cudaMemsetAsync(flags, 0, 2 * sizeof(unsigned int), s));
+    if (n > 0) k_square_pattern<<<grid, 32 * SQ_WARPS, 0, s>>>(n, offs, cols, counts, nullptr, nullptr, flags);
+    k_scan_counts<<<1, 1024, 0, s>>>(counts, n, out_offs, flags + 1);
+    SG_LAUNCH_CHECK("k_square_pattern (count)");
+    unsigned int hf[2];
+    int32_t nnz = 0;
+    SG_CUDA(cudaMemcpyAsync(hf, flags, sizeof(hf), cudaMemcpyDeviceToHost, s));
+    SG_CUDA(cudaMemcpyAsync(&nnz, out_offs + n, sizeof(nnz), cudaMemcpyDeviceToHost, s));
+    SG_CUDA(cudaStreamSynchronize(s));
+    if (hf[0]) { set_error("a row of A^2 has more than %d candidate entries", SQ_CAP); return SG_EUNSUPPORTED; }
+    if (hf[1]) { set_error("A^2 pattern exceeds the int32 index range"); return SG_EUNSUPPORTED; }
+    *out_nnz_host = nnz;
+    return SG_OK;
+  }
+  if (n > 0) k_square_pattern<<<grid, 32 * SQ_WARPS, 0, s>>>(n, offs, cols, nullptr, out_offs, out_cols, flags);
+  SG_LAUNCH_CHECK("k_square_pattern (fill)");
+  return SG_OK;
+}
+
+extern "C" int sg_csr_pad_to_pattern(int64_t n, const int32_t* a_offs, const int32_t* a_cols, const double* a_vals,
+                                     const int32_t* p_offs, const int32_t* p_cols, double* out_vals, void* ws,
+                                     size_t* ws_bytes, void* stream) {
+  Carve c(ws);
+  unsigned int* missing = c.take<unsigned int>(1);
+  if (!ws) { *ws_bytes = c.off; return SG_OK; }
+  cudaStream_t s = as_stream(stream);
+  SG_CUDA(cudaMemsetAsync(missing, 0, sizeof(unsigned int), s));
+  if (n > 0) k_pad_to_pattern<<<grid_for(n), 256, 0, s>>>(n, a_offs, a_cols, a_vals, p_offs, p_cols, out_vals, missing);
+  SG_LAUNCH_CHECK("k_pad_to_pattern");
+  unsigned int h = 0;
+  SG_CUDA(cudaMemcpyAsync(&h, missing, sizeof(h), cudaMemcpyDeviceToHost, s));
+  SG_CUDA(cudaStreamSynchronize(s));
+  if (h) { set_error("target pattern does not contain the matrix pattern"); return SG_EINVAL; }
   return SG_OK;
 }
 

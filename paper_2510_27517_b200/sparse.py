@@ -328,6 +328,38 @@ def spmv_transpose(A: SparseMatrix, x):
     return y if was_t else y.cpu().numpy()
 
 
+def pattern_square(A: SparseMatrix) -> SparsityPattern:
+    """pattern(|A| |A|) on the GPU (SURVEY.md §8(a) a5, config C4's G pattern)."""
+    import torch
+    if A.n_rows != A.n_cols:
+        raise ValueError("pattern square requires a square matrix")
+    d = A.device()
+    n = A.n_rows
+    offs = L.empty(n + 1, torch.int32)
+    nnz = C.c_int64(0)
+    buf, wsb = L.workspace(L.lib().sg_pattern_square, n, L.ptr(d.offs), L.ptr(d.cols), L.ptr(offs), None,
+                           C.byref(nnz))
+    L.check(L.lib().sg_pattern_square(n, L.ptr(d.offs), L.ptr(d.cols), L.ptr(offs), None, C.byref(nnz),
+                                      L.ptr(buf), C.byref(wsb), L.stream_ptr()), "pattern_square")
+    cols = L.empty(int(nnz.value), torch.int32)
+    L.check(L.lib().sg_pattern_square(n, L.ptr(d.offs), L.ptr(d.cols), L.ptr(offs), L.ptr(cols), C.byref(nnz),
+                                      L.ptr(buf), C.byref(wsb), L.stream_ptr()), "pattern_square")
+    return SparsityPattern(n, n, None, None, _dev=(offs, cols))
+
+
+def pad_to_pattern(A: SparseMatrix, pattern: SparsityPattern) -> SparseMatrix:
+    """A's values on a superset pattern with explicit zeros elsewhere (pattern-significant)."""
+    import torch
+    if (pattern.n_rows, pattern.n_cols) != (A.n_rows, A.n_cols):
+        raise ValueError("pattern shape does not match the matrix")
+    d = A.device()
+    po, pc = pattern.device()
+    out = L.empty(int(pc.shape[0]), torch.float64)
+    L.call_ws(L.lib().sg_csr_pad_to_pattern, A.n_rows, L.ptr(d.offs), L.ptr(d.cols), L.ptr(d.vals), L.ptr(po),
+              L.ptr(pc), L.ptr(out), what="pad_to_pattern")
+    return SparseMatrix.from_device(DeviceCsr(A.n_rows, A.n_cols, po, pc, out))
+
+
 def norm_device(vals, nnz: int, kind: int):
     """Device scalar: exact-sum matrix norm (kind 0 mean-abs, 1 frobenius, 2 entrywise l1)."""
     import torch

@@ -367,3 +367,33 @@ def test_batch_matches_single_solves():
     assert [r.k for r in res] == [r.k for r in reps]
     x = solver.x.cpu().numpy()
     assert np.array_equal(x, np.concatenate([r.x for r in reps]))
+
+
+# --------------------------------------------------------------------------- config C4 path (a5, a18)
+def test_c4_pipeline_small():
+    """rand_spd_sparse -> A^2 pattern -> A padded onto it -> graph -> GNN -> PCG (mini C4)."""
+    n = 1500
+    A = P.rand_spd_sparse(n, np.random.default_rng(3), extra_per_row=10)
+    o, c, v = O.rand_spd_sparse(n, np.random.default_rng(3), extra_per_row=10)
+    assert np.array_equal(A.row_offsets, o) and np.array_equal(A.col_indices, c) and np.array_equal(A.values, v)
+    from paper_2510_27517_b200.sparse import pad_to_pattern, pattern_square
+    Pq = pattern_square(A)
+    po, pc = O.pattern_square(n, o, c)
+    assert np.array_equal(Pq.row_offsets, po) and np.array_equal(Pq.col_indices, pc)
+    Ap = pad_to_pattern(A, Pq)
+    pv = O.pad_to_pattern(o, c, v, po, pc)
+    assert np.array_equal(Ap.values, pv)
+    gr = P.build_graph(Ap)
+    node, _, ef, norm = O.graph_features(n, po, pc, pv)
+    assert gr.norm_A == norm  # mean |.| over the padded pattern, explicit zeros included
+    assert np.array_equal(gr.node_features, node)
+    m = P.init_model(P.GnnConfig(d_node=2, seed=0))
+    G = P.forward(m, gr).G
+    want = O.gnn_forward_restructured(O.unflatten(m.params_flat(), O.init_params(2, seed=0)), node, po, pc, ef, 4)
+    assert rel_floor(G.values, want) < G_TOL
+    b = P.gen_rhs(n, 10**6)
+    rep = P.pcg_solve(A, b, P.build_learned_spai(G, 1e-4), P.SolveConfig(rtol=1e-8, max_iters=25))
+    _, k, _, hist = O.pcg_solve(o, c, v, b, lambda r: O.learned_apply(n, po, pc, G.values, 1e-4, r),
+                                rtol=1e-8, max_iters=25)
+    assert rep.k == k == 25
+    assert np.allclose(rep.residual_history, hist, rtol=1e-8, atol=1e-14)

@@ -184,3 +184,22 @@ def test_loss_and_gradient(g_sparse, g_c1):
     loss, grad = O.sai_loss(n, offs, cols, vals, offs, cols, c["G_vals"], 1e-4, c["w"], with_grad=True)
     assert loss == c["loss"] == 104128219.23691551
     assert np.array_equal(grad, c["grad"])
+
+
+def test_pattern_square_restatement_brute_force():
+    """the scipy structural restatement equals a dense boolean product."""
+    rng = np.random.default_rng(9)
+    offs, cols, vals = O.rand_spd_sparse(60, rng, extra_per_row=3)
+    po, pc = O.pattern_square(60, offs, cols)
+    B = np.zeros((60, 60), dtype=bool)
+    B[O.row_expand(offs), cols] = True
+    want = (B.astype(int) @ B.astype(int)) > 0
+    got = np.zeros((60, 60), dtype=bool)
+    got[O.row_expand(po), pc] = True
+    assert np.array_equal(got, want)
+    pv = O.pad_to_pattern(offs, cols, vals, po, pc)
+    dense = np.zeros((60, 60))
+    dense[O.row_expand(po), pc] = pv
+    ref = np.zeros((60, 60))
+    ref[O.row_expand(offs), cols] = vals
+    assert np.array_equal(dense, ref) and len(pv) == len(pc)
