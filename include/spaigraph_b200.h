@@ -178,6 +178,13 @@ int sg_learned_apply(int64_t n, const int32_t* g_offs, const int32_t* g_cols, co
                      const int32_t* gt_offs, const int32_t* gt_cols, const double* gt_vals,
                      double eps, const double* r, double* t_ws, double* s_out, void* stream);
 
+/* Elementwise update with the reference's roundings (pcg.py:186-200 `x + alpha*d`,
+ * `r - alpha*q`, `s + beta*d`): out = a + c*b (mode 0) or a - c*b (mode 1). */
+int sg_axpby(double* out, const double* a, const double* b, double c, int64_t n, int mode, void* stream);
+
+/* Deterministic dot product x.y into a device scalar (fixed reduction tree). */
+int sg_dot(const double* x, const double* y, int64_t n, double* out, void* ws, size_t* ws_bytes, void* stream);
+
 /* ---------------------------------------------------------------- PCG (L4) */
 
 /* pcg_solve (pcg.py:131-233) for a batch of independent systems stored block-diagonally

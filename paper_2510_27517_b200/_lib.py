@@ -56,6 +56,8 @@ SIGNATURES = {
     "sg_spmv": (C.c_int, [i64, vp, vp, vp, vp, vp, vp]),
     "sg_spmv_seq": (C.c_int, [i64, vp, vp, vp, vp, vp, vp]),
     "sg_learned_apply": (C.c_int, [i64, vp, vp, vp, vp, vp, vp, f64, vp, vp, vp, vp]),
+    "sg_axpby": (C.c_int, [vp, vp, vp, f64, i64, C.c_int, vp]),
+    "sg_dot": (C.c_int, [vp, vp, i64, vp, vp, szp, vp]),
     "sg_pcg_create": (C.c_int, [C.POINTER(vp), i32, C.POINTER(C.c_int64), vp, vp, vp, C.c_int,
                                 vp, vp, vp, vp, vp, vp, vp, f64, vp]),
     "sg_pcg_solve": (C.c_int, [vp, vp, vp, C.POINTER(SolveConfigC), C.POINTER(SolveResultC),

@@ -37,9 +37,56 @@ __global__ void __launch_bounds__(kRows) k_apply_g(int64_t n, const int32_t* __r
   }
 }
 
+// out = a + c*b (mode 0) or a - c*b (mode 1), each product rounded first (numpy semantics).
+__global__ void k_axpby(double* __restrict__ out, const double* __restrict__ a, const double* __restrict__ b,
+                        double c, int64_t n, int mode) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double p = mul(c, b[i]);
+    out[i] = mode == 0 ? add(a[i], p) : sub(a[i], p);
+  }
+}
+
+// Deterministic dot product: fixed grid, fixed per-thread strides, fixed trees.
+constexpr int kDotBlocks = 296;
+__global__ void k_dot_partial(const double* __restrict__ x, const double* __restrict__ y, int64_t n, double* part) {
+  __shared__ double red[8];
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    s = add(s, mul(x[i], y[i]));
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+__global__ void k_dot_final(const double* __restrict__ part, int np, double* out) {
+  __shared__ double red[8];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) s = add(s, part[i]);
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) *out = s;
+}
+
 }  // namespace sg
 
 using namespace sg;
+
+extern "C" int sg_axpby(double* out, const double* a, const double* b, double c, int64_t n, int mode, void* stream) {
+  if (n <= 0) return SG_OK;
+  const int64_t g = ceil_div(n, 256);
+  k_axpby<<<(unsigned)(g < 148 * 16 ? g : 148 * 16), 256, 0, as_stream(stream)>>>(out, a, b, c, n, mode);
+  SG_LAUNCH_CHECK("k_axpby");
+  return SG_OK;
+}
+
+extern "C" int sg_dot(const double* x, const double* y, int64_t n, double* out, void* ws, size_t* ws_bytes,
+                      void* stream) {
+  Carve c(ws);
+  double* part = c.take<double>(kDotBlocks);
+  if (!ws) { *ws_bytes = c.off; return SG_OK; }
+  cudaStream_t s = as_stream(stream);
+  k_dot_partial<<<kDotBlocks, 256, 0, s>>>(x, y, n, part);
+  k_dot_final<<<1, 256, 0, s>>>(part, kDotBlocks, out);
+  SG_LAUNCH_CHECK("k_dot");
+  return SG_OK;
+}
 
 extern "C" int sg_spmv(int64_t n_rows, const int32_t* offs, const int32_t* cols, const double* vals,
                        const double* x, double* y, void* stream) {
