@@ -293,20 +293,26 @@ def C_byref(x):
 
 
 class TorchComm:
-    """Collectives over torch.distributed (NCCL on GPUs, gloo on CPU)."""
+    """Collectives over torch.distributed (NCCL on GPUs, gloo on CPU); a single process without
+    a process group behaves as world_size 1."""
 
     def __init__(self, device=None):
         import torch
         import torch.distributed as dist
         self.torch, self.dist, self.device = torch, dist, device
+        self.single = not (dist.is_available() and dist.is_initialized())
 
     def allreduce_sum(self, arr):
+        if self.single:
+            return np.asarray(arr, dtype=np.float64)
         t = self.torch.as_tensor(np.asarray(arr, dtype=np.float64), device=self.device)
         self.dist.all_reduce(t)
         return t.cpu().numpy()
 
     def exchange_lists(self, per_rank):
         """all_to_all of variable-length int64 arrays via all_gather_object (setup only)."""
+        if self.single:
+            return [np.asarray(a, dtype=np.int64) for a in per_rank]
         world = self.dist.get_world_size()
         gathered = [None] * world
         self.dist.all_gather_object(gathered, [np.asarray(a, np.int64).tolist() for a in per_rank])
@@ -314,6 +320,8 @@ class TorchComm:
         return [np.asarray(gathered[p][me], dtype=np.int64) for p in range(world)]
 
     def halo(self, x_ext, plan: HaloPlan):
+        if self.single:
+            return
         torch, dist = self.torch, self.dist
         ops = []
         send_bufs = []
@@ -337,3 +345,51 @@ class TorchComm:
                 req.wait()
         for o_, buf in recv:
             x_ext[o_:o_ + len(buf)].copy_(buf)
+
+
+def solve_rowpart(A, meta, model, b, rtol=1e-8, max_iters=None, period=50, termination="true_residual",
+                  rank=None, world=None, comm=None):
+    """Full hot path for one system on a row partition: global features, receptive-field
+    subgraph GNN (no communication), local G / G^T rows, distributed PCG.  Returns the owned
+    slice of x, k, converged, history, and the plan.  Every rank holds the global A (input)."""
+    import torch
+    import torch.distributed as dist
+
+    from . import _lib as L
+    from .gnn import forward_device
+    from .graphfeat import build_graph
+    from .sparse import DeviceCsr
+    if comm is None:
+        comm = TorchComm(L.device())
+    if rank is None:
+        rank = dist.get_rank() if not comm.single else 0
+        world = dist.get_world_size() if not comm.single else 1
+    n = A.n_rows
+    offs, cols, vals = A.row_offsets, A.col_indices, A.values
+    gr = build_graph(A, meta)
+    node = gr.node_features
+    edge = gr.edge_features[:, 0]
+    plan = build_plan(offs, cols, n, rank, world, comm.exchange_lists)
+    R = hop_closure(offs, cols, np.arange(plan.r0, plan.r1), model.config.n_layers + 2)
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(offs))
+    in_r = np.zeros(n, dtype=bool)
+    in_r[R] = True
+    keep = in_r[rows] & in_r[cols]
+    remap = -np.ones(n, dtype=np.int64)
+    remap[R] = np.arange(len(R))
+    sub_offs = np.zeros(len(R) + 1, dtype=np.int64)
+    np.add.at(sub_offs, remap[rows[keep]] + 1, 1)
+    np.cumsum(sub_offs, out=sub_offs)
+    sub = DeviceCsr(len(R), len(R), L.to_device(sub_offs.astype(np.int32), torch.int32),
+                    L.to_device(remap[cols[keep]].astype(np.int32), torch.int32),
+                    L.to_device(vals[keep], torch.float64))
+    g_sub = forward_device(model, sub, L.to_device(np.ascontiguousarray(node[R]).ravel(), torch.float64),
+                           L.to_device(edge[keep], torch.float64), gr.d_node).cpu().numpy()
+    g = np.full(len(vals), np.nan)
+    g[np.flatnonzero(keep)] = g_sub  # exact for rows within one hop of the owned rows
+    pcg = DistPcg(plan, CudaOps(), comm, local_rows(offs, cols, vals, plan), local_rows(offs, cols, g, plan),
+                  local_transpose_rows(offs, cols, g, plan), model.config.epsilon)
+    b = np.asarray(b, dtype=np.float64)
+    x_own, k, conv, hist = pcg.solve(b[plan.r0:plan.r1], rtol=rtol, max_iters=max_iters, period=period,
+                                     termination=termination)
+    return x_own, k, conv, hist, plan

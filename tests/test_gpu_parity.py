@@ -397,3 +397,18 @@ def test_c4_pipeline_small():
                                 rtol=1e-8, max_iters=25)
     assert rep.k == k == 25
     assert np.allclose(rep.residual_history, hist, rtol=1e-8, atol=1e-14)
+
+
+def test_rowpart_single_rank_matches_pcg_solve():
+    """The row-partition path (CudaOps backend, world size 1) reproduces pcg_solve."""
+    from paper_2510_27517_b200.rowpart import solve_rowpart
+    import os
+    m = P.load_checkpoint(os.path.join(os.path.dirname(__file__), "golden", "trained_heat16.spaignn"))
+    A, meta = P.gen_poisson2d(40, 40, coeff_seed=4)
+    b = P.gen_rhs(meta, 9)
+    x, k, conv, hist, plan = solve_rowpart(A, meta, m, b, rtol=1e-8)
+    rep = P.pcg_solve(A, b, P.build_learned_spai(P.forward(m, P.build_graph(A, meta)).G, m.config.epsilon),
+                      P.SolveConfig(rtol=1e-8))
+    assert conv and rep.converged and _k_close(k, rep.k)
+    res = np.linalg.norm(b - O.spmv(A.row_offsets, A.col_indices, A.values, x))
+    assert res <= 1e-8
