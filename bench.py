@@ -205,6 +205,13 @@ def run_ours(a, rank, world, local):
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    # bytes the diagonal-major layout physically has to move per row (values incl. padding,
+    # 1-byte presence mask, vectors); A read by its lower half when bitwise symmetric
+    nd, a_sym = int(prof[5]), int(prof[6])
+    n_low = (nd // 2 + 1) if a_sym else nd
+    phys = {"k_iter1 (q = A d, d = s + beta d, d.q)": (8 * n_low + 1 + 32) * n1,
+            "k_iter2 (x, r update, t = G^T r, r.r)": (8 * nd + 1 + 56) * n1,
+            "k_iter3 (s = G t + eps r, r.s)": (8 * nd + 1 + 24) * n1} if nd else {}
     kern = {}
     samples = prof[4]
     if samples > 0:
@@ -214,11 +221,20 @@ def run_ours(a, rank, world, local):
             achieved = b * avg_active / (avg_ms * 1e-3) / 1e9
             kern[name] = {"avg_ms": avg_ms, "gbs": achieved, "frac": achieved / peak,
                           "bytes_per_launch": b * avg_active}
+            if name in phys:
+                pg = phys[name] * avg_active / (avg_ms * 1e-3) / 1e9
+                kern[name].update({"physical_bytes_per_launch": phys[name] * avg_active, "physical_gbs": pg,
+                                   "physical_frac": pg / peak})
     dom = max(kern, key=lambda k: kern[k]["avg_ms"]) if kern else None
     roofline = None
     if dom:
         roofline = {"bound": "hbm", "kernel": dom, "achieved": kern[dom]["gbs"], "peak": peak,
                     "unit": "GB/s", "frac": kern[dom]["frac"], "traffic": None,
+                    "achieved_physical": kern[dom].get("physical_gbs"),
+                    "frac_physical": kern[dom].get("physical_frac"),
+                    "bytes_note": "achieved = SURVEY.md §8(d) CSR bytes (12 B/nnz + 4 B/row + vectors); the kernels "
+                                  f"run the diagonal-major layout ({nd} diagonals{', A by its lower half' if a_sym else ''}) "
+                                  "which moves fewer bytes: physical_* counts those (8 B/diagonal/row + 1 B mask + vectors)",
                     "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)" if peak_src == "measured" else peak_src,
                     "per_kernel": kern, "samples": int(samples), "avg_active_systems": prof[3] / samples}
 

@@ -1154,6 +1154,7 @@ extern "C" int sg_pcg_stats(sg_pcg* h, int64_t* kernels_host, int64_t* chunks_ho
     prof_host[3] = h->prof_active;
     prof_host[4] = h->prof_samples;
     prof_host[5] = h->dia_nd;
+    prof_host[6] = h->a_sym;
   }
   if (reset) {
     h->kernels = h->chunks = 0;

@@ -121,7 +121,7 @@ class PcgHandle:
         """(kernels launched, graphs launched, [K1 ms, K2 ms, K3 ms, active-sum, samples, ndiag])
         — ndiag > 0 when the handle runs the diagonal-major (DIA) format, 0 for CSR."""
         k, c = C.c_int64(0), C.c_int64(0)
-        prof = (C.c_double * 6)()
+        prof = (C.c_double * 7)()
         L.check(L.lib().sg_pcg_stats(self._h, C.byref(k), C.byref(c), prof, 1 if reset else 0))
         return int(k.value), int(c.value), list(prof)
 
