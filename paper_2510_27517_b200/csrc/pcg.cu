@@ -65,8 +65,12 @@ struct Dia {
   int off[MAXD];       // ascending column offsets
   int mir[MAXD];       // mirror diagonal: off[mir[d]] == -off[d]
   long long n;
-  const double* a;     // [nd][n]
-  const double* g;     // [nd][n]
+  long long ld;        // diagonal stride: n + 2*guard (guard = max |off| zero rows on both sides,
+                       // so neighbour reads never need clamping)
+  const double* a;     // [nd][ld], pointer at row 0 of diagonal 0
+  const double* g;     // [nd][ld]
+  const double* av[MAXD];  // row-0 pointer of every diagonal of A / G
+  const double* gv[MAXD];
   const unsigned char* mask;  // [n], bit d: entry (i, i+off[d]) stored
 };
 
@@ -144,7 +148,7 @@ __global__ void k_csr_to_dia(const int32_t* __restrict__ offs, const int32_t* __
     }
 #pragma unroll
     for (int d = 0; d < MAXD; ++d)
-      if (d < dia.nd) out[(int64_t)d * n + i] = v[d];
+      if (d < dia.nd) out[(int64_t)d * dia.ld + i] = v[d];
     if (mask) mask[i] = (unsigned char)m;
   }
 }
@@ -310,11 +314,11 @@ struct CsrOps {
 };
 
 // numpy-order reduction over the present diagonals of row i of a diagonal-major matrix.
-// Loads are issued unconditionally first (padded slots are zeros; neighbour indices are clamped
-// into the array), so no load waits for the mask; the mask only selects which products enter
-// the sum, in the reference's order.
-__device__ __forceinline__ long long clampi(long long j, long long n) { return j < 0 ? 0 : (j >= n ? n - 1 : j); }
-
+// Loads are issued unconditionally first (padded slots are zeros; neighbour rows outside the
+// matrix land in the zero guard bands of every vector / diagonal array, so no clamping), so no
+// load waits for the mask; the mask only selects which products enter the sum, in the
+// reference's order.  32-bit row indices (n < 2^31) and per-diagonal base pointers keep the
+// address arithmetic to one IMAD.WIDE per load.
 template <int ND>
 __device__ __forceinline__ double combine_numpy(const double (&p)[ND], unsigned int m) {
   double first = 0.0, s = 0.0;
@@ -330,14 +334,14 @@ __device__ __forceinline__ double combine_numpy(const double (&p)[ND], unsigned 
 }
 
 template <int ND, int XM>
-__device__ __forceinline__ double dia_row_numpy(const Dia& dd, const double* __restrict__ V, long long i,
-                                                unsigned int m, const XF& f) {
+__device__ __forceinline__ double dia_row_numpy(const Dia& dd, const double* const* Vd, int i, unsigned int m,
+                                                const XF& f) {
   constexpr int NA = ND > 0 ? ND : 1;
   double a[NA], x[NA], p[NA];
 #pragma unroll
   for (int d = 0; d < ND; ++d) {
-    a[d] = __ldg(V + (long long)d * dd.n + i);
-    x[d] = xval<XM>(f, (int32_t)clampi(i + dd.off[d], dd.n));
+    a[d] = __ldg(Vd[d] + i);
+    x[d] = xval<XM>(f, i + dd.off[d]);
   }
 #pragma unroll
   for (int d = 0; d < ND; ++d) p[d] = mul(a[d], x[d]);
@@ -348,15 +352,15 @@ __device__ __forceinline__ double dia_row_numpy(const Dia& dd, const double* __r
 // entry on an upper diagonal d (off > 0) is read from the mirror (lower) diagonal at row
 // i + off, so the upper diagonals are never streamed from HBM.
 template <int ND, int XM>
-__device__ __forceinline__ double dia_row_numpy_sym(const Dia& dd, const double* __restrict__ V, long long i,
-                                                    unsigned int m, const XF& f) {
+__device__ __forceinline__ double dia_row_numpy_sym(const Dia& dd, const double* const* Vd, int i, unsigned int m,
+                                                    const XF& f) {
   constexpr int NA = ND > 0 ? ND : 1;
   double a[NA], x[NA], p[NA];
 #pragma unroll
   for (int d = 0; d < ND; ++d) {
-    const long long j = clampi(i + dd.off[d], dd.n);
-    a[d] = dd.off[d] > 0 ? __ldg(V + (long long)dd.mir[d] * dd.n + j) : __ldg(V + (long long)d * dd.n + i);
-    x[d] = xval<XM>(f, (int32_t)j);
+    const int j = i + dd.off[d];
+    a[d] = dd.off[d] > 0 ? __ldg(Vd[dd.mir[d]] + j) : __ldg(Vd[d] + i);
+    x[d] = xval<XM>(f, j);
   }
 #pragma unroll
   for (int d = 0; d < ND; ++d) p[d] = mul(a[d], x[d]);
@@ -364,13 +368,13 @@ __device__ __forceinline__ double dia_row_numpy_sym(const Dia& dd, const double*
 }
 
 // Bitwise check that a diagonal-major matrix equals its transpose on the stored pattern.
-__global__ void k_dia_symcheck(Dia dia, const double* __restrict__ V, unsigned int* asym) {
+__global__ void k_dia_symcheck(Dia dia, unsigned int* asym) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < dia.n; i += (long long)gridDim.x * blockDim.x) {
     const unsigned int m = dia.mask[i];
     for (int d = 0; d < dia.nd; ++d)
       if ((m & (1u << d)) && dia.off[d] > 0) {
-        const double up = V[(long long)d * dia.n + i];
-        const double lo = V[(long long)dia.mir[d] * dia.n + i + dia.off[d]];
+        const double up = dia.av[d][i];
+        const double lo = dia.av[dia.mir[d]][i + dia.off[d]];
         if (__double_as_longlong(up) != __double_as_longlong(lo)) { *asym = 1u; return; }
       }
   }
@@ -378,15 +382,15 @@ __global__ void k_dia_symcheck(Dia dia, const double* __restrict__ V, unsigned i
 
 // add.at order over row i of G^T, read from G's mirror diagonals.
 template <int ND, int XM>
-__device__ __forceinline__ double dia_row_t_seq(const Dia& dd, const double* __restrict__ V, long long i,
-                                                unsigned int m, const XF& f) {
+__device__ __forceinline__ double dia_row_t_seq(const Dia& dd, const double* const* Vd, int i, unsigned int m,
+                                                const XF& f) {
   constexpr int NA = ND > 0 ? ND : 1;
   double a[NA], x[NA];
 #pragma unroll
   for (int d = 0; d < ND; ++d) {
-    const long long j = clampi(i + dd.off[d], dd.n);
-    a[d] = __ldg(V + (long long)dd.mir[d] * dd.n + j);
-    x[d] = xval<XM>(f, (int32_t)j);
+    const int j = i + dd.off[d];
+    a[d] = __ldg(Vd[dd.mir[d]] + j);
+    x[d] = xval<XM>(f, j);
   }
   double s = 0.0;
 #pragma unroll
@@ -413,22 +417,22 @@ struct Fmt {};
 template <int FMT, int ND, bool SH, int XM>
 __device__ __forceinline__ double rowA(const Dev& D, const RowTile<PR, (FMT == 0 ? PCAP : 4)>& T, long long i,
                                        long long r0, unsigned int m, const XF& f) {
-  if (FMT == 1) return dia_row_numpy<ND, XM>(D.dia, D.dia.a, i, m, f);
-  if (FMT == 2) return dia_row_numpy_sym<ND, XM>(D.dia, D.dia.a, i, m, f);
+  if (FMT == 1) return dia_row_numpy<ND, XM>(D.dia, D.dia.av, (int)i, m, f);
+  if (FMT == 2) return dia_row_numpy_sym<ND, XM>(D.dia, D.dia.av, (int)i, m, f);
   return tile_row_dot<kOrderNumpy, SH, XM>(*reinterpret_cast<const RowTile<PR, PCAP>*>(&T), (int)(i - r0),
                                            D.a_cols, D.a_vals, f);
 }
 template <int FMT, int ND, bool SH, int XM>
 __device__ __forceinline__ double rowG(const Dev& D, const RowTile<PR, (FMT == 0 ? PCAP : 4)>& T, long long i,
                                        long long r0, unsigned int m, const XF& f) {
-  if (FMT >= 1) return dia_row_numpy<ND, XM>(D.dia, D.dia.g, i, m, f);
+  if (FMT >= 1) return dia_row_numpy<ND, XM>(D.dia, D.dia.gv, (int)i, m, f);
   return tile_row_dot<kOrderNumpy, SH, XM>(*reinterpret_cast<const RowTile<PR, PCAP>*>(&T), (int)(i - r0),
                                            D.g_cols, D.g_vals, f);
 }
 template <int FMT, int ND, bool SH, int XM>
 __device__ __forceinline__ double rowGt(const Dev& D, const RowTile<PR, (FMT == 0 ? PCAP : 4)>& T, long long i,
                                         long long r0, unsigned int m, const XF& f) {
-  if (FMT >= 1) return dia_row_t_seq<ND, XM>(D.dia, D.dia.g, i, m, f);
+  if (FMT >= 1) return dia_row_t_seq<ND, XM>(D.dia, D.dia.gv, (int)i, m, f);
   return tile_row_dot<kOrderSeq, SH, XM>(*reinterpret_cast<const RowTile<PR, PCAP>*>(&T), (int)(i - r0),
                                          D.gt_cols, D.gt_vals, f);
 }
@@ -661,6 +665,7 @@ struct sg_pcg {
   // DIA format (0 = CSR)
   int dia_nd = 0;
   int a_sym = 0;      // DIA: A bitwise symmetric on its pattern -> lower-half reads only
+  long long guard = 0;  // DIA: zero rows around every vector / diagonal
   unsigned int* d_flag = nullptr;
   void* dia_mem = nullptr;
   double* dia_g = nullptr;
@@ -859,16 +864,28 @@ int setup_dia(sg_pcg* h, const int32_t* a_offs, const int32_t* a_cols, const int
     if (it == offs.end()) return SG_OK;  // offset set not symmetric
     dia.mir[d] = (int)(it - offs.begin());
   }
-  const size_t vbytes = (size_t)cnt * n * sizeof(double);
+  // guard bands: max |offset| zero rows before and after every diagonal (and every vector)
+  long long guard = 0;
+  for (int d = 0; d < cnt; ++d) guard = std::max<long long>(guard, std::abs((long long)offs[d]));
+  guard = (guard + 31) / 32 * 32;  // keep 256-byte alignment of every diagonal
+  const long long ld = n + 2 * guard;
+  const size_t vbytes = (size_t)cnt * ld * sizeof(double);
   SG_CUDA(cudaMalloc(&h->dia_mem, 2 * vbytes + n + 64));
-  h->dia_a = reinterpret_cast<double*>(h->dia_mem);
-  h->dia_g = reinterpret_cast<double*>(reinterpret_cast<char*>(h->dia_mem) + vbytes);
+  SG_CUDA(cudaMemsetAsync(h->dia_mem, 0, 2 * vbytes + n + 64, s));
+  h->dia_a = reinterpret_cast<double*>(h->dia_mem) + guard;
+  h->dia_g = reinterpret_cast<double*>(reinterpret_cast<char*>(h->dia_mem) + vbytes) + guard;
   h->dia_mask = reinterpret_cast<unsigned char*>(h->dia_mem) + 2 * vbytes;
+  dia.ld = ld;
   dia.a = h->dia_a;
   dia.g = h->dia_g;
+  for (int d = 0; d < cnt; ++d) {
+    dia.av[d] = h->dia_a + d * ld;
+    dia.gv[d] = h->dia_g + d * ld;
+  }
   dia.mask = h->dia_mask;
   h->D.dia = dia;
   h->dia_nd = cnt;
+  h->guard = guard;
   return SG_OK;
 }
 
@@ -934,7 +951,8 @@ extern "C" int sg_pcg_create(sg_pcg** out, int32_t n_systems, const int64_t* sys
   const int64_t n = h->n, S = n_systems, nb = h->nblk > 0 ? h->nblk : 1;
   Carve c(nullptr);
   c.take<long long>(nb); c.take<int>(nb); c.take<int>(S + 1); c.take<long long>(S);
-  for (int v = 0; v < 9; ++v) c.take<double>(n + 2);
+  const int64_t gv = h->guard;  // zero guard rows around every vector (DIA neighbour reads)
+  for (int v = 0; v < 9; ++v) c.take<double>(n + 2 * gv + 2);
   c.take<double>(2 * nb); c.take<unsigned int>(S); c.take<SysState>(S); c.take<Ctl>(1);
   int e = cudaMalloc(&h->mem, c.off);
   if (e != cudaSuccess) { delete h; return cuda_fail((cudaError_t)e, "cudaMalloc(pcg workspace)"); }
@@ -944,11 +962,12 @@ extern "C" int sg_pcg_create(sg_pcg** out, int32_t n_systems, const int64_t* sys
   int* d_sys_blk0 = m.take<int>(S + 1);
   long long* d_sys_r1 = m.take<long long>(S);
   double* vec[9];
-  for (int v = 0; v < 9; ++v) vec[v] = m.take<double>(n + 2);
+  for (int v = 0; v < 9; ++v) vec[v] = m.take<double>(n + 2 * gv + 2) + gv;
   double* part = m.take<double>(2 * nb);
   unsigned int* counter = m.take<unsigned int>(S);
   h->st = m.take<SysState>(S);
   h->ctl = m.take<Ctl>(1);
+  SG_CUDA(cudaMemsetAsync(h->mem, 0, c.off, s));  // guards (and everything else) start at zero
   if (h->nblk) {
     SG_CUDA(cudaMemcpyAsync(d_blk_r0, blk_r0.data(), blk_r0.size() * sizeof(long long), cudaMemcpyHostToDevice, s));
     SG_CUDA(cudaMemcpyAsync(d_blk_sys, blk_sys.data(), blk_sys.size() * sizeof(int), cudaMemcpyHostToDevice, s));
@@ -1002,7 +1021,7 @@ extern "C" int sg_pcg_solve(sg_pcg* h, const double* b, double* x, const sg_solv
       k_csr_to_dia<<<gb, 256, 0, s>>>(h->D.g_offs, h->D.g_cols, h->D.g_vals, h->n, h->D.dia, h->dia_g, nullptr);
     if (!h->d_flag) SG_CUDA(cudaMalloc(&h->d_flag, sizeof(unsigned int)));
     SG_CUDA(cudaMemsetAsync(h->d_flag, 0, sizeof(unsigned int), s));
-    k_dia_symcheck<<<gb, 256, 0, s>>>(h->D.dia, h->dia_a, h->d_flag);
+    k_dia_symcheck<<<gb, 256, 0, s>>>(h->D.dia, h->d_flag);
     SG_LAUNCH_CHECK("k_csr_to_dia / k_dia_symcheck");
     h->kernels += h->pre == SG_PRECOND_LEARNED ? 3 : 2;
     unsigned int asym = 1;
