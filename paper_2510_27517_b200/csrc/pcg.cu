@@ -878,9 +878,9 @@ int setup_dia(sg_pcg* h, const int32_t* a_offs, const int32_t* a_cols, const int
   dia.ld = ld;
   dia.a = h->dia_a;
   dia.g = h->dia_g;
-  for (int d = 0; d < cnt; ++d) {
-    dia.av[d] = h->dia_a + d * ld;
-    dia.gv[d] = h->dia_g + d * ld;
+  for (int d = 0; d < MAXD; ++d) {  // unused slots alias diagonal 0 (loaded, never masked in)
+    dia.av[d] = h->dia_a + (d < cnt ? d : 0) * ld;
+    dia.gv[d] = h->dia_g + (d < cnt ? d : 0) * ld;
   }
   dia.mask = h->dia_mask;
   h->D.dia = dia;
