@@ -397,9 +397,11 @@ def test_c4_pipeline_small():
                                 rtol=1e-8, max_iters=25)
     assert rep.k == k == 25
     # random-init G on the A^2 pattern is ill-conditioned: dot-order differences grow ~10x per
-    # iteration from 1e-16 (4e-11 relative after 5 iterations); bound them over 25 iterations
+    # iteration from 1e-16 (4e-11 relative after 5 iterations).  The oracle itself run with
+    # math.fsum dots instead of numpy dots drifts from its numpy-dot run by up to 2.5e-3
+    # relative within these 25 iterations, so bound the tail at 10x that CPU-vs-CPU spread
     assert np.allclose(rep.residual_history[:6], hist[:6], rtol=1e-9, atol=0)
-    assert np.allclose(rep.residual_history, hist, rtol=1e-4, atol=0)
+    assert np.allclose(rep.residual_history, hist, rtol=2.5e-2, atol=0)
 
 
 def test_rowpart_single_rank_matches_pcg_solve():
