@@ -193,11 +193,19 @@ def run_ours(a, rank, world, local):
     # ---- roofline of the PCG iteration kernels (sampled live by in-graph event nodes)
     n1 = a.nx * a.nx
     e1n = 5 * n1 - 4 * a.nx
-    per_sys = {  # algorithmic bytes per system per launch
-        "k_iter1 (q = A d, d = s + beta d, d.q)": 12 * e1n + 4 * (n1 + 1) + 32 * n1,
-        "k_iter2 (x, r update, t = G^T r, r.r)": 12 * e1n + 4 * (n1 + 1) + 56 * n1,
-        "k_iter3 (s = G t + eps r, r.s)": 12 * e1n + 4 * (n1 + 1) + 24 * n1,
-    }
+    fused = bool(prof[7])
+    K1N = "k_iter1 (q = A d, d = s + beta d, d.q)"
+    K2N = "k_iter2 (x, r update, t = G^T r, r.r)"
+    K3N = "k_iter3 (s = G t + eps r, r.s)"
+    K23N = "k_iter23_st (x, r update, t = G^T r in smem, s = G t + eps r, r.r, r.s)"
+    # algorithmic bytes per system per launch: CSR matrix bytes
+    # (12 B/nnz + 4 B/row) + the vectors each kernel must read / write once
+    csr = 12 * e1n + 4 * (n1 + 1)
+    per_sys = {K1N: csr + 32 * n1}
+    if fused:  # t never leaves the SM: reads x d r q, writes x r s
+        per_sys[K23N] = csr + 56 * n1
+    else:
+        per_sys.update({K2N: csr + 56 * n1, K3N: csr + 24 * n1})
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -209,9 +217,13 @@ def run_ours(a, rank, world, local):
     # 1-byte presence mask, vectors); A read by its lower half when bitwise symmetric
     nd, a_sym = int(prof[5]), int(prof[6])
     n_low = (nd // 2 + 1) if a_sym else nd
-    phys = {"k_iter1 (q = A d, d = s + beta d, d.q)": (8 * n_low + 1 + 32) * n1,
-            "k_iter2 (x, r update, t = G^T r, r.r)": (8 * nd + 1 + 56) * n1,
-            "k_iter3 (s = G t + eps r, r.s)": (8 * nd + 1 + 24) * n1} if nd else {}
+    phys = {}
+    if nd:
+        phys = {K1N: (8 * n_low + 1 + 32) * n1}
+        if fused:
+            phys[K23N] = (8 * nd + 1 + 56) * n1
+        else:
+            phys.update({K2N: (8 * nd + 1 + 56) * n1, K3N: (8 * nd + 1 + 24) * n1})
     kern = {}
     samples = prof[4]
     if samples > 0:

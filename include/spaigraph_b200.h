@@ -243,8 +243,9 @@ int sg_pcg_rebind_values(sg_pcg* h, const double* a_vals, const double* g_vals, 
  * prof_host[0..2] (ms), the summed active-system counts at those iterations prof_host[3], the
  * sample count prof_host[4], the storage format prof_host[5] (number of diagonals when the
  * diagonal-major DIA format is in use, 0 for CSR), plus the number of kernels and graphs
- * launched; prof_host[6] = 1 when A is read by its lower half (bitwise-symmetric A in DIA).
- * prof_host must hold 7 doubles. */
+ * launched; prof_host[6] = 1 when A is read by its lower half (bitwise-symmetric A in DIA);
+ * prof_host[7] = 1 when K2 and K3 run fused (halo-staged DIA, learned preconditioner): then
+ * prof_host[1] is the fused kernel and prof_host[2] is 0.  prof_host must hold 8 doubles. */
 int sg_pcg_set_profile(sg_pcg* h, int32_t on);
 int sg_pcg_stats(sg_pcg* h, int64_t* kernels_host, int64_t* chunks_host, double* prof_host,
                  int32_t reset);

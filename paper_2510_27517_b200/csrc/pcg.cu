@@ -27,16 +27,22 @@
 //        PRESENT diagonals only, in ascending column order, so sums match CSR bit for bit.
 //   CSR  (anything else): CSR-stream tiles staged through shared memory (spmv.cuh).
 #include <algorithm>
+#include <cstdlib>
 #include <map>
 #include <vector>
 
 #include "spmv.cuh"
+#include "tma.cuh"
 
 namespace sg {
 
 constexpr int PR = 256;    // rows per tile (= threads per CTA)
 constexpr int PCAP = 2048; // staged nonzeros per tile (8 per row on average)
 constexpr int MAXD = 8;    // DIA: max diagonals
+constexpr int kMaxStageHalo = 512;  // DIA halo staging: shared memory <= 48 KB per CTA
+constexpr int kSwC = PR;              // sliding window: rows per chunk (one per thread)
+constexpr int kSwP = 3;               // sliding window: chunks in flight (bulk-copy prefetch depth)
+constexpr long long kSwRange = 8192;  // sliding window: rows per CTA range
 constexpr int kRpt = 4;    // DIA: rows per thread (tile = PR * kRpt rows; amortises the
                            // per-tile reduction and keeps more independent loads in flight)
 
@@ -62,6 +68,7 @@ struct Ctl {
 
 struct Dia {
   int nd;
+  int halo;            // max |off|
   int off[MAXD];       // ascending column offsets
   int mir[MAXD];       // mirror diagonal: off[mir[d]] == -off[d]
   long long n;
@@ -81,6 +88,10 @@ struct Dev {
   const int* sys_blk0;
   const long long* sys_r1;
   int tile;  // rows per tile: PR (CSR) or PR * kRpt (DIA)
+  // sliding-window range table (halo-staged DIA): ranges of <= kSwRange rows inside one system
+  const long long* rng_r0;
+  const int* rng_sys;
+  const int* sys_rng0;
   // matrices (CSR)
   const int32_t *a_offs, *a_cols; const double* a_vals;
   const int32_t *g_offs, *g_cols; const double* g_vals;
@@ -163,14 +174,16 @@ __device__ __forceinline__ void block_rows(const Dev& D, int& sys, long long& r0
 }
 
 // Publish this CTA's two partials; returns true in ALL threads of the last CTA of `sys`.
-__device__ __forceinline__ bool arrive(const Dev& D, int sys, double p0, double p1, double* red, int* flag) {
+// `sb0`: the per-system first-CTA table of the launch (tiles, or sliding-window ranges).
+__device__ __forceinline__ bool arrive(const Dev& D, const int* sb0, int sys, double p0, double p1, double* red,
+                                       int* flag) {
   const double a = block_sum(p0, red);
   const double b = block_sum(p1, red);
   if (threadIdx.x == 0) {
     D.part[2 * blockIdx.x + 0] = a;
     D.part[2 * blockIdx.x + 1] = b;
     __threadfence();
-    const unsigned int nb = (unsigned)(D.sys_blk0[sys + 1] - D.sys_blk0[sys]);
+    const unsigned int nb = (unsigned)(sb0[sys + 1] - sb0[sys]);
     const unsigned int old = atomicAdd(&D.counter[sys], 1u);
     *flag = (old == nb - 1);
   }
@@ -179,13 +192,19 @@ __device__ __forceinline__ bool arrive(const Dev& D, int sys, double p0, double 
   if (last) __threadfence();
   return last;
 }
+__device__ __forceinline__ bool arrive(const Dev& D, int sys, double p0, double p1, double* red, int* flag) {
+  return arrive(D, D.sys_blk0, sys, p0, p1, red, flag);
+}
 
 // Deterministic per-system sum of partial slot `which` (valid in thread 0).
-__device__ __forceinline__ double gather_partials(const Dev& D, int sys, int which, double* red) {
-  const int b0 = D.sys_blk0[sys], b1 = D.sys_blk0[sys + 1];
+__device__ __forceinline__ double gather_partials(const Dev& D, const int* sb0, int sys, int which, double* red) {
+  const int b0 = sb0[sys], b1 = sb0[sys + 1];
   double v = 0.0;
   for (int b = b0 + threadIdx.x; b < b1; b += blockDim.x) v += __ldcg(&D.part[2 * b + which]);
   return block_sum(v, red);
+}
+__device__ __forceinline__ double gather_partials(const Dev& D, int sys, int which, double* red) {
+  return gather_partials(D, D.sys_blk0, sys, which, red);
 }
 
 __device__ __forceinline__ void finish(const Dev& D, SysState& S, int conv) {
@@ -636,6 +655,371 @@ __global__ void __launch_bounds__(PR, FMT >= 1 ? 8 : 1) k_iter3(Dev D, int par, 
   }
 }
 
+// ------------------------------------------------------------------ halo-staged DIA kernels
+// For stencil patterns with a small halo H = max |offset| the neighbour values a row needs are
+// staged once per tile in shared memory (tile +- H rows, computed on the fly from their inputs)
+// instead of being re-read / re-derived per neighbour.  That turns K2 + K3 into ONE kernel:
+//   r' = r - alpha q over tile +- 2H  ->  t = G^T r' over tile +- H  ->  s = G t + eps r'
+// so t never goes to HBM and G is streamed once per iteration instead of twice.  Every value is
+// computed with the same roundings and summation order as the unstaged kernels (bit-identical
+// results); rows outside the tile's system stage as 0 and are never selected by the masks.
+__device__ __forceinline__ void sys_bounds(const Dev& D, int sys, long long& s0, long long& s1) {
+  s0 = D.blk_r0[D.sys_blk0[sys]];
+  s1 = D.sys_r1[sys];
+}
+
+// numpy-order row of A / G with the neighbour values taken from shared memory (xs[li + off]).
+template <int FMT, int ND>
+__device__ __forceinline__ double dia_row_sm(const Dia& dd, const double* const* Vd, int i, int li,
+                                             unsigned int m, const double* xs) {
+  constexpr int NA = ND > 0 ? ND : 1;
+  double a[NA], p[NA];
+#pragma unroll
+  for (int d = 0; d < ND; ++d)
+    a[d] = (FMT == 2 && dd.off[d] > 0) ? __ldg(Vd[dd.mir[d]] + i + dd.off[d]) : __ldg(Vd[d] + i);
+#pragma unroll
+  for (int d = 0; d < ND; ++d) p[d] = mul(a[d], xs[li + dd.off[d]]);
+  return combine_numpy<NA>(p, m);
+}
+
+// Clamp a neighbour row into the tile's system: staged loads are issued unconditionally (all of
+// a thread's loads in flight at once) and the out-of-system values are replaced by 0 afterwards.
+__device__ __forceinline__ long long clampr(long long j, long long s0, long long s1) {
+  return j < s0 ? s0 : (j >= s1 ? s1 - 1 : j);
+}
+
+// K1 with d' staged: d'[j] = s[j] + beta d[j] for j in tile +- H, then q = A d'.
+// NH = ceil(H / PR) fixes the trip counts of the staging loops.
+template <int FMT, int ND, int NH>
+__global__ void __launch_bounds__(PR, 6) k_iter1_st(Dev D, int par) {
+  extern __shared__ double sm[];
+  __shared__ double red[PR / 32];
+  __shared__ int flag;
+  int sys; long long r0, r1, s0, s1;
+  block_rows(D, sys, r0, r1);
+  const int status = D.st[sys].status;
+  if (status == ST_DONE) return;
+  sys_bounds(D, sys, s0, s1);
+  const bool run = status == ST_RUN;
+  const bool fresh = run ? (D.st[sys].flags & FL_FRESH) != 0 : true;
+  const double beta = D.st[sys].beta;
+  const double* dc = par ? D.d1 : D.d0;
+  double* dn = par ? D.d0 : D.d1;
+  double* rc = par ? D.r1 : D.r0;
+  const int H = D.dia.halo;
+  const long long lo = r0 - H;
+  double pdq = 0.0, prr = 0.0;
+  if (run) {
+    constexpr int NJ = kRpt + 2 * NH;
+    const int span = (int)(r1 - r0) + 2 * H;
+    double sv[NJ], dv[NJ];
+#pragma unroll
+    for (int k = 0; k < NJ; ++k) {
+      const long long jc = clampr(lo + k * PR + threadIdx.x, s0, s1);
+      sv[k] = __ldg(D.s + jc);
+      dv[k] = __ldg(dc + jc);
+    }
+#pragma unroll
+    for (int k = 0; k < NJ; ++k) {
+      const int lj = k * PR + threadIdx.x;
+      if (lj < span) {
+        const long long j = lo + lj;
+        double v = 0.0;
+        if (j >= s0 && j < s1) {
+          v = add(sv[k], mul(beta, dv[k]));
+          if (j >= r0 && j < r1) dn[j] = v;
+        }
+        sm[lj] = v;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int rr = 0; rr < kRpt; ++rr) {
+      const long long i = r0 + (long long)rr * PR + threadIdx.x;
+      if (i >= r1) continue;
+      const int li = (int)(i - lo);
+      const double qi = dia_row_sm<FMT, ND>(D.dia, D.dia.av, (int)i, li, D.dia.mask[i], sm);
+      D.q[i] = qi;
+      pdq += mul(sm[li], qi);
+    }
+  }
+  if (fresh) {
+#pragma unroll
+    for (int rr = 0; rr < kRpt; ++rr) {
+      const long long i = r0 + (long long)rr * PR + threadIdx.x;
+      if (i >= r1) continue;
+      const unsigned int m = D.dia.mask[i];
+      const double ax = FMT == 2 ? dia_row_numpy_sym<ND, 0>(D.dia, D.dia.av, (int)i, m, XF{D.x, nullptr, 0.0})
+                                 : dia_row_numpy<ND, 0>(D.dia, D.dia.av, (int)i, m, XF{D.x, nullptr, 0.0});
+      const double rf = sub(D.b[i], ax);
+      if (run) rc[i] = rf;
+      prr += mul(rf, rf);
+    }
+  }
+  if (arrive(D, sys, pdq, prr, red, &flag)) {
+    const double dq = gather_partials(D, sys, 0, red);
+    const double rrf = gather_partials(D, sys, 1, red);
+    if (threadIdx.x == 0) fin_k1(D, sys, run, dq, rrf);
+  }
+}
+
+// K2 + K3 fused (learned preconditioner, non-refresh iterations).
+//   sr[j - (r0-2H)] = r'[j] = r[j] - alpha q[j]   j in tile +- 2H
+//   st[j - (r0-H)]  = t[j]  = (G^T r')[j]          j in tile +- H
+//   s[i] = G t + eps r'                             own rows;  partials ||r'||^2, r'.s
+template <int ND, int NH>
+__global__ void __launch_bounds__(PR, 5) k_iter23_st(Dev D, int par) {
+  extern __shared__ double sm[];
+  __shared__ double red[PR / 32];
+  __shared__ int flag;
+  int sys; long long r0, r1, s0, s1;
+  block_rows(D, sys, r0, r1);
+  if (D.st[sys].status != ST_RUN) return;
+  sys_bounds(D, sys, s0, s1);
+  const double alpha = D.st[sys].alpha;
+  const double eps = D.ctl->eps;
+  const double* dn = par ? D.d0 : D.d1;
+  const double* rc = par ? D.r1 : D.r0;
+  double* rn = par ? D.r0 : D.r1;
+  const int H = D.dia.halo;
+  const int T = (int)(r1 - r0);
+  double* sr = sm;                      // T + 4H
+  double* st = sm + T + 4 * H;          // T + 2H
+  const long long lo2 = r0 - 2 * H, lo1 = r0 - H;
+  // halo rows of r' (below and above the tile): loads first
+  constexpr int NK = 4 * NH;
+  double hr[NK], hq[NK];
+#pragma unroll
+  for (int k = 0; k < NK; ++k) {
+    const int idx = k * PR + threadIdx.x;
+    const long long j = idx < 2 * H ? lo2 + idx : r1 + (idx - 2 * H);
+    const long long jc = clampr(j, s0, s1);
+    hr[k] = __ldg(rc + jc);
+    hq[k] = __ldg(D.q + jc);
+  }
+#pragma unroll
+  for (int k = 0; k < NK; ++k) {
+    const int idx = k * PR + threadIdx.x;
+    if (idx < 4 * H) {
+      const long long j = idx < 2 * H ? lo2 + idx : r1 + (idx - 2 * H);
+      sr[j - lo2] = (j >= s0 && j < s1) ? sub(hr[k], mul(alpha, hq[k])) : 0.0;
+    }
+  }
+  // own rows: r', x, ||r'||^2 (same per-thread row order as k_iter2)
+  double prr = 0.0, prs = 0.0;
+#pragma unroll
+  for (int rr = 0; rr < kRpt; ++rr) {
+    const long long i = r0 + (long long)rr * PR + threadIdx.x;
+    if (i >= r1) continue;
+    D.x[i] = add(D.x[i], mul(alpha, dn[i]));
+    const double rni = sub(rc[i], mul(alpha, D.q[i]));
+    rn[i] = rni;
+    sr[i - lo2] = rni;
+    prr += mul(rni, rni);
+  }
+  __syncthreads();
+  // t = G^T r' over tile +- H (add.at order; G^T row j on diagonal d = G's mirror at j + off),
+  // two rows per thread per batch with all their loads in flight
+  constexpr int NJ = kRpt + 2 * NH;
+  const int span = T + 2 * H;
+#pragma unroll
+  for (int kb = 0; kb < NJ; kb += 2) {
+    double a[2][ND];
+    unsigned int m[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const long long jc = clampr(lo1 + (kb + u) * PR + threadIdx.x, s0, s1);
+      m[u] = D.dia.mask[jc];
+#pragma unroll
+      for (int d = 0; d < ND; ++d) a[u][d] = __ldg(D.dia.gv[D.dia.mir[d]] + jc + D.dia.off[d]);
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int lj1 = (kb + u) * PR + threadIdx.x;
+      if (kb + u < NJ && lj1 < span) {
+        const long long j = lo1 + lj1;
+        double v = 0.0;
+        if (j >= s0 && j < s1) {
+          const int lj = lj1 + H;  // index of row j in sr
+#pragma unroll
+          for (int d = 0; d < ND; ++d)
+            if (m[u] & (1u << d)) v = add(v, mul(a[u][d], sr[lj + D.dia.off[d]]));
+        }
+        st[lj1] = v;
+      }
+    }
+  }
+  __syncthreads();
+  // s = G t + eps r'
+#pragma unroll
+  for (int rr = 0; rr < kRpt; ++rr) {
+    const long long i = r0 + (long long)rr * PR + threadIdx.x;
+    if (i >= r1) continue;
+    const double y = dia_row_sm<1, ND>(D.dia, D.dia.gv, (int)i, (int)(i - lo1), D.dia.mask[i], st);
+    const double rni = sr[i - lo2];
+    const double si = add(y, mul(eps, rni));
+    D.s[i] = si;
+    prs += mul(rni, si);
+  }
+  if (arrive(D, sys, prr, prs, red, &flag)) {
+    const double rr = gather_partials(D, sys, 0, red);
+    const double rs = gather_partials(D, sys, 1, red);
+    if (threadIdx.x == 0) {
+      D.st[sys].rr = rr;
+      fin_k3(D, sys, rs, 0);
+    }
+  }
+}
+
+
+// ------------------------------------------------------------------ sliding-window K2 + K3
+// The same fused K2 + K3 as k_iter23_st, organised as a stream instead of independent tiles: a
+// CTA walks a long RANGE of rows (kSwRange, inside one system) in chunks of kSwC rows.  The
+// bulk-copy engine (cp.async.bulk + mbarrier) streams each chunk's r, q, G diagonals and mask
+// (the "lead" chunk, 2*NH chunks ahead of the output) and the x, d rows of the output chunk
+// into a ring of NS shared-memory slots, kSwP - 1 chunks ahead of the compute.  Per step k:
+//   A  r' = r - alpha q              lead chunk k         -> r' ring  (own rows: r' to HBM, ||r'||^2)
+//   B  t  = G^T r'                   chunk k - NH         -> t ring   (G, r' of chunks k-2NH .. k)
+//   C  s  = G t + eps r', x += alpha d   chunk k - 2NH    -> HBM      (r'.s)
+// so every byte of A's / G's / the vectors' rows is read from HBM once per iteration (plus the
+// 4*NH-chunk halo at the two ends of a range), with no per-thread load latency on the critical
+// path.  Results are bit-identical to k_iter2 + k_iter3 except the order of the two dot
+// products' partial sums (per range instead of per tile).
+template <int ND, int NH>
+struct Sw23 {
+  static constexpr int NS = kSwP + 2 * NH;                    // stage slots
+  static constexpr int RS = 2 * NH + 2;                       // r' / t ring chunks
+  static constexpr int SLOT_D = (4 + ND) * kSwC;              // r q x d G[ND] (doubles)
+  static constexpr size_t SLOT_B = (size_t)SLOT_D * 8 + kSwC; // + mask bytes
+  static constexpr size_t SMEM = NS * SLOT_B + (size_t)2 * RS * kSwC * 8;
+};
+
+template <int ND, int NH>
+__global__ void __launch_bounds__(PR, 1) k_iter23_sw(Dev D, int par) {
+  using G = Sw23<ND, NH>;
+  constexpr int C = kSwC, NS = G::NS, RS = G::RS;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  __shared__ __align__(8) uint64_t bars[NS];
+  __shared__ double red[PR / 32];
+  __shared__ int flag;
+  const int b = blockIdx.x, tid = threadIdx.x;
+  const int sys = D.rng_sys[b];
+  if (D.st[sys].status != ST_RUN) return;
+  long long s0, s1;
+  sys_bounds(D, sys, s0, s1);
+  const long long R0 = D.rng_r0[b];
+  const long long R1 = R0 + kSwRange < s1 ? R0 + kSwRange : s1;
+  const double alpha = D.st[sys].alpha;
+  const double eps = D.ctl->eps;
+  const double* dn = par ? D.d0 : D.d1;
+  const double* rc = par ? D.r1 : D.r0;
+  double* rn = par ? D.r0 : D.r1;
+  double* rp = reinterpret_cast<double*>(smraw + NS * G::SLOT_B);  // [RS][C]
+  double* tr = rp + RS * C;                                         // [RS][C]
+  auto slot = [&](int sl) { return reinterpret_cast<double*>(smraw + sl * G::SLOT_B); };
+  auto smask = [&](int sl) { return smraw + sl * G::SLOT_B + (size_t)G::SLOT_D * 8; };
+  // chunk k covers rows LB + k*C .. ; LB 16-row aligned so every bulk copy is 16-byte aligned
+  const long long LB = (R0 & ~15LL) - 2LL * NH * C;
+  const int m1 = (int)((R1 - LB + C - 1) / C) - 1;  // last output chunk
+  const int K = m1 + 2 * NH + 1;                     // steps
+  auto issue = [&](int k) {
+    const int sl = k % NS;
+    double* p = slot(sl);
+    const long long row = LB + (long long)k * C;
+    const bool own = k >= 4 * NH;
+    const uint32_t bytes = (uint32_t)((2 + ND + (own ? 2 : 0)) * C * 8 + C);
+    mbar_arrive_expect_tx(&bars[sl], bytes);
+    bulk_g2s(p, rc + row, C * 8, &bars[sl]);
+    bulk_g2s(p + C, D.q + row, C * 8, &bars[sl]);
+#pragma unroll
+    for (int d = 0; d < ND; ++d) bulk_g2s(p + (4 + d) * C, D.dia.gv[d] + row, C * 8, &bars[sl]);
+    bulk_g2s(smask(sl), D.dia.mask + row, C, &bars[sl]);
+    if (own) {
+      const long long ro = row - 2LL * NH * C;
+      bulk_g2s(p + 2 * C, D.x + ro, C * 8, &bars[sl]);
+      bulk_g2s(p + 3 * C, dn + ro, C * 8, &bars[sl]);
+    }
+  };
+  if (tid == 0) {
+#pragma unroll
+    for (int sl = 0; sl < NS; ++sl) mbar_init(&bars[sl], 1);
+    mbar_init_fence();
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int k = 0; k < kSwP - 1 && k < K; ++k) issue(k);
+  double prr = 0.0, prs = 0.0;
+  for (int k = 0; k < K; ++k) {
+    const int sl = k % NS;
+    mbar_wait(&bars[sl], (uint32_t)((k / NS) & 1));
+    {  // A: r' of the lead chunk
+      const double* p = slot(sl);
+      const long long j = LB + (long long)k * C + tid;
+      double v = 0.0;
+      if (j >= s0 && j < s1) v = sub(p[tid], mul(alpha, p[C + tid]));
+      if (j >= R0 && j < R1) {
+        rn[j] = v;
+        prr += mul(v, v);
+      }
+      rp[(k % RS) * C + tid] = v;
+    }
+    __syncthreads();
+    if (tid == 0 && k + kSwP - 1 < K) issue(k + kSwP - 1);
+    const int u = k - NH;
+    if (u >= NH) {  // B: t of chunk u (add.at order over G's mirror diagonals)
+      const long long j = LB + (long long)u * C + tid;
+      double v = 0.0;
+      if (j >= s0 && j < s1) {
+        const unsigned int m = smask(u % NS)[tid];
+        const int lj = u * C + tid;
+        double a[ND], x[ND];
+#pragma unroll
+        for (int d = 0; d < ND; ++d) {
+          const int lr = lj + D.dia.off[d];
+          const int cu = lr / C, of = lr % C;
+          a[d] = slot(cu % NS)[(4 + D.dia.mir[d]) * C + of];
+          x[d] = rp[(cu % RS) * C + of];
+        }
+#pragma unroll
+        for (int d = 0; d < ND; ++d)
+          if (m & (1u << d)) v = add(v, mul(a[d], x[d]));
+      }
+      tr[(u % RS) * C + tid] = v;
+    }
+    __syncthreads();
+    const int mm = k - 2 * NH;
+    if (mm >= 2 * NH) {  // C: s and x of chunk mm
+      const long long i = LB + (long long)mm * C + tid;
+      if (i >= R0 && i < R1) {
+        const double* px = slot(sl);  // x, d of chunk mm travel with lead chunk k
+        D.x[i] = add(px[2 * C + tid], mul(alpha, px[3 * C + tid]));
+        const int sm = mm % NS;
+        const unsigned int m = smask(sm)[tid];
+        const int li = mm * C + tid;
+        double p[ND];
+#pragma unroll
+        for (int d = 0; d < ND; ++d) {
+          const int lr = li + D.dia.off[d];
+          p[d] = mul(slot(sm)[(4 + d) * C + tid], tr[((lr / C) % RS) * C + lr % C]);
+        }
+        const double y = combine_numpy<ND>(p, m);
+        const double rni = rp[(mm % RS) * C + tid];
+        const double si = add(y, mul(eps, rni));
+        D.s[i] = si;
+        prs += mul(rni, si);
+      }
+    }
+  }
+  if (arrive(D, D.sys_rng0, sys, prr, prs, red, &flag)) {
+    const double rr = gather_partials(D, D.sys_rng0, sys, 0, red);
+    const double rs = gather_partials(D, D.sys_rng0, sys, 1, red);
+    if (threadIdx.x == 0) {
+      D.st[sys].rr = rr;
+      fin_k3(D, sys, rs, 0);
+    }
+  }
+}
+
 }  // namespace sg
 
 using namespace sg;
@@ -662,6 +1046,9 @@ struct sg_pcg {
   int chunk = 0;
   int64_t period = 0;
   int short_rows = 0;
+  int nrng = 0;       // sliding-window ranges
+  int k23 = 1;        // fused K2+K3 variant: 1 = sliding window (k_iter23_sw), 0 = tiles (k_iter23_st)
+  int staged = 0;     // DIA with a small halo: halo-staged K1 and fused K2+K3 (k_iter1_st, k_iter23_st)
   // DIA format (0 = CSR)
   int dia_nd = 0;
   int a_sym = 0;      // DIA: A bitwise symmetric on its pattern -> lower-half reads only
@@ -732,8 +1119,33 @@ int launch_iteration(sg_pcg* h, cudaStream_t s, int par, bool refresh, cudaEvent
       k_snapshot<<<1, 1, 0, s>>>(h->ctl); ++k;
       SG_CUDA(cudaEventRecordWithFlags(ev[0], s, cudaEventRecordExternal));
     }
-    k_iter1<PRE, FMT, ND, SH><<<g, PR, 0, s>>>(h->D, par); ++k;
+    constexpr int FS = FMT >= 1 ? FMT : 1;
+    constexpr int NS = ND > 0 ? ND : 1;
+    const bool st = FMT >= 1 && h->staged;
+    const size_t tile = (size_t)PR * kRpt, H = (size_t)h->D.dia.halo;
+    if (st && H <= PR) k_iter1_st<FS, NS, 1><<<g, PR, (tile + 2 * H) * sizeof(double), s>>>(h->D, par);
+    else if (st) k_iter1_st<FS, NS, 2><<<g, PR, (tile + 2 * H) * sizeof(double), s>>>(h->D, par);
+    else k_iter1<PRE, FMT, ND, SH><<<g, PR, 0, s>>>(h->D, par);
+    ++k;
     if (ev) SG_CUDA(cudaEventRecordWithFlags(ev[1], s, cudaEventRecordExternal));
+    if (st && !refresh && PRE == SG_PRECOND_LEARNED) {  // K2 + K3 fused
+      const unsigned gr = (unsigned)h->nrng;
+      if (h->k23 == 1) {
+        if (H <= PR) k_iter23_sw<NS, 1><<<gr, PR, Sw23<NS, 1>::SMEM, s>>>(h->D, par);
+        else k_iter23_sw<NS, 2><<<gr, PR, Sw23<NS, 2>::SMEM, s>>>(h->D, par);
+      } else {
+        if (H <= PR) k_iter23_st<NS, 1><<<g, PR, (2 * tile + 6 * H) * sizeof(double), s>>>(h->D, par);
+        else k_iter23_st<NS, 2><<<g, PR, (2 * tile + 6 * H) * sizeof(double), s>>>(h->D, par);
+      }
+      ++k;
+      if (ev) {
+        SG_CUDA(cudaEventRecordWithFlags(ev[2], s, cudaEventRecordExternal));
+        SG_CUDA(cudaEventRecordWithFlags(ev[3], s, cudaEventRecordExternal));
+      }
+      SG_LAUNCH_CHECK("pcg iteration");
+      *nk += k;
+      return SG_OK;
+    }
     if (!refresh) {
       k_iter2<PRE, FMT, ND, SH><<<g, PR, 0, s>>>(h->D, par); ++k;
     } else {
@@ -864,17 +1276,25 @@ int setup_dia(sg_pcg* h, const int32_t* a_offs, const int32_t* a_cols, const int
     if (it == offs.end()) return SG_OK;  // offset set not symmetric
     dia.mir[d] = (int)(it - offs.begin());
   }
-  // guard bands: max |offset| zero rows before and after every diagonal (and every vector)
-  long long guard = 0;
-  for (int d = 0; d < cnt; ++d) guard = std::max<long long>(guard, std::abs((long long)offs[d]));
-  guard = (guard + 31) / 32 * 32;  // keep 256-byte alignment of every diagonal
-  const long long ld = n + 2 * guard;
+  // guard bands: zero rows before and after every diagonal, every vector and the mask, so
+  // neighbour reads never need clamping: max |offset| rows, or the sliding-window kernel's
+  // reach ((2 * ceil(H / kSwC) + 1) chunks + 16-row alignment) when halo staging is on
+  long long halo = 0;
+  for (int d = 0; d < cnt; ++d) halo = std::max<long long>(halo, std::abs((long long)offs[d]));
+  dia.halo = (int)halo;
+  const char* ns = getenv("SG_PCG_NOSTAGE");
+  h->staged = (halo <= kMaxStageHalo && !(ns && ns[0] == '1')) ? 1 : 0;
+  long long guard = halo;
+  if (h->staged) guard = std::max<long long>(guard, (2 * ((halo + kSwC - 1) / kSwC) + 1) * kSwC + 16);
+  guard = (guard + 31) / 32 * 32;                // 256-byte alignment of every row-0 pointer
+  const long long ld = (n + 2 * guard + 31) / 32 * 32;
   const size_t vbytes = (size_t)cnt * ld * sizeof(double);
-  SG_CUDA(cudaMalloc(&h->dia_mem, 2 * vbytes + n + 64));
-  SG_CUDA(cudaMemsetAsync(h->dia_mem, 0, 2 * vbytes + n + 64, s));
+  const size_t mbytes = (size_t)(n + 2 * guard + 64);
+  SG_CUDA(cudaMalloc(&h->dia_mem, 2 * vbytes + mbytes));
+  SG_CUDA(cudaMemsetAsync(h->dia_mem, 0, 2 * vbytes + mbytes, s));
   h->dia_a = reinterpret_cast<double*>(h->dia_mem) + guard;
   h->dia_g = reinterpret_cast<double*>(reinterpret_cast<char*>(h->dia_mem) + vbytes) + guard;
-  h->dia_mask = reinterpret_cast<unsigned char*>(h->dia_mem) + 2 * vbytes;
+  h->dia_mask = reinterpret_cast<unsigned char*>(h->dia_mem) + 2 * vbytes + guard;
   dia.ld = ld;
   dia.a = h->dia_a;
   dia.g = h->dia_g;
@@ -948,9 +1368,22 @@ extern "C" int sg_pcg_create(sg_pcg** out, int32_t n_systems, const int64_t* sys
   }
   sys_blk0.push_back((int)blk_r0.size());
   h->nblk = (int)blk_r0.size();
+  // sliding-window ranges (halo-staged DIA)
+  std::vector<long long> rng_r0;
+  std::vector<int> rng_sys, sys_rng0;
+  for (int k = 0; k < n_systems; ++k) {
+    sys_rng0.push_back((int)rng_r0.size());
+    for (int64_t r = h->sys_start[k]; r < h->sys_start[k + 1]; r += kSwRange) {
+      rng_r0.push_back(r);
+      rng_sys.push_back(k);
+    }
+  }
+  sys_rng0.push_back((int)rng_r0.size());
+  h->nrng = (int)rng_r0.size();
   const int64_t n = h->n, S = n_systems, nb = h->nblk > 0 ? h->nblk : 1;
   Carve c(nullptr);
   c.take<long long>(nb); c.take<int>(nb); c.take<int>(S + 1); c.take<long long>(S);
+  c.take<long long>(h->nrng); c.take<int>(h->nrng); c.take<int>(S + 1);
   const int64_t gv = h->guard;  // zero guard rows around every vector (DIA neighbour reads)
   for (int v = 0; v < 9; ++v) c.take<double>(n + 2 * gv + 2);
   c.take<double>(2 * nb); c.take<unsigned int>(S); c.take<SysState>(S); c.take<Ctl>(1);
@@ -961,6 +1394,9 @@ extern "C" int sg_pcg_create(sg_pcg** out, int32_t n_systems, const int64_t* sys
   int* d_blk_sys = m.take<int>(nb);
   int* d_sys_blk0 = m.take<int>(S + 1);
   long long* d_sys_r1 = m.take<long long>(S);
+  long long* d_rng_r0 = m.take<long long>(h->nrng);
+  int* d_rng_sys = m.take<int>(h->nrng);
+  int* d_sys_rng0 = m.take<int>(S + 1);
   double* vec[9];
   for (int v = 0; v < 9; ++v) vec[v] = m.take<double>(n + 2 * gv + 2) + gv;
   double* part = m.take<double>(2 * nb);
@@ -974,10 +1410,14 @@ extern "C" int sg_pcg_create(sg_pcg** out, int32_t n_systems, const int64_t* sys
   }
   SG_CUDA(cudaMemcpyAsync(d_sys_blk0, sys_blk0.data(), sys_blk0.size() * sizeof(int), cudaMemcpyHostToDevice, s));
   SG_CUDA(cudaMemcpyAsync(d_sys_r1, sys_r1.data(), sys_r1.size() * sizeof(long long), cudaMemcpyHostToDevice, s));
+  SG_CUDA(cudaMemcpyAsync(d_rng_r0, rng_r0.data(), rng_r0.size() * sizeof(long long), cudaMemcpyHostToDevice, s));
+  SG_CUDA(cudaMemcpyAsync(d_rng_sys, rng_sys.data(), rng_sys.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+  SG_CUDA(cudaMemcpyAsync(d_sys_rng0, sys_rng0.data(), sys_rng0.size() * sizeof(int), cudaMemcpyHostToDevice, s));
   SG_CUDA(cudaMemsetAsync(counter, 0, S * sizeof(unsigned int), s));
   Dev& D = h->D;
   D.blk_r0 = d_blk_r0; D.blk_sys = d_blk_sys; D.sys_blk0 = d_sys_blk0; D.sys_r1 = d_sys_r1;
   D.tile = tile;
+  D.rng_r0 = d_rng_r0; D.rng_sys = d_rng_sys; D.sys_rng0 = d_sys_rng0;
   D.a_offs = a_offs; D.a_cols = a_cols; D.a_vals = a_vals;
   D.g_offs = g_offs; D.g_cols = g_cols; D.g_vals = g_vals;
   D.gt_offs = gt_offs; D.gt_cols = gt_cols; D.gt_vals = gt_vals;
@@ -988,6 +1428,17 @@ extern "C" int sg_pcg_create(sg_pcg** out, int32_t n_systems, const int64_t* sys
   SG_CUDA(cudaHostAlloc(&h->pinned_active, 2 * sizeof(unsigned int), cudaHostAllocDefault));
   SG_CUDA(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
   for (int k = 0; k < 4; ++k) SG_CUDA(cudaEventCreate(&h->ev[k]));
+  if (h->staged) {
+    const char* kv = getenv("SG_PCG_K23");
+    h->k23 = (kv && kv[0] == 't') ? 0 : 1;
+    // the sliding-window kernels need more than the default 48 KB of dynamic shared memory
+    SG_CUDA(cudaFuncSetAttribute(k_iter23_sw<5, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sw23<5, 1>::SMEM));
+    SG_CUDA(cudaFuncSetAttribute(k_iter23_sw<5, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sw23<5, 2>::SMEM));
+    SG_CUDA(cudaFuncSetAttribute(k_iter23_sw<7, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sw23<7, 1>::SMEM));
+    SG_CUDA(cudaFuncSetAttribute(k_iter23_sw<7, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sw23<7, 2>::SMEM));
+    SG_CUDA(cudaFuncSetAttribute(k_iter23_sw<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sw23<8, 1>::SMEM));
+    SG_CUDA(cudaFuncSetAttribute(k_iter23_sw<8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sw23<8, 2>::SMEM));
+  }
   SG_CUDA(cudaStreamSynchronize(s));
   *out = h;
   return SG_OK;
@@ -1174,6 +1625,7 @@ extern "C" int sg_pcg_stats(sg_pcg* h, int64_t* kernels_host, int64_t* chunks_ho
     prof_host[4] = h->prof_samples;
     prof_host[5] = h->dia_nd;
     prof_host[6] = h->a_sym;
+    prof_host[7] = h->staged && h->pre == SG_PRECOND_LEARNED ? 1.0 : 0.0;
   }
   if (reset) {
     h->kernels = h->chunks = 0;

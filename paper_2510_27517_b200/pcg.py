@@ -118,10 +118,11 @@ class PcgHandle:
         L.check(L.lib().sg_pcg_set_profile(self._h, 1 if on else 0))
 
     def stats(self, reset: bool = False):
-        """(kernels launched, graphs launched, [K1 ms, K2 ms, K3 ms, active-sum, samples, ndiag])
-        — ndiag > 0 when the handle runs the diagonal-major (DIA) format, 0 for CSR."""
+        """(kernels launched, graphs launched, [K1 ms, K2 ms, K3 ms, active-sum, samples, ndiag,
+        a_sym, fused]) — ndiag > 0 when the handle runs the diagonal-major (DIA) format, 0 for
+        CSR; fused = 1 when K2 + K3 run as one halo-staged kernel (K2 ms covers both)."""
         k, c = C.c_int64(0), C.c_int64(0)
-        prof = (C.c_double * 7)()
+        prof = (C.c_double * 8)()
         L.check(L.lib().sg_pcg_stats(self._h, C.byref(k), C.byref(c), prof, 1 if reset else 0))
         return int(k.value), int(c.value), list(prof)
 
