@@ -42,7 +42,7 @@ def parse():
     p.add_argument("--systems-per-gpu", type=int, default=128)
     p.add_argument("--nx", type=int, default=256)
     p.add_argument("--rtol", type=float, default=1e-6)
-    p.add_argument("--e2e-steps", type=int, default=2)
+    p.add_argument("--e2e-steps", type=int, default=5)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-workers", type=int, default=0)
@@ -144,7 +144,7 @@ def run_ours(a, rank, world, local):
     import torch.distributed as dist
 
     from paper_2510_27517_b200 import _lib
-    from paper_2510_27517_b200.batch import BatchSolver, SystemBatch, solve_batch
+    from paper_2510_27517_b200.batch import BatchSolver, SystemBatch, solve_batch, solve_batch_stream
     from paper_2510_27517_b200.datasets import ProblemMeta
     from paper_2510_27517_b200.dist import gather_stats, local_systems, max_over_ranks
     from paper_2510_27517_b200.gnn import load_checkpoint
@@ -290,16 +290,19 @@ def run_ours(a, rank, world, local):
             sum(b.nbytes for b in bs) + sum(m.coeff.nbytes for m in metas)
         d2h = sum(b.nbytes for b in bs) + 8 * 2 * S
         reps = solve_batch(As, bs, model, metas, cfg)  # warm-up (allocations, graphs)
+        for reps in solve_batch_stream([(As, bs, metas)] * 2, model, cfg):  # staging areas, host ring
+            pass
         barrier()
         t0 = time.perf_counter()
-        for _ in range(a.e2e_steps):
-            reps = solve_batch(As, bs, model, metas, cfg)
+        for reps in solve_batch_stream([(As, bs, metas)] * a.e2e_steps, model, cfg):
+            pass  # every batch: H2D of all inputs (overlapping the previous solve), solve, D2H of x
         barrier()
         e2e_ms = max_over_ranks(1000.0 * (time.perf_counter() - t0) / a.e2e_steps, dev)
         assert [r.k for r in reps] == ks[-1], "e2e path must reproduce the device path"
         e2e = {"value": world * S / (e2e_ms / 1000.0), "unit": "solves/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms,
-               "api": "paper_2510_27517_b200.solve_batch(host int64 CSR, f64 values/coeff/rhs) -> host x"}
+               "api": "paper_2510_27517_b200.solve_batch_stream(batches of host int64 CSR, f64 values/coeff/rhs) "
+                      "-> host x; the next batch's H2D overlaps the current solve"}
 
     # ---- CPU baseline (rank 0, N = 1 only), bounded sample
     cpu = None

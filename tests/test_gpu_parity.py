@@ -417,3 +417,21 @@ def test_rowpart_single_rank_matches_pcg_solve():
     assert conv and rep.converged and _k_close(k, rep.k)
     res = np.linalg.norm(b - O.spmv(A.row_offsets, A.col_indices, A.values, x))
     assert res <= 1e-8
+
+
+def test_solve_batch_stream_matches_solve_batch():
+    """Pipelined batches (next upload overlapping the current solve) == one-shot solve_batch."""
+    import os
+    m = P.load_checkpoint(os.path.join(os.path.dirname(__file__), "golden", "trained_heat16.spaignn"))
+    systems = [P.gen_poisson2d(20, 20, coeff_seed=s) for s in range(4)]
+    As, metas = [A for A, _ in systems], [meta for _, meta in systems]
+    cfg = P.SolveConfig(rtol=1e-8)
+    batches = [(As, [P.gen_rhs(meta, 100 * j + s) for s, meta in enumerate(metas)], metas) for j in range(3)]
+    want = [P.solve_batch(A_, b_, m, metas=m_, cfg=cfg) for A_, b_, m_ in batches]
+    got = [[(r.k, r.converged, r.x.copy()) for r in reps]
+           for reps in P.solve_batch_stream(batches, m, cfg, depth=2)]
+    assert len(got) == 3
+    for w, g_ in zip(want, got):
+        for rw, (k, conv, x) in zip(w, g_):
+            assert rw.k == k and rw.converged == conv
+            assert np.array_equal(rw.x, x)
