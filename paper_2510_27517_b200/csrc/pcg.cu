@@ -41,8 +41,6 @@ constexpr int PCAP = 2048; // staged nonzeros per tile (8 per row on average)
 constexpr int MAXD = 8;    // DIA: max diagonals
 constexpr int kMaxStageHalo = 512;  // DIA halo staging: shared memory <= 48 KB per CTA
 constexpr int kSwC = PR;              // sliding window: rows per chunk (one per thread)
-constexpr int kSwP = 3;               // sliding window: chunks in flight (bulk-copy prefetch depth)
-constexpr long long kSwRange = 8192;  // sliding window: rows per CTA range
 constexpr int kRpt = 4;    // DIA: rows per thread (tile = PR * kRpt rows; amortises the
                            // per-tile reduction and keeps more independent loads in flight)
 
@@ -88,7 +86,8 @@ struct Dev {
   const int* sys_blk0;
   const long long* sys_r1;
   int tile;  // rows per tile: PR (CSR) or PR * kRpt (DIA)
-  // sliding-window range table (halo-staged DIA): ranges of <= kSwRange rows inside one system
+  // sliding-window range table (halo-staged DIA): ranges of <= rng_len rows inside one system
+  long long rng_len;
   const long long* rng_r0;
   const int* rng_sys;
   const int* sys_rng0;
@@ -874,32 +873,41 @@ __global__ void __launch_bounds__(PR, 5) k_iter23_st(Dev D, int par) {
 
 // ------------------------------------------------------------------ sliding-window K2 + K3
 // The same fused K2 + K3 as k_iter23_st, organised as a stream instead of independent tiles: a
-// CTA walks a long RANGE of rows (kSwRange, inside one system) in chunks of kSwC rows.  The
-// bulk-copy engine (cp.async.bulk + mbarrier) streams each chunk's r, q, G diagonals and mask
-// (the "lead" chunk, 2*NH chunks ahead of the output) and the x, d rows of the output chunk
-// into a ring of NS shared-memory slots, kSwP - 1 chunks ahead of the compute.  Per step k:
-//   A  r' = r - alpha q              lead chunk k         -> r' ring  (own rows: r' to HBM, ||r'||^2)
-//   B  t  = G^T r'                   chunk k - NH         -> t ring   (G, r' of chunks k-2NH .. k)
-//   C  s  = G t + eps r', x += alpha d   chunk k - 2NH    -> HBM      (r'.s)
-// so every byte of A's / G's / the vectors' rows is read from HBM once per iteration (plus the
-// 4*NH-chunk halo at the two ends of a range), with no per-thread load latency on the critical
-// path.  Results are bit-identical to k_iter2 + k_iter3 except the order of the two dot
+// CTA walks a RANGE of rows (inside one system) in chunks of C = kSwC rows.  The bulk-copy
+// engine (cp.async.bulk + mbarrier) streams each chunk's r, q, G diagonals and mask (the "lead"
+// chunk, 2*NH chunks ahead of the output) plus the x, d rows of the output chunk into shared
+// memory one chunk ahead of the compute.  Per step k:
+//   A  r' = r - alpha q             lead chunk k        (own rows: r' to HBM, ||r'||^2)
+//   B  t  = G^T r'                  chunk k - NH        (G, r' of chunks k-2NH .. k)
+//   C  s  = G t + eps r', x += alpha d   chunk k - 2NH  (r'.s)
+// G, the mask, r' and t live in power-of-two RING-row rings indexed by (row - LB) & (RING-1), so
+// a neighbour access is one add, one and, one shared load; the diagonal set is symmetric and
+// sorted, so the mirror of diagonal d is ND-1-d at compile time.  Every byte of A's / G's / the
+// vectors' rows is read from HBM once per iteration (plus a 4*NH-chunk halo at the two ends of a
+// range).  Results are bit-identical to k_iter2 + k_iter3 except for the order of the two dot
 // products' partial sums (per range instead of per tile).
+__host__ __device__ constexpr int pow2ceil(int v) {
+  int p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+
 template <int ND, int NH>
 struct Sw23 {
-  static constexpr int NS = kSwP + 2 * NH;                    // stage slots
-  static constexpr int RS = 2 * NH + 2;                       // r' / t ring chunks
-  static constexpr int SLOT_D = (4 + ND) * kSwC;              // r q x d G[ND] (doubles)
-  static constexpr size_t SLOT_B = (size_t)SLOT_D * 8 + kSwC; // + mask bytes
-  static constexpr size_t SMEM = NS * SLOT_B + (size_t)2 * RS * kSwC * 8;
+  static constexpr int C = kSwC;
+  static constexpr int P = 2;                            // chunks in flight (incl. the current one)
+  static constexpr int RING = pow2ceil((P + 2 * NH) * C);  // ring rows (G, mask, r', t)
+  static constexpr int RM = RING - 1;
+  // bytes: G [ND][RING] | r' [RING] | t [RING] | staging [P][4][C] (r q x d) | mask [RING]
+  static constexpr size_t SMEM = (size_t)(ND + 2) * RING * 8 + (size_t)P * 4 * C * 8 + RING;
 };
 
 template <int ND, int NH>
 __global__ void __launch_bounds__(PR, 1) k_iter23_sw(Dev D, int par) {
   using G = Sw23<ND, NH>;
-  constexpr int C = kSwC, NS = G::NS, RS = G::RS;
+  constexpr int C = G::C, P = G::P, RING = G::RING, RM = G::RM;
   extern __shared__ __align__(128) unsigned char smraw[];
-  __shared__ __align__(8) uint64_t bars[NS];
+  __shared__ __align__(8) uint64_t bars[P];
   __shared__ double red[PR / 32];
   __shared__ int flag;
   const int b = blockIdx.x, tid = threadIdx.x;
@@ -908,102 +916,93 @@ __global__ void __launch_bounds__(PR, 1) k_iter23_sw(Dev D, int par) {
   long long s0, s1;
   sys_bounds(D, sys, s0, s1);
   const long long R0 = D.rng_r0[b];
-  const long long R1 = R0 + kSwRange < s1 ? R0 + kSwRange : s1;
+  const long long R1 = R0 + D.rng_len < s1 ? R0 + D.rng_len : s1;
   const double alpha = D.st[sys].alpha;
   const double eps = D.ctl->eps;
   const double* dn = par ? D.d0 : D.d1;
   const double* rc = par ? D.r1 : D.r0;
   double* rn = par ? D.r0 : D.r1;
-  double* rp = reinterpret_cast<double*>(smraw + NS * G::SLOT_B);  // [RS][C]
-  double* tr = rp + RS * C;                                         // [RS][C]
-  auto slot = [&](int sl) { return reinterpret_cast<double*>(smraw + sl * G::SLOT_B); };
-  auto smask = [&](int sl) { return smraw + sl * G::SLOT_B + (size_t)G::SLOT_D * 8; };
-  // chunk k covers rows LB + k*C .. ; LB 16-row aligned so every bulk copy is 16-byte aligned
+  double* gr = reinterpret_cast<double*>(smraw);  // [ND][RING]
+  double* rp = gr + ND * RING;                      // [RING]
+  double* tr = rp + RING;                           // [RING]
+  double* stg = tr + RING;                          // [P][4][C]
+  unsigned char* mk = reinterpret_cast<unsigned char*>(stg + P * 4 * C);  // [RING]
+  // chunk k covers rows LB + k*C ..; LB 16-row aligned so every bulk copy is 16-byte aligned
   const long long LB = (R0 & ~15LL) - 2LL * NH * C;
   const int m1 = (int)((R1 - LB + C - 1) / C) - 1;  // last output chunk
   const int K = m1 + 2 * NH + 1;                     // steps
+  int off[ND];
+#pragma unroll
+  for (int d = 0; d < ND; ++d) off[d] = D.dia.off[d];
   auto issue = [&](int k) {
-    const int sl = k % NS;
-    double* p = slot(sl);
+    const int ss = k % P, gs = (k * C) & RM;
+    double* st = stg + ss * 4 * C;
     const long long row = LB + (long long)k * C;
     const bool own = k >= 4 * NH;
     const uint32_t bytes = (uint32_t)((2 + ND + (own ? 2 : 0)) * C * 8 + C);
-    mbar_arrive_expect_tx(&bars[sl], bytes);
-    bulk_g2s(p, rc + row, C * 8, &bars[sl]);
-    bulk_g2s(p + C, D.q + row, C * 8, &bars[sl]);
+    mbar_arrive_expect_tx(&bars[ss], bytes);
+    bulk_g2s(st, rc + row, C * 8, &bars[ss]);
+    bulk_g2s(st + C, D.q + row, C * 8, &bars[ss]);
 #pragma unroll
-    for (int d = 0; d < ND; ++d) bulk_g2s(p + (4 + d) * C, D.dia.gv[d] + row, C * 8, &bars[sl]);
-    bulk_g2s(smask(sl), D.dia.mask + row, C, &bars[sl]);
+    for (int d = 0; d < ND; ++d) bulk_g2s(gr + d * RING + gs, D.dia.gv[d] + row, C * 8, &bars[ss]);
+    bulk_g2s(mk + gs, D.dia.mask + row, C, &bars[ss]);
     if (own) {
       const long long ro = row - 2LL * NH * C;
-      bulk_g2s(p + 2 * C, D.x + ro, C * 8, &bars[sl]);
-      bulk_g2s(p + 3 * C, dn + ro, C * 8, &bars[sl]);
+      bulk_g2s(st + 2 * C, D.x + ro, C * 8, &bars[ss]);
+      bulk_g2s(st + 3 * C, dn + ro, C * 8, &bars[ss]);
     }
   };
   if (tid == 0) {
 #pragma unroll
-    for (int sl = 0; sl < NS; ++sl) mbar_init(&bars[sl], 1);
+    for (int q = 0; q < P; ++q) mbar_init(&bars[q], 1);
     mbar_init_fence();
   }
   __syncthreads();
-  if (tid == 0)
-    for (int k = 0; k < kSwP - 1 && k < K; ++k) issue(k);
+  if (tid == 0) issue(0);
   double prr = 0.0, prs = 0.0;
   for (int k = 0; k < K; ++k) {
-    const int sl = k % NS;
-    mbar_wait(&bars[sl], (uint32_t)((k / NS) & 1));
+    const double* st = stg + (k % P) * 4 * C;
+    mbar_wait(&bars[k % P], (uint32_t)((k / P) & 1));
     {  // A: r' of the lead chunk
-      const double* p = slot(sl);
       const long long j = LB + (long long)k * C + tid;
-      double v = 0.0;
-      if (j >= s0 && j < s1) v = sub(p[tid], mul(alpha, p[C + tid]));
+      double v = sub(st[tid], mul(alpha, st[C + tid]));
+      v = (j >= s0 && j < s1) ? v : 0.0;
       if (j >= R0 && j < R1) {
         rn[j] = v;
         prr += mul(v, v);
       }
-      rp[(k % RS) * C + tid] = v;
+      rp[(k * C + tid) & RM] = v;
     }
     __syncthreads();
-    if (tid == 0 && k + kSwP - 1 < K) issue(k + kSwP - 1);
+    if (tid == 0 && k + 1 < K) issue(k + 1);
     const int u = k - NH;
     if (u >= NH) {  // B: t of chunk u (add.at order over G's mirror diagonals)
-      const long long j = LB + (long long)u * C + tid;
+      const int lj = u * C + tid;
+      const unsigned int m = mk[lj & RM];
       double v = 0.0;
-      if (j >= s0 && j < s1) {
-        const unsigned int m = smask(u % NS)[tid];
-        const int lj = u * C + tid;
-        double a[ND], x[ND];
 #pragma unroll
-        for (int d = 0; d < ND; ++d) {
-          const int lr = lj + D.dia.off[d];
-          const int cu = lr / C, of = lr % C;
-          a[d] = slot(cu % NS)[(4 + D.dia.mir[d]) * C + of];
-          x[d] = rp[(cu % RS) * C + of];
-        }
-#pragma unroll
-        for (int d = 0; d < ND; ++d)
-          if (m & (1u << d)) v = add(v, mul(a[d], x[d]));
+      for (int d = 0; d < ND; ++d) {
+        const int ix = (lj + off[d]) & RM;
+        const double a = gr[(ND - 1 - d) * RING + ix], x = rp[ix];
+        if (m & (1u << d)) v = add(v, mul(a, x));
       }
-      tr[(u % RS) * C + tid] = v;
+      const long long j = LB + lj;
+      tr[lj & RM] = (j >= s0 && j < s1) ? v : 0.0;
     }
     __syncthreads();
     const int mm = k - 2 * NH;
-    if (mm >= 2 * NH) {  // C: s and x of chunk mm
-      const long long i = LB + (long long)mm * C + tid;
+    if (mm >= 2 * NH) {  // C: s and x of chunk mm (its x, d travelled with lead chunk k)
+      const int li = mm * C + tid;
+      const long long i = LB + li;
       if (i >= R0 && i < R1) {
-        const double* px = slot(sl);  // x, d of chunk mm travel with lead chunk k
-        D.x[i] = add(px[2 * C + tid], mul(alpha, px[3 * C + tid]));
-        const int sm = mm % NS;
-        const unsigned int m = smask(sm)[tid];
-        const int li = mm * C + tid;
+        D.x[i] = add(st[2 * C + tid], mul(alpha, st[3 * C + tid]));
+        const int io = li & RM;
+        const unsigned int m = mk[io];
         double p[ND];
 #pragma unroll
-        for (int d = 0; d < ND; ++d) {
-          const int lr = li + D.dia.off[d];
-          p[d] = mul(slot(sm)[(4 + d) * C + tid], tr[((lr / C) % RS) * C + lr % C]);
-        }
+        for (int d = 0; d < ND; ++d) p[d] = mul(gr[d * RING + io], tr[(li + off[d]) & RM]);
         const double y = combine_numpy<ND>(p, m);
-        const double rni = rp[(mm % RS) * C + tid];
+        const double rni = rp[io];
         const double si = add(y, mul(eps, rni));
         D.s[i] = si;
         prs += mul(rni, si);
@@ -1047,6 +1046,7 @@ struct sg_pcg {
   int64_t period = 0;
   int short_rows = 0;
   int nrng = 0;       // sliding-window ranges
+  int num_sms = 148;
   int k23 = 1;        // fused K2+K3 variant: 1 = sliding window (k_iter23_sw), 0 = tiles (k_iter23_st)
   int staged = 0;     // DIA with a small halo: halo-staged K1 and fused K2+K3 (k_iter1_st, k_iter23_st)
   // DIA format (0 = CSR)
@@ -1309,6 +1309,23 @@ int setup_dia(sg_pcg* h, const int32_t* a_offs, const int32_t* a_cols, const int
   return SG_OK;
 }
 
+// Opt the sliding-window kernels into their shared memory; blocks per SM of the (nd, nh) one.
+template <int ND, int NH>
+int sw_attr(int* per_sm) {
+  SG_CUDA(cudaFuncSetAttribute(k_iter23_sw<ND, NH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)Sw23<ND, NH>::SMEM));
+  SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_iter23_sw<ND, NH>, PR, Sw23<ND, NH>::SMEM));
+  if (*per_sm < 1) *per_sm = 1;
+  return SG_OK;
+}
+
+int sw_setup(int nd, int nh, int* per_sm) {
+  const int ns = nd == 5 ? 5 : (nd == 7 ? 7 : 8);
+  if (ns == 5) return nh == 1 ? sw_attr<5, 1>(per_sm) : sw_attr<5, 2>(per_sm);
+  if (ns == 7) return nh == 1 ? sw_attr<7, 1>(per_sm) : sw_attr<7, 2>(per_sm);
+  return nh == 1 ? sw_attr<8, 1>(per_sm) : sw_attr<8, 2>(per_sm);
+}
+
 }  // namespace
 
 extern "C" int sg_pcg_create(sg_pcg** out, int32_t n_systems, const int64_t* sys_row_start_host,
@@ -1322,6 +1339,11 @@ extern "C" int sg_pcg_create(sg_pcg** out, int32_t n_systems, const int64_t* sys
   if (precond_kind == SG_PRECOND_LEARNED && epsilon < 0.0) { set_error("epsilon must be nonnegative"); return SG_EINVAL; }
   cudaStream_t s = as_stream(stream);
   sg_pcg* h = new sg_pcg();
+  {
+    int dev = 0;
+    SG_CUDA(cudaGetDevice(&dev));
+    SG_CUDA(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, dev));
+  }
   h->S = n_systems;
   h->pre = precond_kind;
   h->eps = epsilon;
@@ -1368,12 +1390,35 @@ extern "C" int sg_pcg_create(sg_pcg** out, int32_t n_systems, const int64_t* sys
   }
   sys_blk0.push_back((int)blk_r0.size());
   h->nblk = (int)blk_r0.size();
-  // sliding-window ranges (halo-staged DIA)
+  // sliding-window ranges (halo-staged DIA): m ranges per system, m chosen against the number of
+  // co-resident CTAs (whole waves) and the 4*NH-chunk warm-up every range pays
+  long long rng_len = 1;
+  if (h->staged) {
+    const int nh = h->D.dia.halo <= kSwC ? 1 : 2;
+    int per_sm = 1;
+    int rc = sw_setup(h->dia_nd, nh, &per_sm);
+    if (rc) { delete h; return rc; }
+    const long long resident = (long long)h->num_sms * per_sm;
+    long long maxrows = 1;
+    for (int k = 0; k < n_systems; ++k) maxrows = std::max<long long>(maxrows, h->sys_start[k + 1] - h->sys_start[k]);
+    double best = 1e300;
+    const long long mmax = std::max<long long>(1, std::min<long long>(256, maxrows / kSwC));  // ranges >= C rows
+    for (long long m = 1; m <= mmax; ++m) {
+      const long long len = (maxrows + m - 1) / m;
+      const double waves = (double)((n_systems * m + resident - 1) / resident);
+      const double cost = waves * (double)(len + 4LL * nh * kSwC);
+      if (cost < best * 0.999) { best = cost; rng_len = len; }
+    }
+    const char* rl = getenv("SG_SW_RANGE");
+    if (rl && atoll(rl) > 0) rng_len = atoll(rl);
+  } else {
+    rng_len = 1LL << 62;
+  }
   std::vector<long long> rng_r0;
   std::vector<int> rng_sys, sys_rng0;
   for (int k = 0; k < n_systems; ++k) {
     sys_rng0.push_back((int)rng_r0.size());
-    for (int64_t r = h->sys_start[k]; r < h->sys_start[k + 1]; r += kSwRange) {
+    for (int64_t r = h->sys_start[k]; r < h->sys_start[k + 1]; r += rng_len) {
       rng_r0.push_back(r);
       rng_sys.push_back(k);
     }
@@ -1386,7 +1431,8 @@ extern "C" int sg_pcg_create(sg_pcg** out, int32_t n_systems, const int64_t* sys
   c.take<long long>(h->nrng); c.take<int>(h->nrng); c.take<int>(S + 1);
   const int64_t gv = h->guard;  // zero guard rows around every vector (DIA neighbour reads)
   for (int v = 0; v < 9; ++v) c.take<double>(n + 2 * gv + 2);
-  c.take<double>(2 * nb); c.take<unsigned int>(S); c.take<SysState>(S); c.take<Ctl>(1);
+  const int64_t npart = std::max<int64_t>(nb, h->nrng);  // per-CTA partials: tiles or ranges
+  c.take<double>(2 * npart); c.take<unsigned int>(S); c.take<SysState>(S); c.take<Ctl>(1);
   int e = cudaMalloc(&h->mem, c.off);
   if (e != cudaSuccess) { delete h; return cuda_fail((cudaError_t)e, "cudaMalloc(pcg workspace)"); }
   Carve m(h->mem);
@@ -1399,7 +1445,7 @@ extern "C" int sg_pcg_create(sg_pcg** out, int32_t n_systems, const int64_t* sys
   int* d_sys_rng0 = m.take<int>(S + 1);
   double* vec[9];
   for (int v = 0; v < 9; ++v) vec[v] = m.take<double>(n + 2 * gv + 2) + gv;
-  double* part = m.take<double>(2 * nb);
+  double* part = m.take<double>(2 * npart);
   unsigned int* counter = m.take<unsigned int>(S);
   h->st = m.take<SysState>(S);
   h->ctl = m.take<Ctl>(1);
@@ -1417,7 +1463,7 @@ extern "C" int sg_pcg_create(sg_pcg** out, int32_t n_systems, const int64_t* sys
   Dev& D = h->D;
   D.blk_r0 = d_blk_r0; D.blk_sys = d_blk_sys; D.sys_blk0 = d_sys_blk0; D.sys_r1 = d_sys_r1;
   D.tile = tile;
-  D.rng_r0 = d_rng_r0; D.rng_sys = d_rng_sys; D.sys_rng0 = d_sys_rng0;
+  D.rng_r0 = d_rng_r0; D.rng_sys = d_rng_sys; D.sys_rng0 = d_sys_rng0; D.rng_len = rng_len;
   D.a_offs = a_offs; D.a_cols = a_cols; D.a_vals = a_vals;
   D.g_offs = g_offs; D.g_cols = g_cols; D.g_vals = g_vals;
   D.gt_offs = gt_offs; D.gt_cols = gt_cols; D.gt_vals = gt_vals;
@@ -1430,14 +1476,9 @@ extern "C" int sg_pcg_create(sg_pcg** out, int32_t n_systems, const int64_t* sys
   for (int k = 0; k < 4; ++k) SG_CUDA(cudaEventCreate(&h->ev[k]));
   if (h->staged) {
     const char* kv = getenv("SG_PCG_K23");
-    h->k23 = (kv && kv[0] == 't') ? 0 : 1;
-    // the sliding-window kernels need more than the default 48 KB of dynamic shared memory
-    SG_CUDA(cudaFuncSetAttribute(k_iter23_sw<5, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sw23<5, 1>::SMEM));
-    SG_CUDA(cudaFuncSetAttribute(k_iter23_sw<5, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sw23<5, 2>::SMEM));
-    SG_CUDA(cudaFuncSetAttribute(k_iter23_sw<7, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sw23<7, 1>::SMEM));
-    SG_CUDA(cudaFuncSetAttribute(k_iter23_sw<7, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sw23<7, 2>::SMEM));
-    SG_CUDA(cudaFuncSetAttribute(k_iter23_sw<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sw23<8, 1>::SMEM));
-    SG_CUDA(cudaFuncSetAttribute(k_iter23_sw<8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sw23<8, 2>::SMEM));
+    // the sliding window takes the mirror of diagonal d as ND-1-d: only for full diagonal sets
+    const bool full = h->dia_nd == 5 || h->dia_nd == 7 || h->dia_nd == 8;
+    h->k23 = (kv && kv[0] == 't') || !full ? 0 : 1;
   }
   SG_CUDA(cudaStreamSynchronize(s));
   *out = h;
