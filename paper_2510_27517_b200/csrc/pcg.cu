@@ -337,18 +337,34 @@ struct CsrOps {
 // load waits for the mask; the mask only selects which products enter the sum, in the
 // reference's order.  32-bit row indices (n < 2^31) and per-diagonal base pointers keep the
 // address arithmetic to one IMAD.WIDE per load.
+// Branch-free: every sum is evaluated and kept or dropped by selects, so the products of all
+// diagonals are issued together and the dependent adds form one short chain.
 template <int ND>
 __device__ __forceinline__ double combine_numpy(const double (&p)[ND], unsigned int m) {
   double first = 0.0, s = 0.0;
   bool have = false, more = false;
 #pragma unroll
   for (int d = 0; d < ND; ++d) {
-    if (m & (1u << d)) {
-      if (!have) { first = p[d]; have = true; }
-      else { s = add(s, p[d]); more = true; }
-    }
+    const bool pr = (m >> d) & 1u;
+    const double sn = add(s, p[d]);
+    first = (pr && !have) ? p[d] : first;
+    s = (pr && have) ? sn : s;
+    more = more || (pr && have);
+    have = have || pr;
   }
   return more ? add(first, s) : first;
+}
+
+// Sequential (add.at order) sum of the present products, branch-free.
+template <int ND>
+__device__ __forceinline__ double combine_seq(const double (&p)[ND], unsigned int m) {
+  double s = 0.0;
+#pragma unroll
+  for (int d = 0; d < ND; ++d) {
+    const double sn = add(s, p[d]);
+    s = ((m >> d) & 1u) ? sn : s;
+  }
+  return s;
 }
 
 template <int ND, int XM>
@@ -410,11 +426,10 @@ __device__ __forceinline__ double dia_row_t_seq(const Dia& dd, const double* con
     a[d] = __ldg(Vd[dd.mir[d]] + j);
     x[d] = xval<XM>(f, j);
   }
-  double s = 0.0;
+  double p[NA];
 #pragma unroll
-  for (int d = 0; d < ND; ++d)
-    if (m & (1u << d)) s = add(s, mul(a[d], x[d]));
-  return s;
+  for (int d = 0; d < ND; ++d) p[d] = mul(a[d], x[d]);
+  return combine_seq<NA>(p, m);
 }
 
 // ------------------------------------------------------------------ kernels
@@ -931,6 +946,9 @@ __global__ void __launch_bounds__(PR, 1) k_iter23_sw(Dev D, int par) {
   const long long LB = (R0 & ~15LL) - 2LL * NH * C;
   const int m1 = (int)((R1 - LB + C - 1) / C) - 1;  // last output chunk
   const int K = m1 + 2 * NH + 1;                     // steps
+  // system / range bounds relative to LB (32-bit compares in the loop)
+  auto rel = [&](long long v) { return (int)(v - LB < -1 ? -1 : (v - LB > (1LL << 30) ? (1LL << 30) : v - LB)); };
+  const int s0r = rel(s0), s1r = rel(s1), R0r = rel(R0), R1r = rel(R1);
   int off[ND];
 #pragma unroll
   for (int d = 0; d < ND; ++d) off[d] = D.dia.off[d];
@@ -964,14 +982,14 @@ __global__ void __launch_bounds__(PR, 1) k_iter23_sw(Dev D, int par) {
     const double* st = stg + (k % P) * 4 * C;
     mbar_wait(&bars[k % P], (uint32_t)((k / P) & 1));
     {  // A: r' of the lead chunk
-      const long long j = LB + (long long)k * C + tid;
+      const int lj = k * C + tid;
       double v = sub(st[tid], mul(alpha, st[C + tid]));
-      v = (j >= s0 && j < s1) ? v : 0.0;
-      if (j >= R0 && j < R1) {
-        rn[j] = v;
+      v = (lj >= s0r && lj < s1r) ? v : 0.0;
+      if (lj >= R0r && lj < R1r) {
+        rn[LB + lj] = v;
         prr += mul(v, v);
       }
-      rp[(k * C + tid) & RM] = v;
+      rp[lj & RM] = v;
     }
     __syncthreads();
     if (tid == 0 && k + 1 < K) issue(k + 1);
@@ -979,22 +997,21 @@ __global__ void __launch_bounds__(PR, 1) k_iter23_sw(Dev D, int par) {
     if (u >= NH) {  // B: t of chunk u (add.at order over G's mirror diagonals)
       const int lj = u * C + tid;
       const unsigned int m = mk[lj & RM];
-      double v = 0.0;
+      double p[ND];
 #pragma unroll
       for (int d = 0; d < ND; ++d) {
         const int ix = (lj + off[d]) & RM;
-        const double a = gr[(ND - 1 - d) * RING + ix], x = rp[ix];
-        if (m & (1u << d)) v = add(v, mul(a, x));
+        p[d] = mul(gr[(ND - 1 - d) * RING + ix], rp[ix]);
       }
-      const long long j = LB + lj;
-      tr[lj & RM] = (j >= s0 && j < s1) ? v : 0.0;
+      const double v = combine_seq<ND>(p, m);
+      tr[lj & RM] = (lj >= s0r && lj < s1r) ? v : 0.0;
     }
     __syncthreads();
     const int mm = k - 2 * NH;
     if (mm >= 2 * NH) {  // C: s and x of chunk mm (its x, d travelled with lead chunk k)
       const int li = mm * C + tid;
-      const long long i = LB + li;
-      if (i >= R0 && i < R1) {
+      if (li >= R0r && li < R1r) {
+        const long long i = LB + li;
         D.x[i] = add(st[2 * C + tid], mul(alpha, st[3 * C + tid]));
         const int io = li & RM;
         const unsigned int m = mk[io];
