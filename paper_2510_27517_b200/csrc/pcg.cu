@@ -1036,6 +1036,131 @@ __global__ void __launch_bounds__(PR, 1) k_iter23_sw(Dev D, int par) {
   }
 }
 
+// ------------------------------------------------------------------ sliding-window K1
+// K1 as a stream over the same ranges: per step the bulk-copy engine brings the lead chunk's
+// s, d, A diagonals (the lower half only when A is stored by it) and mask; then
+//   A  d' = s + beta d              lead chunk k   -> d' ring (own rows: d' to HBM)
+//   Q  q  = A d'                    chunk k - NH   (numpy order; partial d'.q)
+// One CTA barrier per step.  A pending fresh-residual check (rare: only after a candidate
+// convergence) runs after the stream over the range's own rows with direct loads.
+template <int FMT, int ND, int NH>
+struct Sw1 {
+  static constexpr int C = kSwC;
+  static constexpr int P = 3;                              // chunks in flight (incl. the current one)
+  static constexpr int NA = FMT == 2 ? ND / 2 + 1 : ND;   // diagonals streamed
+  static constexpr int RING = pow2ceil((P + NH) * C);      // A / mask ring: chunks u .. k + P - 1
+  static constexpr int RM = RING - 1;
+  static constexpr int DRING = pow2ceil((2 * NH + 2) * C); // d' ring: chunks u - NH .. k + 1
+  static constexpr int DM = DRING - 1;
+  // bytes: A [NA][RING] | d' [DRING] | staging [P][2][C] (s d) | mask [RING]
+  static constexpr size_t SMEM = (size_t)NA * RING * 8 + (size_t)DRING * 8 + (size_t)P * 2 * C * 8 + RING;
+};
+
+template <int FMT, int ND, int NH>
+__global__ void __launch_bounds__(PR, 5) k_iter1_sw(Dev D, int par) {
+  using G = Sw1<FMT, ND, NH>;
+  constexpr int C = G::C, P = G::P, NA = G::NA, RING = G::RING, RM = G::RM, DM = G::DM;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  __shared__ __align__(8) uint64_t bars[P];
+  __shared__ double red[PR / 32];
+  __shared__ int flag;
+  const int b = blockIdx.x, tid = threadIdx.x;
+  const int sys = D.rng_sys[b];
+  const int status = D.st[sys].status;
+  if (status == ST_DONE) return;
+  long long s0, s1;
+  sys_bounds(D, sys, s0, s1);
+  const long long R0 = D.rng_r0[b];
+  const long long R1 = R0 + D.rng_len < s1 ? R0 + D.rng_len : s1;
+  const bool run = status == ST_RUN;
+  const bool fresh = run ? (D.st[sys].flags & FL_FRESH) != 0 : true;
+  const double beta = D.st[sys].beta;
+  const double* dc = par ? D.d1 : D.d0;
+  double* dn = par ? D.d0 : D.d1;
+  double* rc = par ? D.r1 : D.r0;
+  double pdq = 0.0, prr = 0.0;
+  if (run) {
+    double* ar = reinterpret_cast<double*>(smraw);  // [NA][RING]
+    double* dp = ar + NA * RING;                      // [DRING]
+    double* stg = dp + G::DRING;                      // [P][2][C]
+    unsigned char* mk = reinterpret_cast<unsigned char*>(stg + P * 2 * C);
+    const long long LB = (R0 & ~15LL) - (long long)NH * C;
+    const int m1 = (int)((R1 - LB + C - 1) / C) - 1;
+    const int K = m1 + NH + 1;
+    auto rel = [&](long long v) { return (int)(v - LB < -1 ? -1 : (v - LB > (1LL << 30) ? (1LL << 30) : v - LB)); };
+    const int s0r = rel(s0), s1r = rel(s1), R0r = rel(R0), R1r = rel(R1);
+    int off[ND];
+#pragma unroll
+    for (int d = 0; d < ND; ++d) off[d] = D.dia.off[d];
+    auto issue = [&](int k) {
+      const int ss = k % P, gs = (k * C) & RM;
+      double* st = stg + ss * 2 * C;
+      const long long row = LB + (long long)k * C;
+      mbar_arrive_expect_tx(&bars[ss], (uint32_t)((2 + NA) * C * 8 + C));
+      bulk_g2s(st, D.s + row, C * 8, &bars[ss]);
+      bulk_g2s(st + C, dc + row, C * 8, &bars[ss]);
+#pragma unroll
+      for (int d = 0; d < NA; ++d) bulk_g2s(ar + d * RING + gs, D.dia.av[d] + row, C * 8, &bars[ss]);
+      bulk_g2s(mk + gs, D.dia.mask + row, C, &bars[ss]);
+    };
+    if (tid == 0) {
+#pragma unroll
+      for (int q = 0; q < P; ++q) mbar_init(&bars[q], 1);
+      mbar_init_fence();
+    }
+    __syncthreads();
+    if (tid == 0)
+      for (int k = 0; k < P - 1 && k < K; ++k) issue(k);
+    for (int k = 0; k < K; ++k) {
+      const double* st = stg + (k % P) * 2 * C;
+      mbar_wait(&bars[k % P], (uint32_t)((k / P) & 1));
+      {  // d' of the lead chunk
+        const int lj = k * C + tid;
+        double v = add(st[tid], mul(beta, st[C + tid]));
+        v = (lj >= s0r && lj < s1r) ? v : 0.0;
+        if (lj >= R0r && lj < R1r) dn[LB + lj] = v;
+        dp[lj & DM] = v;
+      }
+      __syncthreads();
+      if (tid == 0 && k + P - 1 < K) issue(k + P - 1);
+      const int u = k - NH;
+      if (u >= 0) {  // q of chunk u
+        const int li = u * C + tid;
+        if (li >= R0r && li < R1r) {
+          const int io = li & RM;
+          const unsigned int m = mk[io];
+          double p[ND];
+#pragma unroll
+          for (int d = 0; d < ND; ++d) {
+            const int ix = (li + off[d]) & RM;
+            // FMT 2: an upper entry (i, i+off) is the lower mirror entry at row i+off
+            const double a = (FMT == 2 && d > ND / 2) ? ar[(ND - 1 - d) * RING + ix] : ar[d * RING + io];
+            p[d] = mul(a, dp[(li + off[d]) & DM]);
+          }
+          const double qi = combine_numpy<ND>(p, m);
+          D.q[LB + li] = qi;
+          pdq += mul(dp[li & DM], qi);
+        }
+      }
+    }
+  }
+  if (fresh) {  // r_fresh = b - A x over the range's own rows (direct loads)
+    for (long long i = R0 + tid; i < R1; i += PR) {
+      const unsigned int m = D.dia.mask[i];
+      const double ax = FMT == 2 ? dia_row_numpy_sym<ND, 0>(D.dia, D.dia.av, (int)i, m, XF{D.x, nullptr, 0.0})
+                                 : dia_row_numpy<ND, 0>(D.dia, D.dia.av, (int)i, m, XF{D.x, nullptr, 0.0});
+      const double rf = sub(D.b[i], ax);
+      if (run) rc[i] = rf;
+      prr += mul(rf, rf);
+    }
+  }
+  if (arrive(D, D.sys_rng0, sys, pdq, prr, red, &flag)) {
+    const double dq = gather_partials(D, D.sys_rng0, sys, 0, red);
+    const double rrf = gather_partials(D, D.sys_rng0, sys, 1, red);
+    if (threadIdx.x == 0) fin_k1(D, sys, run, dq, rrf);
+  }
+}
+
 }  // namespace sg
 
 using namespace sg;
@@ -1064,6 +1189,7 @@ struct sg_pcg {
   int short_rows = 0;
   int nrng = 0;       // sliding-window ranges
   int num_sms = 148;
+  int k1sw = 1;       // K1 variant: 1 = sliding window (k_iter1_sw), 0 = tiles (k_iter1_st)
   int k23 = 1;        // fused K2+K3 variant: 1 = sliding window (k_iter23_sw), 0 = tiles (k_iter23_st)
   int staged = 0;     // DIA with a small halo: halo-staged K1 and fused K2+K3 (k_iter1_st, k_iter23_st)
   // DIA format (0 = CSR)
@@ -1140,13 +1266,16 @@ int launch_iteration(sg_pcg* h, cudaStream_t s, int par, bool refresh, cudaEvent
     constexpr int NS = ND > 0 ? ND : 1;
     const bool st = FMT >= 1 && h->staged;
     const size_t tile = (size_t)PR * kRpt, H = (size_t)h->D.dia.halo;
-    if (st && H <= PR) k_iter1_st<FS, NS, 1><<<g, PR, (tile + 2 * H) * sizeof(double), s>>>(h->D, par);
+    const unsigned gr = (unsigned)h->nrng;
+    if (st && h->k1sw) {
+      if (H <= PR) k_iter1_sw<FS, NS, 1><<<gr, PR, Sw1<FS, NS, 1>::SMEM, s>>>(h->D, par);
+      else k_iter1_sw<FS, NS, 2><<<gr, PR, Sw1<FS, NS, 2>::SMEM, s>>>(h->D, par);
+    } else if (st && H <= PR) k_iter1_st<FS, NS, 1><<<g, PR, (tile + 2 * H) * sizeof(double), s>>>(h->D, par);
     else if (st) k_iter1_st<FS, NS, 2><<<g, PR, (tile + 2 * H) * sizeof(double), s>>>(h->D, par);
     else k_iter1<PRE, FMT, ND, SH><<<g, PR, 0, s>>>(h->D, par);
     ++k;
     if (ev) SG_CUDA(cudaEventRecordWithFlags(ev[1], s, cudaEventRecordExternal));
     if (st && !refresh && PRE == SG_PRECOND_LEARNED) {  // K2 + K3 fused
-      const unsigned gr = (unsigned)h->nrng;
       if (h->k23 == 1) {
         if (H <= PR) k_iter23_sw<NS, 1><<<gr, PR, Sw23<NS, 1>::SMEM, s>>>(h->D, par);
         else k_iter23_sw<NS, 2><<<gr, PR, Sw23<NS, 2>::SMEM, s>>>(h->D, par);
@@ -1331,6 +1460,10 @@ template <int ND, int NH>
 int sw_attr(int* per_sm) {
   SG_CUDA(cudaFuncSetAttribute(k_iter23_sw<ND, NH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)Sw23<ND, NH>::SMEM));
+  SG_CUDA(cudaFuncSetAttribute(k_iter1_sw<1, ND, NH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)Sw1<1, ND, NH>::SMEM));
+  SG_CUDA(cudaFuncSetAttribute(k_iter1_sw<2, ND, NH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)Sw1<2, ND, NH>::SMEM));
   SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_iter23_sw<ND, NH>, PR, Sw23<ND, NH>::SMEM));
   if (*per_sm < 1) *per_sm = 1;
   return SG_OK;
@@ -1496,6 +1629,8 @@ extern "C" int sg_pcg_create(sg_pcg** out, int32_t n_systems, const int64_t* sys
     // the sliding window takes the mirror of diagonal d as ND-1-d: only for full diagonal sets
     const bool full = h->dia_nd == 5 || h->dia_nd == 7 || h->dia_nd == 8;
     h->k23 = (kv && kv[0] == 't') || !full ? 0 : 1;
+    const char* k1v = getenv("SG_PCG_K1");
+    h->k1sw = (k1v && k1v[0] == 't') || !(h->dia_nd == 5 || h->dia_nd == 7) ? 0 : 1;
   }
   SG_CUDA(cudaStreamSynchronize(s));
   *out = h;
