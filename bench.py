@@ -197,7 +197,7 @@ def run_ours(a, rank, world, local):
     K1N = "k_iter1 (q = A d, d = s + beta d, d.q)"
     K2N = "k_iter2 (x, r update, t = G^T r, r.r)"
     K3N = "k_iter3 (s = G t + eps r, r.s)"
-    K23N = "k_iter23_st (x, r update, t = G^T r in smem, s = G t + eps r, r.r, r.s)"
+    K23N = "k_iter23 (fused: x, r update, t = G^T r on chip, s = G t + eps r, r.r, r.s)"
     # algorithmic bytes per system per launch: CSR matrix bytes
     # (12 B/nnz + 4 B/row) + the vectors each kernel must read / write once
     csr = 12 * e1n + 4 * (n1 + 1)
@@ -240,8 +240,11 @@ def run_ours(a, rank, world, local):
     dom = max(kern, key=lambda k: kern[k]["avg_ms"]) if kern else None
     roofline = None
     if dom:
+        traffic = ncu_traffic("k_iter23_sw" if dom == K23N else "k_iter1_sw" if dom == K1N else None)
         roofline = {"bound": "hbm", "kernel": dom, "achieved": kern[dom]["gbs"], "peak": peak,
-                    "unit": "GB/s", "frac": kern[dom]["frac"], "traffic": None,
+                    "unit": "GB/s", "frac": kern[dom]["frac"],
+                    "traffic": traffic["bytes"] if traffic else None,
+                    "traffic_source": traffic["source"] if traffic else None,
                     "achieved_physical": kern[dom].get("physical_gbs"),
                     "frac_physical": kern[dom].get("physical_frac"),
                     "bytes_note": "achieved = SURVEY.md §8(d) CSR bytes (12 B/nnz + 4 B/row + vectors); the kernels "
@@ -326,6 +329,29 @@ def run_ours(a, rank, world, local):
                      "all_converged": bool(np.all(conv_all == 1))},
                "pcg_graph_launches_per_step": chunks / a.steps}
         print(json.dumps(out), flush=True)
+
+
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "r01_ncu_full_pcg_sw_128sys.txt")
+
+
+def ncu_traffic(kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum of `kernel` from the committed ncu --set full
+    capture of this workload (one launch, 128-system batch), in bytes; None if absent."""
+    if not kernel or not os.path.exists(NCU_SUMMARY):
+        return None
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    for line in open(NCU_SUMMARY):
+        if f" {kernel}<" not in line.split("|")[0]:
+            continue
+        vals = {}
+        for cell in line.split("|")[1:]:
+            key, _, v = cell.strip().partition("=")
+            name, _, unit = key.partition("[")
+            vals[name] = float(v) * scale.get(unit.rstrip("]"), float("nan"))
+        if "dram__bytes_read.sum" in vals and "dram__bytes_write.sum" in vals:
+            return {"bytes": vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"],
+                    "source": os.path.relpath(NCU_SUMMARY, ROOT) + " (ncu --set full, one launch)"}
+    return None
 
 
 def main():

@@ -95,8 +95,11 @@ def main():
     peak = float(peaks.get("hbm_gbs", 6650.0))
     per_k = {}
     if prof[4] > 0:
-        per_sys = {"k_iter1": 12 * nnz + 4 * (n + 1) + 32 * n, "k_iter2": 12 * nnz + 4 * (n + 1) + 56 * n,
-                   "k_iter3": 12 * nnz + 4 * (n + 1) + 24 * n}
+        csr = 12 * nnz + 4 * (n + 1)
+        if prof[7]:  # K2 + K3 fused (t stays on chip)
+            per_sys = {"k_iter1": csr + 32 * n, "k_iter23": csr + 56 * n}
+        else:
+            per_sys = {"k_iter1": csr + 32 * n, "k_iter2": csr + 56 * n, "k_iter3": csr + 24 * n}
         for (name, by), ms in zip(per_sys.items(), prof[:3]):
             avg = ms / prof[4]
             per_k[name] = {"avg_ms": avg, "gbs": by / (avg * 1e-3) / 1e9, "frac": by / (avg * 1e-3) / 1e9 / peak}

