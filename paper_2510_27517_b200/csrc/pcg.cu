@@ -67,6 +67,7 @@ struct Ctl {
 struct Dia {
   int nd;
   int halo;            // max |off|
+  int W;               // 5-point grid line width (offsets {-W,-1,0,1,W}), else 0
   int off[MAXD];       // ascending column offsets
   int mir[MAXD];       // mirror diagonal: off[mir[d]] == -off[d]
   long long n;
@@ -1161,6 +1162,285 @@ __global__ void __launch_bounds__(PR, 5) k_iter1_sw(Dev D, int par) {
   }
 }
 
+// ------------------------------------------------------------------ 2-D strip sliding window
+// Wide 5-point grids (offsets {-W, -1, 0, 1, W}, W > 512: the north-star 2048^2 shape) do not
+// fit a 1-D halo ring, so the stream runs over grid LINES inside a column STRIP instead: a CTA
+// owns columns [x0, x0 + 256) of lines [y0, y1) of one system and walks them line by line.  A
+// line segment is loaded with E = 2 columns of x-halo on each side (positions p = x - x0 + 2,
+// 0 <= p < SP); the +-W neighbours are the adjacent line slots of the ring and the +-1
+// neighbours are p +- 1, so all of it is plain 1-D DIA arithmetic (a position past the strip
+// edge is simply the neighbouring row).  Same phases, roundings and summation orders as the
+// 1-D kernels; only the partial sums are grouped per (strip, line range).
+constexpr int kStripC = 256;               // columns per strip (one per thread)
+constexpr int kStripE = 2;                 // x-halo columns on each side
+constexpr int kStripSP = kStripC + 2 * kStripE;  // 260 positions per line segment (2080 B)
+constexpr int kStripMK = kStripSP + 28;    // mask window: 16-row aligned start, 288 bytes
+constexpr int kStripRL = 4;                // ring lines (power of two)
+
+// (line, column) displacement of the 5-point diagonals d = 0..4 (offsets -W, -1, 0, 1, W)
+__device__ __forceinline__ constexpr int s5a(int d) { return d == 0 ? -1 : (d == 4 ? 1 : 0); }
+__device__ __forceinline__ constexpr int s5b(int d) { return d == 1 ? -1 : (d == 3 ? 1 : 0); }
+
+struct Strip23 {
+  static constexpr int P = 2;
+  // bytes: G [5][RL][SP] | r' [RL][SP] | t [RL][SP] | staging [P] (q [SP], x [C], d [C]) | mask [RL][MK]
+  static constexpr size_t SMEM = (size_t)(5 + 2) * kStripRL * kStripSP * 8 +
+                                 (size_t)P * (kStripSP + 2 * kStripC) * 8 + (size_t)kStripRL * kStripMK;
+};
+
+__global__ void __launch_bounds__(PR, 1) k_iter23_s5(Dev D, int par) {
+  constexpr int SP = kStripSP, RL = kStripRL, P = Strip23::P, C = kStripC, E = kStripE;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  __shared__ __align__(8) uint64_t bars[P];
+  __shared__ double red[PR / 32];
+  __shared__ int flag;
+  const int b = blockIdx.x, tid = threadIdx.x;
+  const int sys = D.rng_sys[b];
+  if (D.st[sys].status != ST_RUN) return;
+  long long s0, s1;
+  sys_bounds(D, sys, s0, s1);
+  const long long W = D.dia.W;
+  const long long r0 = D.rng_r0[b] - s0;
+  const int x0 = (int)(r0 % W);
+  const long long y0 = r0 / W, nl = (s1 - s0) / W;
+  const long long y1 = y0 + D.rng_len < nl ? y0 + D.rng_len : nl;
+  const int cx = (int)(W - x0 < C ? W - x0 : C);  // own columns of this strip
+  const double alpha = D.st[sys].alpha;
+  const double eps = D.ctl->eps;
+  const double* dn = par ? D.d0 : D.d1;
+  const double* rc = par ? D.r1 : D.r0;
+  double* rn = par ? D.r0 : D.r1;
+  double* gr = reinterpret_cast<double*>(smraw);  // [5][RL][SP]
+  double* rp = gr + 5 * RL * SP;                    // [RL][SP]
+  double* tr = rp + RL * SP;                        // [RL][SP]
+  double* stg = tr + RL * SP;                       // [P][SP + 2C]
+  unsigned char* mk = reinterpret_cast<unsigned char*>(stg + P * (SP + 2 * C));  // [RL][MK]
+  const long long LBl = y0 - 2;                     // line of step 0
+  const int K = (int)(y1 - y0) + 4;
+  auto rowof = [&](long long line, int p) { return s0 + line * W + x0 - E + p; };
+  auto issue = [&](int k) {
+    const int ss = k % P, ls = k & (RL - 1);
+    double* st = stg + ss * (SP + 2 * C);
+    const long long row = rowof(LBl + k, 0);
+    const bool own = k >= 4;
+    const uint32_t bytes = (uint32_t)((2 + 5) * SP * 8 + kStripMK + (own ? 2 * C * 8 : 0));
+    mbar_arrive_expect_tx(&bars[ss], bytes);
+    bulk_g2s(rp + ls * SP, rc + row, SP * 8, &bars[ss]);
+    bulk_g2s(st, D.q + row, SP * 8, &bars[ss]);
+#pragma unroll
+    for (int d = 0; d < 5; ++d) bulk_g2s(gr + (d * RL + ls) * SP, D.dia.gv[d] + row, SP * 8, &bars[ss]);
+    bulk_g2s(mk + ls * kStripMK, D.dia.mask + (row - 14), kStripMK, &bars[ss]);
+    if (own) {
+      const long long ro = rowof(LBl + k - 2, E);
+      bulk_g2s(st + SP, D.x + ro, C * 8, &bars[ss]);
+      bulk_g2s(st + SP + C, dn + ro, C * 8, &bars[ss]);
+    }
+  };
+  if (tid == 0) {
+#pragma unroll
+    for (int q = 0; q < P; ++q) mbar_init(&bars[q], 1);
+    mbar_init_fence();
+  }
+  __syncthreads();
+  if (tid == 0) issue(0);
+  double prr = 0.0, prs = 0.0;
+  for (int k = 0; k < K; ++k) {
+    const double* st = stg + (k % P) * (SP + 2 * C);
+    mbar_wait(&bars[k % P], (uint32_t)((k / P) & 1));
+    {  // A: r' of the lead line segment (in place over the r copy)
+      const long long line = LBl + k;
+      const int ls = k & (RL - 1);
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        const int p = tid + h2 * PR;
+        if (p < SP) {
+          const long long j = rowof(line, p);
+          double v = sub(rp[ls * SP + p], mul(alpha, st[p]));
+          v = (j >= s0 && j < s1) ? v : 0.0;
+          const int x = x0 - E + p;
+          if (line >= y0 && line < y1 && x >= x0 && x < x0 + cx) {
+            rn[j] = v;
+            prr += mul(v, v);
+          }
+          rp[ls * SP + p] = v;
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0 && k + 1 < K) issue(k + 1);
+    const int u = k - 1;
+    if (u >= 1) {  // B: t on positions 1 .. SP-2 of line u (add.at order over G's mirrors)
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        const int p = 1 + tid + h2 * PR;
+        if (p < SP - 1) {
+          const long long j = rowof(LBl + u, p);
+          const unsigned int m = mk[(u & (RL - 1)) * kStripMK + p + 14];
+          double pr[5];
+#pragma unroll
+          for (int d = 0; d < 5; ++d) {
+            const int ix = ((u + s5a(d)) & (RL - 1)) * SP + p + s5b(d);
+            pr[d] = mul(gr[(4 - d) * RL * SP + ix], rp[ix]);
+          }
+          const double v = combine_seq<5>(pr, m);
+          tr[(u & (RL - 1)) * SP + p] = (j >= s0 && j < s1) ? v : 0.0;
+        }
+      }
+    }
+    __syncthreads();
+    const int mm = k - 2;
+    const long long line = LBl + mm;
+    if (mm >= 2 && tid < cx && line >= y0 && line < y1) {  // C: own columns of line mm
+      const int p = tid + E;
+      const long long i = rowof(line, p);
+      D.x[i] = add(st[SP + tid], mul(alpha, st[SP + C + tid]));
+      const int ls = mm & (RL - 1);
+      const unsigned int m = mk[ls * kStripMK + p + 14];
+      double pr[5];
+#pragma unroll
+      for (int d = 0; d < 5; ++d)
+        pr[d] = mul(gr[(d * RL + ls) * SP + p], tr[((mm + s5a(d)) & (RL - 1)) * SP + p + s5b(d)]);
+      const double y = combine_numpy<5>(pr, m);
+      const double rni = rp[ls * SP + p];
+      const double si = add(y, mul(eps, rni));
+      D.s[i] = si;
+      prs += mul(rni, si);
+    }
+  }
+  if (arrive(D, D.sys_rng0, sys, prr, prs, red, &flag)) {
+    const double rr = gather_partials(D, D.sys_rng0, sys, 0, red);
+    const double rs = gather_partials(D, D.sys_rng0, sys, 1, red);
+    if (threadIdx.x == 0) {
+      D.st[sys].rr = rr;
+      fin_k3(D, sys, rs, 0);
+    }
+  }
+}
+
+// K1 on strips: d' = s + beta d over each lead line segment, q = A d' on the own columns.
+template <int FMT>
+struct Strip1 {
+  static constexpr int P = 3;
+  static constexpr int NA = FMT == 2 ? 3 : 5;
+  // bytes: A [NA][RL][SP] | d' [RL][SP] | staging [P][2][SP] (s, d) | mask [RL][MK]
+  static constexpr size_t SMEM = (size_t)(NA + 1) * kStripRL * kStripSP * 8 + (size_t)P * 2 * kStripSP * 8 +
+                                 (size_t)kStripRL * kStripMK;
+};
+
+template <int FMT>
+__global__ void __launch_bounds__(PR, 4) k_iter1_s5(Dev D, int par) {
+  constexpr int SP = kStripSP, RL = kStripRL, P = Strip1<FMT>::P, NA = Strip1<FMT>::NA, E = kStripE;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  __shared__ __align__(8) uint64_t bars[P];
+  __shared__ double red[PR / 32];
+  __shared__ int flag;
+  const int b = blockIdx.x, tid = threadIdx.x;
+  const int sys = D.rng_sys[b];
+  const int status = D.st[sys].status;
+  if (status == ST_DONE) return;
+  long long s0, s1;
+  sys_bounds(D, sys, s0, s1);
+  const long long W = D.dia.W;
+  const long long r0 = D.rng_r0[b] - s0;
+  const int x0 = (int)(r0 % W);
+  const long long y0 = r0 / W, nl = (s1 - s0) / W;
+  const long long y1 = y0 + D.rng_len < nl ? y0 + D.rng_len : nl;
+  const int cx = (int)(W - x0 < kStripC ? W - x0 : kStripC);
+  const bool run = status == ST_RUN;
+  const bool fresh = run ? (D.st[sys].flags & FL_FRESH) != 0 : true;
+  const double beta = D.st[sys].beta;
+  const double* dc = par ? D.d1 : D.d0;
+  double* dn = par ? D.d0 : D.d1;
+  double* rc = par ? D.r1 : D.r0;
+  auto rowof = [&](long long line, int p) { return s0 + line * W + x0 - E + p; };
+  double pdq = 0.0, prr = 0.0;
+  if (run) {
+    double* ar = reinterpret_cast<double*>(smraw);  // [NA][RL][SP]
+    double* dp = ar + NA * RL * SP;                   // [RL][SP]
+    double* stg = dp + RL * SP;                       // [P][2][SP]
+    unsigned char* mk = reinterpret_cast<unsigned char*>(stg + P * 2 * SP);
+    const long long LBl = y0 - 1;
+    const int K = (int)(y1 - y0) + 2;
+    auto issue = [&](int k) {
+      const int ss = k % P, ls = k & (RL - 1);
+      const long long row = rowof(LBl + k, 0);
+      mbar_arrive_expect_tx(&bars[ss], (uint32_t)((2 + NA) * SP * 8 + kStripMK));
+      bulk_g2s(stg + ss * 2 * SP, D.s + row, SP * 8, &bars[ss]);
+      bulk_g2s(stg + ss * 2 * SP + SP, dc + row, SP * 8, &bars[ss]);
+#pragma unroll
+      for (int d = 0; d < NA; ++d) bulk_g2s(ar + (d * RL + ls) * SP, D.dia.av[d] + row, SP * 8, &bars[ss]);
+      bulk_g2s(mk + ls * kStripMK, D.dia.mask + (row - 14), kStripMK, &bars[ss]);
+    };
+    if (tid == 0) {
+#pragma unroll
+      for (int q = 0; q < P; ++q) mbar_init(&bars[q], 1);
+      mbar_init_fence();
+    }
+    __syncthreads();
+    if (tid == 0)
+      for (int k = 0; k < P - 1 && k < K; ++k) issue(k);
+    for (int k = 0; k < K; ++k) {
+      const double* st = stg + (k % P) * 2 * SP;
+      mbar_wait(&bars[k % P], (uint32_t)((k / P) & 1));
+      {  // d' of the lead line segment
+        const long long line = LBl + k;
+        const int ls = k & (RL - 1);
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int p = tid + h2 * PR;
+          if (p < SP) {
+            const long long j = rowof(line, p);
+            double v = add(st[p], mul(beta, st[SP + p]));
+            v = (j >= s0 && j < s1) ? v : 0.0;
+            const int x = x0 - E + p;
+            if (line >= y0 && line < y1 && x >= x0 && x < x0 + cx) dn[j] = v;
+            dp[ls * SP + p] = v;
+          }
+        }
+      }
+      __syncthreads();
+      if (tid == 0 && k + P - 1 < K) issue(k + P - 1);
+      const int u = k - 1;
+      const long long line = LBl + u;
+      if (u >= 1 && tid < cx && line >= y0 && line < y1) {  // q of the own columns of line u
+        const int p = tid + E;
+        const int ls = u & (RL - 1);
+        const unsigned int m = mk[ls * kStripMK + p + 14];
+        double pr[5];
+#pragma unroll
+        for (int d = 0; d < 5; ++d) {
+          // FMT 2: an upper entry (i, i+off) is the lower mirror entry at row i+off
+          double a;
+          if (FMT == 2 && d > 2) a = ar[((4 - d) * RL + ((u + s5a(d)) & (RL - 1))) * SP + p + s5b(d)];
+          else a = ar[(d * RL + ls) * SP + p];
+          pr[d] = mul(a, dp[((u + s5a(d)) & (RL - 1)) * SP + p + s5b(d)]);
+        }
+        const double qi = combine_numpy<5>(pr, m);
+        const long long i = rowof(line, p);
+        D.q[i] = qi;
+        pdq += mul(dp[ls * SP + p], qi);
+      }
+    }
+  }
+  if (fresh) {  // r_fresh = b - A x over the range's own rows (direct loads)
+    for (long long line = y0; line < y1; ++line) {
+      if (tid >= cx) break;
+      const long long i = s0 + line * W + x0 + tid;
+      const unsigned int m = D.dia.mask[i];
+      const double ax = FMT == 2 ? dia_row_numpy_sym<5, 0>(D.dia, D.dia.av, (int)i, m, XF{D.x, nullptr, 0.0})
+                                 : dia_row_numpy<5, 0>(D.dia, D.dia.av, (int)i, m, XF{D.x, nullptr, 0.0});
+      const double rf = sub(D.b[i], ax);
+      if (run) rc[i] = rf;
+      prr += mul(rf, rf);
+    }
+  }
+  if (arrive(D, D.sys_rng0, sys, pdq, prr, red, &flag)) {
+    const double dq = gather_partials(D, D.sys_rng0, sys, 0, red);
+    const double rrf = gather_partials(D, D.sys_rng0, sys, 1, red);
+    if (threadIdx.x == 0) fin_k1(D, sys, run, dq, rrf);
+  }
+}
+
 }  // namespace sg
 
 using namespace sg;
@@ -1189,6 +1469,7 @@ struct sg_pcg {
   int short_rows = 0;
   int nrng = 0;       // sliding-window ranges
   int num_sms = 148;
+  int strip = 0;      // wide 5-point grid: 2-D strip sliding-window kernels (k_iter1_s5, k_iter23_s5)
   int k1sw = 1;       // K1 variant: 1 = sliding window (k_iter1_sw), 0 = tiles (k_iter1_st)
   int k23 = 1;        // fused K2+K3 variant: 1 = sliding window (k_iter23_sw), 0 = tiles (k_iter23_st)
   int staged = 0;     // DIA with a small halo: halo-staged K1 and fused K2+K3 (k_iter1_st, k_iter23_st)
@@ -1267,7 +1548,9 @@ int launch_iteration(sg_pcg* h, cudaStream_t s, int par, bool refresh, cudaEvent
     const bool st = FMT >= 1 && h->staged;
     const size_t tile = (size_t)PR * kRpt, H = (size_t)h->D.dia.halo;
     const unsigned gr = (unsigned)h->nrng;
-    if (st && h->k1sw) {
+    const bool strip = FMT >= 1 && ND == 5 && h->strip;
+    if (strip) k_iter1_s5<FS><<<gr, PR, Strip1<FS>::SMEM, s>>>(h->D, par);
+    else if (st && h->k1sw) {
       if (H <= PR) k_iter1_sw<FS, NS, 1><<<gr, PR, Sw1<FS, NS, 1>::SMEM, s>>>(h->D, par);
       else k_iter1_sw<FS, NS, 2><<<gr, PR, Sw1<FS, NS, 2>::SMEM, s>>>(h->D, par);
     } else if (st && H <= PR) k_iter1_st<FS, NS, 1><<<g, PR, (tile + 2 * H) * sizeof(double), s>>>(h->D, par);
@@ -1275,8 +1558,10 @@ int launch_iteration(sg_pcg* h, cudaStream_t s, int par, bool refresh, cudaEvent
     else k_iter1<PRE, FMT, ND, SH><<<g, PR, 0, s>>>(h->D, par);
     ++k;
     if (ev) SG_CUDA(cudaEventRecordWithFlags(ev[1], s, cudaEventRecordExternal));
-    if (st && !refresh && PRE == SG_PRECOND_LEARNED) {  // K2 + K3 fused
-      if (h->k23 == 1) {
+    if ((st || strip) && !refresh && PRE == SG_PRECOND_LEARNED) {  // K2 + K3 fused
+      if (strip) {
+        k_iter23_s5<<<gr, PR, Strip23::SMEM, s>>>(h->D, par);
+      } else if (h->k23 == 1) {
         if (H <= PR) k_iter23_sw<NS, 1><<<gr, PR, Sw23<NS, 1>::SMEM, s>>>(h->D, par);
         else k_iter23_sw<NS, 2><<<gr, PR, Sw23<NS, 2>::SMEM, s>>>(h->D, par);
       } else {
@@ -1430,8 +1715,19 @@ int setup_dia(sg_pcg* h, const int32_t* a_offs, const int32_t* a_cols, const int
   dia.halo = (int)halo;
   const char* ns = getenv("SG_PCG_NOSTAGE");
   h->staged = (halo <= kMaxStageHalo && !(ns && ns[0] == '1')) ? 1 : 0;
+  // wide 5-point grid (offsets {-W, -1, 0, 1, W}): line-strip streaming instead of 1-D rings
+  dia.W = 0;
+  h->strip = 0;
+  if (!h->staged && cnt == 5 && !(ns && ns[0] == '1') && offs[0] == -offs[4] && offs[1] == -1 && offs[2] == 0 &&
+      offs[3] == 1 && offs[4] % 16 == 0) {
+    const long long W = offs[4];
+    bool ok = true;
+    for (int k = 0; k < h->S; ++k) ok = ok && (h->sys_start[k + 1] - h->sys_start[k]) % W == 0;
+    if (ok) { dia.W = (int)W; h->strip = 1; }
+  }
   long long guard = halo;
   if (h->staged) guard = std::max<long long>(guard, (2 * ((halo + kSwC - 1) / kSwC) + 1) * kSwC + 16);
+  if (h->strip) guard = std::max<long long>(guard, 2LL * dia.W + 64);
   guard = (guard + 31) / 32 * 32;                // 256-byte alignment of every row-0 pointer
   const long long ld = (n + 2 * guard + 31) / 32 * 32;
   const size_t vbytes = (size_t)cnt * ld * sizeof(double);
@@ -1465,6 +1761,15 @@ int sw_attr(int* per_sm) {
   SG_CUDA(cudaFuncSetAttribute(k_iter1_sw<2, ND, NH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)Sw1<2, ND, NH>::SMEM));
   SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_iter23_sw<ND, NH>, PR, Sw23<ND, NH>::SMEM));
+  if (*per_sm < 1) *per_sm = 1;
+  return SG_OK;
+}
+
+int strip_setup(int* per_sm) {
+  SG_CUDA(cudaFuncSetAttribute(k_iter23_s5, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Strip23::SMEM));
+  SG_CUDA(cudaFuncSetAttribute(k_iter1_s5<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Strip1<1>::SMEM));
+  SG_CUDA(cudaFuncSetAttribute(k_iter1_s5<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Strip1<2>::SMEM));
+  SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_iter23_s5, PR, Strip23::SMEM));
   if (*per_sm < 1) *per_sm = 1;
   return SG_OK;
 }
@@ -1561,6 +1866,23 @@ extern "C" int sg_pcg_create(sg_pcg** out, int32_t n_systems, const int64_t* sys
     }
     const char* rl = getenv("SG_SW_RANGE");
     if (rl && atoll(rl) > 0) rng_len = atoll(rl);
+  } else if (h->strip) {  // (strip, line range) units; rng_len counts LINES
+    int per_sm = 1;
+    int rc = strip_setup(&per_sm);
+    if (rc) { delete h; return rc; }
+    const long long resident = (long long)h->num_sms * per_sm;
+    const long long W = h->D.dia.W, nstrip = (W + kStripC - 1) / kStripC;
+    long long maxl = 1;
+    for (int k = 0; k < n_systems; ++k) maxl = std::max<long long>(maxl, (h->sys_start[k + 1] - h->sys_start[k]) / W);
+    double best = 1e300;
+    for (long long m = 1; m <= std::min<long long>(maxl, 1024); ++m) {
+      const long long len = (maxl + m - 1) / m;
+      const double waves = (double)((n_systems * nstrip * m + resident - 1) / resident);
+      const double cost = waves * (double)(len + 4);
+      if (cost < best * 0.999) { best = cost; rng_len = len; }
+    }
+    const char* rl = getenv("SG_SW_RANGE");
+    if (rl && atoll(rl) > 0) rng_len = atoll(rl);
   } else {
     rng_len = 1LL << 62;
   }
@@ -1568,6 +1890,15 @@ extern "C" int sg_pcg_create(sg_pcg** out, int32_t n_systems, const int64_t* sys
   std::vector<int> rng_sys, sys_rng0;
   for (int k = 0; k < n_systems; ++k) {
     sys_rng0.push_back((int)rng_r0.size());
+    if (h->strip) {
+      const long long W = h->D.dia.W, nl = (h->sys_start[k + 1] - h->sys_start[k]) / W;
+      for (long long y = 0; y < nl; y += rng_len)
+        for (long long x = 0; x < W; x += kStripC) {
+          rng_r0.push_back(h->sys_start[k] + y * W + x);
+          rng_sys.push_back(k);
+        }
+      continue;
+    }
     for (int64_t r = h->sys_start[k]; r < h->sys_start[k + 1]; r += rng_len) {
       rng_r0.push_back(r);
       rng_sys.push_back(k);
@@ -1818,7 +2149,7 @@ extern "C" int sg_pcg_stats(sg_pcg* h, int64_t* kernels_host, int64_t* chunks_ho
     prof_host[4] = h->prof_samples;
     prof_host[5] = h->dia_nd;
     prof_host[6] = h->a_sym;
-    prof_host[7] = h->staged && h->pre == SG_PRECOND_LEARNED ? 1.0 : 0.0;
+    prof_host[7] = (h->staged || h->strip) && h->pre == SG_PRECOND_LEARNED ? 1.0 : 0.0;
   }
   if (reset) {
     h->kernels = h->chunks = 0;

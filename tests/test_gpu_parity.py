@@ -435,3 +435,26 @@ def test_solve_batch_stream_matches_solve_batch():
         for rw, (k, conv, x) in zip(w, g_):
             assert rw.k == k and rw.converged == conv
             assert np.array_equal(rw.x, x)
+
+
+def test_pcg_wide_grid_strip_kernels():
+    """5-point grids wider than the 1-D ring (W > 512) run the 2-D strip kernels
+    (k_iter1_s5 / k_iter23_s5), including a partial last strip (W = 784)."""
+    import os
+    m = P.load_checkpoint(os.path.join(os.path.dirname(__file__), "golden", "trained_heat16.spaignn"))
+    for nx, ny, seed in ((1024, 24, 3), (784, 20, 5)):
+        A, meta = P.gen_poisson2d(nx, ny, coeff_seed=seed)
+        G = P.forward(m, P.build_graph(A, meta)).G
+        M = P.build_learned_spai(G, m.config.epsilon)
+        b = P.gen_rhs(meta, seed + 100)
+        rep = P.pcg_solve(A, b, M, P.SolveConfig(rtol=1e-8))
+        from paper_2510_27517_b200.pcg import _handle_for
+        assert _handle_for(A, M).stats()[2][7] == 1.0  # K2 + K3 ran fused
+        o, c, v = (np.asarray(A.row_offsets), np.asarray(A.col_indices), np.asarray(A.values))
+        gv = np.asarray(G.values)
+        _, k, conv, _ = O.pcg_solve(o, c, v, b, lambda r: O.learned_apply(A.n_rows, o, c, gv, m.config.epsilon, r),
+                                    rtol=1e-8)
+        assert rep.converged and conv
+        assert _k_close(rep.k, k), (nx, rep.k, k)
+        res = np.linalg.norm(b - O.spmv(o, c, v, rep.x)) / np.linalg.norm(b)
+        assert res <= 1e-8 * 1.01, (nx, res)
