@@ -27,7 +27,7 @@ sys.path.insert(0, ROOT)
 
 def main():
     p = argparse.ArgumentParser()
-    p.add_argument("--config", default="c1", choices=["c1", "c3", "c5"])
+    p.add_argument("--config", default="c1", choices=["c1", "c3", "c4", "c5"])
     p.add_argument("--steps", type=int, default=3)
     p.add_argument("--warmup", type=int, default=1)
     p.add_argument("--max-iters", type=int, default=None)
@@ -51,6 +51,23 @@ def main():
         model = P.init_model(P.GnnConfig(d_node=2, seed=0))
         b = P.gen_rhs(meta, 10**6)
         desc = "C3: 3D Poisson 7-point 128^3 (n=2,097,152), algebraic features, random-init GNN (d_node=2), PCG rtol 1e-6"
+    elif a.config == "c4":
+        from paper_2510_27517_b200.sparse import pad_to_pattern, pattern_square
+        t0 = time.perf_counter()
+        A = P.rand_spd_sparse(10**6, np.random.default_rng(0), extra_per_row=10)
+        t_gen = time.perf_counter() - t0
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        Pq = pattern_square(A)
+        Ap = pad_to_pattern(A, Pq)
+        torch.cuda.synchronize()
+        t_pat = time.perf_counter() - t0
+        meta = None
+        model = P.init_model(P.GnnConfig(d_node=2, seed=0))
+        b = P.gen_rhs(A.n_rows, 10**6)
+        desc = (f"C4: rand_spd_sparse(n=1e6, extra_per_row=10) (nnz {A.nnz}), G on the A^2 pattern (nnz {Pq.nnz}), "
+                f"graph on A padded to it, random-init GNN (d_node=2), PCG rtol 1e-6 (generation {t_gen:.1f} s host+GPU, "
+                f"A^2 pattern + padding {1000 * t_pat:.0f} ms GPU)")
     else:
         A, meta = P.gen_poisson2d(2048, 2048)
         model = P.load_checkpoint(os.path.join(ROOT, "tests", "golden", "trained_heat16.spaignn"))
@@ -61,7 +78,7 @@ def main():
     w_dev = torch.as_tensor(np.random.default_rng(0).standard_normal(A.n_rows), device=dev)
 
     def step(profile=False):
-        g = P.build_graph(A, meta if a.config != "c3" else None)
+        g = P.build_graph(Ap if a.config == "c4" else A, meta if a.config not in ("c3", "c4") else None)
         G = P.forward(model, g).G
         M = P.build_learned_spai(G, model.config.epsilon)
         if profile:
@@ -89,17 +106,20 @@ def main():
     h = _handle_for(A, M)
     kernels, chunks, prof = h.stats()
     n, nnz = A.n_rows, A.nnz
-    it_bytes = 36 * nnz + 124 * n  # SURVEY.md §8(d) B_iter (fp64 values, int32 indices)
+    nnz_g = Ap.nnz if a.config == "c4" else nnz  # G (and G^T) live on the A^2 pattern for C4
+    # SURVEY.md §8(d) B_iter (fp64 values, int32 indices): A once, G^T and G once each, vectors
+    it_bytes = (12 * nnz + 4 * (n + 1)) + 2 * (12 * nnz_g + 4 * (n + 1)) + 112 * n
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     peak = float(peaks.get("hbm_gbs", 6650.0))
     per_k = {}
     if prof[4] > 0:
         csr = 12 * nnz + 4 * (n + 1)
+        csr_g = 12 * nnz_g + 4 * (n + 1)
         if prof[7]:  # K2 + K3 fused (t stays on chip)
-            per_sys = {"k_iter1": csr + 32 * n, "k_iter23": csr + 56 * n}
+            per_sys = {"k_iter1": csr + 32 * n, "k_iter23": csr_g + 56 * n}
         else:
-            per_sys = {"k_iter1": csr + 32 * n, "k_iter2": csr + 56 * n, "k_iter3": csr + 24 * n}
+            per_sys = {"k_iter1": csr + 32 * n, "k_iter2": csr_g + 56 * n, "k_iter3": csr_g + 24 * n}
         for (name, by), ms in zip(per_sys.items(), prof[:3]):
             avg = ms / prof[4]
             per_k[name] = {"avg_ms": avg, "gbs": by / (avg * 1e-3) / 1e9, "frac": by / (avg * 1e-3) / 1e9 / peak}
@@ -111,7 +131,7 @@ def main():
            "pcg_us_per_iteration": rep.t_cg_total_ns / 1e3 / max(rep.k, 1),
            "iteration_gbs_survey_bytes": it_bytes * rep.k / (rep.t_cg_total_ns * 1e-9) / 1e9,
            "storage": f"DIA ({int(prof[5])} diagonals)" if prof[5] else "CSR", "per_kernel": per_k,
-           "peak_gbs": peak, "n": n, "nnz": nnz}
+           "peak_gbs": peak, "n": n, "nnz": nnz, "nnz_G": nnz_g}
     if loss is not None:
         torch.cuda.synchronize()
         t0 = time.perf_counter()

@@ -291,7 +291,7 @@ __host__ __device__ constexpr int edge_smem_doubles(int L) {
 }
 
 template <int D, int ACT>
-__global__ void __launch_bounds__(128) k_edge_pass(GnnP p, int64_t nnz, const int32_t* __restrict__ rows,
+__global__ void __launch_bounds__(256) k_edge_pass(GnnP p, int64_t nnz, const int32_t* __restrict__ rows,
                                                    const int32_t* __restrict__ cols,
                                                    const double* __restrict__ ef,
                                                    const double* __restrict__ EPQ, int64_t n,
@@ -366,9 +366,9 @@ __global__ void __launch_bounds__(128) k_edge_pass(GnnP p, int64_t nnz, const in
   }
 }
 
-static int grid_for(int64_t rows, int per_sm) {
+static int grid_for(int64_t rows, int per_sm, int warps = 4) {
   const int64_t groups = (rows + 7) / 8;       // 8 rows per warp
-  int64_t b = (groups + 3) / 4;                // 4 warps per CTA
+  int64_t b = (groups + warps - 1) / warps;    // warps per CTA
   const int64_t cap = 148LL * per_sm;
   return (int)(b > cap ? cap : (b < 1 ? 1 : b));
 }
@@ -397,7 +397,8 @@ int run_forward(const GnnP& p, int64_t n, int64_t nnz, const int32_t* offs, cons
     return SG_EUNSUPPORTED;
   }
   SG_CUDA(cudaFuncSetAttribute(k_edge_pass<D, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_edge_pass<D, ACT><<<grid_for(nnz, 8), 128, smem, s>>>(p, nnz, rows, cols, ef, EPQ, n, g);
+  // 8 warps per CTA share one copy of the edge weights in shared memory (4 CTAs / SM)
+  k_edge_pass<D, ACT><<<grid_for(nnz, 4, 8), 256, smem, s>>>(p, nnz, rows, cols, ef, EPQ, n, g);
   SG_LAUNCH_CHECK("k_edge_pass");
   return SG_OK;
 }
