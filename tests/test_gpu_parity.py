@@ -458,3 +458,42 @@ def test_pcg_wide_grid_strip_kernels():
         assert _k_close(rep.k, k), (nx, rep.k, k)
         res = np.linalg.norm(b - O.spmv(o, c, v, rep.x)) / np.linalg.norm(b)
         assert res <= 1e-8 * 1.01, (nx, res)
+
+
+def test_pcg_3d_small_sliding_window():
+    """7-point 3-D grid with a small halo (8x8x6: offsets +-1, +-8, +-64) runs the 1-D
+    sliding-window kernels with ND = 7 (A by its lower half); k and x against the oracle."""
+    A, meta = P.gen_poisson3d(8, 8, 6)
+    m = P.init_model(P.GnnConfig(d_node=2, seed=0))
+    G = P.forward(m, P.build_graph(A)).G
+    M = P.build_learned_spai(G, m.config.epsilon)
+    b = P.gen_rhs(A.n_rows, 7)
+    rep = P.pcg_solve(A, b, M, P.SolveConfig(rtol=1e-8))
+    from paper_2510_27517_b200.pcg import _handle_for
+    st = _handle_for(A, M).stats()[2]
+    assert st[5] == 7 and st[7] == 1.0  # DIA with 7 diagonals, K2 + K3 fused
+    o, c, v = (np.asarray(A.row_offsets), np.asarray(A.col_indices), np.asarray(A.values))
+    _, k, conv, _ = O.pcg_solve(o, c, v, b, lambda r: O.learned_apply(A.n_rows, o, c, np.asarray(G.values),
+                                                                    m.config.epsilon, r), rtol=1e-8)
+    assert rep.converged == conv and _k_close(rep.k, k), (rep.k, k)
+    assert np.linalg.norm(b - O.spmv(o, c, v, rep.x)) / np.linalg.norm(b) <= 1.01e-8
+
+
+def test_batch_mixed_grids_unaligned_systems():
+    """A batch of differently sized grids (system sizes not multiples of 16, so sliding-window
+    ranges start unaligned; the union of diagonal offsets has 7 entries, each system using 5)."""
+    import os
+    m = P.load_checkpoint(os.path.join(os.path.dirname(__file__), "golden", "trained_heat16.spaignn"))
+    systems = [P.gen_poisson2d(17, 13, coeff_seed=1), P.gen_poisson2d(23, 19, coeff_seed=2),
+               P.gen_poisson2d(17, 11, coeff_seed=3)]
+    As, metas = [A for A, _ in systems], [meta for _, meta in systems]
+    bs = [P.gen_rhs(meta, 50 + s) for s, meta in enumerate(metas)]
+    cfg = P.SolveConfig(rtol=1e-8)
+    reps = P.solve_batch(As, bs, m, metas=metas, cfg=cfg)
+    for (A, meta), b, rb in zip(systems, bs, reps):
+        G = P.forward(m, P.build_graph(A, meta)).G
+        o, c, v = (np.asarray(A.row_offsets), np.asarray(A.col_indices), np.asarray(A.values))
+        _, k, conv, _ = O.pcg_solve(o, c, v, b, lambda r: O.learned_apply(A.n_rows, o, c, np.asarray(G.values),
+                                                                        m.config.epsilon, r), rtol=1e-8)
+        assert rb.converged == conv and _k_close(rb.k, k), (rb.k, k)
+        assert np.linalg.norm(b - O.spmv(o, c, v, rb.x)) / np.linalg.norm(b) <= 1.01e-8
