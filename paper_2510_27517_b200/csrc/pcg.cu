@@ -40,7 +40,7 @@ constexpr int PR = 256;    // rows per tile (= threads per CTA)
 constexpr int PCAP = 2048; // staged nonzeros per tile (8 per row on average)
 constexpr int MAXD = 8;    // DIA: max diagonals
 constexpr int kMaxStageHalo = 512;  // DIA halo staging: shared memory <= 48 KB per CTA
-constexpr int kSwC = PR;              // sliding window: rows per chunk (one per thread)
+constexpr int kSwC = PR;              // sliding window: rows per chunk
 constexpr int kRpt = 4;    // DIA: rows per thread (tile = PR * kRpt rows; amortises the
                            // per-tile reduction and keeps more independent loads in flight)
 
@@ -911,17 +911,24 @@ __host__ __device__ constexpr int pow2ceil(int v) {
 template <int ND, int NH>
 struct Sw23 {
   static constexpr int C = kSwC;
-  static constexpr int P = 2;                            // chunks in flight (incl. the current one)
-  static constexpr int RING = pow2ceil((P + 2 * NH) * C);  // ring rows (G, mask, r', t)
-  static constexpr int RM = RING - 1;
-  // bytes: G [ND][RING] | r' [RING] | t [RING] | staging [P][4][C] (r q x d) | mask [RING]
-  static constexpr size_t SMEM = (size_t)(ND + 2) * RING * 8 + (size_t)P * 4 * C * 8 + RING;
+  static constexpr int P = 3;              // chunks in flight (incl. the current one)
+  static constexpr int NG = P + 2 * NH;    // ring chunks of G, mask and r' (r lands in place)
+  static constexpr int NT = 2 * NH + 1;    // ring chunks of t
+  static constexpr int GR = NG * C, TR = NT * C;
+  // bytes: G [ND][GR] | r' [GR] | t [TR] | q staging [P][C] | mask [GR]
+  static constexpr size_t SMEM = (size_t)(ND + 1) * GR * 8 + (size_t)TR * 8 + (size_t)P * C * 8 + GR;
 };
+
+// Ring index of a neighbour: base + tid + off lies within one ring length of [0, R).
+__device__ __forceinline__ int ring_wrap(int x, int R) {
+  x = x < 0 ? x + R : x;
+  return x >= R ? x - R : x;
+}
 
 template <int ND, int NH>
 __global__ void __launch_bounds__(PR, 1) k_iter23_sw(Dev D, int par) {
   using G = Sw23<ND, NH>;
-  constexpr int C = G::C, P = G::P, RING = G::RING, RM = G::RM;
+  constexpr int C = G::C, P = G::P, NG = G::NG, NT = G::NT, GR = G::GR, TR = G::TR;
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ __align__(8) uint64_t bars[P];
   __shared__ double red[PR / 32];
@@ -938,38 +945,29 @@ __global__ void __launch_bounds__(PR, 1) k_iter23_sw(Dev D, int par) {
   const double* dn = par ? D.d0 : D.d1;
   const double* rc = par ? D.r1 : D.r0;
   double* rn = par ? D.r0 : D.r1;
-  double* gr = reinterpret_cast<double*>(smraw);  // [ND][RING]
-  double* rp = gr + ND * RING;                      // [RING]
-  double* tr = rp + RING;                           // [RING]
-  double* stg = tr + RING;                          // [P][4][C]
-  unsigned char* mk = reinterpret_cast<unsigned char*>(stg + P * 4 * C);  // [RING]
+  double* gr = reinterpret_cast<double*>(smraw);  // [ND][GR]
+  double* rp = gr + ND * GR;                        // [GR]  r (bulk copy) -> r' in place
+  double* tr = rp + GR;                             // [TR]
+  double* qs = tr + TR;                             // [P][C]
+  unsigned char* mk = reinterpret_cast<unsigned char*>(qs + P * C);  // [GR]
   // chunk k covers rows LB + k*C ..; LB 16-row aligned so every bulk copy is 16-byte aligned
   const long long LB = (R0 & ~15LL) - 2LL * NH * C;
   const int m1 = (int)((R1 - LB + C - 1) / C) - 1;  // last output chunk
   const int K = m1 + 2 * NH + 1;                     // steps
-  // system / range bounds relative to LB (32-bit compares in the loop)
   auto rel = [&](long long v) { return (int)(v - LB < -1 ? -1 : (v - LB > (1LL << 30) ? (1LL << 30) : v - LB)); };
   const int s0r = rel(s0), s1r = rel(s1), R0r = rel(R0), R1r = rel(R1);
   int off[ND];
 #pragma unroll
   for (int d = 0; d < ND; ++d) off[d] = D.dia.off[d];
   auto issue = [&](int k) {
-    const int ss = k % P, gs = (k * C) & RM;
-    double* st = stg + ss * 4 * C;
+    const int ss = k % P, gs = (k % NG) * C;
     const long long row = LB + (long long)k * C;
-    const bool own = k >= 4 * NH;
-    const uint32_t bytes = (uint32_t)((2 + ND + (own ? 2 : 0)) * C * 8 + C);
-    mbar_arrive_expect_tx(&bars[ss], bytes);
-    bulk_g2s(st, rc + row, C * 8, &bars[ss]);
-    bulk_g2s(st + C, D.q + row, C * 8, &bars[ss]);
+    mbar_arrive_expect_tx(&bars[ss], (uint32_t)((2 + ND) * C * 8 + C));
+    bulk_g2s(rp + gs, rc + row, C * 8, &bars[ss]);
+    bulk_g2s(qs + ss * C, D.q + row, C * 8, &bars[ss]);
 #pragma unroll
-    for (int d = 0; d < ND; ++d) bulk_g2s(gr + d * RING + gs, D.dia.gv[d] + row, C * 8, &bars[ss]);
+    for (int d = 0; d < ND; ++d) bulk_g2s(gr + d * GR + gs, D.dia.gv[d] + row, C * 8, &bars[ss]);
     bulk_g2s(mk + gs, D.dia.mask + row, C, &bars[ss]);
-    if (own) {
-      const long long ro = row - 2LL * NH * C;
-      bulk_g2s(st + 2 * C, D.x + ro, C * 8, &bars[ss]);
-      bulk_g2s(st + 3 * C, dn + ro, C * 8, &bars[ss]);
-    }
   };
   if (tid == 0) {
 #pragma unroll
@@ -977,54 +975,59 @@ __global__ void __launch_bounds__(PR, 1) k_iter23_sw(Dev D, int par) {
     mbar_init_fence();
   }
   __syncthreads();
-  if (tid == 0) issue(0);
+  if (tid == 0)
+    for (int k = 0; k < P - 1 && k < K; ++k) issue(k);
   double prr = 0.0, prs = 0.0;
   for (int k = 0; k < K; ++k) {
-    const double* st = stg + (k % P) * 4 * C;
+    // x, d of this step's output chunk: plain loads, in flight across the wait and phases A, B
+    const int mm = k - 2 * NH;
+    const int li = mm * C + tid;
+    const bool own_c = mm >= 2 * NH && li >= R0r && li < R1r;
+    double xo = 0.0, dd = 0.0;
+    if (own_c) {
+      xo = D.x[LB + li];
+      dd = __ldg(dn + LB + li);
+    }
     mbar_wait(&bars[k % P], (uint32_t)((k / P) & 1));
-    {  // A: r' of the lead chunk
-      const int lj = k * C + tid;
-      double v = sub(st[tid], mul(alpha, st[C + tid]));
+    {  // A: r' of the lead chunk, in place over its r
+      const int lj = k * C + tid, ix = (k % NG) * C + tid;
+      double v = sub(rp[ix], mul(alpha, qs[(k % P) * C + tid]));
       v = (lj >= s0r && lj < s1r) ? v : 0.0;
       if (lj >= R0r && lj < R1r) {
         rn[LB + lj] = v;
         prr += mul(v, v);
       }
-      rp[lj & RM] = v;
+      rp[ix] = v;
     }
     __syncthreads();
-    if (tid == 0 && k + 1 < K) issue(k + 1);
+    if (tid == 0 && k + P - 1 < K) issue(k + P - 1);
     const int u = k - NH;
     if (u >= NH) {  // B: t of chunk u (add.at order over G's mirror diagonals)
-      const int lj = u * C + tid;
-      const unsigned int m = mk[lj & RM];
+      const int lj = u * C + tid, base = (u % NG) * C + tid;
+      const unsigned int m = mk[base];
       double p[ND];
 #pragma unroll
       for (int d = 0; d < ND; ++d) {
-        const int ix = (lj + off[d]) & RM;
-        p[d] = mul(gr[(ND - 1 - d) * RING + ix], rp[ix]);
+        const int ix = ring_wrap(base + off[d], GR);
+        p[d] = mul(gr[(ND - 1 - d) * GR + ix], rp[ix]);
       }
       const double v = combine_seq<ND>(p, m);
-      tr[lj & RM] = (lj >= s0r && lj < s1r) ? v : 0.0;
+      tr[(u % NT) * C + tid] = (lj >= s0r && lj < s1r) ? v : 0.0;
     }
     __syncthreads();
-    const int mm = k - 2 * NH;
-    if (mm >= 2 * NH) {  // C: s and x of chunk mm (its x, d travelled with lead chunk k)
-      const int li = mm * C + tid;
-      if (li >= R0r && li < R1r) {
-        const long long i = LB + li;
-        D.x[i] = add(st[2 * C + tid], mul(alpha, st[3 * C + tid]));
-        const int io = li & RM;
-        const unsigned int m = mk[io];
-        double p[ND];
+    if (own_c) {  // C: s and x of chunk mm
+      const long long i = LB + li;
+      D.x[i] = add(xo, mul(alpha, dd));
+      const int io = (mm % NG) * C + tid, tb = (mm % NT) * C + tid;
+      const unsigned int m = mk[io];
+      double p[ND];
 #pragma unroll
-        for (int d = 0; d < ND; ++d) p[d] = mul(gr[d * RING + io], tr[(li + off[d]) & RM]);
-        const double y = combine_numpy<ND>(p, m);
-        const double rni = rp[io];
-        const double si = add(y, mul(eps, rni));
-        D.s[i] = si;
-        prs += mul(rni, si);
-      }
+      for (int d = 0; d < ND; ++d) p[d] = mul(gr[d * GR + io], tr[ring_wrap(tb + off[d], TR)]);
+      const double y = combine_numpy<ND>(p, m);
+      const double rni = rp[io];
+      const double si = add(y, mul(eps, rni));
+      D.s[i] = si;
+      prs += mul(rni, si);
     }
   }
   if (arrive(D, D.sys_rng0, sys, prr, prs, red, &flag)) {
