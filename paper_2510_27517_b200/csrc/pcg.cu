@@ -1050,20 +1050,20 @@ __global__ void __launch_bounds__(PR, 1) k_iter23_sw(Dev D, int par) {
 template <int FMT, int ND, int NH>
 struct Sw1 {
   static constexpr int C = kSwC;
-  static constexpr int P = 3;                              // chunks in flight (incl. the current one)
+  static constexpr int P = 4;                              // chunks in flight (incl. the current one)
   static constexpr int NA = FMT == 2 ? ND / 2 + 1 : ND;   // diagonals streamed
-  static constexpr int RING = pow2ceil((P + NH) * C);      // A / mask ring: chunks u .. k + P - 1
-  static constexpr int RM = RING - 1;
+  static constexpr int NR = P + NH;                        // A / mask ring chunks: u .. k + P - 1
+  static constexpr int RING = NR * C;
   static constexpr int DRING = pow2ceil((2 * NH + 2) * C); // d' ring: chunks u - NH .. k + 1
   static constexpr int DM = DRING - 1;
-  // bytes: A [NA][RING] | d' [DRING] | staging [P][2][C] (s d) | mask [RING]
+  // bytes: A [NA][RING] | d' [DRING] | staging [P][2][C] (s, d) | mask [RING]
   static constexpr size_t SMEM = (size_t)NA * RING * 8 + (size_t)DRING * 8 + (size_t)P * 2 * C * 8 + RING;
 };
 
 template <int FMT, int ND, int NH>
 __global__ void __launch_bounds__(PR, 5) k_iter1_sw(Dev D, int par) {
   using G = Sw1<FMT, ND, NH>;
-  constexpr int C = G::C, P = G::P, NA = G::NA, RING = G::RING, RM = G::RM, DM = G::DM;
+  constexpr int C = G::C, P = G::P, NA = G::NA, NR = G::NR, RING = G::RING, DM = G::DM;
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ __align__(8) uint64_t bars[P];
   __shared__ double red[PR / 32];
@@ -1097,7 +1097,7 @@ __global__ void __launch_bounds__(PR, 5) k_iter1_sw(Dev D, int par) {
 #pragma unroll
     for (int d = 0; d < ND; ++d) off[d] = D.dia.off[d];
     auto issue = [&](int k) {
-      const int ss = k % P, gs = (k * C) & RM;
+      const int ss = k % P, gs = (k % NR) * C;
       double* st = stg + ss * 2 * C;
       const long long row = LB + (long long)k * C;
       mbar_arrive_expect_tx(&bars[ss], (uint32_t)((2 + NA) * C * 8 + C));
@@ -1131,12 +1131,12 @@ __global__ void __launch_bounds__(PR, 5) k_iter1_sw(Dev D, int par) {
       if (u >= 0) {  // q of chunk u
         const int li = u * C + tid;
         if (li >= R0r && li < R1r) {
-          const int io = li & RM;
+          const int io = (u % NR) * C + tid;
           const unsigned int m = mk[io];
           double p[ND];
 #pragma unroll
           for (int d = 0; d < ND; ++d) {
-            const int ix = (li + off[d]) & RM;
+            const int ix = ring_wrap(io + off[d], RING);
             // FMT 2: an upper entry (i, i+off) is the lower mirror entry at row i+off
             const double a = (FMT == 2 && d > ND / 2) ? ar[(ND - 1 - d) * RING + ix] : ar[d * RING + io];
             p[d] = mul(a, dp[(li + off[d]) & DM]);
