@@ -537,7 +537,9 @@ __global__ void __launch_bounds__(PR, FMT >= 1 ? 8 : 1) k_setup2(Dev D) {
   }
 }
 
-template <int PRE, int FMT, int ND, bool SH>
+// SPLIT (CSR with scattered columns): d' was written by k_pre_d, so A d' gathers one vector
+// instead of forming s + beta d from two gathers per nonzero.
+template <int PRE, int FMT, int ND, bool SH, bool SPLIT = false>
 __global__ void __launch_bounds__(PR, FMT >= 1 ? 8 : 1) k_iter1(Dev D, int par) {
   SG_KERNEL_PROLOGUE
   const int status = D.st[sys].status;
@@ -556,9 +558,15 @@ __global__ void __launch_bounds__(PR, FMT >= 1 ? 8 : 1) k_iter1(Dev D, int par) 
     if (i >= r1) continue;
     const unsigned int m = dmask(D, i, r1, FMT);
     if (run) {
-      const double dni = add(D.s[i], mul(beta, dc[i]));
-      dn[i] = dni;
-      const double qi = rowA<FMT, ND, SH, 1>(D, T, i, r0, m, XF{D.s, dc, beta});
+      double dni, qi;
+      if (SPLIT) {
+        dni = dn[i];
+        qi = rowA<FMT, ND, SH, 0>(D, T, i, r0, m, XF{dn, nullptr, 0.0});
+      } else {
+        dni = add(D.s[i], mul(beta, dc[i]));
+        dn[i] = dni;
+        qi = rowA<FMT, ND, SH, 1>(D, T, i, r0, m, XF{D.s, dc, beta});
+      }
       D.q[i] = qi;
       pdq += mul(dni, qi);
     }
@@ -575,7 +583,8 @@ __global__ void __launch_bounds__(PR, FMT >= 1 ? 8 : 1) k_iter1(Dev D, int par) 
   }
 }
 
-template <int PRE, int FMT, int ND, bool SH>
+// SPLIT: r' was written by k_pre_r (with the x update), so G^T r' gathers one vector.
+template <int PRE, int FMT, int ND, bool SH, bool SPLIT = false>
 __global__ void __launch_bounds__(PR, FMT >= 1 ? 8 : 1) k_iter2(Dev D, int par) {
   SG_KERNEL_PROLOGUE
   if (D.st[sys].status != ST_RUN) return;
@@ -590,15 +599,48 @@ __global__ void __launch_bounds__(PR, FMT >= 1 ? 8 : 1) k_iter2(Dev D, int par) 
     const long long i = r0 + (long long)rr * PR + threadIdx.x;
     if (i >= r1) continue;
     const unsigned int m = dmask(D, i, r1, FMT);
-    D.x[i] = add(D.x[i], mul(alpha, dn[i]));
-    const double rni = sub(rc[i], mul(alpha, D.q[i]));
-    rn[i] = rni;
+    double rni;
+    if (SPLIT) {
+      rni = rn[i];
+    } else {
+      D.x[i] = add(D.x[i], mul(alpha, dn[i]));
+      rni = sub(rc[i], mul(alpha, D.q[i]));
+      rn[i] = rni;
+    }
     prr += mul(rni, rni);
-    if (PRE == SG_PRECOND_LEARNED) D.t[i] = rowGt<FMT, ND, SH, 2>(D, T, i, r0, m, XF{rc, D.q, alpha});
+    if (PRE == SG_PRECOND_LEARNED) {
+      if (SPLIT) D.t[i] = rowGt<FMT, ND, SH, 0>(D, T, i, r0, m, XF{rn, nullptr, 0.0});
+      else D.t[i] = rowGt<FMT, ND, SH, 2>(D, T, i, r0, m, XF{rc, D.q, alpha});
+    }
   }
   if (arrive(D, sys, prr, 0.0, red, &flag)) {
     const double rr = gather_partials(D, sys, 0, red);
     if (threadIdx.x == 0) fin_rr(D, sys, rr);
+  }
+}
+
+// Elementwise halves of K1 / K2 for the SPLIT path: d' = s + beta d; x += alpha d', r' = r - alpha q.
+__global__ void __launch_bounds__(PR) k_pre_d(Dev D, int par) {
+  int sys; long long r0, r1;
+  block_rows(D, sys, r0, r1);
+  if (D.st[sys].status != ST_RUN) return;
+  const double beta = D.st[sys].beta;
+  const double* dc = par ? D.d1 : D.d0;
+  double* dn = par ? D.d0 : D.d1;
+  for (long long i = r0 + threadIdx.x; i < r1; i += PR) dn[i] = add(D.s[i], mul(beta, dc[i]));
+}
+
+__global__ void __launch_bounds__(PR) k_pre_r(Dev D, int par) {
+  int sys; long long r0, r1;
+  block_rows(D, sys, r0, r1);
+  if (D.st[sys].status != ST_RUN) return;
+  const double alpha = D.st[sys].alpha;
+  const double* dn = par ? D.d0 : D.d1;
+  const double* rc = par ? D.r1 : D.r0;
+  double* rn = par ? D.r0 : D.r1;
+  for (long long i = r0 + threadIdx.x; i < r1; i += PR) {
+    D.x[i] = add(D.x[i], mul(alpha, dn[i]));
+    rn[i] = sub(rc[i], mul(alpha, D.q[i]));
   }
 }
 
@@ -1558,7 +1600,10 @@ int launch_iteration(sg_pcg* h, cudaStream_t s, int par, bool refresh, cudaEvent
       else k_iter1_sw<FS, NS, 2><<<gr, PR, Sw1<FS, NS, 2>::SMEM, s>>>(h->D, par);
     } else if (st && H <= PR) k_iter1_st<FS, NS, 1><<<g, PR, (tile + 2 * H) * sizeof(double), s>>>(h->D, par);
     else if (st) k_iter1_st<FS, NS, 2><<<g, PR, (tile + 2 * H) * sizeof(double), s>>>(h->D, par);
-    else k_iter1<PRE, FMT, ND, SH><<<g, PR, 0, s>>>(h->D, par);
+    else if (FMT == 0 && !SH) {  // CSR, long rows: d' first, then one gather per nonzero
+      k_pre_d<<<g, PR, 0, s>>>(h->D, par); ++k;
+      k_iter1<PRE, FMT, ND, SH, true><<<g, PR, 0, s>>>(h->D, par);
+    } else k_iter1<PRE, FMT, ND, SH><<<g, PR, 0, s>>>(h->D, par);
     ++k;
     if (ev) SG_CUDA(cudaEventRecordWithFlags(ev[1], s, cudaEventRecordExternal));
     if ((st || strip) && !refresh && PRE == SG_PRECOND_LEARNED) {  // K2 + K3 fused
@@ -1580,7 +1625,10 @@ int launch_iteration(sg_pcg* h, cudaStream_t s, int par, bool refresh, cudaEvent
       *nk += k;
       return SG_OK;
     }
-    if (!refresh) {
+    if (!refresh && FMT == 0 && !SH) {
+      k_pre_r<<<g, PR, 0, s>>>(h->D, par); ++k;
+      k_iter2<PRE, FMT, ND, SH, true><<<g, PR, 0, s>>>(h->D, par); ++k;
+    } else if (!refresh) {
       k_iter2<PRE, FMT, ND, SH><<<g, PR, 0, s>>>(h->D, par); ++k;
     } else {
       k_refresh_x<<<g, PR, 0, s>>>(h->D, par); ++k;
