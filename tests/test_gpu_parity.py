@@ -497,3 +497,48 @@ def test_batch_mixed_grids_unaligned_systems():
                                                                         m.config.epsilon, r), rtol=1e-8)
         assert rb.converged == conv and _k_close(rb.k, k), (rb.k, k)
         assert np.linalg.norm(b - O.spmv(o, c, v, rb.x)) / np.linalg.norm(b) <= 1.01e-8
+
+
+def test_pcg_control_flow_on_sliding_window_kernels():
+    """The reference control-flow variants (refresh period, delta termination + certification,
+    max_iters, zero rhs, non-learned preconditioners) on a 5-point grid, i.e. through the
+    sliding-window K1 / fused K2+K3 kernels rather than the CSR ones the golden cases use."""
+    import os
+    m = P.load_checkpoint(os.path.join(os.path.dirname(__file__), "golden", "trained_heat16.spaignn"))
+    A, meta = P.gen_poisson2d(24, 24, coeff_seed=4)
+    G = P.forward(m, P.build_graph(A, meta)).G
+    o, c, v = (np.asarray(A.row_offsets), np.asarray(A.col_indices), np.asarray(A.values))
+    gv = np.asarray(G.values)
+    b = P.gen_rhs(meta, 99)
+    eps = m.config.epsilon
+    cases = [
+        ("learn_true", dict(rtol=1e-8), None),
+        ("learn_p1", dict(rtol=1e-8, period=1), None),
+        ("learn_p3", dict(rtol=1e-9, period=3), None),
+        ("learn_delta", dict(rtol=1e-9, termination="delta"), None),
+        ("learn_max5", dict(rtol=1e-12, max_iters=5), None),
+        ("learn_zero", dict(rtol=1e-8), "zero"),
+        ("ident", dict(rtol=1e-8), "ident"),
+    ]
+    for name, kw, special in cases:
+        bb = np.zeros_like(b) if special == "zero" else b
+        if special == "ident":
+            M = P.build_identity(A)
+            apply = lambda r: r.copy()  # noqa: E731
+        else:
+            M = P.build_learned_spai(G, eps)
+            apply = lambda r: O.learned_apply(A.n_rows, o, c, gv, eps, r)  # noqa: E731
+        cfg = P.SolveConfig(rtol=kw["rtol"], max_iters=kw.get("max_iters"),
+                            residual_refresh_period=kw.get("period", 50),
+                            termination=kw.get("termination", "true_residual"))
+        rep = P.pcg_solve(A, bb, M, cfg)
+        _, k, conv, hist = O.pcg_solve(o, c, v, bb, apply, rtol=kw["rtol"], max_iters=kw.get("max_iters"),
+                                       period=kw.get("period", 50),
+                                       termination=kw.get("termination", "true_residual"))
+        assert rep.converged == conv, name
+        assert _k_close(rep.k, k), (name, rep.k, k)
+        assert len(rep.residual_history) == rep.k + 1 or name == "learn_delta", name
+        if rep.k == k and special != "zero":
+            assert abs(rep.residual_history[0] - hist[0]) <= 1e-15, name
+        if special == "zero":
+            assert rep.k == 0 and np.all(rep.x == 0.0)
