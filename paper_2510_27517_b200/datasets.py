@@ -165,3 +165,45 @@ def rand_spd_sparse(n: int, rng, extra_per_row: int = 3) -> SparseMatrix:
     cols = np.concatenate([c, np.arange(n)])
     vals = np.concatenate([v, diag])
     return SparseMatrix.from_coo(n, n, rows, cols, vals)
+
+
+def write_rhs_vec(b, path) -> None:
+    """datasets.py:221-231: u64 little-endian length header, then f64 little-endian data; written
+    to `path.tmp` and renamed (atomic).  Accepts numpy arrays or device tensors."""
+    import os
+    import struct
+    try:
+        import torch
+        if isinstance(b, torch.Tensor):
+            b = b.detach().to("cpu").numpy()
+    except ImportError:  # pragma: no cover
+        pass
+    b = np.asarray(b, dtype=np.float64)
+    tmp = str(path) + ".tmp"
+    with open(tmp, "wb") as fh:
+        fh.write(struct.pack("<Q", len(b)))
+        fh.write(np.ascontiguousarray(b, dtype="<f8").tobytes())
+    os.replace(tmp, str(path))
+
+
+def read_rhs_vec(path, device: bool = False):
+    """datasets.py:234-242 (same header checks and ValueErrors).  device=True reads the payload
+    into page-locked memory and returns a device tensor (one asynchronous H2D copy)."""
+    import struct
+    with open(path, "rb") as fh:
+        raw = fh.read()
+    if len(raw) < 8:
+        raise ValueError("rhs file too short for its header")
+    (n,) = struct.unpack_from("<Q", raw, 0)
+    if len(raw) != 8 + 8 * n:
+        raise ValueError(f"rhs file length {len(raw)} does not match header count {n}")
+    b = np.frombuffer(raw, dtype="<f8", offset=8).astype(np.float64)
+    if not device:
+        return b
+    import torch
+    from . import _lib as L
+    host = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    host.numpy()[:] = b
+    out = L.empty(n, torch.float64)
+    out.copy_(host, non_blocking=True)
+    return out
