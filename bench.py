@@ -247,6 +247,8 @@ def run_ours(a, rank, world, local):
                     "traffic_source": traffic["source"] if traffic else None,
                     "achieved_physical": kern[dom].get("physical_gbs"),
                     "frac_physical": kern[dom].get("physical_frac"),
+                    "frac_vs_nominal_8tbs": kern[dom]["gbs"] / 8000.0,
+                    "frac_physical_vs_nominal_8tbs": (kern[dom].get("physical_gbs") or 0.0) / 8000.0,
                     "bytes_note": "achieved = SURVEY.md §8(d) CSR bytes (12 B/nnz + 4 B/row + vectors); the kernels "
                                   f"run the diagonal-major layout ({nd} diagonals{', A by its lower half' if a_sym else ''}) "
                                   "which moves fewer bytes: physical_* counts those (8 B/diagonal/row + 1 B mask + vectors)",
