@@ -263,6 +263,33 @@ int sg_sai_loss(int64_t n, const int32_t* a_offs, const int32_t* a_cols, const d
                 const int32_t* g_rows, double eps, const double* w, int norm_kind,
                 double* loss_host, double* grad_out, void* ws, size_t* ws_bytes, void* stream);
 
+/* ---- GNN training step (gnn.py:198-253 backward, training.py:126-147) ----
+ * Plain fp64 primitives with fixed reduction orders (bit-reproducible runs); composed by
+ * paper_2510_27517_b200/training.py into the training forward (all intermediates kept), the
+ * backward through the restructured GNN, and AdamW. */
+
+/* out[r][c] = relu?( sum_k in[r][k] * W[k][c] (W[c][k] if transpose_w) + b[c] ) + add[r][c];
+ * row strides ldi / ldw / ldo (row blocks of a parameter matrix are addressed by pointer).
+ * b, add may be NULL. */
+int sg_dense_affine(int64_t N, int32_t din, int32_t dout, const double* in, int32_t ldi, const double* W,
+                    int32_t ldw, int32_t transpose_w, const double* b, const double* add, double* out,
+                    int32_t ldo, int32_t relu, void* stream);
+/* pre[e][c] = P[rows[e]][c] + Q[cols[e]][c] + ef[e]*crow[c] + H[e][c] + b[c] (crow, H, b optional) */
+int sg_edge_pre(int64_t E, int32_t d, const int32_t* rows, const int32_t* cols, const double* P, const double* Q,
+                const double* ef, const double* crow, const double* H, const double* b, double* pre, void* stream);
+/* dst = src * [pre > 0] */
+int sg_relu_grad(int64_t M, const double* pre, const double* src, double* dst, void* stream);
+/* dst[i] (+)= sum over CSR segment i of src[perm ? perm[k] : k] (rows of width d, segment order) */
+int sg_segment_sum(int64_t n, int32_t d, const int32_t* offs, const int32_t* perm, const double* src, double* dst,
+                   int32_t accumulate, void* stream);
+/* out[a][b] (+)= sum_r A[r][a] * B[r][b] (A NULL: column sums of B), two fixed-order passes.
+ * Workspace query with ws == NULL. */
+int sg_outer_sum(int64_t N, int32_t da, int32_t db, const double* A, int32_t lda, const double* B, int32_t ldb,
+                 double* out, int32_t accumulate, void* ws, size_t* ws_bytes, void* stream);
+/* adamw_step (training.py:126-147) with grads / grad_div, t the 1-based step; in place. */
+int sg_adamw(int64_t n, double* params, const double* grads, double* m, double* v, double lr, double wd,
+             double beta1, double beta2, double eps, int64_t t, double grad_div, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

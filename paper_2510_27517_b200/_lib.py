@@ -69,6 +69,12 @@ SIGNATURES = {
     "sg_pcg_stats": (C.c_int, [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64), vp, i32]),
     "sg_sai_loss": (C.c_int, [i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, f64, vp,
                               C.c_int, C.POINTER(C.c_double), vp, vp, szp, vp]),
+    "sg_dense_affine": (C.c_int, [i64, i32, i32, vp, i32, vp, i32, i32, vp, vp, vp, i32, i32, vp]),
+    "sg_edge_pre": (C.c_int, [i64, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+    "sg_relu_grad": (C.c_int, [i64, vp, vp, vp, vp]),
+    "sg_segment_sum": (C.c_int, [i64, i32, vp, vp, vp, vp, i32, vp]),
+    "sg_outer_sum": (C.c_int, [i64, i32, i32, vp, i32, vp, i32, vp, i32, vp, szp, vp]),
+    "sg_adamw": (C.c_int, [i64, vp, vp, vp, vp, f64, f64, f64, f64, f64, i64, f64, vp]),
 }
 
 _lib = None

@@ -76,3 +76,315 @@ def hutchinson_frobenius_estimate(A: SparseMatrix, m_apply, n_samples: int, seed
         z = spmv(A, m_apply(w)) - w
         samples.append(float(z @ z))
     return math.fsum(samples) / n_samples
+
+
+# ------------------------------------------------------------------------------------------------
+# GNN training step on the GPU: training forward with every intermediate,
+# backward through the restructured GNN, AdamW, and the reference train() loop.
+# ------------------------------------------------------------------------------------------------
+class _Views:
+    """Offsets of every (W, b) of the model inside its flat parameter vector (params_flat order,
+    gnn.py:130-136): mlp k -> [(W offset, d_in, d_out, b offset), ...]."""
+
+    def __init__(self, model):
+        self.mlps = []
+        pos = 0
+        for m in model.mlps():
+            ent = []
+            for W, b in m.weights:
+                din, dout = W.shape
+                ent.append((pos, din, dout, pos + din * dout))
+                pos += din * dout + dout
+            self.mlps.append(ent)
+        self.n = pos
+
+
+class _Dev:
+    """Device primitive calls (sg_dense_affine & co.) with pointer arithmetic on flat tensors."""
+
+    def __init__(self):
+        self.lib = L.lib()
+        self._ws = None
+
+    @staticmethod
+    def p(t, off=0):
+        return C.c_void_p(0 if t is None else t.data_ptr() + 8 * off)
+
+    def affine(self, N, din, dout, x, ldi, W, woff, ldw, out, ldo, b=None, boff=0, add=None, relu=False,
+               trans=False):
+        L.check(self.lib.sg_dense_affine(N, din, dout, self.p(x), ldi, self.p(W, woff), ldw, 1 if trans else 0,
+                                         self.p(b, boff) if b is not None else None,
+                                         self.p(add) if add is not None else None, self.p(out), ldo,
+                                         1 if relu else 0, L.stream_ptr()), "dense_affine")
+
+    def add_into(self, dst, src):
+        """dst = dst + 1.0 * src (sg_axpby)."""
+        L.check(self.lib.sg_axpby(self.p(dst), self.p(dst), self.p(src), 1.0, dst.numel(), 0, L.stream_ptr()))
+
+    def relu_grad(self, pre, src, dst):
+        L.check(self.lib.sg_relu_grad(pre.numel(), self.p(pre), self.p(src), self.p(dst), L.stream_ptr()))
+
+    def seg(self, n, d, offs, perm, src, dst, acc=False):
+        L.check(self.lib.sg_segment_sum(n, d, self.p(offs), self.p(perm) if perm is not None else None,
+                                        self.p(src), self.p(dst), 1 if acc else 0, L.stream_ptr()))
+
+    def outer(self, N, da, db, A, lda, B, ldb, out, ooff, acc=True):
+        import torch
+        need = C.c_size_t(0)
+        L.check(self.lib.sg_outer_sum(N, da, db, None, lda, None, ldb, None, 0, None, C.byref(need), None))
+        if self._ws is None or self._ws.numel() * 8 < need.value:
+            self._ws = L.empty(need.value // 8 + 64, torch.float64)
+        L.check(self.lib.sg_outer_sum(N, da, db, self.p(A) if A is not None else None, lda, self.p(B), ldb,
+                                      self.p(out, ooff), 1 if acc else 0, self.p(self._ws), C.byref(need),
+                                      L.stream_ptr()), "outer_sum")
+
+    def edge_pre(self, E, d, rows, cols, P, Q, ef, crow, crow_off, H, b, boff, pre):
+        L.check(self.lib.sg_edge_pre(E, d, self.p(rows), self.p(cols), self.p(P), self.p(Q),
+                                     self.p(ef) if ef is not None else None,
+                                     self.p(crow, crow_off) if crow is not None else None,
+                                     self.p(H) if H is not None else None,
+                                     self.p(b, boff) if b is not None else None, self.p(pre),
+                                     L.stream_ptr()), "edge_pre")
+
+
+def _check_trainable(cfg):
+    if cfg.mlp_hidden_layers != 1 or cfg.message_uses_hidden_edge or cfg.activation != "relu" or cfg.d_edge != 1:
+        raise NotImplementedError("GPU training supports the reference default model (one hidden layer per MLP, "
+                                  "relu, d_edge = 1, message_uses_hidden_edge = False)")
+
+
+def gnn_train_forward(model, graph):
+    """The GNN forward (gnn.py:208-253 in the restructured form) keeping every intermediate the
+    backward needs.  Returns a dict; `g` is the [nnz] output (equal to `forward` within 1e-12)."""
+    import torch
+    cfg = model.config
+    _check_trainable(cfg)
+    dv, V = _Dev(), _Views(model)
+    W = model.params_device()
+    mat = graph.matrix
+    n, E, d, Lc = mat.n_rows, mat.nnz, cfg.hidden_dim, cfg.n_layers
+    rows, cols = mat.rows(), mat.cols
+    ef = graph.edge_dev
+    f64 = torch.float64
+    z = lambda *s: torch.empty(*s, dtype=f64, device=L.device())  # noqa: E731
+    st = {"n": n, "E": E, "d": d}
+    # node encoder: a0 = V W1 + b1, X0 = relu(a0) W2 + b2
+    (w1, din, _, b1), (w2, _, _, b2) = V.mlps[0]
+    st["a0"] = a0 = z(n, d)
+    dv.affine(n, din, d, graph.node_dev, din, W, w1, d, a0, d, W, b1)
+    r0 = z(n, d)
+    dv.relu_grad(a0, a0, r0)
+    X = z(n, d)
+    dv.affine(n, d, d, r0, d, W, w2, d, X, d, W, b2)
+    st["X"] = [X]
+    st["pre_m"], st["S"], st["m"], st["am"] = [], [], [], []
+    deg = L.to_device(np.diff(mat.offs[:n + 1].cpu().numpy().astype(np.int64)).astype(np.float64), f64)
+    st["deg"] = deg
+    for t in range(Lc):
+        fm, fv = V.mlps[2 + 3 * t], V.mlps[3 + 3 * t]
+        (m1, _, _, mb1), (m2, _, _, mb2) = fm
+        Pm, Qm = z(n, d), z(n, d)
+        dv.affine(n, d, d, X, d, W, m1, d, Pm, d)
+        dv.affine(n, d, d, X, d, W, m1 + d * d, d, Qm, d)
+        pre = z(E, d)
+        dv.edge_pre(E, d, rows, cols, Pm, Qm, ef, W, m1 + 2 * d * d, None, W, mb1, pre)
+        zz = z(E, d)
+        dv.relu_grad(pre, pre, zz)
+        S = z(n, d)
+        dv.seg(n, d, mat.offs, None, zz, S)
+        m = z(n, d)
+        dv.affine(n, d, d, S, d, W, m2, d, m, d)
+        dv.affine(n, 1, d, deg, 1, W, mb2, d, m, d, add=m)  # m = S W2 + deg b2
+        (v1, _, _, vb1), (v2, _, _, vb2) = fv
+        am = z(n, d)
+        dv.affine(n, d, d, m, d, W, v1, d, am, d, W, vb1)
+        zm = z(n, d)
+        dv.relu_grad(am, am, zm)
+        Xn = z(n, d)
+        dv.affine(n, d, d, zm, d, W, v2, d, Xn, d, W, vb2, add=X)
+        st["pre_m"].append(pre); st["S"].append(S); st["m"].append(m); st["am"].append(am)
+        X = Xn
+        st["X"].append(X)
+    # edge path
+    (e1, _, _, eb1), (e2, _, _, eb2) = V.mlps[1]
+    ae = z(E, d)
+    dv.affine(E, 1, d, ef, 1, W, e1, d, ae, d, W, eb1)
+    re = z(E, d)
+    dv.relu_grad(ae, ae, re)
+    h = z(E, d)
+    dv.affine(E, d, d, re, d, W, e2, d, h, d, W, eb2)
+    st["ae"], st["h"], st["pre_f"] = ae, [h], []
+    for t in range(Lc):
+        fe = V.mlps[4 + 3 * t]
+        (f1, _, _, fb1), (f2, _, _, fb2) = fe
+        Xt = st["X"][t + 1]
+        Pf, Qf, Hw = z(n, d), z(n, d), z(E, d)
+        dv.affine(n, d, d, Xt, d, W, f1, d, Pf, d)
+        dv.affine(n, d, d, Xt, d, W, f1 + d * d, d, Qf, d)
+        dv.affine(E, d, d, h, d, W, f1 + 2 * d * d, d, Hw, d)
+        pre = z(E, d)
+        dv.edge_pre(E, d, rows, cols, Pf, Qf, None, None, 0, Hw, W, fb1, pre)
+        rf = z(E, d)
+        dv.relu_grad(pre, pre, rf)
+        hn = z(E, d)
+        dv.affine(E, d, d, rf, d, W, f2, d, hn, d, W, fb2, add=h)
+        st["pre_f"].append(pre)
+        h = hn
+        st["h"].append(h)
+    (d1, _, _, db1), (d2, _, _, db2) = V.mlps[-1]
+    ad = z(E, d)
+    dv.affine(E, d, d, h, d, W, d1, d, ad, d, W, db1)
+    rd = z(E, d)
+    dv.relu_grad(ad, ad, rd)
+    g = z(E)
+    dv.affine(E, d, 1, rd, d, W, d2, 1, g, 1, W, db2)
+    st["ad"], st["g"] = ad, g
+    return st
+
+
+def gnn_backward(model, graph, st, dg):
+    """dL/dθ (params_flat order) from dL/dg through the restructured GNN (reverse of
+    gnn_train_forward).  Column (gather-by-j) sums run over the transposed pattern in ascending
+    source row, i.e. the tape's np.add.at order."""
+    import torch
+    cfg = model.config
+    dv, V = _Dev(), _Views(model)
+    W = model.params_device()
+    mat = graph.matrix
+    n, E, d, Lc = st["n"], st["E"], st["d"], cfg.n_layers
+    rows, cols = mat.rows(), mat.cols
+    offs_t, _, perm = mat.transpose_pattern()
+    ef = graph.edge_dev
+    f64 = torch.float64
+    z = lambda *s: torch.empty(*s, dtype=f64, device=L.device())  # noqa: E731
+    grad = torch.zeros(V.n + 2, dtype=f64, device=L.device())[:V.n]
+    dg = dg if isinstance(dg, torch.Tensor) else L.to_device(np.asarray(dg, dtype=np.float64), f64)
+    dg = dg[:E].reshape(E, 1)
+    # decoder
+    (d1, _, _, db1), (d2, _, _, db2) = V.mlps[-1]
+    ad = st["ad"]
+    rd = z(E, d)
+    dv.relu_grad(ad, ad, rd)
+    dv.outer(E, d, 1, rd, d, dg, 1, grad, d2)           # dW2 = relu(ad)^T dg
+    dv.outer(E, 1, 1, None, 1, dg, 1, grad, db2)        # db2 = sum dg
+    dz = z(E, d)
+    dv.affine(E, 1, d, dg, 1, W, d2, 1, dz, d, trans=True)  # dg W2^T
+    dv.relu_grad(ad, dz, dz)
+    hL = st["h"][-1]
+    dv.outer(E, d, d, hL, d, dz, d, grad, d1)
+    dv.outer(E, 1, d, None, 1, dz, d, grad, db1)
+    dh = z(E, d)
+    dv.affine(E, d, d, dz, d, W, d1, d, dh, d, trans=True)
+    dX = [z(n, d).zero_() for _ in range(Lc + 1)]
+    zero_n = z(n, d).zero_()
+    # edge layers, reverse
+    for t in reversed(range(Lc)):
+        fe = V.mlps[4 + 3 * t]
+        (f1, _, _, fb1), (f2, _, _, fb2) = fe
+        pre, h_t, Xt = st["pre_f"][t], st["h"][t], st["X"][t + 1]
+        rf = z(E, d)
+        dv.relu_grad(pre, pre, rf)
+        dv.outer(E, d, d, rf, d, dh, d, grad, f2)
+        dv.outer(E, 1, d, None, 1, dh, d, grad, fb2)
+        dp = z(E, d)
+        dv.affine(E, d, d, dh, d, W, f2, d, dp, d, trans=True)
+        dv.relu_grad(pre, dp, dp)
+        dv.outer(E, d, d, h_t, d, dp, d, grad, f1 + 2 * d * d)
+        dv.outer(E, 1, d, None, 1, dp, d, grad, fb1)
+        dPf, dQf = z(n, d), z(n, d)
+        dv.seg(n, d, mat.offs, None, dp, dPf)
+        dv.seg(n, d, offs_t, perm, dp, dQf)
+        dv.outer(n, d, d, Xt, d, dPf, d, grad, f1)
+        dv.outer(n, d, d, Xt, d, dQf, d, grad, f1 + d * d)
+        dv.affine(n, d, d, dPf, d, W, f1, d, dX[t + 1], d, trans=True, add=dX[t + 1])
+        dv.affine(n, d, d, dQf, d, W, f1 + d * d, d, dX[t + 1], d, trans=True, add=dX[t + 1])
+        dhn = z(E, d)
+        dv.affine(E, d, d, dp, d, W, f1 + 2 * d * d, d, dhn, d, trans=True, add=dh)
+        dh = dhn
+    # edge encoder
+    (e1, _, _, eb1), (e2, _, _, eb2) = V.mlps[1]
+    ae = st["ae"]
+    re = z(E, d)
+    dv.relu_grad(ae, ae, re)
+    dv.outer(E, d, d, re, d, dh, d, grad, e2)
+    dv.outer(E, 1, d, None, 1, dh, d, grad, eb2)
+    da = z(E, d)
+    dv.affine(E, d, d, dh, d, W, e2, d, da, d, trans=True)
+    dv.relu_grad(ae, da, da)
+    dv.outer(E, 1, d, ef.reshape(E, 1), 1, da, d, grad, e1)
+    dv.outer(E, 1, d, None, 1, da, d, grad, eb1)
+    # node layers, reverse
+    deg = st["deg"]
+    for t in reversed(range(Lc)):
+        fm, fv = V.mlps[2 + 3 * t], V.mlps[3 + 3 * t]
+        (m1, _, _, mb1), (m2, _, _, mb2) = fm
+        (v1, _, _, vb1), (v2, _, _, vb2) = fv
+        dXn, Xt = dX[t + 1], st["X"][t]
+        pre, S, m, am = st["pre_m"][t], st["S"][t], st["m"][t], st["am"][t]
+        dv.add_into(dX[t], dXn)                                # residual
+        zm = z(n, d)
+        dv.relu_grad(am, am, zm)
+        dv.outer(n, d, d, zm, d, dXn, d, grad, v2)
+        dv.outer(n, 1, d, None, 1, dXn, d, grad, vb2)
+        dam = z(n, d)
+        dv.affine(n, d, d, dXn, d, W, v2, d, dam, d, trans=True)
+        dv.relu_grad(am, dam, dam)
+        dv.outer(n, d, d, m, d, dam, d, grad, v1)
+        dv.outer(n, 1, d, None, 1, dam, d, grad, vb1)
+        dm = z(n, d)
+        dv.affine(n, d, d, dam, d, W, v1, d, dm, d, trans=True)
+        dv.outer(n, d, d, S, d, dm, d, grad, m2)
+        dv.outer(n, 1, d, deg, 1, dm, d, grad, mb2)            # m = S W2 + deg b2
+        dS = z(n, d)
+        dv.affine(n, d, d, dm, d, W, m2, d, dS, d, trans=True)
+        # dpre_e = dS[row_e] * [pre_e > 0]
+        dpre = z(E, d)
+        dv.edge_pre(E, d, rows, cols, dS, zero_n, None, None, 0, None, None, 0, dpre)
+        dv.relu_grad(pre, dpre, dpre)
+        dv.outer(E, 1, d, None, 1, dpre, d, grad, mb1)
+        dv.outer(E, 1, d, ef.reshape(E, 1), 1, dpre, d, grad, m1 + 2 * d * d)  # edge-feature row c
+        dP, dQ = z(n, d), z(n, d)
+        dv.seg(n, d, mat.offs, None, dpre, dP)
+        dv.seg(n, d, offs_t, perm, dpre, dQ)
+        dv.outer(n, d, d, Xt, d, dP, d, grad, m1)
+        dv.outer(n, d, d, Xt, d, dQ, d, grad, m1 + d * d)
+        dv.affine(n, d, d, dP, d, W, m1, d, dX[t], d, trans=True, add=dX[t])
+        dv.affine(n, d, d, dQ, d, W, m1 + d * d, d, dX[t], d, trans=True, add=dX[t])
+    # node encoder
+    (w1, din, _, b1), (w2, _, _, b2) = V.mlps[0]
+    a0 = st["a0"]
+    r0 = z(n, d)
+    dv.relu_grad(a0, a0, r0)
+    dv.outer(n, d, d, r0, d, dX[0], d, grad, w2)
+    dv.outer(n, 1, d, None, 1, dX[0], d, grad, b2)
+    da0 = z(n, d)
+    dv.affine(n, d, d, dX[0], d, W, w2, d, da0, d, trans=True)
+    dv.relu_grad(a0, da0, da0)
+    dv.outer(n, din, d, graph.node_dev.reshape(n, din), din, da0, d, grad, w1)
+    dv.outer(n, 1, d, None, 1, da0, d, grad, b1)
+    return grad
+
+
+def matrix_loss_and_grad(model, A: SparseMatrix, graph, rng, n_samples: int = 1,
+                         norm_kind: str = "mean_abs_nonzero"):
+    """training.py:_matrix_loss_and_grad on the GPU: forward, the mean SAI loss over
+    `n_samples` fresh Hutchinson probes drawn from `rng` (same draws as the reference), and
+    dL/dθ (device tensor, params_flat order)."""
+    st = gnn_train_forward(model, graph)
+    mat = graph.matrix
+    G = SparseMatrix.from_device(mat.with_values(st["g"]))
+    losses, dg = [], None
+    for _ in range(n_samples):
+        w = rng.standard_normal(A.n_rows)
+        loss, g = _loss(A, G, model.config.epsilon, w, norm_kind, True)
+        losses.append(loss)
+        import torch
+        gd = g if isinstance(g, torch.Tensor) else L.to_device(g, torch.float64)
+        dg = gd if dg is None else dg + gd
+    total = losses[0]
+    for lv in losses[1:]:
+        total = total + lv
+    mean_loss = total * (1.0 / n_samples)
+    if n_samples > 1:
+        dg = dg * (1.0 / n_samples)
+    return mean_loss, gnn_backward(model, graph, st, dg)

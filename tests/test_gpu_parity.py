@@ -542,3 +542,31 @@ def test_pcg_control_flow_on_sliding_window_kernels():
             assert abs(rep.residual_history[0] - hist[0]) <= 1e-15, name
         if special == "zero":
             assert rep.k == 0 and np.all(rep.x == 0.0)
+
+
+# --------------------------------------------------------------------------- training (§8(f) #1)
+def _train_items():
+    items = []
+    for s in range(8):
+        A, meta = P.gen_poisson2d(8, 8, coeff_seed=s)
+        items.append((A, P.build_graph(A, meta)))
+    return items
+
+
+def test_gnn_gradient_matches_reference_tape():
+    """GNN backward on the GPU vs the reference's Tape.backward (tests/golden/golden_train.npz,
+    made by make_train_golden.py): one matrix, one Hutchinson probe, every parameter."""
+    import os
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "golden_train.npz"))
+    from paper_2510_27517_b200.training import gnn_train_forward, matrix_loss_and_grad
+    m = P.init_model(P.GnnConfig(d_node=3, seed=0))
+    assert np.array_equal(m.params_flat(), g["params0"])
+    A, gr = _train_items()[0]
+    st = gnn_train_forward(m, gr)  # the training forward reproduces the fused inference forward
+    assert rel_floor(st["g"].cpu().numpy(), P.forward(m, gr).g_values.cpu().numpy()) < 1e-12
+    loss, grad = matrix_loss_and_grad(m, A, gr, np.random.default_rng(123))
+    assert abs(loss - float(g["grad_loss"])) <= 1e-10 * abs(float(g["grad_loss"]))
+    want = g["grad"]
+    got = grad.cpu().numpy()
+    scale = np.max(np.abs(want))
+    assert np.max(np.abs(got - want)) <= 1e-9 * scale, np.max(np.abs(got - want)) / scale
