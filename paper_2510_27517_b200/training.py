@@ -3,7 +3,8 @@
 `sai_loss` returns ||(A (G G^T + eps I) w)/||A|| - w||^2; `sai_loss_and_grad` additionally
 returns dL/dg for every stored entry of G — the gradient the reference obtains by recording
 the loss on its tape and calling `Tape.backward` (autodiff.py:203-239, 265-303), in the same
-rounding order.  The training loop itself (AdamW, GNN backward) is SURVEY.md §8(f) "next".
+rounding order.  The GNN training step follows: training forward, backward
+through the restructured GNN, AdamW and `train` (training.py:242-314) with every step on the GPU.
 """
 from __future__ import annotations
 
@@ -15,7 +16,9 @@ import numpy as np
 from . import _lib as L
 from .sparse import SparseMatrix, _as_dev_vector, norm_device
 
-__all__ = ["NORM_KINDS", "matrix_norm", "sai_loss", "sai_loss_and_grad"]
+__all__ = ["NORM_KINDS", "matrix_norm", "sai_loss", "sai_loss_and_grad", "gnn_train_forward", "gnn_backward",
+           "matrix_loss_and_grad", "TrainConfig", "TrainItem", "TrainLog", "TrainingDivergedError", "AdamWDevice",
+           "train"]
 
 NORM_KINDS = ("mean_abs_nonzero", "frobenius", "entrywise_l1")
 
@@ -388,3 +391,164 @@ def matrix_loss_and_grad(model, A: SparseMatrix, graph, rng, n_samples: int = 1,
     if n_samples > 1:
         dg = dg * (1.0 / n_samples)
     return mean_loss, gnn_backward(model, graph, st, dg)
+
+
+# ------------------------------------------------------------------------------------------------
+# training.py:150-314 — TrainConfig / TrainItem / AdamW / train() with the step on the GPU
+# ------------------------------------------------------------------------------------------------
+from dataclasses import dataclass, field  # noqa: E402
+
+
+@dataclass(frozen=True)
+class TrainConfig:
+    """training.py:150-171."""
+
+    epochs: int = 500
+    batch_size: int = 4
+    lr: float = 1e-3
+    weight_decay: float = 1e-2
+    lr_decay: float = 0.99
+    hutchinson_samples_per_matrix: int = 1
+    seed: int = 0
+    norm_kind: str = "mean_abs_nonzero"
+    val_every: int = 50
+    checkpoint_every: int = 0
+
+    def __post_init__(self):
+        if min(self.epochs, self.batch_size, self.hutchinson_samples_per_matrix) < 1:
+            raise ValueError("epochs, batch size, and sample counts must be positive")
+        if self.lr <= 0 or self.weight_decay < 0:
+            raise ValueError("lr must be positive and weight decay nonnegative")
+        if not 0.0 < self.lr_decay <= 1.0:
+            raise ValueError("lr_decay must lie in (0, 1]")
+        if self.norm_kind not in NORM_KINDS:
+            raise ValueError(f"unknown norm kind {self.norm_kind!r}")
+
+
+@dataclass
+class TrainItem:
+    """training.py:174-178."""
+
+    A: SparseMatrix
+    graph: object
+    b: np.ndarray | None = None
+
+
+class TrainingDivergedError(RuntimeError):
+    """training.py:181-189."""
+
+    def __init__(self, epoch: int, loss: float, checkpoint_path):
+        msg = f"non-finite loss {loss} at epoch {epoch}"
+        if checkpoint_path is not None:
+            msg += f"; last good parameters saved to {checkpoint_path}"
+        super().__init__(msg)
+        self.epoch = epoch
+        self.loss = loss
+
+
+@dataclass
+class TrainLog:
+    """training.py:192-197: rows of (epoch, mean_loss, lr, wallclock_s, val_mean_k)."""
+
+    rows: list = field(default_factory=list)
+
+    def losses(self):
+        return np.array([r[1] for r in self.rows])
+
+
+class AdamWDevice:
+    """adamw_step (training.py:126-147) on device: parameters and both moments stay resident."""
+
+    def __init__(self, params_dev, beta1=0.9, beta2=0.999, eps=1e-8):
+        import torch
+        n = params_dev.numel()
+        self.p = params_dev
+        self.m = torch.zeros(n, dtype=torch.float64, device=params_dev.device)
+        self.v = torch.zeros(n, dtype=torch.float64, device=params_dev.device)
+        self.beta1, self.beta2, self.eps = beta1, beta2, eps
+
+    def step(self, grad_sum, t: int, lr: float, weight_decay: float, batch_len: int):
+        L.check(L.lib().sg_adamw(self.p.numel(), L.ptr(self.p), L.ptr(grad_sum), L.ptr(self.m), L.ptr(self.v),
+                                 float(lr), float(weight_decay), self.beta1, self.beta2, self.eps, int(t),
+                                 float(batch_len), L.stream_ptr()), "adamw")
+
+
+def _validation_mean_k(model, val_items) -> float:
+    """training.py:229-239 (learned SPAI + PCG on the GPU)."""
+    from .gnn import forward
+    from .pcg import SolveConfig, pcg_solve
+    from .precond import build_learned_spai
+    ks = []
+    cfg = SolveConfig(rtol=1e-8)
+    for item in val_items:
+        G = forward(model, item.graph).G
+        b = item.b if item.b is not None else np.ones(item.A.n_rows) / math.sqrt(item.A.n_rows)
+        ks.append(pcg_solve(item.A, b, build_learned_spai(G, model.config.epsilon), cfg).k)
+    return float(np.mean(ks))
+
+
+def train(model, train_items, cfg: TrainConfig, val_items=(), log_path=None, checkpoint_path=None) -> TrainLog:
+    """training.py:242-314 with forward, loss, backward and AdamW on the GPU.  Same seeded
+    shuffles and probes (one host PCG64 stream), same batch averaging, lr decay, divergence
+    handling, CSV log and checkpoints."""
+    import csv
+    import time
+    import torch
+    from .gnn import save_checkpoint
+    train_items = list(train_items)
+    if not train_items:
+        raise ValueError("empty training set")
+    rng = np.random.default_rng(cfg.seed)
+    params = L.to_device(model.params_flat(), torch.float64).clone()
+    opt = AdamWDevice(params)
+    lr = cfg.lr
+    t = 0
+    log = TrainLog()
+    fh = writer = None
+    if log_path is not None:
+        fh = open(log_path, "w", newline="")
+        writer = csv.writer(fh)
+        writer.writerow(["epoch", "mean_loss", "lr", "wallclock_s", "val_mean_k"])
+    t0 = time.perf_counter()
+    last_good = model.params_flat().copy()
+    grad_sum = torch.zeros_like(params)
+    try:
+        for epoch in range(1, cfg.epochs + 1):
+            order = rng.permutation(len(train_items))
+            epoch_losses = []
+            for start in range(0, len(order), cfg.batch_size):
+                batch = order[start:start + cfg.batch_size]
+                grad_sum.zero_()
+                for idx in batch:
+                    item = train_items[idx]
+                    loss_val, grad = matrix_loss_and_grad(model, item.A, item.graph, rng,
+                                                          cfg.hutchinson_samples_per_matrix, cfg.norm_kind)
+                    if not math.isfinite(loss_val):
+                        if checkpoint_path is not None:
+                            model.set_params_flat(last_good)
+                            save_checkpoint(model, checkpoint_path)
+                        raise TrainingDivergedError(epoch, loss_val, checkpoint_path)
+                    epoch_losses.append(loss_val)
+                    L.check(L.lib().sg_axpby(L.ptr(grad_sum), L.ptr(grad_sum), L.ptr(grad), 1.0, grad.numel(), 0,
+                                             L.stream_ptr()))
+                t += 1
+                opt.step(grad_sum, t, lr, cfg.weight_decay, len(batch))
+                model.set_params_flat(params.cpu().numpy())
+            val_k = ""
+            if val_items and cfg.val_every > 0 and (epoch % cfg.val_every == 0 or epoch == cfg.epochs):
+                val_k = _validation_mean_k(model, val_items)
+            row = (epoch, float(np.mean(epoch_losses)), lr, time.perf_counter() - t0, val_k)
+            log.rows.append(row)
+            if writer is not None:
+                writer.writerow(row)
+                fh.flush()
+            if checkpoint_path is not None and cfg.checkpoint_every > 0 and epoch % cfg.checkpoint_every == 0:
+                save_checkpoint(model, checkpoint_path)
+            last_good = model.params_flat().copy()
+            lr *= cfg.lr_decay
+    finally:
+        if fh is not None:
+            fh.close()
+    if checkpoint_path is not None:
+        save_checkpoint(model, checkpoint_path)
+    return log

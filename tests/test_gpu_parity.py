@@ -570,3 +570,33 @@ def test_gnn_gradient_matches_reference_tape():
     got = grad.cpu().numpy()
     scale = np.max(np.abs(want))
     assert np.max(np.abs(got - want)) <= 1e-9 * scale, np.max(np.abs(got - want)) / scale
+
+
+def test_training_matches_reference_trajectory(tmp_path):
+    """train() on the GPU vs the reference train(): 3 epochs, batch 4, AdamW + lr decay on 8
+    heat2d 8x8 systems — per-epoch mean losses and the final parameters; CSV log and checkpoint
+    written like the reference's."""
+    import os
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "golden_train.npz"))
+    m = P.init_model(P.GnnConfig(d_node=3, seed=0))
+    items = [P.TrainItem(A, gr) for A, gr in _train_items()]
+    log = P.train(m, items, P.TrainConfig(epochs=3, batch_size=4, seed=0), log_path=tmp_path / "log.csv",
+                  checkpoint_path=tmp_path / "ck.spaignn")
+    assert np.allclose(log.losses(), g["train_losses"], rtol=1e-9, atol=0), (log.losses(), g["train_losses"])
+    assert np.allclose([r[2] for r in log.rows], g["train_lrs"], rtol=0, atol=0)
+    p = m.params_flat()
+    assert np.max(np.abs(p - g["train_params"])) <= 1e-9 * np.max(np.abs(g["train_params"]))
+    assert (tmp_path / "log.csv").read_text().startswith("epoch,mean_loss,lr,wallclock_s,val_mean_k")
+    m2 = P.load_checkpoint(str(tmp_path / "ck.spaignn"))
+    assert np.array_equal(m2.params_flat(), p)
+
+
+def test_training_is_deterministic():
+    """Two identical runs give bit-identical parameters (test_training.py:250-260)."""
+    items = [P.TrainItem(A, gr) for A, gr in _train_items()[:4]]
+    runs = []
+    for _ in range(2):
+        m = P.init_model(P.GnnConfig(d_node=3, seed=0))
+        P.train(m, items, P.TrainConfig(epochs=2, batch_size=2, seed=3))
+        runs.append(m.params_flat())
+    assert np.array_equal(runs[0], runs[1])
