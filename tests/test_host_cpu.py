@@ -153,3 +153,14 @@ def test_rhs_vec_roundtrip_and_errors(tmp_path):
     (tmp_path / "bad.vec").write_bytes(raw[:-8])
     with pytest.raises(ValueError, match="does not match"):
         P.read_rhs_vec(tmp_path / "bad.vec")
+
+
+def test_train_config_validation():
+    """TrainConfig mirrors training.py:150-171 (host-side checks, no GPU needed)."""
+    import pytest
+    import paper_2510_27517_b200 as P
+    P.TrainConfig()
+    for bad in (dict(epochs=0), dict(batch_size=0), dict(lr=0.0), dict(weight_decay=-1.0), dict(lr_decay=0.0),
+                dict(lr_decay=1.5), dict(norm_kind="nope"), dict(hutchinson_samples_per_matrix=0)):
+        with pytest.raises(ValueError):
+            P.TrainConfig(**bad)
