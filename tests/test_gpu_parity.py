@@ -600,3 +600,32 @@ def test_training_is_deterministic():
         P.train(m, items, P.TrainConfig(epochs=2, batch_size=2, seed=3))
         runs.append(m.params_flat())
     assert np.array_equal(runs[0], runs[1])
+
+
+def test_bench_csv_rows_and_schema(tmp_path):
+    """The `spaigraph bench` table (cli.py:280-347) with GPU solves: schema, the learned
+    column's k against pcg_solve, non-GPU baselines rejected."""
+    import os
+    from paper_2510_27517_b200.benchcsv import BENCH_HEADER, bench_rows, summarize, write_bench_csv
+    m = P.load_checkpoint(os.path.join(os.path.dirname(__file__), "golden", "trained_heat16.spaignn"))
+    items = []
+    for s in range(3):
+        A, meta = P.gen_poisson2d(16, 16, coeff_seed=s)
+        items.append((f"heat2d_{s}", A, P.build_graph(A, meta), P.gen_rhs(meta, s + 10**6)))
+    rows = bench_rows(items, ("none", "diag", "learned"), (1e-6, 1e-8), None, m)
+    assert len(rows) == 3 * 3 * 2
+    for r in rows:
+        assert r[7] and r[3] > 0
+        if r[1] == "learned":
+            assert r[4] > 0  # GNN inference is part of the construction time
+    A, gr = items[0][1], items[0][2]
+    want = P.pcg_solve(A, items[0][3], P.build_learned_spai(P.forward(m, gr).G, m.config.epsilon),
+                       P.SolveConfig(rtol=1e-8)).k
+    assert [r[3] for r in rows if r[0] == "heat2d_0" and r[1] == "learned" and r[2] == 1e-8] == [want]
+    write_bench_csv(rows, tmp_path / "bench.csv")
+    assert (tmp_path / "bench.csv").read_text().splitlines()[0] == ",".join(BENCH_HEADER)
+    tight, summ = summarize(rows)
+    assert tight == 1e-8 and summ["learned"][0] < summ["diag"][0]
+    import pytest
+    with pytest.raises(NotImplementedError):
+        bench_rows(items[:1], ("ic0",), (1e-6,), None, m)
