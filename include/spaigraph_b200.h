@@ -290,6 +290,26 @@ int sg_outer_sum(int64_t N, int32_t da, int32_t db, const double* A, int32_t lda
 int sg_adamw(int64_t n, double* params, const double* grads, double* m, double* v, double lr, double wd,
              double beta1, double beta2, double eps, int64_t t, double grad_div, void* stream);
 
+/* ---- row-partitioned solve of ONE system over several ranks ----------
+ * A rank holds an EXTENDED local system: its owned rows [own_lo, own_hi) plus ghost rows on
+ * either side (the neighbours' boundary rows), as one local CSR (pcg_solve's own arguments
+ * otherwise).  Tiles and dot products cover the owned rows only; before every kernel that
+ * reads neighbour rows the ghosts are refreshed by an NCCL send/recv group, and every scalar
+ * the reference's control flow needs is an NCCL all-reduce followed by the finaliser kernel —
+ * all captured in the same CUDA graphs as the iteration kernels (no host round trip per
+ * iteration).  libnccl is opened at run time.  Replaces the host loop of rowpart.DistPcg. */
+int sg_nccl_unique_id(void* out128);
+int sg_nccl_comm_init(void** comm_out, const void* id128, int32_t world, int32_t rank);
+int sg_nccl_comm_destroy(void* comm);
+int sg_pcg_create_part(sg_pcg** out, int64_t n_ext, int64_t own_lo, int64_t own_hi,
+                       const int32_t* a_offs, const int32_t* a_cols, const double* a_vals,
+                       int precond_kind, const int32_t* g_offs, const int32_t* g_cols,
+                       const double* g_vals, const int32_t* gt_offs, const int32_t* gt_cols,
+                       const double* gt_vals, const double* inv_diag, double epsilon, void* stream);
+/* comm: ncclComm_t (NULL = single rank, no communication); left/right: neighbour ranks or -1;
+ * ghost_lo/hi: ghost rows below own_lo / above own_hi (= the neighbours' boundary rows sent). */
+int sg_pcg_set_comm(sg_pcg* h, void* comm, int32_t left, int32_t right, int64_t ghost_lo, int64_t ghost_hi);
+
 #ifdef __cplusplus
 }
 #endif

@@ -28,6 +28,9 @@
 //   CSR  (anything else): CSR-stream tiles staged through shared memory (spmv.cuh).
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
+#include <dlfcn.h>
+#include <nccl.h>
 #include <map>
 #include <vector>
 
@@ -81,6 +84,11 @@ struct Dia {
 };
 
 struct Dev {
+  // row-partitioned mode (one system over several ranks): the last CTA of a reducing kernel
+  // publishes the rank-local sums into gsum instead of finalising; an in-graph all-reduce and
+  // k_fin_* then run the reference control flow on the global sums, identically on every rank
+  int dist;
+  double* gsum;  // [S][2]
   // tile table
   const long long* blk_r0;
   const int* blk_sys;
@@ -211,6 +219,13 @@ __device__ __forceinline__ void finish(const Dev& D, SysState& S, int conv) {
   S.converged = conv;
   S.status = ST_DONE;
   atomicSub(&D.ctl->n_active, 1u);
+}
+
+// Row-partitioned mode: hand the rank-local sums to the all-reduce (thread 0 of the last CTA).
+__device__ __forceinline__ void publish(const Dev& D, int sys, double v0, double v1) {
+  D.gsum[2 * sys + 0] = v0;
+  D.gsum[2 * sys + 1] = v1;
+  D.counter[sys] = 0;
 }
 
 __device__ __forceinline__ void put_hist(const Dev& D, int sys, long long i, double v) {
@@ -502,7 +517,7 @@ __global__ void __launch_bounds__(PR, FMT >= 1 ? 8 : 1) k_setup1(Dev D) {
   }
   if (arrive(D, sys, pbb, 0.0, red, &flag)) {
     const double bb = gather_partials(D, sys, 0, red);
-    if (threadIdx.x == 0) fin_setup1(D, sys, bb);
+    if (threadIdx.x == 0) { if (D.dist) publish(D, sys, bb, 0.0); else fin_setup1(D, sys, bb); }
   }
 }
 
@@ -533,7 +548,7 @@ __global__ void __launch_bounds__(PR, FMT >= 1 ? 8 : 1) k_setup2(Dev D) {
   }
   if (arrive(D, sys, prs, 0.0, red, &flag)) {
     const double rs = gather_partials(D, sys, 0, red);
-    if (threadIdx.x == 0) fin_setup2(D, sys, rs);
+    if (threadIdx.x == 0) { if (D.dist) publish(D, sys, rs, 0.0); else fin_setup2(D, sys, rs); }
   }
 }
 
@@ -579,7 +594,7 @@ __global__ void __launch_bounds__(PR, FMT >= 1 ? 8 : 1) k_iter1(Dev D, int par) 
   if (arrive(D, sys, pdq, prr, red, &flag)) {
     const double dq = gather_partials(D, sys, 0, red);
     const double rrf = gather_partials(D, sys, 1, red);
-    if (threadIdx.x == 0) fin_k1(D, sys, run, dq, rrf);
+    if (threadIdx.x == 0) { if (D.dist) publish(D, sys, dq, rrf); else fin_k1(D, sys, run, dq, rrf); }
   }
 }
 
@@ -615,7 +630,7 @@ __global__ void __launch_bounds__(PR, FMT >= 1 ? 8 : 1) k_iter2(Dev D, int par) 
   }
   if (arrive(D, sys, prr, 0.0, red, &flag)) {
     const double rr = gather_partials(D, sys, 0, red);
-    if (threadIdx.x == 0) fin_rr(D, sys, rr);
+    if (threadIdx.x == 0) { if (D.dist) publish(D, sys, rr, 0.0); else fin_rr(D, sys, rr); }
   }
 }
 
@@ -671,7 +686,7 @@ __global__ void __launch_bounds__(PR, FMT >= 1 ? 8 : 1) k_refresh_r(Dev D, int p
   }
   if (arrive(D, sys, prr, 0.0, red, &flag)) {
     const double rr = gather_partials(D, sys, 0, red);
-    if (threadIdx.x == 0) fin_rr(D, sys, rr);
+    if (threadIdx.x == 0) { if (D.dist) publish(D, sys, rr, 0.0); else fin_rr(D, sys, rr); }
   }
 }
 
@@ -708,7 +723,24 @@ __global__ void __launch_bounds__(PR, FMT >= 1 ? 8 : 1) k_iter3(Dev D, int par, 
   }
   if (arrive(D, sys, prs, 0.0, red, &flag)) {
     const double rs = gather_partials(D, sys, 0, red);
-    if (threadIdx.x == 0) fin_k3(D, sys, rs, refreshed);
+    if (threadIdx.x == 0) { if (D.dist) publish(D, sys, rs, 0.0); else fin_k3(D, sys, rs, refreshed); }
+  }
+}
+
+// Row-partitioned mode: the finalisers on the all-reduced sums (one thread per system; systems
+// the reducing kernel skipped are skipped here too, exactly as the kernel's own early return).
+enum { FIN_SETUP1 = 0, FIN_SETUP2 = 1, FIN_K1 = 2, FIN_RR = 3, FIN_K3 = 4 };
+__global__ void k_fin(Dev D, int kind, int S, int arg) {
+  const int sys = blockIdx.x * blockDim.x + threadIdx.x;
+  if (sys >= S) return;
+  const int status = D.st[sys].status;
+  const double v0 = D.gsum[2 * sys], v1 = D.gsum[2 * sys + 1];
+  switch (kind) {
+    case FIN_SETUP1: fin_setup1(D, sys, v0); break;
+    case FIN_SETUP2: fin_setup2(D, sys, v0); break;
+    case FIN_K1: if (status != ST_DONE) fin_k1(D, sys, status == ST_RUN, v0, v1); break;
+    case FIN_RR: if (status == ST_RUN) fin_rr(D, sys, v0); break;
+    default: if (status == ST_RUN) fin_k3(D, sys, v0, arg); break;
   }
 }
 
@@ -1514,6 +1546,12 @@ struct sg_pcg {
   int short_rows = 0;
   int nrng = 0;       // sliding-window ranges
   int num_sms = 148;
+  // row-partitioned mode (sg_pcg_create_part / sg_pcg_set_comm)
+  int dist = 0;
+  void* comm = nullptr;       // ncclComm_t
+  int left = -1, right = -1;  // neighbour ranks (or -1)
+  long long own_lo = 0, own_hi = 0, ghost_lo = 0, ghost_hi = 0;
+  double* gsum = nullptr;
   int strip = 0;      // wide 5-point grid: 2-D strip sliding-window kernels (k_iter1_s5, k_iter23_s5)
   int k1sw = 1;       // K1 variant: 1 = sliding window (k_iter1_sw), 0 = tiles (k_iter1_st)
   int k23 = 1;        // fused K2+K3 variant: 1 = sliding window (k_iter23_sw), 0 = tiles (k_iter23_st)
@@ -1535,6 +1573,88 @@ struct sg_pcg {
   double prof_ms[3] = {0, 0, 0};
   double prof_active = 0, prof_samples = 0;
 };
+
+// ------------------------------------------------------------------ NCCL (resolved at run time)
+// The row-partitioned solve runs its halo exchanges and scalar all-reduces as NCCL operations
+// captured into the same CUDA graphs as the iteration kernels.  libnccl is opened lazily (the
+// one PyTorch ships), so the library has no link-time NCCL dependency.
+namespace {
+struct NcclApi {
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*groupStart)() = nullptr;
+  ncclResult_t (*groupEnd)() = nullptr;
+  const char* (*getErrorString)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (tried) return api;
+  tried = true;
+  void* hdl = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!hdl) hdl = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!hdl) return api;
+  auto sym = [&](const char* n) { return dlsym(hdl, n); };
+  api.getUniqueId = reinterpret_cast<decltype(api.getUniqueId)>(sym("ncclGetUniqueId"));
+  api.commInitRank = reinterpret_cast<decltype(api.commInitRank)>(sym("ncclCommInitRank"));
+  api.commDestroy = reinterpret_cast<decltype(api.commDestroy)>(sym("ncclCommDestroy"));
+  api.allReduce = reinterpret_cast<decltype(api.allReduce)>(sym("ncclAllReduce"));
+  api.send = reinterpret_cast<decltype(api.send)>(sym("ncclSend"));
+  api.recv = reinterpret_cast<decltype(api.recv)>(sym("ncclRecv"));
+  api.groupStart = reinterpret_cast<decltype(api.groupStart)>(sym("ncclGroupStart"));
+  api.groupEnd = reinterpret_cast<decltype(api.groupEnd)>(sym("ncclGroupEnd"));
+  api.getErrorString = reinterpret_cast<decltype(api.getErrorString)>(sym("ncclGetErrorString"));
+  api.ok = api.getUniqueId && api.commInitRank && api.commDestroy && api.allReduce && api.send && api.recv &&
+           api.groupStart && api.groupEnd;
+  return api;
+}
+
+#define SG_NCCL(call)                                                                        \
+  do {                                                                                       \
+    ncclResult_t r_ = (call);                                                                \
+    if (r_ != ncclSuccess) {                                                                 \
+      set_error("NCCL error %d (%s) at %s:%d", (int)r_,                                      \
+                nccl().getErrorString ? nccl().getErrorString(r_) : "?", __FILE__, __LINE__); \
+      return SG_ECUDA;                                                                       \
+    }                                                                                        \
+  } while (0)
+
+// Fill the ghost rows of `vecs` from the neighbours' owned boundary rows (one grouped call).
+int halo(sg_pcg* h, cudaStream_t s, std::initializer_list<double*> vecs) {
+  if (!h->dist || (h->left < 0 && h->right < 0)) return SG_OK;
+  NcclApi& api = nccl();
+  ncclComm_t comm = static_cast<ncclComm_t>(h->comm);
+  SG_NCCL(api.groupStart());
+  for (double* v : vecs) {
+    if (h->left >= 0) {
+      SG_NCCL(api.send(v + h->own_lo, (size_t)h->ghost_lo, ncclFloat64, h->left, comm, s));
+      SG_NCCL(api.recv(v + h->own_lo - h->ghost_lo, (size_t)h->ghost_lo, ncclFloat64, h->left, comm, s));
+    }
+    if (h->right >= 0) {
+      SG_NCCL(api.send(v + h->own_hi - h->ghost_hi, (size_t)h->ghost_hi, ncclFloat64, h->right, comm, s));
+      SG_NCCL(api.recv(v + h->own_hi, (size_t)h->ghost_hi, ncclFloat64, h->right, comm, s));
+    }
+  }
+  SG_NCCL(api.groupEnd());
+  return SG_OK;
+}
+
+// All-reduce the published sums, then the finaliser (row-partitioned mode only).
+int reduce_fin(sg_pcg* h, cudaStream_t s, int kind, int arg) {
+  if (!h->dist) return SG_OK;
+  SG_NCCL(nccl().allReduce(h->gsum, h->gsum, (size_t)2 * h->S, ncclFloat64, ncclSum,
+                           static_cast<ncclComm_t>(h->comm), s));
+  k_fin<<<(h->S + 127) / 128, 128, 0, s>>>(h->D, kind, h->S, arg);
+  SG_LAUNCH_CHECK("k_fin");
+  return SG_OK;
+}
+}  // namespace
 
 namespace {
 
@@ -1587,6 +1707,38 @@ int launch_iteration(sg_pcg* h, cudaStream_t s, int par, bool refresh, cudaEvent
     if (ev) {
       k_snapshot<<<1, 1, 0, s>>>(h->ctl); ++k;
       SG_CUDA(cudaEventRecordWithFlags(ev[0], s, cudaEventRecordExternal));
+    }
+    if (h->dist) {  // row partition: unfused kernels, in-graph halo exchanges and all-reduces
+      double* dc = par ? h->D.d1 : h->D.d0;
+      double* rc = par ? h->D.r1 : h->D.r0;
+      double* rn = par ? h->D.r0 : h->D.r1;
+      int rc2 = halo(h, s, {h->D.s, dc, h->D.x});
+      if (rc2) return rc2;
+      k_iter1<PRE, FMT, ND, SH><<<g, PR, 0, s>>>(h->D, par); ++k;
+      if ((rc2 = reduce_fin(h, s, FIN_K1, 0))) return rc2;
+      if (ev) SG_CUDA(cudaEventRecordWithFlags(ev[1], s, cudaEventRecordExternal));
+      if (!refresh) {
+        if (PRE == SG_PRECOND_LEARNED && (rc2 = halo(h, s, {rc, h->D.q}))) return rc2;
+        k_iter2<PRE, FMT, ND, SH><<<g, PR, 0, s>>>(h->D, par); ++k;
+        if ((rc2 = reduce_fin(h, s, FIN_RR, 0))) return rc2;
+      } else {
+        k_refresh_x<<<g, PR, 0, s>>>(h->D, par); ++k;
+        if ((rc2 = halo(h, s, {h->D.x}))) return rc2;
+        k_refresh_r<FMT, ND, SH><<<g, PR, 0, s>>>(h->D, par); ++k;
+        if ((rc2 = reduce_fin(h, s, FIN_RR, 0))) return rc2;
+        if (PRE == SG_PRECOND_LEARNED) {
+          if ((rc2 = halo(h, s, {rn}))) return rc2;
+          k_refresh_t<FMT, ND, SH><<<g, PR, 0, s>>>(h->D, par); ++k;
+        }
+      }
+      if (ev) SG_CUDA(cudaEventRecordWithFlags(ev[2], s, cudaEventRecordExternal));
+      if (PRE == SG_PRECOND_LEARNED && (rc2 = halo(h, s, {h->D.t}))) return rc2;
+      k_iter3<PRE, FMT, ND, SH><<<g, PR, 0, s>>>(h->D, par, refresh ? 1 : 0); ++k;
+      if ((rc2 = reduce_fin(h, s, FIN_K3, refresh ? 1 : 0))) return rc2;
+      if (ev) SG_CUDA(cudaEventRecordWithFlags(ev[3], s, cudaEventRecordExternal));
+      SG_LAUNCH_CHECK("pcg iteration (row partition)");
+      *nk += k;
+      return SG_OK;
     }
     constexpr int FS = FMT >= 1 ? FMT : 1;
     constexpr int NS = ND > 0 ? ND : 1;
@@ -2089,6 +2241,17 @@ extern "C" int sg_pcg_solve(sg_pcg* h, const double* b, double* x, const sg_solv
     constexpr int FMT = decltype(Fc)::value;
     constexpr int ND = decltype(Nc)::value;
     constexpr bool SH = decltype(SHc)::value;
+    if (h->dist) {
+      int rc2 = halo(h, s, {h->D.b});
+      if (rc2) return rc2;
+      k_setup1<PRE, FMT, ND, SH><<<g, PR, 0, s>>>(h->D);
+      if ((rc2 = reduce_fin(h, s, FIN_SETUP1, 0))) return rc2;
+      if (PRE == SG_PRECOND_LEARNED && (rc2 = halo(h, s, {h->D.t}))) return rc2;
+      k_setup2<PRE, FMT, ND, SH><<<g, PR, 0, s>>>(h->D);
+      if ((rc2 = reduce_fin(h, s, FIN_SETUP2, 0))) return rc2;
+      SG_LAUNCH_CHECK("pcg setup (row partition)");
+      return SG_OK;
+    }
     k_setup1<PRE, FMT, ND, SH><<<g, PR, 0, s>>>(h->D);
     k_setup2<PRE, FMT, ND, SH><<<g, PR, 0, s>>>(h->D);
     SG_LAUNCH_CHECK("pcg setup");
@@ -2223,4 +2386,87 @@ extern "C" void sg_pcg_destroy(sg_pcg* h) {
   if (h->d_flag) cudaFree(h->d_flag);
   if (h->mem) cudaFree(h->mem);
   delete h;
+}
+
+// ------------------------------------------------------------------ row-partitioned mode API
+extern "C" int sg_nccl_unique_id(void* out128) {
+  if (!nccl().ok) { set_error("libnccl.so.2 not found (needed for the row-partitioned solve)"); return SG_EUNSUPPORTED; }
+  ncclUniqueId id;
+  SG_NCCL(nccl().getUniqueId(&id));
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  memcpy(out128, &id, sizeof(id));
+  return SG_OK;
+}
+
+extern "C" int sg_nccl_comm_init(void** comm_out, const void* id128, int32_t world, int32_t rank) {
+  if (!nccl().ok) { set_error("libnccl.so.2 not found (needed for the row-partitioned solve)"); return SG_EUNSUPPORTED; }
+  ncclUniqueId id;
+  memcpy(&id, id128, sizeof(id));
+  ncclComm_t comm;
+  SG_NCCL(nccl().commInitRank(&comm, world, id, rank));
+  *comm_out = comm;
+  return SG_OK;
+}
+
+extern "C" int sg_nccl_comm_destroy(void* comm) {
+  if (comm && nccl().ok) SG_NCCL(nccl().commDestroy(static_cast<ncclComm_t>(comm)));
+  return SG_OK;
+}
+
+extern "C" int sg_pcg_create_part(sg_pcg** out, int64_t n_ext, int64_t own_lo, int64_t own_hi,
+                                  const int32_t* a_offs, const int32_t* a_cols, const double* a_vals,
+                                  int precond_kind, const int32_t* g_offs, const int32_t* g_cols,
+                                  const double* g_vals, const int32_t* gt_offs, const int32_t* gt_cols,
+                                  const double* gt_vals, const double* inv_diag, double epsilon, void* stream) {
+  if (!(0 <= own_lo && own_lo < own_hi && own_hi <= n_ext)) { set_error("bad owned row range"); return SG_EINVAL; }
+  const int64_t starts[2] = {0, n_ext};
+  int rc = sg_pcg_create(out, 1, starts, a_offs, a_cols, a_vals, precond_kind, g_offs, g_cols, g_vals, gt_offs,
+                         gt_cols, gt_vals, inv_diag, epsilon, stream);
+  if (rc) return rc;
+  sg_pcg* h = *out;
+  cudaStream_t s = as_stream(stream);
+  // tiles (and every dot product) over the owned rows only; ghost rows are read, never written
+  const int tile = h->D.tile;
+  std::vector<long long> blk_r0;
+  std::vector<int> blk_sys;
+  for (int64_t r = own_lo; r < own_hi; r += tile) { blk_r0.push_back(r); blk_sys.push_back(0); }
+  const int sb0[2] = {0, (int)blk_r0.size()};
+  const long long r1 = own_hi;
+  SG_CUDA(cudaMemcpyAsync(const_cast<long long*>(h->D.blk_r0), blk_r0.data(), blk_r0.size() * sizeof(long long),
+                          cudaMemcpyHostToDevice, s));
+  SG_CUDA(cudaMemcpyAsync(const_cast<int*>(h->D.blk_sys), blk_sys.data(), blk_sys.size() * sizeof(int),
+                          cudaMemcpyHostToDevice, s));
+  SG_CUDA(cudaMemcpyAsync(const_cast<int*>(h->D.sys_blk0), sb0, sizeof(sb0), cudaMemcpyHostToDevice, s));
+  SG_CUDA(cudaMemcpyAsync(const_cast<long long*>(h->D.sys_r1), &r1, sizeof(r1), cudaMemcpyHostToDevice, s));
+  SG_CUDA(cudaStreamSynchronize(s));
+  h->nblk = (int)blk_r0.size();
+  h->own_lo = own_lo;
+  h->own_hi = own_hi;
+  h->staged = 0;  // the streaming kernels assume whole systems; the partition uses the tile kernels
+  h->strip = 0;
+  return SG_OK;
+}
+
+extern "C" int sg_pcg_set_comm(sg_pcg* h, void* comm, int32_t left, int32_t right, int64_t ghost_lo,
+                               int64_t ghost_hi) {
+  if (!h) { set_error("null handle"); return SG_EINVAL; }
+  if (comm && !nccl().ok) { set_error("libnccl.so.2 not found"); return SG_EUNSUPPORTED; }
+  if (ghost_lo < 0 || ghost_hi < 0 || ghost_lo > h->own_lo || h->own_hi + ghost_hi > h->n ||
+      (left >= 0 && ghost_lo > h->own_hi - h->own_lo) || (right >= 0 && ghost_hi > h->own_hi - h->own_lo)) {
+    set_error("ghost widths do not fit the extended system");
+    return SG_EINVAL;
+  }
+  if (!h->gsum) SG_CUDA(cudaMalloc(&h->gsum, 2 * (size_t)h->S * sizeof(double)));
+  h->comm = comm;
+  h->dist = comm ? 1 : 0;
+  h->left = left;
+  h->right = right;
+  h->ghost_lo = left >= 0 ? ghost_lo : 0;
+  h->ghost_hi = right >= 0 ? ghost_hi : 0;
+  h->D.dist = h->dist;
+  h->D.gsum = h->gsum;
+  for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);
+  h->graphs.clear();
+  h->graph_kernels.clear();
+  return SG_OK;
 }

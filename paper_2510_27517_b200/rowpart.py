@@ -30,7 +30,8 @@ import numpy as np
 from .batch import shard_range
 from .pcg import NotSpdError
 
-__all__ = ["HaloPlan", "build_plan", "hop_closure", "local_transpose_rows", "DistPcg"]
+__all__ = ["HaloPlan", "build_plan", "hop_closure", "local_transpose_rows", "DistPcg", "BandPart", "band_partition",
+           "band_local", "solve_rowpart_device"]
 
 
 def hop_closure(offs, cols, seeds: np.ndarray, hops: int) -> np.ndarray:
@@ -393,3 +394,173 @@ def solve_rowpart(A, meta, model, b, rtol=1e-8, max_iters=None, period=50, termi
     x_own, k, conv, hist = pcg.solve(b[plan.r0:plan.r1], rtol=rtol, max_iters=max_iters, period=period,
                                      termination=termination)
     return x_own, k, conv, hist, plan
+
+
+# ------------------------------------------------------------------------------------------------
+# Device-resident row partition (banded matrices, e.g. the C5 grid split into blocks of lines)
+# ------------------------------------------------------------------------------------------------
+@dataclass
+class BandPart:
+    """Rank `rank`'s extended local system for a contiguous row split of a banded matrix:
+    owned rows [r0, r1) plus `ghost_lo` / `ghost_hi` ghost rows (the neighbours' boundary rows;
+    ghost width = the half-bandwidth, clipped at the matrix ends)."""
+
+    n: int
+    rank: int
+    world: int
+    r0: int
+    r1: int
+    ghost_lo: int
+    ghost_hi: int
+
+    @property
+    def e0(self):
+        return self.r0 - self.ghost_lo
+
+    @property
+    def e1(self):
+        return self.r1 + self.ghost_hi
+
+    @property
+    def left(self):
+        return self.rank - 1 if self.rank > 0 else -1
+
+    @property
+    def right(self):
+        return self.rank + 1 if self.rank < self.world - 1 else -1
+
+
+def band_partition(offs, cols, n: int, rank: int, world: int) -> BandPart:
+    offs = np.asarray(offs, dtype=np.int64)
+    cols = np.asarray(cols, dtype=np.int64)
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(offs))
+    hb = int(np.max(np.abs(cols - rows))) if len(cols) else 0
+    r0, r1 = shard_range(n, rank, world)
+    gl = min(hb, r0) if rank > 0 else 0
+    gh = min(hb, n - r1) if rank < world - 1 else 0
+    for p in range(world):  # every owned block must be at least one band wide
+        a, b = shard_range(n, p, world)
+        if world > 1 and b - a < hb:
+            raise ValueError(f"rank {p} owns {b - a} rows, fewer than the half-bandwidth {hb}")
+    return BandPart(n, rank, world, r0, r1, gl, gh)
+
+
+def band_local(offs, cols, vals, part: BandPart):
+    """Rows [e0, e1) of a CSR matrix with columns shifted to the extended local index space;
+    entries whose column falls outside it (only possible in the outermost ghost rows) dropped."""
+    offs = np.asarray(offs, dtype=np.int64)
+    cols = np.asarray(cols, dtype=np.int64)
+    vals = np.asarray(vals, dtype=np.float64)
+    lo, hi = offs[part.e0], offs[part.e1]
+    c = cols[lo:hi]
+    v = vals[lo:hi]
+    r = np.repeat(np.arange(part.e0, part.e1), np.diff(offs[part.e0:part.e1 + 1]))
+    keep = (c >= part.e0) & (c < part.e1)
+    lo_offs = np.zeros(part.e1 - part.e0 + 1, dtype=np.int64)
+    np.add.at(lo_offs, r[keep] - part.e0 + 1, 1)
+    np.cumsum(lo_offs, out=lo_offs)
+    return lo_offs, c[keep] - part.e0, v[keep]
+
+
+def _nccl_comm(rank: int, world: int):
+    """One NCCL communicator for the solve: the unique id travels over torch.distributed when a
+    process group exists (a 1-rank communicator otherwise)."""
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    from . import _lib as L
+    uid = (ctypes.c_ubyte * 128)()
+    if rank == 0:
+        L.check(L.lib().sg_nccl_unique_id(ctypes.cast(uid, ctypes.c_void_p)), "nccl unique id")
+    if world > 1:
+        t = torch.tensor(list(bytes(uid)), dtype=torch.uint8,
+                         device=L.device() if dist.get_backend() == "nccl" else "cpu")
+        dist.broadcast(t, 0)
+        uid = (ctypes.c_ubyte * 128)(*t.cpu().tolist())
+    comm = ctypes.c_void_p()
+    L.check(L.lib().sg_nccl_comm_init(ctypes.byref(comm), ctypes.cast(uid, ctypes.c_void_p), world, rank),
+            "nccl comm init")
+    return comm
+
+
+def solve_rowpart_device(A, meta, model, b, rtol=1e-8, max_iters=None, period=50, termination="true_residual",
+                         rank=None, world=None):
+    """The hot path for one banded system split by rows across ranks, with the PCG loop on the
+    device: every rank builds its extended local system (owned rows + ghost rows), runs the GNN
+    on the receptive field of those rows (no communication: features are global),
+    and solves with sg_pcg in row-partitioned mode — halo exchanges and scalar all-reduces are
+    NCCL operations inside the captured iteration graphs.  Returns (x_own, k, converged,
+    history, part)."""
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    from . import _lib as L
+    from .gnn import forward_device
+    from .graphfeat import build_graph
+    from .pcg import SolveConfig, report_from
+    from .sparse import DeviceCsr
+    if rank is None:
+        init = dist.is_available() and dist.is_initialized()
+        rank = dist.get_rank() if init else 0
+        world = dist.get_world_size() if init else 1
+    n = A.n_rows
+    offs, cols, vals = A.row_offsets, A.col_indices, A.values
+    part = band_partition(offs, cols, n, rank, world)
+    gr = build_graph(A, meta)
+    node, edge = gr.node_features, gr.edge_features[:, 0]
+    # GNN on the (L+2)-hop receptive field of the extended rows: their G rows are exact
+    R = hop_closure(offs, cols, np.arange(part.e0, part.e1), model.config.n_layers + 2)
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(offs))
+    in_r = np.zeros(n, dtype=bool)
+    in_r[R] = True
+    keep = in_r[rows] & in_r[cols]
+    remap = -np.ones(n, dtype=np.int64)
+    remap[R] = np.arange(len(R))
+    sub_offs = np.zeros(len(R) + 1, dtype=np.int64)
+    np.add.at(sub_offs, remap[rows[keep]] + 1, 1)
+    np.cumsum(sub_offs, out=sub_offs)
+    sub = DeviceCsr(len(R), len(R), L.to_device(sub_offs.astype(np.int32), torch.int32),
+                    L.to_device(remap[cols[keep]].astype(np.int32), torch.int32),
+                    L.to_device(vals[keep], torch.float64))
+    g_sub = forward_device(model, sub, L.to_device(np.ascontiguousarray(node[R]).ravel(), torch.float64),
+                           L.to_device(edge[keep], torch.float64), gr.d_node).cpu().numpy()
+    g = np.zeros(len(vals))
+    g[np.flatnonzero(keep)] = g_sub
+    ao, ac, av = band_local(offs, cols, vals, part)
+    _, _, gv = band_local(offs, cols, g, part)
+    ne = part.e1 - part.e0
+    a_dev = DeviceCsr(ne, ne, L.to_device(ao.astype(np.int32), torch.int32), L.to_device(ac.astype(np.int32), torch.int32),
+                      L.to_device(av, torch.float64))
+    g_dev = a_dev.with_values(L.to_device(gv, torch.float64))
+    gt_dev = g_dev.transpose()
+    h = ctypes.c_void_p()
+    L.check(L.lib().sg_pcg_create_part(ctypes.byref(h), ne, part.ghost_lo, part.ghost_lo + (part.r1 - part.r0),
+                                       L.ptr(a_dev.offs), L.ptr(a_dev.cols), L.ptr(a_dev.vals), L.PRECOND_LEARNED,
+                                       L.ptr(g_dev.offs), L.ptr(g_dev.cols), L.ptr(g_dev.vals), L.ptr(gt_dev.offs),
+                                       L.ptr(gt_dev.cols), L.ptr(gt_dev.vals), None, float(model.config.epsilon),
+                                       L.stream_ptr()), "pcg_create_part")
+    comm = _nccl_comm(rank, world)
+    try:
+        L.check(L.lib().sg_pcg_set_comm(h, comm, part.left, part.right, part.ghost_lo, part.ghost_hi), "set_comm")
+        cfg = SolveConfig(rtol=rtol, max_iters=max_iters, residual_refresh_period=period, termination=termination)
+        b_ext = np.zeros(ne)
+        b_ext[part.ghost_lo:part.ghost_lo + part.r1 - part.r0] = np.asarray(b, dtype=np.float64)[part.r0:part.r1]
+        bd = L.to_device(b_ext, torch.float64)
+        xd = L.empty(ne, torch.float64)
+        res = (L.SolveResultC * 1)()
+        ns = ctypes.c_int64(0)
+        L.check(L.lib().sg_pcg_solve(h, L.ptr(bd), L.ptr(xd), ctypes.byref(cfg.to_c()), res, ctypes.byref(ns),
+                                     L.stream_ptr()), "pcg_solve (row partition)")
+        hist = np.empty(max(int(res[0].hist_len), 0))
+        if len(hist):
+            L.check(L.lib().sg_pcg_history(h, 0, hist.ctypes.data_as(ctypes.c_void_p), len(hist)))
+        x_own = xd[part.ghost_lo:part.ghost_lo + part.r1 - part.r0].cpu().numpy()
+        rep = report_from(res[0], x_own, hist.tolist(), 0, int(ns.value))
+    finally:
+        L.lib().sg_pcg_destroy(h)
+        L.lib().sg_nccl_comm_destroy(comm)
+    return rep.x, rep.k, rep.converged, rep.residual_history, part

@@ -185,3 +185,25 @@ def test_distributed_pcg_two_gloo_ranks(tmp_path):
     # two valid solutions at rtol 1e-8 differ by ~cond(A) * 1e-8; the residual is the contract
     assert out["res"] <= 1e-8 and out["dx"] < 1e-6
     assert out["hlen"] == out["k"] + 1
+
+
+def test_band_partition_extended_systems():
+    """Contiguous row split of a banded matrix (the device-resident row partition): owned blocks
+    tile the rows, neighbouring ghost widths agree (what one rank sends is what the other
+    receives), and every owned row of the extended local system equals the global row."""
+    from oracle import spaigraph_ref as O
+    from paper_2510_27517_b200.rowpart import band_local, band_partition
+    o, c, v, _ = O.gen_poisson2d(12, 9)
+    n = len(o) - 1
+    for world in (1, 2, 3):
+        parts = [band_partition(o, c, n, r, world) for r in range(world)]
+        assert parts[0].r0 == 0 and parts[-1].r1 == n
+        for a, b in zip(parts[:-1], parts[1:]):
+            assert a.r1 == b.r0 and a.ghost_hi == b.ghost_lo == 12  # half-bandwidth = nx
+        for p in parts:
+            lo, lc, lv = band_local(o, c, v, p)
+            for i in range(p.r0, p.r1):
+                li = i - p.e0
+                gl = slice(o[i], o[i + 1])
+                assert np.array_equal(lc[lo[li]:lo[li + 1]] + p.e0, c[gl])
+                assert np.array_equal(lv[lo[li]:lo[li + 1]], v[gl])
