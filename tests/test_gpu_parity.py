@@ -647,3 +647,23 @@ def test_rowpart_device_single_rank():
     o, c, v = (np.asarray(A.row_offsets), np.asarray(A.col_indices), np.asarray(A.values))
     assert np.linalg.norm(b - O.spmv(o, c, v, x)) / np.linalg.norm(b) <= 1.01e-8
     assert len(hist) == k + 1
+
+
+def test_sliding_window_two_chunk_halo():
+    """5-point grids with 256 < W <= 512 run the sliding-window kernels with a two-chunk halo
+    (NH = 2: deeper rings, 4-chunk warm-up): k and residual against the oracle."""
+    import os
+    m = P.load_checkpoint(os.path.join(os.path.dirname(__file__), "golden", "trained_heat16.spaignn"))
+    for nx, ny, seed in ((400, 12, 1), (300, 9, 2)):
+        A, meta = P.gen_poisson2d(nx, ny, coeff_seed=seed)
+        G = P.forward(m, P.build_graph(A, meta)).G
+        M = P.build_learned_spai(G, m.config.epsilon)
+        b = P.gen_rhs(meta, seed)
+        rep = P.pcg_solve(A, b, M, P.SolveConfig(rtol=1e-8))
+        from paper_2510_27517_b200.pcg import _handle_for
+        assert _handle_for(A, M).stats()[2][7] == 1.0
+        o, c, v = (np.asarray(A.row_offsets), np.asarray(A.col_indices), np.asarray(A.values))
+        _, k, conv, _ = O.pcg_solve(o, c, v, b, lambda r: O.learned_apply(A.n_rows, o, c, np.asarray(G.values),
+                                                                        m.config.epsilon, r), rtol=1e-8)
+        assert rep.converged and conv and _k_close(rep.k, k), (nx, rep.k, k)
+        assert np.linalg.norm(b - O.spmv(o, c, v, rep.x)) / np.linalg.norm(b) <= 1.01e-8
