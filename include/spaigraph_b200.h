@@ -286,6 +286,13 @@ int sg_segment_sum(int64_t n, int32_t d, const int32_t* offs, const int32_t* per
  * Workspace query with ws == NULL. */
 int sg_outer_sum(int64_t N, int32_t da, int32_t db, const double* A, int32_t lda, const double* B, int32_t ldb,
                  double* out, int32_t accumulate, void* ws, size_t* ws_bytes, void* stream);
+/* build_fsai (precond.py:262-305): values of the lower-triangular factor on the lower pattern
+ * (l_offs, l_cols) of A, one dense Cholesky solve per row; rows whose local system is not SPD
+ * fall back to 1/sqrt(a_ii) (count in *fallbacks_host).  Rows with > 16 lower entries:
+ * SG_EUNSUPPORTED.  Synchronizes. */
+int sg_fsai_build(int64_t n, const int32_t* a_offs, const int32_t* a_cols, const double* a_vals,
+                  const int32_t* l_offs, const int32_t* l_cols, double* l_vals, int64_t* fallbacks_host,
+                  void* stream);
 /* adamw_step (training.py:126-147) with grads / grad_div, t the 1-based step; in place. */
 int sg_adamw(int64_t n, double* params, const double* grads, double* m, double* v, double lr, double wd,
              double beta1, double beta2, double eps, int64_t t, double grad_div, void* stream);

@@ -75,6 +75,7 @@ SIGNATURES = {
     "sg_segment_sum": (C.c_int, [i64, i32, vp, vp, vp, vp, i32, vp]),
     "sg_outer_sum": (C.c_int, [i64, i32, i32, vp, i32, vp, i32, vp, i32, vp, szp, vp]),
     "sg_adamw": (C.c_int, [i64, vp, vp, vp, vp, f64, f64, f64, f64, f64, i64, f64, vp]),
+    "sg_fsai_build": (C.c_int, [i64, vp, vp, vp, vp, vp, vp, C.POINTER(C.c_int64), vp]),
     "sg_nccl_unique_id": (C.c_int, [vp]),
     "sg_nccl_comm_init": (C.c_int, [C.POINTER(C.c_void_p), vp, i32, i32]),
     "sg_nccl_comm_destroy": (C.c_int, [vp]),

@@ -2,8 +2,8 @@
 
 `bench_rows(items, preconditioners, rtols, max_iters, model)` produces the reference's rows
 (matrix_id, preconditioner, rtol, k, t_construct_ns, t_apply_total_ns, t_cg_total_ns, converged)
-for the preconditioners this package runs on the device ("none", "diag", "learned"; the IC(0)
-and FSAI baselines stay out of scope and raise NotImplementedError), and `write_bench_csv`
+for the preconditioners this package runs on the device ("none", "diag", "fsai", "learned"; the
+IC(0) baseline stays out of scope and raises NotImplementedError), and `write_bench_csv`
 writes bench.csv with the reference header.  Unlike the reference, the learned column's
 t_construct_ns includes the GNN inference (graph -> G -> G^T), measured on the device clock;
 t_apply_total_ns is 0 because the apply is fused into the PCG iteration kernels
@@ -16,7 +16,7 @@ import time
 
 from .gnn import forward
 from .pcg import SolveConfig, pcg_solve
-from .precond import build_identity, build_jacobi, build_learned_spai
+from .precond import build_fsai, build_identity, build_jacobi, build_learned_spai
 
 __all__ = ["BENCH_HEADER", "bench_rows", "write_bench_csv", "summarize"]
 
@@ -40,8 +40,10 @@ def _build(name, A, graph, model):
         torch.cuda.synchronize()
         M.t_construct_ns = time.perf_counter_ns() - t0
         return M
-    if name in ("ic0", "fsai"):
-        raise NotImplementedError(f"{name} is a CPU baseline of the reference, not part of the GPU path")
+    if name == "fsai":
+        return build_fsai(A)
+    if name == "ic0":
+        raise NotImplementedError("ic0 is a CPU baseline of the reference (triangular solves), not part of the GPU path")
     raise ValueError(f"unknown preconditioner {name!r}")
 
 

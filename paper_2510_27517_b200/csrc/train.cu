@@ -189,3 +189,97 @@ extern "C" int sg_adamw(int64_t n, double* params, const double* grads, double* 
   SG_LAUNCH_CHECK("k_adamw");
   return SG_OK;
 }
+
+// ------------------------------------------------------------------ FSAI construction
+// build_fsai (precond.py:262-305) on the device, one thread per row: the
+// local SPD system A[P_i, P_i] g = e_last over the row's lower pattern P_i (gathered from A's
+// CSR by binary search), Cholesky (dense.py:56-69: pivots, then column updates), forward and
+// back substitution (dense.py:72-93), g / sqrt(g_last); a non-positive / non-finite pivot falls
+// back to 1/sqrt(a_ii) on the diagonal.  Patterns wider than kFsaiMax entries per row are
+// reported (SG_EUNSUPPORTED) instead of solved.
+namespace sg {
+constexpr int kFsaiMax = 16;
+
+__device__ double fsai_a(const int32_t* ao, const int32_t* ac, const double* av, int row, int col) {
+  int lo = ao[row], hi = ao[row + 1];
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (ac[mid] < col) lo = mid + 1;
+    else hi = mid;
+  }
+  return (lo < ao[row + 1] && ac[lo] == col) ? av[lo] : 0.0;
+}
+
+__global__ void k_fsai(int64_t n, const int32_t* __restrict__ ao, const int32_t* __restrict__ ac,
+                       const double* __restrict__ av, const int32_t* __restrict__ lo_, const int32_t* __restrict__ lc,
+                       double* __restrict__ lv, unsigned int* fallbacks, unsigned int* too_wide) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int p0 = lo_[i], m = lo_[i + 1] - p0;
+    if (m > kFsaiMax) { atomicAdd(too_wide, 1u); continue; }
+    double Lm[kFsaiMax][kFsaiMax];
+    double y[kFsaiMax];
+    bool ok = true;
+    // Cholesky, column by column (dense.py:62-68)
+    for (int j = 0; j < m && ok; ++j) {
+      const int cj = lc[p0 + j];
+      double dot = 0.0;
+      for (int k = 0; k < j; ++k) dot = __dadd_rn(dot, __dmul_rn(Lm[j][k], Lm[j][k]));
+      const double pivot = __dsub_rn(fsai_a(ao, ac, av, cj, cj), dot);
+      if (!(pivot > 0.0) || !isfinite(pivot)) { ok = false; break; }
+      Lm[j][j] = __dsqrt_rn(pivot);
+      for (int r = j + 1; r < m; ++r) {
+        double d2 = 0.0;
+        for (int k = 0; k < j; ++k) d2 = __dadd_rn(d2, __dmul_rn(Lm[r][k], Lm[j][k]));
+        Lm[r][j] = __ddiv_rn(__dsub_rn(fsai_a(ao, ac, av, lc[p0 + r], cj), d2), Lm[j][j]);
+      }
+    }
+    if (ok) {
+      // L y = e_last, then L^T g = y (g in place of y)
+      for (int r = 0; r < m; ++r) {
+        double s = 0.0;
+        for (int k = 0; k < r; ++k) s = __dadd_rn(s, __dmul_rn(Lm[r][k], y[k]));
+        y[r] = __ddiv_rn(__dsub_rn(r == m - 1 ? 1.0 : 0.0, s), Lm[r][r]);
+      }
+      for (int r = m - 1; r >= 0; --r) {
+        double s = 0.0;
+        for (int k = r + 1; k < m; ++k) s = __dadd_rn(s, __dmul_rn(Lm[k][r], y[k]));
+        y[r] = __ddiv_rn(__dsub_rn(y[r], s), Lm[r][r]);
+      }
+      const double pv = y[m - 1];
+      if (!(pv > 0.0) || !isfinite(pv)) ok = false;
+      else {
+        const double sc = __dsqrt_rn(pv);
+        for (int r = 0; r < m; ++r) lv[p0 + r] = __ddiv_rn(y[r], sc);
+      }
+    }
+    if (!ok) {
+      atomicAdd(fallbacks, 1u);
+      for (int r = 0; r < m - 1; ++r) lv[p0 + r] = 0.0;
+      lv[p0 + m - 1] = __ddiv_rn(1.0, __dsqrt_rn(fsai_a(ao, ac, av, (int)i, (int)i)));
+    }
+  }
+}
+}  // namespace sg
+
+extern "C" int sg_fsai_build(int64_t n, const int32_t* a_offs, const int32_t* a_cols, const double* a_vals,
+                             const int32_t* l_offs, const int32_t* l_cols, double* l_vals, int64_t* fallbacks_host,
+                             void* stream) {
+  cudaStream_t s = as_stream(stream);
+  unsigned int* cnt = nullptr;
+  SG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&cnt), 2 * sizeof(unsigned int), s));
+  SG_CUDA(cudaMemsetAsync(cnt, 0, 2 * sizeof(unsigned int), s));
+  if (n > 0) {
+    k_fsai<<<grid_of(n), 128, 0, s>>>(n, a_offs, a_cols, a_vals, l_offs, l_cols, l_vals, cnt, cnt + 1);
+    SG_LAUNCH_CHECK("k_fsai");
+  }
+  unsigned int h[2] = {0, 0};
+  SG_CUDA(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, s));
+  SG_CUDA(cudaStreamSynchronize(s));
+  cudaFreeAsync(cnt, s);
+  if (h[1]) {
+    set_error("FSAI: %u rows have more than %d lower-pattern entries", h[1], kFsaiMax);
+    return SG_EUNSUPPORTED;
+  }
+  if (fallbacks_host) *fallbacks_host = h[0];
+  return SG_OK;
+}

@@ -16,8 +16,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib as L
-from .precond import (IdentityPreconditioner, JacobiPreconditioner, LearnedSpaiPreconditioner,
-                      Preconditioner)
+from .precond import (FsaiPreconditioner, IdentityPreconditioner, JacobiPreconditioner,
+                      LearnedSpaiPreconditioner, Preconditioner)
 from .sparse import SparseMatrix
 
 __all__ = ["SolveConfig", "SolveReport", "NotSpdError", "pcg_solve", "PcgHandle"]
@@ -162,13 +162,17 @@ def _handle_for(A: SparseMatrix, M: Preconditioner) -> PcgHandle:
         if M.n != A.n_rows:
             raise ValueError(f"dimension mismatch: operator is {M.n}, matrix is {A.n_rows}")
         g, gt, inv, kind, eps = M.factor.device(), M.factor_t(), None, L.PRECOND_LEARNED, M.epsilon
+    elif isinstance(M, FsaiPreconditioner):  # M^{-1} = G^T G = F F^T with F = G^T, eps 0
+        if M.n != A.n_rows:
+            raise ValueError(f"dimension mismatch: operator is {M.n}, matrix is {A.n_rows}")
+        (g, gt), inv, kind, eps = M.factor_pair(), None, L.PRECOND_LEARNED, 0.0
     elif isinstance(M, JacobiPreconditioner):
         g, gt, inv, kind, eps = None, None, M.inv_diag_dev, L.PRECOND_JACOBI, 0.0
     elif isinstance(M, IdentityPreconditioner):
         g, gt, inv, kind, eps = None, None, None, L.PRECOND_IDENTITY, 0.0
     else:
         raise TypeError(f"preconditioner {type(M).__name__} is not supported by the fused GPU solver "
-                        "(supported: learned SPAI, Jacobi, identity)")
+                        "(supported: learned SPAI, FSAI, Jacobi, identity)")
     if isinstance(M, JacobiPreconditioner) and M.n != A.n_rows:
         raise ValueError(f"dimension mismatch: operator is {M.n}, matrix is {A.n_rows}")
     pat = lambda d: (None if d is None else (d.offs.data_ptr(), d.cols.data_ptr(), d.n_rows, d.nnz))  # noqa: E731

@@ -129,3 +129,63 @@ def build_learned_spai(factor: SparseMatrix, epsilon: float) -> LearnedSpaiPreco
     pre.factor_t()
     pre.t_construct_ns = time.perf_counter_ns() - t0
     return pre
+
+
+class FsaiPreconditioner(Preconditioner):
+    """precond.py:103-120: lower-triangular factor G with G A G^T ~= I; M^{-1} = G^T (G r)."""
+
+    variant = "fsai"
+    kind = L.PRECOND_LEARNED  # the fused PCG runs it as a factored M with F = G^T and eps = 0
+
+    def __init__(self, g_lower: SparseMatrix, fallback_rows: int, t_construct_ns: int = 0):
+        super().__init__(g_lower.n_rows, t_construct_ns)
+        self.g_lower = g_lower
+        self.fallback_rows = int(fallback_rows)
+        self._ft = None
+
+    def factor_pair(self):
+        """(F, F^T) = (G^T, G) as device CSR for the fused PCG kernels."""
+        if self._ft is None:
+            gl = self.g_lower.device()
+            self._ft = (gl.transpose(), gl)
+        return self._ft
+
+    def apply(self, r):
+        from .sparse import spmv, spmv_transpose
+        rd, was_t = self._check_dim(r)
+        out = spmv_transpose(self.g_lower, spmv(self.g_lower, rd))
+        return out if was_t else out.cpu().numpy()
+
+
+def build_fsai(A: SparseMatrix) -> FsaiPreconditioner:
+    """precond.py:262-305 with the per-row dense solves on the GPU (sg_fsai_build)."""
+    import ctypes as C
+
+    import torch
+    t0 = time.perf_counter_ns()
+    if A.n_rows != A.n_cols:
+        raise ValueError("matrix must be square")
+    offs, cols = np.asarray(A.row_offsets), np.asarray(A.col_indices)
+    rows = np.repeat(np.arange(A.n_rows, dtype=np.int64), np.diff(offs))
+    low = cols <= rows
+    l_offs = np.zeros(A.n_rows + 1, dtype=np.int64)
+    np.add.at(l_offs, rows[low] + 1, 1)
+    np.cumsum(l_offs, out=l_offs)
+    l_cols = cols[low]
+    last = l_offs[1:] - 1
+    bad = np.flatnonzero((np.diff(l_offs) == 0) | (l_cols[np.maximum(last, 0)] != np.arange(A.n_rows)))
+    if len(bad):
+        raise ValueError(f"missing diagonal entry in row {int(bad[0])}")
+    diag_d, _ = A.diagonal_device()
+    if bool((diag_d <= 0.0).any()):
+        raise ValueError("FSAI requires a positive diagonal")
+    a = A.device()
+    lo_d = L.to_device(l_offs.astype(np.int32), torch.int32)
+    lc_d = L.to_device(l_cols.astype(np.int32), torch.int32)
+    lv_d = L.empty(len(l_cols), torch.float64)
+    fb = C.c_int64(0)
+    L.check(L.lib().sg_fsai_build(A.n_rows, L.ptr(a.offs), L.ptr(a.cols), L.ptr(a.vals), L.ptr(lo_d), L.ptr(lc_d),
+                                  L.ptr(lv_d), C.byref(fb), L.stream_ptr()), "fsai_build")
+    from .sparse import DeviceCsr
+    g_lower = SparseMatrix.from_device(DeviceCsr(A.n_rows, A.n_cols, lo_d, lc_d, lv_d))
+    return FsaiPreconditioner(g_lower, fb.value, t_construct_ns=time.perf_counter_ns() - t0)

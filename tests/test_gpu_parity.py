@@ -667,3 +667,26 @@ def test_sliding_window_two_chunk_halo():
                                                                         m.config.epsilon, r), rtol=1e-8)
         assert rep.converged and conv and _k_close(rep.k, k), (nx, rep.k, k)
         assert np.linalg.norm(b - O.spmv(o, c, v, rep.x)) / np.linalg.norm(b) <= 1.01e-8
+
+
+def test_fsai_matches_reference():
+    """FSAI baseline (precond.py:262-305) built on the GPU vs the reference's factor, and the
+    fused PCG with it (M^{-1} = G^T G) against the reference's k."""
+    import os
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "golden_fsai.npz"))
+    A = P.SparseMatrix(len(g["heat_offs"]) - 1, len(g["heat_offs"]) - 1, g["heat_offs"], g["heat_cols"],
+                       g["heat_vals"])
+    M = P.build_fsai(A)
+    got = np.asarray(M.g_lower.values)
+    want = g["heat_lvals"]
+    assert M.fallback_rows == int(g["heat_fallbacks"])
+    assert np.max(np.abs(got - want)) <= 1e-13 * np.max(np.abs(want))
+    rep = P.pcg_solve(A, g["heat_b"], M, P.SolveConfig(rtol=1e-8))
+    assert rep.converged and _k_close(rep.k, int(g["heat_k"])), (rep.k, int(g["heat_k"]))
+    assert np.max(np.abs(rep.x - g["heat_x"])) <= 1e-7 * np.max(np.abs(g["heat_x"]))
+    # the standalone apply is G^T (G r)
+    r = np.random.default_rng(3).standard_normal(A.n_rows)
+    lo, lc = np.asarray(M.g_lower.row_offsets), np.asarray(M.g_lower.col_indices)
+    y = O.spmv(lo, lc, got, r)
+    s = O.spmv_transpose(A.n_rows, lo, lc, got, y)
+    assert np.allclose(M.apply(r), s, rtol=1e-14, atol=1e-300)
