@@ -83,7 +83,22 @@ struct Dia {
   const unsigned char* mask;  // [n], bit d: entry (i, i+off[d]) stored
 };
 
+// SELL-32 (sliced ELLPACK, slices of 32 rows stored column-major, padded to the slice's longest
+// row): entry k of row r at sbase[r/32] + 32 k + r%32, so one warp reading entry k of its 32
+// rows is one coalesced transaction.  Used for CSR matrices with long rows (C4) for A and G^T,
+// whose rows are summed strictly in order; row r's entries are still read in order, so the
+// reference's summation orders are unchanged.  (G's numpy-pairwise rows stay CSR: measured
+// faster there.)
+struct Sell {
+  const long long* sbase;  // [n/32 + 1]
+  const int32_t* cols;
+  const double* vals;
+  const int32_t* offs;     // the CSR offsets (row lengths)
+};
+
 struct Dev {
+  int sell_on;      // CSR path reads A, G^T (bit 1: also G) from their SELL-32 copies
+  Sell sa, sg, sgt;
   // row-partitioned mode (one system over several ranks): the last CTA of a reducing kernel
   // publishes the rank-local sums into gsum instead of finalising; an in-graph all-reduce and
   // k_fin_* then run the reference control flow on the global sums, identically on every rank
@@ -169,6 +184,19 @@ __global__ void k_csr_to_dia(const int32_t* __restrict__ offs, const int32_t* __
     for (int d = 0; d < MAXD; ++d)
       if (d < dia.nd) out[(int64_t)d * dia.ld + i] = v[d];
     if (mask) mask[i] = (unsigned char)m;
+  }
+}
+
+// CSR -> SELL-32 (values, or column indices when vals == null); padding entries stay as set.
+__global__ void k_csr_to_sell(int64_t n, const int32_t* __restrict__ offs, const int32_t* __restrict__ cols,
+                              const double* __restrict__ vals, const long long* __restrict__ sbase,
+                              int32_t* __restrict__ scols, double* __restrict__ svals) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const long long b = sbase[i >> 5] + (i & 31);
+    for (int32_t k = offs[i], e = 0; k < offs[i + 1]; ++k, ++e) {
+      if (svals) svals[b + 32LL * e] = vals[k];
+      else scols[b + 32LL * e] = cols[k];
+    }
   }
 }
 
@@ -462,12 +490,27 @@ struct Fmt {};
   constexpr int RPT = FMT >= 1 ? kRpt : 1;      \
   (void)T;
 
+template <int ORDER, int XM>
+__device__ __noinline__ double row_sell(const double* __restrict__ sv, const int32_t* __restrict__ sc, int len,
+                                        XF f) {
+  auto p = [&](int64_t k) { return mul(__ldg(sv + 32 * k), xval<XM>(f, __ldg(sc + 32 * k))); };
+  if (ORDER == kOrderSeq) return sequential_sum(p, 0, len);
+  return reduceat_sum(p, 0, len);
+}
+
+template <int ORDER, int XM>
+__device__ __forceinline__ double sell_row(const Sell& S, long long i, const XF& f) {
+  const long long b = S.sbase[i >> 5] + (i & 31);
+  return row_sell<ORDER, XM>(S.vals + b, S.cols + b, S.offs[i + 1] - S.offs[i], f);
+}
+
 // A-row (numpy order) for either format.
 template <int FMT, int ND, bool SH, int XM>
 __device__ __forceinline__ double rowA(const Dev& D, const RowTile<PR, (FMT == 0 ? PCAP : 4)>& T, long long i,
                                        long long r0, unsigned int m, const XF& f) {
   if (FMT == 1) return dia_row_numpy<ND, XM>(D.dia, D.dia.av, (int)i, m, f);
   if (FMT == 2) return dia_row_numpy_sym<ND, XM>(D.dia, D.dia.av, (int)i, m, f);
+  if (FMT == 0 && D.sell_on) return sell_row<kOrderNumpy, XM>(D.sa, i, f);
   return tile_row_dot<kOrderNumpy, SH, XM>(*reinterpret_cast<const RowTile<PR, PCAP>*>(&T), (int)(i - r0),
                                            D.a_cols, D.a_vals, f);
 }
@@ -475,6 +518,7 @@ template <int FMT, int ND, bool SH, int XM>
 __device__ __forceinline__ double rowG(const Dev& D, const RowTile<PR, (FMT == 0 ? PCAP : 4)>& T, long long i,
                                        long long r0, unsigned int m, const XF& f) {
   if (FMT >= 1) return dia_row_numpy<ND, XM>(D.dia, D.dia.gv, (int)i, m, f);
+  if (D.sell_on & 2) return sell_row<kOrderNumpy, XM>(D.sg, i, f);
   return tile_row_dot<kOrderNumpy, SH, XM>(*reinterpret_cast<const RowTile<PR, PCAP>*>(&T), (int)(i - r0),
                                            D.g_cols, D.g_vals, f);
 }
@@ -482,6 +526,7 @@ template <int FMT, int ND, bool SH, int XM>
 __device__ __forceinline__ double rowGt(const Dev& D, const RowTile<PR, (FMT == 0 ? PCAP : 4)>& T, long long i,
                                         long long r0, unsigned int m, const XF& f) {
   if (FMT >= 1) return dia_row_t_seq<ND, XM>(D.dia, D.dia.gv, (int)i, m, f);
+  if (D.sell_on) return sell_row<kOrderSeq, XM>(D.sgt, i, f);
   return tile_row_dot<kOrderSeq, SH, XM>(*reinterpret_cast<const RowTile<PR, PCAP>*>(&T), (int)(i - r0),
                                          D.gt_cols, D.gt_vals, f);
 }
@@ -489,7 +534,9 @@ __device__ __forceinline__ double rowGt(const Dev& D, const RowTile<PR, (FMT == 
 template <int FMT>
 __device__ __forceinline__ void stage(const Dev& D, RowTile<PR, (FMT == 0 ? PCAP : 4)>& T, long long r0,
                                       long long r1, const int32_t* offs, const int32_t* cols, const double* vals) {
-  if (FMT == 0) stage_rows(*reinterpret_cast<RowTile<PR, PCAP>*>(&T), r0, r1, offs, cols, vals);
+  // A and G^T rows come from their SELL copies when those exist; G (and everything else) stages
+  const bool sell = D.sell_on && (vals == D.a_vals || vals == D.gt_vals);
+  if (FMT == 0 && !sell) stage_rows(*reinterpret_cast<RowTile<PR, PCAP>*>(&T), r0, r1, offs, cols, vals);
 }
 
 __device__ __forceinline__ unsigned int dmask(const Dev& D, long long i, long long r1, int FMT) {
@@ -1555,6 +1602,9 @@ struct sg_pcg {
   int strip = 0;      // wide 5-point grid: 2-D strip sliding-window kernels (k_iter1_s5, k_iter23_s5)
   int k1sw = 1;       // K1 variant: 1 = sliding window (k_iter1_sw), 0 = tiles (k_iter1_st)
   int k23 = 1;        // fused K2+K3 variant: 1 = sliding window (k_iter23_sw), 0 = tiles (k_iter23_st)
+  void* sell_mem[3] = {nullptr, nullptr, nullptr};   // SELL-32 patterns of A, G, G^T
+  void* sell_vals[3] = {nullptr, nullptr, nullptr};
+  long long sell_total[3] = {0, 0, 0};
   int staged = 0;     // DIA with a small halo: halo-staged K1 and fused K2+K3 (k_iter1_st, k_iter23_st)
   // DIA format (0 = CSR)
   int dia_nd = 0;
@@ -1984,6 +2034,57 @@ int sw_setup(int nd, int nh, int* per_sm) {
   return nh == 1 ? sw_attr<8, 1>(per_sm) : sw_attr<8, 2>(per_sm);
 }
 
+
+// SELL-32 copy of a CSR pattern (slice offsets + column indices); values are filled per solve.
+int sell_pattern(sg_pcg* h, const int32_t* offs, const int32_t* cols, cudaStream_t s, Sell* out, void** mem_out,
+                 long long* total_out) {
+  const int64_t n = h->n;
+  std::vector<int32_t> ho(n + 1);
+  SG_CUDA(cudaMemcpyAsync(ho.data(), offs, (n + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  SG_CUDA(cudaStreamSynchronize(s));
+  const int64_t ns = (n + 31) / 32;
+  std::vector<long long> sb(ns + 1, 0);
+  for (int64_t sl = 0; sl < ns; ++sl) {
+    int mx = 0;
+    for (int64_t r = sl * 32; r < std::min<int64_t>(n, sl * 32 + 32); ++r) mx = std::max(mx, ho[r + 1] - ho[r]);
+    sb[sl + 1] = sb[sl] + 32LL * mx;
+  }
+  const long long total = sb[ns];
+  char* mem = nullptr;
+  const size_t bytes = (ns + 1) * sizeof(long long) + (size_t)total * sizeof(int32_t) + 512;
+  SG_CUDA(cudaMalloc(&mem, bytes));
+  long long* d_sb = reinterpret_cast<long long*>(mem);
+  int32_t* d_cols = reinterpret_cast<int32_t*>(mem + (((ns + 1) * sizeof(long long) + 255) / 256) * 256);
+  SG_CUDA(cudaMemcpyAsync(d_sb, sb.data(), (ns + 1) * sizeof(long long), cudaMemcpyHostToDevice, s));
+  const int gb = (int)std::min<int64_t>(n / 256 + 1, 148 * 16);
+  k_csr_to_sell<<<gb, 256, 0, s>>>(n, offs, cols, nullptr, d_sb, d_cols, nullptr);
+  SG_LAUNCH_CHECK("k_csr_to_sell (pattern)");
+  out->sbase = d_sb;
+  out->cols = d_cols;
+  out->offs = offs;
+  *mem_out = mem;
+  *total_out = total;
+  return SG_OK;
+}
+
+int setup_sell(sg_pcg* h, const int32_t* a_offs, const int32_t* a_cols, const int32_t* g_offs,
+               const int32_t* g_cols, const int32_t* gt_offs, const int32_t* gt_cols, cudaStream_t s) {
+  int rc = sell_pattern(h, a_offs, a_cols, s, &h->D.sa, &h->sell_mem[0], &h->sell_total[0]);
+  if (rc) return rc;
+  (void)g_offs; (void)g_cols;
+  if (h->pre == SG_PRECOND_LEARNED &&
+      (rc = sell_pattern(h, gt_offs, gt_cols, s, &h->D.sgt, &h->sell_mem[2], &h->sell_total[2])))
+    return rc;
+  for (int k = 0; k < 3; ++k)
+    if (h->sell_total[k] > 0) SG_CUDA(cudaMalloc(&h->sell_vals[k], (size_t)h->sell_total[k] * sizeof(double) + 64));
+  h->D.sa.vals = static_cast<double*>(h->sell_vals[0]);
+  h->D.sg.vals = static_cast<double*>(h->sell_vals[1]);
+  h->D.sgt.vals = static_cast<double*>(h->sell_vals[2]);
+  // G's rows are summed in numpy's pairwise order, whose 8-wide leaf blocks read better from the
+  // row-contiguous CSR (measured at C4: 3.8 ms CSR vs 5.0 ms SELL); A and G^T use SELL
+  h->D.sell_on = 1;
+  return SG_OK;
+}
 }  // namespace
 
 extern "C" int sg_pcg_create(sg_pcg** out, int32_t n_systems, const int64_t* sys_row_start_host,
@@ -2155,6 +2256,17 @@ extern "C" int sg_pcg_create(sg_pcg** out, int32_t n_systems, const int64_t* sys
   D.b = vec[0]; D.x = vec[1]; D.r0 = vec[2]; D.r1 = vec[3]; D.d0 = vec[4]; D.d1 = vec[5];
   D.q = vec[6]; D.s = vec[7]; D.t = vec[8];
   D.part = part; D.counter = counter; D.st = h->st; D.ctl = h->ctl;
+  D.sell_on = 0;
+  if (!h->dia_nd && !h->short_rows) {  // long CSR rows: SELL-32 copies (coalesced row walks)
+    int32_t nz = 0;
+    SG_CUDA(cudaMemcpyAsync(&nz, a_offs + n, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    SG_CUDA(cudaStreamSynchronize(s));
+    const char* sv = getenv("SG_PCG_SELL");
+    if (!(sv && sv[0] == '0') && n > 0 && (double)nz / (double)n >= 12.0) {
+      int rc = setup_sell(h, a_offs, a_cols, g_offs, g_cols, gt_offs, gt_cols, s);
+      if (rc) { sg_pcg_destroy(h); return rc; }
+    }
+  }
   SG_CUDA(cudaHostAlloc(&h->pinned_active, 2 * sizeof(unsigned int), cudaHostAllocDefault));
   SG_CUDA(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
   for (int k = 0; k < 4; ++k) SG_CUDA(cudaEventCreate(&h->ev[k]));
@@ -2212,6 +2324,16 @@ extern "C" int sg_pcg_solve(sg_pcg* h, const double* b, double* x, const sg_solv
       h->graph_kernels.clear();
       h->a_sym = sym;
     }
+  }
+  if (h->D.sell_on) {  // SELL-32 values of A, G, G^T (they may change between solves)
+    const int gb = (int)(h->n / 256 + 1 < 148 * 16 ? h->n / 256 + 1 : 148 * 16);
+    k_csr_to_sell<<<gb, 256, 0, s>>>(h->n, h->D.a_offs, nullptr, h->D.a_vals, h->D.sa.sbase, nullptr,
+                                     const_cast<double*>(h->D.sa.vals));
+    if (h->pre == SG_PRECOND_LEARNED)
+      k_csr_to_sell<<<gb, 256, 0, s>>>(h->n, h->D.gt_offs, nullptr, h->D.gt_vals, h->D.sgt.sbase, nullptr,
+                                       const_cast<double*>(h->D.sgt.vals));
+    SG_LAUNCH_CHECK("k_csr_to_sell");
+    h->kernels += h->pre == SG_PRECOND_LEARNED ? 2 : 1;
   }
   // per-system state
   std::vector<SysState> st(h->S);
@@ -2383,6 +2505,10 @@ extern "C" void sg_pcg_destroy(sg_pcg* h) {
   cudaDeviceSynchronize();
   if (h->hist) cudaFree(h->hist);
   if (h->dia_mem) cudaFree(h->dia_mem);
+  for (int k = 0; k < 3; ++k) {
+    if (h->sell_mem[k]) cudaFree(h->sell_mem[k]);
+    if (h->sell_vals[k]) cudaFree(h->sell_vals[k]);
+  }
   if (h->d_flag) cudaFree(h->d_flag);
   if (h->mem) cudaFree(h->mem);
   delete h;
