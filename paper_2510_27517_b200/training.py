@@ -17,7 +17,7 @@ from . import _lib as L
 from .sparse import SparseMatrix, _as_dev_vector, norm_device
 
 __all__ = ["NORM_KINDS", "matrix_norm", "sai_loss", "sai_loss_and_grad", "gnn_train_forward", "gnn_backward",
-           "matrix_loss_and_grad", "TrainConfig", "TrainItem", "TrainLog", "TrainingDivergedError", "AdamWDevice",
+           "matrix_loss_and_grad", "union_graph", "batch_loss_and_grad", "TrainConfig", "TrainItem", "TrainLog", "TrainingDivergedError", "AdamWDevice",
            "train"]
 
 NORM_KINDS = ("mean_abs_nonzero", "frobenius", "entrywise_l1")
@@ -393,6 +393,57 @@ def matrix_loss_and_grad(model, A: SparseMatrix, graph, rng, n_samples: int = 1,
     return mean_loss, gnn_backward(model, graph, st, dg)
 
 
+def union_graph(graphs):
+    """Block-diagonal union of MatrixGraphs (one GNN pass for a whole minibatch)."""
+    import torch
+    from .graphfeat import MatrixGraph
+    from .sparse import DeviceCsr
+    offs_parts, cols_parts, node_parts, edge_parts = [], [], [], []
+    n0 = e0 = 0
+    for g in graphs:
+        m = g.matrix
+        offs_parts.append(m.offs[:m.n_rows].to(torch.int64) + e0)
+        cols_parts.append(m.cols[:m.nnz].to(torch.int64) + n0)
+        node_parts.append(g.node_dev[:m.n_rows * g.d_node])
+        edge_parts.append(g.edge_dev[:m.nnz])
+        n0 += m.n_rows
+        e0 += m.nnz
+    dev = L.device()
+    offs = torch.cat(offs_parts + [torch.tensor([e0], dtype=torch.int64, device=dev)]).to(torch.int32)
+    cols = torch.cat(cols_parts).to(torch.int32)
+    mat = DeviceCsr(n0, n0, offs, cols, torch.zeros(e0, dtype=torch.float64, device=dev))
+    return MatrixGraph(n0, matrix=mat, node_dev=torch.cat(node_parts), edge_dev=torch.cat(edge_parts),
+                       norm_dev=None)
+
+
+def batch_loss_and_grad(model, items, rng, n_samples: int = 1, norm_kind: str = "mean_abs_nonzero"):
+    """The minibatch's losses and the SUM of their gradients with ONE training forward and ONE
+    backward over the union graph (probes drawn per matrix in batch order, as the reference)."""
+    import torch
+    ug = union_graph([it.graph for it in items])
+    st = gnn_train_forward(model, ug)
+    g_all = st["g"]
+    losses, dgs = [], []
+    e0 = 0
+    for it in items:
+        mat = it.graph.matrix
+        G = SparseMatrix.from_device(mat.with_values(g_all[e0:e0 + mat.nnz].contiguous()))
+        ls, dg = [], None
+        for _ in range(n_samples):
+            w = rng.standard_normal(it.A.n_rows)
+            loss, g = _loss(it.A, G, model.config.epsilon, w, norm_kind, True)
+            ls.append(loss)
+            gd = g if isinstance(g, torch.Tensor) else L.to_device(g, torch.float64)
+            dg = gd if dg is None else dg + gd
+        total = ls[0]
+        for lv in ls[1:]:
+            total = total + lv
+        losses.append(total * (1.0 / n_samples))
+        dgs.append(dg * (1.0 / n_samples) if n_samples > 1 else dg)
+        e0 += mat.nnz
+    return losses, gnn_backward(model, ug, st, torch.cat(dgs))
+
+
 # ------------------------------------------------------------------------------------------------
 # training.py:150-314 — TrainConfig / TrainItem / AdamW / train() with the step on the GPU
 # ------------------------------------------------------------------------------------------------
@@ -487,10 +538,13 @@ def _validation_mean_k(model, val_items) -> float:
     return float(np.mean(ks))
 
 
-def train(model, train_items, cfg: TrainConfig, val_items=(), log_path=None, checkpoint_path=None) -> TrainLog:
+def train(model, train_items, cfg: TrainConfig, val_items=(), log_path=None, checkpoint_path=None,
+          batched: bool = False) -> TrainLog:
     """training.py:242-314 with forward, loss, backward and AdamW on the GPU.  Same seeded
     shuffles and probes (one host PCG64 stream), same batch averaging, lr decay, divergence
-    handling, CSV log and checkpoints."""
+    handling, CSV log and checkpoints.  batched=True runs each minibatch as ONE union graph
+    (one forward, one backward; the gradient sum is then reduced in a different order than the
+    reference's per-matrix accumulation, so trajectories agree to rounding, not bit for bit)."""
     import csv
     import time
     import torch
@@ -519,18 +573,32 @@ def train(model, train_items, cfg: TrainConfig, val_items=(), log_path=None, che
             for start in range(0, len(order), cfg.batch_size):
                 batch = order[start:start + cfg.batch_size]
                 grad_sum.zero_()
-                for idx in batch:
-                    item = train_items[idx]
-                    loss_val, grad = matrix_loss_and_grad(model, item.A, item.graph, rng,
-                                                          cfg.hutchinson_samples_per_matrix, cfg.norm_kind)
-                    if not math.isfinite(loss_val):
-                        if checkpoint_path is not None:
-                            model.set_params_flat(last_good)
-                            save_checkpoint(model, checkpoint_path)
-                        raise TrainingDivergedError(epoch, loss_val, checkpoint_path)
-                    epoch_losses.append(loss_val)
+
+                def diverged(loss_val):
+                    if checkpoint_path is not None:
+                        model.set_params_flat(last_good)
+                        save_checkpoint(model, checkpoint_path)
+                    raise TrainingDivergedError(epoch, loss_val, checkpoint_path)
+
+                if batched:
+                    losses, grad = batch_loss_and_grad(model, [train_items[i] for i in batch], rng,
+                                                       cfg.hutchinson_samples_per_matrix, cfg.norm_kind)
+                    for loss_val in losses:
+                        if not math.isfinite(loss_val):
+                            diverged(loss_val)
+                        epoch_losses.append(loss_val)
                     L.check(L.lib().sg_axpby(L.ptr(grad_sum), L.ptr(grad_sum), L.ptr(grad), 1.0, grad.numel(), 0,
                                              L.stream_ptr()))
+                else:
+                    for idx in batch:
+                        item = train_items[idx]
+                        loss_val, grad = matrix_loss_and_grad(model, item.A, item.graph, rng,
+                                                              cfg.hutchinson_samples_per_matrix, cfg.norm_kind)
+                        if not math.isfinite(loss_val):
+                            diverged(loss_val)
+                        epoch_losses.append(loss_val)
+                        L.check(L.lib().sg_axpby(L.ptr(grad_sum), L.ptr(grad_sum), L.ptr(grad), 1.0,
+                                                 grad.numel(), 0, L.stream_ptr()))
                 t += 1
                 opt.step(grad_sum, t, lr, cfg.weight_decay, len(batch))
                 model.set_params_flat(params.cpu().numpy())

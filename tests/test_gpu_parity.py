@@ -690,3 +690,16 @@ def test_fsai_matches_reference():
     y = O.spmv(lo, lc, got, r)
     s = O.spmv_transpose(A.n_rows, lo, lc, got, y)
     assert np.allclose(M.apply(r), s, rtol=1e-14, atol=1e-300)
+
+
+def test_training_batched_union_graph():
+    """train(batched=True): one union-graph forward/backward per minibatch; same trajectory as
+    the reference to rounding (the gradient sum is reduced in another order)."""
+    import os
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "golden_train.npz"))
+    m = P.init_model(P.GnnConfig(d_node=3, seed=0))
+    items = [P.TrainItem(A, gr) for A, gr in _train_items()]
+    log = P.train(m, items, P.TrainConfig(epochs=3, batch_size=4, seed=0), batched=True)
+    assert np.allclose(log.losses(), g["train_losses"], rtol=1e-9, atol=0), (log.losses(), g["train_losses"])
+    p = m.params_flat()
+    assert np.max(np.abs(p - g["train_params"])) <= 1e-8 * np.max(np.abs(g["train_params"]))
