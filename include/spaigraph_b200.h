@@ -167,6 +167,11 @@ int sg_gnn_forward(const double* params, int64_t n_params, int n_layers, int hid
 int sg_spmv(int64_t n_rows, const int32_t* offs, const int32_t* cols, const double* vals,
             const double* x, double* y, void* stream);
 
+/* spmv for long rows (>= 32 entries on average, e.g. G on the A^2 pattern): one warp per row,
+ * the same numpy reduceat order (bit-identical to sg_spmv); replaces sparse.py:186-191 there. */
+int sg_spmv_warp(int64_t n_rows, const int32_t* offs, const int32_t* cols, const double* vals,
+                 const double* x, double* y, void* stream);
+
 /* spmv_transpose (sparse.py:194-201) given the explicit transpose (sg_csr_transpose): strictly
  * sequential per row from 0.0 == np.add.at order (bit-identical). */
 int sg_spmv_seq(int64_t n_rows, const int32_t* offs, const int32_t* cols, const double* vals,

@@ -55,6 +55,7 @@ SIGNATURES = {
                                  vp, vp, vp, vp, vp, vp, vp, szp, vp]),
     "sg_spmv": (C.c_int, [i64, vp, vp, vp, vp, vp, vp]),
     "sg_spmv_seq": (C.c_int, [i64, vp, vp, vp, vp, vp, vp]),
+    "sg_spmv_warp": (C.c_int, [i64, vp, vp, vp, vp, vp, vp]),
     "sg_learned_apply": (C.c_int, [i64, vp, vp, vp, vp, vp, vp, f64, vp, vp, vp, vp]),
     "sg_axpby": (C.c_int, [vp, vp, vp, f64, i64, C.c_int, vp]),
     "sg_dot": (C.c_int, [vp, vp, i64, vp, vp, szp, vp]),

@@ -774,6 +774,40 @@ __global__ void __launch_bounds__(PR, FMT >= 1 ? 8 : 1) k_iter3(Dev D, int par, 
   }
 }
 
+// K3 for long CSR rows of G (C4: ~420 per row on the A^2 pattern): one warp per row in numpy's
+// exact pairwise order (warp_row_numpy), coalesced instead of one thread walking each row.  The
+// CTA keeps k_iter3's rows and its per-thread r.s partials (one row per thread slot), so the
+// result, the partial sums and the finaliser are bit-identical to k_iter3's.
+__global__ void __launch_bounds__(PR) k_iter3_wr(Dev D, int par, int refreshed) {
+  __shared__ double red[PR / 32];
+  __shared__ int flag;
+  __shared__ int2 leaf[PR / 32][kWarpLeaves];
+  __shared__ double lsum[PR / 32][kWarpLeaves];
+  __shared__ double prow[PR];
+  int sys; long long r0, r1;
+  block_rows(D, sys, r0, r1);
+  if (D.st[sys].status != ST_RUN) return;
+  const double* rn = par ? D.r0 : D.r1;
+  const double eps = D.ctl->eps;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (long long i = r0 + w; i < r1; i += PR / 32) {
+    const double y = warp_row_numpy<0>(D.g_vals, D.g_cols, D.g_offs[i], D.g_offs[i + 1],
+                                       XF{D.t, nullptr, 0.0}, leaf[w], lsum[w]);
+    if (lane == 0) {
+      const double ri = rn[i];
+      const double si = add(y, mul(eps, ri));
+      D.s[i] = si;
+      prow[i - r0] = mul(ri, si);
+    }
+  }
+  __syncthreads();
+  const double prs = r0 + threadIdx.x < r1 ? prow[threadIdx.x] : 0.0;
+  if (arrive(D, sys, prs, 0.0, red, &flag)) {
+    const double rs = gather_partials(D, sys, 0, red);
+    if (threadIdx.x == 0) fin_k3(D, sys, rs, refreshed);
+  }
+}
+
 // Row-partitioned mode: the finalisers on the all-reduced sums (one thread per system; systems
 // the reducing kernel skipped are skipped here too, exactly as the kernel's own early return).
 enum { FIN_SETUP1 = 0, FIN_SETUP2 = 1, FIN_K1 = 2, FIN_RR = 3, FIN_K3 = 4 };
@@ -1601,6 +1635,7 @@ struct sg_pcg {
   double* gsum = nullptr;
   int strip = 0;      // wide 5-point grid: 2-D strip sliding-window kernels (k_iter1_s5, k_iter23_s5)
   int k1sw = 1;       // K1 variant: 1 = sliding window (k_iter1_sw), 0 = tiles (k_iter1_st)
+  int g_warp = 0;     // CSR G with long rows: K3 one warp per row (k_iter3_wr)
   int k23 = 1;        // fused K2+K3 variant: 1 = sliding window (k_iter23_sw), 0 = tiles (k_iter23_st)
   void* sell_mem[3] = {nullptr, nullptr, nullptr};   // SELL-32 patterns of A, G, G^T
   void* sell_vals[3] = {nullptr, nullptr, nullptr};
@@ -1838,7 +1873,9 @@ int launch_iteration(sg_pcg* h, cudaStream_t s, int par, bool refresh, cudaEvent
       if (PRE == SG_PRECOND_LEARNED) { k_refresh_t<FMT, ND, SH><<<g, PR, 0, s>>>(h->D, par); ++k; }
     }
     if (ev) SG_CUDA(cudaEventRecordWithFlags(ev[2], s, cudaEventRecordExternal));
-    k_iter3<PRE, FMT, ND, SH><<<g, PR, 0, s>>>(h->D, par, refresh ? 1 : 0); ++k;
+    if (FMT == 0 && PRE == SG_PRECOND_LEARNED && h->g_warp) k_iter3_wr<<<g, PR, 0, s>>>(h->D, par, refresh ? 1 : 0);
+    else k_iter3<PRE, FMT, ND, SH><<<g, PR, 0, s>>>(h->D, par, refresh ? 1 : 0);
+    ++k;
     if (ev) SG_CUDA(cudaEventRecordWithFlags(ev[3], s, cudaEventRecordExternal));
     SG_LAUNCH_CHECK("pcg iteration");
     *nk += k;
@@ -2265,6 +2302,13 @@ extern "C" int sg_pcg_create(sg_pcg** out, int32_t n_systems, const int64_t* sys
     if (!(sv && sv[0] == '0') && n > 0 && (double)nz / (double)n >= 12.0) {
       int rc = setup_sell(h, a_offs, a_cols, g_offs, g_cols, gt_offs, gt_cols, s);
       if (rc) { sg_pcg_destroy(h); return rc; }
+    }
+    if (precond_kind == SG_PRECOND_LEARNED && n > 0) {  // G rows of >= 32 entries: a warp per row
+      int32_t gz = 0;
+      SG_CUDA(cudaMemcpyAsync(&gz, g_offs + n, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+      SG_CUDA(cudaStreamSynchronize(s));
+      const char* wv = getenv("SG_PCG_GWARP");
+      h->g_warp = !(wv && wv[0] == '0') && (double)gz / (double)n >= 32.0;
     }
   }
   SG_CUDA(cudaHostAlloc(&h->pinned_active, 2 * sizeof(unsigned int), cudaHostAllocDefault));

@@ -20,6 +20,21 @@ __global__ void __launch_bounds__(kRows) k_spmv(int64_t n, const int32_t* __rest
     y[r0 + lr] = tile_row_dot<ORDER, false, 0>(t, lr, cols, vals, XF{x, nullptr, 0.0});
 }
 
+// Long rows (>= 32 entries on average): one warp per row in numpy's exact order (warp_row_numpy).
+constexpr int kWarpCta = 8;
+__global__ void __launch_bounds__(32 * kWarpCta) k_spmv_warp(int64_t n, const int32_t* __restrict__ offs,
+                                                             const int32_t* __restrict__ cols,
+                                                             const double* __restrict__ vals,
+                                                             const double* __restrict__ x, double* __restrict__ y) {
+  __shared__ int2 leaf[kWarpCta][kWarpLeaves];
+  __shared__ double lsum[kWarpCta][kWarpLeaves];
+  const int w = threadIdx.x >> 5;
+  for (int64_t i = (int64_t)blockIdx.x * kWarpCta + w; i < n; i += (int64_t)gridDim.x * kWarpCta) {
+    const double v = warp_row_numpy<0>(vals, cols, offs[i], offs[i + 1], XF{x, nullptr, 0.0}, leaf[w], lsum[w]);
+    if ((threadIdx.x & 31) == 0) y[i] = v;
+  }
+}
+
 // s = spmv(G, t) + eps * r
 __global__ void __launch_bounds__(kRows) k_apply_g(int64_t n, const int32_t* __restrict__ offs,
                                                    const int32_t* __restrict__ cols,
@@ -94,6 +109,16 @@ extern "C" int sg_spmv(int64_t n_rows, const int32_t* offs, const int32_t* cols,
   k_spmv<kOrderNumpy><<<(unsigned)ceil_div(n_rows, kRows), kRows, 0, as_stream(stream)>>>(
       n_rows, offs, cols, vals, x, y);
   SG_LAUNCH_CHECK("k_spmv<numpy>");
+  return SG_OK;
+}
+
+extern "C" int sg_spmv_warp(int64_t n_rows, const int32_t* offs, const int32_t* cols, const double* vals,
+                            const double* x, double* y, void* stream) {
+  if (n_rows <= 0) return SG_OK;
+  const int64_t g = ceil_div(n_rows, kWarpCta);
+  k_spmv_warp<<<(unsigned)(g < 148 * 64 ? g : 148 * 64), 32 * kWarpCta, 0, as_stream(stream)>>>(n_rows, offs, cols,
+                                                                                             vals, x, y);
+  SG_LAUNCH_CHECK("k_spmv_warp");
   return SG_OK;
 }
 

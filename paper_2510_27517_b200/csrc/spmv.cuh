@@ -121,4 +121,98 @@ __device__ __forceinline__ double tile_row_dot(const RowTile<ROWS, CAP>& t, int 
   return row_reduce<ORDER, SHORT, XM>(vals, cols, lo, hi, f);
 }
 
+// ------------------------------------------------------------------ warp per row, numpy order
+// np.add.reduceat of one long row [lo, hi), evaluated by a whole warp yet bit-identical to
+// reduceat_sum: v[lo] + pairwise(m = hi - lo - 1 values).  numpy's pairwise recursion splits
+// m > 128 into LEAVES of 64..128 values (left to right); each leaf sums 8 stride-8 accumulators
+// sequentially, then ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then its m % 8 tail in order.  Here the
+// 8 accumulators of a leaf are 8 lanes (4 leaves per pass, each lane walking its accumulator's
+// stride-8 subsequence in the same order, 8 consecutive values per 8 lanes => coalesced), the
+// accumulator tree is a 3-level xor butterfly (IEEE a + b == b + a bitwise, so the pairing is the
+// reference's), the tail is added by the leaf's first lane, and lane 0 combines the leaf sums
+// along the recursion.  Leaf table and sums live in the caller's per-warp shared scratch.
+// m > kWarpMaxVals (more than 32 leaves) falls back to lane 0 walking the row alone.
+constexpr int kWarpLeaves = 32;
+constexpr int kWarpMaxVals = 64 * kWarpLeaves;
+
+template <int XM>
+__device__ __noinline__ double warp_row_numpy(const double* __restrict__ vals, const int32_t* __restrict__ cols,
+                                              int lo, int hi, XF f, int2* __restrict__ leaf,
+                                              double* __restrict__ lsum) {
+  const int lane = threadIdx.x & 31;
+  auto p = [&](int k) { return mul(__ldg(vals + k), xval<XM>(f, __ldg(cols + k))); };
+  if (hi <= lo) return 0.0;
+  const int m = hi - lo - 1;
+  double res = 0.0;
+  if (m < 8 || m > kWarpMaxVals) {
+    if (lane == 0) res = reduceat_sum(p, lo, hi);
+    return __shfl_sync(0xffffffffu, res, 0);
+  }
+  int nl = 0;
+  if (lane == 0) {  // leaves of the recursion, left to right (depth <= log2(2048 / 64) + 1)
+    int2 stk[8];
+    int sp = 0;
+    stk[0] = make_int2(0, m);
+    while (sp >= 0) {
+      const int2 fr = stk[sp--];
+      if (fr.y <= 128) {
+        leaf[nl++] = fr;
+      } else {
+        int n2 = fr.y / 2;
+        n2 -= n2 % 8;
+        stk[++sp] = make_int2(fr.x + n2, fr.y - n2);
+        stk[++sp] = make_int2(fr.x, n2);
+      }
+    }
+  }
+  nl = __shfl_sync(0xffffffffu, nl, 0);
+  __syncwarp();
+  const int j = lane & 7;
+  const int base0 = lo + 1;
+  for (int g0 = 0; g0 < nl; g0 += 4) {
+    const int li = g0 + (lane >> 3);
+    double r = 0.0;
+    int2 L = make_int2(0, 0);
+    if (li < nl) {
+      L = leaf[li];
+      const int b = base0 + L.x, full = L.y & ~7;
+      r = p(b + j);
+      int i = j + 8;
+      for (; i + 24 < full; i += 32) {
+        const double v0 = p(b + i), v1 = p(b + i + 8), v2 = p(b + i + 16), v3 = p(b + i + 24);
+        r = add(add(add(add(r, v0), v1), v2), v3);
+      }
+      for (; i < full; i += 8) r = add(r, p(b + i));
+    }
+    r = add(r, __shfl_xor_sync(0xffffffffu, r, 1));
+    r = add(r, __shfl_xor_sync(0xffffffffu, r, 2));
+    r = add(r, __shfl_xor_sync(0xffffffffu, r, 4));
+    if (li < nl && j == 0) {
+      const int b = base0 + L.x;
+      for (int i = L.y & ~7; i < L.y; ++i) r = add(r, p(b + i));
+      lsum[li] = r;
+    }
+  }
+  __syncwarp();
+  if (lane == 0) {  // post-order combine along the same recursion
+    struct Fr { int n, state; double left; };
+    Fr st[8];
+    int sp = 0, next = 0;
+    st[0] = {m, 0, 0.0};
+    double ret = 0.0;
+    while (sp >= 0) {
+      Fr& fr = st[sp];
+      if (fr.n <= 128) { ret = lsum[next++]; --sp; continue; }
+      int n2 = fr.n / 2;
+      n2 -= n2 % 8;
+      if (fr.state == 0) { fr.state = 1; st[++sp] = {n2, 0, 0.0}; }
+      else if (fr.state == 1) { fr.left = ret; fr.state = 2; st[++sp] = {fr.n - n2, 0, 0.0}; }
+      else { ret = add(fr.left, ret); --sp; }
+    }
+    res = add(p(lo), ret);
+  }
+  __syncwarp();
+  return __shfl_sync(0xffffffffu, res, 0);
+}
+
 }  // namespace sg

@@ -309,8 +309,9 @@ def spmv(A: SparseMatrix, x):
     d = A.device()
     xd, was_t = _as_dev_vector(x, A.n_cols)
     y = L.empty(A.n_rows, torch.float64)
-    L.check(L.lib().sg_spmv(A.n_rows, L.ptr(d.offs), L.ptr(d.cols), L.ptr(d.vals), L.ptr(xd), L.ptr(y),
-                            L.stream_ptr()))
+    # long rows (C4's G on the A^2 pattern): a warp per row, same order
+    fn = L.lib().sg_spmv_warp if d.nnz >= 32 * A.n_rows else L.lib().sg_spmv
+    L.check(fn(A.n_rows, L.ptr(d.offs), L.ptr(d.cols), L.ptr(d.vals), L.ptr(xd), L.ptr(y), L.stream_ptr()))
     return y if was_t else y.cpu().numpy()
 
 

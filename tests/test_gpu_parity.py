@@ -107,6 +107,50 @@ def test_spmv_family_bit_exact(g_sparse):
         assert np.array_equal(P.build_learned_spai(Gr, 2e-3).apply(r), g[tag + "_apply"])
 
 
+def test_spmv_warp_rows_every_leaf_shape():
+    """sg_spmv_warp (a warp per row) against the oracle's reduceat order, bit for bit, over row
+    lengths that hit every branch: < 9 (sequential), one 8-accumulator leaf with and without a
+    tail, the first splits (129, 130, 136, 257), many leaves, exactly 32 leaves, and > 2049
+    (lane-0 fallback)."""
+    rng = np.random.default_rng(11)
+    lens = np.array([0, 1, 2, 8, 9, 16, 17, 100, 128, 129, 130, 131, 136, 137, 200, 257, 420, 421, 777, 1000,
+                     1024, 1500, 2048, 2049, 2050, 3000, 5000] * 3)
+    rng.shuffle(lens)
+    m = 6000
+    offs = np.concatenate([[0], np.cumsum(lens)])
+    cols = np.concatenate([np.sort(rng.choice(m, size=k, replace=False)) for k in lens])
+    vals = rng.standard_normal(len(cols)) * np.exp(rng.uniform(-20, 20, size=len(cols)))
+    A = P.SparseMatrix(len(lens), m, offs, cols, vals)
+    assert A.nnz >= 32 * len(lens)  # the Python spmv takes the warp kernel
+    x = rng.standard_normal(m)
+    assert np.array_equal(P.spmv(A, x), O.spmv(offs, cols, vals, x))
+
+
+def test_pcg_long_g_rows_warp_k3_bit_identical(monkeypatch):
+    """PCG on a mini C4 (G on the A^2 pattern, ~400 entries per row): K3 by warps per row
+    (k_iter3_wr) gives bit-identical x and residual history to the thread-per-row k_iter3."""
+    n = 3000
+    A = P.rand_spd_sparse(n, np.random.default_rng(5), extra_per_row=10)
+    from paper_2510_27517_b200.sparse import pad_to_pattern, pattern_square
+    Ap = pad_to_pattern(A, pattern_square(A))
+    m = P.init_model(P.GnnConfig(d_node=2, seed=0))
+    G = P.forward(m, P.build_graph(Ap)).G
+    assert G.nnz >= 32 * n
+    b = P.gen_rhs(n, 10**6)
+    cfg = P.SolveConfig(rtol=1e-8, max_iters=60, residual_refresh_period=7)
+    reps = []
+    import paper_2510_27517_b200.pcg as PC
+    for flag in ("1", "0"):
+        monkeypatch.setenv("SG_PCG_GWARP", flag)
+        for h in (PC._HANDLES or {}).values():  # the variant is chosen when a handle is created
+            h.close()
+        PC._HANDLES = None
+        reps.append(P.pcg_solve(A, b, P.build_learned_spai(G, 1e-4), cfg))
+    assert reps[0].k == reps[1].k
+    assert np.array_equal(reps[0].x, reps[1].x)
+    assert np.array_equal(np.asarray(reps[0].residual_history), np.asarray(reps[1].residual_history))
+
+
 def test_spmv_large_random_rows_vs_oracle():
     rng = np.random.default_rng(3)
     n = 5000
