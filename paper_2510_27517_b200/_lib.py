@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libspaigraph_b200.so")
+# SG_LIB_PATH: an alternative build of the same library (kernel-variant A/B runs in profiles/)
+LIB_PATH = os.environ.get("SG_LIB_PATH") or os.path.join(HERE, "libspaigraph_b200.so")
 
 SG_OK, SG_EINVAL, SG_ENOTSPD, SG_ECUDA, SG_EUNSUPPORTED, SG_EDUPLICATE = range(6)
 PRECOND_IDENTITY, PRECOND_JACOBI, PRECOND_LEARNED = 0, 1, 2

@@ -774,6 +774,47 @@ __global__ void __launch_bounds__(PR, FMT >= 1 ? 8 : 1) k_iter3(Dev D, int par, 
   }
 }
 
+// K2 (SPLIT: r' already written by k_pre_r) for long CSR rows: t = G^T r' from the SELL-32 copy,
+// one row per thread in add.at order, 8 products in flight per thread, no row tile (so 4 CTAs
+// fit an SM; the generic k_iter2 holds 96 registers).  Same rows, roundings and per-thread
+// partials as k_iter2<.., SPLIT>: bit-identical.
+__global__ void __launch_bounds__(PR, 4) k_iter2_sell(Dev D, int par) {
+  __shared__ double red[PR / 32];
+  __shared__ int flag;
+  int sys; long long r0, r1;
+  block_rows(D, sys, r0, r1);
+  if (D.st[sys].status != ST_RUN) return;
+  const double* __restrict__ rn = par ? D.r0 : D.r1;
+  double prr = 0.0;
+  const long long i = r0 + threadIdx.x;
+  if (i < r1) {
+    const double rni = rn[i];
+    prr = mul(rni, rni);
+    const long long b = D.sgt.sbase[i >> 5] + (i & 31);
+    const int len = D.sgt.offs[i + 1] - D.sgt.offs[i];
+    const double* __restrict__ sv = D.sgt.vals + b;
+    const int32_t* __restrict__ sc = D.sgt.cols + b;
+    double s = 0.0;
+    int k = 0;
+    for (; k + 8 <= len; k += 8) {
+      int c[8];
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) c[u] = __ldg(sc + 32 * (k + u));
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = mul(__ldg(sv + 32 * (k + u)), __ldg(rn + c[u]));
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s = add(s, v[u]);
+    }
+    for (; k < len; ++k) s = add(s, mul(__ldg(sv + 32 * k), __ldg(rn + __ldg(sc + 32 * k))));
+    D.t[i] = s;
+  }
+  if (arrive(D, sys, prr, 0.0, red, &flag)) {
+    const double rr = gather_partials(D, sys, 0, red);
+    if (threadIdx.x == 0) fin_rr(D, sys, rr);
+  }
+}
+
 // K3 for long CSR rows of G (C4: ~420 per row on the A^2 pattern): one warp per row in numpy's
 // exact pairwise order (warp_row_numpy), coalesced instead of one thread walking each row.  The
 // CTA keeps k_iter3's rows and its per-thread r.s partials (one row per thread slot), so the
@@ -1864,7 +1905,9 @@ int launch_iteration(sg_pcg* h, cudaStream_t s, int par, bool refresh, cudaEvent
     }
     if (!refresh && FMT == 0 && !SH) {
       k_pre_r<<<g, PR, 0, s>>>(h->D, par); ++k;
-      k_iter2<PRE, FMT, ND, SH, true><<<g, PR, 0, s>>>(h->D, par); ++k;
+      if (PRE == SG_PRECOND_LEARNED && h->D.sell_on && h->g_warp) k_iter2_sell<<<g, PR, 0, s>>>(h->D, par);
+      else k_iter2<PRE, FMT, ND, SH, true><<<g, PR, 0, s>>>(h->D, par);
+      ++k;
     } else if (!refresh) {
       k_iter2<PRE, FMT, ND, SH><<<g, PR, 0, s>>>(h->D, par); ++k;
     } else {
