@@ -107,24 +107,46 @@ __global__ void k_row_expand(int64_t n_rows, const int32_t* __restrict__ offs, i
     for (int32_t k = offs[i]; k < offs[i + 1]; ++k) rows[k] = (int32_t)i;
 }
 
+static inline int grid_for(int64_t n, int threads = 256) {
+  int64_t g = ceil_div(n > 0 ? n : 1, threads);
+  return (int)(g > 148 * 32 ? 148 * 32 : g);
+}
+
 // For entry k = (i, j): position of (j, i) by binary search in row j, or -1 if absent.
+// LPR lanes share a row and search its entries in parallel (4 for stencil rows, a warp for the
+// ~420-entry rows of an A^2 pattern), so a long row is not one thread's chain of dependent
+// searches.
+template <int LPR>
 __global__ void k_partner(int64_t n, const int32_t* __restrict__ offs,
                           const int32_t* __restrict__ cols, int32_t* partner,
                           unsigned int* missing) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    for (int32_t k = offs[i]; k < offs[i + 1]; ++k) {
-      int32_t j = cols[k];
+  const int sub = threadIdx.x % LPR;
+  const int64_t stride = (int64_t)gridDim.x * (blockDim.x / LPR);
+  bool miss = false;
+  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / LPR; i < n; i += stride) {
+    const int32_t e1 = offs[i + 1];
+    for (int32_t k = offs[i] + sub; k < e1; k += LPR) {
+      const int32_t j = cols[k];
       int32_t lo = offs[j], hi = offs[j + 1];
+      const int32_t end = hi;
       while (lo < hi) {
-        int32_t mid = (lo + hi) >> 1;
+        const int32_t mid = (lo + hi) >> 1;
         if (cols[mid] < (int32_t)i) lo = mid + 1; else hi = mid;
       }
-      bool found = lo < offs[j + 1] && cols[lo] == (int32_t)i;
+      const bool found = lo < end && cols[lo] == (int32_t)i;
       partner[k] = found ? lo : -1;
-      if (!found) atomicOr(missing, 1u);
+      miss |= !found;
     }
   }
+  if (miss) atomicOr(missing, 1u);
+}
+
+int launch_partner(int64_t n, int64_t nnz, const int32_t* offs, const int32_t* cols, int32_t* partner,
+                   unsigned int* missing, cudaStream_t s) {
+  if (nnz >= 16 * n) k_partner<32><<<grid_for(32 * n), 256, 0, s>>>(n, offs, cols, partner, missing);
+  else k_partner<4><<<grid_for(4 * n), 256, 0, s>>>(n, offs, cols, partner, missing);
+  SG_LAUNCH_CHECK("k_partner");
+  return SG_OK;
 }
 
 __global__ void k_transpose_keys(int64_t n_rows, int64_t n_cols, const int32_t* __restrict__ offs,
@@ -268,11 +290,6 @@ __global__ void k_scan_counts(const int32_t* __restrict__ counts, int64_t n, int
   __syncthreads();
   long long acc = part[threadIdx.x];
   for (int64_t i = lo; i < hi; ++i) { offs[i] = (int32_t)acc; acc += counts[i]; }
-}
-
-static inline int grid_for(int64_t n, int threads = 256) {
-  int64_t g = ceil_div(n > 0 ? n : 1, threads);
-  return (int)(g > 148 * 32 ? 148 * 32 : g);
 }
 
 static int bits_for(uint64_t maxkey) {
@@ -492,8 +509,8 @@ extern "C" int sg_pattern_is_symmetric(int64_t n, int64_t nnz, const int32_t* of
   cudaStream_t s = as_stream(stream);
   SG_CUDA(cudaMemsetAsync(missing, 0, sizeof(unsigned int), s));
   if (n > 0) {
-    k_partner<<<grid_for(n), 256, 0, s>>>(n, offs, cols, partner, missing);
-    SG_LAUNCH_CHECK("k_partner");
+    const int rc = launch_partner(n, nnz, offs, cols, partner, missing, s);
+    if (rc) return rc;
   }
   unsigned int h = 0;
   SG_CUDA(cudaMemcpyAsync(&h, missing, sizeof(h), cudaMemcpyDeviceToHost, s));
@@ -522,8 +539,8 @@ extern "C" int sg_csr_transpose(int64_t n_rows, int64_t n_cols, int64_t nnz, con
   // Fast path: square symmetric pattern => pattern(A^T) == pattern(A), perm = partner map.
   if (n_rows == n_cols && n_rows > 0) {
     SG_CUDA(cudaMemsetAsync(missing, 0, sizeof(unsigned int), s));
-    k_partner<<<grid_for(n_rows), 256, 0, s>>>(n_rows, offs, cols, perm, missing);
-    SG_LAUNCH_CHECK("k_partner");
+    const int rc = launch_partner(n_rows, nnz, offs, cols, perm, missing, s);
+    if (rc) return rc;
     unsigned int h = 1;
     SG_CUDA(cudaMemcpyAsync(&h, missing, sizeof(h), cudaMemcpyDeviceToHost, s));
     SG_CUDA(cudaStreamSynchronize(s));
