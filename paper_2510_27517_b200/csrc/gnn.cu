@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(128) k_node_layer(GnnP p, int t, int64_t n, co
     // neighbours in batches of NBAT: all their index / edge-feature loads, then all their Q rows,
     // are in flight together (same summation order as one at a time)
 #ifndef SG_NODE_NBAT
-#define SG_NODE_NBAT 4
+#define SG_NODE_NBAT 5
 #endif
     constexpr int NBAT = SG_NODE_NBAT;
     for (int32_t k0 = lo; k0 < hi; k0 += NBAT) {
