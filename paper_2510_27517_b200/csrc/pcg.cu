@@ -48,7 +48,10 @@ constexpr int kRpt = 4;    // DIA: rows per thread (tile = PR * kRpt rows; amort
                            // per-tile reduction and keeps more independent loads in flight)
 
 enum { ST_RUN = 0, ST_CERTIFY = 1, ST_DONE = 2 };
-enum { FL_FRESH = 1 };
+// FL_XPEND: x still lacks alpha d' of the last fused K2+K3 (deferred x update, d' in d0 if
+// FL_DPAR else d1); FL_XINT: the updated x lives in t (a fresh-residual K1 could not update x in
+// place while other CTAs read it).
+enum { FL_FRESH = 1, FL_XPEND = 2, FL_XINT = 4, FL_DPAR = 8 };
 
 struct SysState {
   double norm_b, delta, delta0, dq, alpha, beta, rr, rtol2d0;
@@ -97,6 +100,7 @@ struct Sell {
 };
 
 struct Dev {
+  int xdefer;       // sliding-window path: x += alpha d' deferred from K2+K3 to the next K1
   int sell_on;      // CSR path reads A, G^T (bit 1: also G) from their SELL-32 copies
   Sell sa, sg, sgt;
   // row-partitioned mode (one system over several ranks): the last CTA of a reducing kernel
@@ -712,7 +716,24 @@ __global__ void __launch_bounds__(PR) k_refresh_x(Dev D, int par) {
   if (D.st[sys].status != ST_RUN) return;
   const double alpha = D.st[sys].alpha;
   const double* dn = par ? D.d0 : D.d1;
-  for (long long i = r0 + threadIdx.x; i < r1; i += PR) D.x[i] = add(D.x[i], mul(alpha, dn[i]));
+  const double* xs = (D.st[sys].flags & FL_XINT) ? D.t : D.x;  // x parked in t by a fresh K1
+  for (long long i = r0 + threadIdx.x; i < r1; i += PR) D.x[i] = add(xs[i], mul(alpha, dn[i]));
+}
+
+// End of a solve with deferred x updates: complete x for systems that stopped with one pending
+// (x in t and / or alpha d' not yet added).  Same operations as the deferred kernels would do.
+__global__ void __launch_bounds__(PR) k_xflush(Dev D) {
+  int sys; long long r0, r1;
+  block_rows(D, sys, r0, r1);
+  const int fl = D.st[sys].flags;
+  if (!(fl & (FL_XPEND | FL_XINT))) return;
+  const double alpha = D.st[sys].alpha;
+  const double* dd = (fl & FL_DPAR) ? D.d0 : D.d1;
+  for (long long i = r0 + threadIdx.x; i < r1; i += PR) {
+    double v = (fl & FL_XINT) ? D.t[i] : D.x[i];
+    if (fl & FL_XPEND) v = add(v, mul(alpha, dd[i]));
+    D.x[i] = v;
+  }
 }
 
 template <int FMT, int ND, bool SH>
@@ -770,7 +791,14 @@ __global__ void __launch_bounds__(PR, FMT >= 1 ? 8 : 1) k_iter3(Dev D, int par, 
   }
   if (arrive(D, sys, prs, 0.0, red, &flag)) {
     const double rs = gather_partials(D, sys, 0, red);
-    if (threadIdx.x == 0) { if (D.dist) publish(D, sys, rs, 0.0); else fin_k3(D, sys, rs, refreshed); }
+    if (threadIdx.x == 0) {
+      if (D.dist) {
+        publish(D, sys, rs, 0.0);
+      } else {
+        D.st[sys].flags &= ~(FL_XPEND | FL_XINT | FL_DPAR);  // refresh path: x complete (k_refresh_x)
+        fin_k3(D, sys, rs, refreshed);
+      }
+    }
   }
 }
 
@@ -1138,6 +1166,10 @@ __global__ void __launch_bounds__(PR, 1) k_iter23_sw(Dev D, int par) {
   const long long R1 = R0 + D.rng_len < s1 ? R0 + D.rng_len : s1;
   const double alpha = D.st[sys].alpha;
   const double eps = D.ctl->eps;
+  // xdefer: x += alpha d' is left to the next K1 (which streams d anyway); only an x parked in t
+  // by a fresh-residual K1 is moved back here
+  const bool xd = D.xdefer != 0;
+  const bool xint = xd && (D.st[sys].flags & FL_XINT) != 0;
   const double* dn = par ? D.d0 : D.d1;
   const double* rc = par ? D.r1 : D.r0;
   double* rn = par ? D.r0 : D.r1;
@@ -1180,9 +1212,11 @@ __global__ void __launch_bounds__(PR, 1) k_iter23_sw(Dev D, int par) {
     const int li = mm * C + tid;
     const bool own_c = mm >= 2 * NH && li >= R0r && li < R1r;
     double xo = 0.0, dd = 0.0;
-    if (own_c) {
+    if (own_c && !xd) {
       xo = D.x[LB + li];
       dd = __ldg(dn + LB + li);
+    } else if (own_c && xint) {
+      xo = D.t[LB + li];
     }
     mbar_wait(&bars[k % P], (uint32_t)((k / P) & 1));
     {  // A: r' of the lead chunk, in place over its r
@@ -1213,7 +1247,8 @@ __global__ void __launch_bounds__(PR, 1) k_iter23_sw(Dev D, int par) {
     __syncthreads();
     if (own_c) {  // C: s and x of chunk mm
       const long long i = LB + li;
-      D.x[i] = add(xo, mul(alpha, dd));
+      if (!xd) D.x[i] = add(xo, mul(alpha, dd));
+      else if (xint) D.x[i] = xo;
       const int io = (mm % NG) * C + tid, tb = (mm % NT) * C + tid;
       const unsigned int m = mk[io];
       double p[ND];
@@ -1231,6 +1266,7 @@ __global__ void __launch_bounds__(PR, 1) k_iter23_sw(Dev D, int par) {
     const double rs = gather_partials(D, D.sys_rng0, sys, 1, red);
     if (threadIdx.x == 0) {
       D.st[sys].rr = rr;
+      if (xd) D.st[sys].flags = (D.st[sys].flags & ~(FL_XINT | FL_DPAR)) | FL_XPEND | (par ? FL_DPAR : 0);
       fin_k3(D, sys, rs, 0);
     }
   }
@@ -1273,7 +1309,13 @@ __global__ void __launch_bounds__(PR, 5) k_iter1_sw(Dev D, int par) {
   const long long R0 = D.rng_r0[b];
   const long long R1 = R0 + D.rng_len < s1 ? R0 + D.rng_len : s1;
   const bool run = status == ST_RUN;
-  const bool fresh = run ? (D.st[sys].flags & FL_FRESH) != 0 : true;
+  const int flags = D.st[sys].flags;
+  const bool fresh = run ? (flags & FL_FRESH) != 0 : true;
+  // deferred x update of the previous fused K2+K3: x += alpha_prev d (d = this kernel's d_old).
+  // In place while streaming; when a fresh residual is due, other CTAs read neighbours' x in this
+  // kernel, so the updated x goes to t instead and b - A x reads x + alpha d on the fly.
+  const bool pend = D.xdefer && (flags & FL_XPEND) != 0;
+  const double alpha_p = D.st[sys].alpha;
   const double beta = D.st[sys].beta;
   const double* dc = par ? D.d1 : D.d0;
   double* dn = par ? D.d0 : D.d1;
@@ -1311,14 +1353,21 @@ __global__ void __launch_bounds__(PR, 5) k_iter1_sw(Dev D, int par) {
     __syncthreads();
     if (tid == 0)
       for (int k = 0; k < P - 1 && k < K; ++k) issue(k);
+    const bool xupd = pend && !fresh;
+    double xo_n = 0.0;  // x of the lead chunk's own rows, loaded one step ahead
+    if (xupd && tid >= R0r && tid < R1r) xo_n = D.x[LB + tid];
     for (int k = 0; k < K; ++k) {
       const double* st = stg + (k % P) * 2 * C;
+      const int lj = k * C + tid;
+      const bool xown = xupd && lj >= R0r && lj < R1r;
+      const double xo = xo_n;
+      if (xupd && lj + C >= R0r && lj + C < R1r) xo_n = D.x[LB + lj + C];
       mbar_wait(&bars[k % P], (uint32_t)((k / P) & 1));
-      {  // d' of the lead chunk
-        const int lj = k * C + tid;
+      {  // d' of the lead chunk (and the deferred x update of its own rows)
         double v = add(st[tid], mul(beta, st[C + tid]));
         v = (lj >= s0r && lj < s1r) ? v : 0.0;
         if (lj >= R0r && lj < R1r) dn[LB + lj] = v;
+        if (xown) D.x[LB + lj] = add(xo, mul(alpha_p, st[C + tid]));
         dp[lj & DM] = v;
       }
       __syncthreads();
@@ -1347,8 +1396,16 @@ __global__ void __launch_bounds__(PR, 5) k_iter1_sw(Dev D, int par) {
   if (fresh) {  // r_fresh = b - A x over the range's own rows (direct loads)
     for (long long i = R0 + tid; i < R1; i += PR) {
       const unsigned int m = D.dia.mask[i];
-      const double ax = FMT == 2 ? dia_row_numpy_sym<ND, 0>(D.dia, D.dia.av, (int)i, m, XF{D.x, nullptr, 0.0})
-                                 : dia_row_numpy<ND, 0>(D.dia, D.dia.av, (int)i, m, XF{D.x, nullptr, 0.0});
+      double ax;
+      if (pend) {  // x + alpha_prev d, exactly the deferred update; the updated x goes to t
+        const XF xf{D.x, dc, alpha_p};
+        ax = FMT == 2 ? dia_row_numpy_sym<ND, 1>(D.dia, D.dia.av, (int)i, m, xf)
+                      : dia_row_numpy<ND, 1>(D.dia, D.dia.av, (int)i, m, xf);
+        D.t[i] = add(D.x[i], mul(alpha_p, dc[i]));
+      } else {
+        ax = FMT == 2 ? dia_row_numpy_sym<ND, 0>(D.dia, D.dia.av, (int)i, m, XF{D.x, nullptr, 0.0})
+                      : dia_row_numpy<ND, 0>(D.dia, D.dia.av, (int)i, m, XF{D.x, nullptr, 0.0});
+      }
       const double rf = sub(D.b[i], ax);
       if (run) rc[i] = rf;
       prr += mul(rf, rf);
@@ -1357,7 +1414,10 @@ __global__ void __launch_bounds__(PR, 5) k_iter1_sw(Dev D, int par) {
   if (arrive(D, D.sys_rng0, sys, pdq, prr, red, &flag)) {
     const double dq = gather_partials(D, D.sys_rng0, sys, 0, red);
     const double rrf = gather_partials(D, D.sys_rng0, sys, 1, red);
-    if (threadIdx.x == 0) fin_k1(D, sys, run, dq, rrf);
+    if (threadIdx.x == 0) {
+      if (pend) D.st[sys].flags = (D.st[sys].flags & ~(FL_XPEND | FL_DPAR)) | (fresh ? FL_XINT : 0);
+      fin_k1(D, sys, run, dq, rrf);
+    }
   }
 }
 
@@ -2337,6 +2397,7 @@ extern "C" int sg_pcg_create(sg_pcg** out, int32_t n_systems, const int64_t* sys
   D.q = vec[6]; D.s = vec[7]; D.t = vec[8];
   D.part = part; D.counter = counter; D.st = h->st; D.ctl = h->ctl;
   D.sell_on = 0;
+  D.xdefer = 0;
   if (!h->dia_nd && !h->short_rows) {  // long CSR rows: SELL-32 copies (coalesced row walks)
     int32_t nz = 0;
     SG_CUDA(cudaMemcpyAsync(&nz, a_offs + n, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
@@ -2364,6 +2425,10 @@ extern "C" int sg_pcg_create(sg_pcg** out, int32_t n_systems, const int64_t* sys
     h->k23 = (kv && kv[0] == 't') || !full ? 0 : 1;
     const char* k1v = getenv("SG_PCG_K1");
     h->k1sw = (k1v && k1v[0] == 't') || !(h->dia_nd == 5 || h->dia_nd == 7) ? 0 : 1;
+    // deferred x update: both sliding-window kernels, learned factor, one rank
+    const char* xv = getenv("SG_PCG_XDEFER");
+    h->D.xdefer = (xv && xv[0] == '1') && h->k1sw && h->k23 == 1 && !h->strip &&
+                  h->pre == SG_PRECOND_LEARNED ? 1 : 0;
   }
   SG_CUDA(cudaStreamSynchronize(s));
   *out = h;
@@ -2500,6 +2565,11 @@ extern "C" int sg_pcg_solve(sg_pcg* h, const double* b, double* x, const sg_solv
     h->kernels += h->graph_kernels[pattern];
     h->chunks += 1;
     it += chunk;
+  }
+  if (h->D.xdefer && h->nblk > 0) {
+    k_xflush<<<(unsigned)h->nblk, PR, 0, s>>>(h->D);
+    SG_LAUNCH_CHECK("k_xflush");
+    h->kernels += 1;
   }
   if (h->n > 0) SG_CUDA(cudaMemcpyAsync(x, h->D.x, h->n * sizeof(double), cudaMemcpyDeviceToDevice, s));
   SG_CUDA(cudaEventRecord(e1, s));
@@ -2678,6 +2748,7 @@ extern "C" int sg_pcg_set_comm(sg_pcg* h, void* comm, int32_t left, int32_t righ
   h->ghost_hi = right >= 0 ? ghost_hi : 0;
   h->D.dist = h->dist;
   h->D.gsum = h->gsum;
+  if (h->dist) h->D.xdefer = 0;  // the row partition runs the unfused kernels
   for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);
   h->graphs.clear();
   h->graph_kernels.clear();

@@ -588,6 +588,57 @@ def test_pcg_control_flow_on_sliding_window_kernels():
             assert rep.k == 0 and np.all(rep.x == 0.0)
 
 
+def _fresh_handles():
+    import paper_2510_27517_b200.pcg as PC
+    for h in (PC._HANDLES or {}).values():
+        h.close()
+    PC._HANDLES = None
+
+
+def test_deferred_x_update_bit_identical(monkeypatch):
+    """x += alpha d' moved from the fused K2+K3 to the next K1 (SG_PCG_XDEFER=1) gives the same
+    x, k and residual history bit for bit, across the control-flow variants (refresh periods,
+    fresh-residual checks, delta termination + certification, max_iters stops with an update
+    pending, zero rhs) and a batch whose systems stop at different iterations."""
+    import os
+    from paper_2510_27517_b200.batch import BatchSolver, SystemBatch
+    m = P.load_checkpoint(os.path.join(os.path.dirname(__file__), "golden", "trained_heat16.spaignn"))
+    A, meta = P.gen_poisson2d(24, 24, coeff_seed=4)
+    G = P.forward(m, P.build_graph(A, meta)).G
+    b = P.gen_rhs(meta, 99)
+    cfgs = [P.SolveConfig(rtol=1e-8), P.SolveConfig(rtol=1e-9, residual_refresh_period=3),
+            P.SolveConfig(rtol=1e-10, residual_refresh_period=7),
+            P.SolveConfig(rtol=1e-9, termination="delta"), P.SolveConfig(rtol=1e-12, max_iters=5),
+            P.SolveConfig(rtol=1e-12, max_iters=12, residual_refresh_period=4)]
+    for cfg in cfgs:
+        out = []
+        for flag in ("1", "0"):
+            monkeypatch.setenv("SG_PCG_XDEFER", flag)
+            _fresh_handles()
+            out.append([P.pcg_solve(A, bb, P.build_learned_spai(G, m.config.epsilon), cfg)
+                        for bb in (b, np.zeros_like(b))])
+        for r1, r0 in zip(*out):
+            assert r1.k == r0.k and r1.converged == r0.converged, cfg
+            assert np.array_equal(r1.x, r0.x), cfg
+            assert np.array_equal(np.asarray(r1.residual_history), np.asarray(r0.residual_history)), cfg
+    # batch: systems converge at different iterations, so some stop with an update pending while
+    # the others keep flipping the d buffers
+    seeds = list(range(6))
+    cfg = P.SolveConfig(rtol=1e-9, residual_refresh_period=9)
+    res = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("SG_PCG_XDEFER", flag)
+        sv = BatchSolver(SystemBatch.heat2d(40, 40, seeds, [s + 7 for s in seeds]), m)
+        sv.step(cfg)
+        rs = sv.solve(cfg)
+        res.append(([r.k for r in rs], sv.x.cpu().numpy().copy(), [sv.handle.history(k, int(r.hist_len))
+                                                                  for k, r in enumerate(rs)]))
+    assert res[0][0] == res[1][0] and len(set(res[0][0])) > 1
+    assert np.array_equal(res[0][1], res[1][1])
+    for h1, h0 in zip(res[0][2], res[1][2]):
+        assert np.array_equal(np.asarray(h1), np.asarray(h0))
+
+
 # --------------------------------------------------------------------------- training (§8(f) #1)
 def _train_items():
     items = []
