@@ -877,6 +877,106 @@ __global__ void __launch_bounds__(PR) k_iter3_wr(Dev D, int par, int refreshed) 
   }
 }
 
+// ------------------------------------------------------------------ small systems: one CTA per system
+// For stencil (DIA) systems of <= kSmallRows rows the multi-kernel iteration is launch- and
+// latency-bound (~18-19 us per iteration from 256 to 8100 rows).  Measured per iteration, one
+// CTA / multi-kernel: 256 rows 8.0 / 18.0 us, 1024 rows 9.4 / 19.4, 2304 rows 13.0 / 18.2,
+// 4096 rows 19.0 / 18.9, 8100 rows 31.5 / 19.2 (profiles/small_probe.py).  One 1024-thread CTA runs whole
+// iterations of ONE system with CTA barriers between the phases instead of kernel boundaries:
+// the same phases, roundings, summation orders and finalisers as k_iter1/2/3 + k_refresh_*
+// (dot products: per-thread partials in row order, then the block tree).  `iters` iterations per
+// launch (the host polls the active count between launches, as between graph chunks).
+constexpr int kSmallRows = 3072;
+constexpr int kSmallThreads = 1024;
+
+template <int PRE, int FMT, int ND>
+__global__ void __launch_bounds__(kSmallThreads, 1) k_pcg_small(Dev D, int iters, long long period) {
+  __shared__ double red[32];
+  const int sys = blockIdx.x, tid = threadIdx.x;
+  const long long s0 = D.blk_r0[D.sys_blk0[sys]], s1 = D.sys_r1[sys];
+  const double eps = D.ctl->eps;
+  double* x = D.x;
+  double* r = D.r0;
+  double* d = D.d0;
+  auto rowA = [&](long long i, const XF& f) {
+    const unsigned int m = D.dia.mask[i];
+    return FMT == 2 ? dia_row_numpy_sym<ND, 0>(D.dia, D.dia.av, (int)i, m, f)
+                    : dia_row_numpy<ND, 0>(D.dia, D.dia.av, (int)i, m, f);
+  };
+  for (int c = 0; c < iters; ++c) {
+    SysState& S = D.st[sys];
+    const int status = S.status;
+    if (status == ST_DONE) break;
+    const bool run = status == ST_RUN;
+    const bool fresh = run ? (S.flags & FL_FRESH) != 0 : true;
+    const bool refresh = run && S.i > 0 && S.i % period == 0;
+    const double beta = S.beta;
+    // K1: d = s + beta d; q = A d, d.q; fresh residual b - A x (pcg.py:176-184, 208-215)
+    double pdq = 0.0, prr = 0.0;
+    if (run) {
+      for (long long i = s0 + tid; i < s1; i += kSmallThreads) d[i] = add(D.s[i], mul(beta, d[i]));
+      __syncthreads();
+      for (long long i = s0 + tid; i < s1; i += kSmallThreads) {
+        const double qi = rowA(i, XF{d, nullptr, 0.0});
+        D.q[i] = qi;
+        pdq += mul(d[i], qi);
+      }
+    }
+    if (fresh) {
+      for (long long i = s0 + tid; i < s1; i += kSmallThreads) {
+        const double rf = sub(D.b[i], rowA(i, XF{x, nullptr, 0.0}));
+        if (run) r[i] = rf;
+        prr += mul(rf, rf);
+      }
+    }
+    const double dq = block_sum(pdq, red);
+    const double rrf = block_sum(prr, red);
+    if (tid == 0) fin_k1(D, sys, run, dq, rrf);
+    __syncthreads();
+    if (S.status != ST_RUN) continue;
+    const double alpha = S.alpha;
+    // K2: x += alpha d; r -= alpha q (or, on refresh iterations, r = b - A x); ||r||^2
+    double prn = 0.0;
+    for (long long i = s0 + tid; i < s1; i += kSmallThreads) x[i] = add(x[i], mul(alpha, d[i]));
+    if (refresh) {
+      __syncthreads();
+      for (long long i = s0 + tid; i < s1; i += kSmallThreads) {
+        const double rn = sub(D.b[i], rowA(i, XF{x, nullptr, 0.0}));
+        r[i] = rn;
+        prn += mul(rn, rn);
+      }
+    } else {
+      for (long long i = s0 + tid; i < s1; i += kSmallThreads) {
+        const double rn = sub(r[i], mul(alpha, D.q[i]));
+        r[i] = rn;
+        prn += mul(rn, rn);
+      }
+    }
+    const double rr = block_sum(prn, red);
+    if (tid == 0) fin_rr(D, sys, rr);
+    __syncthreads();
+    // K3: s = M r (learned: t = G^T r, then s = G t + eps r); r.s
+    if (PRE == SG_PRECOND_LEARNED) {
+      for (long long i = s0 + tid; i < s1; i += kSmallThreads)
+        D.t[i] = dia_row_t_seq<ND, 0>(D.dia, D.dia.gv, (int)i, D.dia.mask[i], XF{r, nullptr, 0.0});
+      __syncthreads();
+    }
+    double prs = 0.0;
+    for (long long i = s0 + tid; i < s1; i += kSmallThreads) {
+      double si;
+      if (PRE == SG_PRECOND_IDENTITY) si = r[i];
+      else if (PRE == SG_PRECOND_JACOBI) si = mul(r[i], D.inv_diag[i]);
+      else si = add(dia_row_numpy<ND, 0>(D.dia, D.dia.gv, (int)i, D.dia.mask[i], XF{D.t, nullptr, 0.0}),
+                    mul(eps, r[i]));
+      D.s[i] = si;
+      prs += mul(r[i], si);
+    }
+    const double rs = block_sum(prs, red);
+    if (tid == 0) fin_k3(D, sys, rs, refresh ? 1 : 0);
+    __syncthreads();
+  }
+}
+
 // Row-partitioned mode: the finalisers on the all-reduced sums (one thread per system; systems
 // the reducing kernel skipped are skipped here too, exactly as the kernel's own early return).
 enum { FIN_SETUP1 = 0, FIN_SETUP2 = 1, FIN_K1 = 2, FIN_RR = 3, FIN_K3 = 4 };
@@ -1737,6 +1837,7 @@ struct sg_pcg {
   int strip = 0;      // wide 5-point grid: 2-D strip sliding-window kernels (k_iter1_s5, k_iter23_s5)
   int k1sw = 1;       // K1 variant: 1 = sliding window (k_iter1_sw), 0 = tiles (k_iter1_st)
   int g_warp = 0;     // CSR G with long rows: K3 one warp per row (k_iter3_wr)
+  int small = 0;      // DIA systems of <= kSmallRows rows: one CTA per system (k_pcg_small)
   int k23 = 1;        // fused K2+K3 variant: 1 = sliding window (k_iter23_sw), 0 = tiles (k_iter23_st)
   void* sell_mem[3] = {nullptr, nullptr, nullptr};   // SELL-32 patterns of A, G, G^T
   void* sell_vals[3] = {nullptr, nullptr, nullptr};
@@ -2426,6 +2527,10 @@ extern "C" int sg_pcg_create(sg_pcg** out, int32_t n_systems, const int64_t* sys
     const char* k1v = getenv("SG_PCG_K1");
     h->k1sw = (k1v && k1v[0] == 't') || !(h->dia_nd == 5 || h->dia_nd == 7) ? 0 : 1;
     // deferred x update: both sliding-window kernels, learned factor, one rank
+    const char* sv2 = getenv("SG_PCG_SMALL");
+    long long maxrows = 0;
+    for (int k = 0; k < n_systems; ++k) maxrows = std::max<long long>(maxrows, h->sys_start[k + 1] - h->sys_start[k]);
+    h->small = !(sv2 && sv2[0] == '0') && maxrows <= kSmallRows ? 1 : 0;
     const char* xv = getenv("SG_PCG_XDEFER");
     h->D.xdefer = (xv && xv[0] == '1') && h->k1sw && h->k23 == 1 && !h->strip &&
                   h->pre == SG_PRECOND_LEARNED ? 1 : 0;
@@ -2555,6 +2660,23 @@ extern "C" int sg_pcg_solve(sg_pcg* h, const double* b, double* x, const sg_solv
     if (cfg->track_history) {
       rc = ensure_hist(h, it + chunk + 2, s);
       if (rc) return rc;
+    }
+    if (h->small) {  // one CTA per system runs `chunk` whole iterations
+      rc = dispatch(h, [&](auto P, auto Fc, auto Nc, auto) -> int {
+        constexpr int PRE = decltype(P)::value;
+        constexpr int FMT = decltype(Fc)::value;
+        constexpr int ND = decltype(Nc)::value;
+        if constexpr (FMT >= 1) {
+          k_pcg_small<PRE, FMT, ND><<<(unsigned)h->S, kSmallThreads, 0, s>>>(h->D, chunk, period);
+          SG_LAUNCH_CHECK("k_pcg_small");
+        }
+        return SG_OK;
+      });
+      if (rc) return rc;
+      h->kernels += 1;
+      h->chunks += 1;
+      it += chunk;
+      continue;
     }
     std::vector<int> pattern(chunk);
     for (int c = 0; c < chunk; ++c) pattern[c] = (it + c) > 0 && (it + c) % period == 0;
@@ -2748,7 +2870,7 @@ extern "C" int sg_pcg_set_comm(sg_pcg* h, void* comm, int32_t left, int32_t righ
   h->ghost_hi = right >= 0 ? ghost_hi : 0;
   h->D.dist = h->dist;
   h->D.gsum = h->gsum;
-  if (h->dist) h->D.xdefer = 0;  // the row partition runs the unfused kernels
+  if (h->dist) h->D.xdefer = 0, h->small = 0;  // the row partition runs the unfused kernels
   for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);
   h->graphs.clear();
   h->graph_kernels.clear();

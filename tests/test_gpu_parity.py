@@ -31,6 +31,21 @@ def csr(g, p):
                           g[p + "_vals"])
 
 
+@pytest.fixture
+def multi_kernel(monkeypatch):
+    """Route DIA systems of <= 3072 rows through the multi-kernel sliding-window / tile path
+    instead of the one-CTA-per-system solver (tests that target those kernels on small grids)."""
+    monkeypatch.setenv("SG_PCG_SMALL", "0")
+    import paper_2510_27517_b200.pcg as PC
+    for h in (PC._HANDLES or {}).values():
+        h.close()
+    PC._HANDLES = None
+    yield
+    for h in (PC._HANDLES or {}).values():
+        h.close()
+    PC._HANDLES = None
+
+
 def test_library_loaded_from_tree():
     lib = _lib.lib()
     assert lib.sg_abi_version() == 1
@@ -504,7 +519,7 @@ def test_pcg_wide_grid_strip_kernels():
         assert res <= 1e-8 * 1.01, (nx, res)
 
 
-def test_pcg_3d_small_sliding_window():
+def test_pcg_3d_small_sliding_window(multi_kernel):
     """7-point 3-D grid with a small halo (8x8x6: offsets +-1, +-8, +-64) runs the 1-D
     sliding-window kernels with ND = 7 (A by its lower half); k and x against the oracle."""
     A, meta = P.gen_poisson3d(8, 8, 6)
@@ -523,7 +538,7 @@ def test_pcg_3d_small_sliding_window():
     assert np.linalg.norm(b - O.spmv(o, c, v, rep.x)) / np.linalg.norm(b) <= 1.01e-8
 
 
-def test_batch_mixed_grids_unaligned_systems():
+def test_batch_mixed_grids_unaligned_systems(multi_kernel):
     """A batch of differently sized grids (system sizes not multiples of 16, so sliding-window
     ranges start unaligned; the union of diagonal offsets has 7 entries, each system using 5)."""
     import os
@@ -543,11 +558,18 @@ def test_batch_mixed_grids_unaligned_systems():
         assert np.linalg.norm(b - O.spmv(o, c, v, rb.x)) / np.linalg.norm(b) <= 1.01e-8
 
 
-def test_pcg_control_flow_on_sliding_window_kernels():
+@pytest.mark.parametrize("small", ["0", "1"])
+def test_pcg_control_flow_on_sliding_window_kernels(small, monkeypatch):
     """The reference control-flow variants (refresh period, delta termination + certification,
     max_iters, zero rhs, non-learned preconditioners) on a 5-point grid, i.e. through the
-    sliding-window K1 / fused K2+K3 kernels rather than the CSR ones the golden cases use."""
+    sliding-window K1 / fused K2+K3 kernels rather than the CSR ones the golden cases use
+    (small="1": the same cases through the one-CTA-per-system solver, k_pcg_small)."""
     import os
+    import paper_2510_27517_b200.pcg as PC
+    monkeypatch.setenv("SG_PCG_SMALL", small)
+    for h in (PC._HANDLES or {}).values():
+        h.close()
+    PC._HANDLES = None
     m = P.load_checkpoint(os.path.join(os.path.dirname(__file__), "golden", "trained_heat16.spaignn"))
     A, meta = P.gen_poisson2d(24, 24, coeff_seed=4)
     G = P.forward(m, P.build_graph(A, meta)).G
@@ -595,7 +617,7 @@ def _fresh_handles():
     PC._HANDLES = None
 
 
-def test_deferred_x_update_bit_identical(monkeypatch):
+def test_deferred_x_update_bit_identical(monkeypatch, multi_kernel):
     """x += alpha d' moved from the fused K2+K3 to the next K1 (SG_PCG_XDEFER=1) gives the same
     x, k and residual history bit for bit, across the control-flow variants (refresh periods,
     fresh-residual checks, delta termination + certification, max_iters stops with an update
@@ -744,7 +766,7 @@ def test_rowpart_device_single_rank():
     assert len(hist) == k + 1
 
 
-def test_sliding_window_two_chunk_halo():
+def test_sliding_window_two_chunk_halo(multi_kernel):
     """5-point grids with 256 < W <= 512 run the sliding-window kernels with a two-chunk halo
     (NH = 2: deeper rings, 4-chunk warm-up): k and residual against the oracle."""
     import os
