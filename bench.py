@@ -214,9 +214,10 @@ def run_ours(a, rank, world, local):
     peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
     # bytes the diagonal-major layout physically has to move per row (values incl. padding,
-    # 1-byte presence mask, vectors); A read by its lower half when bitwise symmetric
+    # 1-byte presence mask, vectors); A read by its lower half when bitwise symmetric, or as
+    # one coefficient per row when K1 regenerates it from gen_poisson2d's stencil (a_sym 2)
     nd, a_sym = int(prof[5]), int(prof[6])
-    n_low = (nd // 2 + 1) if a_sym else nd
+    n_low = 1 if a_sym == 2 else (nd // 2 + 1) if a_sym else nd
     phys = {}
     if nd:
         phys = {K1N: (8 * n_low + 1 + 32) * n1}

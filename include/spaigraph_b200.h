@@ -248,9 +248,18 @@ int sg_pcg_rebind_values(sg_pcg* h, const double* a_vals, const double* g_vals, 
  * prof_host[0..2] (ms), the summed active-system counts at those iterations prof_host[3], the
  * sample count prof_host[4], the storage format prof_host[5] (number of diagonals when the
  * diagonal-major DIA format is in use, 0 for CSR), plus the number of kernels and graphs
- * launched; prof_host[6] = 1 when A is read by its lower half (bitwise-symmetric A in DIA);
+ * launched; prof_host[6] = 1 when A is read by its lower half (bitwise-symmetric A in DIA), 2
+ * when K1 regenerates it from the coefficient stencil (sg_pcg_set_stencil);
  * prof_host[7] = 1 when K2 and K3 run fused (halo-staged DIA, learned preconditioner): then
  * prof_host[1] is the fused kernel and prof_host[2] is 0.  prof_host must hold 8 doubles. */
+/* Coefficient stencil (no reference counterpart; the matrix is gen_poisson2d's, datasets.py:
+ * 87-145): `coeff` (device, n doubles aligned with A's rows, every system an nx-by-ny grid;
+ * the caller keeps it alive and may refill it between solves) lets the streamed K1 regenerate
+ * A's entries bitwise from the node coefficients (8 instead of 24 B/row).  Every solve first
+ * verifies the stored A against the stencil bitwise and keeps the diagonals on any mismatch.
+ * coeff = NULL turns it off.  *usable_host = 1 when the handle's format can use it. */
+int sg_pcg_set_stencil(sg_pcg* h, const double* coeff, int64_t nx, int64_t ny, int32_t* usable_host);
+
 int sg_pcg_set_profile(sg_pcg* h, int32_t on);
 int sg_pcg_stats(sg_pcg* h, int64_t* kernels_host, int64_t* chunks_host, double* prof_host,
                  int32_t reset);

@@ -11,6 +11,7 @@ systems over ranks with no collective in the data path (see `shard_range`).
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import numpy as np
 
@@ -312,7 +313,19 @@ class BatchSolver:
             gt_dev = DeviceCsr(a.n_cols, a.n_rows, ot, ct, self.gt_vals)
             self.handle = PcgHandle(a, self.batch.row_start, L.PRECOND_LEARNED, g_dev, gt_dev, None,
                                     self.model.config.epsilon)
+        self._stencil()
         return self.handle.solve(self.batch.b, self.x, cfg)
+
+    def _stencil(self):
+        """gen_poisson2d batches (one grid shape, coefficients on device): with SG_PCG_STENCIL=1
+        K1 regenerates A from the coefficients (the solver verifies A bitwise at every solve).
+        Off by default: bit-identical but measured neutral at C2 (K1 is not bound by A's bytes)."""
+        bt = self.batch
+        grids = set(bt.grids or ())
+        if bt.coeff is None or len(grids) != 1 or os.environ.get("SG_PCG_STENCIL", "0") != "1":
+            return
+        nx, ny = grids.pop()
+        self.handle.set_stencil(bt.coeff, nx, ny)
 
     def step(self, cfg: SolveConfig):
         """One full pass of the hot path for every system: graph -> G -> G^T -> PCG."""

@@ -125,6 +125,10 @@ struct Dev {
   const int32_t *gt_offs, *gt_cols; const double* gt_vals;
   const double* inv_diag;
   Dia dia;
+  // coefficient stencil (sg_pcg_set_stencil): A regenerated from the node coefficients of
+  // gen_poisson2d inside the sliding-window K1 instead of streaming its diagonals
+  const double* coef;  // [n] with the diagonals' guard rows
+  double ihx2, ihy2;
   // vectors
   double *b, *x, *r0, *r1, *d0, *d1, *q, *s, *t;
   // reduction scratch
@@ -459,6 +463,39 @@ __global__ void k_dia_symcheck(Dia dia, unsigned int* asym) {
         const double lo = dia.av[dia.mir[d]][i + dia.off[d]];
         if (__double_as_longlong(up) != __double_as_longlong(lo)) { *asym = 1u; return; }
       }
+  }
+}
+
+// gen_poisson2d's entries of one row (datasets.py:110-137) from the node coefficients c0 (row),
+// cs / cw / ce / cn (rows i - W, i - 1, i + 1, i + W) and the row's presence mask (bits in the
+// ascending offset order {-W, -1, 0, 1, W}): faces are arithmetic means, a wall face keeps the
+// node's own value (a missing neighbour = a wall), off-diagonals are -face / h^2 and the
+// diagonal (w + e) / hx^2 + (s + n) / hy^2 -- numpy's roundings, no FMA, so bitwise its A.
+__device__ __forceinline__ void stencil5(double c0, double cs, double cw, double ce, double cn, unsigned int m,
+                                         double ihx2, double ihy2, double (&a)[5]) {
+  const double fs = (m & 1u) ? mul(0.5, add(c0, cs)) : c0;
+  const double fw = (m & 2u) ? mul(0.5, add(c0, cw)) : c0;
+  const double fe = (m & 8u) ? mul(0.5, add(c0, ce)) : c0;
+  const double fn = (m & 16u) ? mul(0.5, add(c0, cn)) : c0;
+  a[0] = -mul(fs, ihy2);
+  a[1] = -mul(fw, ihx2);
+  a[2] = add(mul(add(fw, fe), ihx2), mul(add(fs, fn), ihy2));
+  a[3] = -mul(fe, ihx2);
+  a[4] = -mul(fn, ihy2);
+}
+
+// Bitwise check that the stored 5-point DIA matrix is exactly gen_poisson2d's A of `coef`
+// (every stored entry of every row); any mismatch disables the coefficient stencil.
+__global__ void k_stencil_check(Dia dia, const double* __restrict__ coef, double ihx2, double ihy2,
+                                unsigned int* bad) {
+  const int W = dia.off[4];
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < dia.n; i += (long long)gridDim.x * blockDim.x) {
+    const unsigned int m = dia.mask[i];
+    double a[5];
+    stencil5(coef[i], coef[i - W], coef[i - 1], coef[i + 1], coef[i + W], m, ihx2, ihy2, a);
+#pragma unroll
+    for (int d = 0; d < 5; ++d)
+      if (((m >> d) & 1u) && __double_as_longlong(a[d]) != __double_as_longlong(dia.av[d][i])) { *bad = 1u; return; }
   }
 }
 
@@ -1379,12 +1416,20 @@ __global__ void __launch_bounds__(PR, 1) k_iter23_sw(Dev D, int par) {
 //   Q  q  = A d'                    chunk k - NH   (numpy order; partial d'.q)
 // One CTA barrier per step.  A pending fresh-residual check (rare: only after a candidate
 // convergence) runs after the stream over the range's own rows with direct loads.
-template <int FMT, int ND, int NH>
+// CS (coefficient stencil, 5-point gen_poisson2d matrices): the ring holds the node
+// coefficients instead of A's diagonals (8 instead of 24 B/row) and A's entries are recomputed
+// bitwise (stencil5); the +-W neighbours of chunk u reach back to chunk u - NH, so the ring
+// spans u - NH .. k + P - 1.
+#ifndef SG_SWP_CS
+#define SG_SWP_CS 6
+#endif
+template <int FMT, int ND, int NH, bool CS = false>
 struct Sw1 {
   static constexpr int C = kSwC;
-  static constexpr int P = 4;                              // chunks in flight (incl. the current one)
-  static constexpr int NA = FMT == 2 ? ND / 2 + 1 : ND;   // diagonals streamed
-  static constexpr int NR = P + NH;                        // A / mask ring chunks: u .. k + P - 1
+  // chunks in flight (incl. the current one); the coefficient ring's smaller footprint buys depth
+  static constexpr int P = CS ? SG_SWP_CS : 4;
+  static constexpr int NA = CS ? 1 : (FMT == 2 ? ND / 2 + 1 : ND);  // diagonals (or coefficients) streamed
+  static constexpr int NR = P + (CS ? 2 : 1) * NH;         // A / mask ring chunks: u (- NH) .. k + P - 1
   static constexpr int RING = NR * C;
   static constexpr int DRING = pow2ceil((2 * NH + 2) * C); // d' ring: chunks u - NH .. k + 1
   static constexpr int DM = DRING - 1;
@@ -1392,9 +1437,10 @@ struct Sw1 {
   static constexpr size_t SMEM = (size_t)NA * RING * 8 + (size_t)DRING * 8 + (size_t)P * 2 * C * 8 + RING;
 };
 
-template <int FMT, int ND, int NH>
+template <int FMT, int ND, int NH, bool CS = false>
 __global__ void __launch_bounds__(PR, 5) k_iter1_sw(Dev D, int par) {
-  using G = Sw1<FMT, ND, NH>;
+  static_assert(!CS || (FMT == 2 && ND == 5), "coefficient stencil: 5-point symmetric DIA only");
+  using G = Sw1<FMT, ND, NH, CS>;
   constexpr int C = G::C, P = G::P, NA = G::NA, NR = G::NR, RING = G::RING, DM = G::DM;
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ __align__(8) uint64_t bars[P];
@@ -1441,8 +1487,11 @@ __global__ void __launch_bounds__(PR, 5) k_iter1_sw(Dev D, int par) {
       mbar_arrive_expect_tx(&bars[ss], (uint32_t)((2 + NA) * C * 8 + C));
       bulk_g2s(st, D.s + row, C * 8, &bars[ss]);
       bulk_g2s(st + C, dc + row, C * 8, &bars[ss]);
+      if (CS) bulk_g2s(ar + gs, D.coef + row, C * 8, &bars[ss]);
+      else {
 #pragma unroll
-      for (int d = 0; d < NA; ++d) bulk_g2s(ar + d * RING + gs, D.dia.av[d] + row, C * 8, &bars[ss]);
+        for (int d = 0; d < NA; ++d) bulk_g2s(ar + d * RING + gs, D.dia.av[d] + row, C * 8, &bars[ss]);
+      }
       bulk_g2s(mk + gs, D.dia.mask + row, C, &bars[ss]);
     };
     if (tid == 0) {
@@ -1479,12 +1528,20 @@ __global__ void __launch_bounds__(PR, 5) k_iter1_sw(Dev D, int par) {
           const int io = (u % NR) * C + tid;
           const unsigned int m = mk[io];
           double p[ND];
+          if constexpr (CS) {
+            double a[5];
+            stencil5(ar[io], ar[ring_wrap(io + off[0], RING)], ar[ring_wrap(io - 1, RING)],
+                     ar[ring_wrap(io + 1, RING)], ar[ring_wrap(io + off[4], RING)], m, D.ihx2, D.ihy2, a);
 #pragma unroll
-          for (int d = 0; d < ND; ++d) {
-            const int ix = ring_wrap(io + off[d], RING);
-            // FMT 2: an upper entry (i, i+off) is the lower mirror entry at row i+off
-            const double a = (FMT == 2 && d > ND / 2) ? ar[(ND - 1 - d) * RING + ix] : ar[d * RING + io];
-            p[d] = mul(a, dp[(li + off[d]) & DM]);
+            for (int d = 0; d < ND; ++d) p[d] = mul(a[d], dp[(li + off[d]) & DM]);
+          } else {
+#pragma unroll
+            for (int d = 0; d < ND; ++d) {
+              const int ix = ring_wrap(io + off[d], RING);
+              // FMT 2: an upper entry (i, i+off) is the lower mirror entry at row i+off
+              const double a = (FMT == 2 && d > ND / 2) ? ar[(ND - 1 - d) * RING + ix] : ar[d * RING + io];
+              p[d] = mul(a, dp[(li + off[d]) & DM]);
+            }
           }
           const double qi = combine_numpy<ND>(p, m);
           D.q[LB + li] = qi;
@@ -1852,6 +1909,11 @@ struct sg_pcg {
   double* dia_g = nullptr;
   double* dia_a = nullptr;
   unsigned char* dia_mask = nullptr;
+  // coefficient stencil (sg_pcg_set_stencil): caller's coefficient array, the guarded copy the
+  // kernels read, and whether the last solve verified A against it (cst)
+  const double* coef_user = nullptr;
+  double* coef = nullptr;
+  int cst = 0;
   // instrumentation: kernel launches, and (when profiling) event nodes around the kernels of
   // one non-refresh iteration per chunk -> per-kernel device time sampled inside the solve
   int64_t kernels = 0, chunks = 0;
@@ -2034,7 +2096,10 @@ int launch_iteration(sg_pcg* h, cudaStream_t s, int par, bool refresh, cudaEvent
     const unsigned gr = (unsigned)h->nrng;
     const bool strip = FMT >= 1 && ND == 5 && h->strip;
     if (strip) k_iter1_s5<FS><<<gr, PR, Strip1<FS>::SMEM, s>>>(h->D, par);
-    else if (st && h->k1sw) {
+    else if (st && h->k1sw && FMT == 2 && ND == 5 && h->cst) {  // A from the coefficient stencil
+      if (H <= PR) k_iter1_sw<2, 5, 1, true><<<gr, PR, Sw1<2, 5, 1, true>::SMEM, s>>>(h->D, par);
+      else k_iter1_sw<2, 5, 2, true><<<gr, PR, Sw1<2, 5, 2, true>::SMEM, s>>>(h->D, par);
+    } else if (st && h->k1sw) {
       if (H <= PR) k_iter1_sw<FS, NS, 1><<<gr, PR, Sw1<FS, NS, 1>::SMEM, s>>>(h->D, par);
       else k_iter1_sw<FS, NS, 2><<<gr, PR, Sw1<FS, NS, 2>::SMEM, s>>>(h->D, par);
     } else if (st && H <= PR) k_iter1_st<FS, NS, 1><<<g, PR, (tile + 2 * H) * sizeof(double), s>>>(h->D, par);
@@ -2254,6 +2319,9 @@ int sw_attr(int* per_sm) {
                                (int)Sw1<1, ND, NH>::SMEM));
   SG_CUDA(cudaFuncSetAttribute(k_iter1_sw<2, ND, NH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)Sw1<2, ND, NH>::SMEM));
+  if constexpr (ND == 5)
+    SG_CUDA(cudaFuncSetAttribute(k_iter1_sw<2, 5, NH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)Sw1<2, 5, NH, true>::SMEM));
   SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_iter23_sw<ND, NH>, PR, Sw23<ND, NH>::SMEM));
   if (*per_sm < 1) *per_sm = 1;
   return SG_OK;
@@ -2566,20 +2634,28 @@ extern "C" int sg_pcg_solve(sg_pcg* h, const double* b, double* x, const sg_solv
     k_csr_to_dia<<<gb, 256, 0, s>>>(h->D.a_offs, h->D.a_cols, h->D.a_vals, h->n, h->D.dia, h->dia_a, h->dia_mask);
     if (h->pre == SG_PRECOND_LEARNED)
       k_csr_to_dia<<<gb, 256, 0, s>>>(h->D.g_offs, h->D.g_cols, h->D.g_vals, h->n, h->D.dia, h->dia_g, nullptr);
-    if (!h->d_flag) SG_CUDA(cudaMalloc(&h->d_flag, sizeof(unsigned int)));
-    SG_CUDA(cudaMemsetAsync(h->d_flag, 0, sizeof(unsigned int), s));
+    if (!h->d_flag) SG_CUDA(cudaMalloc(&h->d_flag, 2 * sizeof(unsigned int)));
+    SG_CUDA(cudaMemsetAsync(h->d_flag, 0, 2 * sizeof(unsigned int), s));
     k_dia_symcheck<<<gb, 256, 0, s>>>(h->D.dia, h->d_flag);
     SG_LAUNCH_CHECK("k_csr_to_dia / k_dia_symcheck");
     h->kernels += h->pre == SG_PRECOND_LEARNED ? 3 : 2;
-    unsigned int asym = 1;
-    SG_CUDA(cudaMemcpyAsync(&asym, h->d_flag, sizeof(asym), cudaMemcpyDeviceToHost, s));
+    if (h->coef) {  // this solve's coefficients -> the guarded copy; verify A against them
+      SG_CUDA(cudaMemcpyAsync(h->coef, h->coef_user, h->n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      k_stencil_check<<<gb, 256, 0, s>>>(h->D.dia, h->coef, h->D.ihx2, h->D.ihy2, h->d_flag + 1);
+      SG_LAUNCH_CHECK("k_stencil_check");
+      h->kernels += 1;
+    }
+    unsigned int flags[2] = {1u, 1u};
+    SG_CUDA(cudaMemcpyAsync(flags, h->d_flag, sizeof(flags), cudaMemcpyDeviceToHost, s));
     SG_CUDA(cudaStreamSynchronize(s));
-    const int sym = asym ? 0 : 1;
-    if (sym != h->a_sym) {  // kernel variant changes: captured graphs are stale
+    const int sym = flags[0] ? 0 : 1;
+    const int cst = (h->coef && sym && !flags[1]) ? 1 : 0;
+    if (sym != h->a_sym || cst != h->cst) {  // kernel variant changes: captured graphs are stale
       for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);
       h->graphs.clear();
       h->graph_kernels.clear();
       h->a_sym = sym;
+      h->cst = cst;
     }
   }
   if (h->D.sell_on) {  // SELL-32 values of A, G, G^T (they may change between solves)
@@ -2742,6 +2818,44 @@ extern "C" int sg_pcg_rebind_values(sg_pcg* h, const double* a_vals, const doubl
   return SG_OK;
 }
 
+extern "C" int sg_pcg_set_stencil(sg_pcg* h, const double* coeff, int64_t nx, int64_t ny, int32_t* usable_host) {
+  if (!h) { set_error("null handle"); return SG_EINVAL; }
+  if (usable_host) *usable_host = 0;
+  const Dia& dd = h->D.dia;
+  const bool fits = coeff && nx > 1 && ny >= 1 && h->dia_nd == 5 && !h->dist && dd.off[1] == -1 && dd.off[2] == 0 &&
+                    dd.off[3] == 1 && dd.off[4] == -dd.off[0] && (int64_t)dd.off[4] == nx;
+  const double ihx2 = (double)((nx + 1) * (nx + 1)), ihy2 = (double)((ny + 1) * (ny + 1));  // datasets.py:109-110
+  if (fits && h->coef && h->D.ihx2 == ihx2 && h->D.ihy2 == ihy2) {  // only the source array moves
+    h->coef_user = coeff;
+    if (usable_host) *usable_host = 1;
+    return SG_OK;
+  }
+  for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);  // the captured Dev changes
+  h->graphs.clear();
+  h->graph_kernels.clear();
+  if (!fits) {
+    if (h->coef) cudaFree(h->coef - h->guard);
+    h->coef = nullptr;
+    h->coef_user = nullptr;
+    h->D.coef = nullptr;
+    h->cst = 0;
+    return SG_OK;
+  }
+  if (!h->coef) {
+    double* base = nullptr;
+    SG_CUDA(cudaMalloc(&base, (size_t)(h->n + 2 * h->guard) * sizeof(double)));
+    SG_CUDA(cudaMemset(base, 0, (size_t)(h->n + 2 * h->guard) * sizeof(double)));
+    h->coef = base + h->guard;
+  }
+  h->coef_user = coeff;
+  h->D.coef = h->coef;
+  h->D.ihx2 = ihx2;
+  h->D.ihy2 = ihy2;
+  h->cst = 0;  // verified against A at every solve
+  if (usable_host) *usable_host = 1;
+  return SG_OK;
+}
+
 extern "C" int sg_pcg_set_profile(sg_pcg* h, int32_t on) {
   if (!h) { set_error("null handle"); return SG_EINVAL; }
   if ((on != 0) != (h->profile != 0)) {
@@ -2763,7 +2877,7 @@ extern "C" int sg_pcg_stats(sg_pcg* h, int64_t* kernels_host, int64_t* chunks_ho
     prof_host[3] = h->prof_active;
     prof_host[4] = h->prof_samples;
     prof_host[5] = h->dia_nd;
-    prof_host[6] = h->a_sym;
+    prof_host[6] = h->a_sym ? (h->cst ? 2.0 : 1.0) : 0.0;
     prof_host[7] = (h->staged || h->strip) && h->pre == SG_PRECOND_LEARNED ? 1.0 : 0.0;
   }
   if (reset) {
@@ -2789,6 +2903,7 @@ extern "C" void sg_pcg_destroy(sg_pcg* h) {
     if (h->sell_vals[k]) cudaFree(h->sell_vals[k]);
   }
   if (h->d_flag) cudaFree(h->d_flag);
+  if (h->coef) cudaFree(h->coef - h->guard);
   if (h->mem) cudaFree(h->mem);
   delete h;
 }

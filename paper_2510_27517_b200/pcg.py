@@ -114,13 +114,26 @@ class PcgHandle:
         self.last_elapsed_ns = int(ns.value)
         return list(res)
 
+    def set_stencil(self, coeff_dev, nx: int, ny: int) -> bool:
+        """Let the sliding-window K1 regenerate A from gen_poisson2d's node coefficients
+        (`coeff_dev`: device f64 aligned with A's rows, every system an nx-by-ny grid) instead of
+        streaming its diagonals.  Each solve verifies A bitwise against the stencil first and
+        silently keeps the stored diagonals when they differ.  `coeff_dev=None` turns it off.
+        Returns whether the handle's format can use it."""
+        ok = C.c_int32(0)
+        L.check(L.lib().sg_pcg_set_stencil(self._h, L.ptr(coeff_dev), int(nx), int(ny), C.byref(ok)),
+                "pcg_set_stencil")
+        self._coeff = coeff_dev  # kept alive: the handle reads it at every solve
+        return bool(ok.value)
+
     def set_profile(self, on: bool):
         L.check(L.lib().sg_pcg_set_profile(self._h, 1 if on else 0))
 
     def stats(self, reset: bool = False):
         """(kernels launched, graphs launched, [K1 ms, K2 ms, K3 ms, active-sum, samples, ndiag,
         a_sym, fused]) — ndiag > 0 when the handle runs the diagonal-major (DIA) format, 0 for
-        CSR; fused = 1 when K2 + K3 run as one halo-staged kernel (K2 ms covers both)."""
+        CSR; a_sym = 1 when A is read by its lower half, 2 when K1 regenerates it from the
+        coefficient stencil; fused = 1 when K2 + K3 run as one halo-staged kernel (K2 ms covers both)."""
         k, c = C.c_int64(0), C.c_int64(0)
         prof = (C.c_double * 8)()
         L.check(L.lib().sg_pcg_stats(self._h, C.byref(k), C.byref(c), prof, 1 if reset else 0))

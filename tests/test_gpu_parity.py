@@ -428,6 +428,42 @@ def test_batch_matches_single_solves():
     assert np.array_equal(x, np.concatenate([r.x for r in reps]))
 
 
+@pytest.mark.parametrize("grid", [(40, 40), (300, 12)])  # ring halo of 1 and 2 chunks
+def test_coefficient_stencil_k1_bit_identical(multi_kernel, monkeypatch, grid):
+    """K1 regenerating A from gen_poisson2d's coefficients (sg_pcg_set_stencil) == K1 streaming
+    A's stored diagonals: same k, x and residual histories, bitwise; and a coefficient array that
+    does not generate A is rejected by the per-solve check (the stored diagonals are used)."""
+    import os
+    from paper_2510_27517_b200.batch import BatchSolver, SystemBatch
+    m = P.load_checkpoint(os.path.join(os.path.dirname(__file__), "golden", "trained_heat16.spaignn"))
+    nx, ny = grid
+    seeds = list(range(5))
+    cfg = P.SolveConfig(rtol=1e-9, residual_refresh_period=7)
+    out = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("SG_PCG_STENCIL", flag)
+        sv = BatchSolver(SystemBatch.heat2d(nx, ny, seeds, [s + 3 for s in seeds]), m)
+        rs = sv.step(cfg)
+        mode = sv.handle.stats()[2][6]
+        out[flag] = ([r.k for r in rs], sv.x.cpu().numpy().copy(),
+                     [sv.handle.history(k, int(r.hist_len)) for k, r in enumerate(rs)], mode)
+    assert out["1"][3] == 2.0 and out["0"][3] == 1.0  # the stencil path ran / did not
+    assert out["1"][0] == out["0"][0]
+    assert np.array_equal(out["1"][1], out["0"][1])
+    for h1, h0 in zip(out["1"][2], out["0"][2]):
+        assert np.array_equal(np.asarray(h1), np.asarray(h0))
+    # mutation: one coefficient changed after A was generated -> check fails -> diagonals used
+    monkeypatch.setenv("SG_PCG_STENCIL", "1")
+    sv = BatchSolver(SystemBatch.heat2d(nx, ny, seeds, [s + 3 for s in seeds]), m)
+    sv.build_graph()
+    sv.build_factor()
+    sv.batch.coeff[nx * ny + 7] *= 1.5
+    rs = sv.solve(cfg)
+    assert sv.handle.stats()[2][6] == 1.0
+    assert [r.k for r in rs] == out["0"][0]
+    assert np.array_equal(sv.x.cpu().numpy(), out["0"][1])
+
+
 # --------------------------------------------------------------------------- config C4 path (a5, a18)
 def test_c4_pipeline_small():
     """rand_spd_sparse -> A^2 pattern -> A padded onto it -> graph -> GNN -> PCG (mini C4)."""
