@@ -393,6 +393,12 @@ struct CsrOps {
 // diagonals are issued together and the dependent adds form one short chain.
 template <int ND>
 __device__ __forceinline__ double combine_numpy(const double (&p)[ND], unsigned int m) {
+  if (m == (1u << ND) - 1u) {  // interior row, every diagonal present: the same adds, no selects
+    double s = add(0.0, p[1 < ND ? 1 : 0]);
+#pragma unroll
+    for (int d = 2; d < ND; ++d) s = add(s, p[d]);
+    return ND > 1 ? add(p[0], s) : p[0];
+  }
   double first = 0.0, s = 0.0;
   bool have = false, more = false;
 #pragma unroll
@@ -410,6 +416,12 @@ __device__ __forceinline__ double combine_numpy(const double (&p)[ND], unsigned 
 // Sequential (add.at order) sum of the present products, branch-free.
 template <int ND>
 __device__ __forceinline__ double combine_seq(const double (&p)[ND], unsigned int m) {
+  if (m == (1u << ND) - 1u) {  // every entry present: the same adds, no selects
+    double s = 0.0;
+#pragma unroll
+    for (int d = 0; d < ND; ++d) s = add(s, p[d]);
+    return s;
+  }
   double s = 0.0;
 #pragma unroll
   for (int d = 0; d < ND; ++d) {
