@@ -18,6 +18,7 @@ rank, no collective in the solve; max-over-ranks device time.
 from __future__ import annotations
 
 import argparse
+import glob
 import json
 import os
 import subprocess
@@ -334,7 +335,8 @@ def run_ours(a, rank, world, local):
         print(json.dumps(out), flush=True)
 
 
-NCU_SUMMARY = os.path.join(ROOT, "profiles", "r01_ncu_full_pcg_sw_128sys.txt")
+NCU_SUMMARY = (sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_full_pcg_sw_128sys.txt"))) or
+               [os.path.join(ROOT, "profiles", "r01_ncu_full_pcg_sw_128sys.txt")])[-1]  # newest round
 
 
 def ncu_traffic(kernel):
