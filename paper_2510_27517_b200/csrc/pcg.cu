@@ -1298,6 +1298,21 @@ __device__ __forceinline__ int ring_wrap(int x, int R) {
   return x >= R ? x - R : x;
 }
 
+// The same for neighbour d of a sorted, symmetric diagonal set with an odd count (ND 5, 7):
+// offsets below the middle are negative, above it positive, the middle one is 0 -- so one
+// wrap test (or none) per diagonal.  Even ND (padded sets) keep the two-sided wrap.
+template <int ND>
+__device__ __forceinline__ int ring_nb(int base, const int (&off)[ND], int d, int R) {
+  if constexpr (ND % 2 == 1) {
+    if (d == ND / 2) return base;
+    const int x = base + off[d];
+    if (d < ND / 2) return x < 0 ? x + R : x;
+    return x >= R ? x - R : x;
+  } else {
+    return ring_wrap(base + off[d], R);
+  }
+}
+
 template <int ND, int NH>
 __global__ void __launch_bounds__(PR, 1) k_iter23_sw(Dev D, int par) {
   using G = Sw23<ND, NH>;
@@ -1387,7 +1402,7 @@ __global__ void __launch_bounds__(PR, 1) k_iter23_sw(Dev D, int par) {
       double p[ND];
 #pragma unroll
       for (int d = 0; d < ND; ++d) {
-        const int ix = ring_wrap(base + off[d], GR);
+        const int ix = ring_nb<ND>(base, off, d, GR);
         p[d] = mul(gr[(ND - 1 - d) * GR + ix], rp[ix]);
       }
       const double v = combine_seq<ND>(p, m);
@@ -1402,7 +1417,7 @@ __global__ void __launch_bounds__(PR, 1) k_iter23_sw(Dev D, int par) {
       const unsigned int m = mk[io];
       double p[ND];
 #pragma unroll
-      for (int d = 0; d < ND; ++d) p[d] = mul(gr[d * GR + io], tr[ring_wrap(tb + off[d], TR)]);
+      for (int d = 0; d < ND; ++d) p[d] = mul(gr[d * GR + io], tr[ring_nb<ND>(tb, off, d, TR)]);
       const double y = combine_numpy<ND>(p, m);
       const double rni = rp[io];
       const double si = add(y, mul(eps, rni));
@@ -1542,14 +1557,14 @@ __global__ void __launch_bounds__(PR, 5) k_iter1_sw(Dev D, int par) {
           double p[ND];
           if constexpr (CS) {
             double a[5];
-            stencil5(ar[io], ar[ring_wrap(io + off[0], RING)], ar[ring_wrap(io - 1, RING)],
-                     ar[ring_wrap(io + 1, RING)], ar[ring_wrap(io + off[4], RING)], m, D.ihx2, D.ihy2, a);
+            stencil5(ar[io], ar[ring_nb<ND>(io, off, 0, RING)], ar[ring_nb<ND>(io, off, 1, RING)],
+                     ar[ring_nb<ND>(io, off, 3, RING)], ar[ring_nb<ND>(io, off, 4, RING)], m, D.ihx2, D.ihy2, a);
 #pragma unroll
             for (int d = 0; d < ND; ++d) p[d] = mul(a[d], dp[(li + off[d]) & DM]);
           } else {
 #pragma unroll
             for (int d = 0; d < ND; ++d) {
-              const int ix = ring_wrap(io + off[d], RING);
+              const int ix = ring_nb<ND>(io, off, d, RING);
               // FMT 2: an upper entry (i, i+off) is the lower mirror entry at row i+off
               const double a = (FMT == 2 && d > ND / 2) ? ar[(ND - 1 - d) * RING + ix] : ar[d * RING + io];
               p[d] = mul(a, dp[(li + off[d]) & DM]);
