@@ -203,3 +203,22 @@ def test_pattern_square_restatement_brute_force():
     ref = np.zeros((60, 60))
     ref[O.row_expand(offs), cols] = vals
     assert np.array_equal(dense, ref) and len(pv) == len(pc)
+
+
+def test_coefficient_stencil_formula_regenerates_reference_A(g_heat):
+    """The per-row formula of the coefficient-stencil K1 (pcg.cu `stencil5`: faces 0.5*(a_i+a_j),
+    a wall face keeps a_i, off-diagonal -face*(n+1)^2, diagonal (w+e)*(nx+1)^2 + (s+n)*(ny+1)^2,
+    presence from the row's pattern) reproduces the reference's gen_poisson2d A bit for bit on its
+    golden heat2d systems (datasets.py:87-145; tests/golden/golden_heat.npz)."""
+    for tag, nx in (("h16", 16), ("h32", 32)):
+        offs, cols, vals = g_heat[tag + "A_offs"], g_heat[tag + "A_cols"], g_heat[tag + "A_vals"]
+        a = [float(v) for v in g_heat[tag + "coeff"]]
+        ihx2 = ihy2 = float((nx + 1) ** 2)
+        for i in range(len(offs) - 1):
+            row = {int(c): float(v) for c, v in zip(cols[offs[i]:offs[i + 1]], vals[offs[i]:offs[i + 1]])}
+            face = {j: (0.5 * (a[i] + a[j]) if j in row else a[i]) for j in (i - nx, i - 1, i + 1, i + nx)}
+            want = {i - nx: -(face[i - nx] * ihy2), i - 1: -(face[i - 1] * ihx2), i + 1: -(face[i + 1] * ihx2),
+                    i + nx: -(face[i + nx] * ihy2),
+                    i: (face[i - 1] + face[i + 1]) * ihx2 + (face[i - nx] + face[i + nx]) * ihy2}
+            for j, v in row.items():
+                assert np.float64(v).tobytes() == np.float64(want[j]).tobytes(), (tag, i, j)
