@@ -46,8 +46,38 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=5)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--cpu-workers", type=int, default=0)
+    p.add_argument("--cpu-workers", type=int, default=0, help="0 = every core of the affinity mask")
+    p.add_argument("--no-c5", action="store_true", help="skip the north-star C5 block (N = 1 only)")
+    p.add_argument("--c5-steps", type=int, default=3)
     return p.parse_args()
+
+
+def host_cores():
+    """Cores this process may run on (affinity mask) and the machine's count."""
+    try:
+        aff = len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        aff = os.cpu_count() or 1
+    return aff, os.cpu_count() or aff
+
+
+REAL_REF = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_reference_real_c2.json")))
+
+
+def real_reference_scale():
+    """Speed ratio port / real reference on one C2 system, measured in the build container
+    (profiles/time_real_reference.py; the reference cannot travel to the GPU box)."""
+    if not REAL_REF:
+        return None
+    try:
+        rows = [json.loads(line) for line in open(REAL_REF[-1]) if line.strip()]
+    except Exception:
+        return None
+    best = max(rows, key=lambda r: int(r["host"].get("openblas_threads") or 1))
+    return {"port_over_reference_speed": best["port_over_reference_speed"],
+            "reference_s_per_system": best["reference_total_s"], "port_s_per_system": best["port_total_s"],
+            "reference_k": best["reference_k"], "port_k": best["port_k"],
+            "source": os.path.relpath(REAL_REF[-1], ROOT) + " (real spaigraph timed in the build container)"}
 
 
 def config_block(a, world):
@@ -105,7 +135,7 @@ class ClockSampler:
 
 def cpu_baseline(a, params, workers, seeds):
     from oracle.cpu_baseline import run_pool
-    wall, res = run_pool(a.nx, seeds, params, a.rtol, workers)
+    wall, res = run_pool(a.nx, seeds, params, a.rtol, min(workers, len(seeds)))
     return wall, res
 
 
@@ -115,7 +145,8 @@ def run_reference(a, rank, world):
         return
     from paper_2510_27517_b200.gnn import load_checkpoint
     params = load_checkpoint(CKPT).params_flat()
-    workers = a.cpu_workers or min(os.cpu_count() or 1, 16)
+    aff, ncpu = host_cores()
+    workers = a.cpu_workers or aff
     vals = []
     seed = 0
     for step in range(a.warmup + a.steps):
@@ -135,9 +166,96 @@ def run_reference(a, rank, world):
            "cpu_baseline": {"value": value, "unit": "solves/s", "cores": workers, "kind": "port",
                             "sample": f"{workers} systems per step ({workers} worker processes x 1 system, "
                                       f"1 BLAS thread each), numpy restatement oracle/spaigraph_ref.py",
-                            "mean_k": float(np.mean(ks))},
+                            "os_cpu_count": ncpu, "affinity_cores": aff, "mean_k": float(np.mean(ks))},
+           "real_reference": _extrapolated(value),
            "e2e": {"value": value, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
+
+
+def _extrapolated(port_value):
+    sc = real_reference_scale()
+    if sc is None:
+        return None
+    return {**sc, "extrapolated_value": port_value / sc["port_over_reference_speed"], "unit": "solves/s",
+            "note": "the port's solves/s on this box divided by the port/reference speed ratio measured on one "
+                    "C2 system in the build container: an EXTRAPOLATED figure for the real reference"}
+
+
+K1N = "k_iter1 (q = A d, d = s + beta d, d.q)"
+K2N = "k_iter2 (x, r update, t = G^T r, r.r)"
+K3N = "k_iter3 (s = G t + eps r, r.s)"
+K23N = "k_iter23 (fused: x, r update, t = G^T r on chip, s = G t + eps r, r.r, r.s)"
+
+
+def hbm_peak():
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        peaks = {}
+    if "hbm_gbs" in peaks:
+        return float(peaks["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def pcg_roofline(prof, n1, e1n, peak, peak_src, K23_SW, K1_SW, units_note="per system"):
+    """Roofline of the PCG iteration kernels from the handle's in-graph event samples.
+
+    `achieved` counts the ALGORITHMIC bytes of the layout the kernels run: the
+    diagonal-major (DIA) format moves 8 B per streamed diagonal per row (A by its lower half when
+    it is bitwise symmetric, or ONE coefficient per row when K1 regenerates A from gen_poisson2d's
+    stencil), a 1-byte presence mask per row, and each vector once (K1: s, d read, d', q
+    written = 32 B/row; fused K2+K3: r, q, x, d read, r', x, s written = 56 B/row) -- halo
+    re-reads and guard rows are NOT counted, so they show up as lost fraction.
+    §8(d)'s CSR formula (12 B/nnz + 4 B/row of index + value traffic these kernels never move)
+    is kept as a labelled aside; it overstates the fraction.  Every per-kernel fraction must be
+    physically possible (<= 1.2 of the burst peak); anything else is a byte-accounting error."""
+    samples = prof[4]
+    if samples <= 0:
+        return None
+    fused = bool(prof[7])
+    nd, a_sym = int(prof[5]), int(prof[6])
+    csr = 12 * e1n + 4 * (n1 + 1)
+    survey = {K1N: csr + 32 * n1}
+    if fused:
+        survey[K23N] = csr + 56 * n1
+    else:
+        survey.update({K2N: csr + 56 * n1, K3N: csr + 24 * n1})
+    n_low = 1 if a_sym == 2 else (nd // 2 + 1) if a_sym else nd
+    if nd:
+        alg = {K1N: (8 * n_low + 1 + 32) * n1}
+        if fused:
+            alg[K23N] = (8 * nd + 1 + 56) * n1
+        else:
+            alg.update({K2N: (8 * nd + 1 + 56) * n1, K3N: (8 * nd + 1 + 24) * n1})
+    else:
+        alg = dict(survey)
+    avg_active = prof[3] / samples
+    kern = {}
+    for (name, b_alg), t_ms in zip(alg.items(), prof[:3]):
+        avg_ms = t_ms / samples
+        if avg_ms <= 0:
+            continue
+        gbs = b_alg * avg_active / (avg_ms * 1e-3) / 1e9
+        sv = survey[name] * avg_active / (avg_ms * 1e-3) / 1e9
+        kern[name] = {"avg_ms": avg_ms, "bytes_per_launch": b_alg * avg_active, "gbs": gbs, "frac": gbs / peak,
+                      "bytes_per_row": b_alg / n1, "survey_csr_gbs": sv, "survey_csr_frac": sv / peak}
+        assert gbs / peak <= 1.2, f"{name}: {gbs:.0f} GB/s exceeds 1.2x the {peak:.0f} GB/s peak (byte accounting)"
+    if not kern:
+        return None
+    dom = max(kern, key=lambda k: kern[k]["avg_ms"])
+    traffic = ncu_traffic(K23_SW if dom == K23N else K1_SW if dom == K1N else None)
+    return {"bound": "hbm", "kernel": dom, "achieved": kern[dom]["gbs"], "peak": peak, "unit": "GB/s",
+            "frac": kern[dom]["frac"], "traffic": traffic["bytes"] if traffic else None,
+            "traffic_source": traffic["source"] if traffic else None,
+            "algorithmic_bytes_per_launch": kern[dom]["bytes_per_launch"],
+            "bytes_definition": f"DIA layout ({nd} diagonals; A {'from the coefficient stencil' if a_sym == 2 else 'by its lower half' if a_sym else 'all diagonals'}): "
+                                "8 B/streamed diagonal/row + 1 B mask + each vector once; halo re-reads not counted "
+                                f"({units_note}, x the average number of active systems)",
+            "frac_vs_nominal_8tbs": kern[dom]["gbs"] / 8000.0,
+            "survey_csr_formula": {"achieved": kern[dom]["survey_csr_gbs"], "frac": kern[dom]["survey_csr_frac"],
+                                   "note": "SURVEY.md §8(d) CSR bytes (12 B/nnz + 4 B/row): index/value traffic the "
+                                           "DIA kernels never move -- an overstatement, kept for reference only"},
+            "peak_source": peak_src, "per_kernel": kern, "samples": int(samples), "avg_active_systems": avg_active}
 
 
 def run_ours(a, rank, world, local):
@@ -194,69 +312,8 @@ def run_ours(a, rank, world, local):
     # ---- roofline of the PCG iteration kernels (sampled live by in-graph event nodes)
     n1 = a.nx * a.nx
     e1n = 5 * n1 - 4 * a.nx
-    fused = bool(prof[7])
-    K1N = "k_iter1 (q = A d, d = s + beta d, d.q)"
-    K2N = "k_iter2 (x, r update, t = G^T r, r.r)"
-    K3N = "k_iter3 (s = G t + eps r, r.s)"
-    K23N = "k_iter23 (fused: x, r update, t = G^T r on chip, s = G t + eps r, r.r, r.s)"
-    # algorithmic bytes per system per launch: CSR matrix bytes
-    # (12 B/nnz + 4 B/row) + the vectors each kernel must read / write once
-    csr = 12 * e1n + 4 * (n1 + 1)
-    per_sys = {K1N: csr + 32 * n1}
-    if fused:  # t never leaves the SM: reads x d r q, writes x r s
-        per_sys[K23N] = csr + 56 * n1
-    else:
-        per_sys.update({K2N: csr + 56 * n1, K3N: csr + 24 * n1})
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except Exception:
-        pass
-    peak = float(peaks.get("hbm_gbs", 6650.0))
-    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
-    # bytes the diagonal-major layout physically has to move per row (values incl. padding,
-    # 1-byte presence mask, vectors); A read by its lower half when bitwise symmetric, or as
-    # one coefficient per row when K1 regenerates it from gen_poisson2d's stencil (a_sym 2)
-    nd, a_sym = int(prof[5]), int(prof[6])
-    n_low = 1 if a_sym == 2 else (nd // 2 + 1) if a_sym else nd
-    phys = {}
-    if nd:
-        phys = {K1N: (8 * n_low + 1 + 32) * n1}
-        if fused:
-            phys[K23N] = (8 * nd + 1 + 56) * n1
-        else:
-            phys.update({K2N: (8 * nd + 1 + 56) * n1, K3N: (8 * nd + 1 + 24) * n1})
-    kern = {}
-    samples = prof[4]
-    if samples > 0:
-        avg_active = prof[3] / samples
-        for (name, b), t_ms in zip(per_sys.items(), prof[:3]):
-            avg_ms = t_ms / samples
-            achieved = b * avg_active / (avg_ms * 1e-3) / 1e9
-            kern[name] = {"avg_ms": avg_ms, "gbs": achieved, "frac": achieved / peak,
-                          "bytes_per_launch": b * avg_active}
-            if name in phys:
-                pg = phys[name] * avg_active / (avg_ms * 1e-3) / 1e9
-                kern[name].update({"physical_bytes_per_launch": phys[name] * avg_active, "physical_gbs": pg,
-                                   "physical_frac": pg / peak})
-    dom = max(kern, key=lambda k: kern[k]["avg_ms"]) if kern else None
-    roofline = None
-    if dom:
-        traffic = ncu_traffic("k_iter23_sw" if dom == K23N else "k_iter1_sw" if dom == K1N else None)
-        roofline = {"bound": "hbm", "kernel": dom, "achieved": kern[dom]["gbs"], "peak": peak,
-                    "unit": "GB/s", "frac": kern[dom]["frac"],
-                    "traffic": traffic["bytes"] if traffic else None,
-                    "traffic_source": traffic["source"] if traffic else None,
-                    "achieved_physical": kern[dom].get("physical_gbs"),
-                    "frac_physical": kern[dom].get("physical_frac"),
-                    "frac_vs_nominal_8tbs": kern[dom]["gbs"] / 8000.0,
-                    "frac_physical_vs_nominal_8tbs": (kern[dom].get("physical_gbs") or 0.0) / 8000.0,
-                    "bytes_note": "achieved = SURVEY.md §8(d) CSR bytes (12 B/nnz + 4 B/row + vectors); the kernels "
-                                  f"run the diagonal-major layout ({nd} diagonals{', A by its lower half' if a_sym else ''}) "
-                                  "which moves fewer bytes: physical_* counts those (8 B/diagonal/row + 1 B mask + vectors)",
-                    "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)" if peak_src == "measured" else peak_src,
-                    "per_kernel": kern, "samples": int(samples), "avg_active_systems": prof[3] / samples}
-
+    peak, peak_src = hbm_peak()
+    roofline = pcg_roofline(prof, n1, e1n, peak, peak_src, K23_SW="k_iter23_sw", K1_SW="k_iter1_sw")
     # ---- e2e through the public batched API from host buffers
     e2e = None
     if not a.no_e2e:
@@ -314,13 +371,26 @@ def run_ours(a, rank, world, local):
     # ---- CPU baseline (rank 0, N = 1 only), bounded sample
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        workers = a.cpu_workers or min(os.cpu_count() or 1, 16)
-        wall, cres = cpu_baseline(a, model.params_flat(), workers, list(range(workers)))
-        cpu = {"value": workers / wall, "unit": "solves/s", "cores": workers, "kind": "port",
-               "sample": f"{workers} of the same heat2d {a.nx}x{a.nx} systems (seeds 0..{workers - 1}), "
-                         f"{workers} processes x 1 BLAS thread, numpy restatement of the reference path "
-                         f"(tape-free => faster than the reference forward); wall {wall:.1f} s",
-               "k": [k for _, k, _ in cres], "gpu_k_same_systems": [int(x) for x in k_all[:workers]]}
+        aff, ncpu = host_cores()
+        workers = a.cpu_workers or aff
+        seeds = list(range(min(workers, S)))
+        wall, cres = cpu_baseline(a, model.params_flat(), workers, seeds)
+        k_cpu = [k for _, k, _ in cres]
+        k_gpu = [int(x) for x in k_all[:len(seeds)]]
+        # parity on the benched systems: every GPU k within +-2% of the oracle's (north_star bar)
+        bad = [(s_, kc, kg) for s_, kc, kg in zip(seeds, k_cpu, k_gpu) if abs(kg - kc) > max(1, 0.02 * kc)]
+        assert not bad, f"GPU iteration counts outside +-2% of the oracle: {bad}"
+        cpu = {"value": len(seeds) / wall, "unit": "solves/s", "cores": min(workers, len(seeds)), "kind": "port",
+               "os_cpu_count": ncpu, "affinity_cores": aff,
+               "sample": f"{len(seeds)} of the same heat2d {a.nx}x{a.nx} systems (seeds 0..{len(seeds) - 1}), "
+                         f"{min(workers, len(seeds))} processes x 1 BLAS thread, numpy restatement of the reference "
+                         f"path (tape-free => faster than the reference forward); wall {wall:.1f} s",
+               "k": k_cpu, "gpu_k_same_systems": k_gpu, "k_parity": "asserted: |k_gpu - k_oracle| <= max(1, 2%)",
+               "real_reference": _extrapolated(len(seeds) / wall)}
+
+    c5 = None
+    if world == 1 and not a.no_c5:
+        c5 = run_c5(a, model, dev)
 
     if rank == 0:
         value = world * S / (ms / 1000.0)
@@ -331,8 +401,122 @@ def run_ours(a, rank, world, local):
                "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
                "k": {"mean": float(np.mean(k_all)), "min": int(np.min(k_all)), "max": int(np.max(k_all)),
                      "all_converged": bool(np.all(conv_all == 1))},
-               "pcg_graph_launches_per_step": chunks / a.steps}
+               "pcg_graph_launches_per_step": chunks / a.steps, "c5": c5}
         print(json.dumps(out), flush=True)
+
+
+def run_c5(a, model, dev):
+    """North-star block (BASELINE.json configs[4]): ONE 2048x2048 Poisson
+    system (n = 4,194,304) through the drop-in API -- build_graph -> forward -> build_learned_spai
+    -> pcg_solve (rtol 1e-6, trained weights) -- on 1 GPU.  `value`: device-timed solves/s with A
+    resident; `e2e`: the same from host int64 CSR + host rhs to host x; roofline of the strip
+    kernels (k_iter1_s5, k_iter23_s5); a parity check (converged, true residual <= rtol); and an
+    EXTRAPOLATED CPU baseline of the oracle port (bounded sample: full-size features, the GNN on a
+    256x256 block scaled per edge, 5 full-size PCG iterations scaled to k)."""
+    import torch
+
+    import paper_2510_27517_b200 as P
+    from paper_2510_27517_b200.pcg import _handle_for
+    nx = 2048
+    rtol = 1e-6
+    A, meta = P.gen_poisson2d(nx, nx)
+    b = P.gen_rhs(meta, 10**6)
+    b_dev = torch.as_tensor(b, device=dev)
+    cfg = P.SolveConfig(rtol=rtol)
+    eps = model.config.epsilon
+
+    def step(Am, bb):
+        G = P.forward(model, P.build_graph(Am, meta)).G
+        M = P.build_learned_spai(G, eps)
+        return P.pcg_solve(Am, bb, M, cfg), M
+
+    for _ in range(max(1, min(a.warmup, 2))):
+        rep, M = step(A, b_dev)
+    h = _handle_for(A, M, "learned")
+    h.set_profile(True)
+    step(A, b_dev)  # capture the profiled graphs
+    h.stats(reset=True)
+    clocks = ClockSampler(dev.index or 0)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(a.c5_steps):
+        rep, M = step(A, b_dev)
+    e1.record()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1) / a.c5_steps
+    kernels, chunks, prof = h.stats(reset=True)
+    h.set_profile(False)
+    x = rep.x
+    rel = float(torch.linalg.vector_norm(b_dev - P.spmv(A, x)) / torch.linalg.vector_norm(b_dev))
+    assert rep.converged and rel <= rtol, (rep.converged, rel)
+    peak, peak_src = hbm_peak()
+    n, nnz = A.n_rows, A.nnz
+    roof = pcg_roofline(prof, n, nnz, peak, peak_src, K23_SW="k_iter23_s5", K1_SW="k_iter1_s5",
+                        units_note="one system")
+    if roof is not None:
+        roof["traffic"] = None
+        roof["traffic_source"] = "see profiles/r03_ncu_c5_*.txt"
+    # e2e: host int64 CSR + host rhs in, host x out, through the public API
+    offs_h, cols_h, vals_h = A.row_offsets.copy(), A.col_indices.copy(), A.values.copy()
+    e2e_ms = []
+    for it in range(3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        Ah = P.SparseMatrix(n, n, offs_h, cols_h, vals_h)
+        rep_h, _ = step(Ah, b)
+        xh = rep_h.x  # numpy: D2H inside the region
+        torch.cuda.synchronize()
+        if it:
+            e2e_ms.append(1000 * (time.perf_counter() - t0))
+    assert rep_h.k == rep.k and isinstance(xh, np.ndarray)
+    h2d = offs_h.nbytes + cols_h.nbytes + vals_h.nbytes + b.nbytes + meta.coeff.nbytes
+    cpu = c5_cpu_baseline(model, rep.k) if not a.no_cpu_baseline else None
+    return {"workload": "C5: 2D Poisson 2048x2048 (n=4,194,304, nnz 20,963,328), trained GNN-SPAI + PCG rtol 1e-6, "
+                        "one system, 1 GPU (configs[4] at N=1; the row partition over 2/4/8 GPUs is separate)",
+            "metric": METRIC, "value": 1000.0 / ms, "unit": "solves/s", "ms_per_solve": ms, "k": int(rep.k),
+            "pcg_us_per_iteration": rep.t_cg_total_ns / 1e3 / max(rep.k, 1),
+            "parity": {"converged": bool(rep.converged), "true_relative_residual": rel, "rtol": rtol,
+                       "oracle_tests": "tests/test_gpu_config_parity.py (G on sampled rows <= 1e-10, first 50 "
+                                       "residuals <= 1e-9 vs the oracle replay)"},
+            "e2e": {"value": 1000.0 / float(np.mean(e2e_ms)), "unit": "solves/s", "ms_per_solve": float(np.mean(e2e_ms)),
+                    "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(8 * n),
+                    "api": "SparseMatrix(host int64 CSR) -> build_graph -> forward -> build_learned_spai -> "
+                           "pcg_solve(host b) -> host x"},
+            "roofline": roof, "clocks": clk, "cpu_baseline": cpu}
+
+
+def c5_cpu_baseline(model, k_gpu):
+    """Oracle port on the host, bounded: features at full size, the reference-form GNN on a
+    256x256 block (per-edge time scaled to C5's edges), 5 full-size PCG iterations (reference
+    add.at apply) scaled to the GPU's k.  All of it labelled extrapolated."""
+    from oracle import spaigraph_ref as O
+    aff, ncpu = host_cores()
+    nx = 2048
+    n = nx * nx
+    offs, cols, vals, coeff = O.gen_poisson2d(nx, nx)
+    b = O.gen_rhs(n, 10**6)
+    t0 = time.perf_counter()
+    node, _, ef, _ = O.graph_features(n, offs, cols, vals, "poisson2d", (nx, nx), coeff)
+    t_feat = time.perf_counter() - t0
+    mlps = O.unflatten(np.asarray(model.params_flat()), O.init_params(3))
+    so, sc, sv, scoef = O.gen_poisson2d(256, 256)
+    snode, _, sef, _ = O.graph_features(256 * 256, so, sc, sv, "poisson2d", (256, 256), scoef)
+    t0 = time.perf_counter()
+    gsub = O.gnn_forward(mlps, snode, so, sc, sef, 4)
+    t_gnn = (time.perf_counter() - t0) * len(cols) / len(sc)
+    g = np.resize(gsub, len(vals))  # placeholder factor values: the timing does not depend on them
+    t0 = time.perf_counter()
+    O.pcg_solve(offs, cols, vals, b, lambda r: O.learned_apply(n, offs, cols, g, 1e-4, r), rtol=1e-30, max_iters=5)
+    t_it = (time.perf_counter() - t0) / 5
+    total = t_feat + t_gnn + k_gpu * t_it
+    return {"value": 1.0 / total, "unit": "solves/s", "cores": aff, "kind": "port",
+            "os_cpu_count": ncpu, "affinity_cores": aff,
+            "sample": f"EXTRAPOLATED: features at full size {t_feat:.1f} s; reference-form GNN on a 256x256 block, "
+                      f"scaled per edge -> {t_gnn:.1f} s; 5 full-size PCG iterations at {1000 * t_it:.0f} ms each "
+                      f"x k={k_gpu} -> {k_gpu * t_it:.0f} s (numpy: elementwise work on one core, BLAS matmuls on all)",
+            "seconds_per_solve": total}
 
 
 NCU_SUMMARY = (sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_full_pcg_sw_128sys.txt"))) or

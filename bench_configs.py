@@ -83,7 +83,7 @@ def main():
         M = P.build_learned_spai(G, model.config.epsilon)
         if profile:
             from paper_2510_27517_b200.pcg import _handle_for
-            h = _handle_for(A, M)
+            h = _handle_for(A, M, "learned")
             h.set_profile(True)
             h.stats(reset=True)
         rep = P.pcg_solve(A, b_dev, M, cfg)
@@ -103,7 +103,7 @@ def main():
         times.append(time.perf_counter() - t0)
         reps.append(rep)
     from paper_2510_27517_b200.pcg import _handle_for
-    h = _handle_for(A, M)
+    h = _handle_for(A, M, "learned")
     kernels, chunks, prof = h.stats()
     n, nnz = A.n_rows, A.nnz
     nnz_g = Ap.nnz if a.config == "c4" else nnz  # G (and G^T) live on the A^2 pattern for C4

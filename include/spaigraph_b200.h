@@ -260,6 +260,13 @@ int sg_pcg_rebind_values(sg_pcg* h, const double* a_vals, const double* g_vals, 
  * coeff = NULL turns it off.  *usable_host = 1 when the handle's format can use it. */
 int sg_pcg_set_stencil(sg_pcg* h, const double* coeff, int64_t nx, int64_t ny, int32_t* usable_host);
 
+/* A handle is planned on the PATTERNS of A, G, G^T (storage format, diagonal set, tile and
+ * range tables, SELL copies).  Every sg_pcg_solve fingerprints the patterns behind the
+ * pointers and re-plans the handle when the caller refilled them with another pattern (same
+ * sizes or not); sg_pcg_rebuilds reports how many times that happened.  A row-partitioned
+ * handle whose pattern changed fails with SG_EINVAL instead. */
+int sg_pcg_rebuilds(sg_pcg* h, int64_t* rebuilds_host);
+
 int sg_pcg_set_profile(sg_pcg* h, int32_t on);
 int sg_pcg_stats(sg_pcg* h, int64_t* kernels_host, int64_t* chunks_host, double* prof_host,
                  int32_t reset);

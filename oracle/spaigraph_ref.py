@@ -162,6 +162,23 @@ def spmv_transpose(n_cols, offs, cols, vals, x):
     return y
 
 
+def spmv_transpose_explicit(n_cols, offs_t, cols_t, vals_t, x):
+    """sparse.py:194-201 evaluated over an explicit transpose (offs_t, cols_t, vals_t from
+    `transpose`): np.add.at visits entries in storage order, so y_j accumulates its products in
+    ascending original row order starting from 0.0 -- exactly a left-to-right sum along row j of
+    the transpose.  Vectorised over rows one position at a time (each step is the same single
+    rounding per element), bit-identical to `spmv_transpose` and much faster at C5 size."""
+    offs_t = np.asarray(offs_t, dtype=np.int64)
+    x = np.asarray(x, dtype=np.float64)
+    lens = np.diff(offs_t)
+    y = np.zeros(n_cols)
+    for p in range(int(lens.max()) if len(lens) else 0):
+        rows = np.flatnonzero(lens > p)
+        k = offs_t[rows] + p
+        y[rows] = y[rows] + np.asarray(vals_t)[k] * x[np.asarray(cols_t)[k]]
+    return y
+
+
 def mean_abs_nonzero_norm(vals):
     """sparse.py:204-213: fsum(|v|)/nnz, correctly rounded sum."""
     vals = np.asarray(vals, dtype=np.float64)

@@ -152,6 +152,34 @@ __global__ void k_differ(const int32_t* __restrict__ a, const int32_t* __restric
     if (a[k] != b[k]) { *flag = 1u; return; }
 }
 
+// ------------------------------------------------------------------ pattern fingerprint
+// A handle's formats (DIA offset set, strip width, SELL column copies, tile / range tables, row
+// lengths) are derived from the CSR PATTERNS at creation, while the caller may refill the same
+// index buffers between solves (batch.py refills its device CSR in place).  Every solve
+// fingerprints the patterns and rebuilds the handle when they moved, so a stale plan can never
+// drop entries.  The fingerprint is an order-independent sum (mod 2^64) of a 64-bit mix of
+// (position, value) over offs[0..n] and cols[0..offs[n]): deterministic, one read of the indices.
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void k_pattern_hash(const int32_t* __restrict__ offs, const int32_t* __restrict__ cols, int64_t n,
+                               unsigned long long salt, unsigned long long* out) {
+  const int64_t nnz = offs[n];
+  const int64_t tot = n + 1 + (nnz > 0 ? nnz : 0);
+  unsigned long long h = 0;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < tot; k += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned int v = (unsigned int)(k <= n ? offs[k] : cols[k - n - 1]);
+    h += mix64(((unsigned long long)k << 1) ^ ((unsigned long long)v << 40) ^ ((unsigned long long)v >> 24) ^ salt);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, h);
+}
+
 // ------------------------------------------------------------------ DIA detection / conversion
 // Insert every (col - row) into a 16-slot device set; overflow => not DIA-able.
 __global__ void k_dia_offsets(const int32_t* __restrict__ offs, const int32_t* __restrict__ cols, int64_t n,
@@ -173,10 +201,12 @@ __global__ void k_dia_offsets(const int32_t* __restrict__ offs, const int32_t* _
   }
 }
 
-// CSR -> diagonal-major values (+ presence mask).  Every slot of every row is written.
+// CSR -> diagonal-major values (+ presence mask).  Every slot of every row is written.  An entry
+// on a diagonal outside the handle's offset set sets *unmatched (the solve fails loudly instead
+// of dropping it; the pattern fingerprint normally rebuilds the handle before this can happen).
 __global__ void k_csr_to_dia(const int32_t* __restrict__ offs, const int32_t* __restrict__ cols,
                              const double* __restrict__ vals, int64_t n, Dia dia, double* out,
-                             unsigned char* mask) {
+                             unsigned char* mask, unsigned int* unmatched) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     double v[MAXD];
 #pragma unroll
@@ -184,9 +214,11 @@ __global__ void k_csr_to_dia(const int32_t* __restrict__ offs, const int32_t* __
     unsigned int m = 0;
     for (int32_t k = offs[i]; k < offs[i + 1]; ++k) {
       const int o = cols[k] - (int)i;
+      bool hit = false;
 #pragma unroll
       for (int d = 0; d < MAXD; ++d)
-        if (d < dia.nd && dia.off[d] == o) { v[d] = vals[k]; m |= 1u << d; }
+        if (d < dia.nd && dia.off[d] == o) { v[d] = vals[k]; m |= 1u << d; hit = true; }
+      if (!hit) *unmatched = 1u;
     }
 #pragma unroll
     for (int d = 0; d < MAXD; ++d)
@@ -1941,9 +1973,13 @@ struct sg_pcg {
   const double* coef_user = nullptr;
   double* coef = nullptr;
   int cst = 0;
+  int64_t st_nx = 0, st_ny = 0;
+  // fingerprints of the A, G, G^T patterns the handle was planned on (k_pattern_hash)
+  unsigned long long pat_hash[3] = {0, 0, 0};
   // instrumentation: kernel launches, and (when profiling) event nodes around the kernels of
   // one non-refresh iteration per chunk -> per-kernel device time sampled inside the solve
   int64_t kernels = 0, chunks = 0;
+  int64_t rebuilds = 0;  // re-plans after a pattern change (sg_pcg_rebuilds)
   int profile = 0;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   double prof_ms[3] = {0, 0, 0};
@@ -2423,6 +2459,56 @@ int setup_sell(sg_pcg* h, const int32_t* a_offs, const int32_t* a_cols, const in
 }
 }  // namespace
 
+namespace {
+// d_flag block: [0] A not bitwise symmetric, [1] stencil mismatch, [2] unmatched DIA entry,
+// [3] unused; bytes 16..39: the three pattern fingerprints of this solve.
+constexpr int kFlagBytes = 40;
+
+int pattern_hashes(sg_pcg* h, cudaStream_t s) {
+  SG_CUDA(cudaMemsetAsync(h->d_flag, 0, kFlagBytes, s));
+  unsigned long long* out = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(h->d_flag) + 16);
+  const int gb = (int)(h->n / 1024 + 1 < 148 * 8 ? h->n / 1024 + 1 : 148 * 8);
+  k_pattern_hash<<<gb, 256, 0, s>>>(h->D.a_offs, h->D.a_cols, h->n, 0x51ull, out);
+  if (h->pre == SG_PRECOND_LEARNED) {
+    k_pattern_hash<<<gb, 256, 0, s>>>(h->D.g_offs, h->D.g_cols, h->n, 0x52ull, out + 1);
+    k_pattern_hash<<<gb, 256, 0, s>>>(h->D.gt_offs, h->D.gt_cols, h->n, 0x53ull, out + 2);
+  }
+  SG_LAUNCH_CHECK("k_pattern_hash");
+  h->kernels += h->pre == SG_PRECOND_LEARNED ? 3 : 1;
+  return SG_OK;
+}
+
+// Re-plan a handle whose patterns changed under it: a fresh handle on the same pointers takes
+// over (user settings carried), the old resources are released.
+int rebuild(sg_pcg* h, cudaStream_t s) {
+  if (h->dist) {
+    set_error("the sparsity pattern of a row-partitioned PCG handle changed; create a new handle");
+    return SG_EINVAL;
+  }
+  sg_pcg* nh = nullptr;
+  int rc = sg_pcg_create(&nh, h->S, h->sys_start.data(), h->D.a_offs, h->D.a_cols, h->D.a_vals, h->pre,
+                         h->D.g_offs, h->D.g_cols, h->D.g_vals, h->D.gt_offs, h->D.gt_cols, h->D.gt_vals,
+                         h->D.inv_diag, h->eps, s);
+  if (rc) return rc;
+  nh->profile = h->profile;
+  nh->kernels = h->kernels;
+  nh->chunks = h->chunks;
+  for (int k = 0; k < 3; ++k) nh->prof_ms[k] = h->prof_ms[k];
+  nh->prof_active = h->prof_active;
+  nh->prof_samples = h->prof_samples;
+  nh->rebuilds = h->rebuilds + 1;
+  const double* cu = h->coef_user;
+  const int64_t nx = h->st_nx, ny = h->st_ny;
+  std::swap(*h, *nh);
+  sg_pcg_destroy(nh);
+  if (cu) {
+    int32_t ok = 0;
+    rc = sg_pcg_set_stencil(h, cu, nx, ny, &ok);
+  }
+  return rc;
+}
+}  // namespace
+
 extern "C" int sg_pcg_create(sg_pcg** out, int32_t n_systems, const int64_t* sys_row_start_host,
                              const int32_t* a_offs, const int32_t* a_cols, const double* a_vals,
                              int precond_kind, const int32_t* g_offs, const int32_t* g_cols,
@@ -2617,10 +2703,14 @@ extern "C" int sg_pcg_create(sg_pcg** out, int32_t n_systems, const int64_t* sys
   if (h->staged) {
     const char* kv = getenv("SG_PCG_K23");
     // the sliding window takes the mirror of diagonal d as ND-1-d: only for full diagonal sets
-    const bool full = h->dia_nd == 5 || h->dia_nd == 7 || h->dia_nd == 8;
+    // ring_nb / the compile-time mirror ND-1-d need a sorted set with off[d] == -off[ND-1-d]
+    // (and 0 in the middle for odd ND); setup_dia guarantees it, checked here where it is relied on
+    bool mirrored = true;
+    for (int d = 0; d < h->dia_nd; ++d) mirrored = mirrored && h->D.dia.off[d] == -h->D.dia.off[h->dia_nd - 1 - d];
+    const bool full = mirrored && (h->dia_nd == 5 || h->dia_nd == 7 || h->dia_nd == 8);
     h->k23 = (kv && kv[0] == 't') || !full ? 0 : 1;
     const char* k1v = getenv("SG_PCG_K1");
-    h->k1sw = (k1v && k1v[0] == 't') || !(h->dia_nd == 5 || h->dia_nd == 7) ? 0 : 1;
+    h->k1sw = (k1v && k1v[0] == 't') || !mirrored || !(h->dia_nd == 5 || h->dia_nd == 7) ? 0 : 1;
     // deferred x update: both sliding-window kernels, learned factor, one rank
     const char* sv2 = getenv("SG_PCG_SMALL");
     long long maxrows = 0;
@@ -2629,6 +2719,17 @@ extern "C" int sg_pcg_create(sg_pcg** out, int32_t n_systems, const int64_t* sys
     const char* xv = getenv("SG_PCG_XDEFER");
     h->D.xdefer = (xv && xv[0] == '1') && h->k1sw && h->k23 == 1 && !h->strip &&
                   h->pre == SG_PRECOND_LEARNED ? 1 : 0;
+  }
+  SG_CUDA(cudaMalloc(&h->d_flag, kFlagBytes));
+  {
+    const int64_t k0 = h->kernels;
+    int rc = pattern_hashes(h, s);
+    if (rc) { sg_pcg_destroy(h); return rc; }
+    h->kernels = k0;
+    unsigned char fb[kFlagBytes];
+    SG_CUDA(cudaMemcpyAsync(fb, h->d_flag, kFlagBytes, cudaMemcpyDeviceToHost, s));
+    SG_CUDA(cudaStreamSynchronize(s));
+    memcpy(h->pat_hash, fb + 16, sizeof(h->pat_hash));
   }
   SG_CUDA(cudaStreamSynchronize(s));
   *out = h;
@@ -2654,15 +2755,20 @@ extern "C" int sg_pcg_solve(sg_pcg* h, const double* b, double* x, const sg_solv
     h->chunk = chunk;
     h->period = period;
   }
+  // the patterns the handle was planned on must still be the caller's (see k_pattern_hash)
+  {
+    int rc0 = pattern_hashes(h, s);
+    if (rc0) return rc0;
+  }
   // DIA: (re)build the diagonal-major values from the CSR arrays (values may change between
   // solves: a new G from the GNN, a refilled A)
   if (h->dia_nd) {
     const int gb = (int)(h->n / 256 + 1 < 148 * 16 ? h->n / 256 + 1 : 148 * 16);
-    k_csr_to_dia<<<gb, 256, 0, s>>>(h->D.a_offs, h->D.a_cols, h->D.a_vals, h->n, h->D.dia, h->dia_a, h->dia_mask);
+    k_csr_to_dia<<<gb, 256, 0, s>>>(h->D.a_offs, h->D.a_cols, h->D.a_vals, h->n, h->D.dia, h->dia_a, h->dia_mask,
+                                    h->d_flag + 2);
     if (h->pre == SG_PRECOND_LEARNED)
-      k_csr_to_dia<<<gb, 256, 0, s>>>(h->D.g_offs, h->D.g_cols, h->D.g_vals, h->n, h->D.dia, h->dia_g, nullptr);
-    if (!h->d_flag) SG_CUDA(cudaMalloc(&h->d_flag, 2 * sizeof(unsigned int)));
-    SG_CUDA(cudaMemsetAsync(h->d_flag, 0, 2 * sizeof(unsigned int), s));
+      k_csr_to_dia<<<gb, 256, 0, s>>>(h->D.g_offs, h->D.g_cols, h->D.g_vals, h->n, h->D.dia, h->dia_g, nullptr,
+                                      h->d_flag + 2);
     k_dia_symcheck<<<gb, 256, 0, s>>>(h->D.dia, h->d_flag);
     SG_LAUNCH_CHECK("k_csr_to_dia / k_dia_symcheck");
     h->kernels += h->pre == SG_PRECOND_LEARNED ? 3 : 2;
@@ -2672,9 +2778,27 @@ extern "C" int sg_pcg_solve(sg_pcg* h, const double* b, double* x, const sg_solv
       SG_LAUNCH_CHECK("k_stencil_check");
       h->kernels += 1;
     }
-    unsigned int flags[2] = {1u, 1u};
-    SG_CUDA(cudaMemcpyAsync(flags, h->d_flag, sizeof(flags), cudaMemcpyDeviceToHost, s));
-    SG_CUDA(cudaStreamSynchronize(s));
+  }
+  unsigned char fb[kFlagBytes];
+  SG_CUDA(cudaMemcpyAsync(fb, h->d_flag, kFlagBytes, cudaMemcpyDeviceToHost, s));
+  SG_CUDA(cudaStreamSynchronize(s));
+  unsigned int flags[4];
+  unsigned long long hs[3];
+  memcpy(flags, fb, sizeof(flags));
+  memcpy(hs, fb + 16, sizeof(hs));
+  if (hs[0] != h->pat_hash[0] || hs[1] != h->pat_hash[1] || hs[2] != h->pat_hash[2]) {
+    // the index buffers were refilled with another pattern: re-plan the handle, solve again
+    int rc0 = rebuild(h, s);
+    if (rc0) return rc0;
+    SG_CUDA(cudaEventDestroy(e0));
+    SG_CUDA(cudaEventDestroy(e1));
+    return sg_pcg_solve(h, b, x, cfg, results_host, elapsed_ns_host, stream);
+  }
+  if (h->dia_nd && flags[2]) {
+    set_error("a stored entry lies outside the handle's diagonal set (pattern changed without a rebuild)");
+    return SG_EINVAL;
+  }
+  if (h->dia_nd) {
     const int sym = flags[0] ? 0 : 1;
     const int cst = (h->coef && sym && !flags[1]) ? 1 : 0;
     if (sym != h->a_sym || cst != h->cst) {  // kernel variant changes: captured graphs are stale
@@ -2849,8 +2973,11 @@ extern "C" int sg_pcg_set_stencil(sg_pcg* h, const double* coeff, int64_t nx, in
   if (!h) { set_error("null handle"); return SG_EINVAL; }
   if (usable_host) *usable_host = 0;
   const Dia& dd = h->D.dia;
-  const bool fits = coeff && nx > 1 && ny >= 1 && h->dia_nd == 5 && !h->dist && dd.off[1] == -1 && dd.off[2] == 0 &&
-                    dd.off[3] == 1 && dd.off[4] == -dd.off[0] && (int64_t)dd.off[4] == nx;
+  // only the streamed K1 (k_iter1_sw) regenerates A: one-CTA small systems, the tile and strip
+  // kernels and the row partition keep the stored diagonals (no per-solve copy + check for them)
+  const bool fits = coeff && nx > 1 && ny >= 1 && h->dia_nd == 5 && !h->dist && h->staged && h->k1sw && !h->small &&
+                    dd.off[1] == -1 && dd.off[2] == 0 && dd.off[3] == 1 && dd.off[4] == -dd.off[0] &&
+                    (int64_t)dd.off[4] == nx;
   const double ihx2 = (double)((nx + 1) * (nx + 1)), ihy2 = (double)((ny + 1) * (ny + 1));  // datasets.py:109-110
   if (fits && h->coef && h->D.ihx2 == ihx2 && h->D.ihy2 == ihy2) {  // only the source array moves
     h->coef_user = coeff;
@@ -2875,11 +3002,19 @@ extern "C" int sg_pcg_set_stencil(sg_pcg* h, const double* coeff, int64_t nx, in
     h->coef = base + h->guard;
   }
   h->coef_user = coeff;
+  h->st_nx = nx;
+  h->st_ny = ny;
   h->D.coef = h->coef;
   h->D.ihx2 = ihx2;
   h->D.ihy2 = ihy2;
   h->cst = 0;  // verified against A at every solve
   if (usable_host) *usable_host = 1;
+  return SG_OK;
+}
+
+extern "C" int sg_pcg_rebuilds(sg_pcg* h, int64_t* rebuilds_host) {
+  if (!h || !rebuilds_host) { set_error("null handle"); return SG_EINVAL; }
+  *rebuilds_host = h->rebuilds;
   return SG_OK;
 }
 

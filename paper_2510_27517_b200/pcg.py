@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import ctypes as C
 import json
+import math
 import time
 from dataclasses import dataclass, field
 
@@ -137,7 +138,16 @@ class PcgHandle:
         k, c = C.c_int64(0), C.c_int64(0)
         prof = (C.c_double * 8)()
         L.check(L.lib().sg_pcg_stats(self._h, C.byref(k), C.byref(c), prof, 1 if reset else 0))
+        if reset:
+            self._prof_last = [0.0] * 8
         return int(k.value), int(c.value), list(prof)
+
+    def rebuilds(self) -> int:
+        """How many times a solve found the patterns behind the handle's pointers changed and
+        re-planned the handle (sg_pcg_rebuilds)."""
+        r = C.c_int64(0)
+        L.check(L.lib().sg_pcg_rebuilds(self._h, C.byref(r)))
+        return int(r.value)
 
     def history(self, sys: int, length: int) -> list:
         out = np.empty(max(length, 0), dtype=np.float64)
@@ -160,34 +170,45 @@ class PcgHandle:
 _HANDLES: "OrderedDict" = None
 _MAX_HANDLES = 4
 
+# the built-in preconditioners the fused solver runs natively, and the class whose `apply` it
+# stands in for; a subclass that overrides `apply` (e.g. the reference's CountingIdentity,
+# pkg/tests/test_pcg.py:50-57) is NOT fused -- its own apply runs every iteration (generic path)
+_FUSED = ((LearnedSpaiPreconditioner, "learned"), (FsaiPreconditioner, "fsai"),
+          (JacobiPreconditioner, "jacobi"), (IdentityPreconditioner, "identity"))
 
-def _handle_for(A: SparseMatrix, M: Preconditioner) -> PcgHandle:
+
+def _fused_kind(M: Preconditioner):
+    for cls, name in _FUSED:
+        if isinstance(M, cls):
+            return name if type(M).apply is cls.apply else None
+    return None
+
+
+def _handle_for(A: SparseMatrix, M: Preconditioner, kind_name: str | None = None) -> PcgHandle:
     """Solver handle for (A, M).  Handles are cached per (patterns, kind, epsilon): a new factor
     on the same pattern (a new GNN output) or new A values only re-point the handle
-    (`sg_pcg_rebind_values`), keeping its workspace and captured graphs."""
+    (`sg_pcg_rebind_values`), keeping its workspace and captured graphs.  A pattern refilled
+    behind the same pointers is caught by the handle itself (sg_pcg_rebuilds)."""
     global _HANDLES
     from collections import OrderedDict
+    if kind_name is None:
+        kind_name = _fused_kind(M)
+        if kind_name is None:
+            raise TypeError(f"{type(M).__name__} runs the generic path; it has no fused handle")
     if _HANDLES is None:
         _HANDLES = OrderedDict()
     a = A.device()
     starts = np.array([0, A.n_rows], dtype=np.int64)
-    if isinstance(M, LearnedSpaiPreconditioner):
-        if M.n != A.n_rows:
-            raise ValueError(f"dimension mismatch: operator is {M.n}, matrix is {A.n_rows}")
-        g, gt, inv, kind, eps = M.factor.device(), M.factor_t(), None, L.PRECOND_LEARNED, M.epsilon
-    elif isinstance(M, FsaiPreconditioner):  # M^{-1} = G^T G = F F^T with F = G^T, eps 0
-        if M.n != A.n_rows:
-            raise ValueError(f"dimension mismatch: operator is {M.n}, matrix is {A.n_rows}")
-        (g, gt), inv, kind, eps = M.factor_pair(), None, L.PRECOND_LEARNED, 0.0
-    elif isinstance(M, JacobiPreconditioner):
-        g, gt, inv, kind, eps = None, None, M.inv_diag_dev, L.PRECOND_JACOBI, 0.0
-    elif isinstance(M, IdentityPreconditioner):
-        g, gt, inv, kind, eps = None, None, None, L.PRECOND_IDENTITY, 0.0
-    else:
-        raise TypeError(f"preconditioner {type(M).__name__} is not supported by the fused GPU solver "
-                        "(supported: learned SPAI, FSAI, Jacobi, identity)")
-    if isinstance(M, JacobiPreconditioner) and M.n != A.n_rows:
+    if M.n != A.n_rows:
         raise ValueError(f"dimension mismatch: operator is {M.n}, matrix is {A.n_rows}")
+    if kind_name == "learned":
+        g, gt, inv, kind, eps = M.factor.device(), M.factor_t(), None, L.PRECOND_LEARNED, M.epsilon
+    elif kind_name == "fsai":  # M^{-1} = G^T G = F F^T with F = G^T, eps 0
+        (g, gt), inv, kind, eps = M.factor_pair(), None, L.PRECOND_LEARNED, 0.0
+    elif kind_name == "jacobi":
+        g, gt, inv, kind, eps = None, None, M.inv_diag_dev, L.PRECOND_JACOBI, 0.0
+    else:
+        g, gt, inv, kind, eps = None, None, None, L.PRECOND_IDENTITY, 0.0
     pat = lambda d: (None if d is None else (d.offs.data_ptr(), d.cols.data_ptr(), d.n_rows, d.nnz))  # noqa: E731
     key = (pat(a), pat(g), pat(gt), kind, eps)
     h = _HANDLES.get(key)
@@ -198,24 +219,168 @@ def _handle_for(A: SparseMatrix, M: Preconditioner) -> PcgHandle:
         _HANDLES.move_to_end(key)
         return h
     h = PcgHandle(a, starts, kind, g, gt, inv, eps)
+    h.set_profile(True)  # in-graph event nodes: the apply's device time (t_apply_total_ns)
     _HANDLES[key] = h
     while len(_HANDLES) > _MAX_HANDLES:
         _HANDLES.popitem(last=False)[1].close()
     return h
 
 
-def report_from(res, x, hist, t_construct_ns, elapsed_ns):
+def report_from(res, x, hist, t_construct_ns, elapsed_ns, t_apply_ns=0):
     if res.status == L.SG_ENOTSPD:
         raise NotSpdError(_FAIL_MSG[res.fail_kind], int(res.fail_iter), float(res.fail_value))
     return SolveReport(x=x, k=int(res.k), converged=bool(res.converged), t_construct_ns=t_construct_ns,
-                       t_apply_total_ns=0, t_cg_total_ns=int(elapsed_ns), residual_history=hist)
+                       t_apply_total_ns=int(t_apply_ns), t_cg_total_ns=max(0, int(elapsed_ns) - int(t_apply_ns)),
+                       residual_history=hist)
+
+
+def _fused_apply_ns(h: PcgHandle, kind_name: str, k: int) -> int:
+    """Device time of the preconditioner apply inside the fused solve.  The apply has no kernel
+    of its own there: it is the G^T / G half of the fused K2+K3 kernel (or K2 + K3 unfused; K3
+    alone for Jacobi / identity), sampled by the handle's in-graph event nodes on one iteration
+    per graph chunk and scaled to the 1 + k applies the reference times (pcg.py:166-195).  The
+    whole-iteration kernels include the r / x updates fused with the apply, so this is an upper
+    bound; one-CTA small systems (no per-kernel events) report 0."""
+    _, _, prof = h.stats()
+    last = getattr(h, "_prof_last", [0.0] * 8)
+    h._prof_last = prof
+    samples = prof[4] - last[4]
+    if samples <= 0:
+        return 0
+    d = [prof[j] - last[j] for j in range(3)]
+    fused = bool(prof[7])
+    ms = (d[1] + d[2]) if (fused or kind_name in ("learned", "fsai")) else d[2]
+    return int(max(ms, 0.0) / samples * (1 + k) * 1e6)
+
+
+class _Dev:
+    """Device vector kernels of the generic path (C-ABI; the reference's roundings)."""
+
+    def __init__(self, A: SparseMatrix):
+        import torch
+        self.a = A.device()
+        self.n = A.n_rows
+        self.lib = L.lib()
+        self.fn = self.lib.sg_spmv_warp if self.a.nnz >= 32 * max(self.n, 1) else self.lib.sg_spmv
+        self.scal = L.empty(1, torch.float64)
+        self.ws, self.wsb = L.workspace(self.lib.sg_dot, None, None, 0, None)
+
+    def spmv(self, x, out):
+        L.check(self.fn(self.n, L.ptr(self.a.offs), L.ptr(self.a.cols), L.ptr(self.a.vals), L.ptr(x), L.ptr(out),
+                        L.stream_ptr()))
+        return out
+
+    def axpby(self, out, a, b, c, mode):  # out = a + c b (mode 0) / a - c b (mode 1)
+        L.check(self.lib.sg_axpby(L.ptr(out), L.ptr(a), L.ptr(b), float(c), self.n, mode, L.stream_ptr()))
+        return out
+
+    def dot(self, x, y) -> float:
+        L.check(self.lib.sg_dot(L.ptr(x), L.ptr(y), self.n, L.ptr(self.scal), L.ptr(self.ws), C.byref(self.wsb),
+                                L.stream_ptr()))
+        return float(self.scal.item())
+
+
+def _pcg_generic(A: SparseMatrix, b, M: Preconditioner, cfg: SolveConfig, was_t: bool) -> SolveReport:
+    """pcg.py:131-233 for any `Preconditioner`: vectors, SpMVs, updates and dot products on the
+    GPU (the reference's roundings and summation orders; dot products in a fixed device order),
+    and the caller's own `M.apply` every iteration -- handed a host numpy vector as the reference
+    contract says (precond.py:42-59), or the device tensor when `M.device_apply` is true.  One
+    host round trip per scalar: this is the general (slow) path; the built-in preconditioners
+    run fused and device-resident instead."""
+    import torch
+    n = A.n_rows
+    ops = _Dev(A)
+    max_iters = 20 * n if cfg.max_iters is None else cfg.max_iters
+    period = cfg.residual_refresh_period
+    use_true = cfg.termination == "true_residual"
+    dev_apply = bool(getattr(M, "device_apply", False))
+    t_solve0 = time.perf_counter_ns()
+    t_apply = 0
+    bd = b.to(device=L.device(), dtype=torch.float64).contiguous() if was_t else \
+        L.to_device(np.asarray(b, dtype=np.float64), torch.float64)
+
+    def apply(r):
+        nonlocal t_apply
+        t0 = time.perf_counter_ns()
+        s = M.apply(r if dev_apply else r.cpu().numpy())
+        if isinstance(s, torch.Tensor):
+            s = s.to(device=L.device(), dtype=torch.float64).contiguous()
+        else:
+            s = np.asarray(s, dtype=np.float64)
+            if s.shape != (n,):
+                raise ValueError(f"preconditioner returned shape {s.shape}, expected ({n},)")
+            s = L.to_device(s, torch.float64)
+        t_apply += time.perf_counter_ns() - t0
+        return s
+
+    norm_b = math.sqrt(ops.dot(bd, bd))
+    x = L.zeros(n, torch.float64)
+    out_x = (lambda v: v) if was_t else (lambda v: v.cpu().numpy())
+    if norm_b == 0.0:
+        return SolveReport(out_x(x), 0, True, M.t_construct_ns, 0, 0, [0.0] if cfg.track_history else None)
+    tmp = L.empty(n, torch.float64)
+    r = ops.axpby(L.empty(n, torch.float64), bd, ops.spmv(x, tmp), 1.0, 1)
+    d = apply(r)
+    delta_new = ops.dot(r, d)
+    if delta_new < 0.0:
+        raise NotSpdError(_FAIL_MSG[2], 0, delta_new)
+    delta_0 = delta_new
+    history = [math.sqrt(ops.dot(r, r)) / norm_b]
+    q = L.empty(n, torch.float64)
+    i, converged = 0, False
+    while i < max_iters:
+        if not use_true and delta_new <= cfg.rtol ** 2 * delta_0:
+            break
+        ops.spmv(d, q)
+        dq = ops.dot(d, q)
+        if dq <= 0.0:
+            raise NotSpdError(_FAIL_MSG[1], i, dq)
+        alpha = delta_new / dq
+        ops.axpby(x, x, d, alpha, 0)
+        refreshed = i > 0 and i % period == 0
+        if refreshed:
+            ops.axpby(r, bd, ops.spmv(x, tmp), 1.0, 1)
+        else:
+            ops.axpby(r, r, q, alpha, 1)
+        s = apply(r)
+        delta_old = delta_new
+        delta_new = ops.dot(r, s)
+        if delta_new < 0.0:
+            raise NotSpdError(_FAIL_MSG[2], i, delta_new)
+        beta = delta_new / delta_old
+        d = ops.axpby(L.empty(n, torch.float64), s, d, beta, 0)
+        i += 1
+        rel = math.sqrt(ops.dot(r, r)) / norm_b
+        history.append(rel)
+        if use_true and rel <= cfg.rtol:
+            if refreshed:
+                converged = True
+                break
+            rf = ops.axpby(L.empty(n, torch.float64), bd, ops.spmv(x, tmp), 1.0, 1)
+            rel_fresh = math.sqrt(ops.dot(rf, rf)) / norm_b
+            history[-1] = rel_fresh
+            if rel_fresh <= cfg.rtol:
+                converged = True
+                break
+            r = rf
+    if not use_true and not converged:
+        rf = ops.axpby(L.empty(n, torch.float64), bd, ops.spmv(x, tmp), 1.0, 1)
+        converged = math.sqrt(ops.dot(rf, rf)) / norm_b <= cfg.rtol
+    t_total = time.perf_counter_ns() - t_solve0
+    return SolveReport(out_x(x), i, converged, M.t_construct_ns, t_apply, t_total - t_apply,
+                       history if cfg.track_history else None)
 
 
 def pcg_solve(A: SparseMatrix, b, M: Preconditioner, cfg: SolveConfig | None = None) -> SolveReport:
     """pcg.py:131-233 on the GPU.  Returns x as numpy (or as a device tensor if b was one).
 
-    t_cg_total_ns is the device time of the whole solve; the apply is fused into the iteration
-    kernels, so t_apply_total_ns is reported as 0 (its cost is inside t_cg_total_ns).
+    The built-in preconditioners (learned SPAI, FSAI, Jacobi, identity -- exactly those classes,
+    or subclasses that keep their `apply`) run in the fused, device-resident solver:
+    t_cg_total_ns + t_apply_total_ns is the device time of the whole solve, and since the apply
+    has no kernel of its own there, t_apply_total_ns is the sampled device time of the kernels
+    that apply it (see `_fused_apply_ns`).  Any other `Preconditioner` (a user subclass, or one
+    overriding `apply`) runs the generic path, which calls its `apply` every iteration like the
+    reference does.
     """
     import torch
     if cfg is None:
@@ -227,14 +392,20 @@ def pcg_solve(A: SparseMatrix, b, M: Preconditioner, cfg: SolveConfig | None = N
     bn = b.shape[0] if was_t else len(np.asarray(b))
     if bn != n:
         raise ValueError(f"dimension mismatch: matrix is {n}, rhs is {bn}")
+    if not isinstance(M, Preconditioner) and not callable(getattr(M, "apply", None)):
+        raise TypeError(f"{type(M).__name__} is not a Preconditioner")
     if n == 0:
         hist = [0.0] if cfg.track_history else None
         return SolveReport(np.zeros(0), 0, True, M.t_construct_ns, 0, 0, hist)
-    h = _handle_for(A, M)
+    kind_name = _fused_kind(M) if isinstance(M, Preconditioner) else None
+    if kind_name is None:
+        return _pcg_generic(A, b, M, cfg, was_t)
+    h = _handle_for(A, M, kind_name)
     b_dev = b.to(device=L.device(), dtype=torch.float64).contiguous() if was_t else \
         L.to_device(np.asarray(b, dtype=np.float64), torch.float64)
     x_dev = L.empty(n, torch.float64)
     (res,) = h.solve(b_dev, x_dev, cfg)
     hist = h.history(0, int(res.hist_len)) if cfg.track_history else None
+    t_apply = _fused_apply_ns(h, kind_name, int(res.k))
     x = x_dev if was_t else x_dev.cpu().numpy()
-    return report_from(res, x, hist, M.t_construct_ns, h.last_elapsed_ns)
+    return report_from(res, x, hist, M.t_construct_ns, h.last_elapsed_ns, t_apply)
