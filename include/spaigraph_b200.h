@@ -242,6 +242,14 @@ void sg_pcg_destroy(sg_pcg* h);
 int sg_pcg_rebind_values(sg_pcg* h, const double* a_vals, const double* g_vals, const double* gt_vals,
                          const double* inv_diag);
 
+/* Re-point a handle at other arrays of the same SIZES (index arrays too: a new G^T, a refilled
+ * matrix).  The next sg_pcg_solve fingerprints the patterns behind the pointers and re-plans the
+ * handle only if they differ from the ones it was planned on (sg_pcg_rebuilds). */
+int sg_pcg_rebind(sg_pcg* h, const int32_t* a_offs, const int32_t* a_cols, const double* a_vals,
+                  const int32_t* g_offs, const int32_t* g_cols, const double* g_vals,
+                  const int32_t* gt_offs, const int32_t* gt_cols, const double* gt_vals,
+                  const double* inv_diag);
+
 /* Instrumentation (no reference counterpart; pcg.py:155-229 only times apply / total on the
  * host).  With profiling on, every chunk graph brackets K1, K2, K3 of one non-refresh
  * iteration with external event-record nodes; sg_pcg_stats returns the summed device times
@@ -318,25 +326,64 @@ int sg_fsai_build(int64_t n, const int32_t* a_offs, const int32_t* a_cols, const
 int sg_adamw(int64_t n, double* params, const double* grads, double* m, double* v, double lr, double wd,
              double beta1, double beta2, double eps, int64_t t, double grad_div, void* stream);
 
-/* ---- row-partitioned solve of ONE system over several ranks ----------
- * A rank holds an EXTENDED local system: its owned rows [own_lo, own_hi) plus ghost rows on
- * either side (the neighbours' boundary rows), as one local CSR (pcg_solve's own arguments
- * otherwise).  Tiles and dot products cover the owned rows only; before every kernel that
- * reads neighbour rows the ghosts are refreshed by an NCCL send/recv group, and every scalar
- * the reference's control flow needs is an NCCL all-reduce followed by the finaliser kernel —
- * all captured in the same CUDA graphs as the iteration kernels (no host round trip per
- * iteration).  libnccl is opened at run time.  Replaces the host loop of rowpart.DistPcg. */
-int sg_nccl_unique_id(void* out128);
-int sg_nccl_comm_init(void** comm_out, const void* id128, int32_t world, int32_t rank);
-int sg_nccl_comm_destroy(void* comm);
-int sg_pcg_create_part(sg_pcg** out, int64_t n_ext, int64_t own_lo, int64_t own_hi,
-                       const int32_t* a_offs, const int32_t* a_cols, const double* a_vals,
-                       int precond_kind, const int32_t* g_offs, const int32_t* g_cols,
-                       const double* g_vals, const int32_t* gt_offs, const int32_t* gt_cols,
-                       const double* gt_vals, const double* inv_diag, double epsilon, void* stream);
-/* comm: ncclComm_t (NULL = single rank, no communication); left/right: neighbour ranks or -1;
- * ghost_lo/hi: ghost rows below own_lo / above own_hi (= the neighbours' boundary rows sent). */
-int sg_pcg_set_comm(sg_pcg* h, void* comm, int32_t left, int32_t right, int64_t ghost_lo, int64_t ghost_hi);
+/* ---- row partition of ONE system (SURVEY.md §8(e)(ii), config C5 over 2/4/8 GPUs) ----------
+ * Design: the system's rows are split into contiguous blocks; partition p holds an
+ * EXTENDED local system = its owned rows plus ghost rows on either side, 3 half-bandwidths deep
+ * (for a grid: 3 lines).  Every PCG kernel runs over the whole extended system exactly as for an
+ * independent system -- the fused sliding-window / strip kernels included -- except that only
+ * owned rows enter the dot products and write s, and the first / last owned rows of s are ALSO
+ * stored into the neighbours' ghost rows from inside the kernel that computes them.  With 3
+ * ghost layers every other vector (d, q, r, x) stays exact on the ghost rows the next kernels
+ * read by redundant computation, so one halo per iteration is all the communication besides the
+ * two scalar reductions, which combine the partitions' sums in partition order (bit-identical
+ * results for any placement of the partitions).
+ *
+ * group mode: all partitions are systems of ONE handle (one GPU: the emulation of P ranks that
+ * the tests run; every kernel covers every partition, so no kernel ever waits for another).
+ * own_lo/own_hi (host, n_systems entries) are the owned rows relative to each system's first
+ * row; the neighbours of partition p are systems p-1 and p+1. */
+int sg_pcg_set_partition(sg_pcg* h, const int64_t* own_lo_host, const int64_t* own_hi_host);
+
+/* peer mode: one partition per rank (one process per GPU), the handle holds one system.  Each
+ * rank exports an opaque blob (sg_pcg_peer_info_size() bytes: CUDA IPC handles of its
+ * workspace and reduction block, the byte offset of s, its extended size and owned rows); the
+ * blobs of all ranks are exchanged out of band (torch.distributed all_gather); sg_pcg_set_peers
+ * maps the neighbours' workspaces and every rank's reduction block.  The s halo is then written
+ * straight into the neighbours' ghost rows over NVLink by the kernels, and each reduction is
+ * one peer store of two doubles per rank plus a flag (release / acquire at system scope)
+ * polled by one thread per rank -- no host round trip, no collective library call. */
+int sg_pcg_peer_info_size(void);
+int sg_pcg_peer_export(sg_pcg* h, int64_t own_lo, int64_t own_hi, int32_t world, void* info_out);
+int sg_pcg_set_peers(sg_pcg* h, int32_t rank, int32_t world, const void* infos);
+
+/* Rows [r0, r1) of a CSR matrix restricted to columns [c0, c1) (stored as col - c0 + col_base),
+ * storage order kept: a row partition's extended local system / a GNN block (no reference
+ * counterpart).  out_offs (r1 - r0 + 1 entries) starts at entry_base; out_src[k] = source entry
+ * index of kept entry k (values gather with sg_gather_f64; may be NULL).  out_offs == NULL: only
+ * count into *out_nnz_host.  Synchronizes when out_nnz_host != NULL. */
+int sg_csr_row_block(const int32_t* offs, const int32_t* cols, int64_t r0, int64_t r1, int64_t c0,
+                     int64_t c1, int64_t col_base, int64_t entry_base, int32_t* out_offs,
+                     int32_t* out_cols, int32_t* out_src, int64_t* out_nnz_host, void* ws,
+                     size_t* ws_bytes, void* stream);
+
+/* build_graph features (graphfeat.py:63-105) of a block of rows of a larger matrix: block row
+ * li is global row grow0 + li of an n_global-row matrix (PDE grid coordinates and the rowsum / n
+ * feature use the global matrix); offs/cols/vals are the block's own CSR (columns block-local),
+ * coeff the block's slice of the node field, norm the GLOBAL norm (device scalar). */
+int sg_graph_features_block(int64_t n_block, int64_t grow0, int64_t n_global, const int32_t* offs,
+                            const int32_t* cols, const double* vals, const double* norm, int family,
+                            int64_t nx, int64_t ny, const double* coeff, double coeff_mean,
+                            double* node_out, double* edge_out, void* stream);
+
+/* mean_abs_nonzero_norm / matrix_norm over values held by several ranks, still exact: each rank
+ * accumulates its values into a transferable accumulator (sg_norm_acc_size() uint64: limbs of
+ * the exact fixed-point sum with carries propagated, inf and nan counts); the ranks add their
+ * accumulators limb by limb (an integer all-reduce) and sg_norm_from_acc rounds once, so the
+ * norm is bit-identical to math.fsum over all values (sparse.py:204-213). */
+int sg_norm_acc_size(void);
+int sg_norm_accum(const double* vals, int64_t nnz, int kind, uint64_t* acc_out, void* ws, size_t* ws_bytes,
+                  void* stream);
+int sg_norm_from_acc(const uint64_t* acc, int64_t count, int kind, double* norm_out, void* stream);
 
 #ifdef __cplusplus
 }

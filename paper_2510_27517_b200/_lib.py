@@ -67,6 +67,7 @@ SIGNATURES = {
     "sg_pcg_history": (C.c_int, [vp, i32, vp, i64]),
     "sg_pcg_destroy": (None, [vp]),
     "sg_pcg_rebind_values": (C.c_int, [vp, vp, vp, vp, vp]),
+    "sg_pcg_rebind": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "sg_pcg_set_profile": (C.c_int, [vp, i32]),
     "sg_pcg_rebuilds": (C.c_int, [vp, C.POINTER(C.c_int64)]),
     "sg_pcg_set_stencil": (C.c_int, [vp, vp, i64, i64, C.POINTER(C.c_int32)]),
@@ -80,12 +81,16 @@ SIGNATURES = {
     "sg_outer_sum": (C.c_int, [i64, i32, i32, vp, i32, vp, i32, vp, i32, vp, szp, vp]),
     "sg_adamw": (C.c_int, [i64, vp, vp, vp, vp, f64, f64, f64, f64, f64, i64, f64, vp]),
     "sg_fsai_build": (C.c_int, [i64, vp, vp, vp, vp, vp, vp, C.POINTER(C.c_int64), vp]),
-    "sg_nccl_unique_id": (C.c_int, [vp]),
-    "sg_nccl_comm_init": (C.c_int, [C.POINTER(C.c_void_p), vp, i32, i32]),
-    "sg_nccl_comm_destroy": (C.c_int, [vp]),
-    "sg_pcg_create_part": (C.c_int, [C.POINTER(C.c_void_p), i64, i64, i64, vp, vp, vp, C.c_int, vp, vp, vp, vp, vp,
-                                     vp, vp, f64, vp]),
-    "sg_pcg_set_comm": (C.c_int, [vp, vp, i32, i32, i64, i64]),
+    "sg_pcg_set_partition": (C.c_int, [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "sg_pcg_peer_info_size": (C.c_int, []),
+    "sg_pcg_peer_export": (C.c_int, [vp, i64, i64, i32, vp]),
+    "sg_pcg_set_peers": (C.c_int, [vp, i32, i32, vp]),
+    "sg_csr_row_block": (C.c_int, [vp, vp, i64, i64, i64, i64, i64, i64, vp, vp, vp, C.POINTER(C.c_int64), vp, szp,
+                                   vp]),
+    "sg_graph_features_block": (C.c_int, [i64, i64, i64, vp, vp, vp, vp, C.c_int, i64, i64, vp, f64, vp, vp, vp]),
+    "sg_norm_acc_size": (C.c_int, []),
+    "sg_norm_accum": (C.c_int, [vp, i64, C.c_int, vp, vp, szp, vp]),
+    "sg_norm_from_acc": (C.c_int, [vp, i64, C.c_int, vp, vp]),
 }
 
 _lib = None

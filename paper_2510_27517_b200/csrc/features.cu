@@ -124,8 +124,11 @@ __global__ void k_norm_finish(const unsigned long long* limbs, const unsigned in
   out[sg] = s;
 }
 
-// graphfeat.py:83 and 93-104, for global rows row0 .. row0+n-1 (local index li = i - row0).
-__global__ void k_graph_features(int64_t n, int64_t row0, const int32_t* __restrict__ offs,
+// graphfeat.py:83 and 93-104, for rows row0 .. row0+n-1 (local index li = i - row0) that are rows
+// grow0 + li of a matrix with n_global rows (grid coordinates and rowsum / n use the global
+// matrix: a row partition's block of rows gets exactly the global features).
+__global__ void k_graph_features(int64_t n, int64_t row0, int64_t grow0, int64_t n_global,
+                                 const int32_t* __restrict__ offs,
                                  const int32_t* __restrict__ cols, const double* __restrict__ vals,
                                  const double* __restrict__ norm_p, int family, int64_t nx,
                                  int64_t ny, const double* __restrict__ coeff, double coeff_mean,
@@ -138,7 +141,7 @@ __global__ void k_graph_features(int64_t n, int64_t row0, const int32_t* __restr
     for (int32_t k = lo; k < hi; ++k) edge_out[k] = __ddiv_rn(vals[k], norm);
     if (family == 1) {
       const double hx = __ddiv_rn(1.0, (double)(nx + 1)), hy = __ddiv_rn(1.0, (double)(ny + 1));
-      const int64_t ix = li % nx, iy = li / nx;
+      const int64_t ix = (grow0 + li) % nx, iy = (grow0 + li) / nx;
       node_out[3 * i + 0] = mul((double)(ix + 1), hx);
       node_out[3 * i + 1] = mul((double)(iy + 1), hy);
       node_out[3 * i + 2] = __ddiv_rn(coeff[li], coeff_mean);
@@ -147,10 +150,36 @@ __global__ void k_graph_features(int64_t n, int64_t row0, const int32_t* __restr
       double dg = 0.0;
       for (int32_t k = lo; k < hi; ++k)
         if (cols[k] == (int32_t)i) dg = vals[k];
-      node_out[2 * i + 0] = __ddiv_rn(__ddiv_rn(rs, (double)n), norm);
+      node_out[2 * i + 0] = __ddiv_rn(__ddiv_rn(rs, (double)n_global), norm);
       node_out[2 * i + 1] = __ddiv_rn(dg, norm);
     }
   }
+}
+
+// Exact-sum accumulator in transferable form: carries propagated (every limb < 2^32) plus the
+// inf / nan counts, so accumulators of several row blocks (ranks) can be added limb by limb.
+__global__ void k_norm_export(const unsigned long long* limbs, const unsigned int* flags, unsigned long long* acc) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  unsigned long long c = 0;
+  for (int i = 0; i < NLIMB; ++i) {
+    const unsigned long long t = limbs[i] + c;
+    acc[i] = t & 0xFFFFFFFFull;
+    c = t >> 32;
+  }
+  acc[NLIMB - 1] += c << 32;  // never reached for finite doubles (2304 bits of headroom)
+  acc[NLIMB] = (flags[0] & 1u) ? 1ull : 0ull;
+  acc[NLIMB + 1] = (flags[0] & 2u) ? 1ull : 0ull;
+}
+
+__global__ void k_norm_import(const unsigned long long* acc, int64_t count, int kind, double* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double s;
+  if (acc[NLIMB + 1]) s = __longlong_as_double(0x7ff8000000000000ll);
+  else if (acc[NLIMB]) s = __longlong_as_double(0x7ff0000000000000ll);
+  else s = round_limbs(acc);
+  if (kind == 0) s = __ddiv_rn(s, (double)count);
+  else if (kind == 1) s = __dsqrt_rn(s);
+  *out = s;
 }
 
 // Batched features: every row of a block-diagonal batch, system found by binary search.
@@ -313,7 +342,7 @@ extern "C" int sg_graph_features(int64_t n, int64_t row0, const int32_t* offs, c
                                  double* node_out, double* edge_out, void* stream) {
   if (family == 1 && nx * ny != n) { set_error("meta grid does not match matrix size"); return SG_EINVAL; }
   if (n <= 0) return SG_OK;
-  k_graph_features<<<grid_for(n), 256, 0, as_stream(stream)>>>(n, row0, offs, cols, vals, norm, family,
+  k_graph_features<<<grid_for(n), 256, 0, as_stream(stream)>>>(n, row0, 0, n, offs, cols, vals, norm, family,
                                                                nx, ny, coeff, coeff_mean,
                                                                node_out, edge_out);
   SG_LAUNCH_CHECK("k_graph_features");
@@ -352,5 +381,55 @@ extern "C" int sg_gen_poisson3d(int64_t nx, int64_t ny, int64_t nz, int32_t* off
   if (7 * nx * ny * nz >= (int64_t)INT32_MAX) { set_error("grid too large for int32 indices"); return SG_EINVAL; }
   k_poisson3d<<<grid_for(nx * ny * nz + 1), 256, 0, as_stream(stream)>>>(nx, ny, nz, offs, cols, vals);
   SG_LAUNCH_CHECK("k_poisson3d");
+  return SG_OK;
+}
+
+extern "C" int sg_graph_features_block(int64_t n_block, int64_t grow0, int64_t n_global, const int32_t* offs,
+                                       const int32_t* cols, const double* vals, const double* norm, int family,
+                                       int64_t nx, int64_t ny, const double* coeff, double coeff_mean,
+                                       double* node_out, double* edge_out, void* stream) {
+  if (family == 1 && nx * ny != n_global) { set_error("meta grid does not match matrix size"); return SG_EINVAL; }
+  if (grow0 < 0 || grow0 + n_block > n_global) { set_error("row block outside the matrix"); return SG_EINVAL; }
+  if (n_block <= 0) return SG_OK;
+  k_graph_features<<<grid_for(n_block), 256, 0, as_stream(stream)>>>(n_block, 0, grow0, n_global, offs, cols, vals,
+                                                                     norm, family, nx, ny, coeff, coeff_mean,
+                                                                     node_out, edge_out);
+  SG_LAUNCH_CHECK("k_graph_features (block)");
+  return SG_OK;
+}
+
+extern "C" int sg_norm_acc_size(void) { return NLIMB + 2; }
+
+extern "C" int sg_norm_accum(const double* vals, int64_t nnz, int kind, uint64_t* acc_out, void* ws,
+                             size_t* ws_bytes, void* stream) {
+  Carve c(ws);
+  unsigned long long* limbs = c.take<unsigned long long>(NLIMB);
+  unsigned int* flags = c.take<unsigned int>(1);
+  int64_t* seg = c.take<int64_t>(2);
+  if (!ws) { *ws_bytes = c.off; return SG_OK; }
+  if (kind < 0 || kind > 2) { set_error("unknown norm kind"); return SG_EINVAL; }
+  cudaStream_t s = as_stream(stream);
+  SG_CUDA(cudaMemsetAsync(limbs, 0, NLIMB * sizeof(unsigned long long), s));
+  SG_CUDA(cudaMemsetAsync(flags, 0, sizeof(unsigned int), s));
+  const int64_t h[2] = {0, nnz > 0 ? nnz : 0};
+  SG_CUDA(cudaMemcpyAsync(seg, h, sizeof(h), cudaMemcpyHostToDevice, s));
+  if (nnz > 0) {
+    int bx = (int)ceil_div(nnz, 256);
+    if (bx > 148 * 16) bx = 148 * 16;
+    k_exact_accum<<<dim3(bx, 1), 256, 0, s>>>(vals, seg, kind == 1 ? 1 : 0, limbs, flags);
+    SG_LAUNCH_CHECK("k_exact_accum");
+  }
+  k_norm_export<<<1, 32, 0, s>>>(limbs, flags, reinterpret_cast<unsigned long long*>(acc_out));
+  SG_LAUNCH_CHECK("k_norm_export");
+  return SG_OK;
+}
+
+extern "C" int sg_norm_from_acc(const uint64_t* acc, int64_t count, int kind, double* norm_out,
+                                void* stream) {
+  if (kind < 0 || kind > 2) { set_error("unknown norm kind"); return SG_EINVAL; }
+  if (kind == 0 && count <= 0) { set_error("norm of a matrix with no stored entries"); return SG_EINVAL; }
+  k_norm_import<<<1, 32, 0, as_stream(stream)>>>(reinterpret_cast<const unsigned long long*>(acc), count, kind,
+                                                 norm_out);
+  SG_LAUNCH_CHECK("k_norm_import");
   return SG_OK;
 }

@@ -292,6 +292,35 @@ __global__ void k_scan_counts(const int32_t* __restrict__ counts, int64_t n, int
   for (int64_t i = lo; i < hi; ++i) { offs[i] = (int32_t)acc; acc += counts[i]; }
 }
 
+// Row block of a CSR matrix: rows [r0, r1), entries with r0c <= col < r1c kept (shifted by
+// -r0c + col_base), in storage order.  counts[i] = kept entries of block row i.
+__global__ void k_block_count(const int32_t* __restrict__ offs, const int32_t* __restrict__ cols, int64_t r0,
+                              int64_t nr, int64_t c0, int64_t c1, int32_t* counts) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nr; i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t c = 0;
+    for (int32_t k = offs[r0 + i]; k < offs[r0 + i + 1]; ++k) c += (cols[k] >= c0 && cols[k] < c1) ? 1 : 0;
+    counts[i] = c;
+  }
+}
+
+__global__ void k_block_fill(const int32_t* __restrict__ offs, const int32_t* __restrict__ cols, int64_t r0,
+                             int64_t nr, int64_t c0, int64_t c1, int64_t col_base, int64_t entry_base,
+                             const int32_t* __restrict__ local_offs, int32_t* out_offs, int32_t* out_cols,
+                             int32_t* out_src) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= nr; i += (int64_t)gridDim.x * blockDim.x) {
+    out_offs[i] = (int32_t)(entry_base + local_offs[i]);
+    if (i == nr) continue;
+    int32_t o = local_offs[i];
+    for (int32_t k = offs[r0 + i]; k < offs[r0 + i + 1]; ++k) {
+      const int32_t c = cols[k];
+      if (c < c0 || c >= c1) continue;
+      if (out_cols) out_cols[o] = (int32_t)(c - c0 + col_base);
+      if (out_src) out_src[o] = k;
+      ++o;
+    }
+  }
+}
+
 static int bits_for(uint64_t maxkey) {
   int b = 1;
   while (b < 64 && (maxkey >> b) != 0) ++b;
@@ -563,5 +592,39 @@ extern "C" int sg_csr_transpose(int64_t n_rows, int64_t n_cols, int64_t nnz, con
   k_offsets_from_sorted<<<grid_for(nnz + 1), 256, 0, s>>>(k_out, nnz, n_cols,
                                                           (uint64_t)(n_rows > 0 ? n_rows : 1), offs_t);
   SG_LAUNCH_CHECK("k_offsets_from_sorted");
+  return SG_OK;
+}
+
+extern "C" int sg_csr_row_block(const int32_t* offs, const int32_t* cols, int64_t r0, int64_t r1, int64_t c0,
+                                int64_t c1, int64_t col_base, int64_t entry_base, int32_t* out_offs,
+                                int32_t* out_cols, int32_t* out_src, int64_t* out_nnz_host, void* ws,
+                                size_t* ws_bytes, void* stream) {
+  const int64_t nr = r1 - r0;
+  Carve c(ws);
+  int32_t* counts = c.take<int32_t>(nr > 0 ? nr : 1);
+  int32_t* loc = c.take<int32_t>(nr + 1);
+  unsigned int* big = c.take<unsigned int>(1);
+  if (!ws) { *ws_bytes = c.off; return SG_OK; }
+  if (*ws_bytes < c.off) { set_error("workspace too small"); return SG_EINVAL; }
+  if (nr < 0 || c1 < c0) { set_error("bad row / column range"); return SG_EINVAL; }
+  cudaStream_t s = as_stream(stream);
+  SG_CUDA(cudaMemsetAsync(big, 0, sizeof(unsigned int), s));
+  if (nr > 0) k_block_count<<<grid_for(nr), 256, 0, s>>>(offs, cols, r0, nr, c0, c1, counts);
+  k_scan_counts<<<1, 1024, 0, s>>>(counts, nr, loc, big);
+  SG_LAUNCH_CHECK("k_block_count");
+  if (out_offs) {
+    k_block_fill<<<grid_for(nr + 1), 256, 0, s>>>(offs, cols, r0, nr, c0, c1, col_base, entry_base, loc, out_offs,
+                                                  out_cols, out_src);
+    SG_LAUNCH_CHECK("k_block_fill");
+  }
+  if (out_nnz_host) {
+    int32_t nz = 0;
+    unsigned int hb = 0;
+    SG_CUDA(cudaMemcpyAsync(&nz, loc + nr, sizeof(nz), cudaMemcpyDeviceToHost, s));
+    SG_CUDA(cudaMemcpyAsync(&hb, big, sizeof(hb), cudaMemcpyDeviceToHost, s));
+    SG_CUDA(cudaStreamSynchronize(s));
+    if (hb || entry_base + (int64_t)nz >= (int64_t)INT32_MAX) { set_error("block exceeds the int32 index range"); return SG_EINVAL; }
+    *out_nnz_host = nz;
+  }
   return SG_OK;
 }

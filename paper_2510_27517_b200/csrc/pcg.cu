@@ -29,8 +29,6 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
-#include <dlfcn.h>
-#include <nccl.h>
 #include <map>
 #include <vector>
 
@@ -103,11 +101,29 @@ struct Dev {
   int xdefer;       // sliding-window path: x += alpha d' deferred from K2+K3 to the next K1
   int sell_on;      // CSR path reads A, G^T (bit 1: also G) from their SELL-32 copies
   Sell sa, sg, sgt;
-  // row-partitioned mode (one system over several ranks): the last CTA of a reducing kernel
-  // publishes the rank-local sums into gsum instead of finalising; an in-graph all-reduce and
-  // k_fin_* then run the reference control flow on the global sums, identically on every rank
-  int dist;
-  double* gsum;  // [S][2]
+  // Row partition of ONE system (sg_pcg_set_partition / sg_pcg_set_peers).  Every system of the
+  // handle is then a PARTITION: an extended local system = owned rows [own0, own1) plus ghost
+  // rows on either side (3 half-bandwidths deep).  The kernels run over the whole extended
+  // system as usual; only the owned rows enter the dot products and store s, and the first /
+  // last owned rows of s are also stored into the neighbour partitions' ghost rows (push_lo /
+  // push_hi: the same vector of the same handle in group mode, peer-mapped NVLink memory in peer
+  // mode).  Every other ghost value stays exact by redundant computation.  The
+  // two-scalar reductions combine the partitions' sums in partition order (part_fin).
+  int part;  // 0 = off, 1 = group (all partitions in this handle), 2 = peer (one per rank)
+  const long long* own0;  // [S] owned rows (absolute; = the system's rows when part == 0)
+  const long long* own1;
+  const long long* plo;   // [S] rows pushed down (into partition sys-1's top ghost rows)
+  const long long* phi;   // [S] rows pushed up (into partition sys+1's bottom ghost rows)
+  double* const* push_lo; // [S] destination of own row own0 (nullptr: none)
+  double* const* push_hi; // [S] destination of own row own1 - phi
+  double* gsum;           // group: [S][2] per-partition sums; peer: [2 parity][R][2] (IPC memory)
+  unsigned int* grp;      // group: arrivals of the current reduction
+  int nsys;               // partitions in this handle (group mode)
+  // peer mode (one partition per rank, NVLink peer memory opened with CUDA IPC)
+  int rank, nranks;
+  double* peer_gsum[8];         // every rank's gsum block (own = local)
+  unsigned int* peer_flag[8];   // every rank's flag array [R]: slot q = last epoch rank q published
+  unsigned int* epoch;          // local reduction counter (thread 0 of a reducing CTA)
   // tile table
   const long long* blk_r0;
   const int* blk_sys;
@@ -132,7 +148,7 @@ struct Dev {
   // vectors
   double *b, *x, *r0, *r1, *d0, *d1, *q, *s, *t;
   // reduction scratch
-  double* part;             // [nblk][2]
+  double* pp;               // per-CTA partials [nblk][2]
   unsigned int* counter;    // [S]
   SysState* st;
   Ctl* ctl;
@@ -253,11 +269,12 @@ __device__ __forceinline__ void block_rows(const Dev& D, int& sys, long long& r0
 // `sb0`: the per-system first-CTA table of the launch (tiles, or sliding-window ranges).
 __device__ __forceinline__ bool arrive(const Dev& D, const int* sb0, int sys, double p0, double p1, double* red,
                                        int* flag) {
+  if (D.part == 2) __threadfence_system();  // every thread's s-halo peer stores precede the arrival
   const double a = block_sum(p0, red);
   const double b = block_sum(p1, red);
   if (threadIdx.x == 0) {
-    D.part[2 * blockIdx.x + 0] = a;
-    D.part[2 * blockIdx.x + 1] = b;
+    D.pp[2 * blockIdx.x + 0] = a;
+    D.pp[2 * blockIdx.x + 1] = b;
     __threadfence();
     const unsigned int nb = (unsigned)(sb0[sys + 1] - sb0[sys]);
     const unsigned int old = atomicAdd(&D.counter[sys], 1u);
@@ -276,7 +293,7 @@ __device__ __forceinline__ bool arrive(const Dev& D, int sys, double p0, double 
 __device__ __forceinline__ double gather_partials(const Dev& D, const int* sb0, int sys, int which, double* red) {
   const int b0 = sb0[sys], b1 = sb0[sys + 1];
   double v = 0.0;
-  for (int b = b0 + threadIdx.x; b < b1; b += blockDim.x) v += __ldcg(&D.part[2 * b + which]);
+  for (int b = b0 + threadIdx.x; b < b1; b += blockDim.x) v += __ldcg(&D.pp[2 * b + which]);
   return block_sum(v, red);
 }
 __device__ __forceinline__ double gather_partials(const Dev& D, int sys, int which, double* red) {
@@ -289,11 +306,38 @@ __device__ __forceinline__ void finish(const Dev& D, SysState& S, int conv) {
   atomicSub(&D.ctl->n_active, 1u);
 }
 
-// Row-partitioned mode: hand the rank-local sums to the all-reduce (thread 0 of the last CTA).
-__device__ __forceinline__ void publish(const Dev& D, int sys, double v0, double v1) {
-  D.gsum[2 * sys + 0] = v0;
-  D.gsum[2 * sys + 1] = v1;
-  D.counter[sys] = 0;
+// Owned-row window and s-push targets of one partition (whole system when not partitioned).
+struct Own {
+  long long o0, o1, pl, ph;
+  double* dl;
+  double* dh;
+};
+__device__ __forceinline__ Own own_of(const Dev& D, int sys) {
+  Own w;
+  w.o0 = D.own0[sys];
+  w.o1 = D.own1[sys];
+  if (D.part) {
+    w.pl = D.plo[sys]; w.ph = D.phi[sys]; w.dl = D.push_lo[sys]; w.dh = D.push_hi[sys];
+  } else {
+    w.pl = w.ph = 0; w.dl = w.dh = nullptr;
+  }
+  return w;
+}
+__device__ __forceinline__ bool owned(const Own& w, long long i) { return i >= w.o0 && i < w.o1; }
+// s of an owned row: local store plus the pushes into the neighbours' ghost rows
+__device__ __forceinline__ void store_s(const Dev& D, const Own& w, long long i, double v) {
+  D.s[i] = v;
+  if (w.dl && i - w.o0 < w.pl) w.dl[i - w.o0] = v;
+  if (w.dh && w.o1 - i <= w.ph) w.dh[i - (w.o1 - w.ph)] = v;
+}
+
+__device__ __forceinline__ unsigned int ld_acquire_sys(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned int* p, unsigned int v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 __device__ __forceinline__ void put_hist(const Dev& D, int sys, long long i, double v) {
@@ -396,6 +440,70 @@ __device__ void fin_k3(const Dev& D, int sys, double rs, int refreshed) {
   } else if (S.i >= S.max_iters || rs <= S.rtol2d0) {
     S.status = ST_CERTIFY;
   }
+}
+
+// ------------------------------------------------------------------ partition reductions
+enum { FIN_SETUP1 = 0, FIN_SETUP2 = 1, FIN_K1 = 2, FIN_RR = 3, FIN_K3 = 4, FIN_K23 = 5 };
+
+__device__ void run_fin(const Dev& D, int sys, int kind, double v0, double v1, int arg) {
+  switch (kind) {
+    case FIN_SETUP1: fin_setup1(D, sys, v0); break;
+    case FIN_SETUP2: fin_setup2(D, sys, v0); break;
+    case FIN_K1: fin_k1(D, sys, arg != 0, v0, v1); break;
+    case FIN_RR: fin_rr(D, sys, v0); break;
+    case FIN_K3: fin_k3(D, sys, v0, arg); break;
+    default: D.st[sys].rr = v0; fin_k3(D, sys, v1, arg); break;
+  }
+}
+
+// Thread 0 of the last CTA of partition `sys` to finish a reducing kernel, with the partition's
+// sums (v0, v1).  The reference control flow then runs on the sums over ALL partitions, added
+// in partition order (0.0 + p0 + p1 + ...), identically for every partition:
+//  group (1): the last partition to arrive adds the published sums and finalises every
+//    partition's state (all partitions run in the same launch: no waiting);
+//  peer (2): the partition stores its sums into every rank's gsum (NVLink peer stores, parity
+//    double-buffered by reduction epoch), releases its epoch flag on every rank, waits for all
+//    ranks' flags of this epoch in local memory, and finalises its own state.  The flag also
+//    orders the s-halo peer stores every CTA issued before arriving (arrive fences at system
+//    scope in peer mode).
+__device__ void part_fin(const Dev& D, int sys, int kind, double v0, double v1, int arg) {
+  D.counter[sys] = 0;
+  if (D.part == 1) {
+    D.gsum[2 * sys + 0] = v0;
+    D.gsum[2 * sys + 1] = v1;
+    __threadfence();
+    if (atomicAdd(D.grp, 1u) != (unsigned int)D.nsys - 1u) return;
+    __threadfence();
+    double s0 = 0.0, s1 = 0.0;
+    for (int q = 0; q < D.nsys; ++q) {
+      s0 = add(s0, __ldcg(&D.gsum[2 * q + 0]));
+      s1 = add(s1, __ldcg(&D.gsum[2 * q + 1]));
+    }
+    for (int q = 0; q < D.nsys; ++q) run_fin(D, q, kind, s0, s1, arg);
+    *D.grp = 0u;
+    return;
+  }
+  const unsigned int e = *D.epoch + 1u;
+  *D.epoch = e;
+  const int par = (int)(e & 1u), R = D.nranks, me = D.rank;
+  for (int q = 0; q < R; ++q) {
+    double* g = D.peer_gsum[q] + 2 * (par * R + me);
+    g[0] = v0;
+    g[1] = v1;
+  }
+  __threadfence_system();
+  for (int q = 0; q < R; ++q) st_release_sys(D.peer_flag[q] + me, e);
+  const unsigned int* mine = D.peer_flag[me];
+  for (int q = 0; q < R; ++q)
+    while ((int)(ld_acquire_sys(mine + q) - e) < 0) {
+    }
+  const double* g = D.peer_gsum[me] + 2 * par * R;
+  double s0 = 0.0, s1 = 0.0;
+  for (int q = 0; q < R; ++q) {
+    s0 = add(s0, __ldcv(&g[2 * q + 0]));
+    s1 = add(s1, __ldcv(&g[2 * q + 1]));
+  }
+  run_fin(D, sys, kind, s0, s1, arg);
 }
 
 // ------------------------------------------------------------------ row operators
@@ -572,8 +680,9 @@ struct Fmt {};
   __shared__ int flag;                          \
   int sys; long long r0, r1;                    \
   block_rows(D, sys, r0, r1);                   \
+  const Own ow = own_of(D, sys);                \
   constexpr int RPT = FMT >= 1 ? kRpt : 1;      \
-  (void)T;
+  (void)T; (void)ow;
 
 template <int ORDER, int XM>
 __device__ __noinline__ double row_sell(const double* __restrict__ sv, const int32_t* __restrict__ sc, int len,
@@ -644,12 +753,12 @@ __global__ void __launch_bounds__(PR, FMT >= 1 ? 8 : 1) k_setup1(Dev D) {
     D.d0[i] = 0.0;
     D.d1[i] = 0.0;
     D.x[i] = 0.0;
-    pbb += mul(bi, bi);
+    if (owned(ow, i)) pbb += mul(bi, bi);
     if (PRE == SG_PRECOND_LEARNED) D.t[i] = rowGt<FMT, ND, SH, 0>(D, T, i, r0, m, XF{D.b, nullptr, 0.0});
   }
   if (arrive(D, sys, pbb, 0.0, red, &flag)) {
     const double bb = gather_partials(D, sys, 0, red);
-    if (threadIdx.x == 0) { if (D.dist) publish(D, sys, bb, 0.0); else fin_setup1(D, sys, bb); }
+    if (threadIdx.x == 0) { if (D.part) part_fin(D, sys, FIN_SETUP1, bb, 0.0, 0); else fin_setup1(D, sys, bb); }
   }
 }
 
@@ -674,13 +783,14 @@ __global__ void __launch_bounds__(PR, FMT >= 1 ? 8 : 1) k_setup2(Dev D) {
     const long long i = r0 + (long long)rr * PR + threadIdx.x;
     if (i >= r1) continue;
     const unsigned int m = dmask(D, i, r1, FMT);
+    if (!owned(ow, i)) continue;  // ghost rows of s come from the neighbour partitions
     const double si = apply_row<PRE, FMT, ND, SH>(D, T, i, r0, m, D.r0, D.ctl->eps);
-    D.s[i] = si;
+    store_s(D, ow, i, si);
     prs += mul(D.r0[i], si);
   }
   if (arrive(D, sys, prs, 0.0, red, &flag)) {
     const double rs = gather_partials(D, sys, 0, red);
-    if (threadIdx.x == 0) { if (D.dist) publish(D, sys, rs, 0.0); else fin_setup2(D, sys, rs); }
+    if (threadIdx.x == 0) { if (D.part) part_fin(D, sys, FIN_SETUP2, rs, 0.0, 0); else fin_setup2(D, sys, rs); }
   }
 }
 
@@ -715,18 +825,18 @@ __global__ void __launch_bounds__(PR, FMT >= 1 ? 8 : 1) k_iter1(Dev D, int par) 
         qi = rowA<FMT, ND, SH, 1>(D, T, i, r0, m, XF{D.s, dc, beta});
       }
       D.q[i] = qi;
-      pdq += mul(dni, qi);
+      if (owned(ow, i)) pdq += mul(dni, qi);
     }
     if (fresh) {
       const double rf = sub(D.b[i], rowA<FMT, ND, SH, 0>(D, T, i, r0, m, XF{D.x, nullptr, 0.0}));
       if (run) rc[i] = rf;
-      prr += mul(rf, rf);
+      if (owned(ow, i)) prr += mul(rf, rf);
     }
   }
   if (arrive(D, sys, pdq, prr, red, &flag)) {
     const double dq = gather_partials(D, sys, 0, red);
     const double rrf = gather_partials(D, sys, 1, red);
-    if (threadIdx.x == 0) { if (D.dist) publish(D, sys, dq, rrf); else fin_k1(D, sys, run, dq, rrf); }
+    if (threadIdx.x == 0) { if (D.part) part_fin(D, sys, FIN_K1, dq, rrf, run); else fin_k1(D, sys, run, dq, rrf); }
   }
 }
 
@@ -754,7 +864,7 @@ __global__ void __launch_bounds__(PR, FMT >= 1 ? 8 : 1) k_iter2(Dev D, int par) 
       rni = sub(rc[i], mul(alpha, D.q[i]));
       rn[i] = rni;
     }
-    prr += mul(rni, rni);
+    if (owned(ow, i)) prr += mul(rni, rni);
     if (PRE == SG_PRECOND_LEARNED) {
       if (SPLIT) D.t[i] = rowGt<FMT, ND, SH, 0>(D, T, i, r0, m, XF{rn, nullptr, 0.0});
       else D.t[i] = rowGt<FMT, ND, SH, 2>(D, T, i, r0, m, XF{rc, D.q, alpha});
@@ -762,7 +872,7 @@ __global__ void __launch_bounds__(PR, FMT >= 1 ? 8 : 1) k_iter2(Dev D, int par) 
   }
   if (arrive(D, sys, prr, 0.0, red, &flag)) {
     const double rr = gather_partials(D, sys, 0, red);
-    if (threadIdx.x == 0) { if (D.dist) publish(D, sys, rr, 0.0); else fin_rr(D, sys, rr); }
+    if (threadIdx.x == 0) { if (D.part) part_fin(D, sys, FIN_RR, rr, 0.0, 0); else fin_rr(D, sys, rr); }
   }
 }
 
@@ -831,11 +941,11 @@ __global__ void __launch_bounds__(PR, FMT >= 1 ? 8 : 1) k_refresh_r(Dev D, int p
     const unsigned int m = dmask(D, i, r1, FMT);
     const double rni = sub(D.b[i], rowA<FMT, ND, SH, 0>(D, T, i, r0, m, XF{D.x, nullptr, 0.0}));
     rn[i] = rni;
-    prr += mul(rni, rni);
+    if (owned(ow, i)) prr += mul(rni, rni);
   }
   if (arrive(D, sys, prr, 0.0, red, &flag)) {
     const double rr = gather_partials(D, sys, 0, red);
-    if (threadIdx.x == 0) { if (D.dist) publish(D, sys, rr, 0.0); else fin_rr(D, sys, rr); }
+    if (threadIdx.x == 0) { if (D.part) part_fin(D, sys, FIN_RR, rr, 0.0, 0); else fin_rr(D, sys, rr); }
   }
 }
 
@@ -865,16 +975,17 @@ __global__ void __launch_bounds__(PR, FMT >= 1 ? 8 : 1) k_iter3(Dev D, int par, 
   for (int rr = 0; rr < RPT; ++rr) {
     const long long i = r0 + (long long)rr * PR + threadIdx.x;
     if (i >= r1) continue;
+    if (!owned(ow, i)) continue;  // ghost rows of s come from the neighbour partitions
     const unsigned int m = dmask(D, i, r1, FMT);
     const double si = apply_row<PRE, FMT, ND, SH>(D, T, i, r0, m, rn, D.ctl->eps);
-    D.s[i] = si;
+    store_s(D, ow, i, si);
     prs += mul(rn[i], si);
   }
   if (arrive(D, sys, prs, 0.0, red, &flag)) {
     const double rs = gather_partials(D, sys, 0, red);
     if (threadIdx.x == 0) {
-      if (D.dist) {
-        publish(D, sys, rs, 0.0);
+      if (D.part) {
+        part_fin(D, sys, FIN_K3, rs, 0.0, refreshed);
       } else {
         D.st[sys].flags &= ~(FL_XPEND | FL_XINT | FL_DPAR);  // refresh path: x complete (k_refresh_x)
         fin_k3(D, sys, rs, refreshed);
@@ -1058,23 +1169,6 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_pcg_small(Dev D, int iters
   }
 }
 
-// Row-partitioned mode: the finalisers on the all-reduced sums (one thread per system; systems
-// the reducing kernel skipped are skipped here too, exactly as the kernel's own early return).
-enum { FIN_SETUP1 = 0, FIN_SETUP2 = 1, FIN_K1 = 2, FIN_RR = 3, FIN_K3 = 4 };
-__global__ void k_fin(Dev D, int kind, int S, int arg) {
-  const int sys = blockIdx.x * blockDim.x + threadIdx.x;
-  if (sys >= S) return;
-  const int status = D.st[sys].status;
-  const double v0 = D.gsum[2 * sys], v1 = D.gsum[2 * sys + 1];
-  switch (kind) {
-    case FIN_SETUP1: fin_setup1(D, sys, v0); break;
-    case FIN_SETUP2: fin_setup2(D, sys, v0); break;
-    case FIN_K1: if (status != ST_DONE) fin_k1(D, sys, status == ST_RUN, v0, v1); break;
-    case FIN_RR: if (status == ST_RUN) fin_rr(D, sys, v0); break;
-    default: if (status == ST_RUN) fin_k3(D, sys, v0, arg); break;
-  }
-}
-
 // ------------------------------------------------------------------ halo-staged DIA kernels
 // For stencil patterns with a small halo H = max |offset| the neighbour values a row needs are
 // staged once per tile in shared memory (tile +- H rows, computed on the fly from their inputs)
@@ -1120,6 +1214,7 @@ __global__ void __launch_bounds__(PR, 6) k_iter1_st(Dev D, int par) {
   const int status = D.st[sys].status;
   if (status == ST_DONE) return;
   sys_bounds(D, sys, s0, s1);
+  const Own ow = own_of(D, sys);
   const bool run = status == ST_RUN;
   const bool fresh = run ? (D.st[sys].flags & FL_FRESH) != 0 : true;
   const double beta = D.st[sys].beta;
@@ -1160,7 +1255,7 @@ __global__ void __launch_bounds__(PR, 6) k_iter1_st(Dev D, int par) {
       const int li = (int)(i - lo);
       const double qi = dia_row_sm<FMT, ND>(D.dia, D.dia.av, (int)i, li, D.dia.mask[i], sm);
       D.q[i] = qi;
-      pdq += mul(sm[li], qi);
+      if (owned(ow, i)) pdq += mul(sm[li], qi);
     }
   }
   if (fresh) {
@@ -1173,13 +1268,13 @@ __global__ void __launch_bounds__(PR, 6) k_iter1_st(Dev D, int par) {
                                  : dia_row_numpy<ND, 0>(D.dia, D.dia.av, (int)i, m, XF{D.x, nullptr, 0.0});
       const double rf = sub(D.b[i], ax);
       if (run) rc[i] = rf;
-      prr += mul(rf, rf);
+      if (owned(ow, i)) prr += mul(rf, rf);
     }
   }
   if (arrive(D, sys, pdq, prr, red, &flag)) {
     const double dq = gather_partials(D, sys, 0, red);
     const double rrf = gather_partials(D, sys, 1, red);
-    if (threadIdx.x == 0) fin_k1(D, sys, run, dq, rrf);
+    if (threadIdx.x == 0) { if (D.part) part_fin(D, sys, FIN_K1, dq, rrf, run); else fin_k1(D, sys, run, dq, rrf); }
   }
 }
 
@@ -1196,6 +1291,7 @@ __global__ void __launch_bounds__(PR, 5) k_iter23_st(Dev D, int par) {
   block_rows(D, sys, r0, r1);
   if (D.st[sys].status != ST_RUN) return;
   sys_bounds(D, sys, s0, s1);
+  const Own ow = own_of(D, sys);
   const double alpha = D.st[sys].alpha;
   const double eps = D.ctl->eps;
   const double* dn = par ? D.d0 : D.d1;
@@ -1235,7 +1331,7 @@ __global__ void __launch_bounds__(PR, 5) k_iter23_st(Dev D, int par) {
     const double rni = sub(rc[i], mul(alpha, D.q[i]));
     rn[i] = rni;
     sr[i - lo2] = rni;
-    prr += mul(rni, rni);
+    if (owned(ow, i)) prr += mul(rni, rni);
   }
   __syncthreads();
   // t = G^T r' over tile +- H (add.at order; G^T row j on diagonal d = G's mirror at j + off),
@@ -1274,19 +1370,23 @@ __global__ void __launch_bounds__(PR, 5) k_iter23_st(Dev D, int par) {
 #pragma unroll
   for (int rr = 0; rr < kRpt; ++rr) {
     const long long i = r0 + (long long)rr * PR + threadIdx.x;
-    if (i >= r1) continue;
+    if (i >= r1 || !owned(ow, i)) continue;
     const double y = dia_row_sm<1, ND>(D.dia, D.dia.gv, (int)i, (int)(i - lo1), D.dia.mask[i], st);
     const double rni = sr[i - lo2];
     const double si = add(y, mul(eps, rni));
-    D.s[i] = si;
+    store_s(D, ow, i, si);
     prs += mul(rni, si);
   }
   if (arrive(D, sys, prr, prs, red, &flag)) {
     const double rr = gather_partials(D, sys, 0, red);
     const double rs = gather_partials(D, sys, 1, red);
     if (threadIdx.x == 0) {
-      D.st[sys].rr = rr;
-      fin_k3(D, sys, rs, 0);
+      if (D.part) {
+        part_fin(D, sys, FIN_K23, rr, rs, 0);
+      } else {
+        D.st[sys].rr = rr;
+        fin_k3(D, sys, rs, 0);
+      }
     }
   }
 }
@@ -1380,6 +1480,8 @@ __global__ void __launch_bounds__(PR, 1) k_iter23_sw(Dev D, int par) {
   const int K = m1 + 2 * NH + 1;                     // steps
   auto rel = [&](long long v) { return (int)(v - LB < -1 ? -1 : (v - LB > (1LL << 30) ? (1LL << 30) : v - LB)); };
   const int s0r = rel(s0), s1r = rel(s1), R0r = rel(R0), R1r = rel(R1);
+  const Own ow = own_of(D, sys);
+  const int o0r = rel(ow.o0), o1r = rel(ow.o1);
   int off[ND];
 #pragma unroll
   for (int d = 0; d < ND; ++d) off[d] = D.dia.off[d];
@@ -1421,7 +1523,7 @@ __global__ void __launch_bounds__(PR, 1) k_iter23_sw(Dev D, int par) {
       v = (lj >= s0r && lj < s1r) ? v : 0.0;
       if (lj >= R0r && lj < R1r) {
         rn[LB + lj] = v;
-        prr += mul(v, v);
+        if (lj >= o0r && lj < o1r) prr += mul(v, v);
       }
       rp[ix] = v;
     }
@@ -1441,29 +1543,35 @@ __global__ void __launch_bounds__(PR, 1) k_iter23_sw(Dev D, int par) {
       tr[(u % NT) * C + tid] = (lj >= s0r && lj < s1r) ? v : 0.0;
     }
     __syncthreads();
-    if (own_c) {  // C: s and x of chunk mm
+    if (own_c) {  // C: s and x of chunk mm (s of owned rows only: ghost s comes from the neighbours)
       const long long i = LB + li;
       if (!xd) D.x[i] = add(xo, mul(alpha, dd));
       else if (xint) D.x[i] = xo;
-      const int io = (mm % NG) * C + tid, tb = (mm % NT) * C + tid;
-      const unsigned int m = mk[io];
-      double p[ND];
+      if (li >= o0r && li < o1r) {
+        const int io = (mm % NG) * C + tid, tb = (mm % NT) * C + tid;
+        const unsigned int m = mk[io];
+        double p[ND];
 #pragma unroll
-      for (int d = 0; d < ND; ++d) p[d] = mul(gr[d * GR + io], tr[ring_nb<ND>(tb, off, d, TR)]);
-      const double y = combine_numpy<ND>(p, m);
-      const double rni = rp[io];
-      const double si = add(y, mul(eps, rni));
-      D.s[i] = si;
-      prs += mul(rni, si);
+        for (int d = 0; d < ND; ++d) p[d] = mul(gr[d * GR + io], tr[ring_nb<ND>(tb, off, d, TR)]);
+        const double y = combine_numpy<ND>(p, m);
+        const double rni = rp[io];
+        const double si = add(y, mul(eps, rni));
+        store_s(D, ow, i, si);
+        prs += mul(rni, si);
+      }
     }
   }
   if (arrive(D, D.sys_rng0, sys, prr, prs, red, &flag)) {
     const double rr = gather_partials(D, D.sys_rng0, sys, 0, red);
     const double rs = gather_partials(D, D.sys_rng0, sys, 1, red);
     if (threadIdx.x == 0) {
-      D.st[sys].rr = rr;
-      if (xd) D.st[sys].flags = (D.st[sys].flags & ~(FL_XINT | FL_DPAR)) | FL_XPEND | (par ? FL_DPAR : 0);
-      fin_k3(D, sys, rs, 0);
+      if (D.part) {
+        part_fin(D, sys, FIN_K23, rr, rs, 0);
+      } else {
+        D.st[sys].rr = rr;
+        if (xd) D.st[sys].flags = (D.st[sys].flags & ~(FL_XINT | FL_DPAR)) | FL_XPEND | (par ? FL_DPAR : 0);
+        fin_k3(D, sys, rs, 0);
+      }
     }
   }
 }
@@ -1525,6 +1633,7 @@ __global__ void __launch_bounds__(PR, 5) k_iter1_sw(Dev D, int par) {
   const double* dc = par ? D.d1 : D.d0;
   double* dn = par ? D.d0 : D.d1;
   double* rc = par ? D.r1 : D.r0;
+  const Own ow = own_of(D, sys);
   double pdq = 0.0, prr = 0.0;
   if (run) {
     double* ar = reinterpret_cast<double*>(smraw);  // [NA][RING]
@@ -1536,6 +1645,7 @@ __global__ void __launch_bounds__(PR, 5) k_iter1_sw(Dev D, int par) {
     const int K = m1 + NH + 1;
     auto rel = [&](long long v) { return (int)(v - LB < -1 ? -1 : (v - LB > (1LL << 30) ? (1LL << 30) : v - LB)); };
     const int s0r = rel(s0), s1r = rel(s1), R0r = rel(R0), R1r = rel(R1);
+    const int o0r = rel(ow.o0), o1r = rel(ow.o1);
     int off[ND];
 #pragma unroll
     for (int d = 0; d < ND; ++d) off[d] = D.dia.off[d];
@@ -1604,7 +1714,7 @@ __global__ void __launch_bounds__(PR, 5) k_iter1_sw(Dev D, int par) {
           }
           const double qi = combine_numpy<ND>(p, m);
           D.q[LB + li] = qi;
-          pdq += mul(dp[li & DM], qi);
+          if (li >= o0r && li < o1r) pdq += mul(dp[li & DM], qi);
         }
       }
     }
@@ -1624,15 +1734,19 @@ __global__ void __launch_bounds__(PR, 5) k_iter1_sw(Dev D, int par) {
       }
       const double rf = sub(D.b[i], ax);
       if (run) rc[i] = rf;
-      prr += mul(rf, rf);
+      if (owned(ow, i)) prr += mul(rf, rf);
     }
   }
   if (arrive(D, D.sys_rng0, sys, pdq, prr, red, &flag)) {
     const double dq = gather_partials(D, D.sys_rng0, sys, 0, red);
     const double rrf = gather_partials(D, D.sys_rng0, sys, 1, red);
     if (threadIdx.x == 0) {
-      if (pend) D.st[sys].flags = (D.st[sys].flags & ~(FL_XPEND | FL_DPAR)) | (fresh ? FL_XINT : 0);
-      fin_k1(D, sys, run, dq, rrf);
+      if (D.part) {
+        part_fin(D, sys, FIN_K1, dq, rrf, run);
+      } else {
+        if (pend) D.st[sys].flags = (D.st[sys].flags & ~(FL_XPEND | FL_DPAR)) | (fresh ? FL_XINT : 0);
+        fin_k1(D, sys, run, dq, rrf);
+      }
     }
   }
 }
@@ -1680,6 +1794,7 @@ __global__ void __launch_bounds__(PR, 1) k_iter23_s5(Dev D, int par) {
   const long long y0 = r0 / W, nl = (s1 - s0) / W;
   const long long y1 = y0 + D.rng_len < nl ? y0 + D.rng_len : nl;
   const int cx = (int)(W - x0 < C ? W - x0 : C);  // own columns of this strip
+  const Own ow = own_of(D, sys);
   const double alpha = D.st[sys].alpha;
   const double eps = D.ctl->eps;
   const double* dn = par ? D.d0 : D.d1;
@@ -1735,7 +1850,7 @@ __global__ void __launch_bounds__(PR, 1) k_iter23_s5(Dev D, int par) {
           const int x = x0 - E + p;
           if (line >= y0 && line < y1 && x >= x0 && x < x0 + cx) {
             rn[j] = v;
-            prr += mul(v, v);
+            if (owned(ow, j)) prr += mul(v, v);
           }
           rp[ls * SP + p] = v;
         }
@@ -1769,25 +1884,31 @@ __global__ void __launch_bounds__(PR, 1) k_iter23_s5(Dev D, int par) {
       const int p = tid + E;
       const long long i = rowof(line, p);
       D.x[i] = add(st[SP + tid], mul(alpha, st[SP + C + tid]));
-      const int ls = mm & (RL - 1);
-      const unsigned int m = mk[ls * kStripMK + p + 14];
-      double pr[5];
+      if (owned(ow, i)) {  // s of owned rows only: ghost s comes from the neighbour partitions
+        const int ls = mm & (RL - 1);
+        const unsigned int m = mk[ls * kStripMK + p + 14];
+        double pr[5];
 #pragma unroll
-      for (int d = 0; d < 5; ++d)
-        pr[d] = mul(gr[(d * RL + ls) * SP + p], tr[((mm + s5a(d)) & (RL - 1)) * SP + p + s5b(d)]);
-      const double y = combine_numpy<5>(pr, m);
-      const double rni = rp[ls * SP + p];
-      const double si = add(y, mul(eps, rni));
-      D.s[i] = si;
-      prs += mul(rni, si);
+        for (int d = 0; d < 5; ++d)
+          pr[d] = mul(gr[(d * RL + ls) * SP + p], tr[((mm + s5a(d)) & (RL - 1)) * SP + p + s5b(d)]);
+        const double y = combine_numpy<5>(pr, m);
+        const double rni = rp[ls * SP + p];
+        const double si = add(y, mul(eps, rni));
+        store_s(D, ow, i, si);
+        prs += mul(rni, si);
+      }
     }
   }
   if (arrive(D, D.sys_rng0, sys, prr, prs, red, &flag)) {
     const double rr = gather_partials(D, D.sys_rng0, sys, 0, red);
     const double rs = gather_partials(D, D.sys_rng0, sys, 1, red);
     if (threadIdx.x == 0) {
-      D.st[sys].rr = rr;
-      fin_k3(D, sys, rs, 0);
+      if (D.part) {
+        part_fin(D, sys, FIN_K23, rr, rs, 0);
+      } else {
+        D.st[sys].rr = rr;
+        fin_k3(D, sys, rs, 0);
+      }
     }
   }
 }
@@ -1821,6 +1942,7 @@ __global__ void __launch_bounds__(PR, 4) k_iter1_s5(Dev D, int par) {
   const long long y0 = r0 / W, nl = (s1 - s0) / W;
   const long long y1 = y0 + D.rng_len < nl ? y0 + D.rng_len : nl;
   const int cx = (int)(W - x0 < kStripC ? W - x0 : kStripC);
+  const Own ow = own_of(D, sys);
   const bool run = status == ST_RUN;
   const bool fresh = run ? (D.st[sys].flags & FL_FRESH) != 0 : true;
   const double beta = D.st[sys].beta;
@@ -1893,7 +2015,7 @@ __global__ void __launch_bounds__(PR, 4) k_iter1_s5(Dev D, int par) {
         const double qi = combine_numpy<5>(pr, m);
         const long long i = rowof(line, p);
         D.q[i] = qi;
-        pdq += mul(dp[ls * SP + p], qi);
+        if (owned(ow, i)) pdq += mul(dp[ls * SP + p], qi);
       }
     }
   }
@@ -1906,13 +2028,13 @@ __global__ void __launch_bounds__(PR, 4) k_iter1_s5(Dev D, int par) {
                                  : dia_row_numpy<5, 0>(D.dia, D.dia.av, (int)i, m, XF{D.x, nullptr, 0.0});
       const double rf = sub(D.b[i], ax);
       if (run) rc[i] = rf;
-      prr += mul(rf, rf);
+      if (owned(ow, i)) prr += mul(rf, rf);
     }
   }
   if (arrive(D, D.sys_rng0, sys, pdq, prr, red, &flag)) {
     const double dq = gather_partials(D, D.sys_rng0, sys, 0, red);
     const double rrf = gather_partials(D, D.sys_rng0, sys, 1, red);
-    if (threadIdx.x == 0) fin_k1(D, sys, run, dq, rrf);
+    if (threadIdx.x == 0) { if (D.part) part_fin(D, sys, FIN_K1, dq, rrf, run); else fin_k1(D, sys, run, dq, rrf); }
   }
 }
 
@@ -1944,12 +2066,13 @@ struct sg_pcg {
   int short_rows = 0;
   int nrng = 0;       // sliding-window ranges
   int num_sms = 148;
-  // row-partitioned mode (sg_pcg_create_part / sg_pcg_set_comm)
-  int dist = 0;
-  void* comm = nullptr;       // ncclComm_t
-  int left = -1, right = -1;  // neighbour ranks (or -1)
-  long long own_lo = 0, own_hi = 0, ghost_lo = 0, ghost_hi = 0;
-  double* gsum = nullptr;
+  // row partition of one system (sg_pcg_set_partition: group; sg_pcg_set_peers: peer)
+  int part = 0;
+  void* part_mem = nullptr;   // own / push tables, group sums and counter
+  void* red_mem = nullptr;    // peer mode: gsum [2][R][2] + flags [R] + epoch (CUDA IPC exported)
+  int red_world = 0;
+  int64_t part_n = 0;         // rows of the whole partitioned system (max_iters default 20 n)
+  std::vector<void*> peer_maps;  // IPC mappings opened by sg_pcg_set_peers
   int strip = 0;      // wide 5-point grid: 2-D strip sliding-window kernels (k_iter1_s5, k_iter23_s5)
   int k1sw = 1;       // K1 variant: 1 = sliding window (k_iter1_sw), 0 = tiles (k_iter1_st)
   int g_warp = 0;     // CSR G with long rows: K3 one warp per row (k_iter3_wr)
@@ -1985,88 +2108,6 @@ struct sg_pcg {
   double prof_ms[3] = {0, 0, 0};
   double prof_active = 0, prof_samples = 0;
 };
-
-// ------------------------------------------------------------------ NCCL (resolved at run time)
-// The row-partitioned solve runs its halo exchanges and scalar all-reduces as NCCL operations
-// captured into the same CUDA graphs as the iteration kernels.  libnccl is opened lazily (the
-// one PyTorch ships), so the library has no link-time NCCL dependency.
-namespace {
-struct NcclApi {
-  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
-  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
-  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
-  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
-  ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
-  ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
-  ncclResult_t (*groupStart)() = nullptr;
-  ncclResult_t (*groupEnd)() = nullptr;
-  const char* (*getErrorString)(ncclResult_t) = nullptr;
-  bool ok = false;
-};
-
-NcclApi& nccl() {
-  static NcclApi api;
-  static bool tried = false;
-  if (tried) return api;
-  tried = true;
-  void* hdl = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-  if (!hdl) hdl = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
-  if (!hdl) return api;
-  auto sym = [&](const char* n) { return dlsym(hdl, n); };
-  api.getUniqueId = reinterpret_cast<decltype(api.getUniqueId)>(sym("ncclGetUniqueId"));
-  api.commInitRank = reinterpret_cast<decltype(api.commInitRank)>(sym("ncclCommInitRank"));
-  api.commDestroy = reinterpret_cast<decltype(api.commDestroy)>(sym("ncclCommDestroy"));
-  api.allReduce = reinterpret_cast<decltype(api.allReduce)>(sym("ncclAllReduce"));
-  api.send = reinterpret_cast<decltype(api.send)>(sym("ncclSend"));
-  api.recv = reinterpret_cast<decltype(api.recv)>(sym("ncclRecv"));
-  api.groupStart = reinterpret_cast<decltype(api.groupStart)>(sym("ncclGroupStart"));
-  api.groupEnd = reinterpret_cast<decltype(api.groupEnd)>(sym("ncclGroupEnd"));
-  api.getErrorString = reinterpret_cast<decltype(api.getErrorString)>(sym("ncclGetErrorString"));
-  api.ok = api.getUniqueId && api.commInitRank && api.commDestroy && api.allReduce && api.send && api.recv &&
-           api.groupStart && api.groupEnd;
-  return api;
-}
-
-#define SG_NCCL(call)                                                                        \
-  do {                                                                                       \
-    ncclResult_t r_ = (call);                                                                \
-    if (r_ != ncclSuccess) {                                                                 \
-      set_error("NCCL error %d (%s) at %s:%d", (int)r_,                                      \
-                nccl().getErrorString ? nccl().getErrorString(r_) : "?", __FILE__, __LINE__); \
-      return SG_ECUDA;                                                                       \
-    }                                                                                        \
-  } while (0)
-
-// Fill the ghost rows of `vecs` from the neighbours' owned boundary rows (one grouped call).
-int halo(sg_pcg* h, cudaStream_t s, std::initializer_list<double*> vecs) {
-  if (!h->dist || (h->left < 0 && h->right < 0)) return SG_OK;
-  NcclApi& api = nccl();
-  ncclComm_t comm = static_cast<ncclComm_t>(h->comm);
-  SG_NCCL(api.groupStart());
-  for (double* v : vecs) {
-    if (h->left >= 0) {
-      SG_NCCL(api.send(v + h->own_lo, (size_t)h->ghost_lo, ncclFloat64, h->left, comm, s));
-      SG_NCCL(api.recv(v + h->own_lo - h->ghost_lo, (size_t)h->ghost_lo, ncclFloat64, h->left, comm, s));
-    }
-    if (h->right >= 0) {
-      SG_NCCL(api.send(v + h->own_hi - h->ghost_hi, (size_t)h->ghost_hi, ncclFloat64, h->right, comm, s));
-      SG_NCCL(api.recv(v + h->own_hi, (size_t)h->ghost_hi, ncclFloat64, h->right, comm, s));
-    }
-  }
-  SG_NCCL(api.groupEnd());
-  return SG_OK;
-}
-
-// All-reduce the published sums, then the finaliser (row-partitioned mode only).
-int reduce_fin(sg_pcg* h, cudaStream_t s, int kind, int arg) {
-  if (!h->dist) return SG_OK;
-  SG_NCCL(nccl().allReduce(h->gsum, h->gsum, (size_t)2 * h->S, ncclFloat64, ncclSum,
-                           static_cast<ncclComm_t>(h->comm), s));
-  k_fin<<<(h->S + 127) / 128, 128, 0, s>>>(h->D, kind, h->S, arg);
-  SG_LAUNCH_CHECK("k_fin");
-  return SG_OK;
-}
-}  // namespace
 
 namespace {
 
@@ -2119,38 +2160,6 @@ int launch_iteration(sg_pcg* h, cudaStream_t s, int par, bool refresh, cudaEvent
     if (ev) {
       k_snapshot<<<1, 1, 0, s>>>(h->ctl); ++k;
       SG_CUDA(cudaEventRecordWithFlags(ev[0], s, cudaEventRecordExternal));
-    }
-    if (h->dist) {  // row partition: unfused kernels, in-graph halo exchanges and all-reduces
-      double* dc = par ? h->D.d1 : h->D.d0;
-      double* rc = par ? h->D.r1 : h->D.r0;
-      double* rn = par ? h->D.r0 : h->D.r1;
-      int rc2 = halo(h, s, {h->D.s, dc, h->D.x});
-      if (rc2) return rc2;
-      k_iter1<PRE, FMT, ND, SH><<<g, PR, 0, s>>>(h->D, par); ++k;
-      if ((rc2 = reduce_fin(h, s, FIN_K1, 0))) return rc2;
-      if (ev) SG_CUDA(cudaEventRecordWithFlags(ev[1], s, cudaEventRecordExternal));
-      if (!refresh) {
-        if (PRE == SG_PRECOND_LEARNED && (rc2 = halo(h, s, {rc, h->D.q}))) return rc2;
-        k_iter2<PRE, FMT, ND, SH><<<g, PR, 0, s>>>(h->D, par); ++k;
-        if ((rc2 = reduce_fin(h, s, FIN_RR, 0))) return rc2;
-      } else {
-        k_refresh_x<<<g, PR, 0, s>>>(h->D, par); ++k;
-        if ((rc2 = halo(h, s, {h->D.x}))) return rc2;
-        k_refresh_r<FMT, ND, SH><<<g, PR, 0, s>>>(h->D, par); ++k;
-        if ((rc2 = reduce_fin(h, s, FIN_RR, 0))) return rc2;
-        if (PRE == SG_PRECOND_LEARNED) {
-          if ((rc2 = halo(h, s, {rn}))) return rc2;
-          k_refresh_t<FMT, ND, SH><<<g, PR, 0, s>>>(h->D, par); ++k;
-        }
-      }
-      if (ev) SG_CUDA(cudaEventRecordWithFlags(ev[2], s, cudaEventRecordExternal));
-      if (PRE == SG_PRECOND_LEARNED && (rc2 = halo(h, s, {h->D.t}))) return rc2;
-      k_iter3<PRE, FMT, ND, SH><<<g, PR, 0, s>>>(h->D, par, refresh ? 1 : 0); ++k;
-      if ((rc2 = reduce_fin(h, s, FIN_K3, refresh ? 1 : 0))) return rc2;
-      if (ev) SG_CUDA(cudaEventRecordWithFlags(ev[3], s, cudaEventRecordExternal));
-      SG_LAUNCH_CHECK("pcg iteration (row partition)");
-      *nk += k;
-      return SG_OK;
     }
     constexpr int FS = FMT >= 1 ? FMT : 1;
     constexpr int NS = ND > 0 ? ND : 1;
@@ -2481,7 +2490,7 @@ int pattern_hashes(sg_pcg* h, cudaStream_t s) {
 // Re-plan a handle whose patterns changed under it: a fresh handle on the same pointers takes
 // over (user settings carried), the old resources are released.
 int rebuild(sg_pcg* h, cudaStream_t s) {
-  if (h->dist) {
+  if (h->part) {
     set_error("the sparsity pattern of a row-partitioned PCG handle changed; create a new handle");
     return SG_EINVAL;
   }
@@ -2636,6 +2645,7 @@ extern "C" int sg_pcg_create(sg_pcg** out, int32_t n_systems, const int64_t* sys
   Carve c(nullptr);
   c.take<long long>(nb); c.take<int>(nb); c.take<int>(S + 1); c.take<long long>(S);
   c.take<long long>(h->nrng); c.take<int>(h->nrng); c.take<int>(S + 1);
+  c.take<long long>(S); c.take<long long>(S);
   const int64_t gv = h->guard;  // zero guard rows around every vector (DIA neighbour reads)
   for (int v = 0; v < 9; ++v) c.take<double>(n + 2 * gv + 2);
   const int64_t npart = std::max<int64_t>(nb, h->nrng);  // per-CTA partials: tiles or ranges
@@ -2650,6 +2660,8 @@ extern "C" int sg_pcg_create(sg_pcg** out, int32_t n_systems, const int64_t* sys
   long long* d_rng_r0 = m.take<long long>(h->nrng);
   int* d_rng_sys = m.take<int>(h->nrng);
   int* d_sys_rng0 = m.take<int>(S + 1);
+  long long* d_own0 = m.take<long long>(S);
+  long long* d_own1 = m.take<long long>(S);
   double* vec[9];
   for (int v = 0; v < 9; ++v) vec[v] = m.take<double>(n + 2 * gv + 2) + gv;
   double* part = m.take<double>(2 * npart);
@@ -2666,18 +2678,22 @@ extern "C" int sg_pcg_create(sg_pcg** out, int32_t n_systems, const int64_t* sys
   SG_CUDA(cudaMemcpyAsync(d_rng_r0, rng_r0.data(), rng_r0.size() * sizeof(long long), cudaMemcpyHostToDevice, s));
   SG_CUDA(cudaMemcpyAsync(d_rng_sys, rng_sys.data(), rng_sys.size() * sizeof(int), cudaMemcpyHostToDevice, s));
   SG_CUDA(cudaMemcpyAsync(d_sys_rng0, sys_rng0.data(), sys_rng0.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+  // owned rows = the whole system until sg_pcg_set_partition / sg_pcg_set_peers say otherwise
+  SG_CUDA(cudaMemcpyAsync(d_own0, h->sys_start.data(), S * sizeof(long long), cudaMemcpyHostToDevice, s));
+  SG_CUDA(cudaMemcpyAsync(d_own1, h->sys_start.data() + 1, S * sizeof(long long), cudaMemcpyHostToDevice, s));
   SG_CUDA(cudaMemsetAsync(counter, 0, S * sizeof(unsigned int), s));
   Dev& D = h->D;
   D.blk_r0 = d_blk_r0; D.blk_sys = d_blk_sys; D.sys_blk0 = d_sys_blk0; D.sys_r1 = d_sys_r1;
   D.tile = tile;
   D.rng_r0 = d_rng_r0; D.rng_sys = d_rng_sys; D.sys_rng0 = d_sys_rng0; D.rng_len = rng_len;
+  D.own0 = d_own0; D.own1 = d_own1; D.part = 0; D.nsys = (int)S;
   D.a_offs = a_offs; D.a_cols = a_cols; D.a_vals = a_vals;
   D.g_offs = g_offs; D.g_cols = g_cols; D.g_vals = g_vals;
   D.gt_offs = gt_offs; D.gt_cols = gt_cols; D.gt_vals = gt_vals;
   D.inv_diag = inv_diag;
   D.b = vec[0]; D.x = vec[1]; D.r0 = vec[2]; D.r1 = vec[3]; D.d0 = vec[4]; D.d1 = vec[5];
   D.q = vec[6]; D.s = vec[7]; D.t = vec[8];
-  D.part = part; D.counter = counter; D.st = h->st; D.ctl = h->ctl;
+  D.pp = part; D.counter = counter; D.st = h->st; D.ctl = h->ctl;
   D.sell_on = 0;
   D.xdefer = 0;
   if (!h->dia_nd && !h->short_rows) {  // long CSR rows: SELL-32 copies (coalesced row walks)
@@ -2824,7 +2840,7 @@ extern "C" int sg_pcg_solve(sg_pcg* h, const double* b, double* x, const sg_solv
   for (int k = 0; k < h->S; ++k) {
     memset(&st[k], 0, sizeof(SysState));
     const int64_t ns = h->sys_start[k + 1] - h->sys_start[k];
-    st[k].max_iters = cfg->max_iters < 0 ? 20 * ns : cfg->max_iters;
+    st[k].max_iters = cfg->max_iters < 0 ? 20 * (h->part ? h->part_n : ns) : cfg->max_iters;
     st[k].status = ST_RUN;
   }
   SG_CUDA(cudaMemcpyAsync(h->st, st.data(), st.size() * sizeof(SysState), cudaMemcpyHostToDevice, s));
@@ -2847,17 +2863,6 @@ extern "C" int sg_pcg_solve(sg_pcg* h, const double* b, double* x, const sg_solv
     constexpr int FMT = decltype(Fc)::value;
     constexpr int ND = decltype(Nc)::value;
     constexpr bool SH = decltype(SHc)::value;
-    if (h->dist) {
-      int rc2 = halo(h, s, {h->D.b});
-      if (rc2) return rc2;
-      k_setup1<PRE, FMT, ND, SH><<<g, PR, 0, s>>>(h->D);
-      if ((rc2 = reduce_fin(h, s, FIN_SETUP1, 0))) return rc2;
-      if (PRE == SG_PRECOND_LEARNED && (rc2 = halo(h, s, {h->D.t}))) return rc2;
-      k_setup2<PRE, FMT, ND, SH><<<g, PR, 0, s>>>(h->D);
-      if ((rc2 = reduce_fin(h, s, FIN_SETUP2, 0))) return rc2;
-      SG_LAUNCH_CHECK("pcg setup (row partition)");
-      return SG_OK;
-    }
     k_setup1<PRE, FMT, ND, SH><<<g, PR, 0, s>>>(h->D);
     k_setup2<PRE, FMT, ND, SH><<<g, PR, 0, s>>>(h->D);
     SG_LAUNCH_CHECK("pcg setup");
@@ -2969,13 +2974,37 @@ extern "C" int sg_pcg_rebind_values(sg_pcg* h, const double* a_vals, const doubl
   return SG_OK;
 }
 
+extern "C" int sg_pcg_rebind(sg_pcg* h, const int32_t* a_offs, const int32_t* a_cols, const double* a_vals,
+                             const int32_t* g_offs, const int32_t* g_cols, const double* g_vals,
+                             const int32_t* gt_offs, const int32_t* gt_cols, const double* gt_vals,
+                             const double* inv_diag) {
+  if (!h) { set_error("null handle"); return SG_EINVAL; }
+  Dev& D = h->D;
+  const bool moved = D.a_offs != a_offs || D.a_cols != a_cols || D.g_offs != g_offs || D.g_cols != g_cols ||
+                     D.gt_offs != gt_offs || D.gt_cols != gt_cols;
+  if (moved && h->part) {
+    set_error("a row-partitioned PCG handle cannot be re-pointed at other index arrays");
+    return SG_EINVAL;
+  }
+  D.a_offs = a_offs; D.a_cols = a_cols;
+  D.g_offs = g_offs; D.g_cols = g_cols;
+  D.gt_offs = gt_offs; D.gt_cols = gt_cols;
+  if (moved && !h->dia_nd) {  // CSR graphs captured the index pointers
+    for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);
+    h->graphs.clear();
+    h->graph_kernels.clear();
+  }
+  // the next solve fingerprints the patterns behind the new pointers and re-plans if they differ
+  return sg_pcg_rebind_values(h, a_vals, g_vals, gt_vals, inv_diag);
+}
+
 extern "C" int sg_pcg_set_stencil(sg_pcg* h, const double* coeff, int64_t nx, int64_t ny, int32_t* usable_host) {
   if (!h) { set_error("null handle"); return SG_EINVAL; }
   if (usable_host) *usable_host = 0;
   const Dia& dd = h->D.dia;
   // only the streamed K1 (k_iter1_sw) regenerates A: one-CTA small systems, the tile and strip
   // kernels and the row partition keep the stored diagonals (no per-solve copy + check for them)
-  const bool fits = coeff && nx > 1 && ny >= 1 && h->dia_nd == 5 && !h->dist && h->staged && h->k1sw && !h->small &&
+  const bool fits = coeff && nx > 1 && ny >= 1 && h->dia_nd == 5 && !h->part && h->staged && h->k1sw && !h->small &&
                     dd.off[1] == -1 && dd.off[2] == 0 && dd.off[3] == 1 && dd.off[4] == -dd.off[0] &&
                     (int64_t)dd.off[4] == nx;
   const double ihx2 = (double)((nx + 1) * (nx + 1)), ihy2 = (double)((ny + 1) * (ny + 1));  // datasets.py:109-110
@@ -3065,91 +3094,202 @@ extern "C" void sg_pcg_destroy(sg_pcg* h) {
     if (h->sell_vals[k]) cudaFree(h->sell_vals[k]);
   }
   if (h->d_flag) cudaFree(h->d_flag);
+  for (void* pm : h->peer_maps) cudaIpcCloseMemHandle(pm);
+  if (h->part_mem) cudaFree(h->part_mem);
+  if (h->red_mem) cudaFree(h->red_mem);
   if (h->coef) cudaFree(h->coef - h->guard);
   if (h->mem) cudaFree(h->mem);
   delete h;
 }
 
-// ------------------------------------------------------------------ row-partitioned mode API
-extern "C" int sg_nccl_unique_id(void* out128) {
-  if (!nccl().ok) { set_error("libnccl.so.2 not found (needed for the row-partitioned solve)"); return SG_EUNSUPPORTED; }
-  ncclUniqueId id;
-  SG_NCCL(nccl().getUniqueId(&id));
-  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
-  memcpy(out128, &id, sizeof(id));
-  return SG_OK;
-}
 
-extern "C" int sg_nccl_comm_init(void** comm_out, const void* id128, int32_t world, int32_t rank) {
-  if (!nccl().ok) { set_error("libnccl.so.2 not found (needed for the row-partitioned solve)"); return SG_EUNSUPPORTED; }
-  ncclUniqueId id;
-  memcpy(&id, id128, sizeof(id));
-  ncclComm_t comm;
-  SG_NCCL(nccl().commInitRank(&comm, world, id, rank));
-  *comm_out = comm;
-  return SG_OK;
-}
-
-extern "C" int sg_nccl_comm_destroy(void* comm) {
-  if (comm && nccl().ok) SG_NCCL(nccl().commDestroy(static_cast<ncclComm_t>(comm)));
-  return SG_OK;
-}
-
-extern "C" int sg_pcg_create_part(sg_pcg** out, int64_t n_ext, int64_t own_lo, int64_t own_hi,
-                                  const int32_t* a_offs, const int32_t* a_cols, const double* a_vals,
-                                  int precond_kind, const int32_t* g_offs, const int32_t* g_cols,
-                                  const double* g_vals, const int32_t* gt_offs, const int32_t* gt_cols,
-                                  const double* gt_vals, const double* inv_diag, double epsilon, void* stream) {
-  if (!(0 <= own_lo && own_lo < own_hi && own_hi <= n_ext)) { set_error("bad owned row range"); return SG_EINVAL; }
-  const int64_t starts[2] = {0, n_ext};
-  int rc = sg_pcg_create(out, 1, starts, a_offs, a_cols, a_vals, precond_kind, g_offs, g_cols, g_vals, gt_offs,
-                         gt_cols, gt_vals, inv_diag, epsilon, stream);
-  if (rc) return rc;
-  sg_pcg* h = *out;
-  cudaStream_t s = as_stream(stream);
-  // tiles (and every dot product) over the owned rows only; ghost rows are read, never written
-  const int tile = h->D.tile;
-  std::vector<long long> blk_r0;
-  std::vector<int> blk_sys;
-  for (int64_t r = own_lo; r < own_hi; r += tile) { blk_r0.push_back(r); blk_sys.push_back(0); }
-  const int sb0[2] = {0, (int)blk_r0.size()};
-  const long long r1 = own_hi;
-  SG_CUDA(cudaMemcpyAsync(const_cast<long long*>(h->D.blk_r0), blk_r0.data(), blk_r0.size() * sizeof(long long),
-                          cudaMemcpyHostToDevice, s));
-  SG_CUDA(cudaMemcpyAsync(const_cast<int*>(h->D.blk_sys), blk_sys.data(), blk_sys.size() * sizeof(int),
-                          cudaMemcpyHostToDevice, s));
-  SG_CUDA(cudaMemcpyAsync(const_cast<int*>(h->D.sys_blk0), sb0, sizeof(sb0), cudaMemcpyHostToDevice, s));
-  SG_CUDA(cudaMemcpyAsync(const_cast<long long*>(h->D.sys_r1), &r1, sizeof(r1), cudaMemcpyHostToDevice, s));
+// ------------------------------------------------------------------ row partition API
+namespace {
+// Owned ranges + push tables (+ the group sums and counter) in one allocation.
+int part_tables(sg_pcg* h, const std::vector<long long>& own0, const std::vector<long long>& own1,
+                const std::vector<long long>& plo, const std::vector<long long>& phi,
+                const std::vector<double*>& dlo, const std::vector<double*>& dhi, cudaStream_t s) {
+  const int S = h->S;
+  Carve c(nullptr);
+  c.take<long long>(S); c.take<long long>(S); c.take<long long>(S); c.take<long long>(S);
+  c.take<double*>(S); c.take<double*>(S); c.take<double>(2 * S); c.take<unsigned int>(4);
+  if (h->part_mem) { cudaFree(h->part_mem); h->part_mem = nullptr; }
+  SG_CUDA(cudaMalloc(&h->part_mem, c.off));
+  SG_CUDA(cudaMemsetAsync(h->part_mem, 0, c.off, s));
+  Carve m(h->part_mem);
+  long long* d0 = m.take<long long>(S);
+  long long* d1 = m.take<long long>(S);
+  long long* dl = m.take<long long>(S);
+  long long* dh = m.take<long long>(S);
+  double** pl = m.take<double*>(S);
+  double** ph = m.take<double*>(S);
+  double* gs = m.take<double>(2 * S);
+  unsigned int* grp = m.take<unsigned int>(4);
+  SG_CUDA(cudaMemcpyAsync(d0, own0.data(), S * sizeof(long long), cudaMemcpyHostToDevice, s));
+  SG_CUDA(cudaMemcpyAsync(d1, own1.data(), S * sizeof(long long), cudaMemcpyHostToDevice, s));
+  SG_CUDA(cudaMemcpyAsync(dl, plo.data(), S * sizeof(long long), cudaMemcpyHostToDevice, s));
+  SG_CUDA(cudaMemcpyAsync(dh, phi.data(), S * sizeof(long long), cudaMemcpyHostToDevice, s));
+  SG_CUDA(cudaMemcpyAsync(pl, dlo.data(), S * sizeof(double*), cudaMemcpyHostToDevice, s));
+  SG_CUDA(cudaMemcpyAsync(ph, dhi.data(), S * sizeof(double*), cudaMemcpyHostToDevice, s));
   SG_CUDA(cudaStreamSynchronize(s));
-  h->nblk = (int)blk_r0.size();
-  h->own_lo = own_lo;
-  h->own_hi = own_hi;
-  h->staged = 0;  // the streaming kernels assume whole systems; the partition uses the tile kernels
-  h->strip = 0;
+  Dev& D = h->D;
+  D.own0 = d0; D.own1 = d1; D.plo = dl; D.phi = dh; D.push_lo = pl; D.push_hi = ph;
+  D.gsum = gs; D.grp = grp; D.nsys = S;
   return SG_OK;
 }
 
-extern "C" int sg_pcg_set_comm(sg_pcg* h, void* comm, int32_t left, int32_t right, int64_t ghost_lo,
-                               int64_t ghost_hi) {
-  if (!h) { set_error("null handle"); return SG_EINVAL; }
-  if (comm && !nccl().ok) { set_error("libnccl.so.2 not found"); return SG_EUNSUPPORTED; }
-  if (ghost_lo < 0 || ghost_hi < 0 || ghost_lo > h->own_lo || h->own_hi + ghost_hi > h->n ||
-      (left >= 0 && ghost_lo > h->own_hi - h->own_lo) || (right >= 0 && ghost_hi > h->own_hi - h->own_lo)) {
-    set_error("ghost widths do not fit the extended system");
-    return SG_EINVAL;
+// What the partition mode turns off: one-CTA systems, the deferred x update, the coefficient
+// stencil (ghost rows are truncated), the CSR long-row kernels; the captured graphs change.
+int part_common(sg_pcg* h) {
+  if (!h->dia_nd) {
+    set_error("the row partition needs a stencil (diagonal-major) pattern");
+    return SG_EUNSUPPORTED;
   }
-  if (!h->gsum) SG_CUDA(cudaMalloc(&h->gsum, 2 * (size_t)h->S * sizeof(double)));
-  h->comm = comm;
-  h->dist = comm ? 1 : 0;
-  h->left = left;
-  h->right = right;
-  h->ghost_lo = left >= 0 ? ghost_lo : 0;
-  h->ghost_hi = right >= 0 ? ghost_hi : 0;
-  h->D.dist = h->dist;
-  h->D.gsum = h->gsum;
-  if (h->dist) h->D.xdefer = 0, h->small = 0;  // the row partition runs the unfused kernels
+  h->small = 0;
+  h->D.xdefer = 0;
+  if (h->coef) { cudaFree(h->coef - h->guard); h->coef = nullptr; }
+  h->coef_user = nullptr; h->D.coef = nullptr; h->cst = 0;
   for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);
   h->graphs.clear();
   h->graph_kernels.clear();
+  return SG_OK;
+}
+
+struct PeerInfo {  // sg_pcg_peer_info_size() bytes, exchanged between ranks as an opaque blob
+  cudaIpcMemHandle_t mem;  // the handle's workspace (vectors)
+  cudaIpcMemHandle_t red;  // its reduction block
+  int64_t s_off;           // byte offset of s (row 0) inside the workspace
+  int64_t n_ext, own_lo, own_hi;
+  int32_t world, pad;
+};
+}  // namespace
+
+extern "C" int sg_pcg_set_partition(sg_pcg* h, const int64_t* own_lo_host, const int64_t* own_hi_host) {
+  if (!h || !own_lo_host || !own_hi_host) { set_error("null argument"); return SG_EINVAL; }
+  const int S = h->S;
+  std::vector<long long> o0(S), o1(S), pl(S, 0), ph(S, 0);
+  std::vector<double*> dl(S, nullptr), dh(S, nullptr);
+  for (int p = 0; p < S; ++p) {
+    const long long n_p = h->sys_start[p + 1] - h->sys_start[p];
+    if (!(0 <= own_lo_host[p] && own_lo_host[p] < own_hi_host[p] && own_hi_host[p] <= n_p)) {
+      set_error("partition %d: owned rows [%lld, %lld) do not fit its %lld rows", p, (long long)own_lo_host[p],
+                (long long)own_hi_host[p], n_p);
+      return SG_EINVAL;
+    }
+    o0[p] = h->sys_start[p] + own_lo_host[p];
+    o1[p] = h->sys_start[p] + own_hi_host[p];
+  }
+  for (int p = 0; p < S; ++p) {  // neighbours are the adjacent systems of the handle
+    const long long own = o1[p] - o0[p];
+    if (p > 0) {
+      pl[p] = h->sys_start[p] - o1[p - 1];  // partition p-1's top ghost rows
+      dl[p] = h->D.s + o1[p - 1];
+    }
+    if (p < S - 1) {
+      ph[p] = o0[p + 1] - h->sys_start[p + 1];  // partition p+1's bottom ghost rows
+      dh[p] = h->D.s + h->sys_start[p + 1];
+    }
+    if (pl[p] > own || ph[p] > own) {
+      set_error("partition %d owns %lld rows, fewer than its neighbours' ghost depth", p, own);
+      return SG_EINVAL;
+    }
+    if (pl[p] == 0) dl[p] = nullptr;
+    if (ph[p] == 0) dh[p] = nullptr;
+  }
+  int rc = part_common(h);
+  if (rc) return rc;
+  rc = part_tables(h, o0, o1, pl, ph, dl, dh, nullptr);
+  if (rc) return rc;
+  h->part_n = 0;
+  for (int p = 0; p < S; ++p) h->part_n += o1[p] - o0[p];
+  h->part = 1;
+  h->D.part = 1;
+  return SG_OK;
+}
+
+extern "C" int sg_pcg_peer_info_size(void) { return (int)sizeof(PeerInfo); }
+
+extern "C" int sg_pcg_peer_export(sg_pcg* h, int64_t own_lo, int64_t own_hi, int32_t world, void* info_out) {
+  if (!h || !info_out) { set_error("null argument"); return SG_EINVAL; }
+  if (h->S != 1) { set_error("peer mode: one partition (system) per rank"); return SG_EINVAL; }
+  if (world < 1 || world > 8) { set_error("peer mode supports 1..8 ranks"); return SG_EUNSUPPORTED; }
+  if (!(0 <= own_lo && own_lo < own_hi && own_hi <= h->n)) { set_error("bad owned row range"); return SG_EINVAL; }
+  if (h->red_mem) { cudaFree(h->red_mem); h->red_mem = nullptr; }
+  const size_t bytes = (size_t)4 * world * sizeof(double) + (size_t)world * sizeof(unsigned int) + 64;
+  SG_CUDA(cudaMalloc(&h->red_mem, bytes));
+  SG_CUDA(cudaMemset(h->red_mem, 0, bytes));
+  h->red_world = world;
+  PeerInfo info{};
+  SG_CUDA(cudaIpcGetMemHandle(&info.mem, h->mem));
+  SG_CUDA(cudaIpcGetMemHandle(&info.red, h->red_mem));
+  info.s_off = (int64_t)(reinterpret_cast<char*>(h->D.s) - static_cast<char*>(h->mem));
+  info.n_ext = h->n;
+  info.own_lo = own_lo;
+  info.own_hi = own_hi;
+  info.world = world;
+  memcpy(info_out, &info, sizeof(info));
+  return SG_OK;
+}
+
+extern "C" int sg_pcg_set_peers(sg_pcg* h, int32_t rank, int32_t world, const void* infos) {
+  if (!h || !infos) { set_error("null argument"); return SG_EINVAL; }
+  if (!h->red_mem || h->red_world != world) { set_error("call sg_pcg_peer_export with this world size first"); return SG_EINVAL; }
+  if (rank < 0 || rank >= world) { set_error("bad rank"); return SG_EINVAL; }
+  std::vector<PeerInfo> in(world);
+  memcpy(in.data(), infos, sizeof(PeerInfo) * world);
+  std::vector<char*> mem(world, nullptr), red(world, nullptr);
+  for (int q = 0; q < world; ++q) {
+    if (in[q].world != world) { set_error("peer %d exported for another world size", q); return SG_EINVAL; }
+    if (q == rank) {
+      mem[q] = static_cast<char*>(h->mem);
+      red[q] = static_cast<char*>(h->red_mem);
+      continue;
+    }
+    void* r = nullptr;
+    SG_CUDA(cudaIpcOpenMemHandle(&r, in[q].red, cudaIpcMemLazyEnablePeerAccess));
+    h->peer_maps.push_back(r);
+    red[q] = static_cast<char*>(r);
+    if (q == rank - 1 || q == rank + 1) {
+      void* mp = nullptr;
+      SG_CUDA(cudaIpcOpenMemHandle(&mp, in[q].mem, cudaIpcMemLazyEnablePeerAccess));
+      h->peer_maps.push_back(mp);
+      mem[q] = static_cast<char*>(mp);
+    }
+  }
+  const PeerInfo& me = in[rank];
+  std::vector<long long> o0{me.own_lo}, o1{me.own_hi}, pl{0}, ph{0};
+  std::vector<double*> dl{nullptr}, dh{nullptr};
+  const long long own = me.own_hi - me.own_lo;
+  if (rank > 0) {  // my first owned rows -> the left neighbour's top ghost rows
+    const PeerInfo& L = in[rank - 1];
+    pl[0] = L.n_ext - L.own_hi;
+    dl[0] = reinterpret_cast<double*>(mem[rank - 1] + L.s_off) + L.own_hi;
+  }
+  if (rank < world - 1) {  // my last owned rows -> the right neighbour's bottom ghost rows
+    const PeerInfo& R = in[rank + 1];
+    ph[0] = R.own_lo;
+    dh[0] = reinterpret_cast<double*>(mem[rank + 1] + R.s_off);
+  }
+  if (pl[0] > own || ph[0] > own) { set_error("rank %d owns fewer rows than its neighbours' ghost depth", rank); return SG_EINVAL; }
+  if (pl[0] == 0) dl[0] = nullptr;
+  if (ph[0] == 0) dh[0] = nullptr;
+  int rc = part_common(h);
+  if (rc) return rc;
+  rc = part_tables(h, o0, o1, pl, ph, dl, dh, nullptr);
+  if (rc) return rc;
+  Dev& D = h->D;
+  D.rank = rank;
+  D.nranks = world;
+  const size_t gbytes = (size_t)4 * world * sizeof(double);
+  for (int q = 0; q < world; ++q) {
+    D.peer_gsum[q] = reinterpret_cast<double*>(red[q]);
+    D.peer_flag[q] = reinterpret_cast<unsigned int*>(red[q] + gbytes);
+  }
+  D.gsum = D.peer_gsum[rank];
+  D.epoch = reinterpret_cast<unsigned int*>(static_cast<char*>(h->red_mem) + gbytes + world * sizeof(unsigned int));
+  h->part_n = 0;
+  for (int q = 0; q < world; ++q) h->part_n += in[q].own_hi - in[q].own_lo;
+  h->part = 2;
+  D.part = 2;
   return SG_OK;
 }

@@ -209,13 +209,16 @@ def _handle_for(A: SparseMatrix, M: Preconditioner, kind_name: str | None = None
         g, gt, inv, kind, eps = None, None, M.inv_diag_dev, L.PRECOND_JACOBI, 0.0
     else:
         g, gt, inv, kind, eps = None, None, None, L.PRECOND_IDENTITY, 0.0
-    pat = lambda d: (None if d is None else (d.offs.data_ptr(), d.cols.data_ptr(), d.n_rows, d.nnz))  # noqa: E731
-    key = (pat(a), pat(g), pat(gt), kind, eps)
+    # keyed by SIZES: a new factor (a new GNN output with its own G^T arrays) or a new matrix of
+    # the same shape re-points the cached handle (sg_pcg_rebind); the handle fingerprints the
+    # patterns at every solve and re-plans itself only when they really changed
+    size = lambda d: (None if d is None else (d.n_rows, d.nnz))  # noqa: E731
+    key = (size(a), size(g), size(gt), kind, eps)
     h = _HANDLES.get(key)
     if h is not None:
-        L.check(L.lib().sg_pcg_rebind_values(h._h, L.ptr(a.vals), L.ptr(g.vals if g else None),
-                                             L.ptr(gt.vals if gt else None), L.ptr(inv)))
-        h.a, h.g, h.gt, h.inv_diag = a, g, gt, inv  # keep the new value arrays alive
+        ptrs = lambda d: (L.ptr(d.offs), L.ptr(d.cols), L.ptr(d.vals)) if d is not None else (None,) * 3  # noqa: E731
+        L.check(L.lib().sg_pcg_rebind(h._h, *ptrs(a), *ptrs(g), *ptrs(gt), L.ptr(inv)))
+        h.a, h.g, h.gt, h.inv_diag = a, g, gt, inv  # keep the new arrays alive
         _HANDLES.move_to_end(key)
         return h
     h = PcgHandle(a, starts, kind, g, gt, inv, eps)

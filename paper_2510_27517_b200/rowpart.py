@@ -1,24 +1,24 @@
-"""Row-partitioned PCG for ONE large system across ranks.
+"""Row-partitioned PCG for ONE large system (BASELINE configs[4] / C5).
 
-Rank p owns the contiguous rows [r0, r1) (balanced split).  Everything a rank needs is built
-once from the global CSR pattern:
+Two implementations:
 
-* halo plan — the columns of the owned rows that other ranks own, grouped by owner; the owners
-  learn which of their values to send (one all_to_all of index lists).  Local vectors are
-  "extended": [owned | halo from rank 0 | halo from rank 1 | ...];
-* the GNN factor: a rank runs the forward pass on the (L+2)-hop induced subgraph of its rows with
-  globally computed features (G's rows within one hop of the owned rows are then
-  exact), so the GNN needs no communication at all; G^T's owned rows are assembled locally from
-  G's rows of the owned + 1-hop halo nodes;
-* per PCG iteration: 3 halo exchanges (d', r', t) and 2 all-reduces (d'.q; [r'.s, ||r'||^2]),
-  plus one halo exchange + SpMV on refresh / fresh-residual iterations.
-
-The control flow is pcg.py:131-233 verbatim, driven from the host (scalars are all-reduced and
-read back every iteration).  Local products and updates go through an `ops` backend: `CudaOps`
-(the C-ABI kernels; numpy summation orders, bit-exact per row) on GPUs with NCCL, or a numpy
-backend in the CPU tests with gloo.  The fused, device-resident multi-rank loop (peer-memory
-halos inside the iteration kernels) is the next step; this module fixes the partitioning, the
-communication schedule and their tests.
+* **Banded systems, device-resident** (the product path): `plan_row_partition`
+  splits the rows into contiguous blocks (whole grid lines); partition p holds an EXTENDED local
+  system = owned rows +- 3 half-bandwidths of ghost rows, and its G rows come from the GNN run on
+  its own block of rows plus the receptive field (global features: exact norm from per-partition
+  accumulators, global grid coordinates) -- no communication.  The PCG kernels (fused
+  sliding-window / strip kernels included) run over the whole extended system; only owned rows
+  enter the dot products and write s, and the kernel that computes s also stores the first /
+  last owned rows into the neighbours' ghost rows.  With 3 ghost layers d, q, r and x stay exact
+  where they are read (tests/test_rowpart_cpu.py::test_ghost_scheme_reproduces_global_pcg), so
+  per iteration the only communication is that one s halo and the two scalar reductions.
+  `PartitionedSolver` runs P partitions as the systems of ONE handle on one GPU (group mode: the
+  tested emulation of P ranks); `PeerPartitionSolver` runs one partition per rank / GPU (peer
+  mode: CUDA-IPC-mapped neighbour memory over NVLink, flag-synchronised reductions).
+* **Any pattern, host-driven** (`DistPcg`, `solve_rowpart`): a general halo plan (the owned
+  rows' off-rank columns, grouped by owner), local SpMVs through the C-ABI kernels and
+  torch.distributed collectives per dot product -- pcg.py:131-233 verbatim with one host round
+  trip per scalar; covered by 2-rank gloo tests with a numpy backend.
 """
 from __future__ import annotations
 
@@ -30,8 +30,9 @@ import numpy as np
 from .batch import shard_range
 from .pcg import NotSpdError
 
-__all__ = ["HaloPlan", "build_plan", "hop_closure", "local_transpose_rows", "DistPcg", "BandPart", "band_partition",
-           "band_local", "solve_rowpart_device"]
+__all__ = ["HaloPlan", "build_plan", "hop_closure", "local_transpose_rows", "DistPcg", "solve_rowpart",
+           "RowPartition", "plan_row_partition", "PartitionedSolver", "solve_partitioned", "PeerPartitionSolver",
+           "partition_factor", "global_norm", "row_block", "exchange_blobs"]
 
 
 def hop_closure(offs, cols, seeds: np.ndarray, hops: int) -> np.ndarray:
@@ -397,170 +398,364 @@ def solve_rowpart(A, meta, model, b, rtol=1e-8, max_iters=None, period=50, termi
 
 
 # ------------------------------------------------------------------------------------------------
-# Device-resident row partition (banded matrices, e.g. the C5 grid split into blocks of lines)
+# Device-resident row partition of a BANDED system (the C5 grid split into blocks of lines)
 # ------------------------------------------------------------------------------------------------
+GHOST_LAYERS = 3  # ghost depth in half-bandwidths: s is exchanged, d, q, r, x stay exact
+
+
 @dataclass
-class BandPart:
-    """Rank `rank`'s extended local system for a contiguous row split of a banded matrix:
-    owned rows [r0, r1) plus `ghost_lo` / `ghost_hi` ghost rows (the neighbours' boundary rows;
-    ghost width = the half-bandwidth, clipped at the matrix ends)."""
+class RowPartition:
+    """Contiguous row split of one banded system into `parts` partitions.
+
+    own[p]  = [lo, hi)   owned rows (global), multiples of `unit` (a grid line for stencils)
+    ext[p]  = own +- GHOST_LAYERS * hb, clipped: the partition's extended local system
+    gnn[p]  = ext +- (n_layers + 2) * hb, clipped: the rows whose GNN inputs make G exact on ext
+              (receptive field)
+    """
 
     n: int
-    rank: int
-    world: int
-    r0: int
-    r1: int
-    ghost_lo: int
-    ghost_hi: int
+    parts: int
+    hb: int          # half-bandwidth max |col - row|
+    unit: int        # owned-block granularity
+    own: list
+    ext: list
+    gnn: list
 
     @property
-    def e0(self):
-        return self.r0 - self.ghost_lo
+    def ghost_lo(self):
+        return [o[0] - e[0] for o, e in zip(self.own, self.ext)]
 
     @property
-    def e1(self):
-        return self.r1 + self.ghost_hi
-
-    @property
-    def left(self):
-        return self.rank - 1 if self.rank > 0 else -1
-
-    @property
-    def right(self):
-        return self.rank + 1 if self.rank < self.world - 1 else -1
+    def ghost_hi(self):
+        return [e[1] - o[1] for o, e in zip(self.own, self.ext)]
 
 
-def band_partition(offs, cols, n: int, rank: int, world: int) -> BandPart:
+def plan_row_partition(offs, cols, n: int, parts: int, n_layers: int, unit: int | None = None) -> RowPartition:
+    """Balanced split of n rows (in units of `unit` rows; default: the half-bandwidth when it
+    divides n, i.e. grid lines of a 5-point / 7-point stencil) with the ghost and receptive-field
+    extents above.  Every partition must own at least its neighbours' ghost depth."""
     offs = np.asarray(offs, dtype=np.int64)
     cols = np.asarray(cols, dtype=np.int64)
     rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(offs))
     hb = int(np.max(np.abs(cols - rows))) if len(cols) else 0
-    r0, r1 = shard_range(n, rank, world)
-    gl = min(hb, r0) if rank > 0 else 0
-    gh = min(hb, n - r1) if rank < world - 1 else 0
-    for p in range(world):  # every owned block must be at least one band wide
-        a, b = shard_range(n, p, world)
-        if world > 1 and b - a < hb:
-            raise ValueError(f"rank {p} owns {b - a} rows, fewer than the half-bandwidth {hb}")
-    return BandPart(n, rank, world, r0, r1, gl, gh)
+    hb = max(hb, 1)
+    if unit is None:
+        unit = hb if n % hb == 0 else 1
+    if n % unit:
+        raise ValueError(f"{n} rows are not a whole number of {unit}-row units")
+    nu = n // unit
+    if parts < 1 or parts > nu:
+        raise ValueError(f"cannot split {nu} units into {parts} partitions")
+    own = []
+    for p in range(parts):
+        a, b = shard_range(nu, p, parts)
+        own.append((a * unit, b * unit))
+    g = GHOST_LAYERS * hb
+    r = (n_layers + 2) * hb
+    ext = [(max(0, lo - g), min(n, hi + g)) for lo, hi in own]
+    gnn = [(max(0, e0 - r), min(n, e1 + r)) for e0, e1 in ext]
+    for p, (lo, hi) in enumerate(own):
+        need = max(g if p > 0 else 0, g if p < parts - 1 else 0)
+        if parts > 1 and hi - lo < need:
+            raise ValueError(f"partition {p} owns {hi - lo} rows, fewer than the ghost depth {need}")
+    return RowPartition(n, parts, hb, unit, own, ext, gnn)
 
 
-def band_local(offs, cols, vals, part: BandPart):
-    """Rows [e0, e1) of a CSR matrix with columns shifted to the extended local index space;
-    entries whose column falls outside it (only possible in the outermost ghost rows) dropped."""
-    offs = np.asarray(offs, dtype=np.int64)
-    cols = np.asarray(cols, dtype=np.int64)
-    vals = np.asarray(vals, dtype=np.float64)
-    lo, hi = offs[part.e0], offs[part.e1]
-    c = cols[lo:hi]
-    v = vals[lo:hi]
-    r = np.repeat(np.arange(part.e0, part.e1), np.diff(offs[part.e0:part.e1 + 1]))
-    keep = (c >= part.e0) & (c < part.e1)
-    lo_offs = np.zeros(part.e1 - part.e0 + 1, dtype=np.int64)
-    np.add.at(lo_offs, r[keep] - part.e0 + 1, 1)
-    np.cumsum(lo_offs, out=lo_offs)
-    return lo_offs, c[keep] - part.e0, v[keep]
-
-
-def _nccl_comm(rank: int, world: int):
-    """One NCCL communicator for the solve: the unique id travels over torch.distributed when a
-    process group exists (a 1-rank communicator otherwise)."""
+def row_block(offs, cols, r0, r1, c0, c1, col_base=0, entry_base=0, out=None):
+    """Rows [r0, r1) of a device CSR restricted to columns [c0, c1) (sg_csr_row_block).
+    Returns (offs, cols, src) int32 device tensors (src = source entry of every kept entry), or
+    fills `out` = (offs_view, cols_view, src_view) and returns the entry count."""
     import ctypes
 
     import torch
-    import torch.distributed as dist
 
     from . import _lib as L
-    uid = (ctypes.c_ubyte * 128)()
-    if rank == 0:
-        L.check(L.lib().sg_nccl_unique_id(ctypes.cast(uid, ctypes.c_void_p)), "nccl unique id")
-    if world > 1:
-        t = torch.tensor(list(bytes(uid)), dtype=torch.uint8,
-                         device=L.device() if dist.get_backend() == "nccl" else "cpu")
-        dist.broadcast(t, 0)
-        uid = (ctypes.c_ubyte * 128)(*t.cpu().tolist())
-    comm = ctypes.c_void_p()
-    L.check(L.lib().sg_nccl_comm_init(ctypes.byref(comm), ctypes.cast(uid, ctypes.c_void_p), world, rank),
-            "nccl comm init")
-    return comm
+    lib = L.lib()
+    nnz = ctypes.c_int64(0)
+    buf, wsb = L.workspace(lib.sg_csr_row_block, None, None, r0, r1, c0, c1, col_base, entry_base, None, None,
+                           None, None)
+    L.check(lib.sg_csr_row_block(L.ptr(offs), L.ptr(cols), r0, r1, c0, c1, col_base, entry_base, None, None, None,
+                                 ctypes.byref(nnz), L.ptr(buf), ctypes.byref(wsb), L.stream_ptr()), "row block")
+    m = int(nnz.value)
+    if out is None:
+        out = (L.empty(r1 - r0 + 1, torch.int32), L.empty(m, torch.int32), L.empty(m, torch.int32))
+        ret = out
+    else:
+        ret = m
+    o, c, sidx = out
+    L.check(lib.sg_csr_row_block(L.ptr(offs), L.ptr(cols), r0, r1, c0, c1, col_base, entry_base, L.ptr(o),
+                                 L.ptr(c[:m]), L.ptr(sidx[:m]), None, L.ptr(buf), ctypes.byref(wsb),
+                                 L.stream_ptr()), "row block")
+    return ret
 
 
-def solve_rowpart_device(A, meta, model, b, rtol=1e-8, max_iters=None, period=50, termination="true_residual",
-                         rank=None, world=None):
-    """The hot path for one banded system split by rows across ranks, with the PCG loop on the
-    device: every rank builds its extended local system (owned rows + ghost rows), runs the GNN
-    on the receptive field of those rows (no communication: features are global),
-    and solves with sg_pcg in row-partitioned mode — halo exchanges and scalar all-reduces are
-    NCCL operations inside the captured iteration graphs.  Returns (x_own, k, converged,
-    history, part)."""
+def _gather(vals, idx):
+    import torch
+
+    from . import _lib as L
+    out = L.empty(idx.shape[0], torch.float64)
+    L.check(L.lib().sg_gather_f64(L.ptr(vals), L.ptr(idx), L.ptr(out), idx.shape[0], L.stream_ptr()))
+    return out
+
+
+def norm_accumulator(vals_dev, kind: int = 0):
+    """Transferable exact-sum accumulator of |v| (sg_norm_accum): int64 device tensor."""
     import ctypes
 
     import torch
-    import torch.distributed as dist
+
+    from . import _lib as L
+    lib = L.lib()
+    acc = L.empty(lib.sg_norm_acc_size(), torch.int64)
+    buf, wsb = L.workspace(lib.sg_norm_accum, None, 0, kind, None)
+    L.check(lib.sg_norm_accum(L.ptr(vals_dev), int(vals_dev.shape[0]), kind, L.ptr(acc), L.ptr(buf),
+                              ctypes.byref(wsb), L.stream_ptr()), "norm accumulate")
+    return acc
+
+
+def norm_from_accumulator(acc_dev, count: int, kind: int = 0):
+    import torch
+
+    from . import _lib as L
+    out = L.empty(1, torch.float64)
+    L.check(L.lib().sg_norm_from_acc(L.ptr(acc_dev), int(count), kind, L.ptr(out), L.stream_ptr()), "norm")
+    return out
+
+
+@dataclass
+class PartitionFactor:
+    """One partition's extended local system on its device: A and G rows [e0, e1) with columns
+    clipped to [e0, e1) (local indices), the pattern shared."""
+
+    p: int
+    own: tuple
+    ext: tuple
+    offs: object
+    cols: object
+    a_vals: object
+    g_vals: object
+
+
+def partition_factor(part: RowPartition, p: int, A_dev, meta, model, norm_dev, coeff_mean=None, src_row0=0):
+    """What rank p does before its solve, with no communication: cut its GNN block out of A
+    (its own rows plus the receptive field), compute the block's features with the GLOBAL
+    norm / grid coordinates / coefficient mean, run the GNN on the block, and keep A's and G's
+    rows of the extended system.  A_dev: a device CSR holding (at least) the block's rows, with
+    GLOBAL column indices, its row 0 being global row `src_row0` -- the whole matrix in the
+    single-GPU emulation, the rank's own row slab on the peer path."""
+    import torch
 
     from . import _lib as L
     from .gnn import forward_device
-    from .graphfeat import build_graph
-    from .pcg import SolveConfig, report_from
     from .sparse import DeviceCsr
-    if rank is None:
-        init = dist.is_available() and dist.is_initialized()
-        rank = dist.get_rank() if init else 0
-        world = dist.get_world_size() if init else 1
-    n = A.n_rows
-    offs, cols, vals = A.row_offsets, A.col_indices, A.values
-    part = band_partition(offs, cols, n, rank, world)
-    gr = build_graph(A, meta)
-    node, edge = gr.node_features, gr.edge_features[:, 0]
-    # GNN on the (L+2)-hop receptive field of the extended rows: their G rows are exact
-    R = hop_closure(offs, cols, np.arange(part.e0, part.e1), model.config.n_layers + 2)
-    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(offs))
-    in_r = np.zeros(n, dtype=bool)
-    in_r[R] = True
-    keep = in_r[rows] & in_r[cols]
-    remap = -np.ones(n, dtype=np.int64)
-    remap[R] = np.arange(len(R))
-    sub_offs = np.zeros(len(R) + 1, dtype=np.int64)
-    np.add.at(sub_offs, remap[rows[keep]] + 1, 1)
-    np.cumsum(sub_offs, out=sub_offs)
-    sub = DeviceCsr(len(R), len(R), L.to_device(sub_offs.astype(np.int32), torch.int32),
-                    L.to_device(remap[cols[keep]].astype(np.int32), torch.int32),
-                    L.to_device(vals[keep], torch.float64))
-    g_sub = forward_device(model, sub, L.to_device(np.ascontiguousarray(node[R]).ravel(), torch.float64),
-                           L.to_device(edge[keep], torch.float64), gr.d_node).cpu().numpy()
-    g = np.zeros(len(vals))
-    g[np.flatnonzero(keep)] = g_sub
-    ao, ac, av = band_local(offs, cols, vals, part)
-    _, _, gv = band_local(offs, cols, g, part)
-    ne = part.e1 - part.e0
-    a_dev = DeviceCsr(ne, ne, L.to_device(ao.astype(np.int32), torch.int32), L.to_device(ac.astype(np.int32), torch.int32),
-                      L.to_device(av, torch.float64))
-    g_dev = a_dev.with_values(L.to_device(gv, torch.float64))
-    gt_dev = g_dev.transpose()
-    h = ctypes.c_void_p()
-    L.check(L.lib().sg_pcg_create_part(ctypes.byref(h), ne, part.ghost_lo, part.ghost_lo + (part.r1 - part.r0),
-                                       L.ptr(a_dev.offs), L.ptr(a_dev.cols), L.ptr(a_dev.vals), L.PRECOND_LEARNED,
-                                       L.ptr(g_dev.offs), L.ptr(g_dev.cols), L.ptr(g_dev.vals), L.ptr(gt_dev.offs),
-                                       L.ptr(gt_dev.cols), L.ptr(gt_dev.vals), None, float(model.config.epsilon),
-                                       L.stream_ptr()), "pcg_create_part")
-    comm = _nccl_comm(rank, world)
-    try:
-        L.check(L.lib().sg_pcg_set_comm(h, comm, part.left, part.right, part.ghost_lo, part.ghost_hi), "set_comm")
-        cfg = SolveConfig(rtol=rtol, max_iters=max_iters, residual_refresh_period=period, termination=termination)
-        b_ext = np.zeros(ne)
-        b_ext[part.ghost_lo:part.ghost_lo + part.r1 - part.r0] = np.asarray(b, dtype=np.float64)[part.r0:part.r1]
+    b0, b1 = part.gnn[p]
+    e0, e1 = part.ext[p]
+    bo, bc, bsrc = row_block(A_dev.offs, A_dev.cols, b0 - src_row0, b1 - src_row0, b0, b1)
+    bv = _gather(A_dev.vals, bsrc)
+    blk = DeviceCsr(b1 - b0, b1 - b0, bo, bc, bv)
+    family = getattr(meta, "family", None)
+    pde = family in ("poisson2d", "heat2d")
+    d_node = 3 if pde else 2
+    node = L.empty((b1 - b0) * d_node, torch.float64)
+    edge = L.empty(blk.nnz, torch.float64)
+    if pde:
+        nx, ny = meta.grid
+        coeff = np.asarray(meta.coeff, dtype=np.float64)
+        cmean = float(coeff.mean()) if coeff_mean is None else coeff_mean
+        cblk = L.to_device(np.ascontiguousarray(coeff[b0:b1]), torch.float64)
+        L.check(L.lib().sg_graph_features_block(b1 - b0, b0, part.n, L.ptr(bo), L.ptr(bc), L.ptr(bv), L.ptr(norm_dev),
+                                                1, int(nx), int(ny), L.ptr(cblk), cmean, L.ptr(node), L.ptr(edge),
+                                                L.stream_ptr()), "block features")
+    else:
+        L.check(L.lib().sg_graph_features_block(b1 - b0, b0, part.n, L.ptr(bo), L.ptr(bc), L.ptr(bv), L.ptr(norm_dev),
+                                                0, 0, 0, None, 1.0, L.ptr(node), L.ptr(edge), L.stream_ptr()),
+                "block features")
+    gb = forward_device(model, blk, node, edge, d_node)
+    eo, ec, esrc = row_block(bo, bc, e0 - b0, e1 - b0, e0 - b0, e1 - b0)
+    return PartitionFactor(p, part.own[p], part.ext[p], eo, ec, _gather(bv, esrc), _gather(gb, esrc))
+
+
+def global_norm(A_dev, part: RowPartition, allreduce=None, parts=None, src_row0=0, nnz_total=None):
+    """norm_A = fsum|A| / nnz from per-partition exact accumulators over the OWNED rows' values:
+    each partition (rank) accumulates its own entries, the accumulators are added as integers
+    (`allreduce`: torch.distributed all_reduce of the int64 tensor on the peer path; a plain sum
+    of every partition's accumulator in the emulation), one rounding -- bit-identical to the
+    reference's math.fsum over all entries (sparse.py:204-213)."""
+    offs = A_dev.offs
+    accs = []
+    for p in (range(part.parts) if parts is None else parts):
+        lo, hi = part.own[p]
+        e_lo, e_hi = int(offs[lo - src_row0].item()), int(offs[hi - src_row0].item())
+        accs.append(norm_accumulator(A_dev.vals[e_lo:e_hi]))
+    acc = accs[0].clone()
+    for a in accs[1:]:
+        acc += a
+    if allreduce is not None:
+        allreduce(acc)
+    return norm_from_accumulator(acc, A_dev.nnz if nnz_total is None else nnz_total)
+
+
+class PartitionedSolver:
+    """The row-partitioned hot path of ONE system in group mode: the partitions are the systems
+    of one sg_pcg handle (sg_pcg_set_partition) on one GPU -- the emulation of `parts` ranks
+    that runs the exact kernels, halo pushes and ordered reductions of the multi-GPU design,
+    with every kernel covering all partitions.  `solve` returns a SolveReport for the whole
+    system (x assembled from the owned rows)."""
+
+    def __init__(self, A, meta, model, parts: int, unit: int | None = None):
+        import torch
+
+        from . import _lib as L
+        from .sparse import DeviceCsr
+        self.A, self.meta, self.model = A, meta, model
+        a = A.device()
+        n = A.n_rows
+        self.part = plan_row_partition(A.row_offsets, A.col_indices, n, parts, model.config.n_layers, unit)
+        norm = global_norm(a, self.part)
+        self.factors = [partition_factor(self.part, p, a, meta, model, norm) for p in range(parts)]
+        sizes = [f.ext[1] - f.ext[0] for f in self.factors]
+        nnzs = [int(f.cols.shape[0]) for f in self.factors]
+        self.row_start = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+        self.nnz_start = np.concatenate([[0], np.cumsum(nnzs)]).astype(np.int64)
+        N, E = int(self.row_start[-1]), int(self.nnz_start[-1])
+        offs, cols = L.empty(N + 1, torch.int32), L.empty(E, torch.int32)
+        av, gv = L.empty(E, torch.float64), L.empty(E, torch.float64)
+        for p, f in enumerate(self.factors):  # block-diagonal union of the extended systems
+            r0, e0 = int(self.row_start[p]), int(self.nnz_start[p])
+            L.check(L.lib().sg_csr_row_block(L.ptr(f.offs), L.ptr(f.cols), 0, sizes[p], 0, sizes[p], r0, e0,
+                                             L.ptr(offs[r0:]), L.ptr(cols[e0:]), None, None,
+                                             *self._ws(f, sizes[p]), L.stream_ptr()), "union")
+            av[e0:e0 + nnzs[p]].copy_(f.a_vals)
+            gv[e0:e0 + nnzs[p]].copy_(f.g_vals)
+        self.a_union = DeviceCsr(N, N, offs, cols, av)
+        self.g_union = self.a_union.with_values(gv)
+        self.gt_union = self.g_union.transpose()
+        from .pcg import PcgHandle
+        self.handle = PcgHandle(self.a_union, self.row_start, L.PRECOND_LEARNED, self.g_union, self.gt_union, None,
+                                model.config.epsilon)
+        lo = np.array([f.own[0] - f.ext[0] for f in self.factors], dtype=np.int64)
+        hi = np.array([f.own[1] - f.ext[0] for f in self.factors], dtype=np.int64)
+        import ctypes
+        L.check(L.lib().sg_pcg_set_partition(self.handle._h, lo.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                             hi.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))), "set_partition")
+
+    @staticmethod
+    def _ws(f, nr):
+        import ctypes
+
+        from . import _lib as L
+        buf, wsb = L.workspace(L.lib().sg_csr_row_block, None, None, 0, nr, 0, nr, 0, 0, None, None, None, None)
+        PartitionedSolver._keep = buf
+        return L.ptr(buf), ctypes.byref(wsb)
+
+    def solve(self, b, cfg=None):
+        import torch
+
+        from . import _lib as L
+        from .pcg import SolveConfig, report_from
+        cfg = cfg or SolveConfig()
+        b = np.asarray(b, dtype=np.float64)
+        b_ext = np.concatenate([b[f.ext[0]:f.ext[1]] for f in self.factors])
         bd = L.to_device(b_ext, torch.float64)
-        xd = L.empty(ne, torch.float64)
-        res = (L.SolveResultC * 1)()
-        ns = ctypes.c_int64(0)
-        L.check(L.lib().sg_pcg_solve(h, L.ptr(bd), L.ptr(xd), ctypes.byref(cfg.to_c()), res, ctypes.byref(ns),
-                                     L.stream_ptr()), "pcg_solve (row partition)")
-        hist = np.empty(max(int(res[0].hist_len), 0))
-        if len(hist):
-            L.check(L.lib().sg_pcg_history(h, 0, hist.ctypes.data_as(ctypes.c_void_p), len(hist)))
-        x_own = xd[part.ghost_lo:part.ghost_lo + part.r1 - part.r0].cpu().numpy()
-        rep = report_from(res[0], x_own, hist.tolist(), 0, int(ns.value))
-    finally:
-        L.lib().sg_pcg_destroy(h)
-        L.lib().sg_nccl_comm_destroy(comm)
-    return rep.x, rep.k, rep.converged, rep.residual_history, part
+        xd = L.empty(len(b_ext), torch.float64)
+        res = self.handle.solve(bd, xd, cfg)
+        xh = xd.cpu().numpy()
+        x = np.concatenate([xh[int(self.row_start[p]) + f.own[0] - f.ext[0]:int(self.row_start[p]) + f.own[1] - f.ext[0]]
+                            for p, f in enumerate(self.factors)])
+        hist = self.handle.history(0, int(res[0].hist_len)) if cfg.track_history else None
+        assert all(r.k == res[0].k and r.converged == res[0].converged for r in res), "partitions diverged"
+        return report_from(res[0], x, hist, 0, self.handle.last_elapsed_ns)
+
+
+def solve_partitioned(A, meta, model, b, parts: int, cfg=None):
+    """GNN build + PCG of one system split into `parts` row partitions on this GPU (group
+    mode).  Same result as pcg_solve on the whole system up to the order of the dot-product
+    partial sums."""
+    return PartitionedSolver(A, meta, model, parts).solve(b, cfg)
+
+
+# ------------------------------------------------------------------------------------------------
+# Peer mode: one partition per rank, one process per GPU (the multi-GPU path of BASELINE configs[4])
+# ------------------------------------------------------------------------------------------------
+def exchange_blobs(blob: bytes, group=None) -> list:
+    """all_gather of one opaque byte string per rank (setup only; gloo or NCCL)."""
+    import torch.distributed as dist
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, bytes(blob), group=group)
+    return out
+
+
+def host_row_slab(A, r0: int, r1: int):
+    """Rows [r0, r1) of a host CSR (reference int64 arrays) uploaded as a device CSR with GLOBAL
+    column indices: the only part of A a rank ever moves to its GPU."""
+    import torch
+
+    from . import _lib as L
+    from .sparse import DeviceCsr
+    offs = np.asarray(A.row_offsets, dtype=np.int64)
+    lo, hi = int(offs[r0]), int(offs[r1])
+    o = L.to_device((offs[r0:r1 + 1] - lo).astype(np.int32), torch.int32)
+    c = L.to_device(np.asarray(A.col_indices[lo:hi], dtype=np.int64).astype(np.int32), torch.int32)
+    v = L.to_device(np.ascontiguousarray(A.values[lo:hi], dtype=np.float64), torch.float64)
+    return DeviceCsr(r1 - r0, A.n_cols, o, c, v)
+
+
+class PeerPartitionSolver:
+    """Rank `rank` of `world` (torch.distributed initialised, one process per GPU): the rank's
+    partition as a one-system sg_pcg handle in peer mode (sg_pcg_peer_export / sg_pcg_set_peers:
+    s halos stored into the neighbours' ghost rows over NVLink by the kernels, reductions by peer
+    stores + system-scope flags).  Setup communicates twice: the exact norm accumulator
+    (integer all-reduce) and the peer blobs (all_gather); the solve communicates only inside the
+    kernels.  Every rank returns the same k / history and its own slice of x."""
+
+    def __init__(self, A, meta, model, rank: int | None = None, world: int | None = None, group=None):
+        import ctypes
+
+        import torch
+        import torch.distributed as dist
+
+        from . import _lib as L
+        from .pcg import PcgHandle
+        from .sparse import DeviceCsr
+        self.rank = dist.get_rank(group) if rank is None else rank
+        self.world = dist.get_world_size(group) if world is None else world
+        n = A.n_rows
+        self.part = part = plan_row_partition(A.row_offsets, A.col_indices, n, self.world, model.config.n_layers)
+        b0, b1 = part.gnn[self.rank]
+        slab = host_row_slab(A, b0, b1)
+
+        def allreduce(acc):
+            if self.world > 1:
+                t = acc.cpu() if dist.get_backend(group) == "gloo" else acc
+                dist.all_reduce(t, group=group)
+                acc.copy_(t)
+
+        norm = global_norm(slab, part, allreduce, parts=[self.rank], src_row0=b0, nnz_total=len(A.col_indices))
+        f = self.factor = partition_factor(part, self.rank, slab, meta, model, norm, src_row0=b0)
+        ne = f.ext[1] - f.ext[0]
+        a = DeviceCsr(ne, ne, f.offs, f.cols, f.a_vals)
+        g = a.with_values(f.g_vals)
+        self._mats = (a, g, g.transpose())
+        self.handle = PcgHandle(a, np.array([0, ne]), L.PRECOND_LEARNED, g, self._mats[2], None,
+                                model.config.epsilon)
+        lib = L.lib()
+        blob = (ctypes.c_ubyte * lib.sg_pcg_peer_info_size())()
+        own_lo, own_hi = f.own[0] - f.ext[0], f.own[1] - f.ext[0]
+        L.check(lib.sg_pcg_peer_export(self.handle._h, own_lo, own_hi, self.world, blob), "peer export")
+        blobs = exchange_blobs(bytes(blob), group) if self.world > 1 else [bytes(blob)]
+        allb = (ctypes.c_ubyte * (len(blob) * self.world)).from_buffer_copy(b"".join(blobs))
+        L.check(lib.sg_pcg_set_peers(self.handle._h, self.rank, self.world, allb), "set peers")
+
+    def solve(self, b, cfg=None):
+        import torch
+
+        from . import _lib as L
+        from .pcg import SolveConfig, report_from
+        cfg = cfg or SolveConfig()
+        f = self.factor
+        bd = L.to_device(np.ascontiguousarray(np.asarray(b, dtype=np.float64)[f.ext[0]:f.ext[1]]), torch.float64)
+        xd = L.empty(f.ext[1] - f.ext[0], torch.float64)
+        (res,) = self.handle.solve(bd, xd, cfg)
+        x = xd[f.own[0] - f.ext[0]:f.own[1] - f.ext[0]].cpu().numpy()
+        hist = self.handle.history(0, int(res.hist_len)) if cfg.track_history else None
+        return report_from(res, x, hist, 0, self.handle.last_elapsed_ns)

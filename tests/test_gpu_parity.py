@@ -784,24 +784,6 @@ def test_bench_csv_rows_and_schema(tmp_path):
         bench_rows(items[:1], ("ic0",), (1e-6,), None, m)
 
 
-def test_rowpart_device_single_rank():
-    """Row-partitioned device solve (in-graph NCCL all-reduces and halo groups; here one rank,
-    so a 1-rank communicator) against pcg_solve on the whole system and the oracle's k."""
-    import os
-    from paper_2510_27517_b200.rowpart import solve_rowpart_device
-    m = P.load_checkpoint(os.path.join(os.path.dirname(__file__), "golden", "trained_heat16.spaignn"))
-    A, meta = P.gen_poisson2d(32, 32, coeff_seed=2)
-    b = P.gen_rhs(meta, 5)
-    x, k, conv, hist, part = solve_rowpart_device(A, meta, m, b, rtol=1e-8)
-    assert part.r0 == 0 and part.r1 == A.n_rows and part.ghost_lo == part.ghost_hi == 0
-    G = P.forward(m, P.build_graph(A, meta)).G
-    rep = P.pcg_solve(A, b, P.build_learned_spai(G, m.config.epsilon), P.SolveConfig(rtol=1e-8))
-    assert conv and rep.converged and _k_close(k, rep.k), (k, rep.k)
-    o, c, v = (np.asarray(A.row_offsets), np.asarray(A.col_indices), np.asarray(A.values))
-    assert np.linalg.norm(b - O.spmv(o, c, v, x)) / np.linalg.norm(b) <= 1.01e-8
-    assert len(hist) == k + 1
-
-
 def test_sliding_window_two_chunk_halo(multi_kernel):
     """5-point grids with 256 < W <= 512 run the sliding-window kernels with a two-chunk halo
     (NH = 2: deeper rings, 4-chunk warm-up): k and residual against the oracle."""

@@ -1,0 +1,95 @@
+"""GPU: ONE system row-partitioned (BASELINE configs[4]) in group mode --
+the P partitions are systems of one sg_pcg handle on this GPU, running the multi-GPU design's
+kernels, in-kernel s-halo pushes and partition-ordered reductions.  Checked
+against pcg_solve on the whole system (k within +-2%, the residual history, the true residual)
+and the per-partition GNN blocks against the global G."""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import spaigraph_ref as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2510_27517_b200 as P  # noqa: E402
+from paper_2510_27517_b200 import rowpart as RP  # noqa: E402
+
+CKPT = os.path.join(os.path.dirname(__file__), "golden", "trained_heat16.spaignn")
+
+
+def _whole(A, meta, m, b, cfg):
+    G = P.forward(m, P.build_graph(A, meta)).G
+    return G, P.pcg_solve(A, b, P.build_learned_spai(G, m.config.epsilon), cfg)
+
+
+@pytest.mark.parametrize("grid,parts,fused", [((96, 40), 1, 1), ((96, 40), 2, 1), ((96, 40), 4, 1), ((1024, 24), 4, 1),
+                                              ((784, 20), 2, 1), ((700, 18), 3, 0)])
+def test_partitioned_solve_matches_whole_system(grid, parts, fused):
+    """(96, 40): 1-D sliding-window kernels (half-bandwidth 96); (1024, 24), (784, 20): the 2-D
+    strip kernels (W > 512; 784 leaves a partial strip); (700, 18): the unfused tile kernels
+    (W not a multiple of 16)."""
+    m = P.load_checkpoint(CKPT)
+    nx, ny = grid
+    A, meta = P.gen_poisson2d(nx, ny, coeff_seed=4)
+    b = P.gen_rhs(meta, 17)
+    cfg = P.SolveConfig(rtol=1e-9, residual_refresh_period=11)
+    _, ref = _whole(A, meta, m, b, cfg)
+    sol = RP.PartitionedSolver(A, meta, m, parts)
+    rep = sol.solve(b, cfg)
+    assert rep.converged and ref.converged
+    assert abs(rep.k - ref.k) <= max(1, 0.02 * ref.k), (rep.k, ref.k)
+    np.testing.assert_allclose(rep.residual_history[:60], ref.residual_history[:60], rtol=1e-6, atol=1e-9)
+    o, c, v = A.row_offsets, A.col_indices, A.values
+    assert np.linalg.norm(b - O.spmv(o, c, v, rep.x)) / np.linalg.norm(b) <= 1e-9
+    assert sol.handle.stats()[2][7] == float(fused)
+
+
+def test_partition_factors_equal_global_g():
+    """Each partition's G (GNN on its own block: global norm from exact per-partition
+    accumulators, global grid coordinates, receptive-field margin) equals the global G rows."""
+    m = P.load_checkpoint(CKPT)
+    A, meta = P.gen_poisson2d(64, 50, coeff_seed=7)
+    G = P.forward(m, P.build_graph(A, meta)).G
+    g = G.values
+    o, c = A.row_offsets, A.col_indices
+    sol = RP.PartitionedSolver(A, meta, m, 3)
+    for f in sol.factors:
+        e0, e1 = f.ext
+        fo, fc, fg = f.offs.cpu().numpy(), f.cols.cpu().numpy(), f.g_vals.cpu().numpy()
+        fa = f.a_vals.cpu().numpy()
+        for i in range(e0, e1):
+            li = i - e0
+            keep = (c[o[i]:o[i + 1]] >= e0) & (c[o[i]:o[i + 1]] < e1)
+            assert np.array_equal(fc[fo[li]:fo[li + 1]] + e0, c[o[i]:o[i + 1]][keep])
+            assert np.array_equal(fa[fo[li]:fo[li + 1]], A.values[o[i]:o[i + 1]][keep])
+            ref = g[o[i]:o[i + 1]][keep]
+            np.testing.assert_allclose(fg[fo[li]:fo[li + 1]], ref, rtol=1e-13, atol=1e-13 * np.max(np.abs(g)))
+
+
+def test_partition_norm_is_exact():
+    """norm_A from per-partition exact accumulators added as integers == fsum over all values."""
+    for parts in (1, 2, 3, 5):
+        A, meta = P.gen_poisson2d(37, 41, coeff_seed=parts)
+        pl = RP.plan_row_partition(A.row_offsets, A.col_indices, A.n_rows, parts, 4, unit=1)
+        nrm = RP.global_norm(A.device(), pl).item()
+        assert nrm == O.mean_abs_nonzero_norm(A.values)
+
+
+def test_c5_four_partitions():
+    """The north-star shape: 2048 x 2048 Poisson, 4 partitions of 512 lines (strip kernels)."""
+    m = P.load_checkpoint(CKPT)
+    A, meta = P.gen_poisson2d(2048, 2048)
+    b = P.gen_rhs(meta, 10**6)
+    cfg = P.SolveConfig(rtol=1e-6)
+    _, ref = _whole(A, meta, m, b, cfg)
+    sol = RP.PartitionedSolver(A, meta, m, 4)
+    rep = sol.solve(b, cfg)
+    assert rep.converged and abs(rep.k - ref.k) <= max(1, 0.02 * ref.k), (rep.k, ref.k)
+    np.testing.assert_allclose(rep.residual_history[:50], ref.residual_history[:50], rtol=1e-9)
+    o, c, v = A.row_offsets, A.col_indices, A.values
+    assert np.linalg.norm(b - O.spmv(o, c, v, rep.x)) / np.linalg.norm(b) <= 1e-6

@@ -187,23 +187,268 @@ def test_distributed_pcg_two_gloo_ranks(tmp_path):
     assert out["hlen"] == out["k"] + 1
 
 
-def test_band_partition_extended_systems():
-    """Contiguous row split of a banded matrix (the device-resident row partition): owned blocks
-    tile the rows, neighbouring ghost widths agree (what one rank sends is what the other
-    receives), and every owned row of the extended local system equals the global row."""
-    from oracle import spaigraph_ref as O
-    from paper_2510_27517_b200.rowpart import band_local, band_partition
-    o, c, v, _ = O.gen_poisson2d(12, 9)
+def test_row_partition_plan():
+    """plan_row_partition: owned blocks tile the rows in whole grid lines, ghosts are 3 half-
+    bandwidths (clipped at the ends), the GNN block adds the (L+2)-hop receptive field."""
+    from paper_2510_27517_b200.rowpart import GHOST_LAYERS, plan_row_partition
+    o, c, v, _ = O.gen_poisson2d(12, 40)
     n = len(o) - 1
-    for world in (1, 2, 3):
-        parts = [band_partition(o, c, n, r, world) for r in range(world)]
-        assert parts[0].r0 == 0 and parts[-1].r1 == n
-        for a, b in zip(parts[:-1], parts[1:]):
-            assert a.r1 == b.r0 and a.ghost_hi == b.ghost_lo == 12  # half-bandwidth = nx
-        for p in parts:
-            lo, lc, lv = band_local(o, c, v, p)
-            for i in range(p.r0, p.r1):
-                li = i - p.e0
-                gl = slice(o[i], o[i + 1])
-                assert np.array_equal(lc[lo[li]:lo[li + 1]] + p.e0, c[gl])
-                assert np.array_equal(lv[lo[li]:lo[li + 1]], v[gl])
+    for parts in (1, 2, 3, 4):
+        pl = plan_row_partition(o, c, n, parts, n_layers=4)
+        assert pl.hb == 12 and pl.unit == 12
+        assert pl.own[0][0] == 0 and pl.own[-1][1] == n
+        for (a0, a1), (b0, b1) in zip(pl.own[:-1], pl.own[1:]):
+            assert a1 == b0 and a1 % 12 == 0
+        for p, ((lo, hi), (e0, e1), (g0, g1)) in enumerate(zip(pl.own, pl.ext, pl.gnn)):
+            assert e0 == max(0, lo - GHOST_LAYERS * 12) and e1 == min(n, hi + GHOST_LAYERS * 12)
+            assert g0 == max(0, e0 - 6 * 12) and g1 == min(n, e1 + 6 * 12)
+    import pytest
+    with pytest.raises(ValueError):
+        plan_row_partition(o, c, n, 20, n_layers=4)  # 2 lines each < 3-line ghosts
+
+
+def _band(offs, cols, vals, e0, e1):
+    """Rows [e0, e1) with columns clipped to [e0, e1), local indices (storage order kept)."""
+    rows = np.repeat(np.arange(len(offs) - 1), np.diff(offs))
+    sel = (rows >= e0) & (rows < e1) & (cols >= e0) & (cols < e1)
+    lo = np.zeros(e1 - e0 + 1, dtype=np.int64)
+    np.add.at(lo, rows[sel] - e0 + 1, 1)
+    return np.cumsum(lo), cols[sel] - e0, vals[sel]
+
+
+def test_ghost_scheme_reproduces_global_pcg():
+    """The partition design of DESIGN.md §7 in numpy: every vector is computed over each
+    partition's WHOLE extended system (3 half-bandwidths of ghost rows, truncated rows at its
+    edges), s only on owned rows and then copied into the neighbours' ghost rows, dot products
+    over owned rows added in partition order -- exactly the kernels' schedule (K1, fused K2+K3,
+    refresh, fresh residual).  Its residual history equals the oracle's global pcg_solve up to
+    dot-product rounding, so the redundant ghost computation is exact where it is read."""
+    from paper_2510_27517_b200.rowpart import plan_row_partition
+    nx, ny = 11, 48
+    offs, cols, vals, coeff = O.gen_poisson2d(nx, ny, 3)
+    n = nx * ny
+    node, _, ef, _ = O.graph_features(n, offs, cols, vals, "heat2d", (nx, ny), coeff)
+    from paper_2510_27517_b200.gnn import load_checkpoint
+    params = load_checkpoint(os.path.join(ROOT, "tests", "golden", "trained_heat16.spaignn")).params_flat()
+    g = O.gnn_forward_restructured(O.unflatten(params, O.init_params(3)), node, offs, cols, ef, 4)
+    eps = 1e-4
+    b = O.gen_rhs(n, 9)
+    rtol, period = 1e-10, 7
+    _, k_ref, conv_ref, hist_ref = O.pcg_solve(offs, cols, vals, b,
+                                               lambda r: O.learned_apply(n, offs, cols, g, eps, r),
+                                               rtol=rtol, period=period)
+    for parts in (2, 3, 4):
+        pl = plan_row_partition(offs, cols, n, parts, n_layers=4)
+        P_ = []
+        for (lo, hi), (e0, e1) in zip(pl.own, pl.ext):
+            ao, ac, av = _band(offs, cols, vals, e0, e1)
+            _, _, gv = _band(offs, cols, g, e0, e1)
+            P_.append(dict(o=slice(lo - e0, hi - e0), e=(e0, e1), n=e1 - e0, a=(ao, ac, av), g=(ao, ac, gv),
+                           b=b[e0:e1].copy()))
+
+        def A(p, x):
+            return O.spmv(*p["a"], x)
+
+        def Gt(p, x):
+            return O.spmv_transpose(p["n"], *p["g"], x)
+
+        def Gm(p, x):
+            return O.spmv(*p["g"], x)
+
+        def dot(u, v):  # owned rows, partition order
+            s = 0.0
+            for p, a, c in zip(P_, u, v):
+                s = s + float(a[p["o"]] @ c[p["o"]])
+            return s
+
+        def exchange_s(S):  # owned s -> every other partition's ghost rows
+            for q, p in enumerate(P_):
+                for r, pr in enumerate(P_):
+                    if r == q:
+                        continue
+                    lo = max(p["e"][0], pr["e"][0] + pr["o"].start)
+                    hi = min(p["e"][1], pr["e"][0] + pr["o"].stop)
+                    if lo < hi:
+                        S[q][lo - p["e"][0]:hi - p["e"][0]] = S[r][lo - pr["e"][0]:hi - pr["e"][0]]
+
+        def apply(r):  # setup2 / K2+K3 / refresh K3: s on owned rows, then the halo push
+            S = []
+            for p, rp in zip(P_, r):
+                s_ = np.zeros(p["n"])
+                s_[p["o"]] = (Gm(p, Gt(p, rp)) + eps * rp)[p["o"]]
+                S.append(s_)
+            exchange_s(S)
+            return S
+
+        x = [np.zeros(p["n"]) for p in P_]
+        r = [p["b"].copy() for p in P_]
+        norm_b = np.sqrt(dot(r, r))
+        s = apply(r)
+        d = [np.zeros(p["n"]) for p in P_]
+        delta = dot(r, s)
+        delta0 = delta
+        hist = [np.sqrt(dot(r, r)) / norm_b]
+        beta, i, fresh, conv = 0.0, 0, False, False
+        while i < 20 * n:
+            d = [si + beta * di for si, di in zip(s, d)]  # K1
+            q = [A(p, di) for p, di in zip(P_, d)]
+            if fresh:
+                rf = [p["b"] - A(p, xi) for p, xi in zip(P_, x)]
+                rel = np.sqrt(dot(rf, rf)) / norm_b
+                hist[-1] = rel
+                if rel <= rtol:
+                    conv = True
+                    break
+                r, fresh = rf, False
+            alpha = delta / dot(d, q)
+            x = [xi + alpha * di for xi, di in zip(x, d)]
+            refreshed = i > 0 and i % period == 0
+            if refreshed:
+                r = [p["b"] - A(p, xi) for p, xi in zip(P_, x)]
+            else:
+                r = [ri - alpha * qi for ri, qi in zip(r, q)]
+            s = apply(r)
+            delta_old, delta = delta, dot(r, s)
+            beta = delta / delta_old
+            i += 1
+            rel = np.sqrt(dot(r, r)) / norm_b
+            hist.append(rel)
+            if rel <= rtol:
+                if refreshed:
+                    conv = True
+                    break
+                fresh = True
+        # a ghost value that were wrong where it is read would break the recurrence at once; the
+        # only difference left is the order of the dot products' additions
+        assert conv and conv_ref and abs(i - k_ref) <= max(1, 0.02 * k_ref), (parts, i, k_ref)
+        np.testing.assert_allclose(hist[:60], hist_ref[:60], rtol=1e-6, atol=1e-9)
+
+
+PEER_WORKER = r"""
+import json, os, sys
+sys.path.insert(0, {root!r})
+import numpy as np
+import torch
+import torch.distributed as dist
+from oracle import spaigraph_ref as O
+from paper_2510_27517_b200.dist import init_from_env
+from paper_2510_27517_b200.rowpart import exchange_blobs, plan_row_partition
+
+rank, world, _ = init_from_env("gloo")
+nx, ny = 9, 30
+offs, cols, vals, coeff = O.gen_poisson2d(nx, ny, 2)
+n = nx * ny
+node, _, ef, _ = O.graph_features(n, offs, cols, vals, "heat2d", (nx, ny), coeff)
+from paper_2510_27517_b200.gnn import load_checkpoint
+params = load_checkpoint(os.path.join({root!r}, "tests", "golden", "trained_heat16.spaignn")).params_flat()
+g = O.gnn_forward_restructured(O.unflatten(params, O.init_params(3)), node, offs, cols, ef, 4)
+b = O.gen_rhs(n, 3)
+eps, rtol, period = 1e-4, 1e-8, 9
+pl = plan_row_partition(offs, cols, n, world, n_layers=4)
+# the peer blobs travel once (sg_pcg_set_peers' input); every rank sees every blob in rank order
+blobs = exchange_blobs(("peer-info-%d" % rank).encode())
+assert blobs == [("peer-info-%d" % q).encode() for q in range(world)], blobs
+(lo, hi), (e0, e1) = pl.own[rank], pl.ext[rank]
+rows = np.repeat(np.arange(n), np.diff(offs))
+sel = (rows >= e0) & (rows < e1) & (cols >= e0) & (cols < e1)
+lo_offs = np.cumsum(np.concatenate([[0], np.bincount(rows[sel] - e0, minlength=e1 - e0)]))
+A = (lo_offs, cols[sel] - e0, vals[sel])
+G = (lo_offs, cols[sel] - e0, g[sel])
+own = slice(lo - e0, hi - e0)
+ne = e1 - e0
+
+def dot(u, v):  # partials in rank order: what part_fin (peer mode) adds
+    parts = [None] * world
+    dist.all_gather_object(parts, float(u[own] @ v[own]))
+    s = 0.0
+    for p in parts:
+        s = s + p
+    return s
+
+def push_s(s):  # the kernels' peer stores: owned boundary rows -> neighbours' ghost rows
+    reqs = []
+    if rank > 0:
+        gh = pl.ext[rank - 1][1] - pl.own[rank - 1][1]
+        reqs.append(dist.isend(torch.from_numpy(s[own][:gh].copy()), rank - 1))
+    if rank < world - 1:
+        gl = pl.own[rank + 1][0] - pl.ext[rank + 1][0]
+        reqs.append(dist.isend(torch.from_numpy(s[own][len(s[own]) - gl:].copy()), rank + 1))
+    if rank > 0:
+        buf = torch.empty(lo - e0, dtype=torch.float64)
+        dist.recv(buf, rank - 1)
+        s[:lo - e0] = buf.numpy()
+    if rank < world - 1:
+        buf = torch.empty(e1 - hi, dtype=torch.float64)
+        dist.recv(buf, rank + 1)
+        s[hi - e0:] = buf.numpy()
+    for r_ in reqs:
+        r_.wait()
+
+def apply(r):
+    s = np.zeros(ne)
+    s[own] = (O.spmv(*G, O.spmv_transpose(ne, *G, r)) + eps * r)[own]
+    push_s(s)
+    return s
+
+bl = b[e0:e1].copy()
+x, r, d = np.zeros(ne), bl.copy(), np.zeros(ne)
+norm_b = np.sqrt(dot(r, r))
+s = apply(r)
+delta = dot(r, s)
+hist = [np.sqrt(dot(r, r)) / norm_b]
+beta, i, fresh, conv = 0.0, 0, False, False
+while i < 20 * n:
+    d = s + beta * d
+    q = O.spmv(*A, d)
+    if fresh:
+        rf = bl - O.spmv(*A, x)
+        rel = np.sqrt(dot(rf, rf)) / norm_b
+        hist[-1] = rel
+        if rel <= rtol:
+            conv = True
+            break
+        r, fresh = rf, False
+    alpha = delta / dot(d, q)
+    x = x + alpha * d
+    refreshed = i > 0 and i % period == 0
+    r = bl - O.spmv(*A, x) if refreshed else r - alpha * q
+    s = apply(r)
+    delta_old, delta = delta, dot(r, s)
+    beta = delta / delta_old
+    i += 1
+    rel = np.sqrt(dot(r, r)) / norm_b
+    hist.append(rel)
+    if rel <= rtol:
+        if refreshed:
+            conv = True
+            break
+        fresh = True
+xs = [None] * world
+dist.all_gather_object(xs, x[own].tolist())
+if rank == 0:
+    xg = np.concatenate([np.asarray(p) for p in xs])
+    _, kr, cr, hr = O.pcg_solve(offs, cols, vals, b, lambda v: O.learned_apply(n, offs, cols, g, eps, v),
+                                rtol=rtol, period=period)
+    print(json.dumps({{"k": i, "kr": kr, "conv": conv, "cr": cr, "hist": hist[:40], "hr": hr[:40],
+                      "res": float(np.linalg.norm(b - O.spmv(offs, cols, vals, xg)) / np.linalg.norm(b))}}))
+dist.barrier()
+dist.destroy_process_group()
+"""
+
+
+def test_peer_partition_schedule_two_gloo_ranks(tmp_path):
+    """The peer-mode schedule across 2 processes: each rank plans the partition itself, builds
+    only its extended system, exchanges its peer blob once, pushes its s boundary rows into the
+    neighbour's ghost rows (send/recv standing in for the NVLink peer stores) and adds the
+    reduction partials in rank order -- the same result as the oracle's global pcg_solve."""
+    script = tmp_path / "peer_worker.py"
+    script.write_text(PEER_WORKER.format(root=ROOT))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(script)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300,
+                       env={**os.environ, "CUDA_VISIBLE_DEVICES": ""})
+    assert r.returncode == 0, r.stderr[-3000:]
+    out = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert out["conv"] and out["cr"] and abs(out["k"] - out["kr"]) <= max(1, 0.02 * out["kr"])
+    np.testing.assert_allclose(out["hist"], out["hr"], rtol=1e-6, atol=1e-10)
+    assert out["res"] <= 1e-8
