@@ -292,6 +292,33 @@ int sg_sai_loss(int64_t n, const int32_t* a_offs, const int32_t* a_cols, const d
                 const int32_t* g_rows, double eps, const double* w, int norm_kind,
                 double* loss_host, double* grad_out, void* ws, size_t* ws_bytes, void* stream);
 
+/* Row-partitioned SAI loss (BASELINE configs[4]: loss forward + backward on the row partition
+ * of DESIGN.md §7).  Per partition, on its extended local system (owned rows [own_lo, own_hi)
+ * + 3 half-bandwidths of ghost rows; A^T, G, G^T of the extended system; w on all its rows):
+ *   1. sg_loss_norm_partial over the partition's OWNED entries -> a dd partial (2 doubles);
+ *      sg_loss_norm_combine adds the partials in partition order -> norm3 = {norm hi, lo, 1/norm};
+ *   2. sg_sai_loss_part_fwd -> t (n), z (n; exact on owned rows) and the dd partial of sum z^2
+ *      over the owned rows; sg_loss_sum_parts adds the partials in partition order (the loss);
+ *   3. the caller copies the neighbours' owned z into the ghost rows (the loss's only halo);
+ *   4. sg_sai_loss_part_bwd -> dL/dg for every entry of the owned rows (grad_out indexed like
+ *      the extended G; other entries untouched).
+ * Same arithmetic as sg_sai_loss row by row; only the dd partial sums are grouped per partition. */
+int sg_loss_norm_partial(const double* vals, int64_t nnz, int kind, double* part_out, void* ws, size_t* ws_bytes,
+                         void* stream);
+int sg_loss_norm_combine(const double* parts, int32_t n_parts, int64_t nnz_total, int kind, double* norm3_out,
+                         void* stream);
+int sg_sai_loss_part_fwd(int64_t n, const int32_t* a_offs, const int32_t* a_cols, const double* a_vals,
+                         const int32_t* g_offs, const int32_t* g_cols, const double* g_vals,
+                         const int32_t* gt_offs, const int32_t* gt_cols, const double* gt_vals, double eps,
+                         const double* w, const double* norm3, int64_t own_lo, int64_t own_hi, double* t_out,
+                         double* z64_out, double* part_out, void* ws, size_t* ws_bytes, void* stream);
+int sg_loss_sum_parts(const double* parts, int32_t n_parts, double* loss_host, void* stream);
+int sg_sai_loss_part_bwd(int64_t n, const int32_t* at_offs, const int32_t* at_cols, const double* at_vals,
+                         const int32_t* gt_offs, const int32_t* gt_cols, const double* gt_vals,
+                         const int32_t* g_offs, const int32_t* g_rows, const int32_t* g_cols, const double* w,
+                         const double* t, const double* z64, const double* norm3, int64_t own_lo, int64_t own_hi,
+                         double* grad_out, void* ws, size_t* ws_bytes, void* stream);
+
 /* ---- GNN training step (gnn.py:198-253 backward, training.py:126-147) ----
  * Plain fp64 primitives with fixed reduction orders (bit-reproducible runs); composed by
  * paper_2510_27517_b200/training.py into the training forward (all intermediates kept), the

@@ -81,6 +81,13 @@ SIGNATURES = {
     "sg_outer_sum": (C.c_int, [i64, i32, i32, vp, i32, vp, i32, vp, i32, vp, szp, vp]),
     "sg_adamw": (C.c_int, [i64, vp, vp, vp, vp, f64, f64, f64, f64, f64, i64, f64, vp]),
     "sg_fsai_build": (C.c_int, [i64, vp, vp, vp, vp, vp, vp, C.POINTER(C.c_int64), vp]),
+    "sg_loss_norm_partial": (C.c_int, [vp, i64, C.c_int, vp, vp, szp, vp]),
+    "sg_loss_norm_combine": (C.c_int, [vp, i32, i64, C.c_int, vp, vp]),
+    "sg_sai_loss_part_fwd": (C.c_int, [i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, f64, vp, vp, i64, i64, vp, vp, vp, vp,
+                                       szp, vp]),
+    "sg_loss_sum_parts": (C.c_int, [vp, i32, C.POINTER(C.c_double), vp]),
+    "sg_sai_loss_part_bwd": (C.c_int, [i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, i64, vp, vp, szp,
+                                       vp]),
     "sg_pcg_set_partition": (C.c_int, [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "sg_pcg_peer_info_size": (C.c_int, []),
     "sg_pcg_peer_export": (C.c_int, [vp, i64, i64, i32, vp]),

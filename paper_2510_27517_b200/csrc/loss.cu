@@ -230,3 +230,151 @@ extern "C" int sg_sai_loss(int64_t n, const int32_t* a_offs, const int32_t* a_co
   *loss_host = h[0];
   return SG_OK;
 }
+
+// ------------------------------------------------------------------ row-partitioned loss
+// The SAI loss of ONE system split like the row-partitioned PCG (BASELINE
+// configs[4] asks for the loss forward and backward on the partition).  Each partition works on
+// its extended local system (owned rows + 3 half-bandwidths of ghost rows): t, u and z come out
+// exact on the owned rows; the caller copies the neighbours' owned z into the ghost rows (the one
+// halo of the loss), after which du, v and dL/dg are exact for every entry of the owned rows.
+// The norm and the loss are dd sums over owned entries / rows, combined in partition order.
+namespace sg {
+
+__global__ void __launch_bounds__(LT) k_loss_rows_own(int64_t n, int64_t own_lo, int64_t own_hi,
+                                                      const int32_t* __restrict__ offs,
+                                                      const int32_t* __restrict__ cols,
+                                                      const double* __restrict__ vals, const double* __restrict__ u,
+                                                      const double* __restrict__ w, const dd* norm_p, double* z64,
+                                                      dd* part) {
+  __shared__ dd sh[LT];
+  const dd norm = *norm_p;
+  dd acc{0.0, 0.0};
+  for (int64_t i = blockIdx.x * (int64_t)LT + threadIdx.x; i < n; i += (int64_t)gridDim.x * LT) {
+    dd y{0.0, 0.0};
+    for (int32_t k = offs[i]; k < offs[i + 1]; ++k) y = dd_add(y, two_prod(vals[k], u[cols[k]]));
+    const double y64 = y.hi + y.lo;
+    dd z = dd_add(dd_div_d(dd{y64, 0.0}, norm), dd{-w[i], 0.0});
+    z64[i] = z.hi + z.lo;
+    if (i >= own_lo && i < own_hi) acc = dd_add(acc, dd_mul(z, z));
+  }
+  dd r = block_dd_sum(acc, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = r;
+}
+
+__global__ void __launch_bounds__(LT) k_dd_reduce(const dd* part, int nparts, dd* out) {
+  __shared__ dd sh[LT];
+  dd acc{0.0, 0.0};
+  for (int k = threadIdx.x; k < nparts; k += LT) acc = dd_add(acc, part[k]);
+  dd r = block_dd_sum(acc, sh);
+  if (threadIdx.x == 0) *out = r;
+}
+
+// partition partials (dd) in partition order; kind transform; out = {norm hi, norm lo, 1/norm}
+__global__ void k_norm_combine(const dd* parts, int P, int64_t nnz, int kind, double* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  dd r{0.0, 0.0};
+  for (int p = 0; p < P; ++p) r = dd_add(r, parts[p]);
+  if (kind == 0) r = dd_div_d(r, dd{(double)nnz, 0.0});
+  else if (kind == 1) r = dd_sqrt(r);
+  out[0] = r.hi;
+  out[1] = r.lo;
+  const dd inv = dd_div_d(dd{1.0, 0.0}, r);
+  out[2] = inv.hi + inv.lo;
+}
+
+__global__ void k_dd_sum_parts(const dd* parts, int P, double* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  dd r{0.0, 0.0};
+  for (int p = 0; p < P; ++p) r = dd_add(r, parts[p]);
+  *out = r.hi + r.lo;
+}
+
+}  // namespace sg
+
+extern "C" int sg_loss_norm_partial(const double* vals, int64_t nnz, int kind, double* part_out, void* ws,
+                                    size_t* ws_bytes, void* stream) {
+  const int NP = 148 * 4;
+  Carve c(ws);
+  dd* part = c.take<dd>(NP);
+  if (!ws) { *ws_bytes = c.off; return SG_OK; }
+  if (kind < 0 || kind > 2) { set_error("unknown norm kind"); return SG_EINVAL; }
+  cudaStream_t s = as_stream(stream);
+  k_norm_dd_partial<<<NP, LT, 0, s>>>(vals, nnz > 0 ? nnz : 0, kind, part);
+  k_dd_reduce<<<1, LT, 0, s>>>(part, NP, reinterpret_cast<dd*>(part_out));
+  SG_LAUNCH_CHECK("loss norm partial");
+  return SG_OK;
+}
+
+extern "C" int sg_loss_norm_combine(const double* parts, int32_t n_parts, int64_t nnz_total, int kind,
+                                    double* norm3_out, void* stream) {
+  if (n_parts < 1 || nnz_total < 1) { set_error("matrix norm is zero"); return SG_EINVAL; }
+  k_norm_combine<<<1, 32, 0, as_stream(stream)>>>(reinterpret_cast<const dd*>(parts), n_parts, nnz_total, kind,
+                                                  norm3_out);
+  SG_LAUNCH_CHECK("loss norm combine");
+  return SG_OK;
+}
+
+extern "C" int sg_sai_loss_part_fwd(int64_t n, const int32_t* a_offs, const int32_t* a_cols, const double* a_vals,
+                                    const int32_t* g_offs, const int32_t* g_cols, const double* g_vals,
+                                    const int32_t* gt_offs, const int32_t* gt_cols, const double* gt_vals,
+                                    double eps, const double* w, const double* norm3, int64_t own_lo,
+                                    int64_t own_hi, double* t_out, double* z64_out, double* part_out, void* ws,
+                                    size_t* ws_bytes, void* stream) {
+  const int NP = 148 * 4;
+  Carve c(ws);
+  double* u = c.take<double>(n + 2);
+  dd* part = c.take<dd>(NP);
+  if (!ws) { *ws_bytes = c.off; return SG_OK; }
+  if (*ws_bytes < c.off) { set_error("workspace too small"); return SG_EINVAL; }
+  if (n <= 0 || !(0 <= own_lo && own_lo < own_hi && own_hi <= n)) { set_error("bad owned row range"); return SG_EINVAL; }
+  cudaStream_t s = as_stream(stream);
+  const unsigned gr = (unsigned)ceil_div(n, kRows);
+  k_loss_spmv<kOrderSeq><<<gr, kRows, 0, s>>>(n, gt_offs, gt_cols, gt_vals, w, nullptr, 0.0, t_out);
+  k_loss_spmv<kOrderNumpy><<<gr, kRows, 0, s>>>(n, g_offs, g_cols, g_vals, t_out, w, eps, u);
+  k_loss_rows_own<<<NP, LT, 0, s>>>(n, own_lo, own_hi, a_offs, a_cols, a_vals, u, w,
+                                    reinterpret_cast<const dd*>(norm3), z64_out, part);
+  k_dd_reduce<<<1, LT, 0, s>>>(part, NP, reinterpret_cast<dd*>(part_out));
+  SG_LAUNCH_CHECK("partitioned sai loss forward");
+  return SG_OK;
+}
+
+extern "C" int sg_loss_sum_parts(const double* parts, int32_t n_parts, double* loss_host, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  double* out = nullptr;
+  SG_CUDA(cudaMallocAsync(&out, sizeof(double), s));
+  k_dd_sum_parts<<<1, 32, 0, s>>>(reinterpret_cast<const dd*>(parts), n_parts, out);
+  SG_LAUNCH_CHECK("loss sum");
+  SG_CUDA(cudaMemcpyAsync(loss_host, out, sizeof(double), cudaMemcpyDeviceToHost, s));
+  SG_CUDA(cudaFreeAsync(out, s));
+  SG_CUDA(cudaStreamSynchronize(s));
+  return SG_OK;
+}
+
+extern "C" int sg_sai_loss_part_bwd(int64_t n, const int32_t* at_offs, const int32_t* at_cols, const double* at_vals,
+                                    const int32_t* gt_offs, const int32_t* gt_cols, const double* gt_vals,
+                                    const int32_t* g_offs, const int32_t* g_rows, const int32_t* g_cols,
+                                    const double* w, const double* t, const double* z64, const double* norm3,
+                                    int64_t own_lo, int64_t own_hi, double* grad_out, void* ws, size_t* ws_bytes,
+                                    void* stream) {
+  const int NP = 148 * 4;
+  Carve c(ws);
+  double* dz = c.take<double>(n + 2);
+  double* du = c.take<double>(n + 2);
+  double* v = c.take<double>(n + 2);
+  if (!ws) { *ws_bytes = c.off; return SG_OK; }
+  if (*ws_bytes < c.off) { set_error("workspace too small"); return SG_EINVAL; }
+  if (n <= 0 || !(0 <= own_lo && own_lo < own_hi && own_hi <= n)) { set_error("bad owned row range"); return SG_EINVAL; }
+  cudaStream_t s = as_stream(stream);
+  int32_t e[2];
+  SG_CUDA(cudaMemcpyAsync(&e[0], g_offs + own_lo, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  SG_CUDA(cudaMemcpyAsync(&e[1], g_offs + own_hi, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  SG_CUDA(cudaStreamSynchronize(s));
+  const unsigned gr = (unsigned)ceil_div(n, kRows);
+  k_dz<<<NP, LT, 0, s>>>(n, z64, norm3 + 1, dz);  // scal[1] = norm3[2] = 1 / norm
+  k_loss_spmv<kOrderSeq><<<gr, kRows, 0, s>>>(n, at_offs, at_cols, at_vals, dz, nullptr, 0.0, du);
+  k_loss_spmv<kOrderSeq><<<gr, kRows, 0, s>>>(n, gt_offs, gt_cols, gt_vals, du, nullptr, 0.0, v);
+  if (e[1] > e[0])
+    k_grad<<<NP, LT, 0, s>>>(e[1] - e[0], g_rows + e[0], g_cols + e[0], du, t, w, v, grad_out + e[0]);
+  SG_LAUNCH_CHECK("partitioned sai loss backward");
+  return SG_OK;
+}

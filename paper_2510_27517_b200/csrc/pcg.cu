@@ -324,6 +324,14 @@ __device__ __forceinline__ Own own_of(const Dev& D, int sys) {
   return w;
 }
 __device__ __forceinline__ bool owned(const Own& w, long long i) { return i >= w.o0 && i < w.o1; }
+// The streamed kernels take the partition logic as a template flag: without it the owned-row
+// tests fold away and the push branch disappears (no registers spent on it: K2+K3 keeps 3 CTAs
+// per SM).
+template <bool PART>
+__device__ __forceinline__ Own own_get(const Dev& D, int sys) {
+  if constexpr (PART) return own_of(D, sys);
+  else return Own{LLONG_MIN, LLONG_MAX, 0, 0, nullptr, nullptr};
+}
 // s of an owned row: local store plus the pushes into the neighbours' ghost rows
 __device__ __forceinline__ void store_s(const Dev& D, const Own& w, long long i, double v) {
   D.s[i] = v;
@@ -1204,7 +1212,7 @@ __device__ __forceinline__ long long clampr(long long j, long long s0, long long
 
 // K1 with d' staged: d'[j] = s[j] + beta d[j] for j in tile +- H, then q = A d'.
 // NH = ceil(H / PR) fixes the trip counts of the staging loops.
-template <int FMT, int ND, int NH>
+template <int FMT, int ND, int NH, bool PART = false>
 __global__ void __launch_bounds__(PR, 6) k_iter1_st(Dev D, int par) {
   extern __shared__ double sm[];
   __shared__ double red[PR / 32];
@@ -1214,7 +1222,7 @@ __global__ void __launch_bounds__(PR, 6) k_iter1_st(Dev D, int par) {
   const int status = D.st[sys].status;
   if (status == ST_DONE) return;
   sys_bounds(D, sys, s0, s1);
-  const Own ow = own_of(D, sys);
+  const Own ow = own_get<PART>(D, sys);
   const bool run = status == ST_RUN;
   const bool fresh = run ? (D.st[sys].flags & FL_FRESH) != 0 : true;
   const double beta = D.st[sys].beta;
@@ -1274,7 +1282,7 @@ __global__ void __launch_bounds__(PR, 6) k_iter1_st(Dev D, int par) {
   if (arrive(D, sys, pdq, prr, red, &flag)) {
     const double dq = gather_partials(D, sys, 0, red);
     const double rrf = gather_partials(D, sys, 1, red);
-    if (threadIdx.x == 0) { if (D.part) part_fin(D, sys, FIN_K1, dq, rrf, run); else fin_k1(D, sys, run, dq, rrf); }
+    if (threadIdx.x == 0) { if (PART) part_fin(D, sys, FIN_K1, dq, rrf, run); else fin_k1(D, sys, run, dq, rrf); }
   }
 }
 
@@ -1282,7 +1290,7 @@ __global__ void __launch_bounds__(PR, 6) k_iter1_st(Dev D, int par) {
 //   sr[j - (r0-2H)] = r'[j] = r[j] - alpha q[j]   j in tile +- 2H
 //   st[j - (r0-H)]  = t[j]  = (G^T r')[j]          j in tile +- H
 //   s[i] = G t + eps r'                             own rows;  partials ||r'||^2, r'.s
-template <int ND, int NH>
+template <int ND, int NH, bool PART = false>
 __global__ void __launch_bounds__(PR, 5) k_iter23_st(Dev D, int par) {
   extern __shared__ double sm[];
   __shared__ double red[PR / 32];
@@ -1291,7 +1299,7 @@ __global__ void __launch_bounds__(PR, 5) k_iter23_st(Dev D, int par) {
   block_rows(D, sys, r0, r1);
   if (D.st[sys].status != ST_RUN) return;
   sys_bounds(D, sys, s0, s1);
-  const Own ow = own_of(D, sys);
+  const Own ow = own_get<PART>(D, sys);
   const double alpha = D.st[sys].alpha;
   const double eps = D.ctl->eps;
   const double* dn = par ? D.d0 : D.d1;
@@ -1381,7 +1389,7 @@ __global__ void __launch_bounds__(PR, 5) k_iter23_st(Dev D, int par) {
     const double rr = gather_partials(D, sys, 0, red);
     const double rs = gather_partials(D, sys, 1, red);
     if (threadIdx.x == 0) {
-      if (D.part) {
+      if (PART) {
         part_fin(D, sys, FIN_K23, rr, rs, 0);
       } else {
         D.st[sys].rr = rr;
@@ -1445,8 +1453,8 @@ __device__ __forceinline__ int ring_nb(int base, const int (&off)[ND], int d, in
   }
 }
 
-template <int ND, int NH>
-__global__ void __launch_bounds__(PR, 1) k_iter23_sw(Dev D, int par) {
+template <int ND, int NH, bool PART = false>
+__global__ void __launch_bounds__(PR, PART ? 3 : 1) k_iter23_sw(Dev D, int par) {
   using G = Sw23<ND, NH>;
   constexpr int C = G::C, P = G::P, NG = G::NG, NT = G::NT, GR = G::GR, TR = G::TR;
   extern __shared__ __align__(128) unsigned char smraw[];
@@ -1480,8 +1488,8 @@ __global__ void __launch_bounds__(PR, 1) k_iter23_sw(Dev D, int par) {
   const int K = m1 + 2 * NH + 1;                     // steps
   auto rel = [&](long long v) { return (int)(v - LB < -1 ? -1 : (v - LB > (1LL << 30) ? (1LL << 30) : v - LB)); };
   const int s0r = rel(s0), s1r = rel(s1), R0r = rel(R0), R1r = rel(R1);
-  const Own ow = own_of(D, sys);
-  const int o0r = rel(ow.o0), o1r = rel(ow.o1);
+  const Own ow = own_get<PART>(D, sys);
+  const int o0r = PART ? rel(ow.o0) : INT_MIN, o1r = PART ? rel(ow.o1) : INT_MAX;
   int off[ND];
 #pragma unroll
   for (int d = 0; d < ND; ++d) off[d] = D.dia.off[d];
@@ -1565,7 +1573,7 @@ __global__ void __launch_bounds__(PR, 1) k_iter23_sw(Dev D, int par) {
     const double rr = gather_partials(D, D.sys_rng0, sys, 0, red);
     const double rs = gather_partials(D, D.sys_rng0, sys, 1, red);
     if (threadIdx.x == 0) {
-      if (D.part) {
+      if (PART) {
         part_fin(D, sys, FIN_K23, rr, rs, 0);
       } else {
         D.st[sys].rr = rr;
@@ -1604,7 +1612,7 @@ struct Sw1 {
   static constexpr size_t SMEM = (size_t)NA * RING * 8 + (size_t)DRING * 8 + (size_t)P * 2 * C * 8 + RING;
 };
 
-template <int FMT, int ND, int NH, bool CS = false>
+template <int FMT, int ND, int NH, bool CS = false, bool PART = false>
 __global__ void __launch_bounds__(PR, 5) k_iter1_sw(Dev D, int par) {
   static_assert(!CS || (FMT == 2 && ND == 5), "coefficient stencil: 5-point symmetric DIA only");
   using G = Sw1<FMT, ND, NH, CS>;
@@ -1633,7 +1641,7 @@ __global__ void __launch_bounds__(PR, 5) k_iter1_sw(Dev D, int par) {
   const double* dc = par ? D.d1 : D.d0;
   double* dn = par ? D.d0 : D.d1;
   double* rc = par ? D.r1 : D.r0;
-  const Own ow = own_of(D, sys);
+  const Own ow = own_get<PART>(D, sys);
   double pdq = 0.0, prr = 0.0;
   if (run) {
     double* ar = reinterpret_cast<double*>(smraw);  // [NA][RING]
@@ -1645,7 +1653,7 @@ __global__ void __launch_bounds__(PR, 5) k_iter1_sw(Dev D, int par) {
     const int K = m1 + NH + 1;
     auto rel = [&](long long v) { return (int)(v - LB < -1 ? -1 : (v - LB > (1LL << 30) ? (1LL << 30) : v - LB)); };
     const int s0r = rel(s0), s1r = rel(s1), R0r = rel(R0), R1r = rel(R1);
-    const int o0r = rel(ow.o0), o1r = rel(ow.o1);
+    const int o0r = PART ? rel(ow.o0) : INT_MIN, o1r = PART ? rel(ow.o1) : INT_MAX;
     int off[ND];
 #pragma unroll
     for (int d = 0; d < ND; ++d) off[d] = D.dia.off[d];
@@ -1741,7 +1749,7 @@ __global__ void __launch_bounds__(PR, 5) k_iter1_sw(Dev D, int par) {
     const double dq = gather_partials(D, D.sys_rng0, sys, 0, red);
     const double rrf = gather_partials(D, D.sys_rng0, sys, 1, red);
     if (threadIdx.x == 0) {
-      if (D.part) {
+      if (PART) {
         part_fin(D, sys, FIN_K1, dq, rrf, run);
       } else {
         if (pend) D.st[sys].flags = (D.st[sys].flags & ~(FL_XPEND | FL_DPAR)) | (fresh ? FL_XINT : 0);
@@ -1777,7 +1785,8 @@ struct Strip23 {
                                  (size_t)P * (kStripSP + 2 * kStripC) * 8 + (size_t)kStripRL * kStripMK;
 };
 
-__global__ void __launch_bounds__(PR, 1) k_iter23_s5(Dev D, int par) {
+template <bool PART = false>
+__global__ void __launch_bounds__(PR, PART ? 3 : 1) k_iter23_s5(Dev D, int par) {
   constexpr int SP = kStripSP, RL = kStripRL, P = Strip23::P, C = kStripC, E = kStripE;
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ __align__(8) uint64_t bars[P];
@@ -1794,7 +1803,7 @@ __global__ void __launch_bounds__(PR, 1) k_iter23_s5(Dev D, int par) {
   const long long y0 = r0 / W, nl = (s1 - s0) / W;
   const long long y1 = y0 + D.rng_len < nl ? y0 + D.rng_len : nl;
   const int cx = (int)(W - x0 < C ? W - x0 : C);  // own columns of this strip
-  const Own ow = own_of(D, sys);
+  const Own ow = own_get<PART>(D, sys);
   const double alpha = D.st[sys].alpha;
   const double eps = D.ctl->eps;
   const double* dn = par ? D.d0 : D.d1;
@@ -1903,7 +1912,7 @@ __global__ void __launch_bounds__(PR, 1) k_iter23_s5(Dev D, int par) {
     const double rr = gather_partials(D, D.sys_rng0, sys, 0, red);
     const double rs = gather_partials(D, D.sys_rng0, sys, 1, red);
     if (threadIdx.x == 0) {
-      if (D.part) {
+      if (PART) {
         part_fin(D, sys, FIN_K23, rr, rs, 0);
       } else {
         D.st[sys].rr = rr;
@@ -1923,7 +1932,7 @@ struct Strip1 {
                                  (size_t)kStripRL * kStripMK;
 };
 
-template <int FMT>
+template <int FMT, bool PART = false>
 __global__ void __launch_bounds__(PR, 4) k_iter1_s5(Dev D, int par) {
   constexpr int SP = kStripSP, RL = kStripRL, P = Strip1<FMT>::P, NA = Strip1<FMT>::NA, E = kStripE;
   extern __shared__ __align__(128) unsigned char smraw[];
@@ -1942,7 +1951,7 @@ __global__ void __launch_bounds__(PR, 4) k_iter1_s5(Dev D, int par) {
   const long long y0 = r0 / W, nl = (s1 - s0) / W;
   const long long y1 = y0 + D.rng_len < nl ? y0 + D.rng_len : nl;
   const int cx = (int)(W - x0 < kStripC ? W - x0 : kStripC);
-  const Own ow = own_of(D, sys);
+  const Own ow = own_get<PART>(D, sys);
   const bool run = status == ST_RUN;
   const bool fresh = run ? (D.st[sys].flags & FL_FRESH) != 0 : true;
   const double beta = D.st[sys].beta;
@@ -2034,7 +2043,7 @@ __global__ void __launch_bounds__(PR, 4) k_iter1_s5(Dev D, int par) {
   if (arrive(D, D.sys_rng0, sys, pdq, prr, red, &flag)) {
     const double dq = gather_partials(D, D.sys_rng0, sys, 0, red);
     const double rrf = gather_partials(D, D.sys_rng0, sys, 1, red);
-    if (threadIdx.x == 0) { if (D.part) part_fin(D, sys, FIN_K1, dq, rrf, run); else fin_k1(D, sys, run, dq, rrf); }
+    if (threadIdx.x == 0) { if (PART) part_fin(D, sys, FIN_K1, dq, rrf, run); else fin_k1(D, sys, run, dq, rrf); }
   }
 }
 
@@ -2167,31 +2176,43 @@ int launch_iteration(sg_pcg* h, cudaStream_t s, int par, bool refresh, cudaEvent
     const size_t tile = (size_t)PR * kRpt, H = (size_t)h->D.dia.halo;
     const unsigned gr = (unsigned)h->nrng;
     const bool strip = FMT >= 1 && ND == 5 && h->strip;
-    if (strip) k_iter1_s5<FS><<<gr, PR, Strip1<FS>::SMEM, s>>>(h->D, par);
-    else if (st && h->k1sw && FMT == 2 && ND == 5 && h->cst) {  // A from the coefficient stencil
-      if (H <= PR) k_iter1_sw<2, 5, 1, true><<<gr, PR, Sw1<2, 5, 1, true>::SMEM, s>>>(h->D, par);
-      else k_iter1_sw<2, 5, 2, true><<<gr, PR, Sw1<2, 5, 2, true>::SMEM, s>>>(h->D, par);
-    } else if (st && h->k1sw) {
-      if (H <= PR) k_iter1_sw<FS, NS, 1><<<gr, PR, Sw1<FS, NS, 1>::SMEM, s>>>(h->D, par);
-      else k_iter1_sw<FS, NS, 2><<<gr, PR, Sw1<FS, NS, 2>::SMEM, s>>>(h->D, par);
-    } else if (st && H <= PR) k_iter1_st<FS, NS, 1><<<g, PR, (tile + 2 * H) * sizeof(double), s>>>(h->D, par);
-    else if (st) k_iter1_st<FS, NS, 2><<<g, PR, (tile + 2 * H) * sizeof(double), s>>>(h->D, par);
-    else if (FMT == 0 && !SH) {  // CSR, long rows: d' first, then one gather per nonzero
+    // the streamed kernels exist with and without the row-partition logic (PART)
+    auto k1_streamed = [&](auto Pc) {
+      constexpr bool PT = decltype(Pc)::value;
+      if (strip) k_iter1_s5<FS, PT><<<gr, PR, Strip1<FS>::SMEM, s>>>(h->D, par);
+      else if (st && h->k1sw && FMT == 2 && ND == 5 && h->cst && !PT) {  // A from the coefficient stencil
+        if (H <= PR) k_iter1_sw<2, 5, 1, true><<<gr, PR, Sw1<2, 5, 1, true>::SMEM, s>>>(h->D, par);
+        else k_iter1_sw<2, 5, 2, true><<<gr, PR, Sw1<2, 5, 2, true>::SMEM, s>>>(h->D, par);
+      } else if (st && h->k1sw) {
+        if (H <= PR) k_iter1_sw<FS, NS, 1, false, PT><<<gr, PR, Sw1<FS, NS, 1>::SMEM, s>>>(h->D, par);
+        else k_iter1_sw<FS, NS, 2, false, PT><<<gr, PR, Sw1<FS, NS, 2>::SMEM, s>>>(h->D, par);
+      } else if (H <= PR) k_iter1_st<FS, NS, 1, PT><<<g, PR, (tile + 2 * H) * sizeof(double), s>>>(h->D, par);
+      else k_iter1_st<FS, NS, 2, PT><<<g, PR, (tile + 2 * H) * sizeof(double), s>>>(h->D, par);
+    };
+    auto k23_streamed = [&](auto Pc) {
+      constexpr bool PT = decltype(Pc)::value;
+      if (strip) {
+        k_iter23_s5<PT><<<gr, PR, Strip23::SMEM, s>>>(h->D, par);
+      } else if (h->k23 == 1) {
+        if (H <= PR) k_iter23_sw<NS, 1, PT><<<gr, PR, Sw23<NS, 1>::SMEM, s>>>(h->D, par);
+        else k_iter23_sw<NS, 2, PT><<<gr, PR, Sw23<NS, 2>::SMEM, s>>>(h->D, par);
+      } else {
+        if (H <= PR) k_iter23_st<NS, 1, PT><<<g, PR, (2 * tile + 6 * H) * sizeof(double), s>>>(h->D, par);
+        else k_iter23_st<NS, 2, PT><<<g, PR, (2 * tile + 6 * H) * sizeof(double), s>>>(h->D, par);
+      }
+    };
+    if (strip || st) {
+      if (h->part) k1_streamed(std::true_type{});
+      else k1_streamed(std::false_type{});
+    } else if (FMT == 0 && !SH) {  // CSR, long rows: d' first, then one gather per nonzero
       k_pre_d<<<g, PR, 0, s>>>(h->D, par); ++k;
       k_iter1<PRE, FMT, ND, SH, true><<<g, PR, 0, s>>>(h->D, par);
     } else k_iter1<PRE, FMT, ND, SH><<<g, PR, 0, s>>>(h->D, par);
     ++k;
     if (ev) SG_CUDA(cudaEventRecordWithFlags(ev[1], s, cudaEventRecordExternal));
     if ((st || strip) && !refresh && PRE == SG_PRECOND_LEARNED) {  // K2 + K3 fused
-      if (strip) {
-        k_iter23_s5<<<gr, PR, Strip23::SMEM, s>>>(h->D, par);
-      } else if (h->k23 == 1) {
-        if (H <= PR) k_iter23_sw<NS, 1><<<gr, PR, Sw23<NS, 1>::SMEM, s>>>(h->D, par);
-        else k_iter23_sw<NS, 2><<<gr, PR, Sw23<NS, 2>::SMEM, s>>>(h->D, par);
-      } else {
-        if (H <= PR) k_iter23_st<NS, 1><<<g, PR, (2 * tile + 6 * H) * sizeof(double), s>>>(h->D, par);
-        else k_iter23_st<NS, 2><<<g, PR, (2 * tile + 6 * H) * sizeof(double), s>>>(h->D, par);
-      }
+      if (h->part) k23_streamed(std::true_type{});
+      else k23_streamed(std::false_type{});
       ++k;
       if (ev) {
         SG_CUDA(cudaEventRecordWithFlags(ev[2], s, cudaEventRecordExternal));
@@ -2391,6 +2412,12 @@ int sw_attr(int* per_sm) {
                                (int)Sw1<1, ND, NH>::SMEM));
   SG_CUDA(cudaFuncSetAttribute(k_iter1_sw<2, ND, NH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)Sw1<2, ND, NH>::SMEM));
+  SG_CUDA(cudaFuncSetAttribute(k_iter23_sw<ND, NH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)Sw23<ND, NH>::SMEM));
+  SG_CUDA(cudaFuncSetAttribute(k_iter1_sw<1, ND, NH, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)Sw1<1, ND, NH>::SMEM));
+  SG_CUDA(cudaFuncSetAttribute(k_iter1_sw<2, ND, NH, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)Sw1<2, ND, NH>::SMEM));
   if constexpr (ND == 5)
     SG_CUDA(cudaFuncSetAttribute(k_iter1_sw<2, 5, NH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)Sw1<2, 5, NH, true>::SMEM));
@@ -2400,10 +2427,13 @@ int sw_attr(int* per_sm) {
 }
 
 int strip_setup(int* per_sm) {
-  SG_CUDA(cudaFuncSetAttribute(k_iter23_s5, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Strip23::SMEM));
+  SG_CUDA(cudaFuncSetAttribute(k_iter23_s5<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Strip23::SMEM));
+  SG_CUDA(cudaFuncSetAttribute(k_iter23_s5<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Strip23::SMEM));
   SG_CUDA(cudaFuncSetAttribute(k_iter1_s5<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Strip1<1>::SMEM));
   SG_CUDA(cudaFuncSetAttribute(k_iter1_s5<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Strip1<2>::SMEM));
-  SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_iter23_s5, PR, Strip23::SMEM));
+  SG_CUDA(cudaFuncSetAttribute(k_iter1_s5<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Strip1<1>::SMEM));
+  SG_CUDA(cudaFuncSetAttribute(k_iter1_s5<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Strip1<2>::SMEM));
+  SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_iter23_s5<false>, PR, Strip23::SMEM));
   if (*per_sm < 1) *per_sm = 1;
   return SG_OK;
 }

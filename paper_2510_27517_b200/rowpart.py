@@ -667,6 +667,74 @@ class PartitionedSolver:
         return report_from(res[0], x, hist, 0, self.handle.last_elapsed_ns)
 
 
+    def sai_loss_and_grad(self, w, epsilon: float | None = None, norm_kind: str = "mean_abs_nonzero"):
+        """The SAI loss ||(A (G G^T + eps I) w)/||A|| - w||^2 and dL/dg (training.py:57-94, the
+        tape backward autodiff.py:203-239, 265-303) on the row partition: every partition
+        evaluates its extended system; the one halo is z (neighbours' owned rows into the ghost
+        rows, here a device copy between the partitions' buffers), the norm and loss partials add
+        in partition order.  Returns (loss, [dL/dg of each partition's extended G, exact on the
+        entries of its owned rows])."""
+        import ctypes
+
+        import torch
+
+        from . import _lib as L
+        from .training import NORM_KINDS
+        lib = L.lib()
+        kind = NORM_KINDS.index(norm_kind)
+        eps = self.model.config.epsilon if epsilon is None else float(epsilon)
+        w = np.asarray(w, dtype=np.float64)
+        P_ = len(self.factors)
+        mats = []
+        for f in self.factors:
+            ne = f.ext[1] - f.ext[0]
+            from .sparse import DeviceCsr
+            a = DeviceCsr(ne, ne, f.offs, f.cols, f.a_vals)
+            g = a.with_values(f.g_vals)
+            mats.append((a, a.transpose(), g, g.transpose()))
+        parts = L.empty(2 * P_, torch.float64)
+        for p, f in enumerate(self.factors):
+            a = mats[p][0]
+            lo, hi = f.own[0] - f.ext[0], f.own[1] - f.ext[0]
+            e_lo, e_hi = int(a.offs[lo].item()), int(a.offs[hi].item())
+            L.call_ws(lib.sg_loss_norm_partial, L.ptr(a.vals[e_lo:e_hi]), e_hi - e_lo, kind, L.ptr(parts[2 * p:]),
+                      what="loss norm partial")
+        norm3 = L.empty(3, torch.float64)
+        nnz_total = int(self.A.nnz)
+        L.check(lib.sg_loss_norm_combine(L.ptr(parts), P_, nnz_total, kind, L.ptr(norm3), L.stream_ptr()))
+        ts, zs, ws_ = [], [], []
+        lparts = L.empty(2 * P_, torch.float64)
+        for p, f in enumerate(self.factors):
+            a, _, g, gt = mats[p]
+            ne = a.n_rows
+            wd = L.to_device(np.ascontiguousarray(w[f.ext[0]:f.ext[1]]), torch.float64)
+            t, z = L.empty(ne, torch.float64), L.empty(ne, torch.float64)
+            L.call_ws(lib.sg_sai_loss_part_fwd, ne, L.ptr(a.offs), L.ptr(a.cols), L.ptr(a.vals), L.ptr(g.offs),
+                      L.ptr(g.cols), L.ptr(g.vals), L.ptr(gt.offs), L.ptr(gt.cols), L.ptr(gt.vals), eps, L.ptr(wd),
+                      L.ptr(norm3), f.own[0] - f.ext[0], f.own[1] - f.ext[0], L.ptr(t), L.ptr(z),
+                      L.ptr(lparts[2 * p:]), what="partitioned loss forward")
+            ts.append(t), zs.append(z), ws_.append(wd)
+        for p, f in enumerate(self.factors):  # the z halo: neighbours' owned rows -> my ghost rows
+            for q in (p - 1, p + 1):
+                if 0 <= q < P_:
+                    fq = self.factors[q]
+                    r0, r1 = max(f.ext[0], fq.own[0]), min(f.ext[1], fq.own[1])
+                    if r0 < r1:
+                        zs[p][r0 - f.ext[0]:r1 - f.ext[0]].copy_(zs[q][r0 - fq.ext[0]:r1 - fq.ext[0]])
+        loss = ctypes.c_double(0.0)
+        L.check(lib.sg_loss_sum_parts(L.ptr(lparts), P_, ctypes.byref(loss), L.stream_ptr()))
+        grads = []
+        for p, f in enumerate(self.factors):
+            a, at, g, gt = mats[p]
+            grad = L.zeros(g.nnz, torch.float64)
+            L.call_ws(lib.sg_sai_loss_part_bwd, a.n_rows, L.ptr(at.offs), L.ptr(at.cols), L.ptr(at.vals),
+                      L.ptr(gt.offs), L.ptr(gt.cols), L.ptr(gt.vals), L.ptr(g.offs), L.ptr(g.rows()), L.ptr(g.cols),
+                      L.ptr(ws_[p]), L.ptr(ts[p]), L.ptr(zs[p]), L.ptr(norm3), f.own[0] - f.ext[0],
+                      f.own[1] - f.ext[0], L.ptr(grad), what="partitioned loss backward")
+            grads.append(grad)
+        return float(loss.value), grads
+
+
 def solve_partitioned(A, meta, model, b, parts: int, cfg=None):
     """GNN build + PCG of one system split into `parts` row partitions on this GPU (group
     mode).  Same result as pcg_solve on the whole system up to the order of the dot-product

@@ -43,7 +43,9 @@ def test_partitioned_solve_matches_whole_system(grid, parts, fused):
     rep = sol.solve(b, cfg)
     assert rep.converged and ref.converged
     assert abs(rep.k - ref.k) <= max(1, 0.02 * ref.k), (rep.k, ref.k)
-    np.testing.assert_allclose(rep.residual_history[:60], ref.residual_history[:60], rtol=1e-6, atol=1e-9)
+    # partials are grouped per partition: the histories start equal to rounding (1e-16) and the
+    # Krylov recurrence amplifies that slowly; a wrong ghost value would show at once
+    np.testing.assert_allclose(rep.residual_history[:25], ref.residual_history[:25], rtol=1e-11)
     o, c, v = A.row_offsets, A.col_indices, A.values
     assert np.linalg.norm(b - O.spmv(o, c, v, rep.x)) / np.linalg.norm(b) <= 1e-9
     assert sol.handle.stats()[2][7] == float(fused)
@@ -93,3 +95,26 @@ def test_c5_four_partitions():
     np.testing.assert_allclose(rep.residual_history[:50], ref.residual_history[:50], rtol=1e-9)
     o, c, v = A.row_offsets, A.col_indices, A.values
     assert np.linalg.norm(b - O.spmv(o, c, v, rep.x)) / np.linalg.norm(b) <= 1e-6
+
+
+@pytest.mark.parametrize("parts", [1, 3])
+def test_partitioned_sai_loss_and_grad(parts):
+    """Loss forward + backward on the row partition == the whole-system loss (1e-13) and its
+    dL/dg on every owned entry (1e-12)."""
+    m = P.load_checkpoint(CKPT)
+    A, meta = P.gen_poisson2d(60, 45, coeff_seed=2)
+    G = P.forward(m, P.build_graph(A, meta)).G
+    w = np.random.default_rng(0).standard_normal(A.n_rows)
+    loss_ref, grad_ref = P.sai_loss_and_grad(A, G, m.config.epsilon, w)
+    sol = RP.PartitionedSolver(A, meta, m, parts)
+    loss, grads = sol.sai_loss_and_grad(w)
+    assert abs(loss - loss_ref) <= 1e-13 * abs(loss_ref)
+    o = A.row_offsets
+    scale = np.max(np.abs(grad_ref))
+    for f, gp in zip(sol.factors, grads):
+        fo = f.offs.cpu().numpy()
+        gp = gp.cpu().numpy()
+        lo, hi = f.own[0] - f.ext[0], f.own[1] - f.ext[0]
+        ours = gp[fo[lo]:fo[hi]]
+        ref = grad_ref[o[f.own[0]]:o[f.own[1]]]
+        np.testing.assert_allclose(ours, ref, rtol=1e-12, atol=1e-12 * scale)
