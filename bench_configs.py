@@ -32,6 +32,8 @@ def main():
     p.add_argument("--warmup", type=int, default=1)
     p.add_argument("--max-iters", type=int, default=None)
     p.add_argument("--cpu", action="store_true", help="also time the CPU restatement (c1 only)")
+    p.add_argument("--parts", type=int, default=0,
+                   help="c5: solve through the row partition with this many partitions on this GPU (group mode)")
     a = p.parse_args()
 
     import torch
@@ -76,6 +78,9 @@ def main():
     cfg = P.SolveConfig(rtol=1e-6, max_iters=a.max_iters)
     b_dev = torch.as_tensor(b, device=dev)
     w_dev = torch.as_tensor(np.random.default_rng(0).standard_normal(A.n_rows), device=dev)
+
+    if a.parts:
+        return run_parts(a, P, A, meta, model, b)
 
     def step(profile=False):
         g = P.build_graph(Ap if a.config == "c4" else A, meta if a.config not in ("c3", "c4") else None)
@@ -151,6 +156,42 @@ def main():
         out["cpu_baseline"] = {"value": 1.0 / (time.perf_counter() - t0), "unit": "solves/s", "cores": 1,
                                "kind": "port", "k": k_ref}
     print(json.dumps(out), flush=True)
+
+
+def run_parts(a, P, A, meta, model, b):
+    """C5 through the row partition in group mode (the P-rank emulation on one GPU): setup
+    (per-partition GNN blocks, extended systems, handle) and solve timed separately."""
+    import torch
+
+    from paper_2510_27517_b200.rowpart import PartitionedSolver
+    cfg = P.SolveConfig(rtol=1e-6, max_iters=a.max_iters)
+    for _ in range(max(a.warmup, 1)):
+        PartitionedSolver(A, meta, model, a.parts).solve(b, cfg)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    sol = PartitionedSolver(A, meta, model, a.parts)
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t0
+    sol.handle.set_profile(True)
+    sol.solve(b, cfg)
+    sol.handle.stats(reset=True)
+    times = []
+    for _ in range(a.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rep = sol.solve(b, cfg)
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+    _, _, prof = sol.handle.stats()
+    per = {}
+    if prof[4] > 0:
+        per = {"k_iter1_ms": prof[0] / prof[4], "k_iter23_ms": prof[1] / prof[4]}
+    ms = 1000 * float(np.median(times))
+    ext_rows = int(sol.row_start[-1])
+    print(json.dumps({"config": "c5", "parts": a.parts, "mode": "group (one handle, one GPU)",
+                      "k": rep.k, "converged": rep.converged, "solve_ms": ms, "setup_ms": 1000 * t_setup,
+                      "us_per_iteration": 1000 * ms / max(rep.k, 1), "extended_rows": ext_rows,
+                      "ghost_overhead": ext_rows / A.n_rows - 1.0, "per_kernel": per}), flush=True)
 
 
 if __name__ == "__main__":
