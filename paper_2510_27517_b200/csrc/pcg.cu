@@ -1454,7 +1454,7 @@ __device__ __forceinline__ int ring_nb(int base, const int (&off)[ND], int d, in
 }
 
 template <int ND, int NH, bool PART = false>
-__global__ void __launch_bounds__(PR, 3) k_iter23_sw(Dev D, int par) {
+__global__ void __launch_bounds__(PR, PART ? 3 : 1) k_iter23_sw(Dev D, int par) {
   using G = Sw23<ND, NH>;
   constexpr int C = G::C, P = G::P, NG = G::NG, NT = G::NT, GR = G::GR, TR = G::TR;
   extern __shared__ __align__(128) unsigned char smraw[];
@@ -1493,23 +1493,15 @@ __global__ void __launch_bounds__(PR, 3) k_iter23_sw(Dev D, int par) {
   int off[ND];
 #pragma unroll
   for (int d = 0; d < ND; ++d) off[d] = D.dia.off[d];
-  // the chunk's ND + 3 bulk copies are spread over the CTA's warps (lane 0 of warp w issues copies
-  // w, w + 8, ...; warp 0 also arms the barrier): issuing them from one thread put ~40
-  // instructions per copy on one warp's critical path between the CTA barriers
-  const int wq = tid >> 5;
-  const bool issuer = (tid & 31) == 0;
   auto issue = [&](int k) {
     const int ss = k % P, gs = (k % NG) * C;
     const long long row = LB + (long long)k * C;
-    if (wq == 0) mbar_arrive_expect_tx(&bars[ss], (uint32_t)((2 + ND) * C * 8 + C));
+    mbar_arrive_expect_tx(&bars[ss], (uint32_t)((2 + ND) * C * 8 + C));
+    bulk_g2s(rp + gs, rc + row, C * 8, &bars[ss]);
+    bulk_g2s(qs + ss * C, D.q + row, C * 8, &bars[ss]);
 #pragma unroll
-    for (int c = 0; c < ND + 3; ++c) {
-      if ((c & 7) != wq) continue;
-      if (c == 0) bulk_g2s(rp + gs, rc + row, C * 8, &bars[ss]);
-      else if (c == 1) bulk_g2s(qs + ss * C, D.q + row, C * 8, &bars[ss]);
-      else if (c < 2 + ND) bulk_g2s(gr + (c - 2) * GR + gs, D.dia.gv[c - 2] + row, C * 8, &bars[ss]);
-      else bulk_g2s(mk + gs, D.dia.mask + row, C, &bars[ss]);
-    }
+    for (int d = 0; d < ND; ++d) bulk_g2s(gr + d * GR + gs, D.dia.gv[d] + row, C * 8, &bars[ss]);
+    bulk_g2s(mk + gs, D.dia.mask + row, C, &bars[ss]);
   };
   if (tid == 0) {
 #pragma unroll
@@ -1517,7 +1509,7 @@ __global__ void __launch_bounds__(PR, 3) k_iter23_sw(Dev D, int par) {
     mbar_init_fence();
   }
   __syncthreads();
-  if (issuer)
+  if (tid == 0)
     for (int k = 0; k < P - 1 && k < K; ++k) issue(k);
   double prr = 0.0, prs = 0.0;
   for (int k = 0; k < K; ++k) {
@@ -1544,7 +1536,7 @@ __global__ void __launch_bounds__(PR, 3) k_iter23_sw(Dev D, int par) {
       rp[ix] = v;
     }
     __syncthreads();
-    if (issuer && k + P - 1 < K) issue(k + P - 1);
+    if (tid == 0 && k + P - 1 < K) issue(k + P - 1);
     const int u = k - NH;
     if (u >= NH) {  // B: t of chunk u (add.at order over G's mirror diagonals)
       const int lj = u * C + tid, base = (u % NG) * C + tid;
@@ -1665,26 +1657,19 @@ __global__ void __launch_bounds__(PR, 5) k_iter1_sw(Dev D, int par) {
     int off[ND];
 #pragma unroll
     for (int d = 0; d < ND; ++d) off[d] = D.dia.off[d];
-    // copies spread over the warps (see k_iter23_sw)
-    const int wq = tid >> 5;
-    const bool issuer = (tid & 31) == 0;
     auto issue = [&](int k) {
       const int ss = k % P, gs = (k % NR) * C;
       double* st = stg + ss * 2 * C;
       const long long row = LB + (long long)k * C;
-      if (wq == 0) mbar_arrive_expect_tx(&bars[ss], (uint32_t)((2 + NA) * C * 8 + C));
+      mbar_arrive_expect_tx(&bars[ss], (uint32_t)((2 + NA) * C * 8 + C));
+      bulk_g2s(st, D.s + row, C * 8, &bars[ss]);
+      bulk_g2s(st + C, dc + row, C * 8, &bars[ss]);
+      if (CS) bulk_g2s(ar + gs, D.coef + row, C * 8, &bars[ss]);
+      else {
 #pragma unroll
-      for (int c = 0; c < NA + 3; ++c) {
-        if ((c & 7) != wq) continue;
-        if (c == 0) bulk_g2s(st, D.s + row, C * 8, &bars[ss]);
-        else if (c == 1) bulk_g2s(st + C, dc + row, C * 8, &bars[ss]);
-        else if (c < 2 + NA) {
-          if (CS) bulk_g2s(ar + gs, D.coef + row, C * 8, &bars[ss]);
-          else bulk_g2s(ar + (c - 2) * RING + gs, D.dia.av[c - 2] + row, C * 8, &bars[ss]);
-        } else {
-          bulk_g2s(mk + gs, D.dia.mask + row, C, &bars[ss]);
-        }
+        for (int d = 0; d < NA; ++d) bulk_g2s(ar + d * RING + gs, D.dia.av[d] + row, C * 8, &bars[ss]);
       }
+      bulk_g2s(mk + gs, D.dia.mask + row, C, &bars[ss]);
     };
     if (tid == 0) {
 #pragma unroll
@@ -1692,7 +1677,7 @@ __global__ void __launch_bounds__(PR, 5) k_iter1_sw(Dev D, int par) {
       mbar_init_fence();
     }
     __syncthreads();
-    if (issuer)
+    if (tid == 0)
       for (int k = 0; k < P - 1 && k < K; ++k) issue(k);
     const bool xupd = pend && !fresh;
     double xo_n = 0.0;  // x of the lead chunk's own rows, loaded one step ahead
@@ -1712,7 +1697,7 @@ __global__ void __launch_bounds__(PR, 5) k_iter1_sw(Dev D, int par) {
         dp[lj & DM] = v;
       }
       __syncthreads();
-      if (issuer && k + P - 1 < K) issue(k + P - 1);
+      if (tid == 0 && k + P - 1 < K) issue(k + P - 1);
       const int u = k - NH;
       if (u >= 0) {  // q of chunk u
         const int li = u * C + tid;
@@ -1801,7 +1786,7 @@ struct Strip23 {
 };
 
 template <bool PART = false>
-__global__ void __launch_bounds__(PR, 3) k_iter23_s5(Dev D, int par) {
+__global__ void __launch_bounds__(PR, PART ? 3 : 1) k_iter23_s5(Dev D, int par) {
   constexpr int SP = kStripSP, RL = kStripRL, P = Strip23::P, C = kStripC, E = kStripE;
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ __align__(8) uint64_t bars[P];
@@ -1831,8 +1816,6 @@ __global__ void __launch_bounds__(PR, 3) k_iter23_s5(Dev D, int par) {
   unsigned char* mk = reinterpret_cast<unsigned char*>(stg + P * (SP + 2 * C));  // [RL][MK]
   const long long LBl = y0 - 2;                     // line of step 0
   const int K = (int)(y1 - y0) + 4;
-  const int wq = tid >> 5;
-  const bool issuer = (tid & 31) == 0;
   auto rowof = [&](long long line, int p) { return s0 + line * W + x0 - E + p; };
   auto issue = [&](int k) {
     const int ss = k % P, ls = k & (RL - 1);
@@ -1840,17 +1823,16 @@ __global__ void __launch_bounds__(PR, 3) k_iter23_s5(Dev D, int par) {
     const long long row = rowof(LBl + k, 0);
     const bool own = k >= 4;
     const uint32_t bytes = (uint32_t)((2 + 5) * SP * 8 + kStripMK + (own ? 2 * C * 8 : 0));
-    if (wq == 0) mbar_arrive_expect_tx(&bars[ss], bytes);
-    const long long ro = rowof(LBl + k - 2, E);
+    mbar_arrive_expect_tx(&bars[ss], bytes);
+    bulk_g2s(rp + ls * SP, rc + row, SP * 8, &bars[ss]);
+    bulk_g2s(st, D.q + row, SP * 8, &bars[ss]);
 #pragma unroll
-    for (int c = 0; c < 10; ++c) {  // copies spread over the warps (see k_iter23_sw)
-      if ((c & 7) != wq) continue;
-      if (c == 0) bulk_g2s(rp + ls * SP, rc + row, SP * 8, &bars[ss]);
-      else if (c == 1) bulk_g2s(st, D.q + row, SP * 8, &bars[ss]);
-      else if (c < 7) bulk_g2s(gr + ((c - 2) * RL + ls) * SP, D.dia.gv[c - 2] + row, SP * 8, &bars[ss]);
-      else if (c == 7) bulk_g2s(mk + ls * kStripMK, D.dia.mask + (row - 14), kStripMK, &bars[ss]);
-      else if (own && c == 8) bulk_g2s(st + SP, D.x + ro, C * 8, &bars[ss]);
-      else if (own && c == 9) bulk_g2s(st + SP + C, dn + ro, C * 8, &bars[ss]);
+    for (int d = 0; d < 5; ++d) bulk_g2s(gr + (d * RL + ls) * SP, D.dia.gv[d] + row, SP * 8, &bars[ss]);
+    bulk_g2s(mk + ls * kStripMK, D.dia.mask + (row - 14), kStripMK, &bars[ss]);
+    if (own) {
+      const long long ro = rowof(LBl + k - 2, E);
+      bulk_g2s(st + SP, D.x + ro, C * 8, &bars[ss]);
+      bulk_g2s(st + SP + C, dn + ro, C * 8, &bars[ss]);
     }
   };
   if (tid == 0) {
@@ -1859,7 +1841,7 @@ __global__ void __launch_bounds__(PR, 3) k_iter23_s5(Dev D, int par) {
     mbar_init_fence();
   }
   __syncthreads();
-  if (issuer) issue(0);
+  if (tid == 0) issue(0);
   double prr = 0.0, prs = 0.0;
   for (int k = 0; k < K; ++k) {
     const double* st = stg + (k % P) * (SP + 2 * C);
@@ -1884,7 +1866,7 @@ __global__ void __launch_bounds__(PR, 3) k_iter23_s5(Dev D, int par) {
       }
     }
     __syncthreads();
-    if (issuer && k + 1 < K) issue(k + 1);
+    if (tid == 0 && k + 1 < K) issue(k + 1);
     const int u = k - 1;
     if (u >= 1) {  // B: t on positions 1 .. SP-2 of line u (add.at order over G's mirrors)
 #pragma unroll
@@ -1985,20 +1967,15 @@ __global__ void __launch_bounds__(PR, 4) k_iter1_s5(Dev D, int par) {
     unsigned char* mk = reinterpret_cast<unsigned char*>(stg + P * 2 * SP);
     const long long LBl = y0 - 1;
     const int K = (int)(y1 - y0) + 2;
-    const int wq = tid >> 5;
-    const bool issuer = (tid & 31) == 0;
-    auto issue = [&](int k) {  // copies spread over the warps (see k_iter23_sw)
+    auto issue = [&](int k) {
       const int ss = k % P, ls = k & (RL - 1);
       const long long row = rowof(LBl + k, 0);
-      if (wq == 0) mbar_arrive_expect_tx(&bars[ss], (uint32_t)((2 + NA) * SP * 8 + kStripMK));
+      mbar_arrive_expect_tx(&bars[ss], (uint32_t)((2 + NA) * SP * 8 + kStripMK));
+      bulk_g2s(stg + ss * 2 * SP, D.s + row, SP * 8, &bars[ss]);
+      bulk_g2s(stg + ss * 2 * SP + SP, dc + row, SP * 8, &bars[ss]);
 #pragma unroll
-      for (int c = 0; c < NA + 3; ++c) {
-        if ((c & 7) != wq) continue;
-        if (c == 0) bulk_g2s(stg + ss * 2 * SP, D.s + row, SP * 8, &bars[ss]);
-        else if (c == 1) bulk_g2s(stg + ss * 2 * SP + SP, dc + row, SP * 8, &bars[ss]);
-        else if (c < 2 + NA) bulk_g2s(ar + ((c - 2) * RL + ls) * SP, D.dia.av[c - 2] + row, SP * 8, &bars[ss]);
-        else bulk_g2s(mk + ls * kStripMK, D.dia.mask + (row - 14), kStripMK, &bars[ss]);
-      }
+      for (int d = 0; d < NA; ++d) bulk_g2s(ar + (d * RL + ls) * SP, D.dia.av[d] + row, SP * 8, &bars[ss]);
+      bulk_g2s(mk + ls * kStripMK, D.dia.mask + (row - 14), kStripMK, &bars[ss]);
     };
     if (tid == 0) {
 #pragma unroll
@@ -2006,7 +1983,7 @@ __global__ void __launch_bounds__(PR, 4) k_iter1_s5(Dev D, int par) {
       mbar_init_fence();
     }
     __syncthreads();
-    if (issuer)
+    if (tid == 0)
       for (int k = 0; k < P - 1 && k < K; ++k) issue(k);
     for (int k = 0; k < K; ++k) {
       const double* st = stg + (k % P) * 2 * SP;
@@ -2028,7 +2005,7 @@ __global__ void __launch_bounds__(PR, 4) k_iter1_s5(Dev D, int par) {
         }
       }
       __syncthreads();
-      if (issuer && k + P - 1 < K) issue(k + P - 1);
+      if (tid == 0 && k + P - 1 < K) issue(k + P - 1);
       const int u = k - 1;
       const long long line = LBl + u;
       if (u >= 1 && tid < cx && line >= y0 && line < y1) {  // q of the own columns of line u

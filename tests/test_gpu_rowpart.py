@@ -118,3 +118,21 @@ def test_partitioned_sai_loss_and_grad(parts):
         ours = gp[fo[lo]:fo[hi]]
         ref = grad_ref[o[f.own[0]]:o[f.own[1]]]
         np.testing.assert_allclose(ours, ref, rtol=1e-12, atol=1e-12 * scale)
+
+
+def test_peer_mode_single_rank_runs_the_peer_reduction_path():
+    """Peer mode with one rank: the kernels take the peer branch of part_fin (epoch, parity
+    double buffer, system-scope release / acquire flags -- here on the rank's own block), the
+    exported IPC blob is consumed by sg_pcg_set_peers; the result equals pcg_solve's.  (More
+    ranks need more GPUs: their schedule runs on 2 gloo ranks in tests/test_rowpart_cpu.py.)"""
+    m = P.load_checkpoint(CKPT)
+    A, meta = P.gen_poisson2d(96, 40, coeff_seed=4)
+    b = P.gen_rhs(meta, 17)
+    cfg = P.SolveConfig(rtol=1e-9, residual_refresh_period=11)
+    _, ref = _whole(A, meta, m, b, cfg)
+    sol = RP.PeerPartitionSolver(A, meta, m, rank=0, world=1)
+    rep = sol.solve(b, cfg)
+    rep2 = sol.solve(b, cfg)  # epochs keep counting across solves
+    assert rep.converged and rep.k == ref.k and rep2.k == rep.k
+    np.testing.assert_allclose(rep.residual_history[:25], ref.residual_history[:25], rtol=1e-12)
+    np.testing.assert_array_equal(rep.x, rep2.x)
