@@ -1453,13 +1453,20 @@ __device__ __forceinline__ int ring_nb(int base, const int (&off)[ND], int d, in
   }
 }
 
+// Warp-specialised: warps 0..7 compute (one row per thread per phase, named barrier 1 between
+// phases), warp 8 only drives the bulk-copy engine -- it refills a ring slot as soon as the
+// consumers' `empty` barrier says the step that last used it is done, so no copy issue ever
+// sits on the consumers' critical path between their barriers.
+constexpr int kSwThreads = PR + 32;
+
 template <int ND, int NH, bool PART = false>
-__global__ void __launch_bounds__(PR, PART ? 3 : 1) k_iter23_sw(Dev D, int par) {
+__global__ void __launch_bounds__(kSwThreads, 3) k_iter23_sw(Dev D, int par) {
   using G = Sw23<ND, NH>;
   constexpr int C = G::C, P = G::P, NG = G::NG, NT = G::NT, GR = G::GR, TR = G::TR;
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ __align__(8) uint64_t bars[P];
-  __shared__ double red[PR / 32];
+  __shared__ __align__(8) uint64_t empty[P];
+  __shared__ double red[kSwThreads / 32];
   __shared__ int flag;
   const int b = blockIdx.x, tid = threadIdx.x;
   const int sys = D.rng_sys[b];
@@ -1482,10 +1489,18 @@ __global__ void __launch_bounds__(PR, PART ? 3 : 1) k_iter23_sw(Dev D, int par) 
   double* tr = rp + GR;                             // [TR]
   double* qs = tr + TR;                             // [P][C]
   unsigned char* mk = reinterpret_cast<unsigned char*>(qs + P * C);  // [GR]
-  // chunk k covers rows LB + k*C ..; LB 16-row aligned so every bulk copy is 16-byte aligned
-  const long long LB = (R0 & ~15LL) - 2LL * NH * C;
-  const int m1 = (int)((R1 - LB + C - 1) / C) - 1;  // last output chunk
-  const int K = m1 + 2 * NH + 1;                     // steps
+  // Ranges alternate direction inside a system: even ranges stream upwards, odd ones downwards,
+  // so two neighbouring ranges reach their shared boundary -- and read the 2*NH-chunk halo each
+  // needs from the other side -- at the same time (both at their ends or both at their starts):
+  // the second read is an L2 hit instead of an HBM re-read.  Rings are indexed by ROW (chunk
+  // c_rel = k upwards, K - 1 - k downwards, relative to LB), so neighbour arithmetic and every
+  // row's summation order are the same in both directions.
+  // LB / the top are 16-row aligned so every bulk copy is 16-byte aligned.
+  const bool down = ((b - D.sys_rng0[sys]) & 1) != 0;
+  const long long R0a = R0 & ~15LL, R1a = (R1 + 15) & ~15LL;
+  const int K = (int)(((down ? R1a - R0 : R1 - R0a) + C - 1) / C) + 4 * NH;  // output chunks + warm-up + lead-out
+  const long long LB = down ? R1a + 2LL * NH * C - (long long)K * C : R0a - 2LL * NH * C;
+  auto crel = [&](int k) { return down ? K - 1 - k : k; };
   auto rel = [&](long long v) { return (int)(v - LB < -1 ? -1 : (v - LB > (1LL << 30) ? (1LL << 30) : v - LB)); };
   const int s0r = rel(s0), s1r = rel(s1), R0r = rel(R0), R1r = rel(R1);
   const Own ow = own_get<PART>(D, sys);
@@ -1494,8 +1509,9 @@ __global__ void __launch_bounds__(PR, PART ? 3 : 1) k_iter23_sw(Dev D, int par) 
 #pragma unroll
   for (int d = 0; d < ND; ++d) off[d] = D.dia.off[d];
   auto issue = [&](int k) {
-    const int ss = k % P, gs = (k % NG) * C;
-    const long long row = LB + (long long)k * C;
+    const int cr = crel(k);
+    const int ss = k % P, gs = (cr % NG) * C;
+    const long long row = LB + (long long)cr * C;
     mbar_arrive_expect_tx(&bars[ss], (uint32_t)((2 + ND) * C * 8 + C));
     bulk_g2s(rp + gs, rc + row, C * 8, &bars[ss]);
     bulk_g2s(qs + ss * C, D.q + row, C * 8, &bars[ss]);
@@ -1505,17 +1521,26 @@ __global__ void __launch_bounds__(PR, PART ? 3 : 1) k_iter23_sw(Dev D, int par) 
   };
   if (tid == 0) {
 #pragma unroll
-    for (int q = 0; q < P; ++q) mbar_init(&bars[q], 1);
+    for (int q = 0; q < P; ++q) {
+      mbar_init(&bars[q], 1);
+      mbar_init(&empty[q], PR / 32);
+    }
     mbar_init_fence();
   }
   __syncthreads();
-  if (tid == 0)
-    for (int k = 0; k < P - 1 && k < K; ++k) issue(k);
   double prr = 0.0, prs = 0.0;
+  if (tid >= PR) {  // producer warp: chunk c once step c - P (the last user of its slots) is done
+    if (tid == PR)
+      for (int c = 0; c < K; ++c) {
+        if (c >= P) mbar_wait(&empty[c % P], (uint32_t)((c / P - 1) & 1));
+        issue(c);
+      }
+  } else
   for (int k = 0; k < K; ++k) {
     // x, d of this step's output chunk: plain loads, in flight across the wait and phases A, B
     const int mm = k - 2 * NH;
-    const int li = mm * C + tid;
+    const int cm = crel(mm);
+    const int li = cm * C + tid;
     const bool own_c = mm >= 2 * NH && li >= R0r && li < R1r;
     double xo = 0.0, dd = 0.0;
     if (own_c && !xd) {
@@ -1526,7 +1551,8 @@ __global__ void __launch_bounds__(PR, PART ? 3 : 1) k_iter23_sw(Dev D, int par) 
     }
     mbar_wait(&bars[k % P], (uint32_t)((k / P) & 1));
     {  // A: r' of the lead chunk, in place over its r
-      const int lj = k * C + tid, ix = (k % NG) * C + tid;
+      const int ck = crel(k);
+      const int lj = ck * C + tid, ix = (ck % NG) * C + tid;
       double v = sub(rp[ix], mul(alpha, qs[(k % P) * C + tid]));
       v = (lj >= s0r && lj < s1r) ? v : 0.0;
       if (lj >= R0r && lj < R1r) {
@@ -1535,11 +1561,11 @@ __global__ void __launch_bounds__(PR, PART ? 3 : 1) k_iter23_sw(Dev D, int par) 
       }
       rp[ix] = v;
     }
-    __syncthreads();
-    if (tid == 0 && k + P - 1 < K) issue(k + P - 1);
+    named_bar_sync(1, PR);
     const int u = k - NH;
     if (u >= NH) {  // B: t of chunk u (add.at order over G's mirror diagonals)
-      const int lj = u * C + tid, base = (u % NG) * C + tid;
+      const int cu = crel(u);
+      const int lj = cu * C + tid, base = (cu % NG) * C + tid;
       const unsigned int m = mk[base];
       double p[ND];
 #pragma unroll
@@ -1548,15 +1574,15 @@ __global__ void __launch_bounds__(PR, PART ? 3 : 1) k_iter23_sw(Dev D, int par) 
         p[d] = mul(gr[(ND - 1 - d) * GR + ix], rp[ix]);
       }
       const double v = combine_seq<ND>(p, m);
-      tr[(u % NT) * C + tid] = (lj >= s0r && lj < s1r) ? v : 0.0;
+      tr[(cu % NT) * C + tid] = (lj >= s0r && lj < s1r) ? v : 0.0;
     }
-    __syncthreads();
+    named_bar_sync(1, PR);
     if (own_c) {  // C: s and x of chunk mm (s of owned rows only: ghost s comes from the neighbours)
       const long long i = LB + li;
       if (!xd) D.x[i] = add(xo, mul(alpha, dd));
       else if (xint) D.x[i] = xo;
       if (li >= o0r && li < o1r) {
-        const int io = (mm % NG) * C + tid, tb = (mm % NT) * C + tid;
+        const int io = (cm % NG) * C + tid, tb = (cm % NT) * C + tid;
         const unsigned int m = mk[io];
         double p[ND];
 #pragma unroll
@@ -1568,6 +1594,9 @@ __global__ void __launch_bounds__(PR, PART ? 3 : 1) k_iter23_sw(Dev D, int par) 
         prs += mul(rni, si);
       }
     }
+    // step k done: its lead chunk's staging and the ring slot read last by phase C are free
+    // (the next phase A of this thread follows a named barrier with every other consumer)
+    if ((tid & 31) == 0) mbar_arrive(&empty[k % P]);
   }
   if (arrive(D, D.sys_rng0, sys, prr, prs, red, &flag)) {
     const double rr = gather_partials(D, D.sys_rng0, sys, 0, red);
@@ -1604,7 +1633,10 @@ struct Sw1 {
   // chunks in flight (incl. the current one); the coefficient ring's smaller footprint buys depth
   static constexpr int P = CS ? SG_SWP_CS : 4;
   static constexpr int NA = CS ? 1 : (FMT == 2 ? ND / 2 + 1 : ND);  // diagonals (or coefficients) streamed
-  static constexpr int NR = P + (CS ? 2 : 1) * NH;         // A / mask ring chunks: u (- NH) .. k + P - 1
+  static constexpr bool BOTHDIR = true;  // the ring holds the row-chunks on both sides of u
+  // A / mask ring chunks u - NH .. k + P - 1 (the rows behind chunk u: the stencil's +-W
+  // neighbours, the lower-half A's upper entries when streaming downwards)
+  static constexpr int NR = P + 2 * NH;
   static constexpr int RING = NR * C;
   static constexpr int DRING = pow2ceil((2 * NH + 2) * C); // d' ring: chunks u - NH .. k + 1
   static constexpr int DM = DRING - 1;
@@ -1648,9 +1680,12 @@ __global__ void __launch_bounds__(PR, 5) k_iter1_sw(Dev D, int par) {
     double* dp = ar + NA * RING;                      // [DRING]
     double* stg = dp + G::DRING;                      // [P][2][C]
     unsigned char* mk = reinterpret_cast<unsigned char*>(stg + P * 2 * C);
-    const long long LB = (R0 & ~15LL) - (long long)NH * C;
-    const int m1 = (int)((R1 - LB + C - 1) / C) - 1;
-    const int K = m1 + NH + 1;
+    // alternating stream direction per range, row-indexed rings (see k_iter23_sw)
+    const bool down = G::BOTHDIR && ((b - D.sys_rng0[sys]) & 1) != 0;
+    const long long R0a = R0 & ~15LL, R1a = (R1 + 15) & ~15LL;
+    const int K = (int)(((down ? R1a - R0 : R1 - R0a) + C - 1) / C) + 2 * NH;
+    const long long LB = down ? R1a + (long long)NH * C - (long long)K * C : R0a - (long long)NH * C;
+    auto crel = [&](int k) { return down ? K - 1 - k : k; };
     auto rel = [&](long long v) { return (int)(v - LB < -1 ? -1 : (v - LB > (1LL << 30) ? (1LL << 30) : v - LB)); };
     const int s0r = rel(s0), s1r = rel(s1), R0r = rel(R0), R1r = rel(R1);
     const int o0r = PART ? rel(ow.o0) : INT_MIN, o1r = PART ? rel(ow.o1) : INT_MAX;
@@ -1658,9 +1693,10 @@ __global__ void __launch_bounds__(PR, 5) k_iter1_sw(Dev D, int par) {
 #pragma unroll
     for (int d = 0; d < ND; ++d) off[d] = D.dia.off[d];
     auto issue = [&](int k) {
-      const int ss = k % P, gs = (k % NR) * C;
+      const int cr = crel(k);
+      const int ss = k % P, gs = (cr % NR) * C;
       double* st = stg + ss * 2 * C;
-      const long long row = LB + (long long)k * C;
+      const long long row = LB + (long long)cr * C;
       mbar_arrive_expect_tx(&bars[ss], (uint32_t)((2 + NA) * C * 8 + C));
       bulk_g2s(st, D.s + row, C * 8, &bars[ss]);
       bulk_g2s(st + C, dc + row, C * 8, &bars[ss]);
@@ -1681,13 +1717,14 @@ __global__ void __launch_bounds__(PR, 5) k_iter1_sw(Dev D, int par) {
       for (int k = 0; k < P - 1 && k < K; ++k) issue(k);
     const bool xupd = pend && !fresh;
     double xo_n = 0.0;  // x of the lead chunk's own rows, loaded one step ahead
-    if (xupd && tid >= R0r && tid < R1r) xo_n = D.x[LB + tid];
+    if (xupd && crel(0) * C + tid >= R0r && crel(0) * C + tid < R1r) xo_n = D.x[LB + crel(0) * C + tid];
     for (int k = 0; k < K; ++k) {
       const double* st = stg + (k % P) * 2 * C;
-      const int lj = k * C + tid;
+      const int lj = crel(k) * C + tid;
       const bool xown = xupd && lj >= R0r && lj < R1r;
       const double xo = xo_n;
-      if (xupd && lj + C >= R0r && lj + C < R1r) xo_n = D.x[LB + lj + C];
+      const int ljn = crel(k + 1) * C + tid;  // the next lead chunk's row (either direction)
+      if (xupd && k + 1 < K && ljn >= R0r && ljn < R1r) xo_n = D.x[LB + ljn];
       mbar_wait(&bars[k % P], (uint32_t)((k / P) & 1));
       {  // d' of the lead chunk (and the deferred x update of its own rows)
         double v = add(st[tid], mul(beta, st[C + tid]));
@@ -1700,9 +1737,10 @@ __global__ void __launch_bounds__(PR, 5) k_iter1_sw(Dev D, int par) {
       if (tid == 0 && k + P - 1 < K) issue(k + P - 1);
       const int u = k - NH;
       if (u >= 0) {  // q of chunk u
-        const int li = u * C + tid;
+        const int cu = crel(u);
+        const int li = cu * C + tid;
         if (li >= R0r && li < R1r) {
-          const int io = (u % NR) * C + tid;
+          const int io = (cu % NR) * C + tid;
           const unsigned int m = mk[io];
           double p[ND];
           if constexpr (CS) {
@@ -2194,8 +2232,8 @@ int launch_iteration(sg_pcg* h, cudaStream_t s, int par, bool refresh, cudaEvent
       if (strip) {
         k_iter23_s5<PT><<<gr, PR, Strip23::SMEM, s>>>(h->D, par);
       } else if (h->k23 == 1) {
-        if (H <= PR) k_iter23_sw<NS, 1, PT><<<gr, PR, Sw23<NS, 1>::SMEM, s>>>(h->D, par);
-        else k_iter23_sw<NS, 2, PT><<<gr, PR, Sw23<NS, 2>::SMEM, s>>>(h->D, par);
+        if (H <= PR) k_iter23_sw<NS, 1, PT><<<gr, kSwThreads, Sw23<NS, 1>::SMEM, s>>>(h->D, par);
+        else k_iter23_sw<NS, 2, PT><<<gr, kSwThreads, Sw23<NS, 2>::SMEM, s>>>(h->D, par);
       } else {
         if (H <= PR) k_iter23_st<NS, 1, PT><<<g, PR, (2 * tile + 6 * H) * sizeof(double), s>>>(h->D, par);
         else k_iter23_st<NS, 2, PT><<<g, PR, (2 * tile + 6 * H) * sizeof(double), s>>>(h->D, par);
@@ -2421,7 +2459,7 @@ int sw_attr(int* per_sm) {
   if constexpr (ND == 5)
     SG_CUDA(cudaFuncSetAttribute(k_iter1_sw<2, 5, NH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)Sw1<2, 5, NH, true>::SMEM));
-  SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_iter23_sw<ND, NH>, PR, Sw23<ND, NH>::SMEM));
+  SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_iter23_sw<ND, NH>, kSwThreads, Sw23<ND, NH>::SMEM));
   if (*per_sm < 1) *per_sm = 1;
   return SG_OK;
 }
