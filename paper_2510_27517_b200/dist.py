@@ -4,7 +4,7 @@ Independent systems shard over ranks (one process per GPU, torch.distributed ove
 solve has NO collective in its data path.  Collectives appear only around it: a barrier before
 timing, a MAX all-reduce of the device-measured step time, and one gather of the per-system
 statistics (k, converged) at the end.  Host-side logic is backend-agnostic so the N>1 path is
-tested with `gloo` on CPU (tests/test_dist_cpu.py).
+tested with `gloo` on CPU (tests/test_host_cpu.py::test_two_rank_gloo_sharding).
 """
 from __future__ import annotations
 

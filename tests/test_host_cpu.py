@@ -164,3 +164,26 @@ def test_train_config_validation():
                 dict(lr_decay=1.5), dict(norm_kind="nope"), dict(hutchinson_samples_per_matrix=0)):
         with pytest.raises(ValueError):
             P.TrainConfig(**bad)
+
+
+def test_fused_preconditioner_selection():
+    """pcg_solve fuses exactly the built-in applies; a subclass overriding apply (the reference's
+    CountingIdentity, pkg/tests/test_pcg.py:50-57) takes the generic path (no GPU needed)."""
+    from paper_2510_27517_b200.pcg import _fused_kind
+    from paper_2510_27517_b200.precond import IdentityPreconditioner, Preconditioner
+
+    class Counting(IdentityPreconditioner):
+        def apply(self, r):
+            return super().apply(r)
+
+    class KeepsApply(IdentityPreconditioner):
+        variant = "renamed"
+
+    class User(Preconditioner):
+        def apply(self, r):
+            return r
+
+    assert _fused_kind(IdentityPreconditioner(3)) == "identity"
+    assert _fused_kind(KeepsApply(3)) == "identity"
+    assert _fused_kind(Counting(3)) is None
+    assert _fused_kind(User(3)) is None
