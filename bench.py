@@ -198,7 +198,7 @@ def hbm_peak():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def pcg_roofline(prof, n1, e1n, peak, peak_src, K23_SW, K1_SW, units_note="per system"):
+def pcg_roofline(prof, n1, e1n, peak, peak_src, K23_SW, K1_SW, units_note="per system", which="c2"):
     """Roofline of the PCG iteration kernels from the handle's in-graph event samples.
 
     `achieved` counts the ALGORITHMIC bytes of the layout the kernels run: the
@@ -244,7 +244,7 @@ def pcg_roofline(prof, n1, e1n, peak, peak_src, K23_SW, K1_SW, units_note="per s
     if not kern:
         return None
     dom = max(kern, key=lambda k: kern[k]["avg_ms"])
-    traffic = ncu_traffic(K23_SW if dom == K23N else K1_SW if dom == K1N else None)
+    traffic = ncu_traffic(K23_SW if dom == K23N else K1_SW if dom == K1N else None, which)
     return {"bound": "hbm", "kernel": dom, "achieved": kern[dom]["gbs"], "peak": peak, "unit": "GB/s",
             "frac": kern[dom]["frac"], "traffic": traffic["bytes"] if traffic else None,
             "traffic_source": traffic["source"] if traffic else None,
@@ -455,10 +455,7 @@ def run_c5(a, model, dev):
     peak, peak_src = hbm_peak()
     n, nnz = A.n_rows, A.nnz
     roof = pcg_roofline(prof, n, nnz, peak, peak_src, K23_SW="k_iter23_s5", K1_SW="k_iter1_s5",
-                        units_note="one system")
-    if roof is not None:
-        roof["traffic"] = None
-        roof["traffic_source"] = "see profiles/r03_ncu_c5_*.txt"
+                        units_note="one system", which="c5")
     # e2e: host int64 CSR + host rhs in, host x out, through the public API
     offs_h, cols_h, vals_h = A.row_offsets.copy(), A.col_indices.copy(), A.values.copy()
     e2e_ms = []
@@ -520,17 +517,23 @@ def c5_cpu_baseline(model, k_gpu):
             "seconds_per_solve": total}
 
 
-NCU_SUMMARY = (sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_full_pcg_sw_128sys.txt"))) or
-               [os.path.join(ROOT, "profiles", "r01_ncu_full_pcg_sw_128sys.txt")])[-1]  # newest round
+def _newest(pattern):
+    found = sorted(glob.glob(os.path.join(ROOT, "profiles", pattern)))
+    return found[-1] if found else None
 
 
-def ncu_traffic(kernel):
+NCU_SUMMARY = {"c2": _newest("r*_ncu_full_pcg_sw_128sys.txt"), "c5": _newest("r*_ncu_full_pcg_s5_c5.txt")}
+
+
+def ncu_traffic(kernel, which="c2"):
     """dram__bytes_read.sum + dram__bytes_write.sum of `kernel` from the committed ncu --set full
-    capture of this workload (one launch, 128-system batch), in bytes; None if absent."""
-    if not kernel or not os.path.exists(NCU_SUMMARY):
+    capture of this workload (one launch; C2: the 128-system batch, C5: the 2048^2 system), in
+    bytes; None if absent."""
+    path = NCU_SUMMARY.get(which)
+    if not kernel or not path or not os.path.exists(path):
         return None
     scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-    for line in open(NCU_SUMMARY):
+    for line in open(path):
         if f" {kernel}<" not in line.split("|")[0]:
             continue
         vals = {}
@@ -540,7 +543,7 @@ def ncu_traffic(kernel):
             vals[name] = float(v) * scale.get(unit.rstrip("]"), float("nan"))
         if "dram__bytes_read.sum" in vals and "dram__bytes_write.sum" in vals:
             return {"bytes": vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"],
-                    "source": os.path.relpath(NCU_SUMMARY, ROOT) + " (ncu --set full, one launch)"}
+                    "source": os.path.relpath(path, ROOT) + " (ncu --set full, one launch)"}
     return None
 
 
