@@ -319,6 +319,13 @@ int sg_sai_loss_part_bwd(int64_t n, const int32_t* at_offs, const int32_t* at_co
                          const double* t, const double* z64, const double* norm3, int64_t own_lo, int64_t own_hi,
                          double* grad_out, void* ws, size_t* ws_bytes, void* stream);
 
+/* tcgen05 building block (diagnostic): one 128-row tile D = A . W (A: 128 x K row-major fp32,
+ * W: K x N row-major fp32, K, N <= 32) on the 5th-generation tensor core, kind::tf32 with operands
+ * in shared memory and the accumulator in TMEM; split3 = 1 runs the 3xTF32 split (~fp32
+ * accuracy).  out: 128 x N row-major.  Used by the tests of the tensor-core edge pass. */
+int sg_tc_gemm_selftest(const float* a, const float* w, int32_t k, int32_t n, int32_t split3, float* out,
+                        void* stream);
+
 /* ---- GNN training step (gnn.py:198-253 backward, training.py:126-147) ----
  * Plain fp64 primitives with fixed reduction orders (bit-reproducible runs); composed by
  * paper_2510_27517_b200/training.py into the training forward (all intermediates kept), the

@@ -88,6 +88,7 @@ SIGNATURES = {
     "sg_loss_sum_parts": (C.c_int, [vp, i32, C.POINTER(C.c_double), vp]),
     "sg_sai_loss_part_bwd": (C.c_int, [i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, i64, vp, vp, szp,
                                        vp]),
+    "sg_tc_gemm_selftest": (C.c_int, [vp, vp, i32, i32, i32, vp, vp]),
     "sg_pcg_set_partition": (C.c_int, [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "sg_pcg_peer_info_size": (C.c_int, []),
     "sg_pcg_peer_export": (C.c_int, [vp, i64, i64, i32, vp]),
