@@ -161,6 +161,16 @@ int sg_gnn_forward(const double* params, int64_t n_params, int n_layers, int hid
                    const double* edge_feat, double* g_out, void* ws, size_t* ws_bytes,
                    void* stream);
 
+/* sg_gnn_forward with a choice of edge-pass arithmetic: edge_mode 0 = the fp64 DMMA edge pass
+ * (sg_gnn_forward), 1 = the edge MLPs on the 5th-generation tensor cores (tcgen05.mma
+ * kind::tf32, 3xTF32 split, fp32 accumulation in TMEM; ~fp32 accuracy, the north_star's fp32 bar
+ * of 1e-5 on G; hidden <= 32).  The node path is fp64 either way. */
+int sg_gnn_forward_ex(const double* params, int64_t n_params, int n_layers, int hidden, int d_node,
+                      int d_edge, int act, int64_t n, int64_t nnz, const int32_t* offs,
+                      const int32_t* cols, const int32_t* rows, const double* node_feat,
+                      const double* edge_feat, double* g_out, int32_t edge_mode, void* ws,
+                      size_t* ws_bytes, void* stream);
+
 /* ---------------------------------------------------------------- SpMV family (L1, L4) */
 
 /* spmv (sparse.py:186-191): y = A x in numpy reduceat order (bit-identical). */

@@ -54,6 +54,8 @@ SIGNATURES = {
     "sg_graph_features": (C.c_int, [i64, i64, vp, vp, vp, vp, C.c_int, i64, i64, vp, f64, vp, vp, vp]),
     "sg_gnn_forward": (C.c_int, [vp, i64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, i64, i64,
                                  vp, vp, vp, vp, vp, vp, vp, szp, vp]),
+    "sg_gnn_forward_ex": (C.c_int, [vp, i64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, i64, i64,
+                                    vp, vp, vp, vp, vp, vp, i32, vp, szp, vp]),
     "sg_spmv": (C.c_int, [i64, vp, vp, vp, vp, vp, vp]),
     "sg_spmv_seq": (C.c_int, [i64, vp, vp, vp, vp, vp, vp]),
     "sg_spmv_warp": (C.c_int, [i64, vp, vp, vp, vp, vp, vp]),

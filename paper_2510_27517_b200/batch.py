@@ -246,9 +246,13 @@ def _rhs(n, seed):
 class BatchSolver:
     """GNN build + PCG solve for a SystemBatch (device buffers and CUDA graphs reused per step)."""
 
-    def __init__(self, batch: SystemBatch, model: GnnModel):
+    def __init__(self, batch: SystemBatch, model: GnnModel, edge_precision: str | None = None):
         import torch
         self.batch, self.model = batch, model
+        # GNN edge pass arithmetic (gnn.forward_device): "fp64" DMMA (default) or "tf32x3" on
+        # tcgen05 -- SG_GNN_EDGE=tf32x3 selects it without code changes (the C2 configuration of
+        # SURVEY.md §8(d) allows an fp32 GNN with the fp64 PCG)
+        self.edge_precision = edge_precision or os.environ.get("SG_GNN_EDGE", "fp64")
         a = batch.a
         S = batch.n_systems
         self.norms = L.empty(S, torch.float64)
@@ -301,7 +305,8 @@ class BatchSolver:
     def build_factor(self):
         """G = GNN(graph) on the union graph; explicit G^T values via the transpose permutation."""
         a = self.batch.a
-        forward_device(self.model, a, self.node, self.edge, self.batch.d_node, out=self.g)
+        forward_device(self.model, a, self.node, self.edge, self.batch.d_node, out=self.g,
+                       edge_precision=self.edge_precision)
         _, _, perm = a.transpose_pattern()
         L.check(L.lib().sg_gather_f64(L.ptr(self.g), L.ptr(perm), L.ptr(self.gt_vals), a.nnz, L.stream_ptr()))
 

@@ -22,6 +22,7 @@
 // Node-level arrays are row-major [node][DP] (DP = D padded to 8), so the 4 lanes of a row read
 // 64 contiguous bytes per n-tile.  fp64 throughout (parity is tolerance-based).
 #include "common.cuh"
+#include "tc.cuh"
 
 namespace sg {
 
@@ -380,6 +381,177 @@ __global__ void __launch_bounds__(256) k_edge_pass(GnnP p, int64_t nnz, const in
   }
 }
 
+// ------------------------------------------------------------------ edge pass on tcgen05
+// The same per-edge computation in fp32 on the 5th-generation tensor core: a CTA of 128 threads
+// owns a tile of 128 edges (thread = edge = accumulator row / TMEM lane), and every [128 x D] .
+// [D x D] product of the edge MLPs is kind::tf32 tcgen05.mma with the 3xTF32 split (a_hi b_hi +
+// a_hi b_lo + a_lo b_hi, fp32 accumulate in TMEM): the activations are written K-major into
+// shared memory by their threads, one elected thread issues the MMAs, tcgen05.commit arrives on
+// an mbarrier, and every thread reads its row back with tcgen05.ld.  Weights (hi / lo splits) stay
+// in shared memory for the CTA's life; the fp64 node path's P'_t / Q'_t rows are read and rounded
+// to fp32 per edge.  Accuracy: ~fp32 (north_star: G within 1e-5 in fp32) -- the fp64 DMMA edge
+// pass stays the default; this one is opt-in (`edge_mode` 1).
+template <int D>
+struct TcEdge {
+  static constexpr int KP = (D + 7) / 8 * 8;       // padded K (multiple of the MMA's 8)
+  static constexpr int NP = 32;                     // padded N (TMEM columns)
+  static constexpr int BW = NP * KP;                // floats per weight matrix (one split)
+  static constexpr int AW = 128 * KP;               // floats per activation tile (one split)
+  static constexpr int NV = 24;                     // padded vector length (<= 32)
+  __host__ __device__ static int nmat(int L) { return 2 + 2 * L; }  // FE2, D1, per layer We1c, We2
+  static size_t smem(int L) {
+    return (size_t)(2 * nmat(L) * BW + 2 * AW) * sizeof(float) + (size_t)(5 + 2 * L) * 32 * sizeof(float) + 64;
+  }
+};
+
+template <int D, int ACT>
+__global__ void __launch_bounds__(128, 2) k_edge_pass_tc(GnnP p, int64_t nnz, const int32_t* __restrict__ rows,
+                                                         const int32_t* __restrict__ cols,
+                                                         const double* __restrict__ ef,
+                                                         const double* __restrict__ EPQ, int64_t n,
+                                                         double* __restrict__ g) {
+  using T = TcEdge<D>;
+  constexpr int KP = T::KP, BW = T::BW, AW = T::AW, DP = Shape<D>::DP;
+  static_assert(KP <= 32 && D <= 32, "tensor-core edge pass: hidden size <= 32");
+  extern __shared__ __align__(128) float smf[];
+  __shared__ uint32_t tmem_base;
+  __shared__ __align__(8) uint64_t bar;
+  const int L = p.L;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  float* Bw = smf;                               // [nmat][2][BW] weight splits, B operand layout
+  float* Ah = Bw + 2 * T::nmat(L) * BW;          // [AW] activation tile, hi split
+  float* Al = Ah + AW;                           // [AW] lo split
+  float* vec = Al + AW;                          // [5 + 2L][32]: e1, eb1, eb2, db1, d2, be1_t, be2_t
+  // matrix m: 0 = FE2 (ee.W2), 1 = D1 (dec.W1), 2 + 2t = We1c_t (fe[t].W1 rows 2D..3D), 3 + 2t = We2_t
+  auto wsrc = [&](int m) -> const double* {
+    if (m == 0) return p.ee.W2;
+    if (m == 1) return p.dec.W1;
+    const int t = (m - 2) >> 1;
+    return ((m - 2) & 1) ? p.fe[t].W2 : p.fe[t].W1 + 2 * D * D;
+  };
+  for (int m = 0; m < T::nmat(L); ++m) {
+    const double* W = wsrc(m);
+    for (int idx = tid; idx < T::NP * KP; idx += 128) {
+      const int nn = idx / KP, k = idx % KP;
+      const float w = (nn < D && k < D) ? (float)W[k * D + nn] : 0.f;
+      const float hi = tf32_rn(w), lo = tf32_rn(w - hi);
+      Bw[(2 * m) * BW + umma_off(nn, k, T::NP) / 4] = hi;
+      Bw[(2 * m + 1) * BW + umma_off(nn, k, T::NP) / 4] = lo;
+    }
+  }
+  for (int f = tid; f < 32; f += 128) {
+    const bool in = f < D;
+    vec[0 * 32 + f] = in ? (float)p.ee.W1[f] : 0.f;
+    vec[1 * 32 + f] = in ? (float)p.ee.b1[f] : 0.f;
+    vec[2 * 32 + f] = in ? (float)p.ee.b2[f] : 0.f;
+    vec[3 * 32 + f] = in ? (float)p.dec.b1[f] : 0.f;
+    vec[4 * 32 + f] = in ? (float)p.dec.W2[f] : 0.f;
+    for (int t = 0; t < L; ++t) {
+      vec[(5 + 2 * t) * 32 + f] = in ? (float)p.fe[t].b1[f] : 0.f;
+      vec[(6 + 2 * t) * 32 + f] = in ? (float)p.fe[t].b2[f] : 0.f;
+    }
+  }
+  const float db2 = (float)p.dec.b2[0];
+  fence_proxy_async_smem();
+  if (warp == 0) tmem_alloc(&tmem_base, T::NP);
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    mbar_init_fence();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t taddr = tmem_base;
+  const uint32_t my_lanes = taddr + ((uint32_t)(warp * 32) << 16);
+  constexpr uint32_t idesc = umma_idesc_tf32(128, T::NP);
+  uint32_t phase = 0;
+  // out = act_in[128 x D] . W_m  (3xTF32), every thread its own row
+  auto gemm = [&](const float (&x)[32], int m, float (&out)[32]) {
+#pragma unroll
+    for (int c = 0; c < KP / 4; ++c) {
+      float4 hi, lo;
+      float* hp = &hi.x;
+      float* lp = &lo.x;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float v = x[4 * c + e];
+        hp[e] = tf32_rn(v);
+        lp[e] = tf32_rn(v - hp[e]);
+      }
+      const uint32_t o = umma_off(tid, 4 * c, 128) / 4;
+      *reinterpret_cast<float4*>(Ah + o) = hi;
+      *reinterpret_cast<float4*>(Al + o) = lo;
+    }
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncthreads();  // the tile is complete; every thread's previous TMEM read has finished
+    tc_fence_after();
+    if (tid == 0) {
+      const float* bh = Bw + (2 * m) * BW;
+      const float* bl = Bw + (2 * m + 1) * BW;
+#pragma unroll
+      for (int s = 0; s < KP / 8; ++s) {
+        const uint64_t dah = umma_desc(smem_u32(Ah) + s * 2 * 128 * 16, 128 * 16, 128);
+        const uint64_t dal = umma_desc(smem_u32(Al) + s * 2 * 128 * 16, 128 * 16, 128);
+        const uint64_t dbh = umma_desc(smem_u32(bh) + s * 2 * T::NP * 16, T::NP * 16, 128);
+        const uint64_t dbl = umma_desc(smem_u32(bl) + s * 2 * T::NP * 16, T::NP * 16, 128);
+        umma_tf32(taddr, dah, dbh, idesc, s > 0);
+        umma_tf32(taddr, dah, dbl, idesc, true);
+        umma_tf32(taddr, dal, dbh, idesc, true);
+      }
+      umma_commit(&bar);
+    }
+    mbar_wait(&bar, phase);
+    phase ^= 1u;
+    tc_fence_after();
+    tmem_ld32(my_lanes, out);
+  };
+  for (int64_t tile = blockIdx.x; tile * 128 < nnz; tile += gridDim.x) {
+    const int64_t k = tile * 128 + tid;
+    const bool ok = k < nnz;
+    const int64_t kc = ok ? k : nnz - 1;
+    const float e = (float)ef[kc];
+    const int64_t i = rows[kc], j = cols[kc];
+    float a[32], h[32], v[32];
+#pragma unroll
+    for (int f = 0; f < 32; ++f) a[f] = f < D ? act_fn<ACT>(fmaf(e, vec[f], vec[32 + f])) : 0.f;
+    gemm(a, 0, v);
+#pragma unroll
+    for (int f = 0; f < 32; ++f) h[f] = f < D ? v[f] + vec[64 + f] : 0.f;
+    for (int t = 0; t < L; ++t) {
+      const double* Pt = EPQ + ((int64_t)t * n) * 2 * DP;
+      const double* pr = Pt + i * 2 * DP;
+      const double* qr = Pt + j * 2 * DP + DP;
+      gemm(h, 2 + 2 * t, v);
+      const float* b1 = vec + (5 + 2 * t) * 32;
+      const float* b2 = vec + (6 + 2 * t) * 32;
+#pragma unroll
+      for (int f = 0; f < 32; f += 2) {
+        if (f < D) {
+          const double2 pp = *reinterpret_cast<const double2*>(pr + f);
+          const double2 qq = *reinterpret_cast<const double2*>(qr + f);
+          a[f] = act_fn<ACT>((float)(pp.x + qq.x) + b1[f] + v[f]);
+          a[f + 1] = f + 1 < D ? act_fn<ACT>((float)(pp.y + qq.y) + b1[f + 1] + v[f + 1]) : 0.f;
+        } else {
+          a[f] = a[f + 1] = 0.f;
+        }
+      }
+      gemm(a, 3 + 2 * t, v);
+#pragma unroll
+      for (int f = 0; f < 32; ++f) h[f] = f < D ? h[f] + (v[f] + b2[f]) : 0.f;
+    }
+    gemm(h, 1, v);
+    float part = 0.f;
+#pragma unroll
+    for (int f = 0; f < 32; ++f)
+      if (f < D) part = fmaf(act_fn<ACT>(v[f] + vec[96 + f]), vec[128 + f], part);
+    if (ok) g[k] = (double)(part + db2);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(taddr, T::NP);
+}
+
 template <class K>
 static int resident(K kernel, int threads, size_t smem) {
   int per_sm = 0;
@@ -400,7 +572,7 @@ static int grid_for(int64_t rows, int per_sm, int warps = 4) {
 template <int D, int ACT>
 int run_forward(const GnnP& p, int64_t n, int64_t nnz, const int32_t* offs, const int32_t* cols,
                 const int32_t* rows, const double* V, const double* ef, double* g, double* X,
-                double* PQa, double* PQb, double* EPQ, cudaStream_t s) {
+                double* PQa, double* PQb, double* EPQ, cudaStream_t s, int edge_mode = 0) {
   using S = Shape<D>;
   const size_t sm_enc = (size_t)(6 * S::DP + 3 * S::FRAG + 16) * sizeof(double);
   SG_CUDA(cudaFuncSetAttribute(k_node_encode<D, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_enc));
@@ -415,6 +587,22 @@ int run_forward(const GnnP& p, int64_t n, int64_t nnz, const int32_t* offs, cons
     k_node_layer<D, ACT><<<grid_for(n, layer_res), 128, sm_layer, s>>>(p, t, n, offs, cols, ef, X, cur, nxt, EPQ);
     SG_LAUNCH_CHECK("k_node_layer");
     double* tmp = cur; cur = nxt; nxt = tmp;
+  }
+  if (edge_mode == 1) {  // tcgen05 3xTF32 edge pass
+    if constexpr (TcEdge<D>::KP <= 32) {
+      const size_t smt = TcEdge<D>::smem(p.L);
+      if (smt > 227 * 1024) {
+        set_error("tensor-core edge pass: weights (%zu bytes) exceed shared memory", smt);
+        return SG_EUNSUPPORTED;
+      }
+      SG_CUDA(cudaFuncSetAttribute(k_edge_pass_tc<D, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smt));
+      const int64_t tiles = (nnz + 127) / 128;
+      const int res = resident(k_edge_pass_tc<D, ACT>, 128, smt);
+      const int64_t cap = 148LL * res;
+      k_edge_pass_tc<D, ACT><<<(unsigned)(tiles < cap ? tiles : cap), 128, smt, s>>>(p, nnz, rows, cols, ef, EPQ, n, g);
+      SG_LAUNCH_CHECK("k_edge_pass_tc");
+      return SG_OK;
+    }
   }
   const size_t smem = (edge_smem_doubles<D>(p.L) + 16) * sizeof(double);
   if (smem > 227 * 1024) {
@@ -433,9 +621,10 @@ int run_forward(const GnnP& p, int64_t n, int64_t nnz, const int32_t* offs, cons
 template <int ACT>
 int dispatch_hidden(int hidden, const GnnP& p, int64_t n, int64_t nnz, const int32_t* offs,
                     const int32_t* cols, const int32_t* rows, const double* V, const double* ef,
-                    double* g, double* X, double* PQa, double* PQb, double* EPQ, cudaStream_t s) {
+                    double* g, double* X, double* PQa, double* PQb, double* EPQ, cudaStream_t s,
+                    int edge_mode) {
 #define SG_H(DD) \
-  case DD: return run_forward<DD, ACT>(p, n, nnz, offs, cols, rows, V, ef, g, X, PQa, PQb, EPQ, s);
+  case DD: return run_forward<DD, ACT>(p, n, nnz, offs, cols, rows, V, ef, g, X, PQa, PQb, EPQ, s, edge_mode);
   switch (hidden) {
     SG_H(4) SG_H(6) SG_H(8) SG_H(12) SG_H(16) SG_H(24) SG_H(32)
   }
@@ -448,11 +637,11 @@ int dispatch_hidden(int hidden, const GnnP& p, int64_t n, int64_t nnz, const int
 
 using namespace sg;
 
-extern "C" int sg_gnn_forward(const double* params, int64_t n_params, int n_layers, int hidden,
-                              int d_node, int d_edge, int act, int64_t n, int64_t nnz,
-                              const int32_t* offs, const int32_t* cols, const int32_t* rows,
-                              const double* node_feat, const double* edge_feat, double* g_out,
-                              void* ws, size_t* ws_bytes, void* stream) {
+extern "C" int sg_gnn_forward_ex(const double* params, int64_t n_params, int n_layers, int hidden,
+                                 int d_node, int d_edge, int act, int64_t n, int64_t nnz,
+                                 const int32_t* offs, const int32_t* cols, const int32_t* rows,
+                                 const double* node_feat, const double* edge_feat, double* g_out,
+                                 int32_t edge_mode, void* ws, size_t* ws_bytes, void* stream) {
   const int64_t D = hidden, L = n_layers, DP = (hidden + 7) / 8 * 8;
   Carve c(ws);
   double* X = c.take<double>(n * DP);
@@ -497,7 +686,19 @@ extern "C" int sg_gnn_forward(const double* params, int64_t n_params, int n_laye
   p.dec = take_mlp(D, 1);
   if (n == 0 || nnz == 0) return SG_OK;
   cudaStream_t s = as_stream(stream);
+  if (edge_mode < 0 || edge_mode > 1) { set_error("edge_mode must be 0 (fp64 DMMA) or 1 (tcgen05 3xTF32)"); return SG_EINVAL; }
   if (act == 0)
-    return dispatch_hidden<0>(hidden, p, n, nnz, offs, cols, rows, node_feat, edge_feat, g_out, X, PQa, PQb, EPQ, s);
-  return dispatch_hidden<1>(hidden, p, n, nnz, offs, cols, rows, node_feat, edge_feat, g_out, X, PQa, PQb, EPQ, s);
+    return dispatch_hidden<0>(hidden, p, n, nnz, offs, cols, rows, node_feat, edge_feat, g_out, X, PQa, PQb, EPQ, s,
+                              edge_mode);
+  return dispatch_hidden<1>(hidden, p, n, nnz, offs, cols, rows, node_feat, edge_feat, g_out, X, PQa, PQb, EPQ, s,
+                            edge_mode);
+}
+
+extern "C" int sg_gnn_forward(const double* params, int64_t n_params, int n_layers, int hidden,
+                              int d_node, int d_edge, int act, int64_t n, int64_t nnz,
+                              const int32_t* offs, const int32_t* cols, const int32_t* rows,
+                              const double* node_feat, const double* edge_feat, double* g_out,
+                              void* ws, size_t* ws_bytes, void* stream) {
+  return sg_gnn_forward_ex(params, n_params, n_layers, hidden, d_node, d_edge, act, n, nnz, offs, cols, rows,
+                           node_feat, edge_feat, g_out, 0, ws, ws_bytes, stream);
 }
