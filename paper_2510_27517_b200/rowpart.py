@@ -620,6 +620,7 @@ class PartitionedSolver:
         N, E = int(self.row_start[-1]), int(self.nnz_start[-1])
         offs, cols = L.empty(N + 1, torch.int32), L.empty(E, torch.int32)
         av, gv = L.empty(E, torch.float64), L.empty(E, torch.float64)
+        self._ws_bufs = []
         for p, f in enumerate(self.factors):  # block-diagonal union of the extended systems
             r0, e0 = int(self.row_start[p]), int(self.nnz_start[p])
             L.check(L.lib().sg_csr_row_block(L.ptr(f.offs), L.ptr(f.cols), 0, sizes[p], 0, sizes[p], r0, e0,
@@ -639,13 +640,14 @@ class PartitionedSolver:
         L.check(L.lib().sg_pcg_set_partition(self.handle._h, lo.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
                                              hi.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))), "set_partition")
 
-    @staticmethod
-    def _ws(f, nr):
+    def _ws(self, f, nr):
+        """Workspace of one sg_csr_row_block call (kept alive on the solver: the call is
+        asynchronous)."""
         import ctypes
 
         from . import _lib as L
         buf, wsb = L.workspace(L.lib().sg_csr_row_block, None, None, 0, nr, 0, nr, 0, 0, None, None, None, None)
-        PartitionedSolver._keep = buf
+        self._ws_bufs.append(buf)
         return L.ptr(buf), ctypes.byref(wsb)
 
     def solve(self, b, cfg=None):
