@@ -1806,7 +1806,10 @@ __global__ void __launch_bounds__(PR, 5) k_iter1_sw(Dev D, int par) {
 // neighbours are p +- 1, so all of it is plain 1-D DIA arithmetic (a position past the strip
 // edge is simply the neighbouring row).  Same phases, roundings and summation orders as the
 // 1-D kernels; only the partial sums are grouped per (strip, line range).
-constexpr int kStripC = 256;               // columns per strip (one per thread)
+#ifndef SG_STRIP_C
+#define SG_STRIP_C 256
+#endif
+constexpr int kStripC = SG_STRIP_C;        // columns per strip (one per thread of the CTA)
 constexpr int kStripE = 2;                 // x-halo columns on each side
 constexpr int kStripSP = kStripC + 2 * kStripE;  // 260 positions per line segment (2080 B)
 constexpr int kStripMK = kStripSP + 28;    // mask window: 16-row aligned start, 288 bytes
@@ -1824,11 +1827,11 @@ struct Strip23 {
 };
 
 template <bool PART = false>
-__global__ void __launch_bounds__(PR, PART ? 3 : 1) k_iter23_s5(Dev D, int par) {
+__global__ void __launch_bounds__(kStripC, PART ? 3 : 768 / kStripC) k_iter23_s5(Dev D, int par) {
   constexpr int SP = kStripSP, RL = kStripRL, P = Strip23::P, C = kStripC, E = kStripE;
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ __align__(8) uint64_t bars[P];
-  __shared__ double red[PR / 32];
+  __shared__ double red[kStripC / 32];
   __shared__ int flag;
   const int b = blockIdx.x, tid = threadIdx.x;
   const int sys = D.rng_sys[b];
@@ -1889,7 +1892,7 @@ __global__ void __launch_bounds__(PR, PART ? 3 : 1) k_iter23_s5(Dev D, int par) 
       const int ls = k & (RL - 1);
 #pragma unroll
       for (int h2 = 0; h2 < 2; ++h2) {
-        const int p = tid + h2 * PR;
+        const int p = tid + h2 * kStripC;
         if (p < SP) {
           const long long j = rowof(line, p);
           double v = sub(rp[ls * SP + p], mul(alpha, st[p]));
@@ -1909,7 +1912,7 @@ __global__ void __launch_bounds__(PR, PART ? 3 : 1) k_iter23_s5(Dev D, int par) 
     if (u >= 1) {  // B: t on positions 1 .. SP-2 of line u (add.at order over G's mirrors)
 #pragma unroll
       for (int h2 = 0; h2 < 2; ++h2) {
-        const int p = 1 + tid + h2 * PR;
+        const int p = 1 + tid + h2 * kStripC;
         if (p < SP - 1) {
           const long long j = rowof(LBl + u, p);
           const unsigned int m = mk[(u & (RL - 1)) * kStripMK + p + 14];
@@ -1971,11 +1974,11 @@ struct Strip1 {
 };
 
 template <int FMT, bool PART = false>
-__global__ void __launch_bounds__(PR, 4) k_iter1_s5(Dev D, int par) {
+__global__ void __launch_bounds__(kStripC, 1024 / kStripC) k_iter1_s5(Dev D, int par) {
   constexpr int SP = kStripSP, RL = kStripRL, P = Strip1<FMT>::P, NA = Strip1<FMT>::NA, E = kStripE;
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ __align__(8) uint64_t bars[P];
-  __shared__ double red[PR / 32];
+  __shared__ double red[kStripC / 32];
   __shared__ int flag;
   const int b = blockIdx.x, tid = threadIdx.x;
   const int sys = D.rng_sys[b];
@@ -2031,7 +2034,7 @@ __global__ void __launch_bounds__(PR, 4) k_iter1_s5(Dev D, int par) {
         const int ls = k & (RL - 1);
 #pragma unroll
         for (int h2 = 0; h2 < 2; ++h2) {
-          const int p = tid + h2 * PR;
+          const int p = tid + h2 * kStripC;
           if (p < SP) {
             const long long j = rowof(line, p);
             double v = add(st[p], mul(beta, st[SP + p]));
@@ -2217,7 +2220,7 @@ int launch_iteration(sg_pcg* h, cudaStream_t s, int par, bool refresh, cudaEvent
     // the streamed kernels exist with and without the row-partition logic (PART)
     auto k1_streamed = [&](auto Pc) {
       constexpr bool PT = decltype(Pc)::value;
-      if (strip) k_iter1_s5<FS, PT><<<gr, PR, Strip1<FS>::SMEM, s>>>(h->D, par);
+      if (strip) k_iter1_s5<FS, PT><<<gr, kStripC, Strip1<FS>::SMEM, s>>>(h->D, par);
       else if (st && h->k1sw && FMT == 2 && ND == 5 && h->cst && !PT) {  // A from the coefficient stencil
         if (H <= PR) k_iter1_sw<2, 5, 1, true><<<gr, PR, Sw1<2, 5, 1, true>::SMEM, s>>>(h->D, par);
         else k_iter1_sw<2, 5, 2, true><<<gr, PR, Sw1<2, 5, 2, true>::SMEM, s>>>(h->D, par);
@@ -2230,7 +2233,7 @@ int launch_iteration(sg_pcg* h, cudaStream_t s, int par, bool refresh, cudaEvent
     auto k23_streamed = [&](auto Pc) {
       constexpr bool PT = decltype(Pc)::value;
       if (strip) {
-        k_iter23_s5<PT><<<gr, PR, Strip23::SMEM, s>>>(h->D, par);
+        k_iter23_s5<PT><<<gr, kStripC, Strip23::SMEM, s>>>(h->D, par);
       } else if (h->k23 == 1) {
         if (H <= PR) k_iter23_sw<NS, 1, PT><<<gr, kSwThreads, Sw23<NS, 1>::SMEM, s>>>(h->D, par);
         else k_iter23_sw<NS, 2, PT><<<gr, kSwThreads, Sw23<NS, 2>::SMEM, s>>>(h->D, par);
@@ -2471,7 +2474,7 @@ int strip_setup(int* per_sm) {
   SG_CUDA(cudaFuncSetAttribute(k_iter1_s5<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Strip1<2>::SMEM));
   SG_CUDA(cudaFuncSetAttribute(k_iter1_s5<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Strip1<1>::SMEM));
   SG_CUDA(cudaFuncSetAttribute(k_iter1_s5<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Strip1<2>::SMEM));
-  SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_iter23_s5<false>, PR, Strip23::SMEM));
+  SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_iter23_s5<false>, kStripC, Strip23::SMEM));
   if (*per_sm < 1) *per_sm = 1;
   return SG_OK;
 }
