@@ -1964,18 +1964,24 @@ __global__ void __launch_bounds__(kStripC, PART ? 3 : 768 / kStripC) k_iter23_s5
 }
 
 // K1 on strips: d' = s + beta d over each lead line segment, q = A d' on the own columns.
-template <int FMT>
+// CS (coefficient stencil, gen_poisson2d matrices; see k_iter1_sw): the A ring holds one node
+// coefficient per position instead of A's three lower diagonals and the row's five entries are
+// recomputed bitwise; the south neighbour's coefficient (line u - 1) makes that ring RA = 8 lines.
+template <int FMT, bool CS = false>
 struct Strip1 {
   static constexpr int P = 3;
-  static constexpr int NA = FMT == 2 ? 3 : 5;
-  // bytes: A [NA][RL][SP] | d' [RL][SP] | staging [P][2][SP] (s, d) | mask [RL][MK]
-  static constexpr size_t SMEM = (size_t)(NA + 1) * kStripRL * kStripSP * 8 + (size_t)P * 2 * kStripSP * 8 +
-                                 (size_t)kStripRL * kStripMK;
+  static constexpr int NA = CS ? 1 : (FMT == 2 ? 3 : 5);
+  static constexpr int RA = CS ? 8 : kStripRL;  // A / coefficient ring lines (power of two)
+  // bytes: A [NA][RA][SP] | d' [RL][SP] | staging [P][2][SP] (s, d) | mask [RL][MK]
+  static constexpr size_t SMEM = (size_t)NA * RA * kStripSP * 8 + (size_t)kStripRL * kStripSP * 8 +
+                                 (size_t)P * 2 * kStripSP * 8 + (size_t)kStripRL * kStripMK;
 };
 
-template <int FMT, bool PART = false>
+template <int FMT, bool PART = false, bool CS = false>
 __global__ void __launch_bounds__(kStripC, 1024 / kStripC) k_iter1_s5(Dev D, int par) {
-  constexpr int SP = kStripSP, RL = kStripRL, P = Strip1<FMT>::P, NA = Strip1<FMT>::NA, E = kStripE;
+  static_assert(!CS || (FMT == 2 && !PART), "coefficient stencil: symmetric 5-point DIA, one partition");
+  using G = Strip1<FMT, CS>;
+  constexpr int SP = kStripSP, RL = kStripRL, P = G::P, NA = G::NA, RA = G::RA, E = kStripE;
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ __align__(8) uint64_t bars[P];
   __shared__ double red[kStripC / 32];
@@ -2002,20 +2008,23 @@ __global__ void __launch_bounds__(kStripC, 1024 / kStripC) k_iter1_s5(Dev D, int
   auto rowof = [&](long long line, int p) { return s0 + line * W + x0 - E + p; };
   double pdq = 0.0, prr = 0.0;
   if (run) {
-    double* ar = reinterpret_cast<double*>(smraw);  // [NA][RL][SP]
-    double* dp = ar + NA * RL * SP;                   // [RL][SP]
+    double* ar = reinterpret_cast<double*>(smraw);  // [NA][RA][SP]
+    double* dp = ar + NA * RA * SP;                   // [RL][SP]
     double* stg = dp + RL * SP;                       // [P][2][SP]
     unsigned char* mk = reinterpret_cast<unsigned char*>(stg + P * 2 * SP);
     const long long LBl = y0 - 1;
     const int K = (int)(y1 - y0) + 2;
     auto issue = [&](int k) {
-      const int ss = k % P, ls = k & (RL - 1);
+      const int ss = k % P, ls = k & (RL - 1), la = k & (RA - 1);
       const long long row = rowof(LBl + k, 0);
       mbar_arrive_expect_tx(&bars[ss], (uint32_t)((2 + NA) * SP * 8 + kStripMK));
       bulk_g2s(stg + ss * 2 * SP, D.s + row, SP * 8, &bars[ss]);
       bulk_g2s(stg + ss * 2 * SP + SP, dc + row, SP * 8, &bars[ss]);
+      if (CS) bulk_g2s(ar + la * SP, D.coef + row, SP * 8, &bars[ss]);
+      else {
 #pragma unroll
-      for (int d = 0; d < NA; ++d) bulk_g2s(ar + (d * RL + ls) * SP, D.dia.av[d] + row, SP * 8, &bars[ss]);
+        for (int d = 0; d < NA; ++d) bulk_g2s(ar + (d * RA + la) * SP, D.dia.av[d] + row, SP * 8, &bars[ss]);
+      }
       bulk_g2s(mk + ls * kStripMK, D.dia.mask + (row - 14), kStripMK, &bars[ss]);
     };
     if (tid == 0) {
@@ -2051,16 +2060,25 @@ __global__ void __launch_bounds__(kStripC, 1024 / kStripC) k_iter1_s5(Dev D, int
       const long long line = LBl + u;
       if (u >= 1 && tid < cx && line >= y0 && line < y1) {  // q of the own columns of line u
         const int p = tid + E;
-        const int ls = u & (RL - 1);
+        const int ls = u & (RL - 1), la = u & (RA - 1);
         const unsigned int m = mk[ls * kStripMK + p + 14];
         double pr[5];
+        if constexpr (CS) {
+          const double* cu = ar + la * SP + p;
+          double a[5];
+          stencil5(cu[0], ar[((u - 1) & (RA - 1)) * SP + p], cu[-1], cu[1], ar[((u + 1) & (RA - 1)) * SP + p], m,
+                   D.ihx2, D.ihy2, a);
 #pragma unroll
-        for (int d = 0; d < 5; ++d) {
-          // FMT 2: an upper entry (i, i+off) is the lower mirror entry at row i+off
-          double a;
-          if (FMT == 2 && d > 2) a = ar[((4 - d) * RL + ((u + s5a(d)) & (RL - 1))) * SP + p + s5b(d)];
-          else a = ar[(d * RL + ls) * SP + p];
-          pr[d] = mul(a, dp[((u + s5a(d)) & (RL - 1)) * SP + p + s5b(d)]);
+          for (int d = 0; d < 5; ++d) pr[d] = mul(a[d], dp[((u + s5a(d)) & (RL - 1)) * SP + p + s5b(d)]);
+        } else {
+#pragma unroll
+          for (int d = 0; d < 5; ++d) {
+            // FMT 2: an upper entry (i, i+off) is the lower mirror entry at row i+off
+            double a;
+            if (FMT == 2 && d > 2) a = ar[((4 - d) * RA + ((u + s5a(d)) & (RA - 1))) * SP + p + s5b(d)];
+            else a = ar[(d * RA + la) * SP + p];
+            pr[d] = mul(a, dp[((u + s5a(d)) & (RL - 1)) * SP + p + s5b(d)]);
+          }
         }
         const double qi = combine_numpy<5>(pr, m);
         const long long i = rowof(line, p);
@@ -2220,7 +2238,9 @@ int launch_iteration(sg_pcg* h, cudaStream_t s, int par, bool refresh, cudaEvent
     // the streamed kernels exist with and without the row-partition logic (PART)
     auto k1_streamed = [&](auto Pc) {
       constexpr bool PT = decltype(Pc)::value;
-      if (strip) k_iter1_s5<FS, PT><<<gr, kStripC, Strip1<FS>::SMEM, s>>>(h->D, par);
+      if (strip && FMT == 2 && h->cst && !PT)  // A from the coefficient stencil (verified per solve)
+        k_iter1_s5<2, false, true><<<gr, kStripC, Strip1<2, true>::SMEM, s>>>(h->D, par);
+      else if (strip) k_iter1_s5<FS, PT><<<gr, kStripC, Strip1<FS>::SMEM, s>>>(h->D, par);
       else if (st && h->k1sw && FMT == 2 && ND == 5 && h->cst && !PT) {  // A from the coefficient stencil
         if (H <= PR) k_iter1_sw<2, 5, 1, true><<<gr, PR, Sw1<2, 5, 1, true>::SMEM, s>>>(h->D, par);
         else k_iter1_sw<2, 5, 2, true><<<gr, PR, Sw1<2, 5, 2, true>::SMEM, s>>>(h->D, par);
@@ -2472,6 +2492,8 @@ int strip_setup(int* per_sm) {
   SG_CUDA(cudaFuncSetAttribute(k_iter23_s5<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Strip23::SMEM));
   SG_CUDA(cudaFuncSetAttribute(k_iter1_s5<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Strip1<1>::SMEM));
   SG_CUDA(cudaFuncSetAttribute(k_iter1_s5<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Strip1<2>::SMEM));
+  SG_CUDA(cudaFuncSetAttribute(k_iter1_s5<2, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)Strip1<2, true>::SMEM));
   SG_CUDA(cudaFuncSetAttribute(k_iter1_s5<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Strip1<1>::SMEM));
   SG_CUDA(cudaFuncSetAttribute(k_iter1_s5<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Strip1<2>::SMEM));
   SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_iter23_s5<false>, kStripC, Strip23::SMEM));
@@ -3073,9 +3095,11 @@ extern "C" int sg_pcg_set_stencil(sg_pcg* h, const double* coeff, int64_t nx, in
   if (!h) { set_error("null handle"); return SG_EINVAL; }
   if (usable_host) *usable_host = 0;
   const Dia& dd = h->D.dia;
-  // only the streamed K1 (k_iter1_sw) regenerates A: one-CTA small systems, the tile and strip
-  // kernels and the row partition keep the stored diagonals (no per-solve copy + check for them)
-  const bool fits = coeff && nx > 1 && ny >= 1 && h->dia_nd == 5 && !h->part && h->staged && h->k1sw && !h->small &&
+  // only the streamed K1 kernels (k_iter1_sw, the strip k_iter1_s5) regenerate A: one-CTA small
+  // systems, the tile kernels and the row partition keep the stored diagonals (no per-solve copy +
+  // check for them)
+  const bool fits = coeff && nx > 1 && ny >= 1 && h->dia_nd == 5 && !h->part &&
+                    ((h->staged && h->k1sw && !h->small) || h->strip) &&
                     dd.off[1] == -1 && dd.off[2] == 0 && dd.off[3] == 1 && dd.off[4] == -dd.off[0] &&
                     (int64_t)dd.off[4] == nx;
   const double ihx2 = (double)((nx + 1) * (nx + 1)), ihy2 = (double)((ny + 1) * (ny + 1));  // datasets.py:109-110

@@ -72,6 +72,9 @@ def gen_poisson2d(nx: int, ny: int, coeff_seed: int | None = None):
     coeff = heat_coeff(nx, ny, coeff_seed)
     coeff_dev = L.to_device(coeff, torch.float64)
     A = SparseMatrix.from_device(poisson2d_device(nx, ny, coeff_dev))
+    # the generator's node field: pcg_solve lets its streamed K1 regenerate A from it (8 instead
+    # of 24 B per row), after verifying A against it bitwise at every solve (sg_pcg_set_stencil)
+    A._stencil = (coeff_dev, nx, ny)
     family = "poisson2d" if coeff_seed is None else "heat2d"
     meta = ProblemMeta(family=family, n=nx * ny, grid=(nx, ny), coeff=coeff, coeff_seed=coeff_seed,
                        coeff_dev=coeff_dev)

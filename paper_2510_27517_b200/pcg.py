@@ -11,6 +11,7 @@ from __future__ import annotations
 import ctypes as C
 import json
 import math
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -404,6 +405,13 @@ def pcg_solve(A: SparseMatrix, b, M: Preconditioner, cfg: SolveConfig | None = N
     if kind_name is None:
         return _pcg_generic(A, b, M, cfg, was_t)
     h = _handle_for(A, M, kind_name)
+    # gen_poisson2d matrices carry their node field: the streamed K1 regenerates A from it
+    # (verified bitwise against A at every solve; SG_PCG_STENCIL=0 turns it off)
+    st = getattr(A, "_stencil", None)
+    if st is not None and os.environ.get("SG_PCG_STENCIL", "1") != "0":
+        h.set_stencil(st[0], st[1], st[2])
+    elif getattr(h, "_coeff", None) is not None:
+        h.set_stencil(None, 0, 0)
     b_dev = b.to(device=L.device(), dtype=torch.float64).contiguous() if was_t else \
         L.to_device(np.asarray(b, dtype=np.float64), torch.float64)
     x_dev = L.empty(n, torch.float64)

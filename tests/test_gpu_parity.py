@@ -838,3 +838,36 @@ def test_training_batched_union_graph():
     assert np.allclose(log.losses(), g["train_losses"], rtol=1e-9, atol=0), (log.losses(), g["train_losses"])
     p = m.params_flat()
     assert np.max(np.abs(p - g["train_params"])) <= 1e-8 * np.max(np.abs(g["train_params"]))
+
+
+@pytest.mark.parametrize("grid", [(1024, 24), (784, 20)])
+def test_strip_coefficient_stencil_bit_identical(monkeypatch, grid):
+    """Wide grids (the C5 strip kernels): K1 regenerating A from gen_poisson2d's coefficients
+    == K1 streaming A's lower-half diagonals, bitwise (k, x, residual history); and a matrix whose
+    values no longer come from the coefficients falls back to the stored diagonals."""
+    import os
+    import paper_2510_27517_b200.pcg as PC
+    m = P.load_checkpoint(os.path.join(os.path.dirname(__file__), "golden", "trained_heat16.spaignn"))
+    nx, ny = grid
+    A, meta = P.gen_poisson2d(nx, ny, coeff_seed=3)
+    G = P.forward(m, P.build_graph(A, meta)).G
+    M = P.build_learned_spai(G, m.config.epsilon)
+    b = P.gen_rhs(meta, 4)
+    cfg = P.SolveConfig(rtol=1e-9, residual_refresh_period=9)
+    out = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("SG_PCG_STENCIL", flag)
+        rep = P.pcg_solve(A, b, M, cfg)
+        mode = PC._handle_for(A, M).stats()[2][6]
+        out[flag] = (rep.k, rep.x.copy(), np.asarray(rep.residual_history), mode)
+    assert out["1"][3] == 2.0 and out["0"][3] == 1.0
+    assert out["1"][0] == out["0"][0]
+    assert np.array_equal(out["1"][1], out["0"][1]) and np.array_equal(out["1"][2], out["0"][2])
+    # values rescaled: A is no longer the coefficients' matrix -> the check rejects the stencil
+    monkeypatch.setenv("SG_PCG_STENCIL", "1")
+    A2 = A.with_values(2.0 * A.values)
+    A2._stencil = A._stencil
+    rep2 = P.pcg_solve(A2, b, M, cfg)
+    assert PC._handle_for(A2, M).stats()[2][6] == 1.0
+    o, c, v = A2.row_offsets, A2.col_indices, A2.values
+    assert rep2.converged and np.linalg.norm(b - O.spmv(o, c, v, rep2.x)) / np.linalg.norm(b) <= 1e-9
