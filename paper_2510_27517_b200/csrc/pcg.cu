@@ -145,6 +145,10 @@ struct Dev {
   // gen_poisson2d inside the sliding-window K1 instead of streaming its diagonals
   const double* coef;  // [n] with the diagonals' guard rows
   double ihx2, ihy2;
+  // wide-grid strips: G + mask of every (strip, line) segment as one contiguous block (see
+  // k_strip_gblocks), so K2+K3 fetches a line's G with ONE bulk copy
+  const unsigned char* gblk;
+  long long gblk_L;  // extended lines per strip (every system's lines + 4 zero lines)
   // vectors
   double *b, *x, *r0, *r1, *d0, *d1, *q, *s, *t;
   // reduction scratch
@@ -1819,16 +1823,58 @@ constexpr int kStripRL = 4;                // ring lines (power of two)
 __device__ __forceinline__ constexpr int s5a(int d) { return d == 0 ? -1 : (d == 4 ? 1 : 0); }
 __device__ __forceinline__ constexpr int s5b(int d) { return d == 1 ? -1 : (d == 3 ? 1 : 0); }
 
+// G of a wide grid in strip blocks: block (strip sx, extended line) = G's five diagonals at the
+// SP positions of that line segment ([5][SP] doubles) followed by their mask bytes.  Extended lines
+// are laid out per strip over all systems, each system framed by two zero lines on each side
+// (the warm-up / lead-out lines of its first and last ranges); positions outside the system are
+// zero (their products are masked out by the centre rows' masks).  Built once per solve after G's
+// diagonals, so the strip K2+K3 streams one contiguous ~10 KB copy per line instead of six ~2 KB
+// ones -- small bulk copies cap the copy engine's bandwidth (profiles/r03_stream_bw.txt), while
+// r, q, x, d come by plain coalesced loads issued a step ahead.
+constexpr int kStripMKB = (kStripSP + 15) / 16 * 16;
+constexpr int kStripBB = 5 * kStripSP * 8 + kStripMKB;  // bytes per block (16-byte multiple)
+
+__global__ void k_strip_gblocks(Dev D, unsigned char* blk) {
+  const int sys = blockIdx.y;
+  long long s0, s1;
+  sys_bounds(D, sys, s0, s1);
+  const long long W = D.dia.W, nl = (s1 - s0) / W, L = D.gblk_L;
+  const long long ns = (W + kStripC - 1) / kStripC;
+  const long long gl0 = s0 / W + 4LL * sys;
+  const long long tot = ns * (nl + 4) * kStripSP;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+    const int p = (int)(e % kStripSP);
+    const long long t = e / kStripSP;
+    const long long yl = t % (nl + 4), sx = t / (nl + 4);
+    const long long row = s0 + (yl - 2) * W + sx * kStripC - kStripE + p;
+    const bool in = yl >= 2 && yl < nl + 2 && row >= s0 && row < s1;
+    unsigned char* bp = blk + (sx * L + gl0 + yl) * kStripBB;
+    double* g = reinterpret_cast<double*>(bp);
+#pragma unroll
+    for (int d = 0; d < 5; ++d) g[d * kStripSP + p] = in ? D.dia.gv[d][row] : 0.0;
+    bp[5 * kStripSP * 8 + p] = in ? D.dia.mask[row] : (unsigned char)0;
+  }
+}
+
+#ifndef SG_STRIP_PG
+#define SG_STRIP_PG 2
+#endif
+
 struct Strip23 {
-  static constexpr int P = 2;
-  // bytes: G [5][RL][SP] | r' [RL][SP] | t [RL][SP] | staging [P] (q [SP], x [C], d [C]) | mask [RL][MK]
-  static constexpr size_t SMEM = (size_t)(5 + 2) * kStripRL * kStripSP * 8 +
-                                 (size_t)P * (kStripSP + 2 * kStripC) * 8 + (size_t)kStripRL * kStripMK;
+  static constexpr int P = SG_STRIP_PG;  // G blocks in flight (incl. the current line)
+  static constexpr int RG = P + 2;       // G block ring (lines k - 2 .. k + P - 1)
+  // bytes: G blocks [RG][BB] | r' [RL][SP] | t [RL][SP]
+  static constexpr size_t SMEM = (size_t)RG * kStripBB + (size_t)2 * kStripRL * kStripSP * 8;
 };
+
+// Position-relative bounds: row j = rb + p of a line segment lies in [lo, hi) iff p lies in
+// [prel(lo - rb), prel(hi - rb)) -- per-line (uniform) 64-bit work, per-position 32-bit compares.
+__device__ __forceinline__ int prel(long long v) { return (int)(v < -1 ? -1 : (v > (1 << 20) ? (1 << 20) : v)); }
 
 template <bool PART = false>
 __global__ void __launch_bounds__(kStripC, PART ? 3 : 768 / kStripC) k_iter23_s5(Dev D, int par) {
-  constexpr int SP = kStripSP, RL = kStripRL, P = Strip23::P, C = kStripC, E = kStripE;
+  constexpr int SP = kStripSP, RL = kStripRL, P = Strip23::P, RG = Strip23::RG, C = kStripC, E = kStripE;
+  constexpr int BBD = kStripBB / 8, MKO = 5 * SP * 8;
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ __align__(8) uint64_t bars[P];
   __shared__ double red[kStripC / 32];
@@ -1850,31 +1896,18 @@ __global__ void __launch_bounds__(kStripC, PART ? 3 : 768 / kStripC) k_iter23_s5
   const double* dn = par ? D.d0 : D.d1;
   const double* rc = par ? D.r1 : D.r0;
   double* rn = par ? D.r0 : D.r1;
-  double* gr = reinterpret_cast<double*>(smraw);  // [5][RL][SP]
-  double* rp = gr + 5 * RL * SP;                    // [RL][SP]
+  double* gb = reinterpret_cast<double*>(smraw);  // [RG][BBD]
+  double* rp = gb + RG * BBD;                       // [RL][SP]
   double* tr = rp + RL * SP;                        // [RL][SP]
-  double* stg = tr + RL * SP;                       // [P][SP + 2C]
-  unsigned char* mk = reinterpret_cast<unsigned char*>(stg + P * (SP + 2 * C));  // [RL][MK]
-  const long long LBl = y0 - 2;                     // line of step 0
   const int K = (int)(y1 - y0) + 4;
-  auto rowof = [&](long long line, int p) { return s0 + line * W + x0 - E + p; };
+  // row of position 0 of step k's lead line (line y0 - 2 + k)
+  const long long rb0 = s0 + (y0 - 2) * W + x0 - E;
+  // the block of step k's line (extended line y0 + k of this system)
+  const unsigned char* gsrc = D.gblk + ((long long)(x0 / C) * D.gblk_L + s0 / W + 4LL * sys + y0) * kStripBB;
+  auto gline = [&](int k) { return gb + (k % RG) * BBD; };
   auto issue = [&](int k) {
-    const int ss = k % P, ls = k & (RL - 1);
-    double* st = stg + ss * (SP + 2 * C);
-    const long long row = rowof(LBl + k, 0);
-    const bool own = k >= 4;
-    const uint32_t bytes = (uint32_t)((2 + 5) * SP * 8 + kStripMK + (own ? 2 * C * 8 : 0));
-    mbar_arrive_expect_tx(&bars[ss], bytes);
-    bulk_g2s(rp + ls * SP, rc + row, SP * 8, &bars[ss]);
-    bulk_g2s(st, D.q + row, SP * 8, &bars[ss]);
-#pragma unroll
-    for (int d = 0; d < 5; ++d) bulk_g2s(gr + (d * RL + ls) * SP, D.dia.gv[d] + row, SP * 8, &bars[ss]);
-    bulk_g2s(mk + ls * kStripMK, D.dia.mask + (row - 14), kStripMK, &bars[ss]);
-    if (own) {
-      const long long ro = rowof(LBl + k - 2, E);
-      bulk_g2s(st + SP, D.x + ro, C * 8, &bars[ss]);
-      bulk_g2s(st + SP + C, dn + ro, C * 8, &bars[ss]);
-    }
+    mbar_arrive_expect_tx(&bars[k % P], (uint32_t)kStripBB);
+    bulk_g2s(gline(k), gsrc + (long long)k * kStripBB, kStripBB, &bars[k % P]);
   };
   if (tid == 0) {
 #pragma unroll
@@ -1882,65 +1915,89 @@ __global__ void __launch_bounds__(kStripC, PART ? 3 : 768 / kStripC) k_iter23_s5
     mbar_init_fence();
   }
   __syncthreads();
-  if (tid == 0) issue(0);
+  if (tid == 0)
+    for (int k = 0; k < P - 1 && k < K; ++k) issue(k);
+  // r, q of the lead line segment: plain loads one step ahead (guard bands cover the lines
+  // beyond the system; those values are masked to zero)
+  const bool two = tid + C < SP;  // this thread also holds halo position tid + C
+  double nr[2] = {0.0, 0.0}, nq[2] = {0.0, 0.0};
+  auto load_rq = [&](long long rb) {
+    nr[0] = __ldcs(rc + rb + tid);
+    nq[0] = __ldcs(D.q + rb + tid);
+    if (two) {
+      nr[1] = __ldcs(rc + rb + tid + C);
+      nq[1] = __ldcs(D.q + rb + tid + C);
+    }
+  };
+  load_rq(rb0);
   double prr = 0.0, prs = 0.0;
   for (int k = 0; k < K; ++k) {
-    const double* st = stg + (k % P) * (SP + 2 * C);
-    mbar_wait(&bars[k % P], (uint32_t)((k / P) & 1));
-    {  // A: r' of the lead line segment (in place over the r copy)
-      const long long line = LBl + k;
+    const double cr[2] = {nr[0], nr[1]}, cq[2] = {nq[0], nq[1]};
+    const long long rb = rb0 + (long long)k * W;  // lead line (A)
+    if (k + 1 < K) load_rq(rb + W);
+    // x, d of this step's output line (phase C): in flight across phases A and B
+    const int mm = k - 2;
+    const long long rbm = rb - 2 * W;
+    const bool ownc = mm >= 2 && tid < cx && mm - 2 < y1 - y0;
+    double xo = 0.0, dd = 0.0;
+    if (ownc) {
+      xo = D.x[rbm + E + tid];
+      dd = __ldcs(dn + rbm + E + tid);
+    }
+    {  // A: r' of the lead line segment
+      const int lo = prel(s0 - rb), hi = prel(s1 - rb);
+      const bool lown = k >= 2 && k - 2 < y1 - y0;  // the lead line is one of the range's own lines
+      const int olo = PART ? prel(ow.o0 - rb) : INT_MIN, ohi = PART ? prel(ow.o1 - rb) : INT_MAX;
       const int ls = k & (RL - 1);
 #pragma unroll
       for (int h2 = 0; h2 < 2; ++h2) {
-        const int p = tid + h2 * kStripC;
-        if (p < SP) {
-          const long long j = rowof(line, p);
-          double v = sub(rp[ls * SP + p], mul(alpha, st[p]));
-          v = (j >= s0 && j < s1) ? v : 0.0;
-          const int x = x0 - E + p;
-          if (line >= y0 && line < y1 && x >= x0 && x < x0 + cx) {
-            rn[j] = v;
-            if (owned(ow, j)) prr += mul(v, v);
+        const int p = tid + h2 * C;
+        if (h2 == 0 || two) {
+          double v = sub(cr[h2], mul(alpha, cq[h2]));
+          v = (p >= lo && p < hi) ? v : 0.0;
+          if (lown && p >= E && p < E + cx) {
+            rn[rb + p] = v;
+            if (p >= olo && p < ohi) prr += mul(v, v);
           }
           rp[ls * SP + p] = v;
         }
       }
     }
+    mbar_wait(&bars[k % P], (uint32_t)((k / P) & 1));  // G of line k (B's u + 1 neighbour)
     __syncthreads();
-    if (tid == 0 && k + 1 < K) issue(k + 1);
+    if (tid == 0 && k + P - 1 < K) issue(k + P - 1);
     const int u = k - 1;
     if (u >= 1) {  // B: t on positions 1 .. SP-2 of line u (add.at order over G's mirrors)
+      const long long rbu = rb - W;
+      const int lo = prel(s0 - rbu), hi = prel(s1 - rbu);
+      const unsigned char* mu = reinterpret_cast<const unsigned char*>(gline(u)) + MKO;
 #pragma unroll
       for (int h2 = 0; h2 < 2; ++h2) {
-        const int p = 1 + tid + h2 * kStripC;
-        if (p < SP - 1) {
-          const long long j = rowof(LBl + u, p);
-          const unsigned int m = mk[(u & (RL - 1)) * kStripMK + p + 14];
+        const int p = 1 + tid + h2 * C;
+        if (h2 == 0 || p < SP - 1) {
+          const unsigned int m = mu[p];
           double pr[5];
 #pragma unroll
-          for (int d = 0; d < 5; ++d) {
-            const int ix = ((u + s5a(d)) & (RL - 1)) * SP + p + s5b(d);
-            pr[d] = mul(gr[(4 - d) * RL * SP + ix], rp[ix]);
-          }
+          for (int d = 0; d < 5; ++d)
+            pr[d] = mul(gline(u + s5a(d))[(4 - d) * SP + p + s5b(d)],
+                        rp[((u + s5a(d)) & (RL - 1)) * SP + p + s5b(d)]);
           const double v = combine_seq<5>(pr, m);
-          tr[(u & (RL - 1)) * SP + p] = (j >= s0 && j < s1) ? v : 0.0;
+          tr[(u & (RL - 1)) * SP + p] = (p >= lo && p < hi) ? v : 0.0;
         }
       }
     }
     __syncthreads();
-    const int mm = k - 2;
-    const long long line = LBl + mm;
-    if (mm >= 2 && tid < cx && line >= y0 && line < y1) {  // C: own columns of line mm
+    if (ownc) {  // C: own columns of line mm
       const int p = tid + E;
-      const long long i = rowof(line, p);
-      D.x[i] = add(st[SP + tid], mul(alpha, st[SP + C + tid]));
+      const long long i = rbm + p;
+      D.x[i] = add(xo, mul(alpha, dd));
       if (owned(ow, i)) {  // s of owned rows only: ghost s comes from the neighbour partitions
         const int ls = mm & (RL - 1);
-        const unsigned int m = mk[ls * kStripMK + p + 14];
+        const double* gm = gline(mm);
+        const unsigned int m = reinterpret_cast<const unsigned char*>(gm)[MKO + p];
         double pr[5];
 #pragma unroll
-        for (int d = 0; d < 5; ++d)
-          pr[d] = mul(gr[(d * RL + ls) * SP + p], tr[((mm + s5a(d)) & (RL - 1)) * SP + p + s5b(d)]);
+        for (int d = 0; d < 5; ++d) pr[d] = mul(gm[d * SP + p], tr[((mm + s5a(d)) & (RL - 1)) * SP + p + s5b(d)]);
         const double y = combine_numpy<5>(pr, m);
         const double rni = rp[ls * SP + p];
         const double si = add(y, mul(eps, rni));
@@ -2156,6 +2213,7 @@ struct sg_pcg {
   long long guard = 0;  // DIA: zero rows around every vector / diagonal
   unsigned int* d_flag = nullptr;
   void* dia_mem = nullptr;
+  void* gblk_mem = nullptr;  // strip G blocks (k_strip_gblocks)
   double* dia_g = nullptr;
   double* dia_a = nullptr;
   unsigned char* dia_mask = nullptr;
@@ -2711,6 +2769,12 @@ extern "C" int sg_pcg_create(sg_pcg** out, int32_t n_systems, const int64_t* sys
     }
     const char* rl = getenv("SG_SW_RANGE");
     if (rl && atoll(rl) > 0) rng_len = atoll(rl);
+    if (h->pre == SG_PRECOND_LEARNED) {  // G strip blocks: every system's lines + 4 zero lines, per strip
+      const long long L = h->n / W + 4LL * n_systems;
+      SG_CUDA(cudaMalloc(&h->gblk_mem, (size_t)(nstrip * L) * kStripBB));
+      h->D.gblk = static_cast<const unsigned char*>(h->gblk_mem);
+      h->D.gblk_L = L;
+    }
   } else {
     rng_len = 1LL << 62;
   }
@@ -2878,6 +2942,11 @@ extern "C" int sg_pcg_solve(sg_pcg* h, const double* b, double* x, const sg_solv
     if (h->pre == SG_PRECOND_LEARNED)
       k_csr_to_dia<<<gb, 256, 0, s>>>(h->D.g_offs, h->D.g_cols, h->D.g_vals, h->n, h->D.dia, h->dia_g, nullptr,
                                       h->d_flag + 2);
+    if (h->gblk_mem) {
+      k_strip_gblocks<<<dim3(148 * 4, (unsigned)h->S), 256, 0, s>>>(h->D, static_cast<unsigned char*>(h->gblk_mem));
+      SG_LAUNCH_CHECK("k_strip_gblocks");
+      h->kernels += 1;
+    }
     k_dia_symcheck<<<gb, 256, 0, s>>>(h->D.dia, h->d_flag);
     SG_LAUNCH_CHECK("k_csr_to_dia / k_dia_symcheck");
     h->kernels += h->pre == SG_PRECOND_LEARNED ? 3 : 2;
@@ -3184,6 +3253,7 @@ extern "C" void sg_pcg_destroy(sg_pcg* h) {
   cudaDeviceSynchronize();
   if (h->hist) cudaFree(h->hist);
   if (h->dia_mem) cudaFree(h->dia_mem);
+  if (h->gblk_mem) cudaFree(h->gblk_mem);
   for (int k = 0; k < 3; ++k) {
     if (h->sell_mem[k]) cudaFree(h->sell_mem[k]);
     if (h->sell_vals[k]) cudaFree(h->sell_vals[k]);

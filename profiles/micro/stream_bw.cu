@@ -156,19 +156,27 @@ int main() {
     cudaMalloc(&arrs[a], n * 8);
     cudaMemset(arrs[a], 0, n * 8);
   }
+  double* blk;
+  cudaMalloc(&blk, 5 * n * 8);
+  cudaMemset(blk, 0, 5 * n * 8);
+  // separate 2 KB streams (the sliding-window / strip kernels' layout): streams x depth x CTAs/SM
   run<2, 3>(arrs, n, 3, 256);
   run<4, 3>(arrs, n, 3, 256);
   run<8, 3>(arrs, n, 3, 256);
-  run<12, 3>(arrs, n, 3, 256);
-  run<8, 4>(arrs, n, 3, 256);
+  run<10, 2>(arrs, n, 3, 256);
+  run<10, 3>(arrs, n, 2, 256);
+  run<10, 4>(arrs, n, 2, 256);
+  run<4, 6>(arrs, n, 4, 256);
+  run<4, 8>(arrs, n, 3, 256);
+  // larger copies
+  run<10, 2>(arrs, n, 1, 1024);
+  run<4, 3>(arrs, n, 2, 1024);
   run<8, 3>(arrs, n, 3, 512);
   run<8, 3>(arrs, n, 2, 512);
   run<4, 3>(arrs, n, 3, 1024);
   run<2, 3>(arrs, n, 3, 2048);
-  run<8, 6>(arrs, n, 2, 256);
-  double* blk;
-  cudaMalloc(&blk, 5 * n * 8);
-  cudaMemset(blk, 0, 5 * n * 8);
+  // 5 diagonals as one interleaved block copy per chunk + vector streams (bulk or plain loads)
+  run_mixed<5, 4, 2, 1>(blk, arrs, n, 3, 256);
   run_mixed<5, 4, 3, 1>(blk, arrs, n, 3, 256);
   run_mixed<5, 4, 3, 0>(blk, arrs, n, 3, 256);
   run_mixed<5, 2, 3, 1>(blk, arrs, n, 3, 256);
