@@ -1,0 +1,5 @@
+O=gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_rowpart.py tests/test_gpu_config_parity.py -m gpu -q -p no:cacheprovider -k "strip or wide or partition or c5 or C5 or control_flow" > $O/r03_k1own_tests.log 2>&1; echo rc=$? >> $O/r03_k1own_tests.log
+for v in 1 0 1 0; do
+  SG_STRIP_K1_OWN=$v timeout 400 python bench_configs.py --config c5 --steps 3 --warmup 1 >> $O/r03_k1own_$v.jsonl 2>> $O/r03_k1own.err
+done

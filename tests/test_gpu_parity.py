@@ -594,12 +594,13 @@ def test_batch_mixed_grids_unaligned_systems(multi_kernel):
         assert np.linalg.norm(b - O.spmv(o, c, v, rb.x)) / np.linalg.norm(b) <= 1.01e-8
 
 
-@pytest.mark.parametrize("small", ["0", "1"])
-def test_pcg_control_flow_on_sliding_window_kernels(small, monkeypatch):
+@pytest.mark.parametrize("small,grid", [("0", (24, 24)), ("1", (24, 24)), ("0", (528, 10))])
+def test_pcg_control_flow_on_sliding_window_kernels(small, grid, monkeypatch):
     """The reference control-flow variants (refresh period, delta termination + certification,
     max_iters, zero rhs, non-learned preconditioners) on a 5-point grid, i.e. through the
     sliding-window K1 / fused K2+K3 kernels rather than the CSR ones the golden cases use
-    (small="1": the same cases through the one-CTA-per-system solver, k_pcg_small)."""
+    (small="1": the same cases through the one-CTA-per-system solver, k_pcg_small; a 528-wide
+    grid: through the 2-D strip kernels, three strips with a partial last one)."""
     import os
     import paper_2510_27517_b200.pcg as PC
     monkeypatch.setenv("SG_PCG_SMALL", small)
@@ -607,7 +608,7 @@ def test_pcg_control_flow_on_sliding_window_kernels(small, monkeypatch):
         h.close()
     PC._HANDLES = None
     m = P.load_checkpoint(os.path.join(os.path.dirname(__file__), "golden", "trained_heat16.spaignn"))
-    A, meta = P.gen_poisson2d(24, 24, coeff_seed=4)
+    A, meta = P.gen_poisson2d(grid[0], grid[1], coeff_seed=4)
     G = P.forward(m, P.build_graph(A, meta)).G
     o, c, v = (np.asarray(A.row_offsets), np.asarray(A.col_indices), np.asarray(A.values))
     gv = np.asarray(G.values)
