@@ -1081,7 +1081,7 @@ __global__ void __launch_bounds__(PR) k_iter3_wr(Dev D, int par, int refreshed) 
   }
 }
 
-// ------------------------------------------------------------------ small systems: one CTA per system
+// ------------------------------------------------------------------ small systems: one CTA / cluster per system
 // For stencil (DIA) systems of <= kSmallRows rows the multi-kernel iteration is launch- and
 // latency-bound (~18-19 us per iteration from 256 to 8100 rows).  Measured per iteration, one
 // CTA / multi-kernel: 256 rows 8.0 / 18.0 us, 1024 rows 9.4 / 19.4, 2304 rows 13.0 / 18.2,
@@ -1090,13 +1090,65 @@ __global__ void __launch_bounds__(PR) k_iter3_wr(Dev D, int par, int refreshed) 
 // the same phases, roundings, summation orders and finalisers as k_iter1/2/3 + k_refresh_*
 // (dot products: per-thread partials in row order, then the block tree).  `iters` iterations per
 // launch (the host polls the active count between launches, as between graph chunks).
+//
+// Mid-size systems (up to kClusterRows rows) run the same loop on a THREAD-BLOCK CLUSTER of CN
+// CTAs (one per SM, CN <= 16): rows interleave over the cluster's CN * 1024 threads, the phase
+// barriers are hardware cluster barriers (barrier.cluster release / acquire: every global write
+// of a phase is visible to the whole cluster after it) and the dot products add the CTAs' block
+// sums in rank order through distributed shared memory (rank 0's slots), so one launch still runs
+// whole iterations with no kernel boundary.
 constexpr int kSmallRows = 3072;
 constexpr int kSmallThreads = 1024;
+#ifndef SG_CLUSTER_ROWS
+#define SG_CLUSTER_ROWS 32768
+#endif
+constexpr int kClusterRows = SG_CLUSTER_ROWS;
 
-template <int PRE, int FMT, int ND>
+template <int CN>
+__device__ __forceinline__ void sm_sync() {
+  if constexpr (CN == 1) __syncthreads();
+  else asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+// The system's dot product: block tree per CTA, then (CN > 1) rank 0 adds the CTAs' sums in rank
+// order from its shared-memory slots (written by the ranks through DSMEM).  Valid in thread 0 of
+// rank 0 after the call; `slots` is a __shared__ [2][16] array used alternately by consecutive
+// calls (`seq` counts them), so a rank's next write never meets rank 0 still reading.
+template <int CN>
+__device__ __forceinline__ double sm_sum(double v, double* red, double* slots_all, int& seq) {
+  const double bs = block_sum(v, red);
+  if constexpr (CN == 1) {
+    return bs;
+  } else {
+    double* slots = slots_all + 16 * (seq++ & 1);
+    if (threadIdx.x == 0) {
+      uint32_t dst;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(dst) : "r"(smem_u32(slots + cluster_rank())));
+      asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(dst), "d"(bs) : "memory");
+    }
+    sm_sync<CN>();
+    double r = 0.0;
+    if (threadIdx.x == 0 && cluster_rank() == 0)
+      for (int k = 0; k < CN; ++k) r += slots[k];
+    return r;
+  }
+}
+
+template <int PRE, int FMT, int ND, int CN = 1>
 __global__ void __launch_bounds__(kSmallThreads, 1) k_pcg_small(Dev D, int iters, long long period) {
   __shared__ double red[32];
-  const int sys = blockIdx.x, tid = threadIdx.x;
+  __shared__ double slots[32];
+  int seq = 0;
+  const int rank = CN == 1 ? 0 : (int)cluster_rank();
+  const int sys = blockIdx.x / CN, tid = rank * kSmallThreads + (int)threadIdx.x;
+  constexpr int NT = CN * kSmallThreads;  // threads per system
+  const bool lead = threadIdx.x == 0 && rank == 0;
   const long long s0 = D.blk_r0[D.sys_blk0[sys]], s1 = D.sys_r1[sys];
   const double eps = D.ctl->eps;
   double* x = D.x;
@@ -1118,55 +1170,55 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_pcg_small(Dev D, int iters
     // K1: d = s + beta d; q = A d, d.q; fresh residual b - A x (pcg.py:176-184, 208-215)
     double pdq = 0.0, prr = 0.0;
     if (run) {
-      for (long long i = s0 + tid; i < s1; i += kSmallThreads) d[i] = add(D.s[i], mul(beta, d[i]));
-      __syncthreads();
-      for (long long i = s0 + tid; i < s1; i += kSmallThreads) {
+      for (long long i = s0 + tid; i < s1; i += NT) d[i] = add(D.s[i], mul(beta, d[i]));
+      sm_sync<CN>();
+      for (long long i = s0 + tid; i < s1; i += NT) {
         const double qi = rowA(i, XF{d, nullptr, 0.0});
         D.q[i] = qi;
         pdq += mul(d[i], qi);
       }
     }
     if (fresh) {
-      for (long long i = s0 + tid; i < s1; i += kSmallThreads) {
+      for (long long i = s0 + tid; i < s1; i += NT) {
         const double rf = sub(D.b[i], rowA(i, XF{x, nullptr, 0.0}));
         if (run) r[i] = rf;
         prr += mul(rf, rf);
       }
     }
-    const double dq = block_sum(pdq, red);
-    const double rrf = block_sum(prr, red);
-    if (tid == 0) fin_k1(D, sys, run, dq, rrf);
-    __syncthreads();
+    const double dq = sm_sum<CN>(pdq, red, slots, seq);
+    const double rrf = sm_sum<CN>(prr, red, slots, seq);
+    if (lead) fin_k1(D, sys, run, dq, rrf);
+    sm_sync<CN>();
     if (S.status != ST_RUN) continue;
     const double alpha = S.alpha;
     // K2: x += alpha d; r -= alpha q (or, on refresh iterations, r = b - A x); ||r||^2
     double prn = 0.0;
-    for (long long i = s0 + tid; i < s1; i += kSmallThreads) x[i] = add(x[i], mul(alpha, d[i]));
+    for (long long i = s0 + tid; i < s1; i += NT) x[i] = add(x[i], mul(alpha, d[i]));
     if (refresh) {
-      __syncthreads();
-      for (long long i = s0 + tid; i < s1; i += kSmallThreads) {
+      sm_sync<CN>();
+      for (long long i = s0 + tid; i < s1; i += NT) {
         const double rn = sub(D.b[i], rowA(i, XF{x, nullptr, 0.0}));
         r[i] = rn;
         prn += mul(rn, rn);
       }
     } else {
-      for (long long i = s0 + tid; i < s1; i += kSmallThreads) {
+      for (long long i = s0 + tid; i < s1; i += NT) {
         const double rn = sub(r[i], mul(alpha, D.q[i]));
         r[i] = rn;
         prn += mul(rn, rn);
       }
     }
-    const double rr = block_sum(prn, red);
-    if (tid == 0) fin_rr(D, sys, rr);
-    __syncthreads();
+    const double rr = sm_sum<CN>(prn, red, slots, seq);
+    if (lead) fin_rr(D, sys, rr);
+    sm_sync<CN>();
     // K3: s = M r (learned: t = G^T r, then s = G t + eps r); r.s
     if (PRE == SG_PRECOND_LEARNED) {
-      for (long long i = s0 + tid; i < s1; i += kSmallThreads)
+      for (long long i = s0 + tid; i < s1; i += NT)
         D.t[i] = dia_row_t_seq<ND, 0>(D.dia, D.dia.gv, (int)i, D.dia.mask[i], XF{r, nullptr, 0.0});
-      __syncthreads();
+      sm_sync<CN>();
     }
     double prs = 0.0;
-    for (long long i = s0 + tid; i < s1; i += kSmallThreads) {
+    for (long long i = s0 + tid; i < s1; i += NT) {
       double si;
       if (PRE == SG_PRECOND_IDENTITY) si = r[i];
       else if (PRE == SG_PRECOND_JACOBI) si = mul(r[i], D.inv_diag[i]);
@@ -1175,9 +1227,9 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_pcg_small(Dev D, int iters
       D.s[i] = si;
       prs += mul(r[i], si);
     }
-    const double rs = block_sum(prs, red);
-    if (tid == 0) fin_k3(D, sys, rs, refresh ? 1 : 0);
-    __syncthreads();
+    const double rs = sm_sum<CN>(prs, red, slots, seq);
+    if (lead) fin_k3(D, sys, rs, refresh ? 1 : 0);
+    sm_sync<CN>();
   }
 }
 
@@ -2202,6 +2254,7 @@ struct sg_pcg {
   int k1sw = 1;       // K1 variant: 1 = sliding window (k_iter1_sw), 0 = tiles (k_iter1_st)
   int g_warp = 0;     // CSR G with long rows: K3 one warp per row (k_iter3_wr)
   int small = 0;      // DIA systems of <= kSmallRows rows: one CTA per system (k_pcg_small)
+  int scn = 1;        // ... of <= kClusterRows rows: one cluster of scn CTAs per system
   int k23 = 1;        // fused K2+K3 variant: 1 = sliding window (k_iter23_sw), 0 = tiles (k_iter23_st)
   void* sell_mem[3] = {nullptr, nullptr, nullptr};   // SELL-32 patterns of A, G, G^T
   void* sell_vals[3] = {nullptr, nullptr, nullptr};
@@ -2542,6 +2595,53 @@ int sw_attr(int* per_sm) {
                                  (int)Sw1<2, 5, NH, true>::SMEM));
   SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_iter23_sw<ND, NH>, kSwThreads, Sw23<ND, NH>::SMEM));
   if (*per_sm < 1) *per_sm = 1;
+  return SG_OK;
+}
+
+// One cluster of CN 1024-thread CTAs per system (k_pcg_small<..., CN>): can the GPU co-schedule it?
+template <int CN>
+int cluster_fits_t(int* nclusters) {
+  auto kern = k_pcg_small<SG_PRECOND_LEARNED, 2, 5, CN>;
+  if (CN > 8) SG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t c = {};
+  c.gridDim = dim3(CN);
+  c.blockDim = dim3(kSmallThreads);
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CN;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  c.attrs = at;
+  c.numAttrs = 1;
+  SG_CUDA(cudaOccupancyMaxActiveClusters(nclusters, kern, &c));
+  return SG_OK;
+}
+int cluster_fits(int cn, int* nclusters) {
+  switch (cn) {
+    case 2: return cluster_fits_t<2>(nclusters);
+    case 4: return cluster_fits_t<4>(nclusters);
+    case 8: return cluster_fits_t<8>(nclusters);
+    default: return cluster_fits_t<16>(nclusters);
+  }
+}
+
+template <int PRE, int FMT, int ND, int CN>
+int launch_cluster(sg_pcg* h, int chunk, long long period, cudaStream_t s) {
+  auto kern = k_pcg_small<PRE, FMT, ND, CN>;
+  if (CN > 8) SG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t c = {};
+  c.gridDim = dim3((unsigned)(h->S * CN));
+  c.blockDim = dim3(kSmallThreads);
+  c.dynamicSmemBytes = 0;
+  c.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CN;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  c.attrs = at;
+  c.numAttrs = 1;
+  SG_CUDA(cudaLaunchKernelEx(&c, kern, h->D, chunk, period));
   return SG_OK;
 }
 
@@ -2888,7 +2988,21 @@ extern "C" int sg_pcg_create(sg_pcg** out, int32_t n_systems, const int64_t* sys
     const char* sv2 = getenv("SG_PCG_SMALL");
     long long maxrows = 0;
     for (int k = 0; k < n_systems; ++k) maxrows = std::max<long long>(maxrows, h->sys_start[k + 1] - h->sys_start[k]);
-    h->small = !(sv2 && sv2[0] == '0') && maxrows <= kSmallRows ? 1 : 0;
+    const bool sm_on = !(sv2 && sv2[0] == '0');
+    h->small = sm_on && maxrows <= kSmallRows ? 1 : 0;
+    h->scn = 1;
+    const char* cv = getenv("SG_PCG_CLUSTER");
+    if (sm_on && !h->small && maxrows <= kClusterRows && !(cv && cv[0] == '0')) {
+      // mid-size systems: one thread-block cluster per system, ~2048 rows per CTA
+      int cn = 2;
+      while (cn < 16 && (long long)cn * 2048 < maxrows) cn *= 2;
+      for (; cn >= 2; cn /= 2) {
+        int nclu = 0;
+        if (cluster_fits(cn, &nclu) == SG_OK && nclu > 0) break;
+      }
+      if (cn >= 2) { h->small = 1; h->scn = cn; }
+      cudaGetLastError();
+    }
     const char* xv = getenv("SG_PCG_XDEFER");
     h->D.xdefer = (xv && xv[0] == '1') && h->k1sw && h->k23 == 1 && !h->strip &&
                   h->pre == SG_PRECOND_LEARNED ? 1 : 0;
@@ -3061,7 +3175,18 @@ extern "C" int sg_pcg_solve(sg_pcg* h, const double* b, double* x, const sg_solv
         constexpr int FMT = decltype(Fc)::value;
         constexpr int ND = decltype(Nc)::value;
         if constexpr (FMT >= 1) {
-          k_pcg_small<PRE, FMT, ND><<<(unsigned)h->S, kSmallThreads, 0, s>>>(h->D, chunk, period);
+          if (h->scn <= 1) {
+            k_pcg_small<PRE, FMT, ND><<<(unsigned)h->S, kSmallThreads, 0, s>>>(h->D, chunk, period);
+          } else {
+            int lrc = SG_OK;
+            switch (h->scn) {
+              case 2: lrc = launch_cluster<PRE, FMT, ND, 2>(h, chunk, period, s); break;
+              case 4: lrc = launch_cluster<PRE, FMT, ND, 4>(h, chunk, period, s); break;
+              case 8: lrc = launch_cluster<PRE, FMT, ND, 8>(h, chunk, period, s); break;
+              default: lrc = launch_cluster<PRE, FMT, ND, 16>(h, chunk, period, s); break;
+            }
+            if (lrc) return lrc;
+          }
           SG_LAUNCH_CHECK("k_pcg_small");
         }
         return SG_OK;

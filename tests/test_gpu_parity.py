@@ -594,12 +594,14 @@ def test_batch_mixed_grids_unaligned_systems(multi_kernel):
         assert np.linalg.norm(b - O.spmv(o, c, v, rb.x)) / np.linalg.norm(b) <= 1.01e-8
 
 
-@pytest.mark.parametrize("small,grid", [("0", (24, 24)), ("1", (24, 24)), ("0", (528, 10))])
+@pytest.mark.parametrize("small,grid", [("0", (24, 24)), ("1", (24, 24)), ("1", (64, 64)), ("1", (96, 96)),
+                                        ("0", (528, 10))])
 def test_pcg_control_flow_on_sliding_window_kernels(small, grid, monkeypatch):
     """The reference control-flow variants (refresh period, delta termination + certification,
     max_iters, zero rhs, non-learned preconditioners) on a 5-point grid, i.e. through the
     sliding-window K1 / fused K2+K3 kernels rather than the CSR ones the golden cases use
-    (small="1": the same cases through the one-CTA-per-system solver, k_pcg_small; a 528-wide
+    (small="1": the same cases through the one-CTA-per-system solver, k_pcg_small, and -- 64^2
+    and 96^2 grids -- its thread-block-cluster form (2 and 8 CTAs per system); a 528-wide
     grid: through the 2-D strip kernels, three strips with a partial last one)."""
     import os
     import paper_2510_27517_b200.pcg as PC
