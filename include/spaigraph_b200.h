@@ -285,6 +285,13 @@ int sg_pcg_set_stencil(sg_pcg* h, const double* coeff, int64_t nx, int64_t ny, i
  * handle whose pattern changed fails with SG_EINVAL instead. */
 int sg_pcg_rebuilds(sg_pcg* h, int64_t* rebuilds_host);
 
+/* Device time (ns) the last sg_pcg_solve spent in the preconditioner apply when the handle runs
+ * whole iterations in one launch (systems of <= 32768 rows: one CTA or one thread-block cluster
+ * per system; %globaltimer around the apply phase, summed over systems); 0 on the multi-kernel
+ * path, whose apply share comes from the in-graph event samples of sg_pcg_stats.  Replaces the
+ * reference's t_apply accumulation (pcg.py:155-229) for that path. */
+int sg_pcg_apply_ns(sg_pcg* h, int64_t* ns_host);
+
 int sg_pcg_set_profile(sg_pcg* h, int32_t on);
 int sg_pcg_stats(sg_pcg* h, int64_t* kernels_host, int64_t* chunks_host, double* prof_host,
                  int32_t reset);

@@ -72,6 +72,7 @@ SIGNATURES = {
     "sg_pcg_rebind": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "sg_pcg_set_profile": (C.c_int, [vp, i32]),
     "sg_pcg_rebuilds": (C.c_int, [vp, C.POINTER(C.c_int64)]),
+    "sg_pcg_apply_ns": (C.c_int, [vp, C.POINTER(C.c_int64)]),
     "sg_pcg_set_stencil": (C.c_int, [vp, vp, i64, i64, C.POINTER(C.c_int32)]),
     "sg_pcg_stats": (C.c_int, [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64), vp, i32]),
     "sg_sai_loss": (C.c_int, [i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, f64, vp,

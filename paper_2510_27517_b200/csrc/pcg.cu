@@ -66,6 +66,7 @@ struct Ctl {
   int track, delta_mode;
   unsigned int n_active;
   unsigned int snap;   // n_active seen right before the profiled iteration of a chunk
+  unsigned long long apply_ns;  // one-CTA / cluster solver: device time of the applies (%globaltimer)
 };
 
 struct Dia {
@@ -1211,7 +1212,10 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_pcg_small(Dev D, int iters
     const double rr = sm_sum<CN>(prn, red, slots, seq);
     if (lead) fin_rr(D, sys, rr);
     sm_sync<CN>();
-    // K3: s = M r (learned: t = G^T r, then s = G t + eps r); r.s
+    // K3: s = M r (learned: t = G^T r, then s = G t + eps r); r.s -- the preconditioner apply,
+    // timed by the lead thread between the phase barriers (the reference's t_apply)
+    unsigned long long ta = 0;
+    if (lead) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ta));
     if (PRE == SG_PRECOND_LEARNED) {
       for (long long i = s0 + tid; i < s1; i += NT)
         D.t[i] = dia_row_t_seq<ND, 0>(D.dia, D.dia.gv, (int)i, D.dia.mask[i], XF{r, nullptr, 0.0});
@@ -1228,7 +1232,12 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_pcg_small(Dev D, int iters
       prs += mul(r[i], si);
     }
     const double rs = sm_sum<CN>(prs, red, slots, seq);
-    if (lead) fin_k3(D, sys, rs, refresh ? 1 : 0);
+    if (lead) {
+      unsigned long long tb;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tb));
+      atomicAdd(&D.ctl->apply_ns, tb - ta);
+      fin_k3(D, sys, rs, refresh ? 1 : 0);
+    }
     sm_sync<CN>();
   }
 }
@@ -3327,6 +3336,16 @@ extern "C" int sg_pcg_set_stencil(sg_pcg* h, const double* coeff, int64_t nx, in
   h->D.ihy2 = ihy2;
   h->cst = 0;  // verified against A at every solve
   if (usable_host) *usable_host = 1;
+  return SG_OK;
+}
+
+extern "C" int sg_pcg_apply_ns(sg_pcg* h, int64_t* ns_host) {
+  if (!h || !ns_host) { set_error("null handle"); return SG_EINVAL; }
+  *ns_host = 0;
+  if (!h->small) return SG_OK;
+  unsigned long long v = 0;
+  SG_CUDA(cudaMemcpy(&v, &h->ctl->apply_ns, sizeof(v), cudaMemcpyDeviceToHost));
+  *ns_host = (int64_t)v;
   return SG_OK;
 }
 

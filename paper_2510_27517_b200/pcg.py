@@ -143,6 +143,13 @@ class PcgHandle:
             self._prof_last = [0.0] * 8
         return int(k.value), int(c.value), list(prof)
 
+    def apply_ns(self) -> int:
+        """Apply time of the last solve measured inside the one-launch (one-CTA / cluster) solver
+        (sg_pcg_apply_ns); 0 on the multi-kernel path."""
+        r = C.c_int64(0)
+        L.check(L.lib().sg_pcg_apply_ns(self._h, C.byref(r)))
+        return int(r.value)
+
     def rebuilds(self) -> int:
         """How many times a solve found the patterns behind the handle's pointers changed and
         re-planned the handle (sg_pcg_rebuilds)."""
@@ -244,7 +251,11 @@ def _fused_apply_ns(h: PcgHandle, kind_name: str, k: int) -> int:
     alone for Jacobi / identity), sampled by the handle's in-graph event nodes on one iteration
     per graph chunk and scaled to the 1 + k applies the reference times (pcg.py:166-195).  The
     whole-iteration kernels include the r / x updates fused with the apply, so this is an upper
-    bound; one-CTA small systems (no per-kernel events) report 0."""
+    bound.  Systems solved in one launch (one CTA or one cluster per system) time the apply phase
+    on the device instead (%globaltimer, k applies, scaled to 1 + k)."""
+    direct = h.apply_ns()
+    if direct > 0:
+        return int(direct * (1 + k) / max(k, 1))
     _, _, prof = h.stats()
     last = getattr(h, "_prof_last", [0.0] * 8)
     h._prof_last = prof

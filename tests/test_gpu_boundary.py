@@ -137,13 +137,15 @@ def test_generic_path_not_spd_and_dimension_errors():
         P.pcg_solve(laplacian5(3, 3), np.ones(9), CountingIdentity(8))
 
 
-def test_fused_learned_reports_apply_time():
+@pytest.mark.parametrize("nx", [40, 96, 200])
+def test_fused_learned_reports_apply_time(nx):
+    """t_apply of the fused learned apply: timed inside the one-launch solvers (40^2: one CTA,
+    96^2: a cluster) and from the in-graph event samples on the multi-kernel path (200^2)."""
     m = P.load_checkpoint(CKPT)
-    A, meta = P.gen_poisson2d(96, 96, coeff_seed=4)  # > 3072 rows: the multi-kernel (evented) path
+    A, meta = P.gen_poisson2d(nx, nx, coeff_seed=4)
     G = P.forward(m, P.build_graph(A, meta)).G
     rep = P.pcg_solve(A, P.gen_rhs(meta, 9), P.build_learned_spai(G, m.config.epsilon), P.SolveConfig(rtol=1e-8))
     assert rep.converged and rep.t_apply_total_ns > 0 and rep.t_cg_total_ns > 0
-    assert rep.t_apply_total_ns < rep.t_apply_total_ns + rep.t_cg_total_ns
 
 
 # --------------------------------------------------------------------------- stale handle re-plan
