@@ -305,10 +305,10 @@ __device__ __forceinline__ double gather_partials(const Dev& D, int sys, int whi
   return gather_partials(D, D.sys_blk0, sys, which, red);
 }
 
-__device__ __forceinline__ void finish(const Dev& D, SysState& S, int conv) {
+__device__ __forceinline__ void finish(const Dev& D, SysState& S, int conv, bool pri = true) {
   S.converged = conv;
   S.status = ST_DONE;
-  atomicSub(&D.ctl->n_active, 1u);
+  if (pri) atomicSub(&D.ctl->n_active, 1u);  // pri: the one copy of a replicated state that reports
 }
 
 // Owned-row window and s-push targets of one partition (whole system when not partitioned).
@@ -353,7 +353,8 @@ __device__ __forceinline__ void st_release_sys(unsigned int* p, unsigned int v) 
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-__device__ __forceinline__ void put_hist(const Dev& D, int sys, long long i, double v) {
+__device__ __forceinline__ void put_hist(const Dev& D, int sys, long long i, double v, bool pri = true) {
+  if (!pri) return;
   const Ctl& c = *D.ctl;
   if (c.track && i < c.hcap) c.hist[(long long)sys * c.hcap + i] = v;
 }
@@ -397,29 +398,33 @@ __device__ void fin_setup2(const Dev& D, int sys, double rs) {
   }
 }
 
-__device__ void fin_k1(const Dev& D, int sys, bool run, double dq, double rrf) {
-  SysState& S = D.st[sys];
+// The finalisers act on a SysState reference: the system's state in global memory (the
+// multi-kernel and one-CTA paths) or a shared-memory copy (k_pcg_smem).
+__device__ void fin_k1_s(const Dev& D, SysState& S, int sys, bool run, double dq, double rrf, bool pri = true) {
   D.counter[sys] = 0;
   const Ctl& c = *D.ctl;
   if (!run) {  // delta-test certification (pcg.py:217-220)
     const double rel = __ddiv_rn(__dsqrt_rn(rrf), S.norm_b);
-    finish(D, S, rel <= c.rtol);
+    finish(D, S, rel <= c.rtol, pri);
     return;
   }
   if (S.flags & FL_FRESH) {  // pcg.py:208-215
     S.flags &= ~FL_FRESH;
     const double rel = __ddiv_rn(__dsqrt_rn(rrf), S.norm_b);
-    put_hist(D, sys, S.i, rel);
-    if (rel <= c.rtol) { finish(D, S, 1); return; }
-    if (S.i >= S.max_iters) { finish(D, S, 0); return; }
+    put_hist(D, sys, S.i, rel, pri);
+    if (rel <= c.rtol) { finish(D, S, 1, pri); return; }
+    if (S.i >= S.max_iters) { finish(D, S, 0, pri); return; }
   }
   if (dq <= 0.0) {  // pcg.py:182-184
     S.notspd = 1; S.fail_iter = S.i; S.fail_value = dq; S.fail_kind = 1;
-    finish(D, S, 0);
+    finish(D, S, 0, pri);
     return;
   }
   S.dq = dq;
   S.alpha = __ddiv_rn(S.delta, dq);
+}
+__device__ void fin_k1(const Dev& D, int sys, bool run, double dq, double rrf) {
+  fin_k1_s(D, D.st[sys], sys, run, dq, rrf);
 }
 
 __device__ void fin_rr(const Dev& D, int sys, double rr) {
@@ -427,32 +432,34 @@ __device__ void fin_rr(const Dev& D, int sys, double rr) {
   D.counter[sys] = 0;
 }
 
-__device__ void fin_k3(const Dev& D, int sys, double rs, int refreshed) {
-  SysState& S = D.st[sys];
+__device__ void fin_k3_s(const Dev& D, SysState& S, int sys, double rs, int refreshed, bool pri = true) {
   D.counter[sys] = 0;
   const Ctl& c = *D.ctl;
   const double delta_old = S.delta;
   S.delta = rs;
   if (rs < 0.0) {  // pcg.py:196-198
     S.notspd = 1; S.fail_iter = S.i; S.fail_value = rs; S.fail_kind = 2;
-    finish(D, S, 0);
+    finish(D, S, 0, pri);
     return;
   }
   S.beta = __ddiv_rn(rs, delta_old);
   S.i += 1;
   const double rel = __ddiv_rn(__dsqrt_rn(S.rr), S.norm_b);
-  put_hist(D, sys, S.i, rel);
+  put_hist(D, sys, S.i, rel, pri);
   S.hist_len = S.i + 1;
   if (!c.delta_mode) {
     if (rel <= c.rtol) {
-      if (refreshed) { finish(D, S, 1); return; }
+      if (refreshed) { finish(D, S, 1, pri); return; }
       S.flags |= FL_FRESH;
     } else if (S.i >= S.max_iters) {
-      finish(D, S, 0);
+      finish(D, S, 0, pri);
     }
   } else if (S.i >= S.max_iters || rs <= S.rtol2d0) {
     S.status = ST_CERTIFY;
   }
+}
+__device__ void fin_k3(const Dev& D, int sys, double rs, int refreshed) {
+  fin_k3_s(D, D.st[sys], sys, rs, refreshed);
 }
 
 // ------------------------------------------------------------------ partition reductions
@@ -1240,6 +1247,300 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_pcg_small(Dev D, int iters
     }
     sm_sync<CN>();
   }
+}
+
+// ------------------------------------------------------------------ small systems, shared-memory resident
+// The same iteration as k_pcg_small with the whole system held in shared memory: a cluster of CN
+// CTAs (CN = 1 .. 16) splits the system into CN blocks of R consecutive rows; each CTA keeps its
+// rows of x, r, d, q, s, t, b, its mask bytes, and A's / G's diagonals on its rows +- H (the
+// mirror entries of the neighbour rows), loaded once per launch and written back at its end.  A
+// neighbour row of another CTA is read from that CTA's shared memory through DSMEM
+// (ld.shared::cluster; H <= R, so only ranks +-1).  Fewer barriers per iteration than the
+// global-memory loop: d' = s + beta d and r' = r - alpha q of NEIGHBOUR rows are recomputed where
+// q = A d' and t = G^T r' need them (bitwise the stored values), the own rows' d', r' wait in
+// registers until the next barrier; the dot products are cluster all-reduces (every rank adds
+// the ranks' block sums in rank order: identical values everywhere), so every CTA runs the
+// finalisers on its own copy of the system state and only rank 0 reports (history, active
+// count).  Three cluster barriers per iteration (five on refresh iterations).  Roundings,
+// summation orders and finalisers are k_pcg_small's.
+struct SmemSys {
+  double *x, *r, *d, *q, *s, *t, *b;  // [R] own rows
+  double* ae;                         // [NA][R + 2H] A's diagonals, rows a0 - H ..
+  double* ge;                         // [ND][R + 2H] G's diagonals
+  unsigned char* mk;                  // [R]
+};
+
+__host__ __device__ constexpr size_t smem_sys_bytes(int R, int H, int NA, int ND) {
+  return ((size_t)7 * R + (size_t)(NA + ND) * (R + 2 * H)) * 8 + (size_t)(R + 15) / 16 * 16;
+}
+
+__device__ __forceinline__ double ld_peer(const double* local, int rank) {
+  uint32_t a;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(smem_u32(local)), "r"(rank));
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+  return v;
+}
+
+// Vector value at system row j (0 outside the system: such entries are masked out anyway).
+template <int CN>
+__device__ __forceinline__ double vsm(const double* v, long long j, long long s0, long long s1, long long a0, int R,
+                                      int rank) {
+  if (j < s0 || j >= s1) return 0.0;
+  const int li = (int)(j - a0);
+  if (CN > 1 && li < 0) return ld_peer(v + li + R, rank - 1);
+  if (CN > 1 && li >= R) return ld_peer(v + li - R, rank + 1);
+  return v[li];
+}
+
+// Two dot products at once: block trees per CTA, then (CN > 1) every rank's thread 0 stores its
+// block sums into every rank's slots and, after the cluster barrier, adds them in rank order.
+// Valid in thread 0 of every CTA.  slots: __shared__ [2 parities][2][16].
+template <int CN>
+__device__ __forceinline__ void sm_allreduce2(double a, double b, double* red, double* slots_all, int& seq, double& ra,
+                                              double& rb) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  a = warp_sum(a);
+  b = warp_sum(b);
+  __syncthreads();
+  if (lane == 0) { red[wid] = a; red[32 + wid] = b; }
+  __syncthreads();
+  const int nw = (blockDim.x + 31) >> 5;
+  double xa = 0.0, xb = 0.0;
+  if (wid == 0) {
+    xa = warp_sum(lane < nw ? red[lane] : 0.0);
+    xb = warp_sum(lane < nw ? red[32 + lane] : 0.0);
+  }
+  if constexpr (CN == 1) {
+    ra = xa;
+    rb = xb;
+  } else {
+    double* slots = slots_all + 32 * (seq++ & 1);
+    const int rank = (int)cluster_rank();
+    if (threadIdx.x == 0)
+      for (int k = 0; k < CN; ++k) {
+        uint32_t pa, pb;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(pa) : "r"(smem_u32(slots + rank)), "r"(k));
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(pb) : "r"(smem_u32(slots + 16 + rank)), "r"(k));
+        asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(pa), "d"(xa) : "memory");
+        asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(pb), "d"(xb) : "memory");
+      }
+    sm_sync<CN>();
+    ra = 0.0;
+    rb = 0.0;
+    if (threadIdx.x == 0)
+      for (int k = 0; k < CN; ++k) { ra += slots[k]; rb += slots[16 + k]; }
+  }
+}
+
+template <int PRE, int FMT, int ND, int CN>
+__global__ void __launch_bounds__(kSmallThreads, 1) k_pcg_smem(Dev D, int iters, long long period, int R) {
+  constexpr int NA = FMT == 2 ? ND / 2 + 1 : ND;
+  constexpr int RPT = 2;  // R <= 2 * kSmallThreads
+  extern __shared__ __align__(16) unsigned char smraw[];
+  __shared__ double red[64];
+  __shared__ double slots[64];
+  __shared__ __align__(16) SysState SS;  // this CTA's copy of the system state
+  int seq = 0;
+  const int rank = CN == 1 ? 0 : (int)cluster_rank();
+  const int sys = blockIdx.x / CN, tid = threadIdx.x;
+  const bool pri = rank == 0;
+  const long long s0 = D.blk_r0[D.sys_blk0[sys]], s1 = D.sys_r1[sys];
+  const int H = D.dia.halo, RE = R + 2 * H;
+  const long long a0 = s0 + (long long)rank * R;
+  const int Rown = (int)(a0 >= s1 ? 0 : (s1 - a0 < R ? s1 - a0 : R));
+  const double eps = D.ctl->eps;
+  SmemSys M;
+  {
+    double* p = reinterpret_cast<double*>(smraw);
+    M.x = p; M.r = p + R; M.d = p + 2 * R; M.q = p + 3 * R; M.s = p + 4 * R; M.t = p + 5 * R; M.b = p + 6 * R;
+    M.ae = p + 7 * R;
+    M.ge = M.ae + NA * RE;
+    M.mk = reinterpret_cast<unsigned char*>(M.ge + ND * RE);
+  }
+  int off[ND], mir[ND];
+#pragma unroll
+  for (int dg = 0; dg < ND; ++dg) { off[dg] = D.dia.off[dg]; mir[dg] = D.dia.mir[dg]; }
+  // load: own rows of the vectors, the diagonals on rows a0 - H .. a0 + R + H (zero outside)
+  for (int li = tid; li < R; li += kSmallThreads) {
+    const bool in = li < Rown;
+    const long long i = a0 + li;
+    M.x[li] = in ? D.x[i] : 0.0;
+    M.r[li] = in ? D.r0[i] : 0.0;
+    M.d[li] = in ? D.d0[i] : 0.0;
+    M.s[li] = in ? D.s[i] : 0.0;
+    M.b[li] = in ? D.b[i] : 0.0;
+    M.q[li] = 0.0;
+    M.t[li] = 0.0;
+    M.mk[li] = in ? D.dia.mask[i] : (unsigned char)0;
+  }
+  for (int e = tid; e < RE; e += kSmallThreads) {
+    const long long i = a0 - H + e;
+    const bool in = i >= s0 && i < s1;
+#pragma unroll
+    for (int dg = 0; dg < NA; ++dg) M.ae[dg * RE + e] = in ? D.dia.av[dg][i] : 0.0;
+    if (PRE == SG_PRECOND_LEARNED)
+#pragma unroll
+      for (int dg = 0; dg < ND; ++dg) M.ge[dg * RE + e] = in ? D.dia.gv[dg][i] : 0.0;
+  }
+  if (tid == 0) SS = D.st[sys];
+  sm_sync<CN>();
+  auto Aval = [&](int li, int dg) {
+    const int e = li + H;
+    return (FMT == 2 && off[dg] > 0) ? M.ae[mir[dg] * RE + e + off[dg]] : M.ae[dg * RE + e];
+  };
+  auto V = [&](const double* v, long long j) { return vsm<CN>(v, j, s0, s1, a0, R, rank); };
+  // b - A x (x of the neighbours as stored)
+  auto resid = [&](int li) {
+    const long long j = a0 + li;
+    double p[ND];
+#pragma unroll
+    for (int dg = 0; dg < ND; ++dg) p[dg] = mul(Aval(li, dg), V(M.x, j + off[dg]));
+    return sub(M.b[li], combine_numpy<ND>(p, M.mk[li]));
+  };
+  for (int c = 0; c < iters; ++c) {
+    const int status = SS.status;
+    if (status == ST_DONE) break;
+    const bool run = status == ST_RUN;
+    const bool fresh = run ? (SS.flags & FL_FRESH) != 0 : true;
+    const bool refresh = run && SS.i > 0 && SS.i % period == 0;
+    const double beta = SS.beta;
+    // K1: q = A d' with d' = s + beta d recomputed for the neighbour rows; fresh residual
+    double pdq = 0.0, prr = 0.0, dn[RPT];
+#pragma unroll
+    for (int h = 0; h < RPT; ++h) {
+      const int li = tid + h * kSmallThreads;
+      dn[h] = 0.0;
+      if (li < Rown) {
+        const long long j = a0 + li;
+        if (run) {
+          double p[ND];
+#pragma unroll
+          for (int dg = 0; dg < ND; ++dg) {
+            const long long jj = j + off[dg];
+            const double dj = add(V(M.s, jj), mul(beta, V(M.d, jj)));
+            p[dg] = mul(Aval(li, dg), dj);
+          }
+          const double qi = combine_numpy<ND>(p, M.mk[li]);
+          dn[h] = add(M.s[li], mul(beta, M.d[li]));
+          M.q[li] = qi;
+          pdq += mul(dn[h], qi);
+        }
+        if (fresh) {
+          const double rf = resid(li);
+          if (run) M.r[li] = rf;
+          prr += mul(rf, rf);
+        }
+      }
+    }
+    double dq, rrf;
+    sm_allreduce2<CN>(pdq, prr, red, slots, seq, dq, rrf);  // cluster barrier: every d read is done
+    if (run)
+#pragma unroll
+      for (int h = 0; h < RPT; ++h)
+        if (tid + h * kSmallThreads < Rown) M.d[tid + h * kSmallThreads] = dn[h];
+    if (tid == 0) fin_k1_s(D, SS, sys, run, dq, rrf, pri);
+    __syncthreads();
+    if (SS.status != ST_RUN) continue;
+    const double alpha = SS.alpha;
+    unsigned long long ta = 0;
+    if (tid == 0 && pri) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ta));
+    double prn = 0.0;
+    if (!refresh) {
+      // x += alpha d'; r' = r - alpha q (own rows in registers); t = G^T r' with the neighbours'
+      // r' recomputed from their r and q (q of every row is final since the all-reduce barrier)
+      double rn[RPT];
+#pragma unroll
+      for (int h = 0; h < RPT; ++h) {
+        const int li = tid + h * kSmallThreads;
+        rn[h] = 0.0;
+        if (li < Rown) {
+          const long long j = a0 + li;
+          M.x[li] = add(M.x[li], mul(alpha, M.d[li]));
+          rn[h] = sub(M.r[li], mul(alpha, M.q[li]));
+          prn += mul(rn[h], rn[h]);
+          if (PRE == SG_PRECOND_LEARNED) {
+            const int e = li + H;
+            double p[ND];
+#pragma unroll
+            for (int dg = 0; dg < ND; ++dg) {
+              const long long jj = j + off[dg];
+              const double rj = sub(V(M.r, jj), mul(alpha, V(M.q, jj)));
+              p[dg] = mul(M.ge[mir[dg] * RE + e + off[dg]], rj);
+            }
+            M.t[li] = combine_seq<ND>(p, M.mk[li]);
+          }
+        }
+      }
+      sm_sync<CN>();  // every r and t read / write of the phase is done
+#pragma unroll
+      for (int h = 0; h < RPT; ++h)
+        if (tid + h * kSmallThreads < Rown) M.r[tid + h * kSmallThreads] = rn[h];
+      if (PRE != SG_PRECOND_LEARNED) __syncthreads();
+    } else {
+      // refresh iteration (every `period`): r = b - A x needs the neighbours' new x first
+      for (int li = tid; li < Rown; li += kSmallThreads) M.x[li] = add(M.x[li], mul(alpha, M.d[li]));
+      sm_sync<CN>();
+      for (int li = tid; li < Rown; li += kSmallThreads) {
+        const double rv = resid(li);
+        M.r[li] = rv;
+        prn += mul(rv, rv);
+      }
+      sm_sync<CN>();
+      if (PRE == SG_PRECOND_LEARNED) {
+        for (int li = tid; li < Rown; li += kSmallThreads) {
+          const long long j = a0 + li;
+          const int e = li + H;
+          double p[ND];
+#pragma unroll
+          for (int dg = 0; dg < ND; ++dg) p[dg] = mul(M.ge[mir[dg] * RE + e + off[dg]], V(M.r, j + off[dg]));
+          M.t[li] = combine_seq<ND>(p, M.mk[li]);
+        }
+        sm_sync<CN>();
+      }
+    }
+    // K3: s = M r' (learned: s = G t + eps r'); r'.s
+    double prs = 0.0;
+    for (int li = tid; li < Rown; li += kSmallThreads) {
+      double si;
+      if (PRE == SG_PRECOND_IDENTITY) si = M.r[li];
+      else if (PRE == SG_PRECOND_JACOBI) si = mul(M.r[li], D.inv_diag[a0 + li]);
+      else {
+        const long long j = a0 + li;
+        const int e = li + H;
+        double p[ND];
+#pragma unroll
+        for (int dg = 0; dg < ND; ++dg) p[dg] = mul(M.ge[dg * RE + e], V(M.t, j + off[dg]));
+        si = add(combine_numpy<ND>(p, M.mk[li]), mul(eps, M.r[li]));
+      }
+      M.s[li] = si;
+      prs += mul(M.r[li], si);
+    }
+    double rr, rs;
+    sm_allreduce2<CN>(prn, prs, red, slots, seq, rr, rs);
+    if (tid == 0) {
+      if (pri) {
+        unsigned long long tb;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tb));
+        atomicAdd(&D.ctl->apply_ns, tb - ta);
+      }
+      SS.rr = rr;
+      fin_k3_s(D, SS, sys, rs, refresh ? 1 : 0, pri);
+    }
+    __syncthreads();
+  }
+  // write back the state the next launch (and the caller) reads
+  if (tid == 0 && pri) D.st[sys] = SS;
+  for (int li = tid; li < Rown; li += kSmallThreads) {
+    const long long i = a0 + li;
+    D.x[i] = M.x[li];
+    D.r0[i] = M.r[li];
+    D.d0[i] = M.d[li];
+    D.s[i] = M.s[li];
+    D.q[i] = M.q[li];
+    D.t[i] = M.t[li];
+  }
+  sm_sync<CN>();  // no CTA leaves while a peer may still read its shared memory
 }
 
 // ------------------------------------------------------------------ halo-staged DIA kernels
@@ -2264,6 +2565,8 @@ struct sg_pcg {
   int g_warp = 0;     // CSR G with long rows: K3 one warp per row (k_iter3_wr)
   int small = 0;      // DIA systems of <= kSmallRows rows: one CTA per system (k_pcg_small)
   int scn = 1;        // ... of <= kClusterRows rows: one cluster of scn CTAs per system
+  int smem_cn = 0;    // > 0: the shared-memory resident solver (k_pcg_smem), smem_cn CTAs of
+  int smem_R = 0;     //      smem_R rows per system
   int k23 = 1;        // fused K2+K3 variant: 1 = sliding window (k_iter23_sw), 0 = tiles (k_iter23_st)
   void* sell_mem[3] = {nullptr, nullptr, nullptr};   // SELL-32 patterns of A, G, G^T
   void* sell_vals[3] = {nullptr, nullptr, nullptr};
@@ -2654,6 +2957,66 @@ int launch_cluster(sg_pcg* h, int chunk, long long period, cudaStream_t s) {
   return SG_OK;
 }
 
+constexpr size_t kSmemSysMax = 227 * 1024 - 4096;  // dynamic shared memory of one k_pcg_smem CTA (+ its static)
+
+template <int CN>
+int smem_fits_t(size_t bytes, int* nclusters) {
+  auto kern = k_pcg_smem<SG_PRECOND_LEARNED, 1, 8, CN>;
+  SG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemSysMax));
+  if (CN > 8) SG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  if (CN == 1) {
+    int nb = 0;
+    SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kSmallThreads, bytes));
+    *nclusters = nb;
+    return SG_OK;
+  }
+  cudaLaunchConfig_t c = {};
+  c.gridDim = dim3(CN);
+  c.blockDim = dim3(kSmallThreads);
+  c.dynamicSmemBytes = bytes;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CN;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  c.attrs = at;
+  c.numAttrs = 1;
+  SG_CUDA(cudaOccupancyMaxActiveClusters(nclusters, kern, &c));
+  return SG_OK;
+}
+int smem_fits(int cn, size_t bytes, int* nclusters) {
+  switch (cn) {
+    case 1: return smem_fits_t<1>(bytes, nclusters);
+    case 2: return smem_fits_t<2>(bytes, nclusters);
+    case 4: return smem_fits_t<4>(bytes, nclusters);
+    case 8: return smem_fits_t<8>(bytes, nclusters);
+    default: return smem_fits_t<16>(bytes, nclusters);
+  }
+}
+
+template <int PRE, int FMT, int ND, int CN>
+int launch_smem(sg_pcg* h, int chunk, long long period, cudaStream_t s) {
+  auto kern = k_pcg_smem<PRE, FMT, ND, CN>;
+  constexpr int NA = FMT == 2 ? ND / 2 + 1 : ND;
+  const size_t bytes = smem_sys_bytes(h->smem_R, h->D.dia.halo, NA, ND);
+  SG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  if (CN > 8) SG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t c = {};
+  c.gridDim = dim3((unsigned)(h->S * CN));
+  c.blockDim = dim3(kSmallThreads);
+  c.dynamicSmemBytes = bytes;
+  c.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CN;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  c.attrs = at;
+  c.numAttrs = CN > 1 ? 1 : 0;
+  SG_CUDA(cudaLaunchKernelEx(&c, kern, h->D, chunk, period, h->smem_R));
+  return SG_OK;
+}
+
 int strip_setup(int* per_sm) {
   SG_CUDA(cudaFuncSetAttribute(k_iter23_s5<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Strip23::SMEM));
   SG_CUDA(cudaFuncSetAttribute(k_iter23_s5<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Strip23::SMEM));
@@ -3000,8 +3363,28 @@ extern "C" int sg_pcg_create(sg_pcg** out, int32_t n_systems, const int64_t* sys
     const bool sm_on = !(sv2 && sv2[0] == '0');
     h->small = sm_on && maxrows <= kSmallRows ? 1 : 0;
     h->scn = 1;
+    h->smem_cn = 0;
+    const char* mv = getenv("SG_PCG_SMEM");
+    if (sm_on && !(mv && mv[0] == '0') && true) {
+      // the whole system in shared memory: the fewest CTAs that hold it with one row per thread,
+      // else with two
+      const int H = h->D.dia.halo, nd = h->dia_nd;
+      for (int pass = 0; pass < 2 && !h->smem_cn; ++pass)
+      for (int cn = 1; cn <= 16; cn *= 2) {
+        const int R = (int)((maxrows + cn - 1) / cn);
+        if (R > (pass + 1) * kSmallThreads || (cn > 1 && R < H)) continue;
+        const size_t bytes = smem_sys_bytes(R, H, nd, nd);
+        if (bytes > kSmemSysMax) continue;
+        int nclu = 1;
+        if (smem_fits(cn, bytes, &nclu) != SG_OK || nclu < 1) { cudaGetLastError(); continue; }
+        h->smem_cn = cn;
+        h->smem_R = R;
+        break;
+      }
+      if (h->smem_cn) h->small = 1;
+    }
     const char* cv = getenv("SG_PCG_CLUSTER");
-    if (sm_on && !h->small && maxrows <= kClusterRows && !(cv && cv[0] == '0')) {
+    if (sm_on && !h->small && !h->smem_cn && maxrows <= kClusterRows && !(cv && cv[0] == '0')) {
       // mid-size systems: one thread-block cluster per system, ~2048 rows per CTA
       int cn = 2;
       while (cn < 16 && (long long)cn * 2048 < maxrows) cn *= 2;
@@ -3184,7 +3567,17 @@ extern "C" int sg_pcg_solve(sg_pcg* h, const double* b, double* x, const sg_solv
         constexpr int FMT = decltype(Fc)::value;
         constexpr int ND = decltype(Nc)::value;
         if constexpr (FMT >= 1) {
-          if (h->scn <= 1) {
+          if (h->smem_cn) {
+            int lrc = SG_OK;
+            switch (h->smem_cn) {
+              case 1: lrc = launch_smem<PRE, FMT, ND, 1>(h, chunk, period, s); break;
+              case 2: lrc = launch_smem<PRE, FMT, ND, 2>(h, chunk, period, s); break;
+              case 4: lrc = launch_smem<PRE, FMT, ND, 4>(h, chunk, period, s); break;
+              case 8: lrc = launch_smem<PRE, FMT, ND, 8>(h, chunk, period, s); break;
+              default: lrc = launch_smem<PRE, FMT, ND, 16>(h, chunk, period, s); break;
+            }
+            if (lrc) return lrc;
+          } else if (h->scn <= 1) {
             k_pcg_small<PRE, FMT, ND><<<(unsigned)h->S, kSmallThreads, 0, s>>>(h->D, chunk, period);
           } else {
             int lrc = SG_OK;
