@@ -87,7 +87,15 @@ def config_block(a, world):
             "systems_per_gpu": a.systems_per_gpu, "global_systems": a.systems_per_gpu * world,
             "n_per_system": a.nx * a.nx, "nnz_per_system": 5 * a.nx * a.nx - 4 * a.nx,
             "parallelism": f"dp{world} (systems sharded by rank, no collective in the solve)",
-            "cache": "inputs larger than L2 (~1.7 GB working set per GPU vs 126 MB L2); no flush"}
+            "cache": cache_note(a)}
+
+
+def cache_note(a):
+    # PCG working set: A / G diagonals, mask, 9 vectors (~13 MB per 256^2 system)
+    ws = a.systems_per_gpu * a.nx * a.nx * 201 / 1e9
+    if ws > 2 * 0.126:
+        return f"inputs larger than L2 (~{ws:.2f} GB PCG working set per GPU vs 126 MB L2); no flush"
+    return f"PCG working set ~{ws:.3f} GB per GPU, NOT larger than 2x the 126 MB L2 and not flushed"
 
 
 class ClockSampler:
@@ -270,6 +278,7 @@ def run_ours(a, rank, world, local):
     from paper_2510_27517_b200.gnn import load_checkpoint
     from paper_2510_27517_b200.pcg import SolveConfig
 
+    local = local % max(1, torch.cuda.device_count())  # one rank per GPU (the gloo check may share one)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     _lib.lib()

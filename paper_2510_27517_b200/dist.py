@@ -27,7 +27,9 @@ def init_from_env(backend: str | None = None):
     if world > 1 and not dist.is_initialized():
         import torch
         if backend is None:
-            backend = "nccl" if torch.cuda.is_available() else "gloo"
+            # SG_DIST_BACKEND=gloo: the multi-process harness on fewer GPUs than ranks (a functional
+            # check of the N > 1 path; ranks share a device, so its timings mean nothing)
+            backend = os.environ.get("SG_DIST_BACKEND") or ("nccl" if torch.cuda.is_available() else "gloo")
         if backend == "nccl":
             torch.cuda.set_device(local)
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
@@ -43,11 +45,18 @@ def local_systems(n_per_rank: int, rank: int, world: int, base_seed: int = 0):
     return ids, [i + 10**6 for i in ids]
 
 
+def _coll_device(device):
+    """Collectives run on `device` under NCCL and on the host under gloo."""
+    import torch.distributed as dist
+    return None if dist.get_backend() == "gloo" else device
+
+
 def max_over_ranks(value: float, device=None) -> float:
     import torch
     import torch.distributed as dist
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
         return float(value)
+    device = _coll_device(device)
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
@@ -62,6 +71,7 @@ def gather_stats(ks, converged, device=None):
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
         return ks, cv
     world = dist.get_world_size()
+    device = _coll_device(device)
     local = torch.tensor(np.stack([ks, cv]), dtype=torch.int64, device=device)
     n = torch.tensor([local.shape[1]], dtype=torch.int64, device=device)
     sizes = [torch.zeros_like(n) for _ in range(world)]
