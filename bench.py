@@ -483,7 +483,9 @@ def run_c5(a, model, dev):
     return {"workload": "C5: 2D Poisson 2048x2048 (n=4,194,304, nnz 20,963,328), trained GNN-SPAI + PCG rtol 1e-6, "
                         "one system, 1 GPU (configs[4] at N=1; the row partition over 2/4/8 GPUs is separate)",
             "metric": METRIC, "value": 1000.0 / ms, "unit": "solves/s", "ms_per_solve": ms, "k": int(rep.k),
-            "pcg_us_per_iteration": rep.t_cg_total_ns / 1e3 / max(rep.k, 1),
+            "pcg_us_per_iteration": (rep.t_cg_total_ns + rep.t_apply_total_ns) / 1e3 / max(rep.k, 1),
+            "pcg_time_split_ns": {"t_cg_total_ns": int(rep.t_cg_total_ns), "t_apply_total_ns": int(rep.t_apply_total_ns),
+                                  "note": "reference split (pcg.py:155-229): t_cg excludes the preconditioner apply"},
             "parity": {"converged": bool(rep.converged), "true_relative_residual": rel, "rtol": rtol,
                        "oracle_tests": "tests/test_gpu_config_parity.py (G on sampled rows <= 1e-10, first 50 "
                                        "residuals <= 1e-9 vs the oracle replay)"},

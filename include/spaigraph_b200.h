@@ -85,6 +85,20 @@ int sg_pattern_is_symmetric(int64_t n, int64_t nnz, const int32_t* offs, const i
 int sg_pattern_square(int64_t n, const int32_t* offs, const int32_t* cols, int32_t* out_offs,
                       int32_t* out_cols, int64_t* out_nnz_host, void* ws, size_t* ws_bytes, void* stream);
 
+/* gen_synthetic (datasets.py:148-193): pattern of the Gram matrix P·Pᵀ + εI, P an n×m CSR
+ * matrix with sorted rows, Pᵀ its transpose (m rows).  Row i = {i} ∪ columns reached through
+ * P's row i; rows sorted.  Two calls like sg_pattern_square.  Rows with more than 2047
+ * candidates return SG_EUNSUPPORTED. */
+int sg_gram_pattern(int64_t n, const int32_t* p_offs, const int32_t* p_cols, const int32_t* pt_offs,
+                    const int32_t* pt_cols, int32_t* out_offs, int32_t* out_cols, int64_t* out_nnz_host, void* ws,
+                    size_t* ws_bytes, void* stream);
+
+/* Gram values on that pattern, the reference's accumulation order: A_ij = 0.0 + P_ic1·P_jc1 +
+ * P_ic2·P_jc2 + ... over shared columns c1 < c2 < ... (datasets.py:163-176), then + shift on the
+ * diagonal (datasets.py:177-178).  Bit-exact. */
+int sg_gram_values(int64_t n, const int32_t* p_offs, const int32_t* p_cols, const double* p_vals,
+                   const int32_t* a_offs, const int32_t* a_cols, double shift, double* a_vals, void* stream);
+
 /* A's values on a superset pattern P (explicit zeros elsewhere; explicit zeros are
  * pattern-significant, sparse.py:3-6).  SG_EINVAL if P does not contain pattern(A). */
 int sg_csr_pad_to_pattern(int64_t n, const int32_t* a_offs, const int32_t* a_cols, const double* a_vals,

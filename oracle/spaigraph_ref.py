@@ -328,6 +328,36 @@ def rand_spd_sparse(n, rng, extra_per_row=3):
                         np.array([entries[k] for k in keys]))
 
 
+SYNTHETIC_EPS = 1e-4  # datasets.py:42
+
+
+def gen_synthetic(n, density, seed):
+    """datasets.py:148-193: A = P·Pᵀ + εI.  Small cases only (dictionary accumulation per column
+    group in ascending column order, as the reference does)."""
+    rng = np.random.default_rng(seed)
+    nnz_p = int(round(density * n * n))
+    flat = rng.choice(n * n, size=nnz_p, replace=False)
+    pr, pc, pv = flat // n, flat % n, rng.standard_normal(nnz_p)
+    order = np.lexsort((pr, pc))
+    pr, pc, pv = pr[order], pc[order], pv[order]
+    acc = {}
+    start = 0
+    while start < nnz_p:
+        stop = start
+        while stop < nnz_p and pc[stop] == pc[start]:
+            stop += 1
+        for p in range(start, stop):
+            for q in range(start, stop):
+                key = (int(pr[p]), int(pr[q]))
+                acc[key] = acc.get(key, 0.0) + float(pv[p]) * float(pv[q])
+        start = stop
+    for i in range(n):
+        acc[(i, i)] = acc.get((i, i), 0.0) + SYNTHETIC_EPS
+    keys = sorted(acc)
+    return csr_from_coo(n, n, np.array([k[0] for k in keys], dtype=np.int64),
+                        np.array([k[1] for k in keys], dtype=np.int64), np.array([acc[k] for k in keys]))
+
+
 # ----------------------------------------------------------------------------------------------
 # L3 graph features  (graphfeat.py)
 # ----------------------------------------------------------------------------------------------

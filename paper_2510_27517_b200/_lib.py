@@ -41,6 +41,8 @@ SIGNATURES = {
     "sg_csr_transpose": (C.c_int, [i64, i64, i64, vp, vp, vp, vp, vp, vp, szp, vp]),
     "sg_pattern_is_symmetric": (C.c_int, [i64, i64, vp, vp, C.POINTER(C.c_int32), vp, szp, vp]),
     "sg_pattern_square": (C.c_int, [i64, vp, vp, vp, vp, C.POINTER(C.c_int64), vp, szp, vp]),
+    "sg_gram_pattern": (C.c_int, [i64, vp, vp, vp, vp, vp, vp, C.POINTER(C.c_int64), vp, szp, vp]),
+    "sg_gram_values": (C.c_int, [i64, vp, vp, vp, vp, vp, C.c_double, vp, vp]),
     "sg_csr_pad_to_pattern": (C.c_int, [i64, vp, vp, vp, vp, vp, vp, vp, szp, vp]),
     "sg_row_expand": (C.c_int, [i64, vp, vp, vp]),
     "sg_gather_f64": (C.c_int, [vp, vp, vp, i64, vp]),

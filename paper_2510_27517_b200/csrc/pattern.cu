@@ -201,15 +201,23 @@ __global__ void k_diagonal(int64_t n, const int32_t* __restrict__ offs,
 constexpr int SQ_CAP = 2048;
 constexpr int SQ_WARPS = 4;
 
+// Candidates of row i of X·Y (X rows give the k, Y rows the columns), plus i itself when
+// `diag` (the Gram matrix P·Pᵀ + εI always stores its diagonal), sorted in buf[0..m).
 __device__ int sq_gather_sort(int64_t i, const int32_t* __restrict__ offs, const int32_t* __restrict__ cols,
-                              int32_t* buf, unsigned int* overflow) {
+                              int32_t* buf, unsigned int* overflow, const int32_t* __restrict__ yoffs = nullptr,
+                              const int32_t* __restrict__ ycols = nullptr, bool diag = false) {
   const int lane = threadIdx.x & 31;
+  if (!yoffs) { yoffs = offs; ycols = cols; }
   int m = 0;
+  if (diag) {
+    if (lane == 0) buf[0] = (int32_t)i;
+    m = 1;
+  }
   for (int32_t a = offs[i]; a < offs[i + 1]; ++a) {
     const int32_t k = cols[a];
-    const int32_t lo = offs[k], len = offs[k + 1] - lo;
+    const int32_t lo = yoffs[k], len = yoffs[k + 1] - lo;
     if (m + len > SQ_CAP) { if (lane == 0) atomicOr(overflow, 1u); return -1; }
-    for (int t = lane; t < len; t += 32) buf[m + t] = cols[lo + t];
+    for (int t = lane; t < len; t += 32) buf[m + t] = ycols[lo + t];
     m += len;
   }
   int p2 = 1;
@@ -251,6 +259,67 @@ __global__ void __launch_bounds__(32 * SQ_WARPS) k_square_pattern(int64_t n, con
     }
     if (!out_cols && lane == 0) counts[i] = written;
     __syncwarp();
+  }
+}
+
+// Gram pattern of P·Pᵀ + εI (datasets.py:148-193, gen_synthetic): row i = {i} ∪ rows of Pᵀ over
+// the columns of P's row i.  Same warp gather / bitonic sort / distinct count as above.
+__global__ void __launch_bounds__(32 * SQ_WARPS) k_gram_pattern(int64_t n, const int32_t* __restrict__ p_offs,
+                                                               const int32_t* __restrict__ p_cols,
+                                                               const int32_t* __restrict__ pt_offs,
+                                                               const int32_t* __restrict__ pt_cols, int32_t* counts,
+                                                               const int32_t* __restrict__ out_offs,
+                                                               int32_t* out_cols, unsigned int* overflow) {
+  __shared__ int32_t sbuf[SQ_WARPS][SQ_CAP];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int32_t* buf = sbuf[w];
+  for (int64_t i = (int64_t)blockIdx.x * SQ_WARPS + w; i < n; i += (int64_t)gridDim.x * SQ_WARPS) {
+    const int m = sq_gather_sort(i, p_offs, p_cols, buf, overflow, pt_offs, pt_cols, true);
+    if (m < 0) continue;
+    int written = 0;
+    for (int base = 0; base < m; base += 32) {
+      const int t = base + lane;
+      const bool first = t < m && (t == 0 || buf[t] != buf[t - 1]);
+      const unsigned int bal = __ballot_sync(0xffffffffu, first);
+      if (out_cols && first) out_cols[out_offs[i] + written + __popc(bal & ((1u << lane) - 1))] = buf[t];
+      written += __popc(bal);
+    }
+    if (!out_cols && lane == 0) counts[i] = written;
+    __syncwarp();
+  }
+}
+
+// Gram values: A_ij = (sum over the columns c shared by P's rows i and j, ASCENDING c, of
+// P_ic·P_jc, added one at a time to 0.0) (+ eps when i == j) -- the reference's dictionary
+// accumulation visits P's column groups in ascending column order (lexsort by column, then
+// row), adds acc.get(key, 0.0) + v_p·v_q, and shifts the diagonal last.  A sequential merge of
+// the two sorted rows reproduces every rounding.  One warp per row, one lane per entry.
+__global__ void k_gram_values(int64_t n, const int32_t* __restrict__ p_offs, const int32_t* __restrict__ p_cols,
+                              const double* __restrict__ p_vals, const int32_t* __restrict__ a_offs,
+                              const int32_t* __restrict__ a_cols, double shift, double* __restrict__ a_vals) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += warps) {
+    const int32_t ib = p_offs[i], ie = p_offs[i + 1];
+    for (int32_t e = a_offs[i] + lane; e < a_offs[i + 1]; e += 32) {
+      const int32_t j = a_cols[e];
+      int32_t a = ib, b = p_offs[j];
+      const int32_t be = p_offs[j + 1];
+      double acc = 0.0;
+      while (a < ie && b < be) {
+        const int32_t ca = p_cols[a], cb = p_cols[b];
+        if (ca == cb) {
+          acc = __dadd_rn(acc, __dmul_rn(p_vals[a], p_vals[b]));
+          ++a; ++b;
+        } else if (ca < cb) {
+          ++a;
+        } else {
+          ++b;
+        }
+      }
+      if (j == (int32_t)i) acc = __dadd_rn(acc, shift);
+      a_vals[e] = acc;
+    }
   }
 }
 
@@ -378,6 +447,49 @@ extern "C" int sg_pattern_square(int64_t n, const int32_t* offs, const int32_t* 
   }
   if (n > 0) k_square_pattern<<<grid, 32 * SQ_WARPS, 0, s>>>(n, offs, cols, nullptr, out_offs, out_cols, flags);
   SG_LAUNCH_CHECK("k_square_pattern (fill)");
+  return SG_OK;
+}
+
+extern "C" int sg_gram_pattern(int64_t n, const int32_t* p_offs, const int32_t* p_cols, const int32_t* pt_offs,
+                               const int32_t* pt_cols, int32_t* out_offs, int32_t* out_cols, int64_t* out_nnz_host,
+                               void* ws, size_t* ws_bytes, void* stream) {
+  Carve c(ws);
+  int32_t* counts = c.take<int32_t>(n + 1);
+  unsigned int* flags = c.take<unsigned int>(2);
+  if (!ws) { *ws_bytes = c.off; return SG_OK; }
+  if (*ws_bytes < c.off) { set_error("workspace too small"); return SG_EINVAL; }
+  if (n < 1) { set_error("matrix size must be positive"); return SG_EINVAL; }
+  cudaStream_t s = as_stream(stream);
+  const int grid = (int)(ceil_div(n, SQ_WARPS) < 148 * 16 ? ceil_div(n, SQ_WARPS) : 148 * 16);
+  if (!out_cols) {  // pass 1: offsets + nnz
+    SG_CUDA(cudaMemsetAsync(flags, 0, 2 * sizeof(unsigned int), s));
+    k_gram_pattern<<<grid, 32 * SQ_WARPS, 0, s>>>(n, p_offs, p_cols, pt_offs, pt_cols, counts, nullptr, nullptr, flags);
+    k_scan_counts<<<1, 1024, 0, s>>>(counts, n, out_offs, flags + 1);
+    SG_LAUNCH_CHECK("k_gram_pattern (count)");
+    unsigned int hf[2];
+    int32_t nnz = 0;
+    SG_CUDA(cudaMemcpyAsync(hf, flags, sizeof(hf), cudaMemcpyDeviceToHost, s));
+    SG_CUDA(cudaMemcpyAsync(&nnz, out_offs + n, sizeof(nnz), cudaMemcpyDeviceToHost, s));
+    SG_CUDA(cudaStreamSynchronize(s));
+    if (hf[0]) { set_error("a row of P P^T has more than %d candidate entries", SQ_CAP - 1); return SG_EUNSUPPORTED; }
+    if (hf[1]) { set_error("P P^T pattern exceeds the int32 index range"); return SG_EUNSUPPORTED; }
+    *out_nnz_host = nnz;
+    return SG_OK;
+  }
+  k_gram_pattern<<<grid, 32 * SQ_WARPS, 0, s>>>(n, p_offs, p_cols, pt_offs, pt_cols, nullptr, out_offs, out_cols, flags);
+  SG_LAUNCH_CHECK("k_gram_pattern (fill)");
+  return SG_OK;
+}
+
+extern "C" int sg_gram_values(int64_t n, const int32_t* p_offs, const int32_t* p_cols, const double* p_vals,
+                              const int32_t* a_offs, const int32_t* a_cols, double shift, double* a_vals,
+                              void* stream) {
+  if (n < 1) { set_error("matrix size must be positive"); return SG_EINVAL; }
+  const int warps_per_block = 8;
+  const int64_t blocks = ceil_div(n, warps_per_block);
+  k_gram_values<<<(int)(blocks < 148 * 16 ? blocks : 148 * 16), 32 * warps_per_block, 0, as_stream(stream)>>>(
+      n, p_offs, p_cols, p_vals, a_offs, a_cols, shift, a_vals);
+  SG_LAUNCH_CHECK("k_gram_values");
   return SG_OK;
 }
 

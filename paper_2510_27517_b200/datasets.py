@@ -117,6 +117,52 @@ def make_split(dataset, ratio: tuple = (4, 1), seed: int = 0):
     return [items[i] for i in perm[n_test:]], [items[i] for i in perm[:n_test]]
 
 
+SYNTHETIC_EPS = 1e-4  # datasets.py:42
+
+
+def gen_synthetic(n: int, density: float, seed: int):
+    """datasets.py:148-193: A = P·Pᵀ + εI, P uniformly random sparse standard-normal.
+
+    The draws are the reference's (host PCG64: ``choice`` without replacement, then
+    ``standard_normal``); everything after them runs on the device: P's rows and its transpose by
+    the radix-sort COO→CSR / transpose kernels, the Gram pattern by the warp symbolic product
+    (``sg_gram_pattern``), and the values by ``sg_gram_values``, which merges rows i and j of P in
+    ascending column order -- the order the reference's dictionary accumulation visits P's column
+    groups in -- so every entry is bit-identical.
+    """
+    import ctypes as C
+
+    import torch
+    if n < 1:
+        raise ValueError("matrix size must be positive")
+    if not 0.0 <= density <= 1.0:
+        raise ValueError("density must lie in [0, 1]")
+    rng = np.random.default_rng(seed)
+    nnz_p = int(round(density * n * n))
+    flat = rng.choice(n * n, size=nnz_p, replace=False)
+    p_vals = rng.standard_normal(nnz_p)
+    P = SparseMatrix.from_coo(n, n, flat // n, flat % n, p_vals).device()
+    ot, ct, _ = P.transpose_pattern()
+    offs = L.empty(n + 1, torch.int32)
+    nnz = C.c_int64(0)
+    lib = L.lib()
+    buf, wsb = L.workspace(lib.sg_gram_pattern, n, L.ptr(P.offs), L.ptr(P.cols), L.ptr(ot), L.ptr(ct),
+                           L.ptr(offs), None, C.byref(nnz))
+    L.check(lib.sg_gram_pattern(n, L.ptr(P.offs), L.ptr(P.cols), L.ptr(ot), L.ptr(ct), L.ptr(offs), None,
+                                C.byref(nnz), L.ptr(buf), C.byref(wsb), L.stream_ptr()), "gen_synthetic")
+    cols = L.empty(int(nnz.value), torch.int32)
+    L.check(lib.sg_gram_pattern(n, L.ptr(P.offs), L.ptr(P.cols), L.ptr(ot), L.ptr(ct), L.ptr(offs),
+                                L.ptr(cols), C.byref(nnz), L.ptr(buf), C.byref(wsb), L.stream_ptr()),
+            "gen_synthetic")
+    vals = L.empty(int(nnz.value), torch.float64)
+    L.check(lib.sg_gram_values(n, L.ptr(P.offs), L.ptr(P.cols), L.ptr(P.vals), L.ptr(offs), L.ptr(cols),
+                               SYNTHETIC_EPS, L.ptr(vals), L.stream_ptr()), "gen_synthetic")
+    A = SparseMatrix.from_device(DeviceCsr(n, n, offs, cols, vals))
+    meta = ProblemMeta(family="synthetic", n=n, gen_seed=seed, density=density,
+                       result_density=A.nnz / (n * n), epsilon_reg=SYNTHETIC_EPS)
+    return A, meta
+
+
 def rand_spd_sparse(n: int, rng, extra_per_row: int = 3) -> SparseMatrix:
     """verify.py:39-61 (config-4 generator): same PCG64 draw sequence, vectorised bookkeeping.
 

@@ -874,3 +874,36 @@ def test_strip_coefficient_stencil_bit_identical(monkeypatch, grid):
     assert PC._handle_for(A2, M).stats()[2][6] == 1.0
     o, c, v = A2.row_offsets, A2.col_indices, A2.values
     assert rep2.converged and np.linalg.norm(b - O.spmv(o, c, v, rep2.x)) / np.linalg.norm(b) <= 1e-9
+
+
+# --------------------------------------------------------------------------- gen_synthetic (datasets.py:148-193)
+def test_gen_synthetic_bit_exact_vs_reference_golden():
+    """Device Gram pattern + ordered Gram values == the REAL reference's gen_synthetic output
+    (tests/golden/golden_synthetic.npz): offsets, columns and every value bit-identical; meta as
+    datasets.py:185-192; SPD (PCG with identity converges); argument errors as the reference."""
+    import os
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "golden_synthetic.npz"))
+    for t, (n, dens, seed) in enumerate(g["cases"]):
+        A, meta = P.gen_synthetic(int(n), float(dens), int(seed))
+        assert np.array_equal(A.row_offsets, g[f"s{t}_offs"]), (n, dens)
+        assert np.array_equal(A.col_indices, g[f"s{t}_cols"]), (n, dens)
+        assert np.array_equal(A.values, g[f"s{t}_vals"]), (n, dens)
+        assert meta.family == "synthetic" and meta.n == int(n) and meta.gen_seed == int(seed)
+        assert meta.result_density == float(g[f"s{t}_result_density"])
+        assert meta.epsilon_reg == P.SYNTHETIC_EPS == 1e-4
+    A, _ = P.gen_synthetic(10, 0.0, 0)
+    assert np.array_equal(A.values, np.full(10, 1e-4)) and np.array_equal(A.col_indices, np.arange(10))
+    with pytest.raises(ValueError):
+        P.gen_synthetic(0, 0.1, 0)
+    with pytest.raises(ValueError):
+        P.gen_synthetic(10, 1.5, 0)
+    A, meta = P.gen_synthetic(50, 0.05, 2)
+    rep = P.pcg_solve(A, P.gen_rhs(meta, 1), P.build_identity(A), P.SolveConfig(rtol=1e-8))
+    assert rep.converged
+
+
+def test_gen_synthetic_larger_vs_oracle():
+    """A mid-size Gram matrix (n = 3000, ~9 entries of P per column) against the oracle."""
+    A, _ = P.gen_synthetic(3000, 3e-3, 11)
+    o, c, v = O.gen_synthetic(3000, 3e-3, 11)
+    assert np.array_equal(A.row_offsets, o) and np.array_equal(A.col_indices, c) and np.array_equal(A.values, v)

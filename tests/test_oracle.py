@@ -222,3 +222,15 @@ def test_coefficient_stencil_formula_regenerates_reference_A(g_heat):
                     i: (face[i - 1] + face[i + 1]) * ihx2 + (face[i - nx] + face[i + nx]) * ihy2}
             for j, v in row.items():
                 assert np.float64(v).tobytes() == np.float64(want[j]).tobytes(), (tag, i, j)
+
+
+def test_gen_synthetic_oracle_matches_reference_golden():
+    """datasets.py:148-193 (A = P·Pᵀ + εI): the oracle's restatement equals the reference's output
+    bit for bit on the reference tests' own calls and the edge cases (n = 1, density 0 and 1)."""
+    import os
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "golden_synthetic.npz"))
+    for t, (n, dens, seed) in enumerate(g["cases"]):
+        offs, cols, vals = O.gen_synthetic(int(n), float(dens), int(seed))
+        assert np.array_equal(offs, g[f"s{t}_offs"]) and np.array_equal(cols, g[f"s{t}_cols"])
+        assert np.array_equal(vals, g[f"s{t}_vals"])
+        assert len(cols) / (n * n) == float(g[f"s{t}_result_density"])
