@@ -156,4 +156,24 @@ __device__ __forceinline__ double block_sum(double v, double* scratch) {
   return r;
 }
 
+// Two block sums sharing one pair of barriers; each value follows block_sum's tree exactly.
+// Results valid in thread 0.
+__device__ __forceinline__ void block_sum2(double& a, double& b) {
+  __shared__ double scratch2[2][32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  a = warp_sum(a);
+  b = warp_sum(b);
+  __syncthreads();
+  if (lane == 0) {
+    scratch2[0][wid] = a;
+    scratch2[1][wid] = b;
+  }
+  __syncthreads();
+  const int nw = (blockDim.x + 31) >> 5;
+  if (wid == 0) {
+    a = warp_sum(lane < nw ? scratch2[0][lane] : 0.0);
+    b = warp_sum(lane < nw ? scratch2[1][lane] : 0.0);
+  }
+}
+
 }  // namespace sg

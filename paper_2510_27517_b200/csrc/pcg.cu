@@ -275,8 +275,8 @@ __device__ __forceinline__ void block_rows(const Dev& D, int& sys, long long& r0
 __device__ __forceinline__ bool arrive(const Dev& D, const int* sb0, int sys, double p0, double p1, double* red,
                                        int* flag) {
   if (D.part == 2) __threadfence_system();  // every thread's s-halo peer stores precede the arrival
-  const double a = block_sum(p0, red);
-  const double b = block_sum(p1, red);
+  double a = p0, b = p1;
+  block_sum2(a, b);
   if (threadIdx.x == 0) {
     D.pp[2 * blockIdx.x + 0] = a;
     D.pp[2 * blockIdx.x + 1] = b;
@@ -300,6 +300,19 @@ __device__ __forceinline__ double gather_partials(const Dev& D, const int* sb0, 
   double v = 0.0;
   for (int b = b0 + threadIdx.x; b < b1; b += blockDim.x) v += __ldcg(&D.pp[2 * b + which]);
   return block_sum(v, red);
+}
+// Both partial slots of `sys` in one pass (one round of loads, one pair of barriers); each value
+// is summed exactly as gather_partials sums it.
+__device__ __forceinline__ void gather_partials2(const Dev& D, const int* sb0, int sys, double& v0, double& v1) {
+  const int b0 = sb0[sys], b1 = sb0[sys + 1];
+  v0 = 0.0;
+  v1 = 0.0;
+  for (int b = b0 + threadIdx.x; b < b1; b += blockDim.x) {
+    const double2 pv = __ldcg(reinterpret_cast<const double2*>(D.pp) + b);
+    v0 += pv.x;
+    v1 += pv.y;
+  }
+  block_sum2(v0, v1);
 }
 __device__ __forceinline__ double gather_partials(const Dev& D, int sys, int which, double* red) {
   return gather_partials(D, D.sys_blk0, sys, which, red);
@@ -854,8 +867,8 @@ __global__ void __launch_bounds__(PR, FMT >= 1 ? 8 : 1) k_iter1(Dev D, int par) 
     }
   }
   if (arrive(D, sys, pdq, prr, red, &flag)) {
-    const double dq = gather_partials(D, sys, 0, red);
-    const double rrf = gather_partials(D, sys, 1, red);
+    double dq, rrf;
+    gather_partials2(D, D.sys_blk0, sys, dq, rrf);
     if (threadIdx.x == 0) { if (D.part) part_fin(D, sys, FIN_K1, dq, rrf, run); else fin_k1(D, sys, run, dq, rrf); }
   }
 }
@@ -1646,8 +1659,8 @@ __global__ void __launch_bounds__(PR, 6) k_iter1_st(Dev D, int par) {
     }
   }
   if (arrive(D, sys, pdq, prr, red, &flag)) {
-    const double dq = gather_partials(D, sys, 0, red);
-    const double rrf = gather_partials(D, sys, 1, red);
+    double dq, rrf;
+    gather_partials2(D, D.sys_blk0, sys, dq, rrf);
     if (threadIdx.x == 0) { if (PART) part_fin(D, sys, FIN_K1, dq, rrf, run); else fin_k1(D, sys, run, dq, rrf); }
   }
 }
@@ -1752,8 +1765,8 @@ __global__ void __launch_bounds__(PR, 5) k_iter23_st(Dev D, int par) {
     prs += mul(rni, si);
   }
   if (arrive(D, sys, prr, prs, red, &flag)) {
-    const double rr = gather_partials(D, sys, 0, red);
-    const double rs = gather_partials(D, sys, 1, red);
+    double rr, rs;
+    gather_partials2(D, D.sys_blk0, sys, rr, rs);
     if (threadIdx.x == 0) {
       if (PART) {
         part_fin(D, sys, FIN_K23, rr, rs, 0);
@@ -1965,8 +1978,8 @@ __global__ void __launch_bounds__(kSwThreads, 3) k_iter23_sw(Dev D, int par) {
     if ((tid & 31) == 0) mbar_arrive(&empty[k % P]);
   }
   if (arrive(D, D.sys_rng0, sys, prr, prs, red, &flag)) {
-    const double rr = gather_partials(D, D.sys_rng0, sys, 0, red);
-    const double rs = gather_partials(D, D.sys_rng0, sys, 1, red);
+    double rr, rs;
+    gather_partials2(D, D.sys_rng0, sys, rr, rs);
     if (threadIdx.x == 0) {
       if (PART) {
         part_fin(D, sys, FIN_K23, rr, rs, 0);
@@ -2150,8 +2163,8 @@ __global__ void __launch_bounds__(PR, 5) k_iter1_sw(Dev D, int par) {
     }
   }
   if (arrive(D, D.sys_rng0, sys, pdq, prr, red, &flag)) {
-    const double dq = gather_partials(D, D.sys_rng0, sys, 0, red);
-    const double rrf = gather_partials(D, D.sys_rng0, sys, 1, red);
+    double dq, rrf;
+    gather_partials2(D, D.sys_rng0, sys, dq, rrf);
     if (threadIdx.x == 0) {
       if (PART) {
         part_fin(D, sys, FIN_K1, dq, rrf, run);
@@ -2369,8 +2382,8 @@ __global__ void __launch_bounds__(kStripC, PART ? 3 : 768 / kStripC) k_iter23_s5
     }
   }
   if (arrive(D, D.sys_rng0, sys, prr, prs, red, &flag)) {
-    const double rr = gather_partials(D, D.sys_rng0, sys, 0, red);
-    const double rs = gather_partials(D, D.sys_rng0, sys, 1, red);
+    double rr, rs;
+    gather_partials2(D, D.sys_rng0, sys, rr, rs);
     if (threadIdx.x == 0) {
       if (PART) {
         part_fin(D, sys, FIN_K23, rr, rs, 0);
@@ -2519,9 +2532,143 @@ __global__ void __launch_bounds__(kStripC, 1024 / kStripC) k_iter1_s5(Dev D, int
     }
   }
   if (arrive(D, D.sys_rng0, sys, pdq, prr, red, &flag)) {
-    const double dq = gather_partials(D, D.sys_rng0, sys, 0, red);
-    const double rrf = gather_partials(D, D.sys_rng0, sys, 1, red);
+    double dq, rrf;
+    gather_partials2(D, D.sys_rng0, sys, dq, rrf);
     if (threadIdx.x == 0) { if (PART) part_fin(D, sys, FIN_K1, dq, rrf, run); else fin_k1(D, sys, run, dq, rrf); }
+  }
+}
+
+// K1 on strips, TWO lines per step (coefficient stencil, the C5 path): per step the bulk-copy
+// engine brings a PAIR of lead line segments (s, d, coefficients, mask), d' of both is formed,
+// one CTA barrier, then q of the two lines behind them.  Same per-row arithmetic and the same
+// per-thread summation order as k_iter1_s5 (bit-identical), half the barriers per row and two
+// independent rows per thread between them.  Rings of 8 lines: a step reads d' / coefficients of
+// lines 2k-2 .. 2k+1 while the next pair's d' and the copies of pair k+P-1 land elsewhere.
+struct Strip1P {
+  static constexpr int P = 3;   // line pairs in flight
+  static constexpr int RL = 8;  // coefficient, d' and mask rings (lines; power of two)
+  // bytes: coefficients [RL][SP] | d' [RL][SP] | staging [P][2 lines][s, d][SP] | mask [RL][MK]
+  static constexpr size_t SMEM = (size_t)2 * RL * kStripSP * 8 + (size_t)P * 4 * kStripSP * 8 +
+                                 (size_t)RL * kStripMK;
+};
+
+__global__ void __launch_bounds__(kStripC, 3) k_iter1_s5p(Dev D, int par) {
+  constexpr int SP = kStripSP, RL = Strip1P::RL, P = Strip1P::P, E = kStripE;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  __shared__ __align__(8) uint64_t bars[P];
+  __shared__ double red[kStripC / 32];
+  __shared__ int flag;
+  const int b = blockIdx.x, tid = threadIdx.x;
+  const int sys = D.rng_sys[b];
+  const int status = D.st[sys].status;
+  if (status == ST_DONE) return;
+  long long s0, s1;
+  sys_bounds(D, sys, s0, s1);
+  const long long W = D.dia.W;
+  const long long r0 = D.rng_r0[b] - s0;
+  const int x0 = (int)(r0 % W);
+  const long long y0 = r0 / W, nl = (s1 - s0) / W;
+  const long long y1 = y0 + D.rng_len < nl ? y0 + D.rng_len : nl;
+  const int cx = (int)(W - x0 < kStripC ? W - x0 : kStripC);
+  const bool run = status == ST_RUN;
+  const bool fresh = run ? (D.st[sys].flags & FL_FRESH) != 0 : true;
+  const double beta = D.st[sys].beta;
+  const double* dc = par ? D.d1 : D.d0;
+  double* dn = par ? D.d0 : D.d1;
+  double* rc = par ? D.r1 : D.r0;
+  auto rowof = [&](long long line, int p) { return s0 + line * W + x0 - E + p; };
+  double pdq = 0.0, prr = 0.0;
+  if (run) {
+    double* ar = reinterpret_cast<double*>(smraw);  // [RL][SP]
+    double* dp = ar + RL * SP;                        // [RL][SP]
+    double* stg = dp + RL * SP;                       // [P][2][2][SP]
+    unsigned char* mk = reinterpret_cast<unsigned char*>(stg + P * 4 * SP);
+    const long long LBl = y0 - 1;
+    const int K = (int)(y1 - y0) + 2;  // lines y0 - 1 .. y1
+    const int NS = (K + 1) / 2;        // steps
+    auto issue = [&](int k) {
+      const int ss = k % P;
+      const int nlines = 2 * k + 1 < K ? 2 : 1;
+      mbar_arrive_expect_tx(&bars[ss], (uint32_t)(nlines * (3 * SP * 8 + kStripMK)));
+      for (int h = 0; h < nlines; ++h) {
+        const int l = 2 * k + h, lr = l & (RL - 1);
+        const long long row = rowof(LBl + l, 0);
+        double* st = stg + (ss * 2 + h) * 2 * SP;
+        bulk_g2s(st, D.s + row, SP * 8, &bars[ss]);
+        bulk_g2s(st + SP, dc + row, SP * 8, &bars[ss]);
+        bulk_g2s(ar + lr * SP, D.coef + row, SP * 8, &bars[ss]);
+        bulk_g2s(mk + lr * kStripMK, D.dia.mask + (row - 14), kStripMK, &bars[ss]);
+      }
+    };
+    if (tid == 0) {
+#pragma unroll
+      for (int q = 0; q < P; ++q) mbar_init(&bars[q], 1);
+      mbar_init_fence();
+    }
+    __syncthreads();
+    if (tid == 0)
+      for (int k = 0; k < P - 1 && k < NS; ++k) issue(k);
+    for (int k = 0; k < NS; ++k) {
+      mbar_wait(&bars[k % P], (uint32_t)((k / P) & 1));
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {  // d' of lead lines 2k, 2k + 1
+        const int l = 2 * k + h;
+        if (l < K) {
+          const long long line = LBl + l;
+          const int lr = l & (RL - 1);
+          const double* st = stg + ((k % P) * 2 + h) * 2 * SP;
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            const int p = tid + h2 * kStripC;
+            if (p < SP) {
+              const long long j = rowof(line, p);
+              double v = add(st[p], mul(beta, st[SP + p]));
+              v = (j >= s0 && j < s1) ? v : 0.0;
+              const int x = x0 - E + p;
+              if (line >= y0 && line < y1 && x >= x0 && x < x0 + cx) dn[j] = v;
+              dp[lr * SP + p] = v;
+            }
+          }
+        }
+      }
+      __syncthreads();
+      if (tid == 0 && k + P - 1 < NS) issue(k + P - 1);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {  // q of the own columns of lines 2k - 1, 2k
+        const int u = 2 * k - 1 + h;
+        const long long line = LBl + u;
+        if (u >= 1 && tid < cx && line >= y0 && line < y1) {
+          const int p = tid + E;
+          const int lr = u & (RL - 1);
+          const unsigned int m = mk[lr * kStripMK + p + 14];
+          const double* cu = ar + lr * SP + p;
+          double a[5], pr[5];
+          stencil5(cu[0], ar[((u - 1) & (RL - 1)) * SP + p], cu[-1], cu[1], ar[((u + 1) & (RL - 1)) * SP + p], m,
+                   D.ihx2, D.ihy2, a);
+#pragma unroll
+          for (int d = 0; d < 5; ++d) pr[d] = mul(a[d], dp[((u + s5a(d)) & (RL - 1)) * SP + p + s5b(d)]);
+          const double qi = combine_numpy<5>(pr, m);
+          D.q[rowof(line, p)] = qi;
+          pdq += mul(dp[lr * SP + p], qi);
+        }
+      }
+    }
+  }
+  if (fresh) {  // r_fresh = b - A x over the range's own rows (direct loads)
+    for (long long line = y0; line < y1; ++line) {
+      if (tid >= cx) break;
+      const long long i = s0 + line * W + x0 + tid;
+      const unsigned int m = D.dia.mask[i];
+      const double ax = dia_row_numpy_sym<5, 0>(D.dia, D.dia.av, (int)i, m, XF{D.x, nullptr, 0.0});
+      const double rf = sub(D.b[i], ax);
+      if (run) rc[i] = rf;
+      prr += mul(rf, rf);
+    }
+  }
+  if (arrive(D, D.sys_rng0, sys, pdq, prr, red, &flag)) {
+    double dq, rrf;
+    gather_partials2(D, D.sys_rng0, sys, dq, rrf);
+    if (threadIdx.x == 0) fin_k1(D, sys, run, dq, rrf);
   }
 }
 
@@ -2567,6 +2714,7 @@ struct sg_pcg {
   int scn = 1;        // ... of <= kClusterRows rows: one cluster of scn CTAs per system
   int smem_cn = 0;    // > 0: the shared-memory resident solver (k_pcg_smem), smem_cn CTAs of
   int smem_R = 0;     //      smem_R rows per system
+  int k1pairs = 1;    // strip K1 with the coefficient stencil: two lines per step (SG_STRIP_K1_PAIRS=0: one)
   int k23 = 1;        // fused K2+K3 variant: 1 = sliding window (k_iter23_sw), 0 = tiles (k_iter23_st)
   void* sell_mem[3] = {nullptr, nullptr, nullptr};   // SELL-32 patterns of A, G, G^T
   void* sell_vals[3] = {nullptr, nullptr, nullptr};
@@ -2661,7 +2809,9 @@ int launch_iteration(sg_pcg* h, cudaStream_t s, int par, bool refresh, cudaEvent
     // the streamed kernels exist with and without the row-partition logic (PART)
     auto k1_streamed = [&](auto Pc) {
       constexpr bool PT = decltype(Pc)::value;
-      if (strip && FMT == 2 && h->cst && !PT)  // A from the coefficient stencil (verified per solve)
+      if (strip && FMT == 2 && h->cst && !PT && h->k1pairs)  // coefficient stencil, two lines per step
+        k_iter1_s5p<<<gr, kStripC, Strip1P::SMEM, s>>>(h->D, par);
+      else if (strip && FMT == 2 && h->cst && !PT)  // A from the coefficient stencil (verified per solve)
         k_iter1_s5<2, false, true><<<gr, kStripC, Strip1<2, true>::SMEM, s>>>(h->D, par);
       else if (strip) k_iter1_s5<FS, PT><<<gr, kStripC, Strip1<FS>::SMEM, s>>>(h->D, par);
       else if (st && h->k1sw && FMT == 2 && ND == 5 && h->cst && !PT) {  // A from the coefficient stencil
@@ -3024,6 +3174,7 @@ int strip_setup(int* per_sm) {
   SG_CUDA(cudaFuncSetAttribute(k_iter1_s5<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Strip1<2>::SMEM));
   SG_CUDA(cudaFuncSetAttribute(k_iter1_s5<2, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)Strip1<2, true>::SMEM));
+  SG_CUDA(cudaFuncSetAttribute(k_iter1_s5p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Strip1P::SMEM));
   SG_CUDA(cudaFuncSetAttribute(k_iter1_s5<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Strip1<1>::SMEM));
   SG_CUDA(cudaFuncSetAttribute(k_iter1_s5<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Strip1<2>::SMEM));
   SG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_iter23_s5<false>, kStripC, Strip23::SMEM));
@@ -3341,6 +3492,10 @@ extern "C" int sg_pcg_create(sg_pcg** out, int32_t n_systems, const int64_t* sys
       const char* wv = getenv("SG_PCG_GWARP");
       h->g_warp = !(wv && wv[0] == '0') && (double)gz / (double)n >= 32.0;
     }
+  }
+  {
+    const char* pv = getenv("SG_STRIP_K1_PAIRS");
+    h->k1pairs = (pv && pv[0] == '0') ? 0 : 1;
   }
   SG_CUDA(cudaHostAlloc(&h->pinned_active, 2 * sizeof(unsigned int), cudaHostAllocDefault));
   SG_CUDA(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));

@@ -907,3 +907,30 @@ def test_gen_synthetic_larger_vs_oracle():
     A, _ = P.gen_synthetic(3000, 3e-3, 11)
     o, c, v = O.gen_synthetic(3000, 3e-3, 11)
     assert np.array_equal(A.row_offsets, o) and np.array_equal(A.col_indices, c) and np.array_equal(A.values, v)
+
+
+@pytest.mark.parametrize("grid", [(1024, 24), (784, 21), (1040, 37)])
+def test_strip_k1_two_lines_per_step_bit_identical(monkeypatch, grid):
+    """The strip K1 that forms d' and q for two grid lines per step (k_iter1_s5p, the C5 default)
+    == the one-line-per-step kernel, bitwise: k, x and every residual, odd and even line counts,
+    residual refreshes and fresh-residual checks included."""
+    import os
+    import paper_2510_27517_b200.pcg as PC
+    m = P.load_checkpoint(os.path.join(os.path.dirname(__file__), "golden", "trained_heat16.spaignn"))
+    nx, ny = grid
+    A, meta = P.gen_poisson2d(nx, ny, coeff_seed=5)
+    G = P.forward(m, P.build_graph(A, meta)).G
+    M = P.build_learned_spai(G, m.config.epsilon)
+    b = P.gen_rhs(meta, 6)
+    cfg = P.SolveConfig(rtol=1e-9, residual_refresh_period=7)
+    out = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("SG_STRIP_K1_PAIRS", flag)
+        for h in (PC._HANDLES or {}).values():  # the variant is chosen when a handle is created
+            h.close()
+        PC._HANDLES = None
+        rep = P.pcg_solve(A, b, M, cfg)
+        assert PC._handle_for(A, M).stats()[2][6] == 2.0  # K1 regenerates A from the coefficients
+        out[flag] = (rep.k, rep.x.copy(), np.asarray(rep.residual_history))
+    assert out["1"][0] == out["0"][0]
+    assert np.array_equal(out["1"][1], out["0"][1]) and np.array_equal(out["1"][2], out["0"][2])
