@@ -463,7 +463,7 @@ def run_c5(a, model, dev):
     assert rep.converged and rel <= rtol, (rep.converged, rel)
     peak, peak_src = hbm_peak()
     n, nnz = A.n_rows, A.nnz
-    roof = pcg_roofline(prof, n, nnz, peak, peak_src, K23_SW="k_iter23_s5", K1_SW="k_iter1_s5",
+    roof = pcg_roofline(prof, n, nnz, peak, peak_src, K23_SW="k_iter23_s5", K1_SW="k_iter1_s5p",
                         units_note="one system", which="c5")
     # e2e: host int64 CSR + host rhs in, host x out, through the public API
     offs_h, cols_h, vals_h = A.row_offsets.copy(), A.col_indices.copy(), A.values.copy()
@@ -545,7 +545,8 @@ def ncu_traffic(kernel, which="c2"):
         return None
     scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     for line in open(path):
-        if f" {kernel}<" not in line.split("|")[0]:
+        head = line.split("|")[0]
+        if f" {kernel}<" not in head and f" {kernel}(" not in head:
             continue
         vals = {}
         for cell in line.split("|")[1:]:

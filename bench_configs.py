@@ -100,6 +100,8 @@ def main():
     for _ in range(a.warmup):
         step()
     torch.cuda.synchronize()
+    import bench as B
+    clocks = B.ClockSampler(dev.index or 0)
     times, reps = [], []
     for s in range(a.steps):
         t0 = time.perf_counter()
@@ -107,6 +109,7 @@ def main():
         torch.cuda.synchronize()
         times.append(time.perf_counter() - t0)
         reps.append(rep)
+    clk = clocks.stop()
     from paper_2510_27517_b200.pcg import _handle_for
     h = _handle_for(A, M, "learned")
     kernels, chunks, prof = h.stats()
@@ -118,7 +121,16 @@ def main():
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     peak = float(peaks.get("hbm_gbs", 6650.0))
     per_k = {}
-    if prof[4] > 0:
+    roof = None
+    if prof[4] > 0 and prof[5]:  # DIA kernels: the algorithmic bytes of the layout they run (bench.py)
+        peak_b, peak_src = B.hbm_peak()
+        strip = a.config == "c5"
+        roof = B.pcg_roofline(prof, n, nnz, peak_b, peak_src, K23_SW="k_iter23_s5" if strip else "k_iter23_sw",
+                              K1_SW="k_iter1_s5p" if strip else "k_iter1_sw", units_note="one system",
+                              which="c5" if strip else "none")
+        if roof:
+            per_k = {name.split(" ")[0]: v for name, v in roof["per_kernel"].items()}
+    elif prof[4] > 0:  # CSR (C4): SURVEY §8(d) bytes, G on its own (A^2) pattern
         csr = 12 * nnz + 4 * (n + 1)
         csr_g = 12 * nnz_g + 4 * (n + 1)
         if prof[7]:  # K2 + K3 fused (t stays on chip)
@@ -138,7 +150,9 @@ def main():
            "pcg_time_split_ns": {"t_cg_total_ns": int(rep.t_cg_total_ns), "t_apply_total_ns": int(rep.t_apply_total_ns)},
            "iteration_gbs_survey_bytes": it_bytes * rep.k / ((rep.t_cg_total_ns + rep.t_apply_total_ns) * 1e-9) / 1e9,
            "storage": f"DIA ({int(prof[5])} diagonals)" if prof[5] else "CSR", "per_kernel": per_k,
-           "peak_gbs": peak, "n": n, "nnz": nnz, "nnz_G": nnz_g}
+           "peak_gbs": peak, "n": n, "nnz": nnz, "nnz_G": nnz_g, "clocks": clk}
+    if roof:
+        out["roofline"] = {k: v for k, v in roof.items() if k != "per_kernel"}
     if loss is not None:
         torch.cuda.synchronize()
         t0 = time.perf_counter()
