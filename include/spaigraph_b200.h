@@ -307,6 +307,12 @@ int sg_pcg_rebuilds(sg_pcg* h, int64_t* rebuilds_host);
 int sg_pcg_apply_ns(sg_pcg* h, int64_t* ns_host);
 
 int sg_pcg_set_profile(sg_pcg* h, int32_t on);
+/* Timeline probe of the wide-grid strip kernels (k_iter1_s5p, k_iter23_s5): with a device buffer
+ * of 2 x 16384 uint64, thread 0 of every CTA writes %globaltimer at entry, end of its stream,
+ * after its arrival and (last CTA) after the finaliser, and its SM id; K1 at [0, 16384), K2+K3
+ * at [16384, 32768), slot 8 * cta + k (k = 0..3 the stamps, 4 the SM).  NULL turns it off.
+ * Diagnostic only (profiles/trace_probe.py). */
+int sg_pcg_set_trace(sg_pcg* h, void* buf);
 int sg_pcg_stats(sg_pcg* h, int64_t* kernels_host, int64_t* chunks_host, double* prof_host,
                  int32_t reset);
 

@@ -73,6 +73,7 @@ SIGNATURES = {
     "sg_pcg_rebind_values": (C.c_int, [vp, vp, vp, vp, vp]),
     "sg_pcg_rebind": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "sg_pcg_set_profile": (C.c_int, [vp, i32]),
+    "sg_pcg_set_trace": (C.c_int, [vp, vp]),
     "sg_pcg_rebuilds": (C.c_int, [vp, C.POINTER(C.c_int64)]),
     "sg_pcg_apply_ns": (C.c_int, [vp, C.POINTER(C.c_int64)]),
     "sg_pcg_set_stencil": (C.c_int, [vp, vp, i64, i64, C.POINTER(C.c_int32)]),

@@ -99,6 +99,7 @@ struct Sell {
 };
 
 struct Dev {
+  unsigned long long* trace;  // sg_pcg_set_trace: per-CTA %globaltimer stamps of the strip kernels (or null)
   int xdefer;       // sliding-window path: x += alpha d' deferred from K2+K3 to the next K1
   int sell_on;      // CSR path reads A, G^T (bit 1: also G) from their SELL-32 copies
   Sell sa, sg, sgt;
@@ -268,6 +269,22 @@ __device__ __forceinline__ void block_rows(const Dev& D, int& sys, long long& r0
   const long long e = r0 + D.tile;
   const long long se = D.sys_r1[sys];
   r1 = e < se ? e : se;
+}
+
+// Timeline probe (sg_pcg_set_trace, off unless a buffer is set): thread 0 of CTA b stamps slot
+// `slot` (0 entry, 1 end of the stream, 2 after the arrival, 3 finaliser done) of kernel `kid`;
+// slot 4 holds the SM the CTA ran on.
+__device__ __forceinline__ void trace_stamp(const Dev& D, int kid, int slot) {
+  if (D.trace && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    D.trace[(size_t)kid * 16384 + 8 * blockIdx.x + slot] = t;
+    if (slot == 0) {
+      unsigned int smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      D.trace[(size_t)kid * 16384 + 8 * blockIdx.x + 4] = smid;
+    }
+  }
 }
 
 // Publish this CTA's two partials; returns true in ALL threads of the last CTA of `sys`.
@@ -2256,6 +2273,7 @@ __global__ void __launch_bounds__(kStripC, PART ? 3 : 768 / kStripC) k_iter23_s5
   __shared__ int flag;
   const int b = blockIdx.x, tid = threadIdx.x;
   const int sys = D.rng_sys[b];
+  trace_stamp(D, 1, 0);
   if (D.st[sys].status != ST_RUN) return;
   long long s0, s1;
   sys_bounds(D, sys, s0, s1);
@@ -2381,7 +2399,10 @@ __global__ void __launch_bounds__(kStripC, PART ? 3 : 768 / kStripC) k_iter23_s5
       }
     }
   }
-  if (arrive(D, D.sys_rng0, sys, prr, prs, red, &flag)) {
+  trace_stamp(D, 1, 1);
+  const bool last = arrive(D, D.sys_rng0, sys, prr, prs, red, &flag);
+  trace_stamp(D, 1, 2);
+  if (last) {
     double rr, rs;
     gather_partials2(D, D.sys_rng0, sys, rr, rs);
     if (threadIdx.x == 0) {
@@ -2392,6 +2413,7 @@ __global__ void __launch_bounds__(kStripC, PART ? 3 : 768 / kStripC) k_iter23_s5
         fin_k3(D, sys, rs, 0);
       }
     }
+    trace_stamp(D, 1, 3);
   }
 }
 
@@ -2560,6 +2582,7 @@ __global__ void __launch_bounds__(kStripC, 3) k_iter1_s5p(Dev D, int par) {
   __shared__ int flag;
   const int b = blockIdx.x, tid = threadIdx.x;
   const int sys = D.rng_sys[b];
+  trace_stamp(D, 0, 0);
   const int status = D.st[sys].status;
   if (status == ST_DONE) return;
   long long s0, s1;
@@ -2654,6 +2677,7 @@ __global__ void __launch_bounds__(kStripC, 3) k_iter1_s5p(Dev D, int par) {
       }
     }
   }
+  trace_stamp(D, 0, 1);
   if (fresh) {  // r_fresh = b - A x over the range's own rows (direct loads)
     for (long long line = y0; line < y1; ++line) {
       if (tid >= cx) break;
@@ -2665,10 +2689,13 @@ __global__ void __launch_bounds__(kStripC, 3) k_iter1_s5p(Dev D, int par) {
       prr += mul(rf, rf);
     }
   }
-  if (arrive(D, D.sys_rng0, sys, pdq, prr, red, &flag)) {
+  const bool last = arrive(D, D.sys_rng0, sys, pdq, prr, red, &flag);
+  trace_stamp(D, 0, 2);
+  if (last) {
     double dq, rrf;
     gather_partials2(D, D.sys_rng0, sys, dq, rrf);
     if (threadIdx.x == 0) fin_k1(D, sys, run, dq, rrf);
+    trace_stamp(D, 0, 3);
   }
 }
 
@@ -3900,6 +3927,15 @@ extern "C" int sg_pcg_apply_ns(sg_pcg* h, int64_t* ns_host) {
 extern "C" int sg_pcg_rebuilds(sg_pcg* h, int64_t* rebuilds_host) {
   if (!h || !rebuilds_host) { set_error("null handle"); return SG_EINVAL; }
   *rebuilds_host = h->rebuilds;
+  return SG_OK;
+}
+
+extern "C" int sg_pcg_set_trace(sg_pcg* h, void* buf) {
+  if (!h) { set_error("null handle"); return SG_EINVAL; }
+  for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);
+  h->graphs.clear();
+  h->graph_kernels.clear();
+  h->D.trace = static_cast<unsigned long long*>(buf);
   return SG_OK;
 }
 

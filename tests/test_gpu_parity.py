@@ -934,3 +934,4 @@ def test_strip_k1_two_lines_per_step_bit_identical(monkeypatch, grid):
         out[flag] = (rep.k, rep.x.copy(), np.asarray(rep.residual_history))
     assert out["1"][0] == out["0"][0]
     assert np.array_equal(out["1"][1], out["0"][1]) and np.array_equal(out["1"][2], out["0"][2])
+
