@@ -419,8 +419,8 @@ def run_c5(a, model, dev):
     """North-star block (BASELINE.json configs[4]): ONE 2048x2048 Poisson
     system (n = 4,194,304) through the drop-in API -- build_graph -> forward -> build_learned_spai
     -> pcg_solve (rtol 1e-6, trained weights) -- on 1 GPU.  `value`: device-timed solves/s with A
-    resident; `e2e`: the same from host int64 CSR + host rhs to host x; roofline of the strip
-    kernels (k_iter1_s5, k_iter23_s5); a parity check (converged, true residual <= rtol); and an
+    resident; `e2e`: the same from host int64 CSR + host rhs (page-locked) to host x; roofline of
+    the strip kernels (k_iter1_s5p, k_iter23_s5); a parity check (converged, true residual <= rtol); and an
     EXTRAPOLATED CPU baseline of the oracle port (bounded sample: full-size features, the GNN on a
     256x256 block scaled per edge, 5 full-size PCG iterations scaled to k)."""
     import torch
@@ -465,14 +465,21 @@ def run_c5(a, model, dev):
     n, nnz = A.n_rows, A.nnz
     roof = pcg_roofline(prof, n, nnz, peak, peak_src, K23_SW="k_iter23_s5", K1_SW="k_iter1_s5p",
                         units_note="one system", which="c5")
-    # e2e: host int64 CSR + host rhs in, host x out, through the public API
-    offs_h, cols_h, vals_h = A.row_offsets.copy(), A.col_indices.copy(), A.values.copy()
+    # e2e: host int64 CSR + host rhs in (page-locked host buffers, as the C2 e2e leg), host x out,
+    # through the public API
+    def pinned(arr):
+        h = torch.empty(arr.shape, dtype=torch.from_numpy(arr[:0]).dtype, pin_memory=True)
+        h.copy_(torch.from_numpy(arr))
+        return h.numpy()
+
+    offs_h, cols_h, vals_h = pinned(A.row_offsets), pinned(A.col_indices), pinned(A.values)
+    b_h = pinned(np.ascontiguousarray(b))
     e2e_ms = []
     for it in range(3):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         Ah = P.SparseMatrix(n, n, offs_h, cols_h, vals_h)
-        rep_h, _ = step(Ah, b)
+        rep_h, _ = step(Ah, b_h)
         xh = rep_h.x  # numpy: D2H inside the region
         torch.cuda.synchronize()
         if it:
@@ -491,8 +498,8 @@ def run_c5(a, model, dev):
                                        "residuals <= 1e-9 vs the oracle replay)"},
             "e2e": {"value": 1000.0 / float(np.mean(e2e_ms)), "unit": "solves/s", "ms_per_solve": float(np.mean(e2e_ms)),
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(8 * n),
-                    "api": "SparseMatrix(host int64 CSR) -> build_graph -> forward -> build_learned_spai -> "
-                           "pcg_solve(host b) -> host x"},
+                    "api": "SparseMatrix(host int64 CSR, page-locked) -> build_graph -> forward -> "
+                           "build_learned_spai -> pcg_solve(host b, page-locked) -> host x"},
             "roofline": roof, "clocks": clk, "cpu_baseline": cpu}
 
 

@@ -935,3 +935,33 @@ def test_strip_k1_two_lines_per_step_bit_identical(monkeypatch, grid):
     assert out["1"][0] == out["0"][0]
     assert np.array_equal(out["1"][1], out["0"][1]) and np.array_equal(out["1"][2], out["0"][2])
 
+
+def test_strip_timeline_probe():
+    """sg_pcg_set_trace: every CTA of the strip kernels stamps its entry, stream end <= arrival, the
+    last CTA the finaliser after every arrival, and its SM id; off again with NULL (no stamps)."""
+    import ctypes as C
+    import paper_2510_27517_b200.pcg as PC
+    from paper_2510_27517_b200 import _lib as L
+    A, meta = P.gen_poisson2d(1024, 40)
+    M = P.build_learned_spai(A.with_values(np.zeros(A.nnz)), 1.0)  # M = I (G = 0, eps = 1)
+    b = P.gen_rhs(meta, 1)
+    cfg = P.SolveConfig(rtol=1e-6, max_iters=50)
+    P.pcg_solve(A, b, M, cfg)
+    h = PC._handle_for(A, M)
+    buf = torch.zeros(2 * 16384, dtype=torch.int64, device="cuda")
+    L.check(L.lib().sg_pcg_set_trace(h._h, C.c_void_p(buf.data_ptr())))
+    rep = P.pcg_solve(A, b, M, cfg)
+    torch.cuda.synchronize()
+    t = buf.cpu().numpy().reshape(2, 2048, 8)
+    for kid in range(2):
+        tk = t[kid][t[kid][:, 0] > 0]
+        assert len(tk) > 0 and np.all(tk[:, 1] > 0) and np.all(tk[:, 2] >= tk[:, 1])
+        fin = tk[:, 3][tk[:, 3] > 0]  # one last CTA per launch; the newest finaliser follows every arrival
+        assert len(fin) >= 1 and fin.max() >= tk[:, 2].max()
+        assert np.all(tk[:, 4] < 1024)  # SM ids
+    L.check(L.lib().sg_pcg_set_trace(h._h, None))
+    buf.zero_()
+    rep2 = P.pcg_solve(A, b, M, cfg)
+    torch.cuda.synchronize()
+    assert int(buf.abs().sum()) == 0
+    assert rep.k == rep2.k and np.array_equal(rep.x, rep2.x)
