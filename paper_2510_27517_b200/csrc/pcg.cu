@@ -2114,14 +2114,20 @@ __global__ void __launch_bounds__(PR, 5) k_iter1_sw(Dev D, int par) {
     const bool xupd = pend && !fresh;
     double xo_n = 0.0;  // x of the lead chunk's own rows, loaded one step ahead
     if (xupd && crel(0) * C + tid >= R0r && crel(0) * C + tid < R1r) xo_n = D.x[LB + crel(0) * C + tid];
+    int ks = 0;        // k % P, kept incrementally (no division per step)
+    uint32_t kph = 0;  // (k / P) & 1
     for (int k = 0; k < K; ++k) {
-      const double* st = stg + (k % P) * 2 * C;
+      const double* st = stg + ks * 2 * C;
       const int lj = crel(k) * C + tid;
-      const bool xown = xupd && lj >= R0r && lj < R1r;
-      const double xo = xo_n;
-      const int ljn = crel(k + 1) * C + tid;  // the next lead chunk's row (either direction)
-      if (xupd && k + 1 < K && ljn >= R0r && ljn < R1r) xo_n = D.x[LB + ljn];
-      mbar_wait(&bars[k % P], (uint32_t)((k / P) & 1));
+      bool xown = false;
+      double xo = 0.0;
+      if (xupd) {  // uniform: off unless the x update is deferred into K1 (SG_PCG_XDEFER)
+        xown = lj >= R0r && lj < R1r;
+        xo = xo_n;
+        const int ljn = crel(k + 1) * C + tid;  // the next lead chunk's row (either direction)
+        if (k + 1 < K && ljn >= R0r && ljn < R1r) xo_n = D.x[LB + ljn];
+      }
+      mbar_wait(&bars[ks], kph);
       {  // d' of the lead chunk (and the deferred x update of its own rows)
         double v = add(st[tid], mul(beta, st[C + tid]));
         v = (lj >= s0r && lj < s1r) ? v : 0.0;
@@ -2141,8 +2147,12 @@ __global__ void __launch_bounds__(PR, 5) k_iter1_sw(Dev D, int par) {
           double p[ND];
           if constexpr (CS) {
             double a[5];
-            stencil5(ar[io], ar[ring_nb<ND>(io, off, 0, RING)], ar[ring_nb<ND>(io, off, 1, RING)],
-                     ar[ring_nb<ND>(io, off, 3, RING)], ar[ring_nb<ND>(io, off, 4, RING)], m, D.ihx2, D.ihy2, a);
+            // a power-of-two ring (the coefficient ring: P + 2 NH chunks) wraps with one mask
+            auto nb = [&](int d) {
+              if constexpr ((RING & (RING - 1)) == 0) return (io + off[d]) & (RING - 1);
+              else return ring_nb<ND>(io, off, d, RING);
+            };
+            stencil5(ar[io], ar[nb(0)], ar[nb(1)], ar[nb(3)], ar[nb(4)], m, D.ihx2, D.ihy2, a);
 #pragma unroll
             for (int d = 0; d < ND; ++d) p[d] = mul(a[d], dp[(li + off[d]) & DM]);
           } else {
@@ -2158,6 +2168,10 @@ __global__ void __launch_bounds__(PR, 5) k_iter1_sw(Dev D, int par) {
           D.q[LB + li] = qi;
           if (li >= o0r && li < o1r) pdq += mul(dp[li & DM], qi);
         }
+      }
+      if (++ks == P) {
+        ks = 0;
+        kph ^= 1u;
       }
     }
   }
